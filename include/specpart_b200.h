@@ -1,0 +1,171 @@
+/*
+ * specpart-b200 — C ABI of the B200-native spectral-partition hot path.
+ *
+ * The reference (``specpart``, pure Python over numpy/scipy) has no FFI of its
+ * own; these entry points are the seams of its hot path, each
+ * replacing the reference routine cited beside it (paths relative to
+ * /root/reference/pkg/src/specpart/). A maintainer binds them with ctypes
+ * (INTEGRATION.md); paper_1708_07481_b200/_native.py is that binding.
+ *
+ * Conventions
+ *  - every pointer marked "device" is CUDA global memory owned by the caller
+ *    (PyTorch allocates it); "host" pointers are ordinary host memory;
+ *  - dense blocks are row-major (vertex-major): element (i, j) at p[i*ld + j];
+ *  - ``stream`` is a cudaStream_t passed as void*; work is enqueued on it and
+ *    functions that need a host decision synchronise that stream;
+ *  - no C++ exception crosses the boundary; every function returns a status
+ *    code and spb_last_error() holds the message of the calling thread;
+ *  - reentrant: no global mutable state besides the per-thread error string.
+ */
+#ifndef SPECPART_B200_H
+#define SPECPART_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#if defined(__GNUC__)
+#define SPB_API __attribute__((visibility("default")))
+#else
+#define SPB_API
+#endif
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* Status codes; map 1:1 onto specpart's exception classes (errors.py:4-53). */
+enum {
+  SPB_OK = 0,
+  SPB_ERR_CONTRACT = 1,       /* ContractError: inconsistent shapes/lengths      */
+  SPB_ERR_DOMAIN = 2,         /* DomainError: argument value outside its domain   */
+  SPB_ERR_CONDITIONING = 3,   /* ConditioningError (lobpcg.py:168-177, :215)      */
+  SPB_ERR_SOLVER = 4,         /* SolverError with a state (lobpcg.py:343-347,:426)*/
+  SPB_ERR_SOLVER_NOSTATE = 5, /* SolverError(state=None) (lobpcg.py:321-327)      */
+  SPB_ERR_ASSIGNMENT = 6,     /* AssignmentError (spectral.py:156-161)            */
+  SPB_ERR_CUDA = 7,           /* CUDA runtime failure                             */
+  SPB_ERR_WORKSPACE = 8,      /* workspace smaller than the size query returned   */
+  SPB_ERR_CALLBACK = 9        /* a host callback reported failure                 */
+};
+
+/* Storage type of the n-row dense blocks and of the operator values. */
+enum { SPB_F32 = 0, SPB_F64 = 1 };
+
+/* CSR build modes. */
+enum {
+  SPB_CSR_DIRECTED = 0,  /* A: from_edges (graph.py:135-145)                     */
+  SPB_CSR_SYMMETRIZED = 1, /* W = A + A', degrees of A (graph.py:220-250)        */
+  SPB_CSR_AS_SYMMETRIC = 2 /* from_edges(symmetric=True): W = A, row-sum degrees */
+};
+
+SPB_API const char* spb_last_error(void);
+SPB_API int spb_version(void);
+SPB_API int spb_device_sm_count(void);
+
+/* ---------------- (a) edge list -> CSR + degrees ------------------------------
+ * Replaces _coerce_edges/from_edges (graph.py:106-145), symmetrize
+ * (graph.py:220-236) and degrees (graph.py:239-250).
+ * src, dst: device int64[m]; w: device float64[m] or NULL (unit weights).
+ * Outputs (device): row_ptr int32[n+1]; col int32[cap]; val float64[cap];
+ * deg float64[n] (may be NULL for SPB_CSR_DIRECTED); cap = m (DIRECTED,
+ * AS_SYMMETRIC) or 2m (SYMMETRIZED). *nnz_out (host) receives the entry count.
+ * Errors: SPB_ERR_DOMAIN for an endpoint outside [0, n) or a negative weight.
+ * Bit-exact to the reference for integer-valued weights (all sums exact);
+ * duplicate weights are summed in input order. */
+SPB_API size_t spb_csr_build_workspace(int64_t m_edges, int32_t n, int mode);
+SPB_API int spb_csr_build(const int64_t* src, const int64_t* dst, const double* w, int64_t m_edges,
+                  int32_t n, int mode, void* ws, size_t ws_bytes, int32_t* row_ptr,
+                  int32_t* col, double* val, double* deg, int64_t* nnz_out, void* stream);
+
+/* float64 -> dtype conversion of a device vector (operator values/degrees). */
+SPB_API int spb_cast(const double* in, int64_t count, int dtype, void* out, void* stream);
+/* Strided 2-D copy/convert between float64 and dtype blocks (device). */
+SPB_API int spb_copy_block(int src_dtype, const void* src, int64_t lds, int dst_dtype, void* dst,
+                   int64_t ldd, int64_t rows, int32_t cols, void* stream);
+/* max over a device float64 vector -> host (LaplacianOperator.scale_hint, graph.py:314). */
+SPB_API int spb_max_f64(const double* v, int64_t count, double* out_host, void* stream);
+
+/* ---------------- (b) Laplacian SpMM ------------------------------------------
+ * Y[i, 0:ncols] = deg[i]*X[i, :] - sum_e val[e] * X[col[e], :] for rows
+ * [row_begin, row_end) of the symmetrised CSR W: laplacian_apply
+ * (graph.py:253-278) on the symmetrised operator. X and Y must not alias. */
+SPB_API int spb_laplacian_spmm(int dtype, int32_t row_begin, int32_t row_end, const int32_t* row_ptr,
+                       const int32_t* col, const void* val, const void* deg, const void* x,
+                       int64_t ldx, int32_t ncols, void* y, int64_t ldy, void* stream);
+
+/* ---------------- (c)(d) LOBPCG -----------------------------------------------
+ * Operator handle for the solve (graph.py:300-317 / lobpcg.py:132-151). */
+enum { SPB_OP_LAPLACIAN = 0, SPB_OP_DENSE = 1 };
+typedef struct {
+  int kind;              /* SPB_OP_LAPLACIAN or SPB_OP_DENSE                       */
+  int32_t n;             /* operator dimension                                     */
+  const int32_t* row_ptr;/* LAPLACIAN: CSR of W (device)                           */
+  const int32_t* col;
+  const void* val;       /* dtype values of W                                      */
+  const void* deg;       /* dtype degrees                                          */
+  const double* dense;   /* DENSE: device float64 n x n row-major                  */
+  double scale_hint;     /* max degree (graph.py:314) / max row abs-sum (lobpcg.py:143) */
+} spb_operator;
+
+/* SolverConfig (lobpcg.py:38-81) plus the solve arguments of lobpcg_solve
+ * (lobpcg.py:263-270). */
+typedef struct {
+  int32_t block_size;    /* l */
+  int32_t max_iter;
+  double tol;
+  double lock_tol;       /* config.lock_tol (0.1*tol unless overridden)            */
+  int32_t n_converge;    /* nc in [1, l]                                           */
+  int32_t deflate_ones;  /* project out the constant vector (lobpcg.py:259-260)    */
+  int32_t has_precond;   /* call the precond callback on R_act (lobpcg.py:361-362) */
+  int32_t reserved;
+} spb_solver_config;
+
+/* callback(it, theta[:l], norms) of lobpcg.py:348-349 (host arrays, copies). */
+typedef void (*spb_iter_cb)(void* user, int32_t it, const double* theta, const double* norms,
+                            int32_t l);
+/* Gaussian refill of dependent columns (lobpcg.py:214): fill rows*cols float64
+ * (row-major) from the solve's numpy Generator; return 0 on success. */
+typedef int (*spb_refill_cb)(void* user, int64_t rows, int32_t cols, double* out);
+/* Preconditioner on the active residual block (host float64 row-major, in place). */
+typedef int (*spb_precond_cb)(void* user, int64_t rows, int32_t cols, double* inout);
+
+SPB_API size_t spb_lobpcg_workspace(int dtype, int32_t n, int32_t l);
+/* x0: device float64 n x l row-major (copied; lobpcg.py:281,304). On return
+ * (status OK or SOLVER) the solver's X block is left in the workspace and
+ * copied to vectors_out (device float64 n x l) when vectors_out != NULL;
+ * theta_out/norms_out/converged_out are host arrays of length l;
+ * stats_out (host, may be NULL) receives {iterations, spmm_calls, rr_calls,
+ * ladder_drop_p, ladder_rebuild, final_scale_bits_hi, final_scale_bits_lo, 0}. */
+SPB_API int spb_lobpcg_solve(const spb_operator* op, int dtype, const double* x0,
+                     const spb_solver_config* cfg, spb_iter_cb cb, spb_refill_cb refill,
+                     spb_precond_cb precond, void* user, void* ws, size_t ws_bytes,
+                     double* vectors_out, double* theta_out, double* norms_out,
+                     uint8_t* converged_out, int64_t* stats_out, void* stream);
+/* Device pointer/ld of the solver's final X block inside ``ws`` (dtype). */
+SPB_API int spb_lobpcg_result_block(int dtype, int32_t n, int32_t l, void* ws, void** x_out,
+                            int64_t* ld_out);
+
+/* Small projected problem (lobpcg.py:168-177): ga, gb are device float64
+ * m x m (symmetrised inside); gb may be NULL for B = I. Outputs: theta
+ * (device, nev smallest, ascending) and c (device m x nev row-major,
+ * B-orthonormal columns). SPB_ERR_CONDITIONING for non-finite input,
+ * cond2(gb) > 1/sqrt(eps) or gb not positive definite. */
+SPB_API size_t spb_sygv_workspace(int32_t m);
+SPB_API int spb_sygv(const double* ga, const double* gb, int32_t m, int32_t nev, double* theta,
+             double* c, void* ws, size_t ws_bytes, void* stream);
+
+/* ---------------- (e) QRCP assignment -----------------------------------------
+ * assign_clusters_qrcp (spectral.py:134-170) on a device embedding x (dtype,
+ * n x k, row stride ldx): pivots = first k dgeqp3 pivots of x'; seeds sorted;
+ * cond(x[seeds]) <= 1e12 else SPB_ERR_ASSIGNMENT; labels = argmax_j
+ * |(x x[seeds]^-1)_ij| (lowest j on ties), zero rows -> 0, compacted to 0..k'-1.
+ * labels_out: device int32[n]; info_out (host double[4]): {k_found,
+ * zero_rows, cond, ortho_err}. pivots_out (device int32[k]) may be NULL. */
+SPB_API size_t spb_assign_workspace(int32_t n, int32_t k);
+SPB_API int spb_assign_qrcp(int dtype, const void* x, int64_t ldx, int32_t n, int32_t k, void* ws,
+                    size_t ws_bytes, int32_t* labels_out, int32_t* pivots_out,
+                    double* info_out, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SPECPART_B200_H */

@@ -1,0 +1,384 @@
+// (a) Edge list -> CSR (directed A or symmetrised W = A + A') + degrees.
+//
+// Replaces graph.py:106-145 (_coerce_edges/from_edges: self-loops dropped,
+// duplicates summed, columns sorted), graph.py:220-236 (symmetrize: W = A + A',
+// zero sums dropped as scipy's canonical csr binop does) and graph.py:239-250
+// (degrees: bincount over rows + bincount over columns, each in CSR order).
+//
+// Pipeline (all device, no atomics on the data path => deterministic):
+//   1. validate endpoints / weights                       (flags)
+//   2. emit (key = row<<b | col, payload = 2*arc + dir)   fixed slots 2e, 2e+1;
+//      self-loops emit a sentinel key that sorts last
+//   3. stable LSD radix sort of (key, payload), 8-bit digits, ceil(2b/8) passes
+//   4. segment heads; per group sequential sums of the forward (A_ij) and the
+//      reverse (A_ji) weights in arc order; keep flag (W != 0 for SYMMETRIZED)
+//   5. exclusive scan of keep flags -> output slots; scatter col / val / row
+//   6. row_ptr from the row of each output entry; degrees per row as
+//      (sum_j A_ij in column order) + (sum_j A_ji in column order)
+#include "common.cuh"
+#include "scan.cuh"
+
+namespace spb {
+namespace {
+
+constexpr int kSortThreads = 256;
+constexpr int kSortRounds = 16;
+constexpr int kSortTile = kSortThreads * kSortRounds;  // 4096 items per tile
+constexpr int kRadix = 256;
+
+struct BuildFlags {
+  int bad_endpoint;
+  int bad_weight;
+  unsigned long long self_loops;
+};
+
+__global__ void validate_edges(const int64_t* __restrict__ src, const int64_t* __restrict__ dst,
+                               const double* __restrict__ w, int64_t m, int64_t n,
+                               BuildFlags* flags) {
+  int bad_e = 0, bad_w = 0;
+  unsigned loops = 0;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < m;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    int64_t s = src[e], d = dst[e];
+    bad_e |= (s < 0) | (s >= n) | (d < 0) | (d >= n);
+    loops += (s == d);
+    if (w) bad_w |= (w[e] < 0.0);
+  }
+  bad_e = __any_sync(0xffffffffu, bad_e);
+  bad_w = __any_sync(0xffffffffu, bad_w);
+  loops = warp_sum(loops);
+  if ((threadIdx.x & 31) == 0) {
+    if (bad_e) atomicOr(&flags->bad_endpoint, 1);
+    if (bad_w) atomicOr(&flags->bad_weight, 1);
+    if (loops) atomicAdd(&flags->self_loops, (unsigned long long)loops);
+  }
+}
+
+__global__ void emit_entries(const int64_t* __restrict__ src, const int64_t* __restrict__ dst,
+                             int64_t m, int b, int two_sided, uint64_t* __restrict__ keys,
+                             uint32_t* __restrict__ pay) {
+  const uint64_t sentinel = ((uint64_t(1) << (2 * b)) - 1);
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < m;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    uint64_t s = (uint64_t)src[e], d = (uint64_t)dst[e];
+    bool loop = (s == d);
+    if (two_sided) {
+      keys[2 * e] = loop ? sentinel : ((s << b) | d);
+      keys[2 * e + 1] = loop ? sentinel : ((d << b) | s);
+      pay[2 * e] = (uint32_t)(2 * e);
+      pay[2 * e + 1] = (uint32_t)(2 * e + 1);
+    } else {
+      keys[e] = loop ? sentinel : ((s << b) | d);
+      pay[e] = (uint32_t)(2 * e);
+    }
+  }
+}
+
+__global__ void radix_hist(const uint64_t* __restrict__ keys, int64_t count, int shift,
+                           int64_t ntiles, int* __restrict__ counts) {
+  __shared__ int h[kRadix];
+  h[threadIdx.x] = 0;
+  __syncthreads();
+  int64_t base = (int64_t)blockIdx.x * kSortTile;
+#pragma unroll 4
+  for (int r = 0; r < kSortRounds; ++r) {
+    int64_t i = base + r * kSortThreads + threadIdx.x;
+    if (i < count) atomicAdd(&h[(keys[i] >> shift) & 0xff], 1);
+  }
+  __syncthreads();
+  counts[(int64_t)threadIdx.x * ntiles + blockIdx.x] = h[threadIdx.x];
+}
+
+// Stable scatter: items of a tile are ranked in index order (round, warp, lane).
+__global__ void radix_scatter(const uint64_t* __restrict__ kin, const uint32_t* __restrict__ pin,
+                              int64_t count, int shift, int64_t ntiles,
+                              const int* __restrict__ offsets, uint64_t* __restrict__ kout,
+                              uint32_t* __restrict__ pout) {
+  __shared__ int running[kRadix];
+  __shared__ int wcnt[kSortThreads / 32][kRadix];
+  const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+  running[t] = offsets[(int64_t)t * ntiles + blockIdx.x];
+  int64_t base = (int64_t)blockIdx.x * kSortTile;
+  const unsigned lt = (1u << lane) - 1u;
+  for (int r = 0; r < kSortRounds; ++r) {
+#pragma unroll
+    for (int w = 0; w < kSortThreads / 32; ++w) wcnt[w][t] = 0;
+    __syncthreads();
+    int64_t i = base + r * kSortThreads + t;
+    bool valid = i < count;
+    uint64_t k = valid ? kin[i] : 0;
+    uint32_t p = valid ? pin[i] : 0;
+    int d = valid ? (int)((k >> shift) & 0xff) : kRadix;  // kRadix = none
+    unsigned peers = __match_any_sync(0xffffffffu, d);
+    int lrank = __popc(peers & lt);
+    if (valid && lrank == 0) wcnt[warp][d] = __popc(peers);
+    __syncthreads();
+    if (valid) {
+      int pos = running[d] + lrank;
+      for (int w = 0; w < warp; ++w) pos += wcnt[w][d];
+      kout[pos] = k;
+      pout[pos] = p;
+    }
+    __syncthreads();
+    int add = 0;
+#pragma unroll
+    for (int w = 0; w < kSortThreads / 32; ++w) add += wcnt[w][t];
+    running[t] += add;
+    __syncthreads();
+  }
+}
+
+// Group sums: head of each (row, col) group sums forward / reverse weights in
+// payload (= input arc) order. keep[i] = 1 iff i is a head that is emitted.
+__global__ void group_reduce(const uint64_t* __restrict__ keys, const uint32_t* __restrict__ pay,
+                             int64_t valid, const double* __restrict__ w, int drop_zero,
+                             int* __restrict__ keep, double* __restrict__ fsum,
+                             double* __restrict__ rsum, uint8_t* __restrict__ has) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < valid;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    uint64_t k = keys[i];
+    bool head = (i == 0) || (keys[i - 1] != k);
+    int flag = 0;
+    if (head) {
+      double f = 0.0, r = 0.0;
+      int hf = 0, hr = 0;
+      for (int64_t j = i; j < valid && keys[j] == k; ++j) {
+        uint32_t p = pay[j];
+        double x = w ? w[p >> 1] : 1.0;
+        if (p & 1u) {
+          r = hr ? r + x : x;
+          hr = 1;
+        } else {
+          f = hf ? f + x : x;
+          hf = 1;
+        }
+      }
+      double tot = hf ? (hr ? f + r : f) : r;
+      flag = drop_zero ? (tot != 0.0) : 1;
+      fsum[i] = f;
+      rsum[i] = r;
+      has[i] = (uint8_t)(hf | (hr << 1));
+    }
+    keep[i] = flag;
+  }
+}
+
+__global__ void scatter_entries(const uint64_t* __restrict__ keys, int64_t valid, int b,
+                                const int* __restrict__ keep, const int* __restrict__ slot,
+                                const double* __restrict__ fsum, const double* __restrict__ rsum,
+                                const uint8_t* __restrict__ has, int32_t* __restrict__ col,
+                                double* __restrict__ val, int32_t* __restrict__ orow,
+                                double* __restrict__ ofs, double* __restrict__ ors,
+                                uint8_t* __restrict__ ohas) {
+  const uint64_t mask = (uint64_t(1) << b) - 1;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < valid;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    if (!keep[i]) continue;
+    int s = slot[i];
+    uint64_t k = keys[i];
+    uint8_t h = has[i];
+    double f = fsum[i], r = rsum[i];
+    col[s] = (int32_t)(k & mask);
+    orow[s] = (int32_t)(k >> b);
+    val[s] = (h & 1) ? ((h & 2) ? f + r : f) : r;
+    ofs[s] = f;
+    ors[s] = r;
+    ohas[s] = h;
+  }
+}
+
+__global__ void fill_row_ptr(const int32_t* __restrict__ orow, int64_t nnz, int32_t n,
+                             int32_t* __restrict__ row_ptr) {
+  for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j <= nnz;
+       j += (int64_t)gridDim.x * blockDim.x) {
+    int32_t r = j < nnz ? orow[j] : n;
+    int32_t rp = j > 0 ? orow[j - 1] : -1;
+    for (int32_t q = rp + 1; q <= r; ++q) row_ptr[q] = (int32_t)j;
+  }
+}
+
+// d_i = (sum_j A_ij) + (sum_j A_ji), both accumulated in column order, exactly
+// as bincount(rows, w) + bincount(cols, w) over the CSR of A (graph.py:246-249).
+__global__ void row_degrees(const int32_t* __restrict__ row_ptr, const double* __restrict__ ofs,
+                            const double* __restrict__ ors, const uint8_t* __restrict__ ohas,
+                            int32_t n, int with_reverse, double* __restrict__ deg) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    double a = 0.0, c = 0.0;
+    for (int32_t e = row_ptr[i]; e < row_ptr[i + 1]; ++e) {
+      uint8_t h = ohas[e];
+      if (h & 1) a += ofs[e];
+      if (h & 2) c += ors[e];
+    }
+    deg[i] = with_reverse ? a + c : a;
+  }
+}
+
+int key_bits(int32_t n) {
+  int b = 1;
+  while ((int64_t(1) << b) <= (int64_t)n) ++b;
+  return b;
+}
+
+struct BuildLayout {
+  uint64_t *ka, *kb;
+  uint32_t *pa, *pb;
+  int *counts, *scan_tmp, *keep, *slot, *dev_ints;
+  double *fsum, *rsum, *ofs, *ors;
+  uint8_t *has, *ohas;
+  int32_t* orow;
+  BuildFlags* flags;
+};
+
+BuildLayout carve(Arena& a, int64_t cap) {
+  BuildLayout L;
+  int64_t ntiles = ceil_div(cap, kSortTile);
+  L.ka = a.take<uint64_t>(cap);
+  L.kb = a.take<uint64_t>(cap);
+  L.pa = a.take<uint32_t>(cap);
+  L.pb = a.take<uint32_t>(cap);
+  L.counts = a.take<int>((size_t)kRadix * ntiles + 1);
+  L.scan_tmp = a.take<int>(scan_workspace_ints(std::max<int64_t>(cap, kRadix * ntiles)) + 8);
+  L.keep = a.take<int>(cap + 1);
+  L.slot = a.take<int>(cap + 1);
+  L.fsum = a.take<double>(cap);
+  L.rsum = a.take<double>(cap);
+  L.ofs = a.take<double>(cap);
+  L.ors = a.take<double>(cap);
+  L.has = a.take<uint8_t>(cap);
+  L.ohas = a.take<uint8_t>(cap);
+  L.orow = a.take<int32_t>(cap);
+  L.dev_ints = a.take<int>(8);
+  L.flags = a.take<BuildFlags>(1);
+  return L;
+}
+
+int grid_for(int64_t work, int threads = 256) {
+  int64_t g = ceil_div(std::max<int64_t>(work, 1), threads);
+  return (int)std::min<int64_t>(g, (int64_t)num_sms() * 16);
+}
+
+}  // namespace
+}  // namespace spb
+
+using namespace spb;
+
+extern "C" size_t spb_csr_build_workspace(int64_t m_edges, int32_t n, int mode) {
+  Arena a;
+  a.dry = true;
+  int64_t cap = (mode == SPB_CSR_SYMMETRIZED ? 2 : 1) * std::max<int64_t>(m_edges, 1);
+  carve(a, cap);
+  (void)n;
+  return a.used + 1024;
+}
+
+extern "C" int spb_csr_build(const int64_t* src, const int64_t* dst, const double* w,
+                             int64_t m, int32_t n, int mode, void* ws, size_t ws_bytes,
+                             int32_t* row_ptr, int32_t* col, double* val, double* deg,
+                             int64_t* nnz_out, void* stream) {
+  cudaStream_t st = (cudaStream_t)stream;
+  if (n < 0 || m < 0) {
+    set_error("negative sizes");
+    return SPB_ERR_CONTRACT;
+  }
+  if (mode < 0 || mode > 2) {
+    set_error("unknown csr build mode %d", mode);
+    return SPB_ERR_DOMAIN;
+  }
+  if (mode == SPB_CSR_DIRECTED && deg) {
+    set_error("degrees need the reverse arcs: build SYMMETRIZED or AS_SYMMETRIC");
+    return SPB_ERR_CONTRACT;
+  }
+  if (m >= (int64_t(1) << 30)) {
+    set_error("edge count %lld exceeds 2^30 per build", (long long)m);
+    return SPB_ERR_CONTRACT;
+  }
+  const int two = (mode == SPB_CSR_SYMMETRIZED);
+  const int64_t cap = (two ? 2 : 1) * std::max<int64_t>(m, 1);
+  Arena a;
+  a.base = (char*)ws;
+  a.cap = ws_bytes;
+  BuildLayout L = carve(a, cap);
+  if (a.used > ws_bytes) {
+    set_error("csr build workspace too small (%zu < %zu)", ws_bytes, a.used);
+    return SPB_ERR_WORKSPACE;
+  }
+  if (n == 0) {
+    if (m > 0) {
+      set_error("edge endpoint out of range");
+      return SPB_ERR_DOMAIN;
+    }
+    SPB_CUDA(cudaMemsetAsync(row_ptr, 0, sizeof(int32_t), st));
+    *nnz_out = 0;
+    return SPB_OK;
+  }
+  SPB_CUDA(cudaMemsetAsync(L.flags, 0, sizeof(BuildFlags), st));
+  if (m > 0) {
+    validate_edges<<<grid_for(m), 256, 0, st>>>(src, dst, w, m, n, L.flags);
+    SPB_LAUNCH_CHECK();
+  }
+  BuildFlags hf;
+  SPB_CUDA(cudaMemcpyAsync(&hf, L.flags, sizeof(hf), cudaMemcpyDeviceToHost, st));
+  SPB_CUDA(cudaStreamSynchronize(st));
+  if (hf.bad_endpoint) {
+    set_error("edge endpoint out of range");
+    return SPB_ERR_DOMAIN;
+  }
+  if (hf.bad_weight) {
+    set_error("negative edge weight");
+    return SPB_ERR_DOMAIN;
+  }
+  if (m == 0) {
+    SPB_CUDA(cudaMemsetAsync(row_ptr, 0, sizeof(int32_t) * (n + 1), st));
+    if (deg) SPB_CUDA(cudaMemsetAsync(deg, 0, sizeof(double) * n, st));
+    *nnz_out = 0;
+    return SPB_OK;
+  }
+  const int b = key_bits(n);
+  const int64_t count = (two ? 2 : 1) * m;
+  emit_entries<<<grid_for(m), 256, 0, st>>>(src, dst, m, b, two, L.ka, L.pa);
+  SPB_LAUNCH_CHECK();
+
+  // stable LSD radix sort over 2b key bits
+  const int64_t ntiles = ceil_div(count, kSortTile);
+  uint64_t *kin = L.ka, *kout = L.kb;
+  uint32_t *pin = L.pa, *pout = L.pb;
+  for (int shift = 0; shift < 2 * b; shift += 8) {
+    radix_hist<<<ntiles, kSortThreads, 0, st>>>(kin, count, shift, ntiles, L.counts);
+    SPB_TRY(exclusive_scan_i32(L.counts, L.counts, (int64_t)kRadix * ntiles, L.scan_tmp,
+                               nullptr, st));
+    radix_scatter<<<ntiles, kSortThreads, 0, st>>>(kin, pin, count, shift, ntiles, L.counts,
+                                                   kout, pout);
+    SPB_LAUNCH_CHECK();
+    std::swap(kin, kout);
+    std::swap(pin, pout);
+  }
+  // self-loops carry the sentinel key and sort to the end
+  const int64_t valid = count - (two ? 2 : 1) * (int64_t)hf.self_loops;
+  int32_t* dev_total = L.dev_ints;
+  int64_t nnz = 0;
+  if (valid > 0) {
+    group_reduce<<<grid_for(valid), 256, 0, st>>>(kin, pin, valid, w,
+                                                   mode == SPB_CSR_SYMMETRIZED, L.keep, L.fsum,
+                                                   L.rsum, L.has);
+    SPB_LAUNCH_CHECK();
+    SPB_TRY(exclusive_scan_i32(L.keep, L.slot, valid, L.scan_tmp, dev_total, st));
+    int htot = 0;
+    SPB_CUDA(cudaMemcpyAsync(&htot, dev_total, sizeof(int), cudaMemcpyDeviceToHost, st));
+    SPB_CUDA(cudaStreamSynchronize(st));
+    nnz = htot;
+    scatter_entries<<<grid_for(valid), 256, 0, st>>>(kin, valid, b, L.keep, L.slot, L.fsum,
+                                                     L.rsum, L.has, col, val, L.orow, L.ofs,
+                                                     L.ors, L.ohas);
+    SPB_LAUNCH_CHECK();
+  }
+  fill_row_ptr<<<grid_for(nnz + 1), 256, 0, st>>>(L.orow, nnz, n, row_ptr);
+  SPB_LAUNCH_CHECK();
+  if (deg) {
+    row_degrees<<<grid_for(n), 256, 0, st>>>(row_ptr, L.ofs, L.ors, L.ohas, n,
+                                              mode == SPB_CSR_SYMMETRIZED, deg);
+    SPB_LAUNCH_CHECK();
+  }
+  *nnz_out = nnz;
+  return SPB_OK;
+}

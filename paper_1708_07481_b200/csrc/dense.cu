@@ -1,0 +1,428 @@
+// (c) Tall-skinny dense products of the LOBPCG body, CUDA-core path.
+//
+// * gram_batched  — G = U' V for a batch of column blocks (the Rayleigh-Ritz
+//   Grams [X R P]'[LX LR LP] and [X R P]'[X R P] of lobpcg.py:418, the
+//   projection X'R of :366 and the CholQR Gram of :228). Split-K over rows,
+//   products and accumulation in float64 (fp32 inputs multiply exactly in
+//   fp64), per-split partials reduced in a fixed order => deterministic.
+// * block_update  — out = init + sum_s A_s C_s with emit points, row-local and
+//   therefore safe in place: X' = [X R P] C and P' = [R P] C[l:] share one
+//   accumulator (lobpcg.py:436-439), R -= X (X'R) (:366-369), R <- R inv (:237).
+// * column_reduce — residual R = LX - X diag(theta) fused with its column norms
+//   (lobpcg.py:338-341), plain column sums of squares (P norms :382) and sums
+//   (mean removal :259-260); per-block partials, fixed-order final reduction.
+// * gather / scale columns — soft-lock compaction (_move_columns :250-256) and
+//   P normalisation (:391-393).
+#include "dense.cuh"
+
+namespace spb {
+namespace {
+
+// ----------------------------------------------------------------------------
+// Gram: 64x64 output tile per CTA, 256 threads, 4x4 fp64 micro-tile each.
+constexpr int GT = 64;
+constexpr int GK = 16;
+
+template <typename T>
+__global__ void __launch_bounds__(256)
+gram_kernel(GramBatch b, int64_t n, int64_t kchunk, int ldo, int64_t split_stride,
+            double* __restrict__ part) {
+  __shared__ double Us[GK][GT + 1];
+  __shared__ double Vs[GK][GT + 1];
+  const int tile = blockIdx.x;
+  int j = 0;
+  while (j + 1 < b.njobs && tile >= b.tile_start[j + 1]) ++j;
+  const GramJob jb = b.job[j];
+  const int local = tile - b.tile_start[j];
+  const int tq_count = (jb.q + GT - 1) / GT;
+  const int tp = local / tq_count, tq = local % tq_count;
+  const int p0 = tp * GT, q0 = tq * GT;
+  const int64_t k0 = (int64_t)blockIdx.y * kchunk;
+  const int64_t k1 = min(n, k0 + kchunk);
+  const int tid = threadIdx.x, tx = tid & 15, ty = tid >> 4;
+  const T* U = (const T*)jb.U;
+  const T* V = (const T*)jb.V;
+  double acc[4][4];
+#pragma unroll
+  for (int a = 0; a < 4; ++a)
+#pragma unroll
+    for (int c = 0; c < 4; ++c) acc[a][c] = 0.0;
+
+  for (int64_t kb = k0; kb < k1; kb += GK) {
+#pragma unroll
+    for (int e = tid; e < GK * GT; e += 256) {
+      const int r = e / GT, c = e % GT;
+      const int64_t k = kb + r;
+      double u = 0.0, v = 0.0;
+      if (k < k1) {
+        if (p0 + c < jb.p) u = (double)U[k * jb.ldu + p0 + c];
+        if (q0 + c < jb.q) v = (double)V[k * jb.ldv + q0 + c];
+      }
+      Us[r][c] = u;
+      Vs[r][c] = v;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < GK; ++k) {
+      double a[4], bv[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) a[i] = Us[k][ty * 4 + i];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) bv[i] = Vs[k][tx * 4 + i];
+#pragma unroll
+      for (int x = 0; x < 4; ++x)
+#pragma unroll
+        for (int y = 0; y < 4; ++y) acc[x][y] = fma(a[x], bv[y], acc[x][y]);
+    }
+    __syncthreads();
+  }
+  double* out = part + (int64_t)blockIdx.y * split_stride;
+#pragma unroll
+  for (int x = 0; x < 4; ++x) {
+    const int i = p0 + ty * 4 + x;
+    if (i >= jb.p) continue;
+#pragma unroll
+    for (int y = 0; y < 4; ++y) {
+      const int c = q0 + tx * 4 + y;
+      if (c < jb.q) out[(int64_t)(jb.out_r + i) * ldo + jb.out_c + c] = acc[x][y];
+    }
+  }
+}
+
+__global__ void sum_splits(const double* __restrict__ part, int ksplit, int64_t split_stride,
+                           int rows, int cols, int ldp, double* __restrict__ out, int ldo) {
+  const int64_t total = (int64_t)rows * cols;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int r = (int)(e / cols), c = (int)(e % cols);
+    double s = 0.0;
+    for (int k = 0; k < ksplit; ++k) s += part[k * split_stride + (int64_t)r * ldp + c];
+    out[(int64_t)r * ldo + c] = s;
+  }
+}
+
+int choose_ksplit(int64_t n, int tiles) {
+  const int target = 2 * num_sms();
+  int64_t ks = ceil_div(target, std::max(tiles, 1));
+  ks = std::min<int64_t>(ks, ceil_div(n, 512));
+  return (int)std::max<int64_t>(ks, 1);
+}
+
+// ----------------------------------------------------------------------------
+// Block update: 32 rows x q columns per CTA (q <= 256), 256 threads as 8 x 32.
+constexpr int UR = 32;   // rows per CTA
+constexpr int UQ = 256;  // max columns
+
+template <typename T>
+__global__ void __launch_bounds__(256)
+update_kernel(UpdParams P, int64_t n) {
+  constexpr int UK = sizeof(T) == 4 ? 32 : 16;  // k chunk (static smem <= 48 KB)
+  __shared__ T As[UR][UK + 1];
+  __shared__ T Cs[UK][UQ];
+  const int tid = threadIdx.x, tx = tid & 31, ty = tid >> 5;  // ty: 8 row groups of 4
+  const int64_t r0 = (int64_t)blockIdx.x * UR;
+  const int q = P.q;
+  const int qv = (q + 31) / 32;
+  T acc[4][8];
+#pragma unroll
+  for (int a = 0; a < 4; ++a)
+#pragma unroll
+    for (int c = 0; c < 8; ++c) {
+      T v = T(0);
+      const int64_t r = r0 + ty * 4 + a;
+      const int col = tx + 32 * c;
+      if (P.init && c < qv && col < q && r < n) v = ((const T*)P.init)[r * P.ldi + col];
+      acc[a][c] = v;
+    }
+  for (int s = 0; s < P.nseg; ++s) {
+    const UpdSeg sg = P.seg[s];
+    const T* A = (const T*)sg.A;
+    for (int k0 = 0; k0 < sg.w; k0 += UK) {
+      const int kc = min(UK, sg.w - k0);
+      for (int e = tid; e < UR * UK; e += 256) {
+        const int r = e / UK, k = e % UK;
+        const int64_t gr = r0 + r;
+        As[r][k] = (gr < n && k < kc) ? A[gr * sg.lda + k0 + k] : T(0);
+      }
+      for (int e = tid; e < UK * qv * 32; e += 256) {
+        const int k = e / (qv * 32), c = e % (qv * 32);
+        Cs[k][c] = (k < kc && c < q) ? (T)sg.C[(int64_t)(k0 + k) * sg.ldc + c] : T(0);
+      }
+      __syncthreads();
+      for (int k = 0; k < kc; ++k) {
+        T a[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) a[i] = As[ty * 4 + i][k];
+#pragma unroll
+        for (int c = 0; c < 8; ++c) {
+          if (c < qv) {
+            const T cv = Cs[k][tx + 32 * c];
+#pragma unroll
+            for (int i = 0; i < 4; ++i) acc[i][c] = fma(a[i], cv, acc[i][c]);
+          }
+        }
+      }
+      __syncthreads();
+    }
+    if (sg.emit) {
+      T* O = (T*)sg.out;
+#pragma unroll
+      for (int a = 0; a < 4; ++a) {
+        const int64_t r = r0 + ty * 4 + a;
+        if (r >= n) continue;
+#pragma unroll
+        for (int c = 0; c < 8; ++c) {
+          const int col = tx + 32 * c;
+          if (c < qv && col < q) O[r * sg.ldo + col] = acc[a][c];
+        }
+      }
+    }
+  }
+}
+
+// ----------------------------------------------------------------------------
+// Column reductions: each CTA covers a contiguous row range; thread layout
+// (ry, cx) with cx over columns (warp-coalesced along a row), ry over rows.
+constexpr int CRB = 256;
+
+template <typename T>
+__global__ void __launch_bounds__(CRB)
+colreduce_kernel(int kind, const T* __restrict__ A, int64_t lda, int cols, int64_t n,
+                 int64_t rows_per_block, const T* __restrict__ X, int64_t ldx,
+                 const double* __restrict__ theta, T* __restrict__ R, int64_t ldr,
+                 double* __restrict__ part) {
+  extern __shared__ double sred[];  // [ry][cw]
+  const int cw = min(((cols + 31) / 32) * 32, CRB);
+  const int nry = CRB / cw;
+  const int tid = threadIdx.x;
+  const int cx = tid % cw, ry = tid / cw;
+  const int64_t rb = (int64_t)blockIdx.x * rows_per_block;
+  const int64_t re = min(n, rb + rows_per_block);
+  for (int c0 = 0; c0 < cols; c0 += cw) {
+    const int c = c0 + cx;
+    double s = 0.0;
+    if (ry < nry && c < cols) {
+      T th = T(0);
+      if (kind == CR_RESIDUAL) th = (T)theta[c];
+      for (int64_t r = rb + ry; r < re; r += nry) {
+        T v = A[r * lda + c];
+        if (kind == CR_RESIDUAL) {
+          v = v - X[r * ldx + c] * th;
+          R[r * ldr + c] = v;
+        }
+        const double dv = (double)v;
+        s += (kind == CR_SUM) ? dv : dv * dv;
+      }
+    }
+    if (ry < nry) sred[ry * cw + cx] = s;
+    __syncthreads();
+    if (ry == 0 && c < cols) {
+      double t = 0.0;
+      for (int y = 0; y < nry; ++y) t += sred[y * cw + cx];
+      part[(int64_t)blockIdx.x * cols + c] = t;
+    }
+    __syncthreads();
+  }
+}
+
+__global__ void colreduce_final(const double* __restrict__ part, int blocks, int cols,
+                                double* __restrict__ out) {
+  for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < cols; c += gridDim.x * blockDim.x) {
+    double s = 0.0;
+    for (int b = 0; b < blocks; ++b) s += part[(int64_t)b * cols + c];
+    out[c] = s;
+  }
+}
+
+int colreduce_blocks(int64_t n) {
+  return (int)std::max<int64_t>(1, std::min<int64_t>(2 * num_sms(), ceil_div(n, 64)));
+}
+
+// ----------------------------------------------------------------------------
+template <typename T>
+__global__ void gather_cols_kernel(T* __restrict__ A, int64_t lda, int64_t n,
+                                   const int* __restrict__ idx, int count) {
+  // one warp per row: read all selected values, then write (left-moving, in place)
+  const int lane = threadIdx.x & 31;
+  const int64_t row = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  if (row >= n) return;
+  T* a = A + row * lda;
+  T v[8];
+#pragma unroll
+  for (int t = 0; t < 8; ++t) {
+    const int j = lane + 32 * t;
+    v[t] = j < count ? a[idx[j]] : T(0);
+  }
+  __syncwarp();
+#pragma unroll
+  for (int t = 0; t < 8; ++t) {
+    const int j = lane + 32 * t;
+    if (j < count) a[j] = v[t];
+  }
+}
+
+template <typename T>
+__global__ void scale_cols_kernel(T* __restrict__ A, int64_t lda, int64_t n,
+                                  const double* __restrict__ s, int count) {
+  const int64_t total = n * count;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = e / count;
+    const int c = (int)(e - r * count);
+    A[r * lda + c] = (T)((double)A[r * lda + c] * s[c]);
+  }
+}
+
+template <typename T>
+__global__ void sub_means_kernel(T* __restrict__ A, int64_t lda, int64_t n, int cols,
+                                 const double* __restrict__ sums) {
+  const int64_t total = n * cols;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = e / cols;
+    const int c = (int)(e - r * cols);
+    A[r * lda + c] = (T)((double)A[r * lda + c] - sums[c] / (double)n);
+  }
+}
+
+int grid_1d(int64_t total) {
+  return (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(total, 256), (int64_t)num_sms() * 8));
+}
+
+}  // namespace
+
+size_t gram_partial_doubles(int64_t n, int tiles, int out_rows, int out_cols, int* ksplit_out) {
+  int ks = choose_ksplit(n, tiles);
+  if (ksplit_out) *ksplit_out = ks;
+  return (size_t)ks * out_rows * out_cols;
+}
+
+int gram_batched(int dtype, const GramBatch& b, int64_t n, int out_rows, int out_cols,
+                 double* partial, size_t partial_cap, double* out, int ldo, cudaStream_t st) {
+  const int tiles = b.tile_start[b.njobs];
+  if (tiles == 0) return SPB_OK;
+  int ks = choose_ksplit(n, tiles);
+  while (ks > 1 && (size_t)ks * out_rows * out_cols > partial_cap) --ks;
+  if ((size_t)ks * out_rows * out_cols > partial_cap) {
+    set_error("gram partial workspace too small");
+    return SPB_ERR_WORKSPACE;
+  }
+  const int64_t kchunk = round_up(ceil_div(std::max<int64_t>(n, 1), ks), GK);
+  const int64_t stride = (int64_t)out_rows * out_cols;
+  dim3 grid(tiles, ks);
+  if (n > 0) {
+    if (dtype == SPB_F32)
+      gram_kernel<float><<<grid, 256, 0, st>>>(b, n, kchunk, out_cols, stride, partial);
+    else
+      gram_kernel<double><<<grid, 256, 0, st>>>(b, n, kchunk, out_cols, stride, partial);
+    SPB_LAUNCH_CHECK();
+  } else {
+    SPB_CUDA(cudaMemsetAsync(partial, 0, sizeof(double) * stride, st));
+    ks = 1;
+  }
+  sum_splits<<<grid_1d(stride), 256, 0, st>>>(partial, ks, stride, out_rows, out_cols, out_cols,
+                                               out, ldo);
+  SPB_LAUNCH_CHECK();
+  return SPB_OK;
+}
+
+int block_update(int dtype, const UpdParams& p, int64_t n, cudaStream_t st) {
+  if (p.q > UQ) {
+    set_error("block update supports at most %d columns (got %d)", UQ, p.q);
+    return SPB_ERR_CONTRACT;
+  }
+  if (n <= 0 || p.q <= 0) return SPB_OK;
+  const int64_t blocks = ceil_div(n, UR);
+  if (dtype == SPB_F32)
+    update_kernel<float><<<blocks, 256, 0, st>>>(p, n);
+  else
+    update_kernel<double><<<blocks, 256, 0, st>>>(p, n);
+  SPB_LAUNCH_CHECK();
+  return SPB_OK;
+}
+
+size_t colreduce_partial_doubles(int64_t n, int cols) {
+  return (size_t)colreduce_blocks(n) * std::max(cols, 1);
+}
+
+int column_reduce(int dtype, int kind, const void* A, int64_t lda, int cols, int64_t n,
+                  const void* X, int64_t ldx, const double* theta, void* R, int64_t ldr,
+                  double* partial, double* out, cudaStream_t st) {
+  if (cols <= 0) return SPB_OK;
+  const int blocks = colreduce_blocks(n);
+  const int64_t rpb = ceil_div(std::max<int64_t>(n, 1), blocks);
+  const size_t smem = sizeof(double) * CRB;
+  if (dtype == SPB_F32)
+    colreduce_kernel<float><<<blocks, CRB, smem, st>>>(kind, (const float*)A, lda, cols, n, rpb,
+                                                       (const float*)X, ldx, theta, (float*)R,
+                                                       ldr, partial);
+  else
+    colreduce_kernel<double><<<blocks, CRB, smem, st>>>(kind, (const double*)A, lda, cols, n,
+                                                        rpb, (const double*)X, ldx, theta,
+                                                        (double*)R, ldr, partial);
+  colreduce_final<<<(int)ceil_div(cols, 256), 256, 0, st>>>(partial, blocks, cols, out);
+  SPB_LAUNCH_CHECK();
+  return SPB_OK;
+}
+
+int gather_columns(int dtype, void* A, int64_t lda, int64_t n, const int* idx, int count,
+                   cudaStream_t st) {
+  if (count > 256) {
+    set_error("column gather supports at most 256 columns");
+    return SPB_ERR_CONTRACT;
+  }
+  if (n <= 0 || count <= 0) return SPB_OK;
+  const int64_t blocks = ceil_div(n * 32, 256);
+  if (dtype == SPB_F32)
+    gather_cols_kernel<float><<<blocks, 256, 0, st>>>((float*)A, lda, n, idx, count);
+  else
+    gather_cols_kernel<double><<<blocks, 256, 0, st>>>((double*)A, lda, n, idx, count);
+  SPB_LAUNCH_CHECK();
+  return SPB_OK;
+}
+
+int scale_columns(int dtype, void* A, int64_t lda, int64_t n, const double* s, int count,
+                  cudaStream_t st) {
+  if (n <= 0 || count <= 0) return SPB_OK;
+  if (dtype == SPB_F32)
+    scale_cols_kernel<float><<<grid_1d(n * count), 256, 0, st>>>((float*)A, lda, n, s, count);
+  else
+    scale_cols_kernel<double><<<grid_1d(n * count), 256, 0, st>>>((double*)A, lda, n, s, count);
+  SPB_LAUNCH_CHECK();
+  return SPB_OK;
+}
+
+int subtract_column_means(int dtype, void* A, int64_t lda, int64_t n, int cols,
+                          const double* sums, cudaStream_t st) {
+  if (n <= 0 || cols <= 0) return SPB_OK;
+  if (dtype == SPB_F32)
+    sub_means_kernel<float><<<grid_1d(n * cols), 256, 0, st>>>((float*)A, lda, n, cols, sums);
+  else
+    sub_means_kernel<double><<<grid_1d(n * cols), 256, 0, st>>>((double*)A, lda, n, cols, sums);
+  SPB_LAUNCH_CHECK();
+  return SPB_OK;
+}
+
+// Dense operator Y = A X (DenseOperator, lobpcg.py:132-151): float64 storage only.
+int dense_apply(const double* Adense, int64_t n, const void* X, int64_t ldx, int cols, void* Y,
+                int64_t ldy, int dtype, double* scratch, cudaStream_t st) {
+  if (dtype != SPB_F64) {
+    set_error("dense operators need float64 storage");
+    return SPB_ERR_DOMAIN;
+  }
+  (void)scratch;
+  UpdParams p{};
+  p.nseg = 1;
+  p.q = cols;
+  p.seg[0].A = Adense;
+  p.seg[0].lda = n;
+  p.seg[0].w = (int)n;
+  p.seg[0].C = (const double*)X;
+  p.seg[0].ldc = ldx;
+  p.seg[0].emit = 1;
+  p.seg[0].out = Y;
+  p.seg[0].ldo = ldy;
+  return block_update(SPB_F64, p, n, st);
+}
+
+}  // namespace spb

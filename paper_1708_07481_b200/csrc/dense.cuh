@@ -1,0 +1,73 @@
+// Tall-skinny dense kernels of the LOBPCG body (CUDA-core path).
+#pragma once
+#include "common.cuh"
+
+namespace spb {
+
+constexpr int kMaxGramJobs = 20;
+
+// One block of a batched Gram: out[out_r + i, out_c + j] = sum_k U[k, i] * V[k, j]
+struct GramJob {
+  const void* U;
+  const void* V;
+  int64_t ldu, ldv;
+  int p, q;
+  int out_r, out_c;
+};
+
+struct GramBatch {
+  GramJob job[kMaxGramJobs];
+  int tile_start[kMaxGramJobs + 1];
+  int njobs;
+};
+
+// Segmented tall-skinny update: acc = init (or 0); for s in segments:
+// acc += A_s[:, 0:w_s] * C_s[0:w_s, 0:q]; if emit_s: out_s = acc.
+struct UpdSeg {
+  const void* A;
+  int64_t lda;
+  const double* C;
+  int64_t ldc;
+  void* out;
+  int64_t ldo;
+  int w;
+  int emit;
+};
+
+struct UpdParams {
+  UpdSeg seg[3];
+  const void* init;
+  int64_t ldi;
+  int nseg;
+  int q;
+};
+
+// Column-reduction kinds.
+enum ColReduce { CR_SUMSQ = 0, CR_SUM = 1, CR_RESIDUAL = 2 };
+
+// ---- host entry points (dense.cu) -------------------------------------------
+size_t gram_partial_doubles(int64_t n, int tiles, int out_rows, int out_cols, int* ksplit_out);
+int gram_batched(int dtype, const GramBatch& b, int64_t n, int out_rows, int out_cols,
+                 double* partial, size_t partial_cap, double* out, int ldo, cudaStream_t st);
+int block_update(int dtype, const UpdParams& p, int64_t n, cudaStream_t st);
+// sums[c] over rows of column c (kind SUMSQ / SUM), or the residual
+// R = LX - X diag(theta) written to R with its column sums of squares.
+size_t colreduce_partial_doubles(int64_t n, int cols);
+int column_reduce(int dtype, int kind, const void* A, int64_t lda, int cols, int64_t n,
+                  const void* X, int64_t ldx, const double* theta, void* R, int64_t ldr,
+                  double* partial, double* out, cudaStream_t st);
+int gather_columns(int dtype, void* A, int64_t lda, int64_t n, const int* idx, int count,
+                   cudaStream_t st);
+int scale_columns(int dtype, void* A, int64_t lda, int64_t n, const double* s, int count,
+                  cudaStream_t st);
+int subtract_column_means(int dtype, void* A, int64_t lda, int64_t n, int cols,
+                          const double* sums, cudaStream_t st);
+int dense_apply(const double* Adense, int64_t n, const void* X, int64_t ldx, int cols, void* Y,
+                int64_t ldy, int dtype, double* scratch, cudaStream_t st);
+int copy_block(int sdt, const void* s, int64_t lds, int ddt, void* d, int64_t ldd, int64_t rows,
+               int32_t cols, cudaStream_t st);
+int laplacian_spmm(int dtype, int32_t r0, int32_t r1, const int32_t* rp, const int32_t* ci,
+                   const void* cv, const void* deg, const void* x, int64_t ldx, int ncols,
+                   void* y, int64_t ldy, cudaStream_t st);
+
+}  // namespace spb

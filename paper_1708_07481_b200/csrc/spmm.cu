@@ -1,0 +1,214 @@
+// (b) Matrix-free Laplacian block product on the symmetrised CSR:
+//     Y[i, :] = d_i X[i, :] - sum_{e in row i} W_e X[col_e, :]
+// Replaces laplacian_apply (graph.py:253-278) / LaplacianOperator.apply
+// (graph.py:316-317), which run scipy's serial csr_matvecs twice (A and A').
+//
+// One warp per row. The row's (col, val) pairs are loaded 32 at a time,
+// coalesced, and broadcast with shuffles. The dense block is vertex-major, so a
+// neighbour's row of X is one contiguous run of ncols values, read as 128-bit
+// vectors (float4 / double2). When the row is narrower than a warp's vector
+// width the warp splits into lane groups that walk different neighbours and
+// are combined with xor-shuffles at the end. Wide blocks are processed in
+// column panels sized so the gathered panel of X stays L2-resident.
+#include "common.cuh"
+
+namespace spb {
+namespace {
+
+template <typename T> struct Vec;
+template <> struct Vec<float> { using type = float4; static constexpr int N = 4; };
+template <> struct Vec<double> { using type = double2; static constexpr int N = 2; };
+
+template <typename V> __device__ __forceinline__ V vzero();
+template <> __device__ __forceinline__ float4 vzero<float4>() { return make_float4(0, 0, 0, 0); }
+template <> __device__ __forceinline__ double2 vzero<double2>() { return make_double2(0, 0); }
+
+__device__ __forceinline__ void vfma(float4& a, float s, const float4& x) {
+  a.x = fmaf(s, x.x, a.x); a.y = fmaf(s, x.y, a.y); a.z = fmaf(s, x.z, a.z); a.w = fmaf(s, x.w, a.w);
+}
+__device__ __forceinline__ void vfma(double2& a, double s, const double2& x) {
+  a.x = fma(s, x.x, a.x); a.y = fma(s, x.y, a.y);
+}
+__device__ __forceinline__ void vshfl_add(float4& a, int o) {
+  a.x += __shfl_xor_sync(0xffffffffu, a.x, o); a.y += __shfl_xor_sync(0xffffffffu, a.y, o);
+  a.z += __shfl_xor_sync(0xffffffffu, a.z, o); a.w += __shfl_xor_sync(0xffffffffu, a.w, o);
+}
+__device__ __forceinline__ void vshfl_add(double2& a, int o) {
+  a.x += __shfl_xor_sync(0xffffffffu, a.x, o); a.y += __shfl_xor_sync(0xffffffffu, a.y, o);
+}
+__device__ __forceinline__ float4 vaxpy_out(float d, const float4& x, const float4& a) {
+  return make_float4(fmaf(d, x.x, -a.x), fmaf(d, x.y, -a.y), fmaf(d, x.z, -a.z), fmaf(d, x.w, -a.w));
+}
+__device__ __forceinline__ double2 vaxpy_out(double d, const double2& x, const double2& a) {
+  return make_double2(fma(d, x.x, -a.x), fma(d, x.y, -a.y));
+}
+__device__ __forceinline__ float vget(const float4& v, int i) {
+  return i == 0 ? v.x : i == 1 ? v.y : i == 2 ? v.z : v.w;
+}
+__device__ __forceinline__ double vget(const double2& v, int i) { return i == 0 ? v.x : v.y; }
+
+// Vectorised path: ldx, ldy multiples of the vector width, pointers aligned.
+// GS = lanes per neighbour group (power of two), chunks = vectors per row panel.
+template <typename T, int GS>
+__global__ void __launch_bounds__(256)
+spmm_vec(int32_t r0, int32_t r1, const int32_t* __restrict__ rp, const int32_t* __restrict__ ci,
+         const T* __restrict__ cv, const T* __restrict__ deg, const T* __restrict__ x,
+         int64_t ldx, int c0, int ncols, T* __restrict__ y, int64_t ldy) {
+  using V = typename Vec<T>::type;
+  constexpr int VN = Vec<T>::N;
+  constexpr int NG = 32 / GS;
+  const int lane = threadIdx.x & 31;
+  const int g = lane / GS, gl = lane % GS;
+  const int32_t row = r0 + (int32_t)((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5);
+  if (row >= r1) return;
+  const int nvec = (ncols + VN - 1) / VN;
+  const int32_t e0 = rp[row], e1 = rp[row + 1];
+  for (int vbase = 0; vbase < nvec; vbase += GS) {
+    const int v = vbase + gl;
+    const bool act = v < nvec;
+    const int64_t coff = c0 + (int64_t)v * VN;
+    V acc = vzero<V>();
+    for (int32_t eb = e0; eb < e1; eb += 32) {
+      const int32_t my = eb + lane;
+      int32_t cj = 0;
+      T wv = T(0);
+      if (my < e1) {
+        cj = __ldg(ci + my);
+        wv = __ldg(cv + my);
+      }
+      const int cnt = min(32, e1 - eb);
+#pragma unroll 4
+      for (int kk = 0; kk < cnt; kk += NG) {  // warp-uniform trip count
+        const int k = kk + g;
+        const int srcl = k < cnt ? k : 0;
+        const int32_t j = __shfl_sync(0xffffffffu, cj, srcl);
+        const T w = __shfl_sync(0xffffffffu, wv, srcl);
+        if (act && k < cnt) {
+          const V xv = __ldg(reinterpret_cast<const V*>(x + (int64_t)j * ldx + coff));
+          vfma(acc, w, xv);
+        }
+      }
+      // keep the warp converged for the shuffles of the next batch
+      __syncwarp();
+    }
+#pragma unroll
+    for (int o = GS; o < 32; o <<= 1) vshfl_add(acc, o);
+    if (g == 0 && act) {
+      const V xi = *reinterpret_cast<const V*>(x + (int64_t)row * ldx + coff);
+      const T d = deg[row];
+      V out = vaxpy_out(d, xi, acc);
+      T* yp = y + (int64_t)row * ldy + coff;
+      if (coff - c0 + VN <= ncols) {
+        *reinterpret_cast<V*>(yp) = out;
+      } else {
+        for (int q = 0; q < VN && coff - c0 + q < ncols; ++q) yp[q] = vget(out, q);
+      }
+    }
+  }
+}
+
+// Scalar fallback for unaligned / odd strides.
+template <typename T>
+__global__ void __launch_bounds__(256)
+spmm_scalar(int32_t r0, int32_t r1, const int32_t* __restrict__ rp, const int32_t* __restrict__ ci,
+            const T* __restrict__ cv, const T* __restrict__ deg, const T* __restrict__ x,
+            int64_t ldx, int ncols, T* __restrict__ y, int64_t ldy) {
+  const int lane = threadIdx.x & 31;
+  const int32_t row = r0 + (int32_t)((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5);
+  if (row >= r1) return;
+  const int32_t e0 = rp[row], e1 = rp[row + 1];
+  for (int c = lane; c < ((ncols + 31) / 32) * 32; c += 32) {
+    T acc = T(0);
+    for (int32_t eb = e0; eb < e1; eb += 32) {
+      const int32_t my = eb + lane;
+      int32_t cj = 0;
+      T wv = T(0);
+      if (my < e1) { cj = ci[my]; wv = cv[my]; }
+      const int cnt = min(32, e1 - eb);
+      for (int k = 0; k < cnt; ++k) {
+        const int32_t j = __shfl_sync(0xffffffffu, cj, k);
+        const T w = __shfl_sync(0xffffffffu, wv, k);
+        if (c < ncols) acc += w * x[(int64_t)j * ldx + c];
+      }
+    }
+    if (c < ncols) y[(int64_t)row * ldy + c] = deg[row] * x[(int64_t)row * ldx + c] - acc;
+  }
+}
+
+template <typename T>
+int launch_spmm(int32_t r0, int32_t r1, const int32_t* rp, const int32_t* ci, const T* cv,
+                const T* deg, const T* x, int64_t ldx, int ncols, T* y, int64_t ldy,
+                cudaStream_t st) {
+  constexpr int VN = Vec<T>::N;
+  const int64_t rows = (int64_t)r1 - r0;
+  if (rows <= 0 || ncols <= 0) return SPB_OK;
+  const int threads = 256;
+  const int64_t blocks = ceil_div(rows * 32, threads);
+  const bool aligned = (ldx % VN == 0) && (ldy % VN == 0) &&
+                       ((uintptr_t)x % (VN * sizeof(T)) == 0) &&
+                       ((uintptr_t)y % (VN * sizeof(T)) == 0);
+  if (!aligned) {
+    spmm_scalar<T><<<blocks, threads, 0, st>>>(r0, r1, rp, ci, cv, deg, x, ldx, ncols, y, ldy);
+    SPB_LAUNCH_CHECK();
+    return SPB_OK;
+  }
+  // column panels: keep the gathered panel of X within ~half of L2
+  static int l2 = -1;
+  if (l2 < 0) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (cudaDeviceGetAttribute(&l2, cudaDevAttrL2CacheSize, dev) != cudaSuccess) l2 = 64 << 20;
+  }
+  int64_t n_all = (int64_t)r1;  // gathered rows span the whole operator
+  int64_t panel = ((int64_t)l2 / 2) / std::max<int64_t>(1, n_all * (int64_t)sizeof(T));
+  panel = std::max<int64_t>(panel / (8 * VN) * (8 * VN), 8 * VN);
+  if (panel >= ncols) panel = ncols;
+  for (int c0 = 0; c0 < ncols; c0 += (int)panel) {
+    const int pc = (int)std::min<int64_t>(panel, ncols - c0);
+    const int nvec = (pc + VN - 1) / VN;
+    if (nvec <= 1)
+      spmm_vec<T, 1><<<blocks, threads, 0, st>>>(r0, r1, rp, ci, cv, deg, x, ldx, c0, pc, y, ldy);
+    else if (nvec <= 2)
+      spmm_vec<T, 2><<<blocks, threads, 0, st>>>(r0, r1, rp, ci, cv, deg, x, ldx, c0, pc, y, ldy);
+    else if (nvec <= 4)
+      spmm_vec<T, 4><<<blocks, threads, 0, st>>>(r0, r1, rp, ci, cv, deg, x, ldx, c0, pc, y, ldy);
+    else if (nvec <= 8)
+      spmm_vec<T, 8><<<blocks, threads, 0, st>>>(r0, r1, rp, ci, cv, deg, x, ldx, c0, pc, y, ldy);
+    else if (nvec <= 16)
+      spmm_vec<T, 16><<<blocks, threads, 0, st>>>(r0, r1, rp, ci, cv, deg, x, ldx, c0, pc, y, ldy);
+    else
+      spmm_vec<T, 32><<<blocks, threads, 0, st>>>(r0, r1, rp, ci, cv, deg, x, ldx, c0, pc, y, ldy);
+    SPB_LAUNCH_CHECK();
+  }
+  return SPB_OK;
+}
+
+}  // namespace
+
+int laplacian_spmm(int dtype, int32_t r0, int32_t r1, const int32_t* rp, const int32_t* ci,
+                   const void* cv, const void* deg, const void* x, int64_t ldx, int ncols,
+                   void* y, int64_t ldy, cudaStream_t st) {
+  if (dtype == SPB_F32)
+    return launch_spmm<float>(r0, r1, rp, ci, (const float*)cv, (const float*)deg,
+                              (const float*)x, ldx, ncols, (float*)y, ldy, st);
+  return launch_spmm<double>(r0, r1, rp, ci, (const double*)cv, (const double*)deg,
+                             (const double*)x, ldx, ncols, (double*)y, ldy, st);
+}
+
+}  // namespace spb
+
+extern "C" int spb_laplacian_spmm(int dtype, int32_t row_begin, int32_t row_end,
+                                  const int32_t* row_ptr, const int32_t* col, const void* val,
+                                  const void* deg, const void* x, int64_t ldx, int32_t ncols,
+                                  void* y, int64_t ldy, void* stream) {
+  if (dtype != SPB_F32 && dtype != SPB_F64) {
+    spb::set_error("unknown dtype %d", dtype);
+    return SPB_ERR_DOMAIN;
+  }
+  if (row_begin < 0 || row_end < row_begin || ncols < 0 || ldx < ncols || ldy < ncols) {
+    spb::set_error("spmm shape contract violated");
+    return SPB_ERR_CONTRACT;
+  }
+  return spb::laplacian_spmm(dtype, row_begin, row_end, row_ptr, col, val, deg, x, ldx, ncols, y,
+                             ldy, (cudaStream_t)stream);
+}

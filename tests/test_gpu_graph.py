@@ -1,0 +1,96 @@
+"""GPU parity of (a) CSR build + degrees and (b) Laplacian SpMM against the oracle."""
+
+import numpy as np
+import pytest
+
+import oracle
+from tests.golden.cases import small_graph_cases
+from tests.helpers import config_input, sha
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def spb():
+    import paper_1708_07481_b200 as spb
+
+    return spb
+
+
+@pytest.mark.parametrize("name", sorted(small_graph_cases()))
+def test_small_graphs_bit_exact(spb, golden_graph, name):
+    edges, n, w = small_graph_cases()[name]
+    g = spb.from_edges(edges, n, weights=w)
+    gold = golden_graph
+    assert np.array_equal(g.row_offsets, gold[f"{name}/a_indptr"])
+    assert np.array_equal(g.col_indices, gold[f"{name}/a_indices"])
+    assert np.array_equal(g.weights, gold[f"{name}/a_data"])
+    s = spb.symmetrize(g)
+    assert np.array_equal(s.row_offsets, gold[f"{name}/w_indptr"])
+    assert np.array_equal(s.col_indices, gold[f"{name}/w_indices"])
+    assert np.array_equal(s.weights, gold[f"{name}/w_data"])
+    assert np.array_equal(spb.degrees(g), gold[f"{name}/deg"])
+    x = np.random.default_rng(11).standard_normal((n, 3))
+    y = spb.laplacian_apply(g, spb.degrees(g), x)
+    assert np.allclose(y, gold[f"{name}/y"], rtol=1e-12, atol=1e-12)
+
+
+@pytest.mark.parametrize("cfg", ["c1", "c2"])
+def test_config_graphs_bit_exact(spb, golden_graph, cfg):
+    spec, edges, _ = config_input(cfg)
+    gold = golden_graph
+    g = spb.from_edges(edges, spec.n)
+    assert sha(g.row_offsets, g.col_indices, g.weights) == str(gold[f"{cfg}/a_sha"])
+    s = spb.symmetrize(g)
+    assert sha(s.row_offsets, s.col_indices, s.weights) == str(gold[f"{cfg}/w_sha"])
+    assert sha(spb.degrees(g)) == str(gold[f"{cfg}/deg_sha"])
+    x = np.random.default_rng(5).standard_normal((spec.n, 8))
+    y = spb.laplacian_apply(g, spb.degrees(g), x)
+    assert np.allclose(np.linalg.norm(y, axis=0), gold[f"{cfg}/y_colnorm"], rtol=1e-12)
+    assert np.allclose(y[:64], gold[f"{cfg}/y_head"], rtol=1e-12, atol=1e-12)
+
+
+@pytest.mark.parametrize("ncols", [1, 3, 8, 21, 49, 108, 176])
+@pytest.mark.parametrize("dtype", ["float32", "float64"])
+def test_spmm_widths_vs_oracle(spb, ncols, dtype):
+    import torch
+
+    spec, edges, _ = config_input("c1")
+    g = spb.from_edges(edges, spec.n)
+    op = spb.LaplacianOperator(g)
+    ip, ix, dv = oracle.directed_csr(edges, spec.n)
+    ref_op = oracle.LaplacianRef(ip, ix, dv, spec.n)
+    x = np.random.default_rng(ncols).standard_normal((spec.n, ncols))
+    want = ref_op.apply(x)
+    ld = ((ncols + 7) // 8) * 8
+    tdt = torch.float32 if dtype == "float32" else torch.float64
+    xt = torch.zeros(spec.n, ld, dtype=tdt, device="cuda")
+    xt[:, :ncols] = torch.from_numpy(x).to(xt)
+    yt = torch.full_like(xt, 7.0)
+    from paper_1708_07481_b200.graph import _spmm
+
+    _spmm(g, op.device_degrees(dtype), xt[:, :ncols], yt[:, :ncols], dtype)
+    got = yt[:, :ncols].double().cpu().numpy()
+    tol = 1e-5 if dtype == "float32" else 1e-12
+    assert np.allclose(got, want, rtol=tol, atol=tol * np.abs(want).max())
+    # padding columns untouched
+    assert torch.all(yt[:, ncols:] == 7.0)
+    assert op.scale_hint == float(oracle.directed_degrees(ip, ix, dv, spec.n).max())
+
+
+def test_domain_errors(spb):
+    with pytest.raises(spb.DomainError):
+        spb.from_edges([(0, 5)], 3)
+    with pytest.raises(spb.DomainError):
+        spb.from_edges([(0, 1, -1.0)], 2)
+
+
+def test_apply_delta_matches_bulk(spb):
+    first = [(0, 1, 1.0), (2, 0, 2.0)]
+    second = [(1, 3, 1.0), (0, 1, 1.0)]
+    g = spb.apply_delta(spb.from_edges(first, 3), second, 4)
+    h = spb.from_edges(first + second, 4)
+    assert np.array_equal(g.row_offsets, h.row_offsets)
+    assert np.array_equal(g.col_indices, h.col_indices)
+    assert np.allclose(g.weights, h.weights)
+    assert spb.degrees(g).tolist() == [4.0, 3.0, 2.0, 1.0]
