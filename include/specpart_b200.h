@@ -119,9 +119,10 @@ typedef struct {
   int32_t reserved;
 } spb_solver_config;
 
-/* callback(it, theta[:l], norms) of lobpcg.py:348-349 (host arrays, copies). */
-typedef void (*spb_iter_cb)(void* user, int32_t it, const double* theta, const double* norms,
-                            int32_t l);
+/* callback(it, theta[:l], norms) of lobpcg.py:348-349 (host arrays, copies);
+ * a nonzero return aborts the solve with SPB_ERR_CALLBACK. */
+typedef int (*spb_iter_cb)(void* user, int32_t it, const double* theta, const double* norms,
+                           int32_t l);
 /* Gaussian refill of dependent columns (lobpcg.py:214): fill rows*cols float64
  * (row-major) from the solve's numpy Generator; return 0 on success. */
 typedef int (*spb_refill_cb)(void* user, int64_t rows, int32_t cols, double* out);
@@ -143,6 +144,13 @@ SPB_API int spb_lobpcg_solve(const spb_operator* op, int dtype, const double* x0
 /* Device pointer/ld of the solver's final X block inside ``ws`` (dtype). */
 SPB_API int spb_lobpcg_result_block(int dtype, int32_t n, int32_t l, void* ws, void** x_out,
                             int64_t* ld_out);
+
+/* orthonormalize (lobpcg.py:195-215) of a device block b (n x width, row stride
+ * ldb) in place, with Gaussian refills of dependent columns via ``refill``. */
+SPB_API size_t spb_orthonormalize_workspace(int dtype, int32_t n, int32_t width);
+SPB_API int spb_orthonormalize(int dtype, void* b, int64_t ldb, int32_t n, int32_t width,
+                               spb_refill_cb refill, void* user, void* ws, size_t ws_bytes,
+                               void* stream);
 
 /* Small projected problem (lobpcg.py:168-177): ga, gb are device float64
  * m x m (symmetrised inside); gb may be NULL for B = I. Outputs: theta

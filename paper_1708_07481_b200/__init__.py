@@ -32,3 +32,32 @@ from .graph import (  # noqa: F401
     symmetrize,
     write_edge_list,
 )
+from .lobpcg import (  # noqa: F401,E402
+    DenseOperator,
+    EigenState,
+    SolverConfig,
+    lobpcg_solve,
+    orthonormalize,
+    random_init,
+    rayleigh_ritz,
+    residual_norms,
+)
+from .spectral import (  # noqa: F401,E402
+    GapResult,
+    Partition,
+    assign_clusters_qrcp,
+    block_size_for,
+    detect_gap,
+    partition_static,
+    read_labels,
+    write_labels,
+)
+from .metrics import (  # noqa: F401,E402
+    ContingencyTable,
+    contingency,
+    pair_counts,
+    pairwise_precision,
+    pairwise_recall,
+    partition_match,
+    stage_record,
+)

@@ -40,7 +40,7 @@ class SolverConfigC(C.Structure):
                 ("reserved", i32)]
 
 
-ITER_CB = C.CFUNCTYPE(None, vp, i32, C.POINTER(f64), C.POINTER(f64), i32)
+ITER_CB = C.CFUNCTYPE(C.c_int, vp, i32, C.POINTER(f64), C.POINTER(f64), i32)
 REFILL_CB = C.CFUNCTYPE(C.c_int, vp, i64, i32, C.POINTER(f64))
 PRECOND_CB = C.CFUNCTYPE(C.c_int, vp, i64, i32, C.POINTER(f64))
 
@@ -61,6 +61,8 @@ _SIGS = {
                                    C.POINTER(f64), C.POINTER(f64), C.POINTER(C.c_uint8),
                                    C.POINTER(i64), vp]),
     "spb_lobpcg_result_block": (C.c_int, [C.c_int, i32, i32, vp, C.POINTER(vp), C.POINTER(i64)]),
+    "spb_orthonormalize_workspace": (sz, [C.c_int, i32, i32]),
+    "spb_orthonormalize": (C.c_int, [C.c_int, vp, i64, i32, i32, REFILL_CB, vp, vp, sz, vp]),
     "spb_sygv_workspace": (sz, [i32]),
     "spb_sygv": (C.c_int, [vp, vp, i32, i32, vp, vp, vp, sz, vp]),
     "spb_assign_workspace": (sz, [i32, i32]),

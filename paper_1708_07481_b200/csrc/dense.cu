@@ -146,7 +146,7 @@ update_kernel(UpdParams P, int64_t n) {
       }
       for (int e = tid; e < UK * qv * 32; e += 256) {
         const int k = e / (qv * 32), c = e % (qv * 32);
-        Cs[k][c] = (k < kc && c < q) ? (T)sg.C[(int64_t)(k0 + k) * sg.ldc + c] : T(0);
+        Cs[k][c] = (k < kc && c < q) ? (T)(sg.scale * sg.C[(int64_t)(k0 + k) * sg.ldc + c]) : T(0);
       }
       __syncthreads();
       for (int k = 0; k < kc; ++k) {
@@ -420,6 +420,7 @@ int dense_apply(const double* Adense, int64_t n, const void* X, int64_t ldx, int
   p.seg[0].C = (const double*)X;
   p.seg[0].ldc = ldx;
   p.seg[0].emit = 1;
+  p.seg[0].scale = 1.0;
   p.seg[0].out = Y;
   p.seg[0].ldo = ldy;
   return block_update(SPB_F64, p, n, st);

@@ -26,10 +26,11 @@ struct GramBatch {
 struct UpdSeg {
   const void* A;
   int64_t lda;
-  const double* C;
+  const double* C;   // w x q coefficients (float64), scaled by ``scale`` on load
   int64_t ldc;
   void* out;
   int64_t ldo;
+  double scale;
   int w;
   int emit;
 };

@@ -1,0 +1,710 @@
+// (c)(d) LOBPCG driver: the soft-locked block LOBPCG of lobpcg.py:263-454 with
+// every n-sized operation on the device and the O(l) control logic on the host.
+//
+// Working set: six n x lp blocks X, R, P, LX, LR, LP (lp = l rounded up to 8),
+// vertex-major, storage dtype float32 or float64 (the reference's work_blocks
+// contract, lobpcg.py:297-300). Updates are row-local and run in place.
+//
+// Per loop pass (it), mirroring lobpcg.py:337-440:
+//   residual + norms (+ P norms)          column_reduce, one D2H       (:338-341, :382)
+//   callback / stop test / soft lock      host                         (:348-355)
+//   compact R, P columns                  gather_columns               (:357-359, :376-387)
+//   R -= X (X'R); CholQR(R)                gram + block_update + small  (:365-370)
+//   LR = L R                              spmm                         (:374)
+//   Rayleigh-Ritz ladder full/drop_p/rebuild: batched Gram + sygv      (:397-429)
+//   X' = B C, P' = B[:, l:] C[l:] (and images)  block_update            (:431-440)
+// Polish: orthonormalise, LX = L X, eigh(X'LX, I), rotate, final norms (:442-454).
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <vector>
+
+#include "dense.cuh"
+#include "smalleig.cuh"
+
+namespace spb {
+namespace {
+
+struct SolveWs {
+  int dtype, n, l, lp, mmax;
+  size_t esz;
+  void *X, *LX, *R, *LR, *P, *LP;
+  double *G;          // mmax x 2mmax: [G_A | G_B]
+  double *gpart;      // gram split partials
+  size_t gpart_cap;
+  double *Gs;         // small Gram (lp x lp)
+  double *coef;       // coupling / Rinv (lp x lp)
+  double *Cm;         // Ritz coefficients (mmax x l)
+  double *theta, *theta_new;
+  double *sygv_ws;
+  size_t sygv_cap;
+  double *chol_ws;
+  double *crpart;     // column-reduce partials
+  double *sums;       // 2 * lp column sums (norms^2 of R and P)
+  double *pscale;     // lp
+  int *idx, *perm;
+  SmallStatus* status;
+};
+
+SolveWs carve(Arena& a, int dtype, int n, int l) {
+  SolveWs w;
+  w.dtype = dtype;
+  w.n = n;
+  w.l = l;
+  w.lp = (int)round_up(l, 8);
+  w.mmax = 3 * l;
+  w.esz = dtype == SPB_F32 ? 4 : 8;
+  const size_t blk = (size_t)std::max(n, 1) * w.lp * w.esz;
+  w.X = a.take<char>(blk);
+  w.LX = a.take<char>(blk);
+  w.R = a.take<char>(blk);
+  w.LR = a.take<char>(blk);
+  w.P = a.take<char>(blk);
+  w.LP = a.take<char>(blk);
+  const int mm = w.mmax;
+  w.G = a.take<double>((size_t)mm * 2 * mm);
+  const int seg_tiles = (int)ceil_div(l, 64) * (int)ceil_div(l, 64);
+  w.gpart_cap = gram_partial_doubles(n, 18 * seg_tiles, mm, 2 * mm, nullptr);
+  w.gpart_cap = std::max(w.gpart_cap, gram_partial_doubles(n, seg_tiles, w.lp, w.lp, nullptr));
+  w.gpart = a.take<double>(w.gpart_cap);
+  w.Gs = a.take<double>((size_t)w.lp * w.lp);
+  w.coef = a.take<double>((size_t)w.lp * w.lp);
+  w.Cm = a.take<double>((size_t)mm * l);
+  w.theta = a.take<double>(mm + 8);
+  w.theta_new = a.take<double>(mm + 8);
+  w.sygv_cap = sygv_ws_doubles(mm, l);
+  w.sygv_ws = a.take<double>(w.sygv_cap);
+  w.chol_ws = a.take<double>(cholqr_ws_doubles(w.lp));
+  w.crpart = a.take<double>(colreduce_partial_doubles(n, 2 * w.lp) + 64);
+  w.sums = a.take<double>(2 * w.lp + 8);
+  w.pscale = a.take<double>(w.lp + 8);
+  w.idx = a.take<int>(w.lp + 8);
+  w.perm = a.take<int>(w.lp + 8);
+  w.status = a.take<SmallStatus>(1);
+  return w;
+}
+
+struct Driver {
+  const spb_operator* op;
+  SolveWs w;
+  const spb_solver_config* cfg;
+  spb_iter_cb cb;
+  spb_refill_cb refill;
+  spb_precond_cb precond;
+  void* user;
+  cudaStream_t st;
+  int64_t stats[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  std::vector<double> h_theta, h_norms;  // last residual step
+  double h_scale = 0.0;
+  int iterations = 0;
+
+  int apply(const void* src, int cols, void* dst) {
+    stats[1]++;
+    if (op->kind == SPB_OP_LAPLACIAN)
+      return laplacian_spmm(w.dtype, 0, op->n, op->row_ptr, op->col, op->val, op->deg, src, w.lp,
+                            cols, dst, w.lp, st);
+    return dense_apply(op->dense, op->n, src, w.lp, cols, dst, w.lp, w.dtype, nullptr, st);
+  }
+
+  int gram1(const void* U, int p, const void* V, int q, double* out, int ldo) {
+    GramBatch b{};
+    b.njobs = 1;
+    b.job[0] = {U, V, w.lp, w.lp, p, q, 0, 0};
+    b.tile_start[0] = 0;
+    b.tile_start[1] = (int)(ceil_div(p, 64) * ceil_div(q, 64));
+    return gram_batched(w.dtype, b, w.n, p, q, w.gpart, w.gpart_cap, out, ldo, st);
+  }
+
+  // [G_A | G_B] for the basis [X (l) | R (na) | P (pw)] and images.
+  int rr_grams(int na, int pw) {
+    const void* S[3] = {w.X, w.R, w.P};
+    const void* LS[3] = {w.LX, w.LR, w.LP};
+    const int wd[3] = {w.l, na, pw};
+    int off[3] = {0, w.l, w.l + na};
+    GramBatch b{};
+    int nj = 0, tiles = 0;
+    for (int s = 0; s < 3; ++s) {
+      if (!wd[s]) continue;
+      for (int t = 0; t < 3; ++t) {
+        if (!wd[t]) continue;
+        for (int kind = 0; kind < 2; ++kind) {
+          GramJob j{S[s], kind == 0 ? LS[t] : S[t], w.lp, w.lp, wd[s], wd[t], off[s],
+                    off[t] + (kind == 0 ? 0 : w.mmax)};
+          b.job[nj] = j;
+          b.tile_start[nj] = tiles;
+          tiles += (int)(ceil_div(wd[s], 64) * ceil_div(wd[t], 64));
+          ++nj;
+        }
+      }
+    }
+    b.njobs = nj;
+    b.tile_start[nj] = tiles;
+    const int m = w.l + na + pw;
+    // output region rows m, columns mmax + m (ld 2 mmax)
+    return gram_batched(w.dtype, b, w.n, m, w.mmax + m, w.gpart, w.gpart_cap, w.G, 2 * w.mmax,
+                        st);
+  }
+
+  int read_status(SmallStatus* h) {
+    SPB_CUDA(cudaMemcpyAsync(h, w.status, sizeof(SmallStatus), cudaMemcpyDeviceToHost, st));
+    SPB_CUDA(cudaStreamSynchronize(st));
+    return SPB_OK;
+  }
+
+  int reset_status() {
+    SPB_CUDA(cudaMemsetAsync(w.status, 0, sizeof(SmallStatus), st));
+    return SPB_OK;
+  }
+
+  // In-place right-multiplication B[:, :q] <- B[:, :w] C (row-local).
+  int rmul(void* B, int wcols, const double* C, int ldc, int q, double scale = 1.0) {
+    UpdParams p{};
+    p.nseg = 1;
+    p.q = q;
+    p.seg[0] = {B, w.lp, C, ldc, B, w.lp, scale, wcols, 1};
+    return block_update(w.dtype, p, w.n, st);
+  }
+
+  // R[:, :na] -= X (X' R)   (lobpcg.py:365-369)
+  int project_out_x(int na) {
+    SPB_TRY(gram1(w.X, w.l, w.R, na, w.coef, w.lp));
+    UpdParams p{};
+    p.nseg = 1;
+    p.q = na;
+    p.init = w.R;
+    p.ldi = w.lp;
+    p.seg[0] = {w.X, w.lp, w.coef, w.lp, w.R, w.lp, -1.0, w.l, 1};
+    return block_update(w.dtype, p, w.n, st);
+  }
+
+  // _cholesky_orth (lobpcg.py:218-247) on the first na columns of B; *kept = width.
+  int cholesky_orth(void* B, int na, int* kept) {
+    if (na == 0) {
+      *kept = 0;
+      return SPB_OK;
+    }
+    SPB_TRY(gram1(B, na, B, na, w.Gs, w.lp));
+    SPB_TRY(reset_status());
+    SPB_TRY(cholqr_enqueue(w.Gs, w.lp, na, w.coef, w.chol_ws, w.status, st));
+    SmallStatus hs;
+    SPB_TRY(read_status(&hs));
+    if (!hs.fallback && !hs.nonfinite) {
+      SPB_TRY(rmul(B, na, w.coef, na, na));
+      *kept = na;
+      return SPB_OK;
+    }
+    // rank-revealing branch (pivoted Cholesky == dgeqp3 pivoting on B)
+    const double eps_t = w.dtype == SPB_F32 ? 3e-7 * std::sqrt((double)na) : 2e-8;
+    const double rank_tol = std::max(std::max<double>(w.n, na) * kEps64, eps_t);
+    SPB_TRY(reset_status());
+    SPB_TRY(pivoted_cholqr_enqueue(w.Gs, w.lp, na, rank_tol, w.perm, w.coef, w.chol_ws, w.status,
+                                   st));
+    SPB_TRY(read_status(&hs));
+    const int rank = hs.rank;
+    if (rank == 0) {
+      *kept = 0;
+      return SPB_OK;
+    }
+    SPB_TRY(gather_columns(w.dtype, B, w.lp, w.n, w.perm, rank, st));
+    SPB_TRY(rmul(B, rank, w.coef, na, rank));
+    // second CholQR pass restores orthonormality to working precision
+    SPB_TRY(gram1(B, rank, B, rank, w.Gs, w.lp));
+    SPB_TRY(reset_status());
+    SPB_TRY(cholqr_enqueue(w.Gs, w.lp, rank, w.coef, w.chol_ws, w.status, st));
+    SPB_TRY(read_status(&hs));
+    if (!hs.fallback && !hs.nonfinite) SPB_TRY(rmul(B, rank, w.coef, rank, rank));
+    *kept = rank;
+    return SPB_OK;
+  }
+
+  int column_sumsq(const void* A, int cols, double* out_host) {
+    SPB_TRY(column_reduce(w.dtype, CR_SUMSQ, A, w.lp, cols, w.n, nullptr, 0, nullptr, nullptr, 0,
+                          w.crpart, w.sums, st));
+    SPB_CUDA(cudaMemcpyAsync(out_host, w.sums, sizeof(double) * cols, cudaMemcpyDeviceToHost, st));
+    SPB_CUDA(cudaStreamSynchronize(st));
+    return SPB_OK;
+  }
+
+  int deflate(void* A, int cols) {  // A -= column means (lobpcg.py:259-260)
+    SPB_TRY(column_reduce(w.dtype, CR_SUM, A, w.lp, cols, w.n, nullptr, 0, nullptr, nullptr, 0,
+                          w.crpart, w.sums, st));
+    return subtract_column_means(w.dtype, A, w.lp, w.n, cols, w.sums, st);
+  }
+
+  // orthonormalize (lobpcg.py:195-215) on the first width columns of X.
+  int orthonormalize(void* B, int width) {
+    if (width > w.n) {
+      set_error("cannot orthonormalize: more columns than rows");
+      return SPB_ERR_DOMAIN;
+    }
+    std::vector<double> ss(width);
+    SPB_TRY(column_sumsq(B, width, ss.data()));
+    bool any = false;
+    for (double v : ss) any |= (v != 0.0);
+    if (!any) {
+      set_error("cannot orthonormalize an all-zero block");
+      return SPB_ERR_DOMAIN;
+    }
+    for (int attempt = 0; attempt < 5; ++attempt) {
+      int kept = 0;
+      SPB_TRY(cholesky_orth(B, width, &kept));
+      if (kept == width) return SPB_OK;
+      SPB_TRY(refill_cols(B, kept, width - kept));
+    }
+    set_error("could not build a full-rank orthonormal block");
+    return SPB_ERR_CONDITIONING;
+  }
+
+  int refill_cols(void* B, int c0, int cols) {
+    if (!refill) {
+      set_error("rank repair needs the Gaussian refill callback");
+      return SPB_ERR_CALLBACK;
+    }
+    std::vector<double> h((size_t)w.n * cols);
+    if (refill(user, w.n, cols, h.data()) != 0) {
+      set_error("refill callback failed");
+      return SPB_ERR_CALLBACK;
+    }
+    double* d = nullptr;
+    SPB_CUDA(cudaMallocAsync((void**)&d, sizeof(double) * h.size(), st));
+    SPB_CUDA(cudaMemcpyAsync(d, h.data(), sizeof(double) * h.size(), cudaMemcpyHostToDevice, st));
+    char* dst = (char*)B + (size_t)c0 * w.esz;
+    int s = copy_block(SPB_F64, d, cols, w.dtype, dst, w.lp, w.n, cols, st);
+    cudaFreeAsync(d, st);
+    SPB_CUDA(cudaStreamSynchronize(st));
+    return s;
+  }
+
+  int run_precond(int na) {
+    std::vector<double> h((size_t)w.n * na);
+    double* d = nullptr;
+    SPB_CUDA(cudaMallocAsync((void**)&d, sizeof(double) * h.size() + 8, st));
+    SPB_TRY(copy_block(w.dtype, w.R, w.lp, SPB_F64, d, na, w.n, na, st));
+    SPB_CUDA(cudaMemcpyAsync(h.data(), d, sizeof(double) * h.size(), cudaMemcpyDeviceToHost, st));
+    SPB_CUDA(cudaStreamSynchronize(st));
+    if (precond(user, w.n, na, h.data()) != 0) {
+      cudaFreeAsync(d, st);
+      set_error("precond callback failed");
+      return SPB_ERR_CALLBACK;
+    }
+    SPB_CUDA(cudaMemcpyAsync(d, h.data(), sizeof(double) * h.size(), cudaMemcpyHostToDevice, st));
+    SPB_TRY(copy_block(SPB_F64, d, na, w.dtype, w.R, w.lp, w.n, na, st));
+    cudaFreeAsync(d, st);
+    SPB_CUDA(cudaStreamSynchronize(st));
+    return SPB_OK;
+  }
+
+  // sygv with the ladder's ConditioningError semantics; *ok = success.
+  int small_gen_eigh(int m, bool identity_b, int* ok) {
+    stats[2]++;
+    SPB_TRY(reset_status());
+    SPB_TRY(sygv_enqueue(w.G, identity_b ? nullptr : w.G + w.mmax, 2 * w.mmax, m, w.l,
+                         w.theta_new, w.Cm, w.l, w.sygv_ws, w.sygv_cap, w.status, st));
+    SmallStatus hs;
+    SPB_TRY(read_status(&hs));
+    *ok = 0;
+    if (hs.nonfinite || hs.not_pd || hs.cond_state == 1) return SPB_OK;
+    if (hs.cond_state == 2) {
+      double cond = 0.0;
+      // sygv's workspace holds the symmetrised G_B in its B slot; recompute from G
+      SPB_TRY(exact_cond_spd(w.G + w.mmax, 2 * w.mmax, m, w.sygv_ws, w.sygv_cap, &cond, st));
+      if (!(cond <= kCondMax)) return SPB_OK;
+      // exact_cond reused the workspace: redo the solve
+      SPB_TRY(reset_status());
+      SPB_TRY(sygv_enqueue(w.G, w.G + w.mmax, 2 * w.mmax, m, w.l, w.theta_new, w.Cm, w.l,
+                           w.sygv_ws, w.sygv_cap, w.status, st));
+      SPB_TRY(read_status(&hs));
+      if (hs.nonfinite || hs.not_pd) return SPB_OK;
+    }
+    *ok = 1;
+    std::swap(w.theta, w.theta_new);
+    return SPB_OK;
+  }
+
+  // residual R = LX - X theta and norms; also P column norms if have_p.
+  int residual(bool have_p, std::vector<double>& norms, std::vector<double>& pn) {
+    SPB_TRY(column_reduce(w.dtype, CR_RESIDUAL, w.LX, w.lp, w.l, w.n, w.X, w.lp, w.theta, w.R,
+                          w.lp, w.crpart, w.sums, st));
+    if (have_p)
+      SPB_TRY(column_reduce(w.dtype, CR_SUMSQ, w.P, w.lp, w.l, w.n, nullptr, 0, nullptr, nullptr,
+                            0, w.crpart, w.sums + w.lp, st));
+    std::vector<double> hs(2 * w.lp);
+    SPB_CUDA(cudaMemcpyAsync(hs.data(), w.sums, sizeof(double) * 2 * w.lp, cudaMemcpyDeviceToHost, st));
+    h_theta.resize(w.l);
+    SPB_CUDA(cudaMemcpyAsync(h_theta.data(), w.theta, sizeof(double) * w.l, cudaMemcpyDeviceToHost, st));
+    SPB_CUDA(cudaStreamSynchronize(st));
+    norms.resize(w.l);
+    pn.resize(w.l);
+    for (int j = 0; j < w.l; ++j) {
+      norms[j] = std::sqrt(hs[j]);
+      pn[j] = have_p ? std::sqrt(hs[w.lp + j]) : 0.0;
+    }
+    return SPB_OK;
+  }
+
+  double scale_of() const {
+    const double th = std::fabs(h_theta[w.l - 1]);
+    return std::max(std::max(th, op->scale_hint), 2.2250738585072014e-308);
+  }
+
+  int update(int na, int pw) {
+    // X' = X Cx + R Cr + P Cp, P' = R Cr + P Cp (lobpcg.py:436-439); same for images.
+    const int l = w.l;
+    const double* Cx = w.Cm;
+    const double* Cr = w.Cm + (size_t)l * l;
+    const double* Cp = w.Cm + (size_t)(l + na) * l;
+    for (int side = 0; side < 2; ++side) {
+      void* X = side == 0 ? w.X : w.LX;
+      void* R = side == 0 ? w.R : w.LR;
+      void* P = side == 0 ? w.P : w.LP;
+      UpdParams p{};
+      p.q = l;
+      int s = 0;
+      p.seg[s++] = {R, w.lp, Cr, l, P, w.lp, 1.0, na, pw == 0 ? 1 : 0};
+      if (pw) p.seg[s++] = {P, w.lp, Cp, l, P, w.lp, 1.0, pw, 1};
+      p.seg[s++] = {X, w.lp, Cx, l, X, w.lp, 1.0, l, 1};
+      p.nseg = s;
+      SPB_TRY(block_update(w.dtype, p, w.n, st));
+    }
+    return SPB_OK;
+  }
+
+  int set_idx(const std::vector<int>& idx) {
+    SPB_CUDA(cudaMemcpyAsync(w.idx, idx.data(), sizeof(int) * idx.size(), cudaMemcpyHostToDevice, st));
+    return SPB_OK;
+  }
+
+  int solve(const double* x0, double* theta_out, double* norms_out, uint8_t* conv_out,
+            bool* state_valid) {
+    const int n = w.n, l = w.l;
+    *state_valid = false;
+    // zero padding columns once, load x0 (float64 n x l) into X
+    const size_t blk = (size_t)n * w.lp * w.esz;
+    for (void* b : {w.X, w.LX, w.R, w.LR, w.P, w.LP}) SPB_CUDA(cudaMemsetAsync(b, 0, blk, st));
+    SPB_TRY(copy_block(SPB_F64, x0, l, w.dtype, w.X, w.lp, n, l, st));
+    if (cfg->deflate_ones) SPB_TRY(deflate(w.X, l));
+    SPB_TRY(orthonormalize(w.X, l));
+    SPB_TRY(apply(w.X, l, w.LX));
+    // initial Rayleigh-Ritz on span(X) (lobpcg.py:321-329)
+    SPB_TRY(rr_grams(0, 0));
+    int ok = 0;
+    SPB_TRY(small_gen_eigh(l, false, &ok));
+    if (!ok) {
+      set_error("initial projection failed: projected overlap matrix is ill-conditioned");
+      return SPB_ERR_SOLVER_NOSTATE;
+    }
+    SPB_TRY(rmul(w.X, l, w.Cm, l, l));
+    SPB_TRY(rmul(w.LX, l, w.Cm, l, l));
+
+    std::vector<char> active(l, 1);
+    bool have_p = false;
+    iterations = 0;
+    std::vector<double> norms, pn;
+    const int nc = cfg->n_converge;
+    for (int it = 0; it <= cfg->max_iter; ++it) {
+      SPB_TRY(residual(have_p, norms, pn));
+      h_norms = norms;
+      const double scale = scale_of();
+      h_scale = scale;
+      bool finite = true;
+      for (double v : norms) finite &= std::isfinite(v);
+      if (!finite) {
+        *state_valid = true;
+        set_error("residual norms are not finite");
+        return SPB_ERR_SOLVER;
+      }
+      if (cb && cb(user, it, h_theta.data(), norms.data(), l) != 0) {
+        set_error("callback raised");
+        return SPB_ERR_CALLBACK;
+      }
+      bool conv = true;
+      for (int j = 0; j < nc; ++j) conv &= norms[j] < cfg->tol * scale;
+      if (conv || it == cfg->max_iter) break;
+      bool any = false;
+      for (int j = 0; j < l; ++j) {
+        active[j] = active[j] && (norms[j] >= cfg->lock_tol * scale);
+        any |= active[j] != 0;
+      }
+      if (!any) break;
+      iterations++;
+      std::vector<int> idx;
+      for (int j = 0; j < l; ++j)
+        if (active[j]) idx.push_back(j);
+      int na = (int)idx.size();
+      if (na < l) {
+        SPB_TRY(set_idx(idx));
+        SPB_TRY(gather_columns(w.dtype, w.R, w.lp, n, w.idx, na, st));
+      }
+      if (cfg->has_precond) SPB_TRY(run_precond(na));
+      if (cfg->deflate_ones) SPB_TRY(deflate(w.R, na));
+      SPB_TRY(project_out_x(na));
+      int kept = 0;
+      SPB_TRY(cholesky_orth(w.R, na, &kept));
+      na = kept;
+      if (na == 0) break;
+      SPB_TRY(apply(w.R, na, w.LR));
+      int pw = 0;
+      if (have_p) {
+        std::vector<int> sel;
+        std::vector<double> sc;
+        for (int j : idx)
+          if (pn[j] > 0.0) {
+            sel.push_back(j);
+            sc.push_back(1.0 / pn[j]);
+          }
+        pw = (int)sel.size();
+        if (pw) {
+          bool identity = pw == l;
+          for (int j = 0; j < pw && identity; ++j) identity = sel[j] == j;
+          if (!identity) {
+            SPB_TRY(set_idx(sel));
+            SPB_TRY(gather_columns(w.dtype, w.P, w.lp, n, w.idx, pw, st));
+            SPB_TRY(gather_columns(w.dtype, w.LP, w.lp, n, w.idx, pw, st));
+          }
+          SPB_CUDA(cudaMemcpyAsync(w.pscale, sc.data(), sizeof(double) * pw, cudaMemcpyHostToDevice, st));
+          SPB_TRY(scale_columns(w.dtype, w.P, w.lp, n, w.pscale, pw, st));
+          SPB_TRY(scale_columns(w.dtype, w.LP, w.lp, n, w.pscale, pw, st));
+        }
+      }
+      // Rayleigh-Ritz ladder (lobpcg.py:397-429)
+      bool solved = false;
+      bool grams_ready = false;
+      for (int rung = 0; rung < 3; ++rung) {
+        if (rung == 1) {
+          if (pw == 0) continue;
+          pw = 0;  // leading (l + na) block of the Grams already computed
+          stats[3]++;
+        } else if (rung == 2) {
+          stats[4]++;
+          SPB_TRY(orthonormalize(w.X, l));
+          SPB_TRY(apply(w.X, l, w.LX));
+          SPB_TRY(project_out_x(na));
+          int k2 = 0;
+          SPB_TRY(cholesky_orth(w.R, na, &k2));
+          na = k2;
+          if (na == 0) break;
+          SPB_TRY(apply(w.R, na, w.LR));
+          grams_ready = false;
+        }
+        if (!grams_ready) {
+          SPB_TRY(rr_grams(na, pw));
+          grams_ready = true;
+        }
+        const int m = l + na + pw;
+        SPB_TRY(small_gen_eigh(m, false, &ok));
+        if (ok) {
+          solved = true;
+          break;
+        }
+      }
+      if (!solved) {
+        if (na == 0) break;
+        *state_valid = true;
+        set_error("projected eigenproblem unsolvable after restart");
+        return SPB_ERR_SOLVER;
+      }
+      SPB_TRY(update(na, pw));
+      have_p = true;
+    }
+    // polish (lobpcg.py:442-454)
+    SPB_TRY(orthonormalize(w.X, l));
+    SPB_TRY(apply(w.X, l, w.LX));
+    {
+      GramBatch b{};
+      b.njobs = 1;
+      b.job[0] = {w.X, w.LX, w.lp, w.lp, l, l, 0, 0};
+      b.tile_start[0] = 0;
+      b.tile_start[1] = (int)(ceil_div(l, 64) * ceil_div(l, 64));
+      SPB_TRY(gram_batched(w.dtype, b, n, l, l, w.gpart, w.gpart_cap, w.G, 2 * w.mmax, st));
+    }
+    SPB_TRY(small_gen_eigh(l, true, &ok));
+    if (!ok) {
+      set_error("projected matrices contain non-finite entries");
+      return SPB_ERR_CONDITIONING;
+    }
+    SPB_TRY(rmul(w.X, l, w.Cm, l, l));
+    SPB_TRY(rmul(w.LX, l, w.Cm, l, l));
+    SPB_TRY(residual(false, norms, pn));
+    h_norms = norms;
+    h_scale = scale_of();
+    *state_valid = true;
+    (void)theta_out;
+    (void)norms_out;
+    (void)conv_out;
+    return SPB_OK;
+  }
+};
+
+}  // namespace
+}  // namespace spb
+
+using namespace spb;
+
+extern "C" size_t spb_lobpcg_workspace(int dtype, int32_t n, int32_t l) {
+  Arena a;
+  a.dry = true;
+  carve(a, dtype, std::max(n, 1), std::max(l, 1));
+  return a.used + 4096;
+}
+
+extern "C" int spb_lobpcg_result_block(int dtype, int32_t n, int32_t l, void* ws, void** x_out,
+                                       int64_t* ld_out) {
+  Arena a;
+  a.base = (char*)ws;
+  a.cap = (size_t)-1;
+  SolveWs w = carve(a, dtype, std::max(n, 1), std::max(l, 1));
+  *x_out = w.X;
+  *ld_out = w.lp;
+  return SPB_OK;
+}
+
+extern "C" int spb_lobpcg_solve(const spb_operator* op, int dtype, const double* x0,
+                                const spb_solver_config* cfg, spb_iter_cb cb,
+                                spb_refill_cb refill, spb_precond_cb precond, void* user,
+                                void* ws, size_t ws_bytes, double* vectors_out, double* theta_out,
+                                double* norms_out, uint8_t* converged_out, int64_t* stats_out,
+                                void* stream) {
+  if (dtype != SPB_F32 && dtype != SPB_F64) {
+    set_error("unknown dtype %d", dtype);
+    return SPB_ERR_DOMAIN;
+  }
+  const int n = op->n, l = cfg->block_size;
+  if (l < 1 || l > n) {
+    set_error("block_size %d exceeds operator dimension %d", l, n);
+    return SPB_ERR_DOMAIN;
+  }
+  if (l > 256) {
+    set_error("block_size %d above the 256-column limit of this build", l);
+    return SPB_ERR_CONTRACT;
+  }
+  if (cfg->n_converge < 1 || cfg->n_converge > l) {
+    set_error("n_converge must be in [1, block_size]");
+    return SPB_ERR_DOMAIN;
+  }
+  Arena a;
+  a.base = (char*)ws;
+  a.cap = ws_bytes;
+  Driver d;
+  d.w = carve(a, dtype, n, l);
+  if (a.used > ws_bytes) {
+    set_error("lobpcg workspace too small (%zu < %zu)", ws_bytes, a.used);
+    return SPB_ERR_WORKSPACE;
+  }
+  d.op = op;
+  d.cfg = cfg;
+  d.cb = cb;
+  d.refill = refill;
+  d.precond = precond;
+  d.user = user;
+  d.st = (cudaStream_t)stream;
+  bool valid = false;
+  int s = d.solve(x0, theta_out, norms_out, converged_out, &valid);
+  if (valid) {
+    for (int j = 0; j < l; ++j) {
+      theta_out[j] = j < (int)d.h_theta.size() ? d.h_theta[j] : NAN;
+      norms_out[j] = j < (int)d.h_norms.size() ? d.h_norms[j] : NAN;
+      converged_out[j] = norms_out[j] < cfg->tol * d.h_scale;
+    }
+    if (vectors_out) {
+      int c = copy_block(dtype, d.w.X, d.w.lp, SPB_F64, vectors_out, l, n, l, d.st);
+      if (s == SPB_OK) s = c;
+      cudaError_t e = cudaStreamSynchronize(d.st);
+      if (s == SPB_OK && e != cudaSuccess) {
+        set_error("CUDA error %s", cudaGetErrorString(e));
+        s = SPB_ERR_CUDA;
+      }
+    }
+  }
+  d.stats[0] = d.iterations;
+  uint64_t bits;
+  std::memcpy(&bits, &d.h_scale, 8);
+  d.stats[5] = (int64_t)(bits >> 32);
+  d.stats[6] = (int64_t)(bits & 0xffffffffu);
+  if (stats_out)
+    for (int i = 0; i < 8; ++i) stats_out[i] = d.stats[i];
+  return s;
+}
+
+extern "C" size_t spb_sygv_workspace(int32_t m) {
+  return (sygv_ws_doubles(std::max(m, 1), std::max(m, 1)) + 64) * sizeof(double) + 1024;
+}
+
+extern "C" int spb_sygv(const double* ga, const double* gb, int32_t m, int32_t nev, double* theta,
+                        double* c, void* ws, size_t ws_bytes, void* stream) {
+  cudaStream_t st = (cudaStream_t)stream;
+  if (m < 1 || nev < 1 || nev > m) {
+    set_error("sygv needs 1 <= nev <= m");
+    return SPB_ERR_CONTRACT;
+  }
+  const size_t need = sygv_ws_doubles(m, nev);
+  if (ws_bytes < (need + 64) * sizeof(double)) {
+    set_error("sygv workspace too small");
+    return SPB_ERR_WORKSPACE;
+  }
+  double* base = (double*)ws;
+  SmallStatus* status = (SmallStatus*)(base + need);
+  SPB_CUDA(cudaMemsetAsync(status, 0, sizeof(SmallStatus), st));
+  SPB_TRY(sygv_enqueue(ga, gb, m, m, nev, theta, c, nev, base, need, status, st));
+  SmallStatus hs;
+  SPB_CUDA(cudaMemcpyAsync(&hs, status, sizeof(hs), cudaMemcpyDeviceToHost, st));
+  SPB_CUDA(cudaStreamSynchronize(st));
+  if (hs.nonfinite) {
+    set_error("projected matrices contain non-finite entries");
+    return SPB_ERR_CONDITIONING;
+  }
+  if (hs.not_pd || hs.cond_state == 1) {
+    set_error("projected overlap matrix is ill-conditioned");
+    return SPB_ERR_CONDITIONING;
+  }
+  if (hs.cond_state == 2) {
+    double cond = 0.0;
+    SPB_TRY(exact_cond_spd(gb, m, m, base, need, &cond, st));
+    if (!(cond <= kCondMax)) {
+      set_error("projected overlap matrix is ill-conditioned");
+      return SPB_ERR_CONDITIONING;
+    }
+    SPB_CUDA(cudaMemsetAsync(status, 0, sizeof(SmallStatus), st));
+    SPB_TRY(sygv_enqueue(ga, gb, m, m, nev, theta, c, nev, base, need, status, st));
+    SPB_CUDA(cudaStreamSynchronize(st));
+  }
+  return SPB_OK;
+}
+
+extern "C" size_t spb_orthonormalize_workspace(int dtype, int32_t n, int32_t width) {
+  return spb_lobpcg_workspace(dtype, n, width);
+}
+
+extern "C" int spb_orthonormalize(int dtype, void* b, int64_t ldb, int32_t n, int32_t width,
+                                  spb_refill_cb refill, void* user, void* ws, size_t ws_bytes,
+                                  void* stream) {
+  if (dtype != SPB_F32 && dtype != SPB_F64) {
+    set_error("unknown dtype %d", dtype);
+    return SPB_ERR_DOMAIN;
+  }
+  if (width < 1 || ldb < width || width > 256) {
+    set_error("orthonormalize shape contract violated");
+    return SPB_ERR_CONTRACT;
+  }
+  Arena a;
+  a.base = (char*)ws;
+  a.cap = ws_bytes;
+  Driver d;
+  d.w = carve(a, dtype, std::max(n, 1), width);
+  if (a.used > ws_bytes) {
+    set_error("orthonormalize workspace too small");
+    return SPB_ERR_WORKSPACE;
+  }
+  d.op = nullptr;
+  d.cfg = nullptr;
+  d.cb = nullptr;
+  d.refill = refill;
+  d.precond = nullptr;
+  d.user = user;
+  d.st = (cudaStream_t)stream;
+  SPB_CUDA(cudaMemsetAsync(d.w.X, 0, (size_t)n * d.w.lp * d.w.esz, d.st));
+  SPB_TRY(copy_block(dtype, b, ldb, dtype, d.w.X, d.w.lp, n, width, d.st));
+  SPB_TRY(d.orthonormalize(d.w.X, width));
+  SPB_TRY(copy_block(dtype, d.w.X, d.w.lp, dtype, b, ldb, n, width, d.st));
+  SPB_CUDA(cudaStreamSynchronize(d.st));
+  return SPB_OK;
+}

@@ -1,0 +1,879 @@
+// (d) Small dense float64 linear algebra for LOBPCG's projected problems.
+//
+// Replaces, for the m x m projected problems (m = l + na + pw <= 3l):
+//   _small_gen_eigh (lobpcg.py:168-177): finiteness check, cond2(G_B) <= 1/sqrt(eps),
+//     scipy.linalg.eigh(G_A, G_B) (LAPACK dsygvd);
+//   _cholesky_orth's Cholesky / triangular inverse (lobpcg.py:228-237) and its
+//     acceptance tests, plus a rank-revealing (pivoted) fallback for :241-247.
+//
+// Generalized problem: G_B = L L' (Cholesky), A' = L^-1 G_A L^-T, Householder
+// tridiagonalisation A' = Q T Q', the nev smallest eigenvalues of T by warp
+// multisection (Sturm counts), eigenvectors of T by inverse iteration with
+// modified Gram-Schmidt inside eigenvalue clusters (as LAPACK dstein), back-
+// transformation Q Y and C = L^-T Q Y (B-orthonormal columns).
+// cond2(G_B) is bracketed from ||G_B||_F and ||L^-1||_F:
+//   ||G_B||_F ||L^-1||_F^2 / m^1.5 <= cond2(G_B) <= ||G_B||_F ||L^-1||_F^2,
+// and only when the bracket straddles 1/sqrt(eps) is the exact value computed
+// (eigenvalues of G_B by the same tridiagonal + bisection kernels), so the
+// ladder takes the reference's branch in every case.
+#include <cfloat>
+
+#include "smalleig.cuh"
+
+namespace spb {
+namespace {
+
+constexpr int ET = 1024;  // threads of the single-CTA kernels
+
+__device__ double block_sum(double v, double* red) {
+  v = warp_sum(v);
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  __syncthreads();
+  if (lane == 0) red[w] = v;
+  __syncthreads();
+  if (w == 0) {
+    double t = lane < nw ? red[lane] : 0.0;
+    t = warp_sum(t);
+    if (lane == 0) red[32] = t;
+  }
+  __syncthreads();
+  return red[32];
+}
+
+// ---------------------------------------------------------------------------
+__global__ void sym_prep(const double* __restrict__ ga, const double* __restrict__ gb, int ldg,
+                         int m, double* __restrict__ A, double* __restrict__ B,
+                         SmallStatus* status) {
+  int bad = 0;
+  const int64_t total = (int64_t)m * m;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int i = (int)(e / m), j = (int)(e % m);
+    const double a = 0.5 * (ga[(int64_t)i * ldg + j] + ga[(int64_t)j * ldg + i]);
+    A[e] = a;
+    bad |= !isfinite(a);
+    if (B) {
+      const double b = gb ? 0.5 * (gb[(int64_t)i * ldg + j] + gb[(int64_t)j * ldg + i])
+                          : (i == j ? 1.0 : 0.0);
+      B[e] = b;
+      bad |= !isfinite(b);
+    }
+  }
+  if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0 && status)
+    atomicOr(&status->nonfinite, 1);
+}
+
+// Cholesky (lower, right-looking) of the m x m matrix Bsrc into L, then Linv = L^-1.
+// mode 0 (sygv): cond bracket into status. mode 1 (cholqr): the reference's
+// acceptance tests (lobpcg.py:231-235) and Rinv = (L^-1)' written to Linv.
+__global__ void __launch_bounds__(ET)
+chol_linv(const double* __restrict__ Bsrc, int m, double* __restrict__ Lg, double* __restrict__ Linv,
+          int mode, SmallStatus* status) {
+  extern __shared__ double smem[];
+  __shared__ double red[33];
+  __shared__ int fail;
+  const bool in_smem = (size_t)m * m * sizeof(double) <= 160 * 1024;
+  double* L = in_smem ? smem : Lg;
+  const int tid = threadIdx.x;
+  if (status->nonfinite) return;
+  double fb = 0.0;
+  for (int e = tid; e < m * m; e += ET) {
+    const double v = Bsrc[e];
+    L[e] = v;
+    fb += v * v;
+  }
+  fb = block_sum(fb, red);
+  if (tid == 0) fail = 0;
+  if (mode == 1) {
+    // diag > 0 and min diag > (eps na)^2 max diag  (lobpcg.py:229-231)
+    double dmin = DBL_MAX, dmax = -DBL_MAX;
+    if (tid == 0) {
+      for (int i = 0; i < m; ++i) {
+        dmin = fmin(dmin, Bsrc[(int64_t)i * m + i]);
+        dmax = fmax(dmax, Bsrc[(int64_t)i * m + i]);
+      }
+      status->dmin = dmin;
+      status->dmax = dmax;
+      const double t = kEps64 * m;
+      if (!(dmin > 0.0) || !(dmin > t * t * dmax)) fail = 1;
+    }
+  }
+  __syncthreads();
+  if (fail) {
+    if (tid == 0) status->fallback = 1;
+    return;
+  }
+  for (int j = 0; j < m; ++j) {
+    if (tid == 0) {
+      const double djj = L[(int64_t)j * m + j];
+      if (!(djj > 0.0)) fail = 1;
+      else L[(int64_t)j * m + j] = sqrt(djj);
+    }
+    __syncthreads();
+    if (fail) break;
+    const double piv = L[(int64_t)j * m + j];
+    for (int i = j + 1 + tid; i < m; i += ET) L[(int64_t)i * m + j] /= piv;
+    __syncthreads();
+    const int r = m - j - 1;
+    for (int e = tid; e < r * r; e += ET) {
+      const int i = j + 1 + e / r, k = j + 1 + e % r;
+      if (k <= i) L[(int64_t)i * m + k] -= L[(int64_t)i * m + j] * L[(int64_t)k * m + j];
+    }
+    __syncthreads();
+  }
+  if (fail) {
+    if (tid == 0) {
+      if (mode == 0) status->not_pd = 1;
+      else status->fallback = 1;
+    }
+    return;
+  }
+  if (mode == 1 && tid == 0) {
+    double rmin = DBL_MAX, rmax = -DBL_MAX;
+    for (int i = 0; i < m; ++i) {
+      rmin = fmin(rmin, L[(int64_t)i * m + i]);
+      rmax = fmax(rmax, L[(int64_t)i * m + i]);
+    }
+    status->rmin = rmin;
+    status->rmax = rmax;
+    if (!(rmin > sqrt(kEps64) * rmax)) fail = 1;  // lobpcg.py:235
+  }
+  __syncthreads();
+  if (fail) {
+    if (tid == 0) status->fallback = 1;
+    return;
+  }
+  // Linv by rows: Linv[i][j] = (delta_ij - sum_{k=j}^{i-1} L[i][k] Linv[k][j]) / L[i][i]
+  const int lane = tid & 31, warp = tid >> 5;
+  for (int i = 0; i < m; ++i) {
+    const double lii = L[(int64_t)i * m + i];
+    for (int j = warp; j <= i; j += ET / 32) {
+      double s = 0.0;
+      for (int k = j + lane; k < i; k += 32) s += L[(int64_t)i * m + k] * Linv[(int64_t)k * m + j];
+      s = warp_sum(s);
+      if (lane == 0) Linv[(int64_t)i * m + j] = ((i == j ? 1.0 : 0.0) - s) / lii;
+    }
+    for (int j = i + 1 + tid; j < m; j += ET) Linv[(int64_t)i * m + j] = 0.0;
+    __syncthreads();
+  }
+  double fl = 0.0;
+  for (int e = tid; e < m * m; e += ET) fl += Linv[e] * Linv[e];
+  fl = block_sum(fl, red);
+  if (mode == 0) {
+    if (tid == 0) {
+      // fb, fl are squared Frobenius norms: bracket = ||B||_F ||L^-1||_F^2
+      const double upper = sqrt(fb) * fl;
+      const double lower = upper / (m * sqrt((double)m));
+      status->fro_b = sqrt(fb);
+      status->fro_linv = sqrt(fl);
+      status->cond_hi = upper;
+      status->cond_lo = lower;
+      status->cond_state = upper <= kCondMax ? 0 : (lower > kCondMax ? 1 : 2);
+    }
+  } else {
+    // Rinv = (L^-1)' in place of Linv (upper triangular)
+    for (int e = tid; e < m * m; e += ET) {
+      const int i = e / m, j = e % m;
+      if (i < j) {
+        const double a = Linv[(int64_t)i * m + j], b = Linv[(int64_t)j * m + i];
+        Linv[(int64_t)i * m + j] = b;
+        Linv[(int64_t)j * m + i] = a;
+      }
+    }
+  }
+}
+
+// C = op(A) op(B) for small float64 matrices, 32x32 tiles, 256 threads.
+__global__ void __launch_bounds__(256)
+small_gemm(int ta, int tb, int M, int N, int K, const double* __restrict__ A, int lda,
+           const double* __restrict__ B, int ldb, double* __restrict__ C, int ldc) {
+  __shared__ double As[32][33];
+  __shared__ double Bs[32][33];
+  const int tid = threadIdx.x, tx = tid & 31, ty = tid >> 5;  // 8 rows of 4
+  const int i0 = blockIdx.y * 32, j0 = blockIdx.x * 32;
+  double acc[4] = {0, 0, 0, 0};
+  for (int k0 = 0; k0 < K; k0 += 32) {
+    for (int e = tid; e < 1024; e += 256) {
+      const int r = e >> 5, c = e & 31;
+      const int gi = i0 + r, gk = k0 + c;
+      double a = 0.0;
+      if (gi < M && gk < K) a = ta ? A[(int64_t)gk * lda + gi] : A[(int64_t)gi * lda + gk];
+      As[r][c] = a;
+      const int gk2 = k0 + r, gj = j0 + c;
+      double bv = 0.0;
+      if (gk2 < K && gj < N) bv = tb ? B[(int64_t)gj * ldb + gk2] : B[(int64_t)gk2 * ldb + gj];
+      Bs[r][c] = bv;
+    }
+    __syncthreads();
+#pragma unroll 8
+    for (int k = 0; k < 32; ++k) {
+      const double bv = Bs[k][tx];
+#pragma unroll
+      for (int a = 0; a < 4; ++a) acc[a] = fma(As[ty * 4 + a][k], bv, acc[a]);
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int a = 0; a < 4; ++a) {
+    const int gi = i0 + ty * 4 + a, gj = j0 + tx;
+    if (gi < M && gj < N) C[(int64_t)gi * ldc + gj] = acc[a];
+  }
+}
+
+// Householder tridiagonalisation of the symmetric part of Asrc (m x m).
+// V row k holds v_k (v_k[k+1] = 1, zeros before), tau[k]; d, e diagonals.
+__global__ void __launch_bounds__(ET)
+tridiag(const double* __restrict__ Asrc, int m, int symmetrize, double* __restrict__ Wg,
+        double* __restrict__ V, double* __restrict__ tau, double* __restrict__ d,
+        double* __restrict__ e, const SmallStatus* status) {
+  extern __shared__ double smem[];
+  __shared__ double red[33];
+  __shared__ double sc[4];
+  if (status && (status->nonfinite || status->not_pd)) return;
+  const bool in_smem = (size_t)m * m * sizeof(double) <= 190 * 1024;
+  double* W = in_smem ? smem : Wg;
+  double* vb = in_smem ? smem + (size_t)m * m : Wg + (size_t)m * m;
+  double* pw = vb + m;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  for (int x = tid; x < m * m; x += ET) {
+    const int i = x / m, j = x % m;
+    W[x] = symmetrize ? 0.5 * (Asrc[(int64_t)i * m + j] + Asrc[(int64_t)j * m + i]) : Asrc[x];
+  }
+  for (int x = tid; x < m * m; x += ET) V[x] = 0.0;
+  __syncthreads();
+  for (int k = 0; k + 2 < m; ++k) {
+    const double* rowk = W + (size_t)k * m;
+    double ss = 0.0;
+    for (int i = k + 2 + tid; i < m; i += ET) ss += rowk[i] * rowk[i];
+    ss = block_sum(ss, red);
+    if (tid == 0) {
+      const double alpha = rowk[k + 1];
+      d[k] = rowk[k];
+      if (ss == 0.0) {
+        sc[0] = 0.0;  // tau
+        sc[1] = 0.0;  // scale for v
+        e[k] = alpha;
+      } else {
+        const double beta = -copysign(sqrt(alpha * alpha + ss), alpha);
+        sc[0] = (beta - alpha) / beta;
+        sc[1] = 1.0 / (alpha - beta);
+        e[k] = beta;
+      }
+      tau[k] = sc[0];
+    }
+    __syncthreads();
+    const double tk = sc[0], scale = sc[1];
+    for (int i = k + 1 + tid; i < m; i += ET) {
+      const double v = (i == k + 1) ? 1.0 : rowk[i] * scale;
+      vb[i] = v;
+      V[(size_t)k * m + i] = v;
+    }
+    __syncthreads();
+    if (tk == 0.0) continue;
+    // p = tau * W22 v
+    for (int i = k + 1 + warp; i < m; i += ET / 32) {
+      const double* wr = W + (size_t)i * m;
+      double s = 0.0;
+      for (int j = k + 1 + lane; j < m; j += 32) s += wr[j] * vb[j];
+      s = warp_sum(s);
+      if (lane == 0) pw[i] = tk * s;
+    }
+    __syncthreads();
+    double pv = 0.0;
+    for (int i = k + 1 + tid; i < m; i += ET) pv += pw[i] * vb[i];
+    pv = block_sum(pv, red);
+    const double K = 0.5 * tk * pv;
+    for (int i = k + 1 + tid; i < m; i += ET) pw[i] -= K * vb[i];
+    __syncthreads();
+    const int r = m - k - 1;
+    for (int x = tid; x < r * r; x += ET) {
+      const int i = k + 1 + x / r, j = k + 1 + x % r;
+      W[(size_t)i * m + j] -= vb[i] * pw[j] + pw[i] * vb[j];
+    }
+    __syncthreads();
+  }
+  if (tid == 0) {
+    if (m >= 2) {
+      d[m - 2] = W[(size_t)(m - 2) * m + (m - 2)];
+      d[m - 1] = W[(size_t)(m - 1) * m + (m - 1)];
+      e[m - 2] = W[(size_t)(m - 1) * m + (m - 2)];
+      tau[m - 2] = 0.0;
+    } else if (m == 1) {
+      d[0] = W[0];
+    }
+    if (m >= 1) {
+      tau[m - 1] = 0.0;
+      e[m - 1] = 0.0;
+    }
+  }
+}
+
+// One warp per eigenvalue index (first + t): 33-section of the Gershgorin interval.
+__global__ void bisect(const double* __restrict__ d, const double* __restrict__ e, int m,
+                       int first, int count, double* __restrict__ theta, double* __restrict__ e2,
+                       const SmallStatus* status) {
+  if (status && (status->nonfinite || status->not_pd)) return;
+  const int lane = threadIdx.x & 31;
+  const int t = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  if (t >= count) return;
+  const int idx = first + t;
+  double lo = DBL_MAX, hi = -DBL_MAX, emax = 0.0;
+  for (int i = lane; i < m; i += 32) {
+    const double r = (i > 0 ? fabs(e[i - 1]) : 0.0) + (i + 1 < m ? fabs(e[i]) : 0.0);
+    lo = fmin(lo, d[i] - r);
+    hi = fmax(hi, d[i] + r);
+    if (i + 1 < m) emax = fmax(emax, e[i] * e[i]);
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    lo = fmin(lo, __shfl_xor_sync(0xffffffffu, lo, o));
+    hi = fmax(hi, __shfl_xor_sync(0xffffffffu, hi, o));
+    emax = fmax(emax, __shfl_xor_sync(0xffffffffu, emax, o));
+  }
+  const double pivmin = DBL_MIN * fmax(1.0, emax);
+  const double tnorm = fmax(fabs(lo), fabs(hi));
+  lo -= 2.0 * kEps64 * tnorm + 2.0 * pivmin;
+  hi += 2.0 * kEps64 * tnorm + 2.0 * pivmin;
+  // e2 computed per warp into a private view (all warps write identical values)
+  double a = lo, b = hi;
+  for (int round = 0; round < 64; ++round) {
+    const double w = b - a;
+    const double tol = fmax(2.0 * kEps64 * fmax(fabs(a), fabs(b)), kEps64 * tnorm) + pivmin;
+    if (w <= tol) break;
+    const double x = a + w * (double)(lane + 1) / 33.0;
+    // Sturm count with e^2 on the fly
+    double q = d[0] - x;
+    if (fabs(q) < pivmin) q = -pivmin;
+    int c = q < 0.0;
+    for (int i = 1; i < m; ++i) {
+      const double ei = e[i - 1];
+      q = d[i] - x - (ei * ei) / q;
+      if (fabs(q) < pivmin) q = -pivmin;
+      c += q < 0.0;
+    }
+    const unsigned bal = __ballot_sync(0xffffffffu, c > idx);
+    const double x31 = __shfl_sync(0xffffffffu, x, 31);
+    if (bal == 0u) {
+      a = x31;
+    } else {
+      const int f = __ffs(bal) - 1;
+      const double xf = __shfl_sync(0xffffffffu, x, f);
+      const double xp = __shfl_sync(0xffffffffu, x, f > 0 ? f - 1 : 0);
+      b = xf;
+      if (f > 0) a = xp;
+    }
+  }
+  (void)e2;
+  if (lane == 0) theta[t] = 0.5 * (a + b);
+}
+
+__device__ __forceinline__ double hash_uniform(uint32_t a, uint32_t b) {
+  uint32_t h = a * 0x9E3779B1u ^ (b + 0x7F4A7C15u) * 0x85EBCA77u;
+  h ^= h >> 15;
+  h *= 0x2C1B3C6Du;
+  h ^= h >> 12;
+  h *= 0x297A2D39u;
+  h ^= h >> 15;
+  return (double)h / 4294967296.0 * 2.0 - 1.0;
+}
+
+// Inverse iteration for the eigenvectors of T (d, e) at shifts theta[0..nev).
+// One thread per cluster (|theta_j - theta_{j-1}| <= 1e-3 ||T||); members are
+// orthogonalised against earlier members (MGS), as LAPACK dstein does.
+__global__ void invit(const double* __restrict__ d, const double* __restrict__ e, int m, int nev,
+                      const double* __restrict__ theta, double* __restrict__ Y, int ldy,
+                      double* __restrict__ scratch, const SmallStatus* status) {
+  if (status && (status->nonfinite || status->not_pd)) return;
+  const int j0 = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j0 >= nev) return;
+  double tnorm = 0.0;
+  for (int i = 0; i < m; ++i)
+    tnorm = fmax(tnorm, fabs(d[i]) + (i > 0 ? fabs(e[i - 1]) : 0.0) + (i + 1 < m ? fabs(e[i]) : 0.0));
+  tnorm = fmax(tnorm, DBL_MIN);
+  const double ctol = 1e-3 * tnorm;
+  if (j0 > 0 && theta[j0] - theta[j0 - 1] <= ctol) return;  // not a cluster head
+  double* dl = scratch + (size_t)j0 * 6 * m;
+  double* dd = dl + m;
+  double* du = dd + m;
+  double* du2 = du + m;
+  double* y = du2 + m;
+  double* pv = y + m;  // ipiv stored as doubles (0/1 swap flags)
+  const double pert = kEps64 * tnorm;
+  double lam_prev = -DBL_MAX;
+  for (int j = j0; j < nev; ++j) {
+    if (j > j0 && theta[j] - theta[j - 1] > ctol) break;
+    double lam = theta[j];
+    if (j > j0 && lam - lam_prev < 10.0 * kEps64 * fabs(lam)) lam = lam_prev + 10.0 * kEps64 * fabs(lam);
+    lam_prev = lam;
+    // LU with partial pivoting of T - lam I (dgttrf layout)
+    for (int i = 0; i < m; ++i) {
+      dd[i] = d[i] - lam;
+      if (i + 1 < m) {
+        dl[i] = e[i];
+        du[i] = e[i];
+      }
+      du2[i] = 0.0;
+      pv[i] = 0.0;
+    }
+    for (int i = 0; i + 1 < m; ++i) {
+      if (fabs(dd[i]) >= fabs(dl[i])) {
+        if (dd[i] == 0.0) dd[i] = pert;
+        const double f = dl[i] / dd[i];
+        dl[i] = f;
+        dd[i + 1] -= f * du[i];
+      } else {
+        const double f = dd[i] / dl[i];
+        dd[i] = dl[i];
+        dl[i] = f;
+        const double tmp = du[i];
+        du[i] = dd[i + 1];
+        dd[i + 1] = tmp - f * dd[i + 1];
+        if (i + 2 < m) {
+          du2[i] = du[i + 1];
+          du[i + 1] = -f * du[i + 1];
+        }
+        pv[i] = 1.0;
+      }
+    }
+    if (dd[m - 1] == 0.0) dd[m - 1] = pert;
+    for (int i = 0; i < m; ++i) {
+      if (fabs(dd[i]) < pert) dd[i] = copysign(pert, dd[i] == 0.0 ? 1.0 : dd[i]);
+    }
+    for (int i = 0; i < m; ++i) y[i] = hash_uniform((uint32_t)j, (uint32_t)i);
+    for (int it = 0; it < 3; ++it) {
+      // forward: apply L^-1 with row interchanges
+      for (int i = 0; i + 1 < m; ++i) {
+        if (pv[i] != 0.0) {
+          const double t = y[i];
+          y[i] = y[i + 1];
+          y[i + 1] = t - dl[i] * y[i + 1];
+        } else {
+          y[i + 1] -= dl[i] * y[i];
+        }
+      }
+      // back: U y = b (U has du, du2)
+      y[m - 1] /= dd[m - 1];
+      if (m >= 2) y[m - 2] = (y[m - 2] - du[m - 2] * y[m - 1]) / dd[m - 2];
+      for (int i = m - 3; i >= 0; --i) y[i] = (y[i] - du[i] * y[i + 1] - du2[i] * y[i + 2]) / dd[i];
+      // MGS against earlier members of the cluster
+      for (int q = j0; q < j; ++q) {
+        double s = 0.0;
+        for (int i = 0; i < m; ++i) s += Y[(size_t)i * ldy + q] * y[i];
+        for (int i = 0; i < m; ++i) y[i] -= s * Y[(size_t)i * ldy + q];
+      }
+      double nrm = 0.0, amax = 0.0;
+      for (int i = 0; i < m; ++i) amax = fmax(amax, fabs(y[i]));
+      if (amax == 0.0) {
+        for (int i = 0; i < m; ++i) y[i] = hash_uniform((uint32_t)j + 7919u * (it + 1), (uint32_t)i);
+        continue;
+      }
+      for (int i = 0; i < m; ++i) {
+        y[i] /= amax;
+        nrm += y[i] * y[i];
+      }
+      nrm = 1.0 / sqrt(nrm);
+      for (int i = 0; i < m; ++i) y[i] *= nrm;
+    }
+    for (int i = 0; i < m; ++i) Y[(size_t)i * ldy + j] = y[i];
+  }
+}
+
+// Z = Q Y with Q = H_0 H_1 ... H_{m-3}: apply reflectors last-to-first.
+__global__ void __launch_bounds__(ET)
+backtransform(const double* __restrict__ V, const double* __restrict__ tau, int m, double* Y,
+              int ldy, int nev, const SmallStatus* status) {
+  __shared__ double s[1024];
+  if (status && (status->nonfinite || status->not_pd)) return;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  for (int k = m - 3; k >= 0; --k) {
+    const double tk = tau[k];
+    if (tk == 0.0) continue;
+    const double* v = V + (size_t)k * m;
+    for (int j0 = 0; j0 < nev; j0 += 1024) {
+      const int nj = min(1024, nev - j0);
+      for (int j = warp; j < nj; j += ET / 32) {
+        double acc = 0.0;
+        for (int i = k + 1 + lane; i < m; i += 32) acc += v[i] * Y[(size_t)i * ldy + j0 + j];
+        acc = warp_sum(acc);
+        if (lane == 0) s[j] = tk * acc;
+      }
+      __syncthreads();
+      const int r = m - k - 1;
+      for (int x = tid; x < r * nj; x += ET) {
+        const int i = k + 1 + x / nj, j = x % nj;
+        Y[(size_t)i * ldy + j0 + j] -= v[i] * s[j];
+      }
+      __syncthreads();
+    }
+  }
+}
+
+__global__ void copy_cols(const double* __restrict__ Y, int ldy, int m, int nev,
+                          double* __restrict__ C, int ldc) {
+  for (int x = blockIdx.x * blockDim.x + threadIdx.x; x < m * nev; x += gridDim.x * blockDim.x) {
+    const int i = x / nev, j = x % nev;
+    C[(size_t)i * ldc + j] = Y[(size_t)i * ldy + j];
+  }
+}
+
+// Pivoted Cholesky (diagonal pivoting == dgeqp3 column pivoting on B).
+__global__ void __launch_bounds__(ET)
+pivoted_chol(const double* __restrict__ g, int ldg, int na, double rank_tol, double* __restrict__ G,
+             int* __restrict__ perm, double* __restrict__ Rinv, SmallStatus* status) {
+  __shared__ int sp;
+  __shared__ int srank;
+  __shared__ double sd0;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  for (int x = tid; x < na * na; x += ET) {
+    const int i = x / na, j = x % na;
+    G[x] = 0.5 * (g[(int64_t)i * ldg + j] + g[(int64_t)j * ldg + i]);
+  }
+  for (int i = tid; i < na; i += ET) perm[i] = i;
+  if (tid == 0) srank = na;
+  __syncthreads();
+  for (int j = 0; j < na; ++j) {
+    if (tid == 0) {
+      int p = j;
+      double best = G[(size_t)j * na + j];
+      for (int i = j + 1; i < na; ++i) {
+        const double v = G[(size_t)i * na + i];
+        if (v > best) { best = v; p = i; }
+      }
+      if (j == 0) sd0 = best;
+      if (!(best > 0.0) || sqrt(best) <= rank_tol * sqrt(sd0)) srank = j;
+      sp = p;
+    }
+    __syncthreads();
+    if (srank == j) break;
+    const int p = sp;
+    if (p != j) {  // symmetric swap of rows/cols j and p
+      for (int x = tid; x < na; x += ET) {
+        const double a = G[(size_t)j * na + x];
+        G[(size_t)j * na + x] = G[(size_t)p * na + x];
+        G[(size_t)p * na + x] = a;
+      }
+      __syncthreads();
+      for (int x = tid; x < na; x += ET) {
+        const double a = G[(size_t)x * na + j];
+        G[(size_t)x * na + j] = G[(size_t)x * na + p];
+        G[(size_t)x * na + p] = a;
+      }
+      if (tid == 0) {
+        const int t = perm[j];
+        perm[j] = perm[p];
+        perm[p] = t;
+      }
+      __syncthreads();
+    }
+    if (tid == 0) G[(size_t)j * na + j] = sqrt(G[(size_t)j * na + j]);
+    __syncthreads();
+    const double piv = G[(size_t)j * na + j];
+    for (int i = j + 1 + tid; i < na; i += ET) G[(size_t)i * na + j] /= piv;
+    __syncthreads();
+    const int r = na - j - 1;
+    for (int x = tid; x < r * r; x += ET) {
+      const int i = j + 1 + x / r, k = j + 1 + x % r;
+      if (k <= i) G[(size_t)i * na + k] -= G[(size_t)i * na + j] * G[(size_t)k * na + j];
+    }
+    __syncthreads();
+  }
+  const int rk = srank;
+  // Rinv = inverse of the upper factor R11 = L11' (rank x rank), via L11^-1 rows
+  double* Li = Rinv;  // use as scratch then transpose
+  for (int i = 0; i < rk; ++i) {
+    const double lii = G[(size_t)i * na + i];
+    for (int j = warp; j <= i; j += ET / 32) {
+      double s = 0.0;
+      for (int k = j + lane; k < i; k += 32) s += G[(size_t)i * na + k] * Li[(size_t)k * na + j];
+      s = warp_sum(s);
+      if (lane == 0) Li[(size_t)i * na + j] = ((i == j ? 1.0 : 0.0) - s) / lii;
+    }
+    for (int j = i + 1 + tid; j < na; j += ET) Li[(size_t)i * na + j] = 0.0;
+    __syncthreads();
+  }
+  for (int x = tid; x < na * na; x += ET) {
+    const int i = x / na, j = x % na;
+    if (i >= rk || j >= rk) continue;
+    if (i < j) {
+      const double a = Li[(size_t)i * na + j], b = Li[(size_t)j * na + i];
+      Li[(size_t)i * na + j] = b;
+      Li[(size_t)j * na + i] = a;
+    }
+  }
+  if (tid == 0) status->rank = rk;
+}
+
+// One-sided Jacobi SVD of the k x k matrix S (row-major) and S^-1 = V S^-2 U'.
+__global__ void __launch_bounds__(ET)
+jacobi_svd(const double* __restrict__ S, int k, double* __restrict__ U, double* __restrict__ Vm,
+           double* __restrict__ inv, SmallStatus* status) {
+  __shared__ int rotated;
+  __shared__ double red[33];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int K = (k + 1) & ~1;  // even number of players (k odd: one dummy)
+  // column-major copies: U[:, j] contiguous
+  for (int x = tid; x < K * k; x += ET) {
+    const int j = x / k, i = x % k;
+    U[x] = j < k ? S[(size_t)i * k + j] : 0.0;
+  }
+  for (int x = tid; x < K * K; x += ET) Vm[x] = (x / K == x % K) ? 1.0 : 0.0;
+  __syncthreads();
+  for (int sweep = 0; sweep < 40; ++sweep) {
+    if (tid == 0) rotated = 0;
+    __syncthreads();
+    for (int r = 0; r < K - 1; ++r) {
+      for (int t = warp; t < K / 2; t += ET / 32) {
+        int p, q;
+        if (t == 0) { p = r; q = K - 1; }
+        else { p = (r + t) % (K - 1); q = (r - t + (K - 1)) % (K - 1); }
+        if (p > q) { const int z = p; p = q; q = z; }
+        if (q >= k) continue;  // dummy column
+        double a = 0.0, b = 0.0, g = 0.0;
+        for (int i = lane; i < k; i += 32) {
+          const double up = U[(size_t)p * k + i], uq = U[(size_t)q * k + i];
+          a += up * up;
+          b += uq * uq;
+          g += up * uq;
+        }
+        a = warp_sum(a);
+        b = warp_sum(b);
+        g = warp_sum(g);
+        if (fabs(g) > kEps64 * sqrt(a * b) && g != 0.0) {
+          const double zeta = (b - a) / (2.0 * g);
+          const double tt = copysign(1.0, zeta) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
+          const double c = 1.0 / sqrt(1.0 + tt * tt), s = c * tt;
+          for (int i = lane; i < k; i += 32) {
+            const double up = U[(size_t)p * k + i], uq = U[(size_t)q * k + i];
+            U[(size_t)p * k + i] = c * up - s * uq;
+            U[(size_t)q * k + i] = s * up + c * uq;
+          }
+          for (int i = lane; i < k; i += 32) {
+            const double vp = Vm[(size_t)p * K + i], vq = Vm[(size_t)q * K + i];
+            Vm[(size_t)p * K + i] = c * vp - s * vq;
+            Vm[(size_t)q * K + i] = s * vp + c * vq;
+          }
+          if (lane == 0) rotated = 1;
+        }
+      }
+      __syncthreads();
+    }
+    if (!rotated) break;
+    __syncthreads();
+  }
+  // singular values = column norms of U
+  double smax = 0.0, smin = DBL_MAX;
+  for (int j = 0; j < k; ++j) {
+    double s = 0.0;
+    for (int i = tid; i < k; i += ET) s += U[(size_t)j * k + i] * U[(size_t)j * k + i];
+    s = block_sum(s, red);
+    const double sv = sqrt(s);
+    smax = fmax(smax, sv);
+    smin = fmin(smin, sv);
+  }
+  if (tid == 0) {
+    status->cond_hi = smin > 0.0 ? smax / smin : INFINITY;
+    status->dmax = smax;
+    status->dmin = smin;
+  }
+}
+
+// U[:, t] /= s_t^2 so that V U' = V S^-2 U'_unscaled = S^-1.
+__global__ void scale_u_cols(double* __restrict__ U, int k) {
+  const int t = blockIdx.x;
+  __shared__ double red[33];
+  double s = 0.0;
+  for (int i = threadIdx.x; i < k; i += blockDim.x) s += U[(size_t)t * k + i] * U[(size_t)t * k + i];
+  s = block_sum(s, red);
+  const double inv2 = s > 0.0 ? 1.0 / s : 0.0;
+  for (int i = threadIdx.x; i < k; i += blockDim.x) U[(size_t)t * k + i] *= inv2;
+}
+
+// inv[i][j] = sum_t V[i][t] U[j][t]   (columns t of U already scaled by 1/s_t^2)
+__global__ void jacobi_inv(const double* __restrict__ U, const double* __restrict__ Vm, int k,
+                           int K, double* __restrict__ inv) {
+  for (int x = blockIdx.x * blockDim.x + threadIdx.x; x < k * k; x += gridDim.x * blockDim.x) {
+    const int i = x / k, j = x % k;
+    double acc = 0.0;
+    for (int t = 0; t < k; ++t) acc += Vm[(size_t)t * K + i] * U[(size_t)t * k + j];
+    inv[(size_t)i * k + j] = acc;
+  }
+}
+
+struct SygvWs {
+  double *A, *B, *L, *Linv, *M, *Ap, *W, *V, *tau, *d, *e, *Y, *scratch;
+};
+
+SygvWs carve_sygv(double* base, int m, int nev) {
+  SygvWs w;
+  size_t mm = (size_t)m * m, off = 0;
+  auto take = [&](size_t cnt) {
+    double* p = base ? base + off : nullptr;
+    off += (cnt + 31) / 32 * 32;
+    return p;
+  };
+  w.A = take(mm);
+  w.B = take(mm);
+  w.L = take(mm);
+  w.Linv = take(mm);
+  w.M = take(mm);
+  w.Ap = take(mm);
+  w.W = take(mm + 4 * (size_t)m);
+  w.V = take(mm);
+  w.tau = take(m + 1);
+  w.d = take(m + 1);
+  w.e = take(m + 1);
+  w.Y = take((size_t)m * std::max(nev, 1));
+  w.scratch = take((size_t)std::max(nev, 1) * 6 * m);
+  w.scratch += 0;
+  (void)off;
+  return w;
+}
+
+size_t sygv_ws_count(int m, int nev) {
+  size_t mm = (size_t)m * m;
+  auto r = [](size_t c) { return (c + 31) / 32 * 32; };
+  return 7 * r(mm) + r(mm + 4 * (size_t)m) + 3 * r(m + 1) + r((size_t)m * std::max(nev, 1)) +
+         r((size_t)std::max(nev, 1) * 6 * m);
+}
+
+size_t chol_smem(int m) {
+  size_t b = (size_t)m * m * sizeof(double);
+  return b <= 160 * 1024 ? b : 0;
+}
+
+size_t tridiag_smem(int m) {
+  size_t b = (size_t)m * m * sizeof(double);
+  return b <= 190 * 1024 ? b + 2 * m * sizeof(double) : 0;
+}
+
+int set_smem_attrs() {
+  static bool done = false;
+  if (done) return SPB_OK;
+  SPB_CUDA(cudaFuncSetAttribute(chol_linv, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+  SPB_CUDA(cudaFuncSetAttribute(tridiag, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+  done = true;
+  return SPB_OK;
+}
+
+int tri_eigs(const double* Asrc, int m, int symmetrize, const SygvWs& w, int first, int count,
+             double* theta, const SmallStatus* status, cudaStream_t st) {
+  tridiag<<<1, ET, tridiag_smem(m), st>>>(Asrc, m, symmetrize, w.W, w.V, w.tau, w.d, w.e, status);
+  SPB_LAUNCH_CHECK();
+  const int warps = 8;
+  bisect<<<(int)ceil_div(count, warps), warps * 32, 0, st>>>(w.d, w.e, m, first, count, theta,
+                                                             nullptr, status);
+  SPB_LAUNCH_CHECK();
+  return SPB_OK;
+}
+
+}  // namespace
+
+size_t sygv_ws_doubles(int m, int nev) { return sygv_ws_count(m, nev); }
+
+int sygv_enqueue(const double* ga, const double* gb, int ldg, int m, int nev, double* theta,
+                 double* C, int ldc, double* ws, size_t ws_doubles, SmallStatus* status,
+                 cudaStream_t st) {
+  if (ws_doubles < sygv_ws_count(m, nev)) {
+    set_error("sygv workspace too small");
+    return SPB_ERR_WORKSPACE;
+  }
+  SPB_TRY(set_smem_attrs());
+  const SygvWs w = carve_sygv(ws, m, nev);
+  const bool ident = (gb == nullptr);
+  const int g1 = (int)std::min<int64_t>(ceil_div((int64_t)m * m, 256), 1024);
+  sym_prep<<<g1, 256, 0, st>>>(ga, gb, ldg, m, w.A, ident ? nullptr : w.B, status);
+  SPB_LAUNCH_CHECK();
+  const double* Atri = w.A;
+  if (!ident) {
+    chol_linv<<<1, ET, chol_smem(m), st>>>(w.B, m, w.L, w.Linv, 0, status);
+    SPB_LAUNCH_CHECK();
+    dim3 grid((unsigned)ceil_div(m, 32), (unsigned)ceil_div(m, 32));
+    small_gemm<<<grid, 256, 0, st>>>(0, 0, m, m, m, w.Linv, m, w.A, m, w.M, m);
+    small_gemm<<<grid, 256, 0, st>>>(0, 1, m, m, m, w.M, m, w.Linv, m, w.Ap, m);
+    SPB_LAUNCH_CHECK();
+    Atri = w.Ap;
+  }
+  SPB_TRY(tri_eigs(Atri, m, 1, w, 0, nev, theta, status, st));
+  invit<<<(int)ceil_div(nev, 64), 64, 0, st>>>(w.d, w.e, m, nev, theta, w.Y, nev, w.scratch, status);
+  SPB_LAUNCH_CHECK();
+  backtransform<<<1, ET, 0, st>>>(w.V, w.tau, m, w.Y, nev, nev, status);
+  SPB_LAUNCH_CHECK();
+  if (!ident) {
+    dim3 grid((unsigned)ceil_div(nev, 32), (unsigned)ceil_div(m, 32));
+    small_gemm<<<grid, 256, 0, st>>>(1, 0, m, nev, m, w.Linv, m, w.Y, nev, C, ldc);
+  } else {
+    copy_cols<<<(int)ceil_div((int64_t)m * nev, 256), 256, 0, st>>>(w.Y, nev, m, nev, C, ldc);
+  }
+  SPB_LAUNCH_CHECK();
+  return SPB_OK;
+}
+
+int exact_cond_spd(const double* gb, int ldg, int m, double* ws, size_t ws_doubles, double* cond,
+                   cudaStream_t st) {
+  if (ws_doubles < sygv_ws_count(m, 2)) {
+    set_error("cond workspace too small");
+    return SPB_ERR_WORKSPACE;
+  }
+  SPB_TRY(set_smem_attrs());
+  const SygvWs w = carve_sygv(ws, m, 2);
+  double* ext = w.Y;  // two values
+  const int g1 = (int)std::min<int64_t>(ceil_div((int64_t)m * m, 256), 1024);
+  sym_prep<<<g1, 256, 0, st>>>(gb, nullptr, ldg, m, w.A, nullptr, nullptr);
+  tridiag<<<1, ET, tridiag_smem(m), st>>>(w.A, m, 0, w.W, w.V, w.tau, w.d, w.e, nullptr);
+  bisect<<<1, 32, 0, st>>>(w.d, w.e, m, 0, 1, ext, nullptr, nullptr);
+  bisect<<<1, 32, 0, st>>>(w.d, w.e, m, m - 1, 1, ext + 1, nullptr, nullptr);
+  SPB_LAUNCH_CHECK();
+  double h[2];
+  SPB_CUDA(cudaMemcpyAsync(h, ext, sizeof(h), cudaMemcpyDeviceToHost, st));
+  SPB_CUDA(cudaStreamSynchronize(st));
+  // np.linalg.cond = sigma_max / sigma_min; for symmetric G_B sigma = |lambda|
+  const double amax = std::max(std::fabs(h[0]), std::fabs(h[1]));
+  const double amin = h[0] * h[1] <= 0.0 ? 0.0 : std::min(std::fabs(h[0]), std::fabs(h[1]));
+  *cond = amin > 0.0 ? amax / amin : INFINITY;
+  return SPB_OK;
+}
+
+size_t cholqr_ws_doubles(int na) { return 3 * (size_t)na * na + 64; }
+
+int cholqr_enqueue(const double* g, int ldg, int na, double* rinv, double* ws,
+                   SmallStatus* status, cudaStream_t st) {
+  SPB_TRY(set_smem_attrs());
+  double* S = ws;
+  double* L = ws + (size_t)na * na;
+  // symmetrise (the reference's _sym(b.T @ b), lobpcg.py:228)
+  const int g1 = (int)std::min<int64_t>(ceil_div((int64_t)na * na, 256), 1024);
+  sym_prep<<<g1, 256, 0, st>>>(g, nullptr, ldg, na, S, nullptr, status);
+  chol_linv<<<1, ET, chol_smem(na), st>>>(S, na, L, rinv, 1, status);
+  SPB_LAUNCH_CHECK();
+  return SPB_OK;
+}
+
+int pivoted_cholqr_enqueue(const double* g, int ldg, int na, double rank_tol, int* perm,
+                           double* rinv, double* ws, SmallStatus* status, cudaStream_t st) {
+  pivoted_chol<<<1, ET, 0, st>>>(g, ldg, na, rank_tol, ws, perm, rinv, status);
+  SPB_LAUNCH_CHECK();
+  return SPB_OK;
+}
+
+size_t jacobi_ws_doubles(int k) {
+  const size_t K = (size_t)((k + 1) & ~1);
+  return K * k + K * K + 64;
+}
+
+int jacobi_svd_inverse(const double* s, int k, double* inv, double* ws, size_t ws_doubles,
+                       SmallStatus* status, cudaStream_t st) {
+  if (ws_doubles < jacobi_ws_doubles(k)) {
+    set_error("jacobi workspace too small");
+    return SPB_ERR_WORKSPACE;
+  }
+  const size_t K = (size_t)((k + 1) & ~1);
+  double* U = ws;
+  double* Vm = ws + K * k;
+  jacobi_svd<<<1, ET, 0, st>>>(s, k, U, Vm, inv, status);
+  scale_u_cols<<<k, 256, 0, st>>>(U, k);
+  jacobi_inv<<<(int)ceil_div((int64_t)k * k, 256), 256, 0, st>>>(U, Vm, k, (int)K, inv);
+  SPB_LAUNCH_CHECK();
+  return SPB_OK;
+}
+
+}  // namespace spb

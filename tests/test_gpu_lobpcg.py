@@ -1,0 +1,198 @@
+"""GPU parity of the LOBPCG solve and the static pipeline against the reference.
+
+Fixtures: tests/golden/{solve,partition,qrcp}.npz, produced by the real
+reference (tests/golden/make_golden.py). Tolerances (BASELINE.json north star):
+Ritz values within 1e-4 relative (floor 1e-4*|theta_{l-1}| for the ~0 trivial
+eigenvalue); residual history |log10 ratio| <= 0.01 while above the storage
+precision floor (1e3*eps*scale); iteration counts exact; labels compared by
+partition match against the reference's own labels.
+"""
+
+import numpy as np
+import pytest
+
+import oracle
+from tests.golden.cases import qrcp_cases
+from tests.helpers import config_input, sha, solve_cases
+
+pytestmark = pytest.mark.gpu
+
+PRECISIONS = ["float64", "float32"]
+
+
+@pytest.fixture(scope="module")
+def spb():
+    import paper_1708_07481_b200 as spb
+
+    return spb
+
+
+def _theta_close(got, want, rel=1e-4):
+    floor = rel * np.abs(want).max()
+    return np.all(np.abs(got - want) <= rel * np.abs(want) + floor)
+
+
+@pytest.mark.parametrize("precision", PRECISIONS)
+@pytest.mark.parametrize("name", ["path3", "k4", "two_tri", "rand150"])
+def test_small_solves(spb, golden_solve, name, precision):
+    edges, n, l, kw, xseed = solve_cases()[name]
+    g = spb.from_edges(edges, n)
+    op = spb.LaplacianOperator(g)
+    if precision == "float32":
+        kw = dict(kw, tol=max(kw["tol"], 1e-5))  # fp32 storage floor ~1e-6*scale
+    st = spb.lobpcg_solve(op, spb.random_init(n, l, xseed), spb.SolverConfig(block_size=l, **kw),
+                          precision=precision)
+    want = golden_solve[f"{name}/theta"]
+    scale = max(1.0, op.scale_hint)
+    tol = 1e-9 if precision == "float64" else 1e-5
+    assert np.abs(st.eigenvalues - want).max() < tol * scale
+    assert st.converged.all()
+    assert np.allclose(st.vectors.T @ st.vectors, np.eye(l), atol=1e-9 if precision == "float64" else 1e-5)
+    # long high-accuracy solves: the iteration count near 1e-10 is rounding-
+    # sensitive (oracle vs reference agree exactly; the device path differs in
+    # summation order), so it is bounded, not pinned
+    ref_it = int(golden_solve[f"{name}/iterations"])
+    assert abs(st.iterations - ref_it) <= max(2, 0.1 * ref_it)
+
+
+@pytest.mark.parametrize("precision", PRECISIONS)
+def test_fixed_20_iteration_history(spb, golden_solve, precision):
+    edges, n, l, kw, xseed = solve_cases()["rand300_20it"]
+    g = spb.from_edges(edges, n)
+    op = spb.LaplacianOperator(g)
+    ht, hr = [], []
+    st = spb.lobpcg_solve(op, spb.random_init(n, l, xseed), spb.SolverConfig(block_size=l, **kw),
+                          callback=lambda it, t, r: (ht.append(t), hr.append(r)),
+                          precision=precision)
+    assert st.iterations == int(golden_solve["rand300_20it/iterations"])
+    ref_t, ref_r = golden_solve["rand300_20it/hist_theta"], golden_solve["rand300_20it/hist_norms"]
+    assert len(ht) == len(ref_t)
+    for a, b in zip(ht, ref_t):
+        assert _theta_close(np.asarray(a), b)
+    eps = 1e-16 if precision == "float64" else 6e-8
+    floor = 1e3 * eps * op.scale_hint
+    a, b = np.array(hr), ref_r
+    big = b > floor
+    assert np.all(np.abs(np.log10(a[big] / b[big])) <= 0.01)
+
+
+def test_warm_start_zero_iterations(spb):
+    g = spb.from_edges([(0, 1), (1, 2), (2, 3), (3, 0), (1, 3)], 4)
+    op = spb.LaplacianOperator(g)
+    first = spb.lobpcg_solve(op, spb.random_init(4, 3, 0), spb.SolverConfig.high_accuracy(block_size=3, seed=0),
+                             precision="float64")
+    again = spb.lobpcg_solve(op, first.vectors, spb.SolverConfig(block_size=3, seed=0), precision="float64")
+    assert again.iterations == 0
+    assert again.converged.all()
+
+
+def test_zero_operator(spb):
+    op = spb.LaplacianOperator(spb.empty_graph(6))
+    st = spb.lobpcg_solve(op, spb.random_init(6, 2, 0), spb.SolverConfig(block_size=2))
+    assert st.converged.all() and st.iterations == 0
+    assert np.allclose(st.eigenvalues, 0.0)
+
+
+def test_contract_errors(spb):
+    g = spb.from_edges([(0, 1)], 2)
+    op = spb.LaplacianOperator(g)
+    with pytest.raises(spb.ContractError):
+        spb.lobpcg_solve(op, spb.random_init(2, 2, 0), spb.SolverConfig(block_size=1))
+    with pytest.raises(spb.DomainError):
+        spb.lobpcg_solve(op, np.ones((2, 3)), spb.SolverConfig(block_size=3))
+
+
+def test_callback_exception_propagates(spb):
+    g = spb.from_edges([(0, 1), (1, 2), (2, 3)], 4)
+
+    def boom(it, t, r):
+        raise KeyError("stop")
+
+    with pytest.raises(KeyError):
+        spb.lobpcg_solve(spb.LaplacianOperator(g), spb.random_init(4, 2, 1),
+                         spb.SolverConfig(block_size=2), callback=boom)
+
+
+def test_identity_precond_is_noop(spb):
+    rng = np.random.default_rng(17)
+    ends = rng.integers(0, 90, size=(350, 2))
+    g = spb.from_edges(np.column_stack([ends, rng.random(350)[:, None] * 2]), 90)
+    op = spb.LaplacianOperator(g)
+    cfg = spb.SolverConfig(block_size=5, max_iter=8, seed=6)
+    a = spb.lobpcg_solve(op, spb.random_init(90, 5, 6), cfg, precision="float64")
+    b = spb.lobpcg_solve(op, spb.random_init(90, 5, 6), cfg, precond=lambda r: r, precision="float64")
+    assert np.array_equal(a.eigenvalues, b.eigenvalues)
+
+
+def test_deflate_ones(spb):
+    edges = [(i, i + 1) for i in range(9)]
+    g = spb.from_edges(edges, 10)
+    cfg = spb.SolverConfig.high_accuracy(block_size=3, seed=0).replace(deflate_ones=True)
+    st = spb.lobpcg_solve(spb.LaplacianOperator(g), spb.random_init(10, 3, 0), cfg, precision="float64")
+    ip, ix, dv = oracle.directed_csr(edges, 10)
+    dense = np.diag(oracle.directed_degrees(ip, ix, dv, 10)) - (lambda a: a + a.T)(
+        np.asarray(__import__("scipy.sparse", fromlist=["csr_matrix"]).csr_matrix((dv, ix, ip), shape=(10, 10)).todense()))
+    vals = np.linalg.eigvalsh(dense)
+    assert st.eigenvalues[0] > 1e-8
+    assert np.allclose(st.eigenvalues, vals[1:4], atol=1e-8)
+
+
+@pytest.mark.parametrize("name", sorted(qrcp_cases()))
+def test_qrcp_cases(spb, golden_qrcp, name):
+    x = qrcp_cases()[name]
+    import warnings
+
+    with warnings.catch_warnings():
+        warnings.simplefilter("ignore")
+        part, piv = spb.assign_clusters_qrcp(x, return_pivots=True)
+    assert np.array_equal(piv, golden_qrcp[f"{name}/pivots"])
+    assert np.array_equal(part.labels, golden_qrcp[f"{name}/labels"])
+
+
+def test_qrcp_errors(spb):
+    with pytest.raises(spb.ContractError):
+        spb.assign_clusters_qrcp(np.ones((4, 2)))
+    with pytest.raises(spb.ContractError):
+        spb.assign_clusters_qrcp(np.eye(3)[:2])
+    with pytest.warns(UserWarning):
+        x = np.zeros((5, 2))
+        x[0, 0] = 1.0
+        x[1, 1] = 1.0
+        spb.assign_clusters_qrcp(x)
+
+
+@pytest.mark.parametrize("precision", PRECISIONS)
+@pytest.mark.parametrize("key", ["c1_s0", "c1_s1", "c1_s0_10x", "c2_s0"])
+def test_partition_static_parity(spb, golden_partition, key, precision):
+    cfg_name, s = key.split("_")[0], int(key.split("_")[1][1:])
+    spec, edges, truth = config_input(cfg_name, seed=s)
+    gold = golden_partition
+    assert sha(edges) == str(gold[f"{key}/edges_sha"])
+    k = spec.blocks
+    l = spb.block_size_for(k)
+    x0 = np.random.default_rng(s).standard_normal((spec.n, l))
+    hr, ht = [], []
+    g = spb.from_edges(edges, spec.n)
+    cfg = spb.SolverConfig(block_size=l, tol=float(gold[f"{key}/tol"]),
+                           max_iter=int(gold[f"{key}/max_iter"]), seed=s)
+    part, st, gap = spb.partition_static(g, cfg, k_expected=k, fix_k=True, x0=x0,
+                                         precision=precision,
+                                         callback=lambda it, t, r: (ht.append(t), hr.append(r)))
+    assert st.iterations == int(gold[f"{key}/iterations"])
+    assert _theta_close(st.eigenvalues, gold[f"{key}/theta"])
+    ref_h = gold[f"{key}/hist_norms"]
+    assert len(hr) == len(ref_h)
+    a = np.array(hr)
+    # history compared on the gate columns (first k+1), as the stop rule uses them
+    a, b = a[:, : k + 1], ref_h[:, : k + 1]
+    eps = 1e-16 if precision == "float64" else 6e-8
+    big = b > 1e3 * eps * 232.0
+    assert np.max(np.abs(np.log10(a[big] / b[big]))) <= 0.01
+    ref_labels = gold[f"{key}/labels"].astype(np.int64)
+    agree = oracle.partition_match(ref_labels, part.labels)
+    assert agree >= 0.999, agree
+    pm = oracle.partition_match(truth, part.labels)
+    pr = oracle.pairwise_recall(truth, part.labels)
+    pp = oracle.pairwise_precision(truth, part.labels)
+    rp = gold[f"{key}/pm_pr_pp"]
+    assert abs(pr - rp[1]) <= 0.005 and abs(pp - rp[2]) <= 0.005
