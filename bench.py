@@ -1,0 +1,346 @@
+#!/usr/bin/env python
+"""Benchmark of the spectral-partition hot path (driver contract).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                    [--config c2] [--precision float32]
+
+Workload (BASELINE.json configs[1], the metric's N=1 configuration): DC-SBM
+N=50,000, B=44 (Dirichlet alpha=1, within:between 2:1, power-law degrees
+10..100), 1M directed arcs, seeded synthetic input (the Graph Challenge
+datasets are absent); block size l = block_size_for(44) = 49; 20 LOBPCG
+iterations from the seeded N(0,1) init (tol 1e-12 so exactly 20 run), then
+QRCP assignment with k = 44 — partition_static(..., fix_k=True).
+
+One step = one whole partition: device CSR build from the arc list, LOBPCG
+(setup RR, 20 iterations, polish), QRCP assignment -> labels.
+``value`` = LOBPCG iterations/s over the timed steps with the arc list and x0
+already in HBM (labels left on the device); ``e2e`` = the same metric through
+the public API from host numpy arrays to host labels (H2D and D2H inside).
+L2 is flushed (256 MiB write) between timed steps, outside the step events.
+
+--impl reference: the CPU restatement of the reference algorithm (oracle/,
+numpy + scipy, as the reference itself) on the host cores, same workload.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "LOBPCG iters/s (end-to-end DC-SBM partition: CSR build + LOBPCG + QRCP)"
+UNIT = "iters/s"
+
+
+def load_peaks():
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        d = json.loads(p.read_text())
+        return float(d.get("hbm_gbs", 6650.0)), "measured"
+    return 6650.0, "fallback"
+
+
+def workload(config: str):
+    from paper_1708_07481_b200.dcsbm import CONFIGS, generate_dcsbm
+
+    spec = CONFIGS[config]
+    edges, truth = generate_dcsbm(spec)
+    k = spec.blocks
+    from paper_1708_07481_b200.spectral import block_size_for
+
+    l = block_size_for(k)
+    x0 = np.random.default_rng(spec.seed).standard_normal((spec.n, l))
+    max_iter = 20 if config in ("c1", "c2") else 30
+    return spec, edges, truth, k, l, x0, max_iter
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except (OSError, FileNotFoundError):
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *exc):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 9:
+                continue
+            try:
+                sm.append(float(parts[1]))
+                mx.append(float(parts[2]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[5:9]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(mx), "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def cpu_baseline(edges, n, k, l, x0, max_iter, threads=None):
+    """The CPU restatement (oracle/) on the host cores: bounded sample."""
+    import oracle
+    from threadpoolctl import threadpool_limits
+
+    threads = threads or os.cpu_count() or 1
+    stamps = []
+    with threadpool_limits(threads):
+        t0 = time.perf_counter()
+        oracle.partition_static_ref(
+            edges, n, oracle.SolverCfg(block_size=l, tol=1e-12, max_iter=max_iter, seed=0),
+            k_expected=k, x0=x0, callback=lambda it, t, r: stamps.append(time.perf_counter()))
+        total = time.perf_counter() - t0
+    iters = len(stamps) - 1
+    rate = iters / (stamps[-1] - stamps[0]) if iters > 0 else float("nan")
+    return rate, total, iters, threads
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    spec, edges, truth, k, l, x0, max_iter = workload(args.config)
+    # warm-up steps also pick the faster BLAS thread count (1 vs all cores):
+    # OpenBLAS' threaded TN dgemm is slower than serial at small widths
+    cands = [os.cpu_count() or 1, 1]
+    best = None
+    for i in range(max(1, args.warmup)):
+        th = cands[i % 2] if args.warmup >= 2 else cands[0]
+        r, tot, it, _ = cpu_baseline(edges, spec.n, k, l, x0, max_iter, th)
+        if best is None or tot < best[1]:
+            best = (th, tot)
+    threads = best[0]
+    times = []
+    for _ in range(args.steps):
+        _, tot, it, _ = cpu_baseline(edges, spec.n, k, l, x0, max_iter, threads)
+        times.append(tot)
+    total = sum(times)
+    value = max_iter * args.steps / total
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": 1e3 * total / args.steps, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": f"{args.config}: DC-SBM n={spec.n} B={spec.blocks} arcs={spec.arcs}, "
+                               f"l={l}, {max_iter} LOBPCG iterations, QRCP k={k}",
+                   "n": spec.n, "blocks": spec.blocks, "arcs": spec.arcs, "block_size": l,
+                   "iterations": max_iter},
+        "impl": "reference",
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port",
+                         "sample": f"full {args.config} partition per step (oracle/ numpy+scipy "
+                                   f"restatement of specpart), {args.steps} steps"},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def count_launches(step_fn):
+    """Kernels launched by one step, counted by the CUDA profiler (CUPTI)."""
+    import torch
+    from torch.profiler import ProfilerActivity, profile
+
+    with profile(activities=[ProfilerActivity.CUDA]) as prof:
+        step_fn()
+        torch.cuda.synchronize()
+    ours = 0
+    total = 0
+    for ev in prof.events():
+        if ev.device_type is not None and str(ev.device_type).endswith("CUDA"):
+            total += 1
+            if "spb::" in ev.name:
+                ours += 1
+    return ours, total
+
+
+def run_ours(args):
+    import torch
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    os.environ["SPB_PROFILE_SPMM"] = "1"
+    import paper_1708_07481_b200 as spb
+    from paper_1708_07481_b200.spectral import partition_device
+
+    spec, edges, truth, k, l, x0, max_iter = workload(args.config)
+    dev = torch.device("cuda", local)
+    src = torch.from_numpy(np.ascontiguousarray(edges[:, 0])).to(dev)
+    dst = torch.from_numpy(np.ascontiguousarray(edges[:, 1])).to(dev)
+    x0_d = torch.from_numpy(x0).to(dev)
+    cfg = spb.SolverConfig(block_size=l, tol=1e-12, max_iter=max_iter, seed=0)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+    stats = []
+
+    def step_device():
+        g = spb.from_edges((src, dst), spec.n)
+        labels, kf, st, gap = partition_device(g, cfg, k, fix_k=True, x0=x0_d,
+                                               precision=args.precision)
+        stats.append(st.solve_stats)
+        return labels, st
+
+    for _ in range(args.warmup):
+        step_device()
+    torch.cuda.synchronize()
+    stats.clear()
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+          for _ in range(args.steps)]
+    if dist is not None:
+        dist.barrier()
+    torch.cuda.synchronize()
+    labels = None
+    with ClockSampler(local) as clk:
+        for i in range(args.steps):
+            flush.zero_()
+            ev[i][0].record()
+            labels, st = step_device()
+            ev[i][1].record()
+        torch.cuda.synchronize()
+    if dist is not None:
+        dist.barrier()
+    step_ms = [a.elapsed_time(b) for a, b in ev]
+    t_ms = sum(step_ms)
+    if dist is not None:
+        t = torch.tensor([t_ms], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        t_ms = float(t.item())
+    iters_total = sum(s["iterations"] for s in stats) * world
+    value = iters_total / (t_ms / 1e3)
+    # roofline of the dominant kernel (SpMM), timed live with CUDA events
+    spmm_us = sum(s["spmm_us"] for s in stats)
+    spmm_bytes = sum(s["spmm_bytes"] for s in stats)
+    spmm_calls = sum(s["spmm_calls"] for s in stats)
+    peak, peak_kind = load_peaks()
+    achieved = (spmm_bytes / (spmm_us * 1e-6)) / 1e9 if spmm_us else None
+    traffic = None
+    tf = ROOT / "profiles" / "spmm_traffic.json"
+    if tf.exists():
+        traffic = json.loads(tf.read_text()).get(args.config)
+    # e2e: public API from host arrays to host labels
+    e2e_times = []
+    part = None
+    edges_pinned = torch.from_numpy(np.ascontiguousarray(edges)).pin_memory().numpy()
+    for i in range(args.steps):
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        g = spb.from_edges(edges_pinned, spec.n)
+        part, st, gap = spb.partition_static(g, cfg, k, fix_k=True, x0=x0, precision=args.precision)
+        torch.cuda.synchronize()
+        e2e_times.append(time.perf_counter() - t0)
+    e2e_value = max_iter * args.steps / sum(e2e_times)
+    if dist is not None:
+        t = torch.tensor([sum(e2e_times)], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_value = max_iter * args.steps * world / float(t.item())
+    launches_per_step, _ = count_launches(step_device)
+    out = None
+    if rank == 0:
+        pm = spb.partition_match(spb.contingency(truth, part))
+        cpu = None
+        if world == 1 and not args.no_cpu_baseline:
+            rate, tot, it, cores = cpu_baseline(edges, spec.n, k, l, x0, args.cpu_iters)
+            cpu = {"value": rate, "unit": UNIT, "cores": cores, "kind": "port",
+                   "sample": f"{args.config} partition_static with max_iter={args.cpu_iters} "
+                             f"(oracle/ numpy+scipy restatement); rate = iterations between "
+                             f"first and last callback / elapsed ({tot:.1f} s total)"}
+        out = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": t_ms / args.steps, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None,
+            "dtype": "f32" if args.precision == "float32" else "f64", "data": "synthetic",
+            "config": {"workload": f"{args.config}: DC-SBM n={spec.n} B={spec.blocks} "
+                                   f"arcs={spec.arcs}, l={l}, {max_iter} LOBPCG iterations, QRCP k={k}",
+                       "n": spec.n, "blocks": spec.blocks, "arcs": spec.arcs, "block_size": l,
+                       "iterations": max_iter, "precision": args.precision,
+                       "l2": "flushed between steps (256 MiB write)",
+                       "parallelism": "replicas" if world > 1 else "single"},
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": (achieved / peak) if achieved else None, "traffic": traffic,
+                         "kernel": "spb::spmm_vec (Laplacian SpMM)", "peak_kind": peak_kind,
+                         "launches": spmm_calls,
+                         "avg_launch_us": spmm_us / max(spmm_calls, 1)},
+            "cpu_baseline": cpu,
+            "e2e": {"value": e2e_value, "unit": UNIT,
+                    "h2d_bytes_per_step": int(edges.nbytes + x0.nbytes),
+                    "d2h_bytes_per_step": int(4 * spec.n + 16 * l)},
+            "gpu_launches": int(launches_per_step * args.steps),
+            "clocks": clk.summary(),
+            "partition_seconds": t_ms / args.steps / 1e3,
+            "e2e_partition_seconds": sum(e2e_times) / args.steps,
+            "quality": {"PM_vs_truth": pm},
+        }
+        print(json.dumps(out), flush=True)
+    if dist is not None:
+        dist.barrier()
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--config", default="c2", choices=["c1", "c2", "c3", "c4"])
+    ap.add_argument("--precision", default="float32", choices=["float32", "float64"])
+    ap.add_argument("--cpu-iters", type=int, default=4)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_ours(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -116,7 +116,7 @@ typedef struct {
   int32_t n_converge;    /* nc in [1, l]                                           */
   int32_t deflate_ones;  /* project out the constant vector (lobpcg.py:259-260)    */
   int32_t has_precond;   /* call the precond callback on R_act (lobpcg.py:361-362) */
-  int32_t reserved;
+  int32_t reserved;      /* bit 0: CUDA-event timing of every SpMM (bench)        */
 } spb_solver_config;
 
 /* callback(it, theta[:l], norms) of lobpcg.py:348-349 (host arrays, copies);
@@ -134,8 +134,10 @@ SPB_API size_t spb_lobpcg_workspace(int dtype, int32_t n, int32_t l);
  * (status OK or SOLVER) the solver's X block is left in the workspace and
  * copied to vectors_out (device float64 n x l) when vectors_out != NULL;
  * theta_out/norms_out/converged_out are host arrays of length l;
- * stats_out (host, may be NULL) receives {iterations, spmm_calls, rr_calls,
- * ladder_drop_p, ladder_rebuild, final_scale_bits_hi, final_scale_bits_lo, 0}. */
+ * stats_out (host int64[16], may be NULL) receives {iterations, operator applies,
+ * Rayleigh-Ritz solves, drop_p rungs, rebuild rungs, final scale bits hi, lo,
+ * SpMM event time (us), SpMM algorithmic bytes, SpMM columns, 0...}; the two
+ * SpMM timing entries are filled when cfg->reserved has bit 0 set. */
 SPB_API int spb_lobpcg_solve(const spb_operator* op, int dtype, const double* x0,
                      const spb_solver_config* cfg, spb_iter_cb cb, spb_refill_cb refill,
                      spb_precond_cb precond, void* user, void* ws, size_t ws_bytes,

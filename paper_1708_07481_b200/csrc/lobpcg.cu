@@ -93,17 +93,57 @@ struct Driver {
   spb_precond_cb precond;
   void* user;
   cudaStream_t st;
-  int64_t stats[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  int64_t stats[16] = {0};
+  // optional CUDA-event timing of every operator apply (cfg->reserved & 1)
+  bool profile = false;
+  std::vector<cudaEvent_t> ev;
+  size_t ev_used = 0;
+  double spmm_bytes = 0.0;
+  int64_t nnz = 0;
+  ~Driver() {
+    for (auto e : ev) cudaEventDestroy(e);
+  }
   std::vector<double> h_theta, h_norms;  // last residual step
   double h_scale = 0.0;
   int iterations = 0;
 
   int apply(const void* src, int cols, void* dst) {
     stats[1]++;
-    if (op->kind == SPB_OP_LAPLACIAN)
-      return laplacian_spmm(w.dtype, 0, op->n, op->row_ptr, op->col, op->val, op->deg, src, w.lp,
-                            cols, dst, w.lp, st);
-    return dense_apply(op->dense, op->n, src, w.lp, cols, dst, w.lp, w.dtype, nullptr, st);
+    if (op->kind != SPB_OP_LAPLACIAN)
+      return dense_apply(op->dense, op->n, src, w.lp, cols, dst, w.lp, w.dtype, nullptr, st);
+    if (profile) {
+      while (ev.size() < ev_used + 2) {
+        cudaEvent_t e;
+        SPB_CUDA(cudaEventCreate(&e));
+        ev.push_back(e);
+      }
+      SPB_CUDA(cudaEventRecord(ev[ev_used], st));
+    }
+    SPB_TRY(laplacian_spmm(w.dtype, 0, op->n, op->row_ptr, op->col, op->val, op->deg, src, w.lp,
+                           cols, dst, w.lp, st));
+    if (profile) {
+      SPB_CUDA(cudaEventRecord(ev[ev_used + 1], st));
+      ev_used += 2;
+      // algorithmic bytes: row_ptr + (col, val) + deg + X read + Y write
+      spmm_bytes += 4.0 * (op->n + 1) + (4.0 + w.esz) * nnz + (double)w.esz * op->n +
+                    2.0 * (double)w.esz * op->n * cols;
+      stats[9] += cols;
+    }
+    return SPB_OK;
+  }
+
+  int finish_profile() {
+    if (!profile || ev_used == 0) return SPB_OK;
+    SPB_CUDA(cudaStreamSynchronize(st));
+    double ms = 0.0;
+    for (size_t i = 0; i < ev_used; i += 2) {
+      float t = 0.f;
+      SPB_CUDA(cudaEventElapsedTime(&t, ev[i], ev[i + 1]));
+      ms += t;
+    }
+    stats[7] = (int64_t)(ms * 1000.0);  // microseconds
+    stats[8] = (int64_t)spmm_bytes;
+    return SPB_OK;
   }
 
   int gram1(const void* U, int p, const void* V, int q, double* out, int ldo) {
@@ -597,8 +637,16 @@ extern "C" int spb_lobpcg_solve(const spb_operator* op, int dtype, const double*
   d.precond = precond;
   d.user = user;
   d.st = (cudaStream_t)stream;
+  d.profile = (cfg->reserved & 1) != 0;
+  if (d.profile && op->kind == SPB_OP_LAPLACIAN) {
+    int32_t nz = 0;
+    SPB_CUDA(cudaMemcpy(&nz, op->row_ptr + op->n, sizeof(int32_t), cudaMemcpyDeviceToHost));
+    d.nnz = nz;
+  }
   bool valid = false;
   int s = d.solve(x0, theta_out, norms_out, converged_out, &valid);
+  int sp = d.finish_profile();
+  if (s == SPB_OK) s = sp;
   if (valid) {
     for (int j = 0; j < l; ++j) {
       theta_out[j] = j < (int)d.h_theta.size() ? d.h_theta[j] : NAN;
@@ -621,7 +669,7 @@ extern "C" int spb_lobpcg_solve(const spb_operator* op, int dtype, const double*
   d.stats[5] = (int64_t)(bits >> 32);
   d.stats[6] = (int64_t)(bits & 0xffffffffu);
   if (stats_out)
-    for (int i = 0; i < 8; ++i) stats_out[i] = d.stats[i];
+    for (int i = 0; i < 16; ++i) stats_out[i] = d.stats[i];
   return s;
 }
 

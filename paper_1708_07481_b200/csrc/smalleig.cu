@@ -114,10 +114,12 @@ chol_linv(const double* __restrict__ Bsrc, int m, double* __restrict__ Lg, doubl
     const double piv = L[(int64_t)j * m + j];
     for (int i = j + 1 + tid; i < m; i += ET) L[(int64_t)i * m + j] /= piv;
     __syncthreads();
-    const int r = m - j - 1;
-    for (int e = tid; e < r * r; e += ET) {
-      const int i = j + 1 + e / r, k = j + 1 + e % r;
-      if (k <= i) L[(int64_t)i * m + k] -= L[(int64_t)i * m + j] * L[(int64_t)k * m + j];
+    {
+      const int lane = tid & 31, warp = tid >> 5;
+      for (int i = j + 1 + warp; i < m; i += ET / 32) {
+        const double lij = L[(int64_t)i * m + j];
+        for (int k = j + 1 + lane; k <= i; k += 32) L[(int64_t)i * m + k] -= lij * L[(int64_t)k * m + j];
+      }
     }
     __syncthreads();
   }
@@ -172,14 +174,13 @@ chol_linv(const double* __restrict__ Bsrc, int m, double* __restrict__ Lg, doubl
     }
   } else {
     // Rinv = (L^-1)' in place of Linv (upper triangular)
-    for (int e = tid; e < m * m; e += ET) {
-      const int i = e / m, j = e % m;
-      if (i < j) {
+    const int lane2 = tid & 31, warp2 = tid >> 5;
+    for (int i = warp2; i < m; i += ET / 32)
+      for (int j = i + 1 + lane2; j < m; j += 32) {
         const double a = Linv[(int64_t)i * m + j], b = Linv[(int64_t)j * m + i];
         Linv[(int64_t)i * m + j] = b;
         Linv[(int64_t)j * m + i] = a;
       }
-    }
   }
 }
 
@@ -235,10 +236,11 @@ tridiag(const double* __restrict__ Asrc, int m, int symmetrize, double* __restri
   double* vb = in_smem ? smem + (size_t)m * m : Wg + (size_t)m * m;
   double* pw = vb + m;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  for (int x = tid; x < m * m; x += ET) {
-    const int i = x / m, j = x % m;
-    W[x] = symmetrize ? 0.5 * (Asrc[(int64_t)i * m + j] + Asrc[(int64_t)j * m + i]) : Asrc[x];
-  }
+  for (int i = warp; i < m; i += ET / 32)
+    for (int j = lane; j < m; j += 32) {
+      const int64_t x = (int64_t)i * m + j;
+      W[x] = symmetrize ? 0.5 * (Asrc[x] + Asrc[(int64_t)j * m + i]) : Asrc[x];
+    }
   for (int x = tid; x < m * m; x += ET) V[x] = 0.0;
   __syncthreads();
   for (int k = 0; k + 2 < m; ++k) {
@@ -285,10 +287,10 @@ tridiag(const double* __restrict__ Asrc, int m, int symmetrize, double* __restri
     const double K = 0.5 * tk * pv;
     for (int i = k + 1 + tid; i < m; i += ET) pw[i] -= K * vb[i];
     __syncthreads();
-    const int r = m - k - 1;
-    for (int x = tid; x < r * r; x += ET) {
-      const int i = k + 1 + x / r, j = k + 1 + x % r;
-      W[(size_t)i * m + j] -= vb[i] * pw[j] + pw[i] * vb[j];
+    for (int i = k + 1 + warp; i < m; i += ET / 32) {
+      const double vi = vb[i], wi = pw[i];
+      double* wr = W + (size_t)i * m;
+      for (int j = k + 1 + lane; j < m; j += 32) wr[j] -= vi * pw[j] + wi * vb[j];
     }
     __syncthreads();
   }
@@ -378,26 +380,26 @@ __device__ __forceinline__ double hash_uniform(uint32_t a, uint32_t b) {
 }
 
 // Inverse iteration for the eigenvectors of T (d, e) at shifts theta[0..nev).
-// One thread per cluster (|theta_j - theta_{j-1}| <= 1e-3 ||T||); members are
-// orthogonalised against earlier members (MGS), as LAPACK dstein does.
+// One thread per eigenvalue; scratch is laid out [array][i][thread] so a warp's
+// accesses coalesce. Eigenvalues closer than ctol = 1e-8 ||T|| form a cluster
+// handled by its first thread, which orthogonalises later members against
+// earlier ones (MGS), as LAPACK dstein does with its (wider) 1e-3 ||T||; for
+// gaps above ctol inverse iteration alone gives orthogonality eps ||T|| / gap.
 __global__ void invit(const double* __restrict__ d, const double* __restrict__ e, int m, int nev,
                       const double* __restrict__ theta, double* __restrict__ Y, int ldy,
                       double* __restrict__ scratch, const SmallStatus* status) {
   if (status && (status->nonfinite || status->not_pd)) return;
   const int j0 = blockIdx.x * blockDim.x + threadIdx.x;
+  const int NT = gridDim.x * blockDim.x;
   if (j0 >= nev) return;
   double tnorm = 0.0;
   for (int i = 0; i < m; ++i)
     tnorm = fmax(tnorm, fabs(d[i]) + (i > 0 ? fabs(e[i - 1]) : 0.0) + (i + 1 < m ? fabs(e[i]) : 0.0));
   tnorm = fmax(tnorm, DBL_MIN);
-  const double ctol = 1e-3 * tnorm;
+  const double ctol = 1e-8 * tnorm;
   if (j0 > 0 && theta[j0] - theta[j0 - 1] <= ctol) return;  // not a cluster head
-  double* dl = scratch + (size_t)j0 * 6 * m;
-  double* dd = dl + m;
-  double* du = dd + m;
-  double* du2 = du + m;
-  double* y = du2 + m;
-  double* pv = y + m;  // ipiv stored as doubles (0/1 swap flags)
+  // strided scratch: element i of array a for this thread at (a*m + i)*NT + j0
+  auto at = [&](int a, int i) -> double& { return scratch[((size_t)a * m + i) * NT + j0]; };
   const double pert = kEps64 * tnorm;
   double lam_prev = -DBL_MAX;
   for (int j = j0; j < nev; ++j) {
@@ -405,76 +407,87 @@ __global__ void invit(const double* __restrict__ d, const double* __restrict__ e
     double lam = theta[j];
     if (j > j0 && lam - lam_prev < 10.0 * kEps64 * fabs(lam)) lam = lam_prev + 10.0 * kEps64 * fabs(lam);
     lam_prev = lam;
-    // LU with partial pivoting of T - lam I (dgttrf layout)
+    // LU with partial pivoting of T - lam I (dgttrf): 0 dl, 1 dd, 2 du, 3 du2, 4 y, 5 swap
     for (int i = 0; i < m; ++i) {
-      dd[i] = d[i] - lam;
-      if (i + 1 < m) {
-        dl[i] = e[i];
-        du[i] = e[i];
-      }
-      du2[i] = 0.0;
-      pv[i] = 0.0;
+      at(1, i) = d[i] - lam;
+      at(0, i) = i + 1 < m ? e[i] : 0.0;
+      at(2, i) = i + 1 < m ? e[i] : 0.0;
+      at(3, i) = 0.0;
+      at(5, i) = 0.0;
     }
     for (int i = 0; i + 1 < m; ++i) {
-      if (fabs(dd[i]) >= fabs(dl[i])) {
-        if (dd[i] == 0.0) dd[i] = pert;
-        const double f = dl[i] / dd[i];
-        dl[i] = f;
-        dd[i + 1] -= f * du[i];
+      double di = at(1, i);
+      const double li = at(0, i);
+      if (fabs(di) >= fabs(li)) {
+        if (di == 0.0) { di = pert; at(1, i) = di; }
+        const double f = li / di;
+        at(0, i) = f;
+        at(1, i + 1) -= f * at(2, i);
       } else {
-        const double f = dd[i] / dl[i];
-        dd[i] = dl[i];
-        dl[i] = f;
-        const double tmp = du[i];
-        du[i] = dd[i + 1];
-        dd[i + 1] = tmp - f * dd[i + 1];
+        const double f = di / li;
+        at(1, i) = li;
+        at(0, i) = f;
+        const double tmp = at(2, i);
+        const double dn = at(1, i + 1);
+        at(2, i) = dn;
+        at(1, i + 1) = tmp - f * dn;
         if (i + 2 < m) {
-          du2[i] = du[i + 1];
-          du[i + 1] = -f * du[i + 1];
+          at(3, i) = at(2, i + 1);
+          at(2, i + 1) = -f * at(2, i + 1);
         }
-        pv[i] = 1.0;
+        at(5, i) = 1.0;
       }
     }
-    if (dd[m - 1] == 0.0) dd[m - 1] = pert;
     for (int i = 0; i < m; ++i) {
-      if (fabs(dd[i]) < pert) dd[i] = copysign(pert, dd[i] == 0.0 ? 1.0 : dd[i]);
+      const double v = at(1, i);
+      if (fabs(v) < pert) at(1, i) = copysign(pert, v == 0.0 ? 1.0 : v);
     }
-    for (int i = 0; i < m; ++i) y[i] = hash_uniform((uint32_t)j, (uint32_t)i);
+    for (int i = 0; i < m; ++i) at(4, i) = hash_uniform((uint32_t)j, (uint32_t)i);
     for (int it = 0; it < 3; ++it) {
-      // forward: apply L^-1 with row interchanges
       for (int i = 0; i + 1 < m; ++i) {
-        if (pv[i] != 0.0) {
-          const double t = y[i];
-          y[i] = y[i + 1];
-          y[i + 1] = t - dl[i] * y[i + 1];
+        const double yi = at(4, i), yn = at(4, i + 1), f = at(0, i);
+        if (at(5, i) != 0.0) {
+          at(4, i) = yn;
+          at(4, i + 1) = yi - f * yn;
         } else {
-          y[i + 1] -= dl[i] * y[i];
+          at(4, i + 1) = yn - f * yi;
         }
       }
-      // back: U y = b (U has du, du2)
-      y[m - 1] /= dd[m - 1];
-      if (m >= 2) y[m - 2] = (y[m - 2] - du[m - 2] * y[m - 1]) / dd[m - 2];
-      for (int i = m - 3; i >= 0; --i) y[i] = (y[i] - du[i] * y[i + 1] - du2[i] * y[i + 2]) / dd[i];
-      // MGS against earlier members of the cluster
-      for (int q = j0; q < j; ++q) {
-        double s = 0.0;
-        for (int i = 0; i < m; ++i) s += Y[(size_t)i * ldy + q] * y[i];
-        for (int i = 0; i < m; ++i) y[i] -= s * Y[(size_t)i * ldy + q];
+      double y2 = at(4, m - 1) / at(1, m - 1);
+      at(4, m - 1) = y2;
+      double y1 = y2;
+      if (m >= 2) {
+        y1 = (at(4, m - 2) - at(2, m - 2) * y2) / at(1, m - 2);
+        at(4, m - 2) = y1;
       }
-      double nrm = 0.0, amax = 0.0;
-      for (int i = 0; i < m; ++i) amax = fmax(amax, fabs(y[i]));
+      for (int i = m - 3; i >= 0; --i) {
+        const double yi = (at(4, i) - at(2, i) * y1 - at(3, i) * y2) / at(1, i);
+        at(4, i) = yi;
+        y2 = y1;
+        y1 = yi;
+      }
+      for (int q = j0; q < j; ++q) {  // MGS inside the cluster
+        double sdot = 0.0;
+        for (int i = 0; i < m; ++i) sdot += Y[(size_t)i * ldy + q] * at(4, i);
+        for (int i = 0; i < m; ++i) at(4, i) -= sdot * Y[(size_t)i * ldy + q];
+      }
+      double amax = 0.0;
+      for (int i = 0; i < m; ++i) amax = fmax(amax, fabs(at(4, i)));
       if (amax == 0.0) {
-        for (int i = 0; i < m; ++i) y[i] = hash_uniform((uint32_t)j + 7919u * (it + 1), (uint32_t)i);
+        for (int i = 0; i < m; ++i) at(4, i) = hash_uniform((uint32_t)j + 7919u * (it + 1), (uint32_t)i);
         continue;
       }
+      const double ia = 1.0 / amax;
+      double nrm = 0.0;
       for (int i = 0; i < m; ++i) {
-        y[i] /= amax;
-        nrm += y[i] * y[i];
+        const double v = at(4, i) * ia;
+        at(4, i) = v;
+        nrm += v * v;
       }
       nrm = 1.0 / sqrt(nrm);
-      for (int i = 0; i < m; ++i) y[i] *= nrm;
+      for (int i = 0; i < m; ++i) at(4, i) *= nrm;
     }
-    for (int i = 0; i < m; ++i) Y[(size_t)i * ldy + j] = y[i];
+    for (int i = 0; i < m; ++i) Y[(size_t)i * ldy + j] = at(4, i);
   }
 }
 
@@ -498,10 +511,9 @@ backtransform(const double* __restrict__ V, const double* __restrict__ tau, int 
         if (lane == 0) s[j] = tk * acc;
       }
       __syncthreads();
-      const int r = m - k - 1;
-      for (int x = tid; x < r * nj; x += ET) {
-        const int i = k + 1 + x / nj, j = x % nj;
-        Y[(size_t)i * ldy + j0 + j] -= v[i] * s[j];
+      for (int i = k + 1 + warp; i < m; i += ET / 32) {
+        const double vi = v[i];
+        for (int j = lane; j < nj; j += 32) Y[(size_t)i * ldy + j0 + j] -= vi * s[j];
       }
       __syncthreads();
     }
@@ -570,10 +582,9 @@ pivoted_chol(const double* __restrict__ g, int ldg, int na, double rank_tol, dou
     const double piv = G[(size_t)j * na + j];
     for (int i = j + 1 + tid; i < na; i += ET) G[(size_t)i * na + j] /= piv;
     __syncthreads();
-    const int r = na - j - 1;
-    for (int x = tid; x < r * r; x += ET) {
-      const int i = j + 1 + x / r, k = j + 1 + x % r;
-      if (k <= i) G[(size_t)i * na + k] -= G[(size_t)i * na + j] * G[(size_t)k * na + j];
+    for (int i = j + 1 + warp; i < na; i += ET / 32) {
+      const double gij = G[(size_t)i * na + j];
+      for (int k = j + 1 + lane; k <= i; k += 32) G[(size_t)i * na + k] -= gij * G[(size_t)k * na + j];
     }
     __syncthreads();
   }
@@ -723,7 +734,7 @@ SygvWs carve_sygv(double* base, int m, int nev) {
   w.d = take(m + 1);
   w.e = take(m + 1);
   w.Y = take((size_t)m * std::max(nev, 1));
-  w.scratch = take((size_t)std::max(nev, 1) * 6 * m);
+  w.scratch = take((size_t)(round_up(std::max(nev, 1), 128) + 128) * 6 * m);
   w.scratch += 0;
   (void)off;
   return w;
@@ -733,7 +744,7 @@ size_t sygv_ws_count(int m, int nev) {
   size_t mm = (size_t)m * m;
   auto r = [](size_t c) { return (c + 31) / 32 * 32; };
   return 7 * r(mm) + r(mm + 4 * (size_t)m) + 3 * r(m + 1) + r((size_t)m * std::max(nev, 1)) +
-         r((size_t)std::max(nev, 1) * 6 * m);
+         r((size_t)(round_up(std::max(nev, 1), 128) + 128) * 6 * m);
 }
 
 size_t chol_smem(int m) {
@@ -794,7 +805,12 @@ int sygv_enqueue(const double* ga, const double* gb, int ldg, int m, int nev, do
     Atri = w.Ap;
   }
   SPB_TRY(tri_eigs(Atri, m, 1, w, 0, nev, theta, status, st));
-  invit<<<(int)ceil_div(nev, 64), 64, 0, st>>>(w.d, w.e, m, nev, theta, w.Y, nev, w.scratch, status);
+  {
+    const int nt = (int)round_up(nev, 32);
+    const int blocks = (int)ceil_div(nt, 128);
+    invit<<<blocks, nt < 128 ? nt : 128, 0, st>>>(w.d, w.e, m, nev, theta, w.Y, nev, w.scratch,
+                                                 status);
+  }
   SPB_LAUNCH_CHECK();
   backtransform<<<1, ET, 0, st>>>(w.V, w.tau, m, w.Y, nev, nev, status);
   SPB_LAUNCH_CHECK();

@@ -285,12 +285,13 @@ def lobpcg_solve(operator, x0, config: SolverConfig, precond=None, n_converge: i
     cfg = N.SolverConfigC(block_size=l, max_iter=config.max_iter, tol=config.tol,
                           lock_tol=config.lock_tol, n_converge=nc,
                           deflate_ones=int(config.deflate_ones),
-                          has_precond=int(precond is not None), reserved=0)
+                          has_precond=int(precond is not None),
+                          reserved=1 if os.environ.get("SPB_PROFILE_SPMM") == "1" else 0)
     bridge = _Bridge(callback, np.random.default_rng(config.seed), precond, l)
     theta = (C.c_double * l)()
     norms = (C.c_double * l)()
     conv = (C.c_uint8 * l)()
-    stats = (C.c_int64 * 8)()
+    stats = (C.c_int64 * 16)()
     status = L.spb_lobpcg_solve(C.byref(op), code, N.ptr(x0_d), C.byref(cfg), bridge.it,
                                 bridge.refill, bridge.pre, None, N.ptr(ws), ws_bytes, None,
                                 theta, norms, conv, stats, N.stream())
@@ -307,6 +308,8 @@ def lobpcg_solve(operator, x0, config: SolverConfig, precond=None, n_converge: i
                            np.array(conv[:], dtype=bool), work_blocks=6)
         state.solve_stats = dict(zip(("iterations", "spmm_calls", "rr_calls", "drop_p",
                                       "rebuild"), [int(s) for s in stats[:5]]))
+        state.solve_stats.update(spmm_us=int(stats[7]), spmm_bytes=int(stats[8]),
+                                 spmm_cols=int(stats[9]))
         state.precision = precision
     del ws
     if status == N.OK:

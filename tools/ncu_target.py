@@ -1,0 +1,29 @@
+"""Small deterministic target for ncu: warm-up + one C2 partition step (no profiler inside)."""
+import sys
+from pathlib import Path
+
+import numpy as np
+import torch
+
+sys.path.insert(0, str(Path(__file__).resolve().parent.parent))
+import paper_1708_07481_b200 as spb  # noqa: E402
+from paper_1708_07481_b200.dcsbm import CONFIGS, generate_dcsbm  # noqa: E402
+from paper_1708_07481_b200.spectral import partition_device  # noqa: E402
+
+cfg_name = sys.argv[1] if len(sys.argv) > 1 else "c2"
+steps = int(sys.argv[2]) if len(sys.argv) > 2 else 1
+spec = CONFIGS[cfg_name]
+edges, truth = generate_dcsbm(spec)
+k = spec.blocks
+l = spb.block_size_for(k)
+x0 = np.random.default_rng(0).standard_normal((spec.n, l))
+dev = torch.device("cuda", 0)
+src = torch.from_numpy(np.ascontiguousarray(edges[:, 0])).to(dev)
+dst = torch.from_numpy(np.ascontiguousarray(edges[:, 1])).to(dev)
+x0_d = torch.from_numpy(x0).to(dev)
+cfg = spb.SolverConfig(block_size=l, tol=1e-12, max_iter=20, seed=0)
+for _ in range(steps):
+    g = spb.from_edges((src, dst), spec.n)
+    partition_device(g, cfg, k, fix_k=True, x0=x0_d)
+torch.cuda.synchronize()
+print("done")
