@@ -165,7 +165,7 @@ struct Driver {
     int nj = 0, tiles = 0;
     for (int s = 0; s < 3; ++s) {
       if (!wd[s]) continue;
-      for (int t = 0; t < 3; ++t) {
+      for (int t = s; t < 3; ++t) {  // upper blocks only: both Grams are symmetric
         if (!wd[t]) continue;
         for (int kind = 0; kind < 2; ++kind) {
           GramJob j{S[s], kind == 0 ? LS[t] : S[t], w.lp, w.lp, wd[s], wd[t], off[s],
@@ -335,11 +335,12 @@ struct Driver {
   }
 
   // sygv with the ladder's ConditioningError semantics; *ok = success.
-  int small_gen_eigh(int m, bool identity_b, int* ok) {
+  int small_gen_eigh(int m, bool identity_b, int* ok, int seg1 = 1 << 30, int seg2 = 1 << 30) {
     stats[2]++;
     SPB_TRY(reset_status());
     SPB_TRY(sygv_enqueue(w.G, identity_b ? nullptr : w.G + w.mmax, 2 * w.mmax, m, w.l,
-                         w.theta_new, w.Cm, w.l, w.sygv_ws, w.sygv_cap, w.status, st));
+                         w.theta_new, w.Cm, w.l, w.sygv_ws, w.sygv_cap, w.status, st, seg1,
+                         seg2));
     SmallStatus hs;
     SPB_TRY(read_status(&hs));
     *ok = 0;
@@ -347,12 +348,12 @@ struct Driver {
     if (hs.cond_state == 2) {
       double cond = 0.0;
       // sygv's workspace holds the symmetrised G_B in its B slot; recompute from G
-      SPB_TRY(exact_cond_spd(w.G + w.mmax, 2 * w.mmax, m, w.sygv_ws, w.sygv_cap, &cond, st));
+      SPB_TRY(exact_cond_spd(w.G + w.mmax, 2 * w.mmax, m, w.sygv_ws, w.sygv_cap, &cond, st, seg1, seg2));
       if (!(cond <= kCondMax)) return SPB_OK;
       // exact_cond reused the workspace: redo the solve
       SPB_TRY(reset_status());
       SPB_TRY(sygv_enqueue(w.G, w.G + w.mmax, 2 * w.mmax, m, w.l, w.theta_new, w.Cm, w.l,
-                           w.sygv_ws, w.sygv_cap, w.status, st));
+                           w.sygv_ws, w.sygv_cap, w.status, st, seg1, seg2));
       SPB_TRY(read_status(&hs));
       if (hs.nonfinite || hs.not_pd) return SPB_OK;
     }
@@ -531,7 +532,7 @@ struct Driver {
           grams_ready = true;
         }
         const int m = l + na + pw;
-        SPB_TRY(small_gen_eigh(m, false, &ok));
+        SPB_TRY(small_gen_eigh(m, false, &ok, l, l + na));
         if (ok) {
           solved = true;
           break;

@@ -41,20 +41,30 @@ __device__ double block_sum(double v, double* red) {
 }
 
 // ---------------------------------------------------------------------------
+// A = sym(G_A), B = sym(G_B) (lobpcg.py:164-165). With segment boundaries
+// s1 <= s2 < m the Grams were computed only for blocks seg(i) <= seg(j); the
+// strictly lower blocks are taken from their upper mirror (the symmetric value).
 __global__ void sym_prep(const double* __restrict__ ga, const double* __restrict__ gb, int ldg,
                          int m, double* __restrict__ A, double* __restrict__ B,
-                         SmallStatus* status) {
+                         SmallStatus* status, int s1 = 1 << 30, int s2 = 1 << 30) {
   int bad = 0;
   const int64_t total = (int64_t)m * m;
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
        e += (int64_t)gridDim.x * blockDim.x) {
     const int i = (int)(e / m), j = (int)(e % m);
-    const double a = 0.5 * (ga[(int64_t)i * ldg + j] + ga[(int64_t)j * ldg + i]);
+    const int si = (i >= s1) + (i >= s2), sj = (j >= s1) + (j >= s2);
+    const int64_t ij = (int64_t)i * ldg + j, ji = (int64_t)j * ldg + i;
+    double a;
+    if (si == sj) a = 0.5 * (ga[ij] + ga[ji]);
+    else a = si < sj ? ga[ij] : ga[ji];
     A[e] = a;
     bad |= !isfinite(a);
     if (B) {
-      const double b = gb ? 0.5 * (gb[(int64_t)i * ldg + j] + gb[(int64_t)j * ldg + i])
-                          : (i == j ? 1.0 : 0.0);
+      double b = (i == j ? 1.0 : 0.0);
+      if (gb) {
+        if (si == sj) b = 0.5 * (gb[ij] + gb[ji]);
+        else b = si < sj ? gb[ij] : gb[ji];
+      }
       B[e] = b;
       bad |= !isfinite(b);
     }
@@ -63,31 +73,38 @@ __global__ void sym_prep(const double* __restrict__ ga, const double* __restrict
     atomicOr(&status->nonfinite, 1);
 }
 
-// Cholesky (lower, right-looking) of the m x m matrix Bsrc into L, then Linv = L^-1.
+// Blocked Cholesky (lower) of the m x m matrix Bsrc into L, then Linv = L^-1.
+// NB = 32 panels: the diagonal block is factored by warp 0 (warp-synchronous),
+// the sub-panel by a triangular solve (thread per row) and the trailing matrix
+// by a rank-32 update (warp per row) -> 3 CTA barriers per panel. Linv: the
+// 32 x 32 diagonal blocks are inverted by one warp each, then block rows are
+// formed in order (2 barriers per block row).
 // mode 0 (sygv): cond bracket into status. mode 1 (cholqr): the reference's
 // acceptance tests (lobpcg.py:231-235) and Rinv = (L^-1)' written to Linv.
+constexpr int CB = 32;
+
 __global__ void __launch_bounds__(ET)
 chol_linv(const double* __restrict__ Bsrc, int m, double* __restrict__ Lg, double* __restrict__ Linv,
           int mode, SmallStatus* status) {
   extern __shared__ double smem[];
   __shared__ double red[33];
   __shared__ int fail;
-  const bool in_smem = (size_t)m * m * sizeof(double) <= 160 * 1024;
+  const bool in_smem = (size_t)m * m * sizeof(double) <= 200 * 1024;
   double* L = in_smem ? smem : Lg;
-  const int tid = threadIdx.x;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   if (status->nonfinite) return;
   double fb = 0.0;
-  for (int e = tid; e < m * m; e += ET) {
-    const double v = Bsrc[e];
-    L[e] = v;
-    fb += v * v;
-  }
+  for (int i = warp; i < m; i += ET / 32)
+    for (int j = lane; j < m; j += 32) {
+      const double v = Bsrc[(int64_t)i * m + j];
+      L[(int64_t)i * m + j] = v;
+      fb += v * v;
+    }
   fb = block_sum(fb, red);
-  if (tid == 0) fail = 0;
-  if (mode == 1) {
-    // diag > 0 and min diag > (eps na)^2 max diag  (lobpcg.py:229-231)
-    double dmin = DBL_MAX, dmax = -DBL_MAX;
-    if (tid == 0) {
+  if (tid == 0) {
+    fail = 0;
+    if (mode == 1) {  // diag > 0 and min diag > (eps na)^2 max diag (lobpcg.py:229-231)
+      double dmin = DBL_MAX, dmax = -DBL_MAX;
       for (int i = 0; i < m; ++i) {
         dmin = fmin(dmin, Bsrc[(int64_t)i * m + i]);
         dmax = fmax(dmax, Bsrc[(int64_t)i * m + i]);
@@ -103,22 +120,55 @@ chol_linv(const double* __restrict__ Bsrc, int m, double* __restrict__ Lg, doubl
     if (tid == 0) status->fallback = 1;
     return;
   }
-  for (int j = 0; j < m; ++j) {
-    if (tid == 0) {
-      const double djj = L[(int64_t)j * m + j];
-      if (!(djj > 0.0)) fail = 1;
-      else L[(int64_t)j * m + j] = sqrt(djj);
+  for (int kb = 0; kb < m; kb += CB) {
+    const int nb = min(CB, m - kb);
+    if (warp == 0) {  // (a) diagonal block, warp-synchronous
+      int f = 0;
+      for (int c = 0; c < nb; ++c) {
+        double* Lc = L + (int64_t)(kb + c) * m + kb;
+        const double dcc = Lc[c];
+        f = !(dcc > 0.0);
+        if (f) break;
+        const double piv = sqrt(dcc);
+        __syncwarp();
+        if (lane == 0) Lc[c] = piv;
+        if (lane > c && lane < nb) L[(int64_t)(kb + lane) * m + kb + c] /= piv;
+        __syncwarp();
+        if (lane > c && lane < nb) {
+          double* Li = L + (int64_t)(kb + lane) * m + kb;
+          const double lic = Li[c];
+          for (int q = c + 1; q <= lane; ++q) Li[q] -= lic * L[(int64_t)(kb + q) * m + kb + c];
+        }
+        __syncwarp();
+      }
+      if (lane == 0 && f) fail = 1;
     }
     __syncthreads();
     if (fail) break;
-    const double piv = L[(int64_t)j * m + j];
-    for (int i = j + 1 + tid; i < m; i += ET) L[(int64_t)i * m + j] /= piv;
+    // (b) sub-panel: x L11' = A21 row by row
+    for (int i = kb + nb + tid; i < m; i += ET) {
+      double* Li = L + (int64_t)i * m + kb;
+      for (int c = 0; c < nb; ++c) {
+        const double* Lc = L + (int64_t)(kb + c) * m + kb;
+        double x = Li[c];
+        for (int q = 0; q < c; ++q) x -= Li[q] * Lc[q];
+        Li[c] = x / Lc[c];
+      }
+    }
     __syncthreads();
-    {
-      const int lane = tid & 31, warp = tid >> 5;
-      for (int i = j + 1 + warp; i < m; i += ET / 32) {
-        const double lij = L[(int64_t)i * m + j];
-        for (int k = j + 1 + lane; k <= i; k += 32) L[(int64_t)i * m + k] -= lij * L[(int64_t)k * m + j];
+    // (c) trailing update, lower triangle
+    for (int i = kb + nb + warp; i < m; i += ET / 32) {
+      const double* Lip = L + (int64_t)i * m + kb;
+      double li[CB];
+#pragma unroll
+      for (int c = 0; c < CB; ++c) li[c] = c < nb ? Lip[c] : 0.0;
+      for (int q = kb + nb + lane; q <= i; q += 32) {
+        const double* Lqp = L + (int64_t)q * m + kb;
+        double acc = 0.0;
+#pragma unroll
+        for (int c = 0; c < CB; ++c)
+          if (c < nb) acc += li[c] * Lqp[c];
+        L[(int64_t)i * m + q] -= acc;
       }
     }
     __syncthreads();
@@ -145,21 +195,67 @@ chol_linv(const double* __restrict__ Bsrc, int m, double* __restrict__ Lg, doubl
     if (tid == 0) status->fallback = 1;
     return;
   }
-  // Linv by rows: Linv[i][j] = (delta_ij - sum_{k=j}^{i-1} L[i][k] Linv[k][j]) / L[i][i]
-  const int lane = tid & 31, warp = tid >> 5;
-  for (int i = 0; i < m; ++i) {
-    const double lii = L[(int64_t)i * m + i];
-    for (int j = warp; j <= i; j += ET / 32) {
-      double s = 0.0;
-      for (int k = j + lane; k < i; k += 32) s += L[(int64_t)i * m + k] * Linv[(int64_t)k * m + j];
-      s = warp_sum(s);
-      if (lane == 0) Linv[(int64_t)i * m + j] = ((i == j ? 1.0 : 0.0) - s) / lii;
+  // ---- Linv. L is copied to global (read-mostly, L1/L2-cached broadcasts); the
+  // inverse is built in the shared buffer when it fits: diagonal 32 x 32 blocks
+  // by one warp each, then block rows in order (2 barriers per block row).
+  if (in_smem) {
+    for (int i = warp; i < m; i += ET / 32)
+      for (int j = lane; j <= i; j += 32) Lg[(int64_t)i * m + j] = L[(int64_t)i * m + j];
+    __syncthreads();
+  }
+  const double* Lr = Lg;  // L (lower) in global memory from here on
+  const bool inv_smem = in_smem && ((size_t)m * m + (size_t)CB * m) * sizeof(double) <= 224 * 1024;
+  double* Vi = inv_smem ? smem : Linv;                    // inverse being built
+  double* T = inv_smem ? smem + (size_t)m * m : Lg + (size_t)m * m;  // 32 x m scratch
+  for (int i = warp; i < m; i += ET / 32)
+    for (int j = lane; j < m; j += 32) Vi[(int64_t)i * m + j] = 0.0;
+  __syncthreads();
+  const int nbk = (m + CB - 1) / CB;
+  for (int bdx = warp; bdx < nbk; bdx += ET / 32) {
+    const int kb = bdx * CB, nb = min(CB, m - kb);
+    for (int i = 0; i < nb; ++i) {  // column lane of the inverse block, row by row
+      const double* Li = Lr + (int64_t)(kb + i) * m + kb;
+      if (lane <= i && lane < nb) {
+        double x = (i == lane) ? 1.0 : 0.0;
+        for (int q = lane; q < i; ++q) x -= Li[q] * Vi[(int64_t)(kb + q) * m + kb + lane];
+        Vi[(int64_t)(kb + i) * m + kb + lane] = x / Li[i];
+      }
+      __syncwarp();
     }
-    for (int j = i + 1 + tid; j < m; j += ET) Linv[(int64_t)i * m + j] = 0.0;
+  }
+  __syncthreads();
+  for (int bi = 1; bi < nbk; ++bi) {
+    const int ib = bi * CB, ni = min(CB, m - ib);
+    // T[r][c] = sum_{q=c..ib-1} L[ib+r][q] Linv[q][c], c < ib
+    for (int r = warp; r < ni; r += ET / 32) {
+      const double* Lrow = Lr + (int64_t)(ib + r) * m;
+      for (int c = lane; c < ib; c += 32) {
+        double acc = 0.0;
+        for (int q = c; q < ib; ++q) acc += Lrow[q] * Vi[(int64_t)q * m + c];
+        T[(size_t)r * m + c] = acc;
+      }
+    }
+    __syncthreads();
+    for (int r = warp; r < ni; r += ET / 32) {
+      for (int c = lane; c < ib; c += 32) {
+        double acc = 0.0;
+        for (int q = 0; q <= r; ++q) acc += Vi[(int64_t)(ib + r) * m + ib + q] * T[(size_t)q * m + c];
+        Vi[(int64_t)(ib + r) * m + c] = -acc;
+      }
+    }
+    __syncthreads();
+  }
+  if (inv_smem) {
+    for (int i = warp; i < m; i += ET / 32)
+      for (int j = lane; j < m; j += 32) Linv[(int64_t)i * m + j] = Vi[(int64_t)i * m + j];
     __syncthreads();
   }
   double fl = 0.0;
-  for (int e = tid; e < m * m; e += ET) fl += Linv[e] * Linv[e];
+  for (int i = warp; i < m; i += ET / 32)
+    for (int j = lane; j <= i; j += 32) {
+      const double v = Linv[(int64_t)i * m + j];
+      fl += v * v;
+    }
   fl = block_sum(fl, red);
   if (mode == 0) {
     if (tid == 0) {
@@ -174,9 +270,8 @@ chol_linv(const double* __restrict__ Bsrc, int m, double* __restrict__ Lg, doubl
     }
   } else {
     // Rinv = (L^-1)' in place of Linv (upper triangular)
-    const int lane2 = tid & 31, warp2 = tid >> 5;
-    for (int i = warp2; i < m; i += ET / 32)
-      for (int j = i + 1 + lane2; j < m; j += 32) {
+    for (int i = warp; i < m; i += ET / 32)
+      for (int j = i + 1 + lane; j < m; j += 32) {
         const double a = Linv[(int64_t)i * m + j], b = Linv[(int64_t)j * m + i];
         Linv[(int64_t)i * m + j] = b;
         Linv[(int64_t)j * m + i] = a;
@@ -223,13 +318,18 @@ small_gemm(int ta, int tb, int M, int N, int K, const double* __restrict__ A, in
 
 // Householder tridiagonalisation of the symmetric part of Asrc (m x m).
 // V row k holds v_k (v_k[k+1] = 1, zeros before), tau[k]; d, e diagonals.
+// Three CTA barriers per step: (1) warp 0 forms the reflector of row k;
+// (2) p = tau W22 v with the row reductions of each warp batched, plus the
+// per-warp partials of p'v; (3) the rank-2 update W22 -= v w' + w v' with
+// w = p - (tau/2)(p'v) v formed on the fly.
+template <int TRB>  // rows per warp per batch in the matvec (ceil(m/32) when it fits)
 __global__ void __launch_bounds__(ET)
 tridiag(const double* __restrict__ Asrc, int m, int symmetrize, double* __restrict__ Wg,
         double* __restrict__ V, double* __restrict__ tau, double* __restrict__ d,
         double* __restrict__ e, const SmallStatus* status) {
   extern __shared__ double smem[];
-  __shared__ double red[33];
   __shared__ double sc[4];
+  __shared__ double wpart[ET / 32];
   if (status && (status->nonfinite || status->not_pd)) return;
   const bool in_smem = (size_t)m * m * sizeof(double) <= 190 * 1024;
   double* W = in_smem ? smem : Wg;
@@ -238,67 +338,89 @@ tridiag(const double* __restrict__ Asrc, int m, int symmetrize, double* __restri
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   for (int i = warp; i < m; i += ET / 32)
     for (int j = lane; j < m; j += 32) {
-      const int64_t x = (int64_t)i * m + j;
-      W[x] = symmetrize ? 0.5 * (Asrc[x] + Asrc[(int64_t)j * m + i]) : Asrc[x];
+      const int x = i * m + j;
+      W[x] = symmetrize ? 0.5 * (Asrc[x] + Asrc[j * m + i]) : Asrc[x];
+      V[x] = 0.0;
     }
-  for (int x = tid; x < m * m; x += ET) V[x] = 0.0;
   __syncthreads();
   for (int k = 0; k + 2 < m; ++k) {
-    const double* rowk = W + (size_t)k * m;
-    double ss = 0.0;
-    for (int i = k + 2 + tid; i < m; i += ET) ss += rowk[i] * rowk[i];
-    ss = block_sum(ss, red);
-    if (tid == 0) {
+    if (warp == 0) {
+      const double* rowk = W + k * m;
+      double ss = 0.0;
+      for (int i = k + 2 + lane; i < m; i += 32) ss += rowk[i] * rowk[i];
+      ss = warp_sum(ss);
       const double alpha = rowk[k + 1];
-      d[k] = rowk[k];
-      if (ss == 0.0) {
-        sc[0] = 0.0;  // tau
-        sc[1] = 0.0;  // scale for v
-        e[k] = alpha;
-      } else {
-        const double beta = -copysign(sqrt(alpha * alpha + ss), alpha);
-        sc[0] = (beta - alpha) / beta;
-        sc[1] = 1.0 / (alpha - beta);
-        e[k] = beta;
+      double tk = 0.0, scale = 0.0, beta = alpha;
+      if (ss != 0.0) {
+        beta = -copysign(sqrt(alpha * alpha + ss), alpha);
+        tk = (beta - alpha) / beta;
+        scale = 1.0 / (alpha - beta);
       }
-      tau[k] = sc[0];
+      if (lane == 0) {
+        d[k] = rowk[k];
+        e[k] = beta;
+        tau[k] = tk;
+        sc[0] = tk;
+      }
+      for (int i = k + 1 + lane; i < m; i += 32) {
+        const double v = (i == k + 1) ? 1.0 : rowk[i] * scale;
+        vb[i] = v;
+        V[k * m + i] = v;
+      }
     }
-    __syncthreads();
-    const double tk = sc[0], scale = sc[1];
-    for (int i = k + 1 + tid; i < m; i += ET) {
-      const double v = (i == k + 1) ? 1.0 : rowk[i] * scale;
-      vb[i] = v;
-      V[(size_t)k * m + i] = v;
-    }
-    __syncthreads();
+    __syncthreads();  // (1) reflector ready
+    const double tk = sc[0];
     if (tk == 0.0) continue;
-    // p = tau * W22 v
-    for (int i = k + 1 + warp; i < m; i += ET / 32) {
-      const double* wr = W + (size_t)i * m;
-      double s = 0.0;
-      for (int j = k + 1 + lane; j < m; j += 32) s += wr[j] * vb[j];
-      s = warp_sum(s);
-      if (lane == 0) pw[i] = tk * s;
-    }
-    __syncthreads();
     double pv = 0.0;
-    for (int i = k + 1 + tid; i < m; i += ET) pv += pw[i] * vb[i];
-    pv = block_sum(pv, red);
-    const double K = 0.5 * tk * pv;
-    for (int i = k + 1 + tid; i < m; i += ET) pw[i] -= K * vb[i];
-    __syncthreads();
+    const int j0 = k + 1 + lane;
+    for (int i0 = k + 1 + warp; i0 < m; i0 += (ET / 32) * TRB) {
+      double acc[TRB];
+      const double* wr[TRB];
+#pragma unroll
+      for (int r = 0; r < TRB; ++r) {
+        acc[r] = 0.0;
+        const int i = min(i0 + r * (ET / 32), m - 1);  // clamped rows are discarded below
+        wr[r] = W + i * m;
+      }
+      for (int j = j0; j < m; j += 32) {
+        const double vj = vb[j];
+#pragma unroll
+        for (int r = 0; r < TRB; ++r) acc[r] = fma(wr[r][j], vj, acc[r]);
+      }
+#pragma unroll
+      for (int r = 0; r < TRB; ++r) acc[r] = warp_sum(acc[r]);
+      if (lane == 0) {
+#pragma unroll
+        for (int r = 0; r < TRB; ++r) {
+          const int i = i0 + r * (ET / 32);
+          if (i < m) {
+            const double p = tk * acc[r];
+            pw[i] = p;
+            pv = fma(p, vb[i], pv);
+          }
+        }
+      }
+    }
+    if (lane == 0) wpart[warp] = pv;
+    __syncthreads();  // (2) p and the p'v partials ready
+    double tot = 0.0;
+#pragma unroll 8
+    for (int w = 0; w < ET / 32; ++w) tot += wpart[w];
+    const double K = 0.5 * tk * tot;
+    for (int i = k + 1 + tid; i < m; i += ET) pw[i] = fma(-K, vb[i], pw[i]);  // w = p - K v
+    __syncthreads();  // (3) w ready
     for (int i = k + 1 + warp; i < m; i += ET / 32) {
       const double vi = vb[i], wi = pw[i];
-      double* wr = W + (size_t)i * m;
-      for (int j = k + 1 + lane; j < m; j += 32) wr[j] -= vi * pw[j] + wi * vb[j];
+      double* row = W + i * m;
+      for (int j = j0; j < m; j += 32) row[j] = fma(-vi, pw[j], fma(-wi, vb[j], row[j]));
     }
-    __syncthreads();
+    __syncthreads();  // (4) trailing matrix updated
   }
   if (tid == 0) {
     if (m >= 2) {
-      d[m - 2] = W[(size_t)(m - 2) * m + (m - 2)];
-      d[m - 1] = W[(size_t)(m - 1) * m + (m - 1)];
-      e[m - 2] = W[(size_t)(m - 1) * m + (m - 2)];
+      d[m - 2] = W[(m - 2) * m + (m - 2)];
+      d[m - 1] = W[(m - 1) * m + (m - 1)];
+      e[m - 2] = W[(m - 1) * m + (m - 2)];
       tau[m - 2] = 0.0;
     } else if (m == 1) {
       d[0] = W[0];
@@ -308,6 +430,23 @@ tridiag(const double* __restrict__ Asrc, int m, int symmetrize, double* __restri
       e[m - 1] = 0.0;
     }
   }
+}
+
+void launch_tridiag(const double* Asrc, int m, int symmetrize, double* Wg, double* V, double* tau,
+                    double* d, double* e, const SmallStatus* status, size_t smem, cudaStream_t st) {
+  const int rows = (m + 31) / 32;
+  if (rows <= 1)
+    tridiag<1><<<1, ET, smem, st>>>(Asrc, m, symmetrize, Wg, V, tau, d, e, status);
+  else if (rows <= 2)
+    tridiag<2><<<1, ET, smem, st>>>(Asrc, m, symmetrize, Wg, V, tau, d, e, status);
+  else if (rows <= 3)
+    tridiag<3><<<1, ET, smem, st>>>(Asrc, m, symmetrize, Wg, V, tau, d, e, status);
+  else if (rows <= 4)
+    tridiag<4><<<1, ET, smem, st>>>(Asrc, m, symmetrize, Wg, V, tau, d, e, status);
+  else if (rows <= 5)
+    tridiag<5><<<1, ET, smem, st>>>(Asrc, m, symmetrize, Wg, V, tau, d, e, status);
+  else
+    tridiag<8><<<1, ET, smem, st>>>(Asrc, m, symmetrize, Wg, V, tau, d, e, status);
 }
 
 // One warp per eigenvalue index (first + t): 33-section of the Gershgorin interval.
@@ -387,11 +526,15 @@ __device__ __forceinline__ double hash_uniform(uint32_t a, uint32_t b) {
 // gaps above ctol inverse iteration alone gives orthogonality eps ||T|| / gap.
 __global__ void invit(const double* __restrict__ d, const double* __restrict__ e, int m, int nev,
                       const double* __restrict__ theta, double* __restrict__ Y, int ldy,
-                      double* __restrict__ scratch, const SmallStatus* status) {
+                      double* __restrict__ gscratch, int use_smem, const SmallStatus* status) {
+  extern __shared__ double ssc[];
   if (status && (status->nonfinite || status->not_pd)) return;
   const int j0 = blockIdx.x * blockDim.x + threadIdx.x;
-  const int NT = gridDim.x * blockDim.x;
   if (j0 >= nev) return;
+  // scratch: shared memory [array][i][thread-in-block] when it fits, else global
+  double* scratch = use_smem ? ssc : gscratch;
+  const int NT = use_smem ? blockDim.x : gridDim.x * blockDim.x;
+  const int tsl = use_smem ? threadIdx.x : j0;
   double tnorm = 0.0;
   for (int i = 0; i < m; ++i)
     tnorm = fmax(tnorm, fabs(d[i]) + (i > 0 ? fabs(e[i - 1]) : 0.0) + (i + 1 < m ? fabs(e[i]) : 0.0));
@@ -399,7 +542,7 @@ __global__ void invit(const double* __restrict__ d, const double* __restrict__ e
   const double ctol = 1e-8 * tnorm;
   if (j0 > 0 && theta[j0] - theta[j0 - 1] <= ctol) return;  // not a cluster head
   // strided scratch: element i of array a for this thread at (a*m + i)*NT + j0
-  auto at = [&](int a, int i) -> double& { return scratch[((size_t)a * m + i) * NT + j0]; };
+  auto at = [&](int a, int i) -> double& { return scratch[((size_t)a * m + i) * NT + tsl]; };
   const double pert = kEps64 * tnorm;
   double lam_prev = -DBL_MAX;
   for (int j = j0; j < nev; ++j) {
@@ -443,7 +586,7 @@ __global__ void invit(const double* __restrict__ d, const double* __restrict__ e
       if (fabs(v) < pert) at(1, i) = copysign(pert, v == 0.0 ? 1.0 : v);
     }
     for (int i = 0; i < m; ++i) at(4, i) = hash_uniform((uint32_t)j, (uint32_t)i);
-    for (int it = 0; it < 3; ++it) {
+    for (int it = 0; it < 2; ++it) {
       for (int i = 0; i + 1 < m; ++i) {
         const double yi = at(4, i), yn = at(4, i + 1), f = at(0, i);
         if (at(5, i) != 0.0) {
@@ -491,32 +634,84 @@ __global__ void invit(const double* __restrict__ d, const double* __restrict__ e
   }
 }
 
-// Z = Q Y with Q = H_0 H_1 ... H_{m-3}: apply reflectors last-to-first.
+// Z = Q Y with Q = H_0 H_1 ... H_{m-3}, applied in blocks of 32 reflectors
+// (compact WY, as LAPACK dormtr/dlarft): B_b = I - V_b T_b V_b', Z = B_0 (B_1 (... (B_last Y))).
+// Per block: G = V_b'V_b, T_b by the forward column recurrence (one warp),
+// W = T_b (V_b' Y), Y -= V_b W  -> four CTA barriers per 32 reflectors.
 __global__ void __launch_bounds__(ET)
 backtransform(const double* __restrict__ V, const double* __restrict__ tau, int m, double* Y,
               int ldy, int nev, const SmallStatus* status) {
-  __shared__ double s[1024];
+  extern __shared__ double bsm[];  // W1 [32][nev], W2 [32][nev]
+  __shared__ double G[32][33];
+  __shared__ double Tm[32][33];
   if (status && (status->nonfinite || status->not_pd)) return;
+  double* W1 = bsm;
+  double* W2 = bsm + 32 * (size_t)nev;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  for (int k = m - 3; k >= 0; --k) {
-    const double tk = tau[k];
-    if (tk == 0.0) continue;
-    const double* v = V + (size_t)k * m;
-    for (int j0 = 0; j0 < nev; j0 += 1024) {
-      const int nj = min(1024, nev - j0);
-      for (int j = warp; j < nj; j += ET / 32) {
-        double acc = 0.0;
-        for (int i = k + 1 + lane; i < m; i += 32) acc += v[i] * Y[(size_t)i * ldy + j0 + j];
+  const int nrefl = m - 2;
+  if (nrefl <= 0) return;
+  for (int kb = ((nrefl - 1) / 32) * 32; kb >= 0; kb -= 32) {
+    const int nb = min(32, nrefl - kb);
+    const int r0 = kb + 1;  // first row touched by the block
+    // (1) G = V_b' V_b (upper part used)
+    for (int x = warp; x < nb * nb; x += ET / 32) {
+      const int i = x / nb, j = x % nb;
+      double acc = 0.0;
+      if (i <= j) {
+        const double* vi = V + (size_t)(kb + i) * m;
+        const double* vj = V + (size_t)(kb + j) * m;
+        for (int r = r0 + lane; r < m; r += 32) acc += vi[r] * vj[r];
         acc = warp_sum(acc);
-        if (lane == 0) s[j] = tk * acc;
       }
-      __syncthreads();
-      for (int i = k + 1 + warp; i < m; i += ET / 32) {
-        const double vi = v[i];
-        for (int j = lane; j < nj; j += 32) Y[(size_t)i * ldy + j0 + j] -= vi * s[j];
-      }
-      __syncthreads();
+      if (lane == 0) G[i][j] = acc;
     }
+    __syncthreads();
+    // (2) T (forward, columnwise): T[j][j] = tau_j; T[0:j, j] = -tau_j T[0:j,0:j] G[0:j, j]
+    if (warp == 0) {
+      for (int j = 0; j < nb; ++j) {
+        const double tj = tau[kb + j];
+        double x = 0.0;
+        if (lane < j) {
+          for (int q = lane; q < j; ++q) x += Tm[lane][q] * G[q][j];
+          x = -tj * x;
+        }
+        __syncwarp();
+        if (lane < j) Tm[lane][j] = x;
+        if (lane == j) Tm[j][j] = tj;
+        if (lane > j && lane < 32) Tm[lane][j] = 0.0;
+        __syncwarp();
+      }
+    }
+    // (3) W1 = V_b' Y  (warp j, lanes over columns)
+    for (int j = warp; j < nb; j += ET / 32) {
+      const double* vj = V + (size_t)(kb + j) * m;
+      for (int c0 = 0; c0 < nev; c0 += 32) {
+        const int c = c0 + lane;
+        double acc = 0.0;
+        if (c < nev)
+          for (int r = kb + j + 1; r < m; ++r) acc += vj[r] * Y[(size_t)r * ldy + c];
+        if (c < nev) W1[(size_t)j * nev + c] = acc;
+      }
+    }
+    __syncthreads();
+    // (4) W2 = T W1
+    for (int j = warp; j < nb; j += ET / 32)
+      for (int c = lane; c < nev; c += 32) {
+        double acc = 0.0;
+        for (int q = j; q < nb; ++q) acc += Tm[j][q] * W1[(size_t)q * nev + c];
+        W2[(size_t)j * nev + c] = acc;
+      }
+    __syncthreads();
+    // (5) Y -= V_b W2
+    for (int r = r0 + warp; r < m; r += ET / 32) {
+      const int jmax = min(nb, r - kb);  // v_{kb+j}[r] = 0 for r <= kb + j
+      for (int c = lane; c < nev; c += 32) {
+        double acc = 0.0;
+        for (int j = 0; j < jmax; ++j) acc += V[(size_t)(kb + j) * m + r] * W2[(size_t)j * nev + c];
+        Y[(size_t)r * ldy + c] -= acc;
+      }
+    }
+    __syncthreads();
   }
 }
 
@@ -724,7 +919,7 @@ SygvWs carve_sygv(double* base, int m, int nev) {
   };
   w.A = take(mm);
   w.B = take(mm);
-  w.L = take(mm);
+  w.L = take(2 * mm);
   w.Linv = take(mm);
   w.M = take(mm);
   w.Ap = take(mm);
@@ -743,13 +938,15 @@ SygvWs carve_sygv(double* base, int m, int nev) {
 size_t sygv_ws_count(int m, int nev) {
   size_t mm = (size_t)m * m;
   auto r = [](size_t c) { return (c + 31) / 32 * 32; };
-  return 7 * r(mm) + r(mm + 4 * (size_t)m) + 3 * r(m + 1) + r((size_t)m * std::max(nev, 1)) +
+  return 7 * r(mm) + r(2 * mm) + r(mm + 4 * (size_t)m) + 3 * r(m + 1) + r((size_t)m * std::max(nev, 1)) +
          r((size_t)(round_up(std::max(nev, 1), 128) + 128) * 6 * m);
 }
 
 size_t chol_smem(int m) {
   size_t b = (size_t)m * m * sizeof(double);
-  return b <= 160 * 1024 ? b : 0;
+  if (b > 200 * 1024) return 0;
+  size_t b2 = ((size_t)m * m + 32 * (size_t)m) * sizeof(double);
+  return b2 <= 224 * 1024 ? b2 : b;
 }
 
 size_t tridiag_smem(int m) {
@@ -760,15 +957,22 @@ size_t tridiag_smem(int m) {
 int set_smem_attrs() {
   static bool done = false;
   if (done) return SPB_OK;
-  SPB_CUDA(cudaFuncSetAttribute(chol_linv, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-  SPB_CUDA(cudaFuncSetAttribute(tridiag, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+  SPB_CUDA(cudaFuncSetAttribute(chol_linv, cudaFuncAttributeMaxDynamicSharedMemorySize, 224 * 1024));
+  SPB_CUDA(cudaFuncSetAttribute(tridiag<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+  SPB_CUDA(cudaFuncSetAttribute(tridiag<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+  SPB_CUDA(cudaFuncSetAttribute(tridiag<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+  SPB_CUDA(cudaFuncSetAttribute(tridiag<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+  SPB_CUDA(cudaFuncSetAttribute(tridiag<5>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+  SPB_CUDA(cudaFuncSetAttribute(tridiag<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+  SPB_CUDA(cudaFuncSetAttribute(invit, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+  SPB_CUDA(cudaFuncSetAttribute(backtransform, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
   done = true;
   return SPB_OK;
 }
 
 int tri_eigs(const double* Asrc, int m, int symmetrize, const SygvWs& w, int first, int count,
              double* theta, const SmallStatus* status, cudaStream_t st) {
-  tridiag<<<1, ET, tridiag_smem(m), st>>>(Asrc, m, symmetrize, w.W, w.V, w.tau, w.d, w.e, status);
+  launch_tridiag(Asrc, m, symmetrize, w.W, w.V, w.tau, w.d, w.e, status, tridiag_smem(m), st);
   SPB_LAUNCH_CHECK();
   const int warps = 8;
   bisect<<<(int)ceil_div(count, warps), warps * 32, 0, st>>>(w.d, w.e, m, first, count, theta,
@@ -783,7 +987,7 @@ size_t sygv_ws_doubles(int m, int nev) { return sygv_ws_count(m, nev); }
 
 int sygv_enqueue(const double* ga, const double* gb, int ldg, int m, int nev, double* theta,
                  double* C, int ldc, double* ws, size_t ws_doubles, SmallStatus* status,
-                 cudaStream_t st) {
+                 cudaStream_t st, int seg1, int seg2) {
   if (ws_doubles < sygv_ws_count(m, nev)) {
     set_error("sygv workspace too small");
     return SPB_ERR_WORKSPACE;
@@ -792,7 +996,7 @@ int sygv_enqueue(const double* ga, const double* gb, int ldg, int m, int nev, do
   const SygvWs w = carve_sygv(ws, m, nev);
   const bool ident = (gb == nullptr);
   const int g1 = (int)std::min<int64_t>(ceil_div((int64_t)m * m, 256), 1024);
-  sym_prep<<<g1, 256, 0, st>>>(ga, gb, ldg, m, w.A, ident ? nullptr : w.B, status);
+  sym_prep<<<g1, 256, 0, st>>>(ga, gb, ldg, m, w.A, ident ? nullptr : w.B, status, seg1, seg2);
   SPB_LAUNCH_CHECK();
   const double* Atri = w.A;
   if (!ident) {
@@ -806,13 +1010,21 @@ int sygv_enqueue(const double* ga, const double* gb, int ldg, int m, int nev, do
   }
   SPB_TRY(tri_eigs(Atri, m, 1, w, 0, nev, theta, status, st));
   {
-    const int nt = (int)round_up(nev, 32);
-    const int blocks = (int)ceil_div(nt, 128);
-    invit<<<blocks, nt < 128 ? nt : 128, 0, st>>>(w.d, w.e, m, nev, theta, w.Y, nev, w.scratch,
-                                                 status);
+    const size_t per_thread = 6 * (size_t)m * sizeof(double);
+    const int tpb = 16;
+    if (per_thread * tpb <= 200 * 1024) {
+      invit<<<(int)ceil_div(nev, tpb), tpb, per_thread * tpb, st>>>(w.d, w.e, m, nev, theta, w.Y,
+                                                                    nev, w.scratch, 1, status);
+    } else {
+      const int nt = (int)round_up(nev, 32);
+      const int blocks = (int)ceil_div(nt, 128);
+      invit<<<blocks, nt < 128 ? nt : 128, 0, st>>>(w.d, w.e, m, nev, theta, w.Y, nev, w.scratch,
+                                                   0, status);
+    }
   }
   SPB_LAUNCH_CHECK();
-  backtransform<<<1, ET, 0, st>>>(w.V, w.tau, m, w.Y, nev, nev, status);
+  backtransform<<<1, ET, 2 * 32 * sizeof(double) * (size_t)nev, st>>>(w.V, w.tau, m, w.Y, nev,
+                                                                     nev, status);
   SPB_LAUNCH_CHECK();
   if (!ident) {
     dim3 grid((unsigned)ceil_div(nev, 32), (unsigned)ceil_div(m, 32));
@@ -825,7 +1037,7 @@ int sygv_enqueue(const double* ga, const double* gb, int ldg, int m, int nev, do
 }
 
 int exact_cond_spd(const double* gb, int ldg, int m, double* ws, size_t ws_doubles, double* cond,
-                   cudaStream_t st) {
+                   cudaStream_t st, int seg1, int seg2) {
   if (ws_doubles < sygv_ws_count(m, 2)) {
     set_error("cond workspace too small");
     return SPB_ERR_WORKSPACE;
@@ -834,8 +1046,8 @@ int exact_cond_spd(const double* gb, int ldg, int m, double* ws, size_t ws_doubl
   const SygvWs w = carve_sygv(ws, m, 2);
   double* ext = w.Y;  // two values
   const int g1 = (int)std::min<int64_t>(ceil_div((int64_t)m * m, 256), 1024);
-  sym_prep<<<g1, 256, 0, st>>>(gb, nullptr, ldg, m, w.A, nullptr, nullptr);
-  tridiag<<<1, ET, tridiag_smem(m), st>>>(w.A, m, 0, w.W, w.V, w.tau, w.d, w.e, nullptr);
+  sym_prep<<<g1, 256, 0, st>>>(gb, nullptr, ldg, m, w.A, nullptr, nullptr, seg1, seg2);
+  launch_tridiag(w.A, m, 0, w.W, w.V, w.tau, w.d, w.e, nullptr, tridiag_smem(m), st);
   bisect<<<1, 32, 0, st>>>(w.d, w.e, m, 0, 1, ext, nullptr, nullptr);
   bisect<<<1, 32, 0, st>>>(w.d, w.e, m, m - 1, 1, ext + 1, nullptr, nullptr);
   SPB_LAUNCH_CHECK();

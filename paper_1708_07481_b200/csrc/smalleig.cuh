@@ -23,13 +23,15 @@ constexpr double kCondMax = 67108864.0;  // 1/sqrt(eps) (lobpcg.py:35)
 size_t sygv_ws_doubles(int m, int nev);
 // G_A, G_B: device float64 m x m (ld ldg); gb may be null (B = I).
 // theta: device nev; C: device m x nev (ld ldc). status: device.
+// seg1 <= seg2: column-block boundaries of the basis when only the upper
+// blocks of the Grams were computed (default: one block, full symmetrisation).
 int sygv_enqueue(const double* ga, const double* gb, int ldg, int m, int nev, double* theta,
                  double* C, int ldc, double* ws, size_t ws_doubles, SmallStatus* status,
-                 cudaStream_t st);
+                 cudaStream_t st, int seg1 = 1 << 30, int seg2 = 1 << 30);
 // Exact cond2 of the symmetrised G_B (tridiagonal + bisection for the extreme
 // eigenvalues), for the undecided case; writes host *cond.
 int exact_cond_spd(const double* gb, int ldg, int m, double* ws, size_t ws_doubles, double* cond,
-                   cudaStream_t st);
+                   cudaStream_t st, int seg1 = 1 << 30, int seg2 = 1 << 30);
 
 // CholQR factors (lobpcg.py:228-237): Rinv (na x na, upper, ld na) with
 // B <- B Rinv orthonormal; status->fallback set when the reference would take
