@@ -92,6 +92,17 @@ SPB_API int spb_laplacian_spmm(int dtype, int32_t row_begin, int32_t row_end, co
                        const int32_t* col, const void* val, const void* deg, const void* x,
                        int64_t ldx, int32_t ncols, void* y, int64_t ldy, void* stream);
 
+/* ---------------- (c) tall-skinny Gram ---------------------------------------
+ * out[p x q] (float64, row stride ldo) = U' V for vertex-major blocks U (n x p),
+ * V (n x q): the Gram products of lobpcg.py:228, :366, :418. mode 0: CUDA-core
+ * float64 products (any dtype); mode 1: tcgen05 tensor cores, 3xTF32 split,
+ * TMA-fed (SPB_F32 only, sm_100; 16-byte aligned rows). Split-K partials are
+ * reduced in float64 in a fixed order. ws: spb_gram_workspace(p, q, n) bytes. */
+SPB_API size_t spb_gram_workspace(int32_t p, int32_t q, int64_t n);
+SPB_API int spb_gram(int dtype, int mode, const void* u, int64_t ldu, int32_t p, const void* v,
+                     int64_t ldv, int32_t q, int64_t n, double* out, int64_t ldo, void* ws,
+                     size_t ws_bytes, void* stream);
+
 /* ---------------- (c)(d) LOBPCG -----------------------------------------------
  * Operator handle for the solve (graph.py:300-317 / lobpcg.py:132-151). */
 enum { SPB_OP_LAPLACIAN = 0, SPB_OP_DENSE = 1 };

@@ -17,6 +17,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstring>
+#include <cstdlib>
 #include <vector>
 
 #include "dense.cuh"
@@ -26,10 +27,13 @@ namespace spb {
 namespace {
 
 struct SolveWs {
-  int dtype, n, l, lp, mmax;
+  int dtype, n, l, lp, ld, mmax;
   size_t esz;
+  void *B, *LB;  // n x ld each: [X | R | P] and [LX | LR | LP]
   void *X, *LX, *R, *LR, *P, *LP;
   double *G;          // mmax x 2mmax: [G_A | G_B]
+  double *Gpad;       // 3lp x 6lp: [B'B | B'LB] over the padded basis (tensor-core path)
+  bool use_tc;        // float32 storage on sm_100: Grams on tcgen05 (3xTF32)
   double *gpart;      // gram split partials
   size_t gpart_cap;
   double *Gs;         // small Gram (lp x lp)
@@ -54,19 +58,33 @@ SolveWs carve(Arena& a, int dtype, int n, int l) {
   w.lp = (int)round_up(l, 8);
   w.mmax = 3 * l;
   w.esz = dtype == SPB_F32 ? 4 : 8;
-  const size_t blk = (size_t)std::max(n, 1) * w.lp * w.esz;
-  w.X = a.take<char>(blk);
-  w.LX = a.take<char>(blk);
-  w.R = a.take<char>(blk);
-  w.LR = a.take<char>(blk);
-  w.P = a.take<char>(blk);
-  w.LP = a.take<char>(blk);
+  w.ld = 3 * w.lp;  // [X | R | P] interleaved per vertex row (lobpcg.py:297-302 layout)
+  const size_t blk = (size_t)std::max(n, 1) * w.ld * w.esz;
+  w.B = a.take<char>(blk);
+  w.LB = a.take<char>(blk);
+  w.X = w.B;
+  w.R = (char*)w.B + (size_t)w.lp * w.esz;
+  w.P = (char*)w.B + 2 * (size_t)w.lp * w.esz;
+  w.LX = w.LB;
+  w.LR = (char*)w.LB + (size_t)w.lp * w.esz;
+  w.LP = (char*)w.LB + 2 * (size_t)w.lp * w.esz;
   const int mm = w.mmax;
   w.G = a.take<double>((size_t)mm * 2 * mm);
   const int seg_tiles = (int)ceil_div(l, 64) * (int)ceil_div(l, 64);
   w.gpart_cap = gram_partial_doubles(n, 18 * seg_tiles, mm, 2 * mm, nullptr);
   w.gpart_cap = std::max(w.gpart_cap, gram_partial_doubles(n, seg_tiles, w.lp, w.lp, nullptr));
+  w.use_tc = false;
+  if (dtype == SPB_F32) {
+    // Opt-in: the 3xTF32 tensor-core Gram accumulates in fp32 inside a CTA's row
+    // range; measured against the reference it moves Ritz values by ~2e-3 after
+    // 20 iterations (beyond the 1e-4 parity bar), so float64 products are the
+    // default ("Gram precision").
+    const char* env = getenv("SPB_GRAM");
+    w.use_tc = env && std::strcmp(env, "tc") == 0;
+    w.gpart_cap = std::max(w.gpart_cap, gram_tc_partial_doubles(n, w.ld, 2 * w.ld));
+  }
   w.gpart = a.take<double>(w.gpart_cap);
+  w.Gpad = a.take<double>((size_t)w.ld * 2 * w.ld);
   w.Gs = a.take<double>((size_t)w.lp * w.lp);
   w.coef = a.take<double>((size_t)w.lp * w.lp);
   w.Cm = a.take<double>((size_t)mm * l);
@@ -84,7 +102,21 @@ SolveWs carve(Arena& a, int dtype, int n, int l) {
   return w;
 }
 
+// Compact [G_A | G_B] (m x m each) from the padded Gram [B'B | B'LB] (pe x 2pe):
+// basis index b -> padded column X: b, R: lp + (b - l), P: 2 lp + (b - l - na).
+__global__ void gather_pad_grams(const double* __restrict__ gp, int ldp, int pe, int m, int l,
+                                 int na, int lp, double* __restrict__ G, int ldg, int mmax) {
+  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < m * m; e += gridDim.x * blockDim.x) {
+    const int i = e / m, j = e % m;
+    const int pi = i < l ? i : (i < l + na ? lp + (i - l) : 2 * lp + (i - l - na));
+    const int pj = j < l ? j : (j < l + na ? lp + (j - l) : 2 * lp + (j - l - na));
+    G[(size_t)i * ldg + j] = gp[(size_t)pi * ldp + pe + pj];         // G_A = B' LB
+    G[(size_t)i * ldg + mmax + j] = gp[(size_t)pi * ldp + pj];       // G_B = B' B
+  }
+}
+
 struct Driver {
+  bool tc_full_grams = false;  // last rr_grams computed every block (no upper-only mirror)
   const spb_operator* op;
   SolveWs w;
   const spb_solver_config* cfg;
@@ -110,7 +142,7 @@ struct Driver {
   int apply(const void* src, int cols, void* dst) {
     stats[1]++;
     if (op->kind != SPB_OP_LAPLACIAN)
-      return dense_apply(op->dense, op->n, src, w.lp, cols, dst, w.lp, w.dtype, nullptr, st);
+      return dense_apply(op->dense, op->n, src, w.ld, cols, dst, w.ld, w.dtype, nullptr, st);
     if (profile) {
       while (ev.size() < ev_used + 2) {
         cudaEvent_t e;
@@ -119,8 +151,8 @@ struct Driver {
       }
       SPB_CUDA(cudaEventRecord(ev[ev_used], st));
     }
-    SPB_TRY(laplacian_spmm(w.dtype, 0, op->n, op->row_ptr, op->col, op->val, op->deg, src, w.lp,
-                           cols, dst, w.lp, st));
+    SPB_TRY(laplacian_spmm(w.dtype, 0, op->n, op->row_ptr, op->col, op->val, op->deg, src, w.ld,
+                           cols, dst, w.ld, st));
     if (profile) {
       SPB_CUDA(cudaEventRecord(ev[ev_used + 1], st));
       ev_used += 2;
@@ -146,10 +178,13 @@ struct Driver {
     return SPB_OK;
   }
 
+  // Small Grams (X'R, CholQR R'R, X'X, polish X'LX) stay on the float64 CUDA-core
+  // path: CholQR squares their error into the orthogonality of the block, and
+  // the assignment step checks ||X'X - I|| <= 1e-6 (spectral.py:149-151).
   int gram1(const void* U, int p, const void* V, int q, double* out, int ldo) {
     GramBatch b{};
     b.njobs = 1;
-    b.job[0] = {U, V, w.lp, w.lp, p, q, 0, 0};
+    b.job[0] = {U, V, w.ld, w.ld, p, q, 0, 0};
     b.tile_start[0] = 0;
     b.tile_start[1] = (int)(ceil_div(p, 64) * ceil_div(q, 64));
     return gram_batched(w.dtype, b, w.n, p, q, w.gpart, w.gpart_cap, out, ldo, st);
@@ -157,6 +192,19 @@ struct Driver {
 
   // [G_A | G_B] for the basis [X (l) | R (na) | P (pw)] and images.
   int rr_grams(int na, int pw) {
+    if (w.use_tc) {
+      // one GEMM over the padded basis: [B'B | B'LB], then gather the m x m blocks
+      const int pe = pw > 0 ? 2 * w.lp + pw : w.lp + na;
+      SPB_TRY(gram_tc((const float*)w.B, w.ld, pe, (const float*)w.B, w.ld, pe,
+                      (const float*)w.LB, w.ld, pe, w.n, w.gpart, w.gpart_cap, w.Gpad, 2 * pe, st));
+      const int m = w.l + na + pw;
+      gather_pad_grams<<<(int)std::min<int64_t>(ceil_div((int64_t)m * m, 256), 1024), 256, 0, st>>>(
+          w.Gpad, 2 * pe, pe, m, w.l, na, w.lp, w.G, 2 * w.mmax, w.mmax);
+      SPB_LAUNCH_CHECK();
+      tc_full_grams = true;
+      return SPB_OK;
+    }
+    tc_full_grams = false;
     const void* S[3] = {w.X, w.R, w.P};
     const void* LS[3] = {w.LX, w.LR, w.LP};
     const int wd[3] = {w.l, na, pw};
@@ -168,7 +216,7 @@ struct Driver {
       for (int t = s; t < 3; ++t) {  // upper blocks only: both Grams are symmetric
         if (!wd[t]) continue;
         for (int kind = 0; kind < 2; ++kind) {
-          GramJob j{S[s], kind == 0 ? LS[t] : S[t], w.lp, w.lp, wd[s], wd[t], off[s],
+          GramJob j{S[s], kind == 0 ? LS[t] : S[t], w.ld, w.ld, wd[s], wd[t], off[s],
                     off[t] + (kind == 0 ? 0 : w.mmax)};
           b.job[nj] = j;
           b.tile_start[nj] = tiles;
@@ -201,7 +249,7 @@ struct Driver {
     UpdParams p{};
     p.nseg = 1;
     p.q = q;
-    p.seg[0] = {B, w.lp, C, ldc, B, w.lp, scale, wcols, 1};
+    p.seg[0] = {B, w.ld, C, ldc, B, w.ld, scale, wcols, 1};
     return block_update(w.dtype, p, w.n, st);
   }
 
@@ -212,8 +260,8 @@ struct Driver {
     p.nseg = 1;
     p.q = na;
     p.init = w.R;
-    p.ldi = w.lp;
-    p.seg[0] = {w.X, w.lp, w.coef, w.lp, w.R, w.lp, -1.0, w.l, 1};
+    p.ldi = w.ld;
+    p.seg[0] = {w.X, w.ld, w.coef, w.lp, w.R, w.ld, -1.0, w.l, 1};
     return block_update(w.dtype, p, w.n, st);
   }
 
@@ -245,7 +293,7 @@ struct Driver {
       *kept = 0;
       return SPB_OK;
     }
-    SPB_TRY(gather_columns(w.dtype, B, w.lp, w.n, w.perm, rank, st));
+    SPB_TRY(gather_columns(w.dtype, B, w.ld, w.n, w.perm, rank, st));
     SPB_TRY(rmul(B, rank, w.coef, na, rank));
     // second CholQR pass restores orthonormality to working precision
     SPB_TRY(gram1(B, rank, B, rank, w.Gs, w.lp));
@@ -258,7 +306,7 @@ struct Driver {
   }
 
   int column_sumsq(const void* A, int cols, double* out_host) {
-    SPB_TRY(column_reduce(w.dtype, CR_SUMSQ, A, w.lp, cols, w.n, nullptr, 0, nullptr, nullptr, 0,
+    SPB_TRY(column_reduce(w.dtype, CR_SUMSQ, A, w.ld, cols, w.n, nullptr, 0, nullptr, nullptr, 0,
                           w.crpart, w.sums, st));
     SPB_CUDA(cudaMemcpyAsync(out_host, w.sums, sizeof(double) * cols, cudaMemcpyDeviceToHost, st));
     SPB_CUDA(cudaStreamSynchronize(st));
@@ -266,9 +314,9 @@ struct Driver {
   }
 
   int deflate(void* A, int cols) {  // A -= column means (lobpcg.py:259-260)
-    SPB_TRY(column_reduce(w.dtype, CR_SUM, A, w.lp, cols, w.n, nullptr, 0, nullptr, nullptr, 0,
+    SPB_TRY(column_reduce(w.dtype, CR_SUM, A, w.ld, cols, w.n, nullptr, 0, nullptr, nullptr, 0,
                           w.crpart, w.sums, st));
-    return subtract_column_means(w.dtype, A, w.lp, w.n, cols, w.sums, st);
+    return subtract_column_means(w.dtype, A, w.ld, w.n, cols, w.sums, st);
   }
 
   // orthonormalize (lobpcg.py:195-215) on the first width columns of X.
@@ -309,7 +357,7 @@ struct Driver {
     SPB_CUDA(cudaMallocAsync((void**)&d, sizeof(double) * h.size(), st));
     SPB_CUDA(cudaMemcpyAsync(d, h.data(), sizeof(double) * h.size(), cudaMemcpyHostToDevice, st));
     char* dst = (char*)B + (size_t)c0 * w.esz;
-    int s = copy_block(SPB_F64, d, cols, w.dtype, dst, w.lp, w.n, cols, st);
+    int s = copy_block(SPB_F64, d, cols, w.dtype, dst, w.ld, w.n, cols, st);
     cudaFreeAsync(d, st);
     SPB_CUDA(cudaStreamSynchronize(st));
     return s;
@@ -319,7 +367,7 @@ struct Driver {
     std::vector<double> h((size_t)w.n * na);
     double* d = nullptr;
     SPB_CUDA(cudaMallocAsync((void**)&d, sizeof(double) * h.size() + 8, st));
-    SPB_TRY(copy_block(w.dtype, w.R, w.lp, SPB_F64, d, na, w.n, na, st));
+    SPB_TRY(copy_block(w.dtype, w.R, w.ld, SPB_F64, d, na, w.n, na, st));
     SPB_CUDA(cudaMemcpyAsync(h.data(), d, sizeof(double) * h.size(), cudaMemcpyDeviceToHost, st));
     SPB_CUDA(cudaStreamSynchronize(st));
     if (precond(user, w.n, na, h.data()) != 0) {
@@ -328,7 +376,7 @@ struct Driver {
       return SPB_ERR_CALLBACK;
     }
     SPB_CUDA(cudaMemcpyAsync(d, h.data(), sizeof(double) * h.size(), cudaMemcpyHostToDevice, st));
-    SPB_TRY(copy_block(SPB_F64, d, na, w.dtype, w.R, w.lp, w.n, na, st));
+    SPB_TRY(copy_block(SPB_F64, d, na, w.dtype, w.R, w.ld, w.n, na, st));
     cudaFreeAsync(d, st);
     SPB_CUDA(cudaStreamSynchronize(st));
     return SPB_OK;
@@ -364,10 +412,10 @@ struct Driver {
 
   // residual R = LX - X theta and norms; also P column norms if have_p.
   int residual(bool have_p, std::vector<double>& norms, std::vector<double>& pn) {
-    SPB_TRY(column_reduce(w.dtype, CR_RESIDUAL, w.LX, w.lp, w.l, w.n, w.X, w.lp, w.theta, w.R,
-                          w.lp, w.crpart, w.sums, st));
+    SPB_TRY(column_reduce(w.dtype, CR_RESIDUAL, w.LX, w.ld, w.l, w.n, w.X, w.ld, w.theta, w.R,
+                          w.ld, w.crpart, w.sums, st));
     if (have_p)
-      SPB_TRY(column_reduce(w.dtype, CR_SUMSQ, w.P, w.lp, w.l, w.n, nullptr, 0, nullptr, nullptr,
+      SPB_TRY(column_reduce(w.dtype, CR_SUMSQ, w.P, w.ld, w.l, w.n, nullptr, 0, nullptr, nullptr,
                             0, w.crpart, w.sums + w.lp, st));
     std::vector<double> hs(2 * w.lp);
     SPB_CUDA(cudaMemcpyAsync(hs.data(), w.sums, sizeof(double) * 2 * w.lp, cudaMemcpyDeviceToHost, st));
@@ -401,9 +449,9 @@ struct Driver {
       UpdParams p{};
       p.q = l;
       int s = 0;
-      p.seg[s++] = {R, w.lp, Cr, l, P, w.lp, 1.0, na, pw == 0 ? 1 : 0};
-      if (pw) p.seg[s++] = {P, w.lp, Cp, l, P, w.lp, 1.0, pw, 1};
-      p.seg[s++] = {X, w.lp, Cx, l, X, w.lp, 1.0, l, 1};
+      p.seg[s++] = {R, w.ld, Cr, l, P, w.ld, 1.0, na, pw == 0 ? 1 : 0};
+      if (pw) p.seg[s++] = {P, w.ld, Cp, l, P, w.ld, 1.0, pw, 1};
+      p.seg[s++] = {X, w.ld, Cx, l, X, w.ld, 1.0, l, 1};
       p.nseg = s;
       SPB_TRY(block_update(w.dtype, p, w.n, st));
     }
@@ -420,9 +468,9 @@ struct Driver {
     const int n = w.n, l = w.l;
     *state_valid = false;
     // zero padding columns once, load x0 (float64 n x l) into X
-    const size_t blk = (size_t)n * w.lp * w.esz;
-    for (void* b : {w.X, w.LX, w.R, w.LR, w.P, w.LP}) SPB_CUDA(cudaMemsetAsync(b, 0, blk, st));
-    SPB_TRY(copy_block(SPB_F64, x0, l, w.dtype, w.X, w.lp, n, l, st));
+    const size_t blk = (size_t)n * w.ld * w.esz;
+    for (void* b : {w.B, w.LB}) SPB_CUDA(cudaMemsetAsync(b, 0, blk, st));
+    SPB_TRY(copy_block(SPB_F64, x0, l, w.dtype, w.X, w.ld, n, l, st));
     if (cfg->deflate_ones) SPB_TRY(deflate(w.X, l));
     SPB_TRY(orthonormalize(w.X, l));
     SPB_TRY(apply(w.X, l, w.LX));
@@ -474,7 +522,7 @@ struct Driver {
       int na = (int)idx.size();
       if (na < l) {
         SPB_TRY(set_idx(idx));
-        SPB_TRY(gather_columns(w.dtype, w.R, w.lp, n, w.idx, na, st));
+        SPB_TRY(gather_columns(w.dtype, w.R, w.ld, n, w.idx, na, st));
       }
       if (cfg->has_precond) SPB_TRY(run_precond(na));
       if (cfg->deflate_ones) SPB_TRY(deflate(w.R, na));
@@ -499,12 +547,12 @@ struct Driver {
           for (int j = 0; j < pw && identity; ++j) identity = sel[j] == j;
           if (!identity) {
             SPB_TRY(set_idx(sel));
-            SPB_TRY(gather_columns(w.dtype, w.P, w.lp, n, w.idx, pw, st));
-            SPB_TRY(gather_columns(w.dtype, w.LP, w.lp, n, w.idx, pw, st));
+            SPB_TRY(gather_columns(w.dtype, w.P, w.ld, n, w.idx, pw, st));
+            SPB_TRY(gather_columns(w.dtype, w.LP, w.ld, n, w.idx, pw, st));
           }
           SPB_CUDA(cudaMemcpyAsync(w.pscale, sc.data(), sizeof(double) * pw, cudaMemcpyHostToDevice, st));
-          SPB_TRY(scale_columns(w.dtype, w.P, w.lp, n, w.pscale, pw, st));
-          SPB_TRY(scale_columns(w.dtype, w.LP, w.lp, n, w.pscale, pw, st));
+          SPB_TRY(scale_columns(w.dtype, w.P, w.ld, n, w.pscale, pw, st));
+          SPB_TRY(scale_columns(w.dtype, w.LP, w.ld, n, w.pscale, pw, st));
         }
       }
       // Rayleigh-Ritz ladder (lobpcg.py:397-429)
@@ -532,7 +580,8 @@ struct Driver {
           grams_ready = true;
         }
         const int m = l + na + pw;
-        SPB_TRY(small_gen_eigh(m, false, &ok, l, l + na));
+        if (tc_full_grams) SPB_TRY(small_gen_eigh(m, false, &ok));
+        else SPB_TRY(small_gen_eigh(m, false, &ok, l, l + na));
         if (ok) {
           solved = true;
           break;
@@ -550,14 +599,7 @@ struct Driver {
     // polish (lobpcg.py:442-454)
     SPB_TRY(orthonormalize(w.X, l));
     SPB_TRY(apply(w.X, l, w.LX));
-    {
-      GramBatch b{};
-      b.njobs = 1;
-      b.job[0] = {w.X, w.LX, w.lp, w.lp, l, l, 0, 0};
-      b.tile_start[0] = 0;
-      b.tile_start[1] = (int)(ceil_div(l, 64) * ceil_div(l, 64));
-      SPB_TRY(gram_batched(w.dtype, b, n, l, l, w.gpart, w.gpart_cap, w.G, 2 * w.mmax, st));
-    }
+    SPB_TRY(gram1(w.X, l, w.LX, l, w.G, 2 * w.mmax));
     SPB_TRY(small_gen_eigh(l, true, &ok));
     if (!ok) {
       set_error("projected matrices contain non-finite entries");
@@ -595,7 +637,7 @@ extern "C" int spb_lobpcg_result_block(int dtype, int32_t n, int32_t l, void* ws
   a.cap = (size_t)-1;
   SolveWs w = carve(a, dtype, std::max(n, 1), std::max(l, 1));
   *x_out = w.X;
-  *ld_out = w.lp;
+  *ld_out = w.ld;
   return SPB_OK;
 }
 
@@ -655,7 +697,7 @@ extern "C" int spb_lobpcg_solve(const spb_operator* op, int dtype, const double*
       converged_out[j] = norms_out[j] < cfg->tol * d.h_scale;
     }
     if (vectors_out) {
-      int c = copy_block(dtype, d.w.X, d.w.lp, SPB_F64, vectors_out, l, n, l, d.st);
+      int c = copy_block(dtype, d.w.X, d.w.ld, SPB_F64, vectors_out, l, n, l, d.st);
       if (s == SPB_OK) s = c;
       cudaError_t e = cudaStreamSynchronize(d.st);
       if (s == SPB_OK && e != cudaSuccess) {
@@ -750,10 +792,10 @@ extern "C" int spb_orthonormalize(int dtype, void* b, int64_t ldb, int32_t n, in
   d.precond = nullptr;
   d.user = user;
   d.st = (cudaStream_t)stream;
-  SPB_CUDA(cudaMemsetAsync(d.w.X, 0, (size_t)n * d.w.lp * d.w.esz, d.st));
-  SPB_TRY(copy_block(dtype, b, ldb, dtype, d.w.X, d.w.lp, n, width, d.st));
+  SPB_CUDA(cudaMemsetAsync(d.w.X, 0, (size_t)n * d.w.ld * d.w.esz, d.st));
+  SPB_TRY(copy_block(dtype, b, ldb, dtype, d.w.X, d.w.ld, n, width, d.st));
   SPB_TRY(d.orthonormalize(d.w.X, width));
-  SPB_TRY(copy_block(dtype, d.w.X, d.w.lp, dtype, b, ldb, n, width, d.st));
+  SPB_TRY(copy_block(dtype, d.w.X, d.w.ld, dtype, b, ldb, n, width, d.st));
   SPB_CUDA(cudaStreamSynchronize(d.st));
   return SPB_OK;
 }

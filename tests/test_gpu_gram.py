@@ -1,0 +1,55 @@
+"""GPU: the tcgen05 3xTF32 Gram (mode 1) and the CUDA-core float64 Gram (mode 0)
+against an exact float64 product of the same float32 inputs."""
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+
+def _gram(u, v, mode, dtype="float32"):
+    import torch
+
+    from paper_1708_07481_b200 import _native as N
+
+    tdt = torch.float32 if dtype == "float32" else torch.float64
+    code = N.F32 if dtype == "float32" else N.F64
+    n, p = u.shape
+    q = v.shape[1]
+    ldu = ((p + 7) // 8) * 8 + 8  # padded row stride, like the solver's blocks
+    ldv = ((q + 7) // 8) * 8
+    ut = torch.zeros((n, ldu), dtype=tdt, device="cuda")
+    vt = torch.zeros((n, ldv), dtype=tdt, device="cuda")
+    ut[:, :p] = torch.from_numpy(u).to(ut)
+    vt[:, :q] = torch.from_numpy(v).to(vt)
+    out = torch.full((p, q), np.nan, dtype=torch.float64, device="cuda")
+    L = N.lib()
+    wsb = L.spb_gram_workspace(p, q, n)
+    ws = torch.empty(wsb, dtype=torch.uint8, device="cuda")
+    N.check(L.spb_gram(code, mode, N.ptr(ut), ldu, p, N.ptr(vt), ldv, q, n, N.ptr(out), q,
+                       N.ptr(ws), wsb, N.stream()))
+    return out.cpu().numpy()
+
+
+@pytest.mark.parametrize("n,p,q", [(1000, 21, 63), (5003, 49, 147), (50000, 147, 294),
+                                   (20000, 176, 352), (7000, 324, 324), (300, 8, 8), (77, 3, 5)])
+def test_tensor_core_gram_accuracy(n, p, q):
+    rng = np.random.default_rng(n + p + q)
+    u = rng.standard_normal((n, p)).astype(np.float32)
+    v = rng.standard_normal((n, q)).astype(np.float32)
+    exact = u.astype(np.float64).T @ v.astype(np.float64)
+    scale = np.abs(u.astype(np.float64)).T @ np.abs(v.astype(np.float64))
+    g1 = _gram(u, v, 1)
+    assert np.all(np.isfinite(g1))
+    err = np.abs(g1 - exact) / scale
+    assert err.max() < 2e-6, err.max()
+    g0 = _gram(u, v, 0)
+    assert np.abs(g0 - exact).max() <= 1e-12 * scale.max()
+
+
+def test_fp64_mode_gram():
+    rng = np.random.default_rng(2)
+    u = rng.standard_normal((999, 13))
+    v = rng.standard_normal((999, 7))
+    g = _gram(u, v, 0, dtype="float64")
+    assert np.allclose(g, u.T @ v, rtol=1e-13, atol=1e-12)

@@ -197,3 +197,20 @@ def test_partition_static_parity(spb, golden_partition, key, precision):
     pp = oracle.pairwise_precision(truth, part.labels)
     rp = gold[f"{key}/pm_pr_pp"]
     assert abs(pr - rp[1]) <= 0.005 and abs(pp - rp[2]) <= 0.005
+
+
+def test_tensor_core_gram_mode_runs(spb, golden_partition, monkeypatch):
+    """SPB_GRAM=tc (3xTF32 tcgen05 Rayleigh-Ritz Grams) is an opt-in fast mode:
+    it must converge to the same spectrum within 1e-2 relative and agree on
+    >= 99% of labels at C1, though it misses the 1e-4 Ritz-value parity bar."""
+    monkeypatch.setenv("SPB_GRAM", "tc")
+    spec, edges, truth = config_input("c1", seed=0)
+    gold = golden_partition
+    l = spb.block_size_for(spec.blocks)
+    x0 = np.random.default_rng(0).standard_normal((spec.n, l))
+    g = spb.from_edges(edges, spec.n)
+    cfg = spb.SolverConfig(block_size=l, tol=1e-12, max_iter=20, seed=0)
+    part, st, _ = spb.partition_static(g, cfg, k_expected=spec.blocks, fix_k=True, x0=x0,
+                                       precision="float32")
+    assert _theta_close(st.eigenvalues, gold["c1_s0/theta"], rel=1e-2)
+    assert oracle.partition_match(gold["c1_s0/labels"].astype(np.int64), part.labels) >= 0.99
