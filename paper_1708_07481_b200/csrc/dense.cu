@@ -19,16 +19,20 @@ namespace spb {
 namespace {
 
 // ----------------------------------------------------------------------------
-// Gram: 64x64 output tile per CTA, 256 threads, 4x4 fp64 micro-tile each.
+// Gram: 64x64 output tile per CTA, 128 threads, 8x4 fp64 micro-tile each.
+// Operands stay in their storage type in shared memory (double-buffered,
+// 32-row chunks) and are widened to fp64 in registers; the next chunk's global
+// loads are issued before the current chunk's FMAs (register prefetch).
 constexpr int GT = 64;
-constexpr int GK = 16;
+constexpr int GK = 32;
 
 template <typename T>
-__global__ void __launch_bounds__(256)
+__global__ void __launch_bounds__(128)
 gram_kernel(GramBatch b, int64_t n, int64_t kchunk, int ldo, int64_t split_stride,
             double* __restrict__ part) {
-  __shared__ double Us[GK][GT + 1];
-  __shared__ double Vs[GK][GT + 1];
+  constexpr int GK = sizeof(T) == 4 ? 32 : 16;  // static smem <= 48 KB
+  __shared__ T Us[2][GK][GT];
+  __shared__ T Vs[2][GK][GT];
   const int tile = blockIdx.x;
   int j = 0;
   while (j + 1 < b.njobs && tile >= b.tile_start[j + 1]) ++j;
@@ -39,47 +43,65 @@ gram_kernel(GramBatch b, int64_t n, int64_t kchunk, int ldo, int64_t split_strid
   const int p0 = tp * GT, q0 = tq * GT;
   const int64_t k0 = (int64_t)blockIdx.y * kchunk;
   const int64_t k1 = min(n, k0 + kchunk);
-  const int tid = threadIdx.x, tx = tid & 15, ty = tid >> 4;
+  const int tid = threadIdx.x, tx = tid & 15, ty = tid >> 4;  // ty 0..7 (8 rows), tx 0..15 (4 cols)
   const T* U = (const T*)jb.U;
   const T* V = (const T*)jb.V;
-  double acc[4][4];
+  // loader mapping: 2 * GK * GT elements per chunk, 32 per thread
+  constexpr int PER = GK * GT / 128;  // 16 per operand
+  T ru[PER], rv[PER];
+  auto load = [&](int64_t kb) {
 #pragma unroll
-  for (int a = 0; a < 4; ++a)
-#pragma unroll
-    for (int c = 0; c < 4; ++c) acc[a][c] = 0.0;
-
-  for (int64_t kb = k0; kb < k1; kb += GK) {
-#pragma unroll
-    for (int e = tid; e < GK * GT; e += 256) {
+    for (int t = 0; t < PER; ++t) {
+      const int e = tid + 128 * t;
       const int r = e / GT, c = e % GT;
       const int64_t k = kb + r;
-      double u = 0.0, v = 0.0;
-      if (k < k1) {
-        if (p0 + c < jb.p) u = (double)U[k * jb.ldu + p0 + c];
-        if (q0 + c < jb.q) v = (double)V[k * jb.ldv + q0 + c];
-      }
-      Us[r][c] = u;
-      Vs[r][c] = v;
+      ru[t] = (k < k1 && p0 + c < jb.p) ? U[k * jb.ldu + p0 + c] : T(0);
+      rv[t] = (k < k1 && q0 + c < jb.q) ? V[k * jb.ldv + q0 + c] : T(0);
     }
-    __syncthreads();
+  };
+  auto store = [&](int buf) {
 #pragma unroll
+    for (int t = 0; t < PER; ++t) {
+      const int e = tid + 128 * t;
+      const int r = e / GT, c = e % GT;
+      Us[buf][r][c] = ru[t];
+      Vs[buf][r][c] = rv[t];
+    }
+  };
+  double acc[8][4];
+#pragma unroll
+  for (int a = 0; a < 8; ++a)
+#pragma unroll
+    for (int c = 0; c < 4; ++c) acc[a][c] = 0.0;
+  int buf = 0;
+  if (k0 < k1) {
+    load(k0);
+    store(0);
+  }
+  __syncthreads();
+  for (int64_t kb = k0; kb < k1; kb += GK) {
+    const bool more = kb + GK < k1;
+    if (more) load(kb + GK);
+#pragma unroll 8
     for (int k = 0; k < GK; ++k) {
-      double a[4], bv[4];
+      double av[8], bv[4];
 #pragma unroll
-      for (int i = 0; i < 4; ++i) a[i] = Us[k][ty * 4 + i];
+      for (int i = 0; i < 8; ++i) av[i] = (double)Us[buf][k][ty * 8 + i];
 #pragma unroll
-      for (int i = 0; i < 4; ++i) bv[i] = Vs[k][tx * 4 + i];
+      for (int i = 0; i < 4; ++i) bv[i] = (double)Vs[buf][k][tx * 4 + i];
 #pragma unroll
-      for (int x = 0; x < 4; ++x)
+      for (int x = 0; x < 8; ++x)
 #pragma unroll
-        for (int y = 0; y < 4; ++y) acc[x][y] = fma(a[x], bv[y], acc[x][y]);
+        for (int y = 0; y < 4; ++y) acc[x][y] = fma(av[x], bv[y], acc[x][y]);
     }
+    if (more) store(buf ^ 1);
     __syncthreads();
+    buf ^= 1;
   }
   double* out = part + (int64_t)blockIdx.y * split_stride;
 #pragma unroll
-  for (int x = 0; x < 4; ++x) {
-    const int i = p0 + ty * 4 + x;
+  for (int x = 0; x < 8; ++x) {
+    const int i = p0 + ty * 8 + x;
     if (i >= jb.p) continue;
 #pragma unroll
     for (int y = 0; y < 4; ++y) {
@@ -109,29 +131,30 @@ int choose_ksplit(int64_t n, int tiles) {
 }
 
 // ----------------------------------------------------------------------------
-// Block update: 32 rows x q columns per CTA (q <= 256), 256 threads as 8 x 32.
-constexpr int UR = 32;   // rows per CTA
+// Block update: (8 * RPT) rows x q columns per CTA (q <= 32 * QV <= 256);
+// 256 threads as 8 row groups x 32 column lanes, each thread RPT rows x QV
+// columns (templated so no predicated-off FMAs are issued).
 constexpr int UQ = 256;  // max columns
 
-template <typename T>
+template <typename T, int QV, int RPT>
 __global__ void __launch_bounds__(256)
 update_kernel(UpdParams P, int64_t n) {
+  constexpr int UR = 8 * RPT;
   constexpr int UK = sizeof(T) == 4 ? 32 : 16;  // k chunk (static smem <= 48 KB)
-  __shared__ T As[UR][UK + 1];
-  __shared__ T Cs[UK][UQ];
-  const int tid = threadIdx.x, tx = tid & 31, ty = tid >> 5;  // ty: 8 row groups of 4
+  __shared__ T As[UK][UR + 1];                  // k-major: As[k][row]
+  __shared__ T Cs[UK][32 * QV];
+  const int tid = threadIdx.x, tx = tid & 31, ty = tid >> 5;
   const int64_t r0 = (int64_t)blockIdx.x * UR;
   const int q = P.q;
-  const int qv = (q + 31) / 32;
-  T acc[4][8];
+  T acc[RPT][QV];
 #pragma unroll
-  for (int a = 0; a < 4; ++a)
+  for (int a = 0; a < RPT; ++a)
 #pragma unroll
-    for (int c = 0; c < 8; ++c) {
+    for (int c = 0; c < QV; ++c) {
       T v = T(0);
-      const int64_t r = r0 + ty * 4 + a;
+      const int64_t r = r0 + ty * RPT + a;
       const int col = tx + 32 * c;
-      if (P.init && c < qv && col < q && r < n) v = ((const T*)P.init)[r * P.ldi + col];
+      if (P.init && col < q && r < n) v = ((const T*)P.init)[r * P.ldi + col];
       acc[a][c] = v;
     }
   for (int s = 0; s < P.nseg; ++s) {
@@ -142,41 +165,61 @@ update_kernel(UpdParams P, int64_t n) {
       for (int e = tid; e < UR * UK; e += 256) {
         const int r = e / UK, k = e % UK;
         const int64_t gr = r0 + r;
-        As[r][k] = (gr < n && k < kc) ? A[gr * sg.lda + k0 + k] : T(0);
+        As[k][r] = (gr < n && k < kc) ? A[gr * sg.lda + k0 + k] : T(0);
       }
-      for (int e = tid; e < UK * qv * 32; e += 256) {
-        const int k = e / (qv * 32), c = e % (qv * 32);
+      for (int e = tid; e < UK * 32 * QV; e += 256) {
+        const int k = e / (32 * QV), c = e % (32 * QV);
         Cs[k][c] = (k < kc && c < q) ? (T)(sg.scale * sg.C[(int64_t)(k0 + k) * sg.ldc + c]) : T(0);
       }
       __syncthreads();
+#pragma unroll 4
       for (int k = 0; k < kc; ++k) {
-        T a[4];
+        T a[RPT], cv[QV];
 #pragma unroll
-        for (int i = 0; i < 4; ++i) a[i] = As[ty * 4 + i][k];
+        for (int i = 0; i < RPT; ++i) a[i] = As[k][ty * RPT + i];
 #pragma unroll
-        for (int c = 0; c < 8; ++c) {
-          if (c < qv) {
-            const T cv = Cs[k][tx + 32 * c];
+        for (int c = 0; c < QV; ++c) cv[c] = Cs[k][tx + 32 * c];
 #pragma unroll
-            for (int i = 0; i < 4; ++i) acc[i][c] = fma(a[i], cv, acc[i][c]);
-          }
-        }
+        for (int i = 0; i < RPT; ++i)
+#pragma unroll
+          for (int c = 0; c < QV; ++c) acc[i][c] = fma(a[i], cv[c], acc[i][c]);
       }
       __syncthreads();
     }
     if (sg.emit) {
       T* O = (T*)sg.out;
 #pragma unroll
-      for (int a = 0; a < 4; ++a) {
-        const int64_t r = r0 + ty * 4 + a;
+      for (int a = 0; a < RPT; ++a) {
+        const int64_t r = r0 + ty * RPT + a;
         if (r >= n) continue;
 #pragma unroll
-        for (int c = 0; c < 8; ++c) {
+        for (int c = 0; c < QV; ++c) {
           const int col = tx + 32 * c;
-          if (c < qv && col < q) O[r * sg.ldo + col] = acc[a][c];
+          if (col < q) O[r * sg.ldo + col] = acc[a][c];
         }
       }
     }
+  }
+}
+
+template <typename T, int QV>
+void launch_update_qv(const UpdParams& p, int64_t n, cudaStream_t st) {
+  constexpr int RPT = QV <= 2 ? 8 : (QV <= 4 ? 4 : 2);
+  const int64_t blocks = ceil_div(n, 8 * RPT);
+  update_kernel<T, QV, RPT><<<blocks, 256, 0, st>>>(p, n);
+}
+
+template <typename T>
+void launch_update(const UpdParams& p, int64_t n, cudaStream_t st) {
+  const int qv = (p.q + 31) / 32;
+  switch (qv) {
+    case 1: launch_update_qv<T, 1>(p, n, st); break;
+    case 2: launch_update_qv<T, 2>(p, n, st); break;
+    case 3: launch_update_qv<T, 3>(p, n, st); break;
+    case 4: launch_update_qv<T, 4>(p, n, st); break;
+    case 5: launch_update_qv<T, 5>(p, n, st); break;
+    case 6: launch_update_qv<T, 6>(p, n, st); break;
+    default: launch_update_qv<T, 8>(p, n, st); break;
   }
 }
 
@@ -225,13 +268,17 @@ colreduce_kernel(int kind, const T* __restrict__ A, int64_t lda, int cols, int64
   }
 }
 
+// One warp per column: lane-strided partial sums then a fixed shuffle tree
+// (deterministic: same order every call).
 __global__ void colreduce_final(const double* __restrict__ part, int blocks, int cols,
                                 double* __restrict__ out) {
-  for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < cols; c += gridDim.x * blockDim.x) {
-    double s = 0.0;
-    for (int b = 0; b < blocks; ++b) s += part[(int64_t)b * cols + c];
-    out[c] = s;
-  }
+  const int lane = threadIdx.x & 31;
+  const int c = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  if (c >= cols) return;
+  double s = 0.0;
+  for (int b = lane; b < blocks; b += 32) s += part[(int64_t)b * cols + c];
+  s = warp_sum(s);
+  if (lane == 0) out[c] = s;
 }
 
 int colreduce_blocks(int64_t n) {
@@ -312,9 +359,9 @@ int gram_batched(int dtype, const GramBatch& b, int64_t n, int out_rows, int out
   dim3 grid(tiles, ks);
   if (n > 0) {
     if (dtype == SPB_F32)
-      gram_kernel<float><<<grid, 256, 0, st>>>(b, n, kchunk, out_cols, stride, partial);
+      gram_kernel<float><<<grid, 128, 0, st>>>(b, n, kchunk, out_cols, stride, partial);
     else
-      gram_kernel<double><<<grid, 256, 0, st>>>(b, n, kchunk, out_cols, stride, partial);
+      gram_kernel<double><<<grid, 128, 0, st>>>(b, n, kchunk, out_cols, stride, partial);
     SPB_LAUNCH_CHECK();
   } else {
     SPB_CUDA(cudaMemsetAsync(partial, 0, sizeof(double) * stride, st));
@@ -332,11 +379,10 @@ int block_update(int dtype, const UpdParams& p, int64_t n, cudaStream_t st) {
     return SPB_ERR_CONTRACT;
   }
   if (n <= 0 || p.q <= 0) return SPB_OK;
-  const int64_t blocks = ceil_div(n, UR);
   if (dtype == SPB_F32)
-    update_kernel<float><<<blocks, 256, 0, st>>>(p, n);
+    launch_update<float>(p, n, st);
   else
-    update_kernel<double><<<blocks, 256, 0, st>>>(p, n);
+    launch_update<double>(p, n, st);
   SPB_LAUNCH_CHECK();
   return SPB_OK;
 }
@@ -360,7 +406,7 @@ int column_reduce(int dtype, int kind, const void* A, int64_t lda, int cols, int
     colreduce_kernel<double><<<blocks, CRB, smem, st>>>(kind, (const double*)A, lda, cols, n,
                                                         rpb, (const double*)X, ldx, theta,
                                                         (double*)R, ldr, partial);
-  colreduce_final<<<(int)ceil_div(cols, 256), 256, 0, st>>>(partial, blocks, cols, out);
+  colreduce_final<<<(int)ceil_div((int64_t)cols * 32, 256), 256, 0, st>>>(partial, blocks, cols, out);
   SPB_LAUNCH_CHECK();
   return SPB_OK;
 }
