@@ -32,4 +32,5 @@ from .spectral_ref import (  # noqa: F401
     qrcp_assign_ref,
     partition_static_ref,
 )
+from .streaming_ref import partition_stream_ref, warm_start_ref  # noqa: F401
 from .metrics_ref import contingency_counts, partition_match, pairwise_recall, pairwise_precision  # noqa: F401

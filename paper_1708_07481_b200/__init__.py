@@ -61,3 +61,11 @@ from .metrics import (  # noqa: F401,E402
     partition_match,
     stage_record,
 )
+from .streaming import (  # noqa: F401,E402
+    StageResult,
+    StreamStage,
+    load_manifest,
+    partition_stream,
+    warm_start,
+    write_manifest,
+)

@@ -185,10 +185,40 @@ def qrcp_fixture():
     np.savez_compressed(HERE / "qrcp.npz", **out)
 
 
+def stream_fixture():
+    """partition_stream of the reference on small DC-SBM streams (emerging, snowball)."""
+    from specpart import streaming as rstr
+    from paper_1708_07481_b200.dcsbm import DcsbmSpec, emerging_slices, snowball_slices
+
+    out = {}
+    spec = DcsbmSpec(n=1500, blocks=6, arcs=30_000, alpha=3.0, ratio=8.0, seed=11)
+    edges, truth = generate_dcsbm(spec)
+    k = spec.blocks
+    streams = {
+        "emerging": [(d, spec.n) for d in emerging_slices(edges, 5, seed=11)],
+        "snowball": snowball_slices(edges, spec.n, 5, seed=11)[1],
+    }
+    for mode, st in streams.items():
+        stages = [rstr.StreamStage(index=i + 1, mode=mode, edge_delta=d, n_after=n)
+                  for i, (d, n) in enumerate(st)]
+        for init in ("warm", "random"):
+            cfg = rl.SolverConfig(block_size=8, tol=1e-4, max_iter=200, seed=11)
+            res = rstr.partition_stream(rg.empty_graph(0), stages, cfg, init_mode=init,
+                                        k_expected=k, fix_k=True)
+            key = f"{mode}_{init}"
+            out[f"{key}/iterations"] = np.array([r.iterations for r in res])
+            for i, r in enumerate(res):
+                out[f"{key}/theta{i}"] = r.eigenstate.eigenvalues
+                out[f"{key}/labels{i}"] = r.partition.labels.astype(np.int16)
+            print(key, [r.iterations for r in res], flush=True)
+    np.savez_compressed(HERE / "stream.npz", **out)
+
+
 def main():
     assert specpart.__version__ == "0.1.0"
     graph_fixture()
     solve_fixture()
+    stream_fixture()
     qrcp_fixture()
     out = {}
     out.update(partition_fixture("c1", seeds=[0, 1], max_iter=20))

@@ -103,3 +103,28 @@ def test_partition_static_matches_reference(golden_partition, key):
     assert np.array_equal(labels, g[f"{key}/labels"].astype(np.int64))
     pm = oracle.partition_match(truth, labels)
     assert abs(pm - g[f"{key}/pm_pr_pp"][0]) < 1e-12
+
+
+def _stream_stages(mode):
+    from paper_1708_07481_b200.dcsbm import DcsbmSpec, emerging_slices, generate_dcsbm, snowball_slices
+
+    spec = DcsbmSpec(n=1500, blocks=6, arcs=30_000, alpha=3.0, ratio=8.0, seed=11)
+    edges, _ = generate_dcsbm(spec)
+    if mode == "emerging":
+        return spec, [(d, spec.n) for d in emerging_slices(edges, 5, seed=11)]
+    return spec, snowball_slices(edges, spec.n, 5, seed=11)[1]
+
+
+@pytest.mark.parametrize("key", ["emerging_warm", "emerging_random", "snowball_warm", "snowball_random"])
+def test_stream_matches_reference(key):
+    from tests.conftest import load_golden
+
+    g = load_golden("stream")
+    mode, init = key.split("_")
+    spec, stages = _stream_stages(mode)
+    res = oracle.partition_stream_ref(stages, SolverCfg(block_size=8, tol=1e-4, max_iter=200, seed=11),
+                                      init_mode=init, k_expected=spec.blocks, fix_k=True)
+    assert [r["iterations"] for r in res] == g[f"{key}/iterations"].tolist()
+    for i, r in enumerate(res):
+        assert np.allclose(r["theta"], g[f"{key}/theta{i}"], rtol=1e-7, atol=1e-7)
+        assert oracle.partition_match(g[f"{key}/labels{i}"].astype(np.int64), r["labels"]) >= 0.999
