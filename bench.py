@@ -197,6 +197,17 @@ def count_launches(step_fn):
     return ours, total
 
 
+def ten_x_tol(spb, g, x0, l, k, precision):
+    """SURVEY §8(d) stop rule for C3/C4: T = 0.1 r0 / scale from the it=0 callback."""
+    seen = {}
+    op = spb.LaplacianOperator(g)
+    spb.lobpcg_solve(op, x0, spb.SolverConfig(block_size=l, tol=1e-12, max_iter=1, seed=0),
+                     n_converge=min(k + 1, l), precision=precision,
+                     callback=lambda it, t, r: seen.setdefault(it, (t, r)))
+    t0, r0 = seen[0]
+    return 0.1 * float(np.max(r0[: k + 1])) / max(abs(float(t0[l - 1])), op.scale_hint)
+
+
 def run_ours(args):
     import torch
 
@@ -218,12 +229,29 @@ def run_ours(args):
     src = torch.from_numpy(np.ascontiguousarray(edges[:, 0])).to(dev)
     dst = torch.from_numpy(np.ascontiguousarray(edges[:, 1])).to(dev)
     x0_d = torch.from_numpy(x0).to(dev)
-    cfg = spb.SolverConfig(block_size=l, tol=1e-12, max_iter=max_iter, seed=0)
+    tol = 1e-12
+    if args.config in ("c3", "c4"):
+        tol = ten_x_tol(spb, spb.from_edges((src, dst), spec.n), x0_d, l, k, args.precision)
+    cfg = spb.SolverConfig(block_size=l, tol=tol, max_iter=max_iter, seed=0)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
     stats = []
+    # C1/C2: one partition per GPU (replicas, weak scaling); C3/C4: one partition
+    # row-sharded across the GPUs (NCCL all-gather + float64 all-reduce), strong scaling
+    sharded = world > 1 and args.config in ("c3", "c4")
+    comm = None
+    if sharded:
+        from paper_1708_07481_b200.sharded import RowShardedLaplacian, _Comm, partition_static_sharded
+
+        comm = _Comm()
 
     def step_device():
         g = spb.from_edges((src, dst), spec.n)
+        if sharded:
+            op = RowShardedLaplacian(g, comm=comm)
+            part_, st, gap = partition_static_sharded(g, cfg, k, fix_k=True, x0=x0_d,
+                                                      precision=args.precision, op=op)
+            stats.append(dict(st.solve_stats, spmm_us=0, spmm_bytes=0))
+            return part_, st
         labels, kf, st, gap = partition_device(g, cfg, k, fix_k=True, x0=x0_d,
                                                precision=args.precision)
         stats.append(st.solve_stats)
@@ -254,7 +282,7 @@ def run_ours(args):
         t = torch.tensor([t_ms], dtype=torch.float64, device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         t_ms = float(t.item())
-    iters_total = sum(s["iterations"] for s in stats) * world
+    iters_total = sum(s["iterations"] for s in stats) * (1 if sharded else world)
     value = iters_total / (t_ms / 1e3)
     # roofline of the dominant kernel (SpMM), timed live with CUDA events
     spmm_us = sum(s["spmm_us"] for s in stats)
@@ -274,18 +302,25 @@ def run_ours(args):
         torch.cuda.synchronize()
         t0 = time.perf_counter()
         g = spb.from_edges(edges_pinned, spec.n)
-        part, st, gap = spb.partition_static(g, cfg, k, fix_k=True, x0=x0, precision=args.precision)
+        if sharded:
+            part, st, gap = partition_static_sharded(g, cfg, k, fix_k=True, x0=x0,
+                                                     precision=args.precision,
+                                                     op=RowShardedLaplacian(g, comm=comm))
+        else:
+            part, st, gap = spb.partition_static(g, cfg, k, fix_k=True, x0=x0,
+                                                 precision=args.precision)
         torch.cuda.synchronize()
         e2e_times.append(time.perf_counter() - t0)
-    e2e_value = max_iter * args.steps / sum(e2e_times)
+    e2e_iters = st.iterations * args.steps
+    e2e_value = e2e_iters / sum(e2e_times)
     if dist is not None:
         t = torch.tensor([sum(e2e_times)], dtype=torch.float64, device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        e2e_value = max_iter * args.steps * world / float(t.item())
-    launches_per_step, _ = count_launches(step_device)
+        e2e_value = e2e_iters * (1 if sharded else world) / float(t.item())
+    launches_per_step = count_launches(step_device)[0] if not sharded else None
     out = None
     if rank == 0:
-        pm = spb.partition_match(spb.contingency(truth, part))
+        pm = spb.partition_match(spb.contingency(truth, part.labels if hasattr(part, "labels") else part))
         cpu = None
         if world == 1 and not args.no_cpu_baseline:
             rate, tot, it, cores = cpu_baseline(edges, spec.n, k, l, x0, args.cpu_iters)
@@ -296,14 +331,15 @@ def run_ours(args):
         out = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": t_ms / args.steps, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None,
+            "scaling": "strong" if sharded else "weak", "vs_baseline": None,
             "dtype": "f32" if args.precision == "float32" else "f64", "data": "synthetic",
             "config": {"workload": f"{args.config}: DC-SBM n={spec.n} B={spec.blocks} "
                                    f"arcs={spec.arcs}, l={l}, {max_iter} LOBPCG iterations, QRCP k={k}",
                        "n": spec.n, "blocks": spec.blocks, "arcs": spec.arcs, "block_size": l,
                        "iterations": max_iter, "precision": args.precision,
                        "l2": "flushed between steps (256 MiB write)",
-                       "parallelism": "replicas" if world > 1 else "single"},
+                       "tol": tol,
+                       "parallelism": ("row-sharded" if sharded else "replicas") if world > 1 else "single"},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": (achieved / peak) if achieved else None, "traffic": traffic,
                          "kernel": "spb::spmm_vec (Laplacian SpMM)", "peak_kind": peak_kind,
@@ -313,7 +349,7 @@ def run_ours(args):
             "e2e": {"value": e2e_value, "unit": UNIT,
                     "h2d_bytes_per_step": int(edges.nbytes + x0.nbytes),
                     "d2h_bytes_per_step": int(4 * spec.n + 16 * l)},
-            "gpu_launches": int(launches_per_step * args.steps),
+            "gpu_launches": int(launches_per_step * args.steps) if launches_per_step is not None else None,
             "clocks": clk.summary(),
             "partition_seconds": t_ms / args.steps / 1e3,
             "e2e_partition_seconds": sum(e2e_times) / args.steps,

@@ -154,6 +154,39 @@ SPB_API int spb_lobpcg_solve(const spb_operator* op, int dtype, const double* x0
                      spb_precond_cb precond, void* user, void* ws, size_t ws_bytes,
                      double* vectors_out, double* theta_out, double* norms_out,
                      uint8_t* converged_out, int64_t* stats_out, void* stream);
+/* ---------------- (e) row-sharded solves over NCCL ----------
+ * One process per GPU. spb_comm_unique_id (rank 0) -> broadcast by the caller
+ * -> spb_comm_init on every rank. The local operator holds this rank's rows of
+ * W (row_ptr local, col indices remapped to the gathered layout rank*n_max +
+ * local row, see spb_csr_shard), local degrees and the GLOBAL max degree in
+ * scale_hint. Per operator apply the input block is all-gathered; Gram
+ * partials and column sums are all-reduced in float64; the small problems are
+ * solved redundantly (identical on every rank). x0 / results are local rows. */
+typedef struct {
+  void* comm;         /* spb_comm_init handle (NULL when nranks == 1)          */
+  int32_t nranks;
+  int32_t rank;
+  int64_t n_global;   /* rows of the whole operator                             */
+  int32_t row_begin;  /* first global row owned by this rank                    */
+  int32_t n_max;      /* max rows per rank (gather padding)                     */
+} spb_shard;
+SPB_API int spb_comm_unique_id(void* out, int32_t bytes);
+SPB_API int spb_comm_init(int32_t nranks, int32_t rank, const void* unique_id, void** comm_out);
+SPB_API int spb_comm_destroy(void* comm);
+/* Local CSR of rows [row_begin, row_end) of a global CSR, columns remapped to
+ * rank(col) * n_max + (col - bounds[rank(col)]); bounds: device int32[nranks+1]. */
+SPB_API int spb_csr_shard(const int32_t* row_ptr, const int32_t* col, const double* val,
+                          int32_t row_begin, int32_t row_end, const int32_t* bounds,
+                          int32_t nranks, int32_t n_max, int32_t* out_row_ptr, int32_t* out_col,
+                          double* out_val, void* stream);
+SPB_API size_t spb_lobpcg_workspace_sharded(int dtype, int32_t n_local, int32_t l, int32_t nranks,
+                                            int32_t n_max);
+SPB_API int spb_lobpcg_solve_sharded(const spb_operator* op, const spb_shard* shard, int dtype,
+                                     const double* x0, const spb_solver_config* cfg,
+                                     spb_iter_cb cb, spb_refill_cb refill, void* user, void* ws,
+                                     size_t ws_bytes, double* theta_out, double* norms_out,
+                                     uint8_t* converged_out, int64_t* stats_out, void* stream);
+
 /* Device pointer/ld of the solver's final X block inside ``ws`` (dtype). */
 SPB_API int spb_lobpcg_result_block(int dtype, int32_t n, int32_t l, void* ws, void** x_out,
                             int64_t* ld_out);

@@ -23,8 +23,20 @@ OUT = PKG / "_lib" / "libspb200.so"
 OBJ = ROOT / "build" / "obj"
 
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
+def _nccl_include() -> str:
+    try:
+        import nvidia.nccl as nn  # the NCCL torch loads (venv wheel)
+
+        inc = Path(list(nn.__path__)[0]) / "include"
+        if (inc / "nccl.h").exists():
+            return str(inc)
+    except ImportError:
+        pass
+    return "/usr/include"
+
+
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "--expt-relaxed-constexpr", "-Xcompiler", "-fPIC",
-         "-Xcompiler", "-fvisibility=hidden", "-I", str(ROOT / "include")]
+         "-Xcompiler", "-fvisibility=hidden", "-I", str(ROOT / "include"), "-I", _nccl_include()]
 
 
 def nvcc() -> str:
@@ -56,7 +68,7 @@ def build(force: bool = False, jobs: int | None = None) -> Path:
         objs = list(ex.map(lambda s: _compile(s, force), sources))
     if force or not OUT.exists() or OUT.stat().st_mtime < max(o.stat().st_mtime for o in objs):
         tmp = OUT.with_suffix(".so.tmp")
-        cmd = [nvcc(), *ARCH, "-shared", "-cudart", "static", "-o", str(tmp), *map(str, objs)]
+        cmd = [nvcc(), *ARCH, "-shared", "-cudart", "static", "-o", str(tmp), *map(str, objs), "-ldl"]
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
             raise RuntimeError(f"link failed:\n{r.stderr}")

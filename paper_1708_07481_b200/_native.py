@@ -34,6 +34,11 @@ class Operator(C.Structure):
                 ("deg", vp), ("dense", vp), ("scale_hint", f64)]
 
 
+class Shard(C.Structure):
+    _fields_ = [("comm", vp), ("nranks", i32), ("rank", i32), ("n_global", i64),
+                ("row_begin", i32), ("n_max", i32)]
+
+
 class SolverConfigC(C.Structure):
     _fields_ = [("block_size", i32), ("max_iter", i32), ("tol", f64), ("lock_tol", f64),
                 ("n_converge", i32), ("deflate_ones", i32), ("has_precond", i32),
@@ -63,6 +68,15 @@ _SIGS = {
                                    C.POINTER(f64), C.POINTER(f64), C.POINTER(C.c_uint8),
                                    C.POINTER(i64), vp]),
     "spb_lobpcg_result_block": (C.c_int, [C.c_int, i32, i32, vp, C.POINTER(vp), C.POINTER(i64)]),
+    "spb_comm_unique_id": (C.c_int, [vp, i32]),
+    "spb_comm_init": (C.c_int, [i32, i32, vp, C.POINTER(vp)]),
+    "spb_comm_destroy": (C.c_int, [vp]),
+    "spb_csr_shard": (C.c_int, [vp, vp, vp, i32, i32, vp, i32, i32, vp, vp, vp, vp]),
+    "spb_lobpcg_workspace_sharded": (sz, [C.c_int, i32, i32, i32, i32]),
+    "spb_lobpcg_solve_sharded": (C.c_int, [C.POINTER(Operator), C.POINTER(Shard), C.c_int, vp,
+                                           C.POINTER(SolverConfigC), ITER_CB, REFILL_CB, vp, vp,
+                                           sz, C.POINTER(f64), C.POINTER(f64),
+                                           C.POINTER(C.c_uint8), C.POINTER(i64), vp]),
     "spb_orthonormalize_workspace": (sz, [C.c_int, i32, i32]),
     "spb_orthonormalize": (C.c_int, [C.c_int, vp, i64, i32, i32, REFILL_CB, vp, vp, sz, vp]),
     "spb_sygv_workspace": (sz, [i32]),

@@ -382,3 +382,59 @@ extern "C" int spb_csr_build(const int64_t* src, const int64_t* dst, const doubl
   *nnz_out = nnz;
   return SPB_OK;
 }
+
+// ---------------------------------------------------------------------------
+// Row shard of a CSR for the multi-GPU solve: rows [r0, r1), columns remapped to
+// the all-gathered layout (rank * n_max + local row of the owning rank).
+namespace spb {
+namespace {
+
+__global__ void shard_rows(const int32_t* __restrict__ rp, int32_t r0, int32_t r1,
+                           int32_t* __restrict__ orp) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i <= (int64_t)(r1 - r0);
+       i += (int64_t)gridDim.x * blockDim.x)
+    orp[i] = rp[r0 + i] - rp[r0];
+}
+
+__global__ void shard_cols(const int32_t* __restrict__ col, const double* __restrict__ val,
+                           int64_t e0, int64_t count, const int32_t* __restrict__ bounds,
+                           int32_t nranks, int32_t n_max, int32_t* __restrict__ ocol,
+                           double* __restrict__ oval) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < count;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int32_t c = col[e0 + e];
+    int lo = 0, hi = nranks;  // owner: bounds[lo] <= c < bounds[lo + 1]
+    while (hi - lo > 1) {
+      const int mid = (lo + hi) >> 1;
+      if (bounds[mid] <= c) lo = mid; else hi = mid;
+    }
+    ocol[e] = lo * n_max + (c - bounds[lo]);
+    oval[e] = val[e0 + e];
+  }
+}
+
+}  // namespace
+}  // namespace spb
+
+extern "C" int spb_csr_shard(const int32_t* row_ptr, const int32_t* col, const double* val,
+                             int32_t row_begin, int32_t row_end, const int32_t* bounds,
+                             int32_t nranks, int32_t n_max, int32_t* out_row_ptr, int32_t* out_col,
+                             double* out_val, void* stream) {
+  cudaStream_t st = (cudaStream_t)stream;
+  if (row_end < row_begin || nranks < 1 || n_max < 0) {
+    set_error("csr shard contract violated");
+    return SPB_ERR_CONTRACT;
+  }
+  int32_t e[2];
+  SPB_CUDA(cudaMemcpyAsync(&e[0], row_ptr + row_begin, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+  SPB_CUDA(cudaMemcpyAsync(&e[1], row_ptr + row_end, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+  SPB_CUDA(cudaStreamSynchronize(st));
+  shard_rows<<<grid_for(row_end - row_begin + 1), 256, 0, st>>>(row_ptr, row_begin, row_end,
+                                                                 out_row_ptr);
+  const int64_t count = (int64_t)e[1] - e[0];
+  if (count > 0)
+    shard_cols<<<grid_for(count), 256, 0, st>>>(col, val, e[0], count, bounds, nranks, n_max,
+                                                 out_col, out_val);
+  SPB_LAUNCH_CHECK();
+  return SPB_OK;
+}

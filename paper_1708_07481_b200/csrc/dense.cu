@@ -322,13 +322,13 @@ __global__ void scale_cols_kernel(T* __restrict__ A, int64_t lda, int64_t n,
 
 template <typename T>
 __global__ void sub_means_kernel(T* __restrict__ A, int64_t lda, int64_t n, int cols,
-                                 const double* __restrict__ sums) {
+                                 const double* __restrict__ sums, double ndiv) {
   const int64_t total = n * cols;
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
        e += (int64_t)gridDim.x * blockDim.x) {
     const int64_t r = e / cols;
     const int c = (int)(e - r * cols);
-    A[r * lda + c] = (T)((double)A[r * lda + c] - sums[c] / (double)n);
+    A[r * lda + c] = (T)((double)A[r * lda + c] - sums[c] / ndiv);
   }
 }
 
@@ -439,12 +439,13 @@ int scale_columns(int dtype, void* A, int64_t lda, int64_t n, const double* s, i
 }
 
 int subtract_column_means(int dtype, void* A, int64_t lda, int64_t n, int cols,
-                          const double* sums, cudaStream_t st) {
+                          const double* sums, cudaStream_t st, double n_div) {
   if (n <= 0 || cols <= 0) return SPB_OK;
+  const double nd = n_div > 0 ? n_div : (double)n;
   if (dtype == SPB_F32)
-    sub_means_kernel<float><<<grid_1d(n * cols), 256, 0, st>>>((float*)A, lda, n, cols, sums);
+    sub_means_kernel<float><<<grid_1d(n * cols), 256, 0, st>>>((float*)A, lda, n, cols, sums, nd);
   else
-    sub_means_kernel<double><<<grid_1d(n * cols), 256, 0, st>>>((double*)A, lda, n, cols, sums);
+    sub_means_kernel<double><<<grid_1d(n * cols), 256, 0, st>>>((double*)A, lda, n, cols, sums, nd);
   SPB_LAUNCH_CHECK();
   return SPB_OK;
 }

@@ -61,15 +61,18 @@ int gather_columns(int dtype, void* A, int64_t lda, int64_t n, const int* idx, i
                    cudaStream_t st);
 int scale_columns(int dtype, void* A, int64_t lda, int64_t n, const double* s, int count,
                   cudaStream_t st);
+// A[:, :cols] -= sums / n_div (n_div = rows of the whole operator; <= 0 -> n)
 int subtract_column_means(int dtype, void* A, int64_t lda, int64_t n, int cols,
-                          const double* sums, cudaStream_t st);
+                          const double* sums, cudaStream_t st, double n_div = 0.0);
 int dense_apply(const double* Adense, int64_t n, const void* X, int64_t ldx, int cols, void* Y,
                 int64_t ldy, int dtype, double* scratch, cudaStream_t st);
 int copy_block(int sdt, const void* s, int64_t lds, int ddt, void* d, int64_t ldd, int64_t rows,
                int32_t cols, cudaStream_t st);
+// Rows [r0, r1) of W; the row's own X entry is x[(xoff + row) * ldx]; x_rows =
+// rows of x the gathers can touch (L2 panel sizing; 0 -> r1).
 int laplacian_spmm(int dtype, int32_t r0, int32_t r1, const int32_t* rp, const int32_t* ci,
                    const void* cv, const void* deg, const void* x, int64_t ldx, int ncols,
-                   void* y, int64_t ldy, cudaStream_t st);
+                   void* y, int64_t ldy, cudaStream_t st, int64_t xoff = 0, int64_t x_rows = 0);
 
 // tcgen05 3xTF32 Gram (gram_tc.cu): out[p x (q0+q1)] = U' [V0 | V1], float32 operands.
 bool gram_tc_supported();

@@ -20,6 +20,7 @@
 #include <cstdlib>
 #include <vector>
 
+#include "comm.cuh"
 #include "dense.cuh"
 #include "smalleig.cuh"
 
@@ -48,9 +49,10 @@ struct SolveWs {
   double *pscale;     // lp
   int *idx, *perm;
   SmallStatus* status;
+  void *gsend, *grecv;  // row-sharded solves: packed local rows / all-gathered block
 };
 
-SolveWs carve(Arena& a, int dtype, int n, int l) {
+SolveWs carve(Arena& a, int dtype, int n, int l, int nranks = 1, int n_max = 0) {
   SolveWs w;
   w.dtype = dtype;
   w.n = n;
@@ -99,6 +101,11 @@ SolveWs carve(Arena& a, int dtype, int n, int l) {
   w.idx = a.take<int>(w.lp + 8);
   w.perm = a.take<int>(w.lp + 8);
   w.status = a.take<SmallStatus>(1);
+  w.gsend = w.grecv = nullptr;
+  if (n_max > 0) {  // row-sharded solve (any rank count): gather buffers
+    w.gsend = a.take<char>((size_t)n_max * w.lp * w.esz);
+    w.grecv = a.take<char>((size_t)nranks * n_max * w.lp * w.esz);
+  }
   return w;
 }
 
@@ -117,7 +124,13 @@ __global__ void gather_pad_grams(const double* __restrict__ gp, int ldp, int pe,
 
 struct Driver {
   bool tc_full_grams = false;  // last rr_grams computed every block (no upper-only mirror)
+  const spb_shard* sh = nullptr;  // row-sharded solve (null: one GPU owns every row)
+  const Comm* comm = nullptr;
+  int64_t n_glob = 0;             // rows of the whole operator
   const spb_operator* op;
+
+  // sum over ranks of a float64 device buffer (no-op on one GPU)
+  int allreduce(double* p, size_t count) { return comm_allreduce_f64(comm, p, count, st); }
   SolveWs w;
   const spb_solver_config* cfg;
   spb_iter_cb cb;
@@ -151,8 +164,18 @@ struct Driver {
       }
       SPB_CUDA(cudaEventRecord(ev[ev_used], st));
     }
-    SPB_TRY(laplacian_spmm(w.dtype, 0, op->n, op->row_ptr, op->col, op->val, op->deg, src, w.ld,
-                           cols, dst, w.ld, st));
+    if (sh) {
+      // all-gather the input block: local rows packed (ld lp), padded to n_max per rank;
+      // the local CSR's columns index the gathered (rank * n_max + local row) layout
+      SPB_TRY(copy_block(w.dtype, src, w.ld, w.dtype, w.gsend, w.lp, w.n, cols, st));
+      SPB_TRY(comm_allgather_bytes(comm, w.gsend, w.grecv, (size_t)sh->n_max * w.lp * w.esz, st));
+      SPB_TRY(laplacian_spmm(w.dtype, 0, op->n, op->row_ptr, op->col, op->val, op->deg, w.grecv,
+                             w.lp, cols, dst, w.ld, st, (int64_t)sh->rank * sh->n_max,
+                             (int64_t)sh->nranks * sh->n_max));
+    } else {
+      SPB_TRY(laplacian_spmm(w.dtype, 0, op->n, op->row_ptr, op->col, op->val, op->deg, src, w.ld,
+                             cols, dst, w.ld, st));
+    }
     if (profile) {
       SPB_CUDA(cudaEventRecord(ev[ev_used + 1], st));
       ev_used += 2;
@@ -187,7 +210,8 @@ struct Driver {
     b.job[0] = {U, V, w.ld, w.ld, p, q, 0, 0};
     b.tile_start[0] = 0;
     b.tile_start[1] = (int)(ceil_div(p, 64) * ceil_div(q, 64));
-    return gram_batched(w.dtype, b, w.n, p, q, w.gpart, w.gpart_cap, out, ldo, st);
+    SPB_TRY(gram_batched(w.dtype, b, w.n, p, q, w.gpart, w.gpart_cap, out, ldo, st));
+    return allreduce(out, (size_t)(p - 1) * ldo + q);
   }
 
   // [G_A | G_B] for the basis [X (l) | R (na) | P (pw)] and images.
@@ -197,6 +221,7 @@ struct Driver {
       const int pe = pw > 0 ? 2 * w.lp + pw : w.lp + na;
       SPB_TRY(gram_tc((const float*)w.B, w.ld, pe, (const float*)w.B, w.ld, pe,
                       (const float*)w.LB, w.ld, pe, w.n, w.gpart, w.gpart_cap, w.Gpad, 2 * pe, st));
+      SPB_TRY(allreduce(w.Gpad, (size_t)pe * 2 * pe));
       const int m = w.l + na + pw;
       gather_pad_grams<<<(int)std::min<int64_t>(ceil_div((int64_t)m * m, 256), 1024), 256, 0, st>>>(
           w.Gpad, 2 * pe, pe, m, w.l, na, w.lp, w.G, 2 * w.mmax, w.mmax);
@@ -229,8 +254,9 @@ struct Driver {
     b.tile_start[nj] = tiles;
     const int m = w.l + na + pw;
     // output region rows m, columns mmax + m (ld 2 mmax)
-    return gram_batched(w.dtype, b, w.n, m, w.mmax + m, w.gpart, w.gpart_cap, w.G, 2 * w.mmax,
-                        st);
+    SPB_TRY(gram_batched(w.dtype, b, w.n, m, w.mmax + m, w.gpart, w.gpart_cap, w.G, 2 * w.mmax,
+                         st));
+    return allreduce(w.G, (size_t)(m - 1) * 2 * w.mmax + w.mmax + m);
   }
 
   int read_status(SmallStatus* h) {
@@ -283,7 +309,7 @@ struct Driver {
     }
     // rank-revealing branch (pivoted Cholesky == dgeqp3 pivoting on B)
     const double eps_t = w.dtype == SPB_F32 ? 3e-7 * std::sqrt((double)na) : 2e-8;
-    const double rank_tol = std::max(std::max<double>(w.n, na) * kEps64, eps_t);
+    const double rank_tol = std::max(std::max<double>((double)n_glob, na) * kEps64, eps_t);
     SPB_TRY(reset_status());
     SPB_TRY(pivoted_cholqr_enqueue(w.Gs, w.lp, na, rank_tol, w.perm, w.coef, w.chol_ws, w.status,
                                    st));
@@ -308,6 +334,7 @@ struct Driver {
   int column_sumsq(const void* A, int cols, double* out_host) {
     SPB_TRY(column_reduce(w.dtype, CR_SUMSQ, A, w.ld, cols, w.n, nullptr, 0, nullptr, nullptr, 0,
                           w.crpart, w.sums, st));
+    SPB_TRY(allreduce(w.sums, cols));
     SPB_CUDA(cudaMemcpyAsync(out_host, w.sums, sizeof(double) * cols, cudaMemcpyDeviceToHost, st));
     SPB_CUDA(cudaStreamSynchronize(st));
     return SPB_OK;
@@ -316,12 +343,13 @@ struct Driver {
   int deflate(void* A, int cols) {  // A -= column means (lobpcg.py:259-260)
     SPB_TRY(column_reduce(w.dtype, CR_SUM, A, w.ld, cols, w.n, nullptr, 0, nullptr, nullptr, 0,
                           w.crpart, w.sums, st));
-    return subtract_column_means(w.dtype, A, w.ld, w.n, cols, w.sums, st);
+    SPB_TRY(allreduce(w.sums, cols));
+    return subtract_column_means(w.dtype, A, w.ld, w.n, cols, w.sums, st, (double)n_glob);
   }
 
   // orthonormalize (lobpcg.py:195-215) on the first width columns of X.
   int orthonormalize(void* B, int width) {
-    if (width > w.n) {
+    if (width > n_glob) {
       set_error("cannot orthonormalize: more columns than rows");
       return SPB_ERR_DOMAIN;
     }
@@ -348,14 +376,17 @@ struct Driver {
       set_error("rank repair needs the Gaussian refill callback");
       return SPB_ERR_CALLBACK;
     }
-    std::vector<double> h((size_t)w.n * cols);
-    if (refill(user, w.n, cols, h.data()) != 0) {
+    // the Generator draws the global block (identical on every rank); keep our rows
+    std::vector<double> h((size_t)n_glob * cols);
+    if (refill(user, n_glob, cols, h.data()) != 0) {
       set_error("refill callback failed");
       return SPB_ERR_CALLBACK;
     }
+    const int64_t r0 = sh ? sh->row_begin : 0;
     double* d = nullptr;
-    SPB_CUDA(cudaMallocAsync((void**)&d, sizeof(double) * h.size(), st));
-    SPB_CUDA(cudaMemcpyAsync(d, h.data(), sizeof(double) * h.size(), cudaMemcpyHostToDevice, st));
+    SPB_CUDA(cudaMallocAsync((void**)&d, sizeof(double) * (size_t)w.n * cols + 8, st));
+    SPB_CUDA(cudaMemcpyAsync(d, h.data() + r0 * cols, sizeof(double) * (size_t)w.n * cols,
+                             cudaMemcpyHostToDevice, st));
     char* dst = (char*)B + (size_t)c0 * w.esz;
     int s = copy_block(SPB_F64, d, cols, w.dtype, dst, w.ld, w.n, cols, st);
     cudaFreeAsync(d, st);
@@ -417,6 +448,9 @@ struct Driver {
     if (have_p)
       SPB_TRY(column_reduce(w.dtype, CR_SUMSQ, w.P, w.ld, w.l, w.n, nullptr, 0, nullptr, nullptr,
                             0, w.crpart, w.sums + w.lp, st));
+    else
+      SPB_CUDA(cudaMemsetAsync(w.sums + w.lp, 0, sizeof(double) * w.lp, st));
+    SPB_TRY(allreduce(w.sums, 2 * w.lp));
     std::vector<double> hs(2 * w.lp);
     SPB_CUDA(cudaMemcpyAsync(hs.data(), w.sums, sizeof(double) * 2 * w.lp, cudaMemcpyDeviceToHost, st));
     h_theta.resize(w.l);
@@ -641,18 +675,27 @@ extern "C" int spb_lobpcg_result_block(int dtype, int32_t n, int32_t l, void* ws
   return SPB_OK;
 }
 
-extern "C" int spb_lobpcg_solve(const spb_operator* op, int dtype, const double* x0,
-                                const spb_solver_config* cfg, spb_iter_cb cb,
-                                spb_refill_cb refill, spb_precond_cb precond, void* user,
-                                void* ws, size_t ws_bytes, double* vectors_out, double* theta_out,
-                                double* norms_out, uint8_t* converged_out, int64_t* stats_out,
-                                void* stream) {
+static int solve_impl(const spb_operator* op, const spb_shard* sh, int dtype, const double* x0,
+                      const spb_solver_config* cfg, spb_iter_cb cb, spb_refill_cb refill,
+                      spb_precond_cb precond, void* user, void* ws, size_t ws_bytes,
+                      double* vectors_out, double* theta_out, double* norms_out,
+                      uint8_t* converged_out, int64_t* stats_out, void* stream) {
   if (dtype != SPB_F32 && dtype != SPB_F64) {
     set_error("unknown dtype %d", dtype);
     return SPB_ERR_DOMAIN;
   }
   const int n = op->n, l = cfg->block_size;
-  if (l < 1 || l > n) {
+  const int64_t n_glob = sh ? sh->n_global : n;
+  if (sh && (sh->nranks < 1 || sh->rank < 0 || sh->rank >= sh->nranks || n > sh->n_max ||
+             (sh->nranks > 1 && !sh->comm))) {
+    set_error("inconsistent shard descriptor");
+    return SPB_ERR_CONTRACT;
+  }
+  if (sh && sh->nranks > 1 && (precond || op->kind != SPB_OP_LAPLACIAN)) {
+    set_error("row-sharded solves take a Laplacian operator and no preconditioner");
+    return SPB_ERR_CONTRACT;
+  }
+  if (l < 1 || l > n_glob) {
     set_error("block_size %d exceeds operator dimension %d", l, n);
     return SPB_ERR_DOMAIN;
   }
@@ -668,11 +711,14 @@ extern "C" int spb_lobpcg_solve(const spb_operator* op, int dtype, const double*
   a.base = (char*)ws;
   a.cap = ws_bytes;
   Driver d;
-  d.w = carve(a, dtype, n, l);
+  d.w = carve(a, dtype, n, l, sh ? sh->nranks : 1, sh ? sh->n_max : 0);
   if (a.used > ws_bytes) {
     set_error("lobpcg workspace too small (%zu < %zu)", ws_bytes, a.used);
     return SPB_ERR_WORKSPACE;
   }
+  d.sh = sh;
+  d.comm = sh ? (const Comm*)sh->comm : nullptr;
+  d.n_glob = n_glob;
   d.op = op;
   d.cfg = cfg;
   d.cb = cb;
@@ -714,6 +760,33 @@ extern "C" int spb_lobpcg_solve(const spb_operator* op, int dtype, const double*
   if (stats_out)
     for (int i = 0; i < 16; ++i) stats_out[i] = d.stats[i];
   return s;
+}
+
+extern "C" int spb_lobpcg_solve(const spb_operator* op, int dtype, const double* x0,
+                                const spb_solver_config* cfg, spb_iter_cb cb,
+                                spb_refill_cb refill, spb_precond_cb precond, void* user,
+                                void* ws, size_t ws_bytes, double* vectors_out, double* theta_out,
+                                double* norms_out, uint8_t* converged_out, int64_t* stats_out,
+                                void* stream) {
+  return solve_impl(op, nullptr, dtype, x0, cfg, cb, refill, precond, user, ws, ws_bytes,
+                    vectors_out, theta_out, norms_out, converged_out, stats_out, stream);
+}
+
+extern "C" size_t spb_lobpcg_workspace_sharded(int dtype, int32_t n_local, int32_t l,
+                                               int32_t nranks, int32_t n_max) {
+  Arena a;
+  a.dry = true;
+  carve(a, dtype, std::max(n_local, 1), std::max(l, 1), nranks, n_max);
+  return a.used + 4096;
+}
+
+extern "C" int spb_lobpcg_solve_sharded(const spb_operator* op, const spb_shard* shard, int dtype,
+                                        const double* x0, const spb_solver_config* cfg,
+                                        spb_iter_cb cb, spb_refill_cb refill, void* user, void* ws,
+                                        size_t ws_bytes, double* theta_out, double* norms_out,
+                                        uint8_t* converged_out, int64_t* stats_out, void* stream) {
+  return solve_impl(op, shard, dtype, x0, cfg, cb, refill, nullptr, user, ws, ws_bytes, nullptr,
+                    theta_out, norms_out, converged_out, stats_out, stream);
 }
 
 extern "C" size_t spb_sygv_workspace(int32_t m) {

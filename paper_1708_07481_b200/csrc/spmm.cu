@@ -53,7 +53,7 @@ template <typename T, int GS>
 __global__ void __launch_bounds__(256)
 spmm_vec(int32_t r0, int32_t r1, const int32_t* __restrict__ rp, const int32_t* __restrict__ ci,
          const T* __restrict__ cv, const T* __restrict__ deg, const T* __restrict__ x,
-         int64_t ldx, int c0, int ncols, T* __restrict__ y, int64_t ldy) {
+         int64_t ldx, int c0, int ncols, T* __restrict__ y, int64_t ldy, int64_t xoff) {
   using V = typename Vec<T>::type;
   constexpr int VN = Vec<T>::N;
   constexpr int NG = 32 / GS;
@@ -94,7 +94,7 @@ spmm_vec(int32_t r0, int32_t r1, const int32_t* __restrict__ rp, const int32_t* 
 #pragma unroll
     for (int o = GS; o < 32; o <<= 1) vshfl_add(acc, o);
     if (g == 0 && act) {
-      const V xi = *reinterpret_cast<const V*>(x + (int64_t)row * ldx + coff);
+      const V xi = *reinterpret_cast<const V*>(x + (xoff + row) * ldx + coff);
       const T d = deg[row];
       V out = vaxpy_out(d, xi, acc);
       T* yp = y + (int64_t)row * ldy + coff;
@@ -112,7 +112,7 @@ template <typename T>
 __global__ void __launch_bounds__(256)
 spmm_scalar(int32_t r0, int32_t r1, const int32_t* __restrict__ rp, const int32_t* __restrict__ ci,
             const T* __restrict__ cv, const T* __restrict__ deg, const T* __restrict__ x,
-            int64_t ldx, int ncols, T* __restrict__ y, int64_t ldy) {
+            int64_t ldx, int ncols, T* __restrict__ y, int64_t ldy, int64_t xoff) {
   const int lane = threadIdx.x & 31;
   const int32_t row = r0 + (int32_t)((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5);
   if (row >= r1) return;
@@ -131,14 +131,14 @@ spmm_scalar(int32_t r0, int32_t r1, const int32_t* __restrict__ rp, const int32_
         if (c < ncols) acc += w * x[(int64_t)j * ldx + c];
       }
     }
-    if (c < ncols) y[(int64_t)row * ldy + c] = deg[row] * x[(int64_t)row * ldx + c] - acc;
+    if (c < ncols) y[(int64_t)row * ldy + c] = deg[row] * x[(xoff + row) * ldx + c] - acc;
   }
 }
 
 template <typename T>
 int launch_spmm(int32_t r0, int32_t r1, const int32_t* rp, const int32_t* ci, const T* cv,
                 const T* deg, const T* x, int64_t ldx, int ncols, T* y, int64_t ldy,
-                cudaStream_t st) {
+                cudaStream_t st, int64_t xoff, int64_t x_rows) {
   constexpr int VN = Vec<T>::N;
   const int64_t rows = (int64_t)r1 - r0;
   if (rows <= 0 || ncols <= 0) return SPB_OK;
@@ -148,7 +148,7 @@ int launch_spmm(int32_t r0, int32_t r1, const int32_t* rp, const int32_t* ci, co
                        ((uintptr_t)x % (VN * sizeof(T)) == 0) &&
                        ((uintptr_t)y % (VN * sizeof(T)) == 0);
   if (!aligned) {
-    spmm_scalar<T><<<blocks, threads, 0, st>>>(r0, r1, rp, ci, cv, deg, x, ldx, ncols, y, ldy);
+    spmm_scalar<T><<<blocks, threads, 0, st>>>(r0, r1, rp, ci, cv, deg, x, ldx, ncols, y, ldy, xoff);
     SPB_LAUNCH_CHECK();
     return SPB_OK;
   }
@@ -159,7 +159,7 @@ int launch_spmm(int32_t r0, int32_t r1, const int32_t* rp, const int32_t* ci, co
     cudaGetDevice(&dev);
     if (cudaDeviceGetAttribute(&l2, cudaDevAttrL2CacheSize, dev) != cudaSuccess) l2 = 64 << 20;
   }
-  int64_t n_all = (int64_t)r1;  // gathered rows span the whole operator
+  int64_t n_all = x_rows > 0 ? x_rows : (int64_t)r1;  // rows the gathers can touch
   int64_t panel = ((int64_t)l2 / 2) / std::max<int64_t>(1, n_all * (int64_t)sizeof(T));
   panel = std::max<int64_t>(panel / (8 * VN) * (8 * VN), 8 * VN);
   if (panel >= ncols) panel = ncols;
@@ -167,17 +167,17 @@ int launch_spmm(int32_t r0, int32_t r1, const int32_t* rp, const int32_t* ci, co
     const int pc = (int)std::min<int64_t>(panel, ncols - c0);
     const int nvec = (pc + VN - 1) / VN;
     if (nvec <= 1)
-      spmm_vec<T, 1><<<blocks, threads, 0, st>>>(r0, r1, rp, ci, cv, deg, x, ldx, c0, pc, y, ldy);
+      spmm_vec<T, 1><<<blocks, threads, 0, st>>>(r0, r1, rp, ci, cv, deg, x, ldx, c0, pc, y, ldy, xoff);
     else if (nvec <= 2)
-      spmm_vec<T, 2><<<blocks, threads, 0, st>>>(r0, r1, rp, ci, cv, deg, x, ldx, c0, pc, y, ldy);
+      spmm_vec<T, 2><<<blocks, threads, 0, st>>>(r0, r1, rp, ci, cv, deg, x, ldx, c0, pc, y, ldy, xoff);
     else if (nvec <= 4)
-      spmm_vec<T, 4><<<blocks, threads, 0, st>>>(r0, r1, rp, ci, cv, deg, x, ldx, c0, pc, y, ldy);
+      spmm_vec<T, 4><<<blocks, threads, 0, st>>>(r0, r1, rp, ci, cv, deg, x, ldx, c0, pc, y, ldy, xoff);
     else if (nvec <= 8)
-      spmm_vec<T, 8><<<blocks, threads, 0, st>>>(r0, r1, rp, ci, cv, deg, x, ldx, c0, pc, y, ldy);
+      spmm_vec<T, 8><<<blocks, threads, 0, st>>>(r0, r1, rp, ci, cv, deg, x, ldx, c0, pc, y, ldy, xoff);
     else if (nvec <= 16)
-      spmm_vec<T, 16><<<blocks, threads, 0, st>>>(r0, r1, rp, ci, cv, deg, x, ldx, c0, pc, y, ldy);
+      spmm_vec<T, 16><<<blocks, threads, 0, st>>>(r0, r1, rp, ci, cv, deg, x, ldx, c0, pc, y, ldy, xoff);
     else
-      spmm_vec<T, 32><<<blocks, threads, 0, st>>>(r0, r1, rp, ci, cv, deg, x, ldx, c0, pc, y, ldy);
+      spmm_vec<T, 32><<<blocks, threads, 0, st>>>(r0, r1, rp, ci, cv, deg, x, ldx, c0, pc, y, ldy, xoff);
     SPB_LAUNCH_CHECK();
   }
   return SPB_OK;
@@ -187,12 +187,12 @@ int launch_spmm(int32_t r0, int32_t r1, const int32_t* rp, const int32_t* ci, co
 
 int laplacian_spmm(int dtype, int32_t r0, int32_t r1, const int32_t* rp, const int32_t* ci,
                    const void* cv, const void* deg, const void* x, int64_t ldx, int ncols,
-                   void* y, int64_t ldy, cudaStream_t st) {
+                   void* y, int64_t ldy, cudaStream_t st, int64_t xoff, int64_t x_rows) {
   if (dtype == SPB_F32)
     return launch_spmm<float>(r0, r1, rp, ci, (const float*)cv, (const float*)deg,
-                              (const float*)x, ldx, ncols, (float*)y, ldy, st);
+                              (const float*)x, ldx, ncols, (float*)y, ldy, st, xoff, x_rows);
   return launch_spmm<double>(r0, r1, rp, ci, (const double*)cv, (const double*)deg,
-                             (const double*)x, ldx, ncols, (double*)y, ldy, st);
+                             (const double*)x, ldx, ncols, (double*)y, ldy, st, xoff, x_rows);
 }
 
 }  // namespace spb
@@ -210,5 +210,5 @@ extern "C" int spb_laplacian_spmm(int dtype, int32_t row_begin, int32_t row_end,
     return SPB_ERR_CONTRACT;
   }
   return spb::laplacian_spmm(dtype, row_begin, row_end, row_ptr, col, val, deg, x, ldx, ncols, y,
-                             ldy, (cudaStream_t)stream);
+                             ldy, (cudaStream_t)stream, 0, 0);
 }

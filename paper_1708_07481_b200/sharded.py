@@ -1,0 +1,217 @@
+"""Row-sharded multi-GPU solves: one process per GPU, NCCL.
+
+Every rank builds the symmetrised CSR W from the full arc list (the build is
+cheap relative to the solve and needs no collective), keeps its contiguous row
+range (balanced by nnz + rows) with columns remapped to the all-gathered
+layout, and runs the device LOBPCG driver with:
+
+* an all-gather of the operator's input block before every SpMM;
+* float64 all-reduces of the Gram partials and column sums (norms, means);
+* the small projected problems solved redundantly (identical on every rank).
+
+The assignment all-gathers the first k eigenvector columns and runs the QRCP
+kernel on every rank, so every rank returns the same labels.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+
+import numpy as np
+import torch
+
+from . import _native as N
+from .errors import ContractError, DomainError, SolverError, SpecpartError
+from .graph import DTYPES, SparseGraph, _device
+from .lobpcg import EigenState, SolverConfig, _Bridge, default_precision, random_init
+from .spectral import GapResult, Partition, _assign_device, block_size_for, detect_gap
+
+__all__ = ["partition_rows", "RowShardedLaplacian", "lobpcg_solve_sharded", "partition_static_sharded"]
+
+
+def partition_rows(row_ptr: np.ndarray, nranks: int) -> np.ndarray:
+    """Contiguous row ranges balanced by (nnz + rows); returns bounds[nranks + 1]."""
+    row_ptr = np.asarray(row_ptr, dtype=np.int64)
+    n = row_ptr.size - 1
+    if nranks < 1:
+        raise DomainError("nranks must be positive")
+    cost = row_ptr + np.arange(n + 1)
+    targets = cost[-1] * np.arange(1, nranks) / nranks
+    inner = np.searchsorted(cost, targets, side="left")
+    bounds = np.concatenate([[0], inner, [n]]).astype(np.int64)
+    return np.maximum.accumulate(np.clip(bounds, 0, n))
+
+
+class _Comm:
+    """NCCL communicator created from a unique id broadcast over torch.distributed."""
+
+    def __init__(self, group=None):
+        import torch.distributed as dist
+
+        self.nranks = dist.get_world_size(group) if dist.is_initialized() else 1
+        self.rank = dist.get_rank(group) if dist.is_initialized() else 0
+        L = N.lib()
+        uid = (C.c_char * 128)()
+        if self.nranks > 1:
+            if self.rank == 0:
+                N.check(L.spb_comm_unique_id(uid, 128))
+            obj = [bytes(uid) if self.rank == 0 else None]
+            dist.broadcast_object_list(obj, src=0, group=group)
+            C.memmove(uid, obj[0], 128)
+        h = C.c_void_p()
+        N.check(L.spb_comm_init(self.nranks, self.rank, uid, C.byref(h)))
+        self.handle = h
+
+    def __del__(self):
+        try:
+            N.lib().spb_comm_destroy(self.handle)
+        except Exception:  # noqa: BLE001 - interpreter shutdown
+            pass
+
+
+class RowShardedLaplacian:
+    """This rank's rows of L = D - W, in the gathered-column layout."""
+
+    def __init__(self, g: SparseGraph, group=None, comm: _Comm | None = None):
+        self.graph = g
+        self.comm = comm or _Comm(group)
+        self.nranks, self.rank = self.comm.nranks, self.comm.rank
+        row_ptr, col, val, nnz = g.device_csr()
+        self.n = g.n_vertices
+        self.bounds = partition_rows(row_ptr.cpu().numpy(), self.nranks)
+        self.row_begin = int(self.bounds[self.rank])
+        self.row_end = int(self.bounds[self.rank + 1])
+        self.n_local = self.row_end - self.row_begin
+        self.n_max = int(np.diff(self.bounds).max())
+        if self.n_local < 1:
+            raise ContractError("a rank received no rows; use fewer ranks")
+        dev = row_ptr.device
+        b = torch.from_numpy(self.bounds.astype(np.int32)).to(dev)
+        lo_hi = row_ptr[[self.row_begin, self.row_end]].cpu().numpy()
+        lnnz = int(lo_hi[1] - lo_hi[0])
+        self.row_ptr = torch.empty(self.n_local + 1, dtype=torch.int32, device=dev)
+        self.col = torch.empty(max(lnnz, 1), dtype=torch.int32, device=dev)
+        self.val64 = torch.empty(max(lnnz, 1), dtype=torch.float64, device=dev)
+        N.check(N.lib().spb_csr_shard(N.ptr(row_ptr), N.ptr(col), N.ptr(val), self.row_begin,
+                                      self.row_end, N.ptr(b), self.nranks, self.n_max,
+                                      N.ptr(self.row_ptr), N.ptr(self.col), N.ptr(self.val64),
+                                      N.stream()))
+        self.nnz_local = lnnz
+        deg = g.device_degrees()
+        self.deg64 = deg[self.row_begin:self.row_end].contiguous()
+        mx = C.c_double(0.0)
+        N.check(N.lib().spb_max_f64(N.ptr(deg), self.n, C.byref(mx), N.stream()))
+        self.scale_hint = float(mx.value)
+        self._cast = {}
+
+    def _typed(self, dtype):
+        if dtype == "float64":
+            return self.val64, self.deg64
+        if dtype not in self._cast:
+            v = self.val64.to(torch.float32)
+            d = self.deg64.to(torch.float32)
+            self._cast[dtype] = (v, d)
+        return self._cast[dtype]
+
+    def native(self, dtype: str):
+        v, d = self._typed(dtype)
+        op = N.Operator()
+        op.kind = N.OP_LAPLACIAN
+        op.n = self.n_local
+        op.row_ptr = N.ptr(self.row_ptr)
+        op.col = N.ptr(self.col)
+        op.val = N.ptr(v)
+        op.deg = N.ptr(d)
+        op.dense = None
+        op.scale_hint = self.scale_hint
+        sh = N.Shard(comm=self.comm.handle if self.nranks > 1 else None, nranks=self.nranks,
+                     rank=self.rank, n_global=self.n, row_begin=self.row_begin, n_max=self.n_max)
+        op._keep = (v, d)
+        return op, sh
+
+
+def lobpcg_solve_sharded(op: RowShardedLaplacian, x0, config: SolverConfig, n_converge=None,
+                         callback=None, *, precision: str | None = None) -> EigenState:
+    """lobpcg_solve on this rank's rows; x0 is the global (n, l) block (host)."""
+    precision = precision or default_precision()
+    if not isinstance(x0, torch.Tensor):
+        x0 = np.asarray(x0, dtype=np.float64)
+    if x0.ndim != 2 or x0.shape[0] != op.n:
+        raise ContractError(f"x0 must be ({op.n}, block_size)")
+    l = x0.shape[1]
+    if l != config.block_size:
+        raise ContractError(f"x0 has {l} columns but config.block_size is {config.block_size}")
+    nc = l if n_converge is None else int(n_converge)
+    code, tdt = DTYPES[precision]
+    L = N.lib()
+    native, sh = op.native(precision)
+    dev = _device()
+    if isinstance(x0, torch.Tensor):
+        x0_d = x0[op.row_begin:op.row_end].to(device=dev, dtype=torch.float64).contiguous()
+    else:
+        x0_d = torch.from_numpy(np.ascontiguousarray(x0[op.row_begin:op.row_end])).to(dev)
+    wsb = L.spb_lobpcg_workspace_sharded(code, op.n_local, l, op.nranks, op.n_max)
+    ws = torch.empty(wsb, dtype=torch.uint8, device=dev)
+    cfg = N.SolverConfigC(block_size=l, max_iter=config.max_iter, tol=config.tol,
+                          lock_tol=config.lock_tol, n_converge=nc, deflate_ones=int(config.deflate_ones),
+                          has_precond=0, reserved=0)
+    bridge = _Bridge(callback, np.random.default_rng(config.seed), None, l)
+    theta, norms, conv, stats = (C.c_double * l)(), (C.c_double * l)(), (C.c_uint8 * l)(), (C.c_int64 * 16)()
+    status = L.spb_lobpcg_solve_sharded(C.byref(native), C.byref(sh), code, N.ptr(x0_d), C.byref(cfg),
+                                        bridge.it, bridge.refill, None, N.ptr(ws), wsb, theta, norms,
+                                        conv, stats, N.stream())
+    if bridge.exc is not None:
+        raise bridge.exc
+    state = None
+    if status in (N.OK, N.E_SOLVER):
+        xp, ldx = C.c_void_p(), C.c_int64()
+        N.check(L.spb_lobpcg_result_block(code, op.n_local, l, N.ptr(ws), C.byref(xp), C.byref(ldx)))
+        vec = torch.empty((op.n_local, l), dtype=tdt, device=dev)
+        N.check(L.spb_copy_block(code, xp.value, ldx.value, code, N.ptr(vec), l, op.n_local, l, N.stream()))
+        state = EigenState(np.array(theta[:]), vec, np.array(norms[:]), int(stats[0]),
+                           np.array(conv[:], dtype=bool), work_blocks=6)
+        state.solve_stats = dict(iterations=int(stats[0]), spmm_calls=int(stats[1]))
+        state.row_range = (op.row_begin, op.row_end)
+    if status == N.OK:
+        return state
+    msg = (L.spb_last_error() or b"").decode(errors="replace")
+    if status in (N.E_SOLVER, N.E_SOLVER_NOSTATE):
+        raise SolverError(msg, state=state)
+    N.check(status)
+    raise SpecpartError(msg)
+
+
+def _gather_rows(op: RowShardedLaplacian, local: torch.Tensor, group=None) -> torch.Tensor:
+    """All-gather variable-length row blocks (padded to n_max) into the global block."""
+    if op.nranks == 1:
+        return local
+    import torch.distributed as dist
+
+    pad = torch.zeros((op.n_max, local.shape[1]), dtype=local.dtype, device=local.device)
+    pad[: local.shape[0]] = local
+    out = torch.empty((op.nranks * op.n_max, local.shape[1]), dtype=local.dtype, device=local.device)
+    dist.all_gather_into_tensor(out, pad, group=group)
+    parts = [out[r * op.n_max: r * op.n_max + int(op.bounds[r + 1] - op.bounds[r])] for r in range(op.nranks)]
+    return torch.cat(parts).contiguous()
+
+
+def partition_static_sharded(g: SparseGraph, cfg: SolverConfig, k_expected: int | None = None, *,
+                             alpha: float = 3.0, k_min: int = 2, fix_k: bool = False, x0=None,
+                             precision: str | None = None, group=None, op: RowShardedLaplacian | None = None):
+    """partition_static with the rows of the operator split across the ranks of ``group``."""
+    n = g.n_vertices
+    if n < 1:
+        raise DomainError("cannot partition an empty graph")
+    l = block_size_for(k_expected) if k_expected is not None else cfg.block_size
+    l = min(l, n)
+    cfg_run = cfg.replace(block_size=l)
+    start = random_init(n, l, cfg.seed) if x0 is None else x0
+    nc = min(k_expected + 1, l) if k_expected is not None else None
+    op = op or RowShardedLaplacian(g, group)
+    state = lobpcg_solve_sharded(op, start, cfg_run, n_converge=nc, precision=precision)
+    gap = (detect_gap(state.eigenvalues, k_min=min(k_min, l - 1), alpha=alpha) if l >= 2
+           else GapResult(k=1, increments=np.empty(0), confidence=0.0, reliable=False))
+    k_used = k_expected if (fix_k and k_expected is not None) else gap.k
+    emb = _gather_rows(op, state.device_vectors[:, :k_used].contiguous(), group)
+    labels, _, info = _assign_device(emb, k_used)
+    return Partition(labels.cpu().numpy().astype(np.int64), int(info[0])), state, gap
