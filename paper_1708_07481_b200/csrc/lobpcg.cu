@@ -859,6 +859,7 @@ extern "C" int spb_orthonormalize(int dtype, void* b, int64_t ldb, int32_t n, in
     return SPB_ERR_WORKSPACE;
   }
   d.op = nullptr;
+  d.n_glob = n;
   d.cfg = nullptr;
   d.cb = nullptr;
   d.refill = refill;

@@ -38,20 +38,32 @@ __device__ __forceinline__ bool better(double v, int p, double bv, int bp) {
   return v > bv || (v == bv && p < bp);
 }
 
+// Cooperative pivot kernel: ONE grid barrier per step. Every CTA owns a
+// contiguous range of columns of X' (rows of X) and keeps their partial norms
+// (vn1, vn2) and current positions; after the barrier each CTA reduces the
+// per-CTA maxima (double-buffered by step parity), replays the column swap
+// dgeqp3 performs (perm[j] from a k-entry swap history in shared memory) and
+// forms q_j redundantly (identical arithmetic on every CTA), then downdates its
+// own columns and produces its next local maximum.
 template <typename T>
 __global__ void __launch_bounds__(QT)
 qrcp_pivots(const T* __restrict__ X, int64_t ldx, int n, int k, double* __restrict__ vn1,
-            double* __restrict__ vn2, int* __restrict__ pos, int* __restrict__ perm,
-            double* __restrict__ Q, BestRec* __restrict__ bb, int* __restrict__ piv) {
+            double* __restrict__ vn2, int* __restrict__ pos, int* __restrict__ perm_unused,
+            double* __restrict__ Q_unused, BestRec* __restrict__ bb, int* __restrict__ piv) {
   cg::grid_group grid = cg::this_grid();
-  extern __shared__ double qs[];  // q_0..q_{k-1} (k x k) in shared memory
+  extern __shared__ double qs[];         // q_0..q_{k-1} (k x k), then xp[k], cdot[k]
+  double* xp = qs + (size_t)k * k;       // pivot column (then residual)
+  double* cdot = xp + k;                 // q_t' r
   __shared__ BestRec wb[QT / 32];
+  __shared__ int swap_pp[1024], swap_cj[1024];  // swap history (position pp, column moved)
+  __shared__ int s_p, s_pp, s_cj;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int gw = blockIdx.x * (QT / 32) + warp, nwarps = gridDim.x * (QT / 32);
+  const int per = (n + gridDim.x - 1) / gridDim.x;
+  const int c_lo = blockIdx.x * per, c_hi = min(n, c_lo + per);
   const double tol3z = sqrt(kEps64);
 
-  // initial norms (one warp per column of X' = row of X)
-  for (int c = gw; c < n; c += nwarps) {
+  // initial norms of my columns (warp per column), positions = identity
+  for (int c = c_lo + warp; c < c_hi; c += QT / 32) {
     double s = 0.0;
     for (int t = lane; t < k; t += 32) {
       const double v = (double)X[(int64_t)c * ldx + t];
@@ -62,15 +74,14 @@ qrcp_pivots(const T* __restrict__ X, int64_t ldx, int n, int k, double* __restri
       vn1[c] = sqrt(s);
       vn2[c] = vn1[c];
       pos[c] = c;
-      perm[c] = c;
     }
   }
-  grid.sync();
+  __syncthreads();
   for (int j = 0; j < k; ++j) {
-    // ---- phase A: local argmax over remaining columns
+    // ---- local argmax over my remaining columns (ties: lowest position)
     double bv = -1.0;
     int bp = INT_MAX, bc = -1;
-    for (int c = blockIdx.x * QT + tid; c < n; c += gridDim.x * QT) {
+    for (int c = c_lo + tid; c < c_hi; c += QT) {
       const int p = pos[c];
       if (p < j) continue;
       const double v = vn1[c];
@@ -85,57 +96,64 @@ qrcp_pivots(const T* __restrict__ X, int64_t ldx, int n, int k, double* __restri
     }
     if (lane == 0) wb[warp] = {bv, bp, bc};
     __syncthreads();
+    BestRec* slot = bb + (j & 1) * gridDim.x;
     if (tid == 0) {
       BestRec b = wb[0];
       for (int w = 1; w < QT / 32; ++w)
         if (better(wb[w].val, wb[w].pos, b.val, b.pos)) b = wb[w];
-      bb[blockIdx.x] = b;
+      slot[blockIdx.x] = b;
     }
     grid.sync();
-    // ---- phase B (every CTA redundantly): global pivot, swap, new direction q_j
+    // ---- every CTA: global pivot, swap replay, q_j
     if (tid == 0) {
-      BestRec b = bb[0];
+      BestRec b = slot[0];
       for (int g = 1; g < (int)gridDim.x; ++g)
-        if (better(bb[g].val, bb[g].pos, b.val, b.pos)) b = bb[g];
-      wb[0] = b;
+        if (better(slot[g].val, slot[g].pos, b.val, b.pos)) b = slot[g];
+      // perm[j]: column currently at position j = column moved there by the latest
+      // earlier swap whose pivot came from position j, else j itself
+      int cj = j;
+      for (int t = j - 1; t >= 0; --t)
+        if (swap_pp[t] == j) { cj = swap_cj[t]; break; }
+      s_p = b.col;
+      s_pp = b.pos;
+      s_cj = cj;
+      swap_pp[j] = b.pos;  // column cj moves to the pivot's old position
+      swap_cj[j] = cj;
+      if (blockIdx.x == 0) piv[j] = b.col;
     }
     __syncthreads();
-    const int p = wb[0].col;
-    const int pp = wb[0].pos;
-    // r = x_p - sum_{t<j} (q_t' x_p) q_t, twice (CGS2); warp 0 of each CTA
+    const int p = s_p, pp = s_pp, cj = s_cj;
+    if (p >= c_lo && p < c_hi && tid == 0) { pos[p] = j; vn1[p] = 0.0; }
+    if (cj != p && cj >= c_lo && cj < c_hi && tid == 0) pos[cj] = pp;
+    // q_j = normalize((I - Q Q')^2 x_p): CGS2 with thread-parallel dots and updates
+    for (int t = tid; t < k; t += QT) xp[t] = (double)X[(int64_t)p * ldx + t];
+    __syncthreads();
+    for (int pass = 0; pass < 2; ++pass) {
+      for (int t0 = tid; t0 < j; t0 += QT) {
+        const double* qt = qs + (size_t)t0 * k;
+        double s = 0.0;
+        for (int t = 0; t < k; ++t) s += qt[t] * xp[t];
+        cdot[t0] = s;
+      }
+      __syncthreads();
+      for (int t = tid; t < k; t += QT) {
+        double r = xp[t];
+        for (int t0 = 0; t0 < j; ++t0) r -= cdot[t0] * qs[(size_t)t0 * k + t];
+        xp[t] = r;
+      }
+      __syncthreads();
+    }
     double* qj = qs + (size_t)j * k;
     if (warp == 0) {
-      for (int t = lane; t < k; t += 32) qj[t] = (double)X[(int64_t)p * ldx + t];
-      __syncwarp();
-      for (int pass = 0; pass < 2; ++pass) {
-        for (int t0 = 0; t0 < j; ++t0) {
-          const double* qt = qs + (size_t)t0 * k;
-          double s = 0.0;
-          for (int t = lane; t < k; t += 32) s += qt[t] * qj[t];
-          s = warp_sum(s);
-          for (int t = lane; t < k; t += 32) qj[t] -= s * qt[t];
-          __syncwarp();
-        }
-      }
       double s = 0.0;
-      for (int t = lane; t < k; t += 32) s += qj[t] * qj[t];
+      for (int t = lane; t < k; t += 32) s += xp[t] * xp[t];
       s = warp_sum(s);
       const double inv = s > 0.0 ? 1.0 / sqrt(s) : 0.0;
-      for (int t = lane; t < k; t += 32) qj[t] *= inv;
-    }
-    if (blockIdx.x == 0 && tid == 0) {
-      piv[j] = p;
-      const int cj = perm[j];
-      perm[pp] = cj;
-      pos[cj] = pp;
-      perm[j] = p;
-      pos[p] = j;
-      vn1[p] = 0.0;
+      for (int t = lane; t < k; t += 32) qj[t] = xp[t] * inv;
     }
     __syncthreads();
-    grid.sync();
-    // ---- phase C: downdate partial norms of the remaining columns
-    for (int c = gw; c < n; c += nwarps) {
+    // ---- downdate my remaining columns (dlaqp2: recompute when |q_j'x|/vn1 loses digits)
+    for (int c = c_lo + warp; c < c_hi; c += QT / 32) {
       if (pos[c] <= j) continue;
       const double v1 = vn1[c];
       if (v1 == 0.0) continue;
@@ -145,31 +163,31 @@ qrcp_pivots(const T* __restrict__ X, int64_t ldx, int n, int k, double* __restri
       double temp = fabs(s) / v1;
       temp = fmax(0.0, (1.0 + temp) * (1.0 - temp));
       const double r = v1 / vn2[c];
-      const double temp2 = temp * r * r;
-      if (temp2 <= tol3z) {
-        // recompute || x_c - sum_{t<=j} (q_t' x_c) q_t ||
+      if (temp * r * r <= tol3z) {
         double nn = 0.0;
         if (j + 1 < k) {
           double acc[8];
-          for (int t = 0; t < 8; ++t) acc[t] = 0.0;
-          // residual components held lane-wise (k <= 256)
-          for (int tt = 0; tt < (k + 31) / 32 && tt < 8; ++tt) {
+#pragma unroll
+          for (int tt = 0; tt < 8; ++tt) {
             const int t = lane + 32 * tt;
             acc[tt] = t < k ? (double)X[(int64_t)c * ldx + t] : 0.0;
           }
           for (int t0 = 0; t0 <= j; ++t0) {
             const double* qt = qs + (size_t)t0 * k;
             double d = 0.0;
-            for (int tt = 0; tt < (k + 31) / 32 && tt < 8; ++tt) {
+#pragma unroll
+            for (int tt = 0; tt < 8; ++tt) {
               const int t = lane + 32 * tt;
               if (t < k) d += qt[t] * acc[tt];
             }
             d = warp_sum(d);
-            for (int tt = 0; tt < (k + 31) / 32 && tt < 8; ++tt) {
+#pragma unroll
+            for (int tt = 0; tt < 8; ++tt) {
               const int t = lane + 32 * tt;
               if (t < k) acc[tt] -= d * qt[t];
             }
           }
+#pragma unroll
           for (int tt = 0; tt < 8; ++tt) nn += acc[tt] * acc[tt];
           nn = sqrt(warp_sum(nn));
         }
@@ -181,7 +199,7 @@ qrcp_pivots(const T* __restrict__ X, int64_t ldx, int n, int k, double* __restri
         vn1[c] = v1 * sqrt(temp);
       }
     }
-    grid.sync();
+    __syncthreads();
   }
 }
 
@@ -348,7 +366,7 @@ int assign_t(const void* xv, int64_t ldx, int n, int k, const AssignWs& w, int* 
     return SPB_ERR_CONTRACT;
   }
   // ---- pivots (cooperative: all CTAs co-resident)
-  const size_t qsmem = sizeof(double) * (size_t)k * k;
+  const size_t qsmem = sizeof(double) * ((size_t)k * k + 2 * (size_t)k);
   if (qsmem > 200 * 1024) {
     set_error("QRCP supports k <= 160 columns in this build (got %d)", k);
     return SPB_ERR_CONTRACT;
@@ -357,9 +375,9 @@ int assign_t(const void* xv, int64_t ldx, int n, int k, const AssignWs& w, int* 
                                 (int)qsmem));
   int per_sm = 0;
   SPB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, qrcp_pivots<T>, QT, qsmem));
-  int grid = std::max(1, std::min(per_sm, 2)) * num_sms();
-  grid = (int)std::min<int64_t>(grid, std::max<int64_t>(1, ceil_div(n, QT)));
-  grid = std::min(grid, 4096);
+  int grid = std::max(1, std::min(per_sm, 1)) * num_sms();
+  grid = (int)std::min<int64_t>(grid, std::max<int64_t>(1, ceil_div(n, 64)));
+  grid = std::min(grid, 2048);
   const T* Xa = X;
   int64_t ldxa = ldx;
   int na = n, ka = k;
