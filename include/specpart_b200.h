@@ -219,6 +219,17 @@ SPB_API int spb_assign_qrcp(int dtype, const void* x, int64_t ldx, int32_t n, in
                     size_t ws_bytes, int32_t* labels_out, int32_t* pivots_out,
                     double* info_out, void* stream);
 
+/* Optional k-means mode (north star (e); the reference has none, so parity is
+ * unpinned): Lloyd iterations on the rows of x (n x d, dtype, row stride ldx),
+ * optionally row-normalised, from the rows ``seeds`` (device int32[k], e.g.
+ * the QRCP pivots). labels_out device int32[n] (0..k-1, lowest index on ties);
+ * centroids_out device float32[k*d]; *iterations_out = Lloyd steps run. */
+SPB_API size_t spb_kmeans_workspace(int32_t k, int32_t d);
+SPB_API int spb_kmeans(int dtype, const void* x, int64_t ldx, int32_t n, int32_t d, int32_t k,
+                       const int32_t* seeds, int32_t max_iter, int32_t normalize_rows, void* ws,
+                       size_t ws_bytes, int32_t* labels_out, float* centroids_out,
+                       int32_t* iterations_out, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -45,6 +45,7 @@ from .lobpcg import (  # noqa: F401,E402
 from .spectral import (  # noqa: F401,E402
     GapResult,
     Partition,
+    assign_clusters_kmeans,
     assign_clusters_qrcp,
     block_size_for,
     detect_gap,

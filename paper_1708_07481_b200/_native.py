@@ -81,6 +81,9 @@ _SIGS = {
     "spb_orthonormalize": (C.c_int, [C.c_int, vp, i64, i32, i32, REFILL_CB, vp, vp, sz, vp]),
     "spb_sygv_workspace": (sz, [i32]),
     "spb_sygv": (C.c_int, [vp, vp, i32, i32, vp, vp, vp, sz, vp]),
+    "spb_kmeans_workspace": (sz, [i32, i32]),
+    "spb_kmeans": (C.c_int, [C.c_int, vp, i64, i32, i32, i32, vp, i32, i32, vp, sz, vp, vp,
+                             C.POINTER(i32), vp]),
     "spb_assign_workspace": (sz, [i32, i32]),
     "spb_assign_qrcp": (C.c_int, [C.c_int, vp, i64, i32, i32, vp, sz, vp, vp, C.POINTER(f64), vp]),
 }
