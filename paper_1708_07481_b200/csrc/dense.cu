@@ -13,6 +13,8 @@
 //   (mean removal :259-260); per-block partials, fixed-order final reduction.
 // * gather / scale columns — soft-lock compaction (_move_columns :250-256) and
 //   P normalisation (:391-393).
+#include <cstdlib>
+
 #include "dense.cuh"
 
 namespace spb {
@@ -111,6 +113,114 @@ gram_kernel(GramBatch b, int64_t n, int64_t kchunk, int ldo, int64_t split_strid
   }
 }
 
+// Gram on the FP64 tensor pipe: mma.sync m8n8k4 f64 (DMMA). 64x64 output tile
+// per CTA, 4 warps as 2x2 of 32x32 (4x4 DMMA tiles each). Operands are widened
+// to fp64 once, when a 32-row chunk is staged in shared memory (rows padded to
+// 68 doubles so the four k-rows of a fragment load hit disjoint bank groups);
+// the next chunk's global loads are in registers while the current one
+// multiplies. fp32 inputs multiply exactly in fp64, so the result matches the
+// CUDA-core path up to fp64 summation order.
+constexpr int DK = 32;   // rows per staged chunk
+constexpr int DLD = 68;  // padded row length (doubles)
+constexpr size_t kDmmaSmem = sizeof(double) * 2 * 2 * DK * DLD;
+
+template <typename T>
+__global__ void __launch_bounds__(128, 3)
+gram_dmma(GramBatch b, int64_t n, int64_t kchunk, int ldo, int64_t split_stride,
+          double* __restrict__ part) {
+  extern __shared__ double dsm[];
+  double* Us = dsm;                 // [2][DK][DLD]
+  double* Vs = dsm + 2 * DK * DLD;  // [2][DK][DLD]
+  const int tile = blockIdx.x;
+  int j = 0;
+  while (j + 1 < b.njobs && tile >= b.tile_start[j + 1]) ++j;
+  const GramJob jb = b.job[j];
+  const int local = tile - b.tile_start[j];
+  const int tq_count = (jb.q + GT - 1) / GT;
+  const int tp = local / tq_count, tq = local % tq_count;
+  const int p0 = tp * GT, q0 = tq * GT;
+  const int64_t k0 = (int64_t)blockIdx.y * kchunk;
+  const int64_t k1 = min(n, k0 + kchunk);
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int wm = warp >> 1, wn = warp & 1;
+  const T* U = (const T*)jb.U;
+  const T* V = (const T*)jb.V;
+  constexpr int PER = DK * GT / 128;  // 16 per operand
+  T ru[PER], rv[PER];
+  const bool ufull = p0 + GT <= jb.p, vfull = q0 + GT <= jb.q;
+  auto load = [&](int64_t kb) {
+#pragma unroll
+    for (int t = 0; t < PER; ++t) {
+      const int e = tid + 128 * t;
+      const int r = e / GT, c = e % GT;
+      const int64_t k = kb + r;
+      const bool kin = k < k1;
+      ru[t] = (kin && (ufull || p0 + c < jb.p)) ? U[k * jb.ldu + p0 + c] : T(0);
+      rv[t] = (kin && (vfull || q0 + c < jb.q)) ? V[k * jb.ldv + q0 + c] : T(0);
+    }
+  };
+  auto store = [&](int buf) {
+#pragma unroll
+    for (int t = 0; t < PER; ++t) {
+      const int e = tid + 128 * t;
+      const int r = e / GT, c = e % GT;
+      Us[(buf * DK + r) * DLD + c] = (double)ru[t];
+      Vs[(buf * DK + r) * DLD + c] = (double)rv[t];
+    }
+  };
+  double acc[4][4][2];
+#pragma unroll
+  for (int a = 0; a < 4; ++a)
+#pragma unroll
+    for (int c = 0; c < 4; ++c) acc[a][c][0] = acc[a][c][1] = 0.0;
+  const int fr = lane & 3, fc = lane >> 2;  // fragment k-row, m/n index
+  int buf = 0;
+  if (k0 < k1) {
+    load(k0);
+    store(0);
+  }
+  __syncthreads();
+  for (int64_t kb = k0; kb < k1; kb += DK) {
+    const bool more = kb + DK < k1;
+    if (more) load(kb + DK);
+    const double* ub = Us + buf * DK * DLD + wm * 32 + fc;
+    const double* vb = Vs + buf * DK * DLD + wn * 32 + fc;
+#pragma unroll
+    for (int k4 = 0; k4 < DK; k4 += 4) {
+      double af[4], bf[4];
+#pragma unroll
+      for (int t = 0; t < 4; ++t) {
+        af[t] = ub[(k4 + fr) * DLD + t * 8];
+        bf[t] = vb[(k4 + fr) * DLD + t * 8];
+      }
+#pragma unroll
+      for (int mt = 0; mt < 4; ++mt)
+#pragma unroll
+        for (int nt = 0; nt < 4; ++nt)
+          asm volatile(
+              "mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+              : "+d"(acc[mt][nt][0]), "+d"(acc[mt][nt][1])
+              : "d"(af[mt]), "d"(bf[nt]));
+    }
+    if (more) store(buf ^ 1);
+    __syncthreads();
+    buf ^= 1;
+  }
+  double* out = part + (int64_t)blockIdx.y * split_stride;
+#pragma unroll
+  for (int mt = 0; mt < 4; ++mt) {
+    const int i = p0 + wm * 32 + mt * 8 + fc;
+    if (i >= jb.p) continue;
+#pragma unroll
+    for (int nt = 0; nt < 4; ++nt)
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int c = q0 + wn * 32 + nt * 8 + fr * 2 + h;
+        if (c < jb.q) out[(int64_t)(jb.out_r + i) * ldo + jb.out_c + c] = acc[mt][nt][h];
+      }
+  }
+}
+
 __global__ void sum_splits(const double* __restrict__ part, int ksplit, int64_t split_stride,
                            int rows, int cols, int ldp, double* __restrict__ out, int ldo) {
   const int64_t total = (int64_t)rows * cols;
@@ -124,8 +234,9 @@ __global__ void sum_splits(const double* __restrict__ part, int ksplit, int64_t 
 }
 
 int choose_ksplit(int64_t n, int tiles) {
-  const int target = 2 * num_sms();
-  int64_t ks = ceil_div(target, std::max(tiles, 1));
+  // one full wave of the DMMA Gram (3 CTAs per SM): tiles * ks <= 3 * SMs
+  const int target = 3 * num_sms();
+  int64_t ks = std::max<int64_t>(1, target / std::max(tiles, 1));
   ks = std::min<int64_t>(ks, ceil_div(n, 512));
   return (int)std::max<int64_t>(ks, 1);
 }
@@ -357,11 +468,26 @@ int gram_batched(int dtype, const GramBatch& b, int64_t n, int out_rows, int out
   const int64_t kchunk = round_up(ceil_div(std::max<int64_t>(n, 1), ks), GK);
   const int64_t stride = (int64_t)out_rows * out_cols;
   dim3 grid(tiles, ks);
-  if (n > 0) {
+  static const bool use_fma = getenv("SPB_GRAM_FMA") != nullptr;  // A/B switch (CUDA-core DFMA)
+  if (n > 0 && use_fma) {
     if (dtype == SPB_F32)
       gram_kernel<float><<<grid, 128, 0, st>>>(b, n, kchunk, out_cols, stride, partial);
     else
       gram_kernel<double><<<grid, 128, 0, st>>>(b, n, kchunk, out_cols, stride, partial);
+    SPB_LAUNCH_CHECK();
+  } else if (n > 0) {
+    static bool attr = false;
+    if (!attr) {
+      SPB_CUDA(cudaFuncSetAttribute(gram_dmma<float>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    (int)kDmmaSmem));
+      SPB_CUDA(cudaFuncSetAttribute(gram_dmma<double>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    (int)kDmmaSmem));
+      attr = true;
+    }
+    if (dtype == SPB_F32)
+      gram_dmma<float><<<grid, 128, kDmmaSmem, st>>>(b, n, kchunk, out_cols, stride, partial);
+    else
+      gram_dmma<double><<<grid, 128, kDmmaSmem, st>>>(b, n, kchunk, out_cols, stride, partial);
     SPB_LAUNCH_CHECK();
   } else {
     SPB_CUDA(cudaMemsetAsync(partial, 0, sizeof(double) * stride, st));
