@@ -17,6 +17,7 @@
 // (eigenvalues of G_B by the same tridiagonal + bisection kernels), so the
 // ladder takes the reference's branch in every case.
 #include <cfloat>
+#include <cstdlib>
 
 #include "smalleig.cuh"
 
@@ -82,6 +83,40 @@ __global__ void sym_prep(const double* __restrict__ ga, const double* __restrict
 // mode 0 (sygv): cond bracket into status. mode 1 (cholqr): the reference's
 // acceptance tests (lobpcg.py:231-235) and Rinv = (L^-1)' written to Linv.
 constexpr int CB = 32;
+
+// ||L^-1||_F and the cond2 bracket (mode 0), or Rinv = (L^-1)' in place (mode 1).
+__device__ void chol_epilogue(int m, double fb, double* __restrict__ Linv, int mode,
+                              SmallStatus* status, double* red) {
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  double fl = 0.0;
+  for (int i = warp; i < m; i += ET / 32)
+    for (int j = lane; j <= i; j += 32) {
+      const double v = Linv[(int64_t)i * m + j];
+      fl += v * v;
+    }
+  fl = block_sum(fl, red);
+  if (mode == 0) {
+    if (tid == 0) {
+      // fb, fl are squared Frobenius norms: bracket = ||B||_F ||L^-1||_F^2
+      const double upper = sqrt(fb) * fl;
+      const double lower = upper / (m * sqrt((double)m));
+      status->fro_b = sqrt(fb);
+      status->fro_linv = sqrt(fl);
+      status->cond_hi = upper;
+      status->cond_lo = lower;
+      status->cond_state = upper <= kCondMax ? 0 : (lower > kCondMax ? 1 : 2);
+    }
+  } else {
+    // Rinv = (L^-1)' in place of Linv (upper triangular)
+    for (int i = warp; i < m; i += ET / 32)
+      for (int j = i + 1 + lane; j < m; j += 32) {
+        const double a = Linv[(int64_t)i * m + j], b = Linv[(int64_t)j * m + i];
+        Linv[(int64_t)i * m + j] = b;
+        Linv[(int64_t)j * m + i] = a;
+      }
+  }
+}
+
 
 __global__ void __launch_bounds__(ET)
 chol_linv(const double* __restrict__ Bsrc, int m, double* __restrict__ Lg, double* __restrict__ Linv,
@@ -250,33 +285,128 @@ chol_linv(const double* __restrict__ Bsrc, int m, double* __restrict__ Lg, doubl
       for (int j = lane; j < m; j += 32) Linv[(int64_t)i * m + j] = Vi[(int64_t)i * m + j];
     __syncthreads();
   }
-  double fl = 0.0;
+  chol_epilogue(m, fb, Linv, mode, status, red);
+}
+
+// Cholesky + inverse for m <= kCholLdlMax in one shared-memory pass, one CTA
+// barrier per column: right-looking LDL' (no square root or division on the
+// critical path besides one reciprocal per column, computed by the thread that
+// produced the next pivot), with the unit-lower inverse built alongside in the
+// upper triangle (Linv'[r][j] stored at [j][r]); L = L' D^1/2 and
+// L^-1 = D^-1/2 L'^-1 are formed at the end. Same outputs and status protocol
+// as chol_linv.
+constexpr int kCholLdlMax = 164;
+
+__global__ void __launch_bounds__(ET)
+chol_ldl(const double* __restrict__ Bsrc, int m, double* __restrict__ Lg, double* __restrict__ Linv,
+         int mode, SmallStatus* status) {
+  extern __shared__ double smem[];
+  __shared__ double red[33];
+  __shared__ int fail;
+  const int ld = m | 1;  // odd row stride: column walks are bank-conflict free
+  double* A = smem;      // m x ld
+  double* dinv = smem + (size_t)m * ld;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  if (status->nonfinite) return;
+  double fb = 0.0;
   for (int i = warp; i < m; i += ET / 32)
-    for (int j = lane; j <= i; j += 32) {
-      const double v = Linv[(int64_t)i * m + j];
-      fl += v * v;
+    for (int j = lane; j < m; j += 32) {
+      const double v = Bsrc[(int64_t)i * m + j];
+      A[i * ld + j] = v;
+      fb += v * v;
     }
-  fl = block_sum(fl, red);
-  if (mode == 0) {
-    if (tid == 0) {
-      // fb, fl are squared Frobenius norms: bracket = ||B||_F ||L^-1||_F^2
-      const double upper = sqrt(fb) * fl;
-      const double lower = upper / (m * sqrt((double)m));
-      status->fro_b = sqrt(fb);
-      status->fro_linv = sqrt(fl);
-      status->cond_hi = upper;
-      status->cond_lo = lower;
-      status->cond_state = upper <= kCondMax ? 0 : (lower > kCondMax ? 1 : 2);
-    }
-  } else {
-    // Rinv = (L^-1)' in place of Linv (upper triangular)
-    for (int i = warp; i < m; i += ET / 32)
-      for (int j = i + 1 + lane; j < m; j += 32) {
-        const double a = Linv[(int64_t)i * m + j], b = Linv[(int64_t)j * m + i];
-        Linv[(int64_t)i * m + j] = b;
-        Linv[(int64_t)j * m + i] = a;
+  fb = block_sum(fb, red);
+  if (tid == 0) {
+    fail = 0;
+    if (mode == 1) {  // diag > 0 and min diag > (eps na)^2 max diag (lobpcg.py:229-231)
+      double dmin = DBL_MAX, dmax = -DBL_MAX;
+      for (int i = 0; i < m; ++i) {
+        dmin = fmin(dmin, A[i * ld + i]);
+        dmax = fmax(dmax, A[i * ld + i]);
       }
+      status->dmin = dmin;
+      status->dmax = dmax;
+      const double t = kEps64 * m;
+      if (!(dmin > 0.0) || !(dmin > t * t * dmax)) fail = 1;
+    }
+    if (!fail) {
+      const double d0 = A[0];
+      if (!(d0 > 0.0)) fail = 2;
+      dinv[0] = 1.0 / d0;
+    }
   }
+  __syncthreads();
+  if (fail == 1) {
+    if (tid == 0) status->fallback = 1;
+    return;
+  }
+  for (int c = 0; c < m && !fail; ++c) {
+    const double rc = dinv[c];
+    // (a) trailing update A[i][q] -= (A[i][c] / d_c) A[q][c], c < q <= i
+    for (int i = c + 1 + warp; i < m; i += ET / 32) {
+      const double lic = A[i * ld + c] * rc;
+      double* Ai = A + i * ld;
+      for (int q = c + 1 + lane; q <= i; q += 32) Ai[q] = fma(-lic, A[q * ld + c], Ai[q]);
+      if (i == c + 1 && lane == 0) {  // next pivot is final: its reciprocal
+        const double dn = Ai[c + 1];
+        if (!(dn > 0.0)) fail = 2;
+        dinv[c + 1] = 1.0 / dn;
+      }
+    }
+    // (b) unit-lower inverse, column c-1: Linv'[r][j] -= L'[r][c-1] Linv'[c-1][j]
+    if (c >= 1) {
+      const int i = c - 1;
+      const double ri = dinv[i];
+      for (int r = c + warp; r < m; r += ET / 32) {
+        const double lri = A[r * ld + i] * ri;
+        for (int j = lane; j < i; j += 32) A[j * ld + r] = fma(-lri, A[j * ld + i], A[j * ld + r]);
+        if (lane == 0) A[i * ld + r] = -lri;
+      }
+    }
+    __syncthreads();
+  }
+  if (fail) {
+    if (tid == 0) {
+      if (mode == 0) status->not_pd = 1;
+      else status->fallback = 1;
+    }
+    return;
+  }
+  if (mode == 1 && tid == 0) {
+    double rmin = DBL_MAX, rmax = -DBL_MAX;
+    for (int i = 0; i < m; ++i) {
+      const double r = sqrt(A[i * ld + i]);
+      rmin = fmin(rmin, r);
+      rmax = fmax(rmax, r);
+    }
+    status->rmin = rmin;
+    status->rmax = rmax;
+    if (!(rmin > sqrt(kEps64) * rmax)) fail = 1;  // lobpcg.py:235
+  }
+  // D^-1/2 into dinv
+  for (int i = tid; i < m; i += ET) dinv[i] = 1.0 / sqrt(A[i * ld + i]);
+  __syncthreads();
+  if (fail) {
+    if (tid == 0) status->fallback = 1;
+    return;
+  }
+  for (int i = warp; i < m; i += ET / 32) {
+    const double ri = dinv[i];
+    for (int j = lane; j < m; j += 32) {
+      double l = 0.0, v = 0.0;
+      if (j < i) {
+        l = A[i * ld + j] * dinv[j];  // L'[i][j] sqrt(d_j) = A[i][j] / sqrt(d_j)
+        v = A[j * ld + i] * ri;       // D^-1/2 row scaling of Linv'
+      } else if (j == i) {
+        l = 1.0 / ri;
+        v = ri;
+      }
+      Lg[(int64_t)i * m + j] = l;
+      Linv[(int64_t)i * m + j] = v;
+    }
+  }
+  __syncthreads();
+  chol_epilogue(m, fb, Linv, mode, status, red);
 }
 
 // C = op(A) op(B) for small float64 matrices, 32x32 tiles, 256 threads.
@@ -432,8 +562,221 @@ tridiag(const double* __restrict__ Asrc, int m, int symmetrize, double* __restri
   }
 }
 
+// Cluster variant (m in [kTriClusterMin, kTriClusterMax]): the columns of the
+// matrix are split over the C CTAs of one thread-block cluster and stay in their
+// shared memory for the whole reduction; per step k every CTA
+//   (1) forms the reflector of row k redundantly from an all-gathered copy of
+//       row k (identical inputs, identical order => identical v, tau in every CTA),
+//   (2) computes p_i = tau sum_j W_ji v_j for its own columns i and pushes p_i and
+//       its share of p'v into every CTA's shared memory (DSMEM),
+//   (3) after one cluster barrier applies W -= v w' + w v' (w = p - (tau/2)(p'v) v)
+//       to its own columns and pushes its slice of row k+1 to every CTA,
+// so a step costs two cluster barriers instead of one SM streaming the whole
+// matrix. Exchange buffers are double-buffered by step parity.
+constexpr int TCT = 512;
+constexpr int kTriClusterMin = 48;
+constexpr int kTriClusterMax = 560;
+
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;\n" ::
+                   : "memory");
+}
+
+__device__ __forceinline__ void dsmem_store(double* local_addr, int rank, double v) {
+  uint32_t a = (uint32_t)__cvta_generic_to_shared(local_addr), r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;\n" : "=r"(r) : "r"(a), "r"(rank));
+  asm volatile("st.shared::cluster.f64 [%0], %1;\n" ::"r"(r), "d"(v) : "memory");
+}
+
+__global__ void __launch_bounds__(TCT)
+tridiag_cluster(const double* __restrict__ Asrc, int m, int symmetrize, double* __restrict__ V,
+                double* __restrict__ tau, double* __restrict__ d, double* __restrict__ e,
+                const SmallStatus* status) {
+  if (status && (status->nonfinite || status->not_pd)) return;  // uniform over the cluster
+  unsigned rank_u, csize_u;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;\n" : "=r"(rank_u));
+  asm volatile("mov.u32 %0, %%cluster_nctarank;\n" : "=r"(csize_u));
+  const int rank = (int)rank_u, C = (int)csize_u;
+  const int nc = (m + C - 1) / C;
+  const int c0 = rank * nc;
+  const int ncl = max(0, min(m, c0 + nc) - c0);
+  extern __shared__ double tsm[];
+  double* Wl = tsm;                        // m x nc, row j / local column c
+  double* rowbuf = Wl + (size_t)m * nc;    // [2][m]  row k (all-gathered)
+  double* pbuf = rowbuf + 2 * m;           // [2][m]  p (all-gathered)
+  double* vbuf = pbuf + 2 * m;             // [m]     v of the current step
+  double* dotbuf = vbuf + m;               // [2][16] per-CTA shares of p'v
+  double* red = dotbuf + 32;               // [G][nc]
+  __shared__ double wdot[2];
+  __shared__ double sc[2];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int G = TCT / nc;
+  const int g = tid / nc, lc = tid - (tid / nc) * nc;
+  const bool active = g < G && lc < ncl;
+  const int icol = c0 + lc;
+  for (int x = tid; x < m * ncl; x += TCT) {
+    const int j = x / ncl, c = x - (x / ncl) * ncl, i = c0 + c;
+    const double a = Asrc[(int64_t)j * m + i];
+    Wl[j * nc + c] = symmetrize ? 0.5 * (a + Asrc[(int64_t)i * m + j]) : a;
+    V[(int64_t)j * m + i] = 0.0;
+  }
+  __syncthreads();
+  for (int x = tid; x < ncl * C; x += TCT) {
+    const int r = x / ncl, c = x - (x / ncl) * ncl;
+    dsmem_store(rowbuf + c0 + c, r, Wl[c]);
+  }
+  cluster_sync_all();
+  for (int k = 0; k + 2 < m; ++k) {
+    const int b = k & 1;
+    const double* row = rowbuf + b * m;
+    double* pb = pbuf + b * m;
+    double* nextrow = rowbuf + (b ^ 1) * m;
+    // (1) reflector of row k (warp 0), v into vbuf
+    if (warp == 0) {
+      double ss = 0.0;
+      for (int i = k + 2 + lane; i < m; i += 32) ss = fma(row[i], row[i], ss);
+      ss = warp_sum(ss);
+      const double alpha = row[k + 1];
+      double tk = 0.0, scale = 0.0, beta = alpha;
+      if (ss != 0.0) {
+        beta = -copysign(sqrt(alpha * alpha + ss), alpha);
+        tk = (beta - alpha) / beta;
+        scale = 1.0 / (alpha - beta);
+      }
+      for (int i = k + 1 + lane; i < m; i += 32) vbuf[i] = i == k + 1 ? 1.0 : row[i] * scale;
+      if (lane == 0) {
+        sc[0] = tk;
+        if (rank == 0) {
+          d[k] = row[k];
+          e[k] = beta;
+          tau[k] = tk;
+        }
+      }
+    }
+    __syncthreads();
+    const double tk = sc[0];
+    const int j0 = k + 1 + g;
+    const bool own = active && icol > k;
+    if (tid < ncl && icol > k) V[(int64_t)k * m + icol] = vbuf[icol];
+    if (tk == 0.0) {  // identity reflector: row k+1 is unchanged, pass it on
+      if (tid < ncl && icol > k) {
+        const double wv = Wl[(k + 1) * nc + tid];
+        for (int r = 0; r < C; ++r) dsmem_store(nextrow + icol, r, wv);
+      }
+      cluster_sync_all();
+      continue;
+    }
+    // (2) p = tau W v on own columns
+    if (own) {
+      double a0 = 0.0, a1 = 0.0;
+      const double* wp = Wl + j0 * nc + lc;
+      const double* vp = vbuf + j0;
+      const int step = G * nc;
+      int j = j0;
+      for (; j + G < m; j += 2 * G, wp += 2 * step, vp += 2 * G) {
+        a0 = fma(wp[0], vp[0], a0);
+        a1 = fma(wp[step], vp[G], a1);
+      }
+      if (j < m) a0 = fma(wp[0], vp[0], a0);
+      red[g * nc + lc] = a0 + a1;
+    }
+    __syncthreads();
+    if (tid < 64) {
+      double pv = 0.0;
+      if (tid < ncl && icol > k) {
+        double sacc = 0.0;
+        const int gmax = min(G, m - (k + 1));  // groups that saw a row
+        for (int q = 0; q < gmax; ++q) sacc += red[q * nc + tid];
+        const double p = tk * sacc;
+        pv = p * vbuf[icol];
+        for (int r = 0; r < C; ++r) dsmem_store(pb + icol, r, p);
+      }
+      pv = warp_sum(pv);
+      if (lane == 0) wdot[tid >> 5] = pv;
+      asm volatile("bar.sync 1, 64;\n" ::: "memory");
+      if (tid < C) dsmem_store(dotbuf + b * 16 + rank, tid, wdot[0] + wdot[1]);
+    }
+    cluster_sync_all();
+    // (3) rank-2 update of own columns, push row k+1
+    if (own) {
+      double tot = 0.0;
+      for (int r = 0; r < C; ++r) tot += dotbuf[b * 16 + r];
+      const double K = 0.5 * tk * tot;
+      const double vi = vbuf[icol];
+      const double wi = fma(-K, vi, pb[icol]);
+      double* wp = Wl + j0 * nc + lc;
+      const double* vp = vbuf + j0;
+      const double* pp = pb + j0;
+      const int step = G * nc;
+      int j = j0;
+      if (g == 0) {  // row k+1 goes to every CTA for the next reflector
+        const double wj = fma(-K, vp[0], pp[0]);
+        const double wv = fma(-vp[0], wi, fma(-wj, vi, wp[0]));
+        wp[0] = wv;
+        for (int r = 0; r < C; ++r) dsmem_store(nextrow + icol, r, wv);
+        j += G, wp += step, vp += G, pp += G;
+      }
+#pragma unroll 2
+      for (; j < m; j += G, wp += step, vp += G, pp += G) {
+        const double vj = vp[0];
+        const double wj = fma(-K, vj, pp[0]);
+        wp[0] = fma(-vj, wi, fma(-wj, vi, wp[0]));
+      }
+    }
+    cluster_sync_all();
+  }
+  if (m >= 2) {
+    const double* row = rowbuf + ((m - 2) & 1) * m;
+    if (rank == 0 && tid == 0) {
+      d[m - 2] = row[m - 2];
+      e[m - 2] = row[m - 1];
+      tau[m - 2] = 0.0;
+      tau[m - 1] = 0.0;
+      e[m - 1] = 0.0;
+    }
+    if (tid == 0 && m - 1 >= c0 && m - 1 < c0 + ncl) d[m - 1] = Wl[(m - 1) * nc + (m - 1 - c0)];
+  }
+}
+
+size_t tridiag_cluster_smem(int m, int C);
+
+int tridiag_cluster_size(int m) {
+  static const int forced = getenv("SPB_TRI_CLUSTER") ? atoi(getenv("SPB_TRI_CLUSTER")) : 0;
+  if (m < kTriClusterMin || m > kTriClusterMax) return 0;
+  if (forced == 2 || forced == 4 || forced == 8 || forced == 16)
+    if ((m + forced - 1) / forced <= 64 && tridiag_cluster_smem(m, forced) <= 200 * 1024) return forced;
+  return m <= 160 ? 4 : (m <= 400 ? 8 : 16);
+}
+
+size_t tridiag_cluster_smem(int m, int C) {
+  const int nc = (m + C - 1) / C;
+  return sizeof(double) * ((size_t)m * nc + 5 * (size_t)m + 32 + (size_t)(TCT / nc) * nc);
+}
+
 void launch_tridiag(const double* Asrc, int m, int symmetrize, double* Wg, double* V, double* tau,
                     double* d, double* e, const SmallStatus* status, size_t smem, cudaStream_t st) {
+  if (const int C = tridiag_cluster_size(m)) {
+    static bool attr = false;
+    if (!attr) {
+      cudaFuncSetAttribute(tridiag_cluster, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+      cudaFuncSetAttribute(tridiag_cluster, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+      attr = true;
+    }
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(C);
+    cfg.blockDim = dim3(TCT);
+    cfg.dynamicSmemBytes = tridiag_cluster_smem(m, C);
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = C;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    cudaLaunchKernelEx(&cfg, tridiag_cluster, Asrc, m, symmetrize, V, tau, d, e, status);
+    return;
+  }
   const int rows = (m + 31) / 32;
   if (rows <= 1)
     tridiag<1><<<1, ET, smem, st>>>(Asrc, m, symmetrize, Wg, V, tau, d, e, status);
@@ -942,6 +1285,11 @@ size_t sygv_ws_count(int m, int nev) {
          r((size_t)(round_up(std::max(nev, 1), 128) + 128) * 6 * m);
 }
 
+size_t chol_ldl_smem(int m) { return ((size_t)m * (m | 1) + m) * sizeof(double); }
+
+void launch_chol(const double* B, int m, double* L, double* Linv, int mode, SmallStatus* status,
+                 cudaStream_t st);
+
 size_t chol_smem(int m) {
   size_t b = (size_t)m * m * sizeof(double);
   if (b > 200 * 1024) return 0;
@@ -954,10 +1302,20 @@ size_t tridiag_smem(int m) {
   return b <= 190 * 1024 ? b + 2 * m * sizeof(double) : 0;
 }
 
+void launch_chol(const double* B, int m, double* L, double* Linv, int mode, SmallStatus* status,
+                 cudaStream_t st) {
+  static const bool old = getenv("SPB_CHOL_BLOCKED") != nullptr;  // A/B switch
+  if (!old && m <= kCholLdlMax && chol_ldl_smem(m) <= 224 * 1024)
+    chol_ldl<<<1, ET, chol_ldl_smem(m), st>>>(B, m, L, Linv, mode, status);
+  else
+    chol_linv<<<1, ET, chol_smem(m), st>>>(B, m, L, Linv, mode, status);
+}
+
 int set_smem_attrs() {
   static bool done = false;
   if (done) return SPB_OK;
   SPB_CUDA(cudaFuncSetAttribute(chol_linv, cudaFuncAttributeMaxDynamicSharedMemorySize, 224 * 1024));
+  SPB_CUDA(cudaFuncSetAttribute(chol_ldl, cudaFuncAttributeMaxDynamicSharedMemorySize, 224 * 1024));
   SPB_CUDA(cudaFuncSetAttribute(tridiag<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
   SPB_CUDA(cudaFuncSetAttribute(tridiag<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
   SPB_CUDA(cudaFuncSetAttribute(tridiag<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
@@ -1000,7 +1358,7 @@ int sygv_enqueue(const double* ga, const double* gb, int ldg, int m, int nev, do
   SPB_LAUNCH_CHECK();
   const double* Atri = w.A;
   if (!ident) {
-    chol_linv<<<1, ET, chol_smem(m), st>>>(w.B, m, w.L, w.Linv, 0, status);
+    launch_chol(w.B, m, w.L, w.Linv, 0, status, st);
     SPB_LAUNCH_CHECK();
     dim3 grid((unsigned)ceil_div(m, 32), (unsigned)ceil_div(m, 32));
     small_gemm<<<grid, 256, 0, st>>>(0, 0, m, m, m, w.Linv, m, w.A, m, w.M, m);
@@ -1071,7 +1429,7 @@ int cholqr_enqueue(const double* g, int ldg, int na, double* rinv, double* ws,
   // symmetrise (the reference's _sym(b.T @ b), lobpcg.py:228)
   const int g1 = (int)std::min<int64_t>(ceil_div((int64_t)na * na, 256), 1024);
   sym_prep<<<g1, 256, 0, st>>>(g, nullptr, ldg, na, S, nullptr, status);
-  chol_linv<<<1, ET, chol_smem(na), st>>>(S, na, L, rinv, 1, status);
+  launch_chol(S, na, L, rinv, 1, status, st);
   SPB_LAUNCH_CHECK();
   return SPB_OK;
 }
