@@ -16,6 +16,7 @@
 #include <cooperative_groups.h>
 
 #include <algorithm>
+#include <cstdint>
 #include <vector>
 
 #include "dense.cuh"
@@ -32,83 +33,262 @@ struct BestRec {
   double val;
   int pos;
   int col;
+  double dmax;  // largest norm bound among this CTA's deferred columns
 };
 
 __device__ __forceinline__ bool better(double v, int p, double bv, int bp) {
   return v > bv || (v == bv && p < bp);
 }
 
-// Cooperative pivot kernel: ONE grid barrier per step. Every CTA owns a
-// contiguous range of columns of X' (rows of X) and keeps their partial norms
-// (vn1, vn2) and current positions; after the barrier each CTA reduces the
-// per-CTA maxima (double-buffered by step parity), replays the column swap
-// dgeqp3 performs (perm[j] from a k-entry swap history in shared memory) and
-// forms q_j redundantly (identical arithmetic on every CTA), then downdates its
-// own columns and produces its next local maximum.
+constexpr int QG = 8;           // lanes per column group
+constexpr int QKMAX = 160;      // largest k (shared-memory Q)
+constexpr int QPER = QKMAX / QG;
+
+__device__ __forceinline__ double group_sum(double v, unsigned gmask) {
+  v += __shfl_xor_sync(gmask, v, 4);
+  v += __shfl_xor_sync(gmask, v, 2);
+  v += __shfl_xor_sync(gmask, v, 1);
+  return v;
+}
+
+// q' x for one column by an 8-lane group (fixed order: the downdate and the
+// deferred replay must produce identical values). fp32 rows with 16-byte
+// alignment are read as float4, all loads issued before the FMAs.
+template <typename T>
+__device__ __forceinline__ double dot_group(const double* __restrict__ q, const T* __restrict__ x,
+                                            int k, int gl, unsigned gmask) {
+  double s = 0.0;
+  if constexpr (sizeof(T) == 4) {
+    if ((reinterpret_cast<uintptr_t>(x) & 15) == 0) {
+      constexpr int NV = QKMAX / (4 * QG);
+      const int k4 = k >> 2;
+      float4 v[NV];
+#pragma unroll
+      for (int i = 0; i < NV; ++i) {
+        const int c = gl + QG * i;
+        v[i] = c < k4 ? __ldg(reinterpret_cast<const float4*>(x) + c) : make_float4(0.f, 0.f, 0.f, 0.f);
+      }
+#pragma unroll
+      for (int i = 0; i < NV; ++i) {
+        const int c = gl + QG * i;
+        if (c < k4) {
+          const double* qq = q + 4 * c;
+          s = fma(qq[0], (double)v[i].x, s);
+          s = fma(qq[1], (double)v[i].y, s);
+          s = fma(qq[2], (double)v[i].z, s);
+          s = fma(qq[3], (double)v[i].w, s);
+        }
+      }
+      for (int t = 4 * k4 + gl; t < k; t += QG) s = fma(q[t], (double)x[t], s);
+      return group_sum(s, gmask);
+    }
+  }
+  for (int t = gl; t < k; t += QG) s = fma(q[t], (double)x[t], s);
+  return group_sum(s, gmask);
+}
+
+// Exact partial norm ||(I - Q_s Q_s') x|| (MGS over q_0..q_s): dlaqp2's recompute.
+template <typename T>
+__device__ double recompute_group(const double* __restrict__ qs, const T* __restrict__ x, int k,
+                                  int s, int gl, unsigned gmask) {
+  if (s + 1 >= k) return 0.0;
+  double acc[QPER];
+#pragma unroll
+  for (int i = 0; i < QPER; ++i) {
+    const int t = gl + QG * i;
+    acc[i] = t < k ? (double)x[t] : 0.0;
+  }
+  for (int t0 = 0; t0 <= s; ++t0) {
+    const double* qt = qs + (size_t)t0 * k;
+    double d = 0.0;
+#pragma unroll
+    for (int i = 0; i < QPER; ++i) {
+      const int t = gl + QG * i;
+      if (t < k) d = fma(qt[t], acc[i], d);
+    }
+    d = group_sum(d, gmask);
+#pragma unroll
+    for (int i = 0; i < QPER; ++i) {
+      const int t = gl + QG * i;
+      if (t < k) acc[i] = fma(-d, qt[t], acc[i]);
+    }
+  }
+  double nn = 0.0;
+#pragma unroll
+  for (int i = 0; i < QPER; ++i) nn = fma(acc[i], acc[i], nn);
+  return sqrt(group_sum(nn, gmask));
+}
+
+// Cooperative pivot kernel: ONE grid barrier per step (two on the rare steps
+// that resolve deferred columns). Every CTA owns a contiguous range of columns
+// of X' (rows of X); per column it keeps (vn1, vn2) in one 16-byte record, the
+// current position, and one bit of an "exact and unpivoted" mask in shared
+// memory. After the barrier each CTA reduces the per-CTA maxima (double-
+// buffered by step parity), replays the column swap dgeqp3 performs (swap
+// history in shared memory), forms q_j redundantly (identical arithmetic on
+// every CTA), and then makes ONE pass over its exact columns that downdates
+// them and already tracks the candidates of the next step.
+//
+// dlaqp2 recomputes a partial norm exactly when the downdate loses more than
+// half the digits. Those columns have lost almost all their norm, so the
+// recompute is DEFERRED: the column leaves the mask, remembers the step s0 at
+// which dlaqp2 would recompute and carries a bound on the recomputed value
+// (2e-4 of its last exact norm: the downdate only defers below sqrt(tol3z) vn2,
+// plus a rounding allowance). Whenever a deferred bound reaches
+// the best exact candidate, the affected columns are brought up to date by
+// replaying dlaqp2's steps s0..j-1 for them (same dots, same formulas) before
+// the pivot is chosen, so the pivot sequence is the one dlaqp2 produces.
+constexpr int QU = 2;  // columns in flight per lane group
+
 template <typename T>
 __global__ void __launch_bounds__(QT)
-qrcp_pivots(const T* __restrict__ X, int64_t ldx, int n, int k, double* __restrict__ vn1,
-            double* __restrict__ vn2, int* __restrict__ pos, int* __restrict__ perm_unused,
-            double* __restrict__ Q_unused, BestRec* __restrict__ bb, int* __restrict__ piv) {
+qrcp_pivots(const T* __restrict__ X, int64_t ldx, int n, int k, double2* __restrict__ vn,
+            int* __restrict__ pos, int* __restrict__ dirty, BestRec* __restrict__ bb,
+            int* __restrict__ piv) {
   cg::grid_group grid = cg::this_grid();
-  extern __shared__ double qs[];         // q_0..q_{k-1} (k x k), then xp[k], cdot[k]
+  extern __shared__ double qs[];         // q_0..q_{k-1} (k x k), xp[k], cdot[k], mask words
   double* xp = qs + (size_t)k * k;       // pivot column (then residual)
   double* cdot = xp + k;                 // q_t' r
+  unsigned* amask = reinterpret_cast<unsigned*>(cdot + k);
   __shared__ BestRec wb[QT / 32];
   __shared__ int swap_pp[1024], swap_cj[1024];  // swap history (position pp, column moved)
   __shared__ int s_p, s_pp, s_cj;
+  __shared__ BestRec s_best;
+  __shared__ double s_dpersist;  // max bound over this CTA's deferred columns
+  __shared__ double s_gmax0;     // largest initial column norm (scale of rounding noise)
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int grp = tid / QG, gl = tid % QG;
+  const unsigned gmask = 0xFFu << (lane & ~(QG - 1));
+  constexpr int NGRP = QT / QG;
   const int per = (n + gridDim.x - 1) / gridDim.x;
   const int c_lo = blockIdx.x * per, c_hi = min(n, c_lo + per);
+  const int cnt = max(0, c_hi - c_lo);
   const double tol3z = sqrt(kEps64);
 
-  // initial norms of my columns (warp per column), positions = identity
-  for (int c = c_lo + warp; c < c_hi; c += QT / 32) {
+  // per-thread running candidate (exact columns) and deferred bound
+  double bv = -1.0, dm = -1.0;
+  int bp = INT_MAX, bc = -1;
+  auto offer = [&](double v, int p, int c) {
+    if (better(v, p, bv, bp)) { bv = v; bp = p; bc = c; }
+  };
+
+  for (int w = tid; w < (cnt + 31) / 32; w += QT) {
+    const int rem = cnt - 32 * w;
+    amask[w] = rem >= 32 ? 0xFFFFFFFFu : ((1u << rem) - 1u);
+  }
+  if (tid == 0) s_dpersist = -1.0;
+  for (int li = grp; li < cnt; li += NGRP) {
+    const int c = c_lo + li;
+    const T* x = X + (int64_t)c * ldx;
     double s = 0.0;
-    for (int t = lane; t < k; t += 32) {
-      const double v = (double)X[(int64_t)c * ldx + t];
-      s += v * v;
+    for (int t = gl; t < k; t += QG) {
+      const double v = (double)x[t];
+      s = fma(v, v, s);
     }
-    s = warp_sum(s);
-    if (lane == 0) {
-      vn1[c] = sqrt(s);
-      vn2[c] = vn1[c];
+    s = sqrt(group_sum(s, gmask));
+    if (gl == 0) {
+      vn[c] = make_double2(s, s);
       pos[c] = c;
+      dirty[c] = -1;
     }
+    offer(s, c, c);
   }
   __syncthreads();
-  for (int j = 0; j < k; ++j) {
-    // ---- local argmax over my remaining columns (ties: lowest position)
-    double bv = -1.0;
-    int bp = INT_MAX, bc = -1;
-    for (int c = c_lo + tid; c < c_hi; c += QT) {
-      const int p = pos[c];
-      if (p < j) continue;
-      const double v = vn1[c];
-      if (better(v, p, bv, bp)) { bv = v; bp = p; bc = c; }
-    }
+
+  // block reduction of the running candidates into slot[blockIdx.x]
+  auto publish = [&](BestRec* slot) {
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
       const double ov = __shfl_xor_sync(0xffffffffu, bv, o);
       const int op = __shfl_xor_sync(0xffffffffu, bp, o);
       const int oc = __shfl_xor_sync(0xffffffffu, bc, o);
+      dm = fmax(dm, __shfl_xor_sync(0xffffffffu, dm, o));
       if (better(ov, op, bv, bp)) { bv = ov; bp = op; bc = oc; }
     }
-    if (lane == 0) wb[warp] = {bv, bp, bc};
+    if (lane == 0) wb[warp] = {bv, bp, bc, dm};
     __syncthreads();
-    BestRec* slot = bb + (j & 1) * gridDim.x;
     if (tid == 0) {
       BestRec b = wb[0];
-      for (int w = 1; w < QT / 32; ++w)
+      double d = fmax(b.dmax, s_dpersist);
+      for (int w = 1; w < QT / 32; ++w) {
+        d = fmax(d, wb[w].dmax);
         if (better(wb[w].val, wb[w].pos, b.val, b.pos)) b = wb[w];
+      }
+      b.dmax = d;
+      s_dpersist = d;
       slot[blockIdx.x] = b;
     }
-    grid.sync();
-    // ---- every CTA: global pivot, swap replay, q_j
+    bv = -1.0;
+    dm = -1.0;
+    bp = INT_MAX;
+    bc = -1;
+  };
+  auto global_best = [&](const BestRec* slot) {
     if (tid == 0) {
       BestRec b = slot[0];
-      for (int g = 1; g < (int)gridDim.x; ++g)
+      double d = b.dmax;
+      for (int g = 1; g < (int)gridDim.x; ++g) {
+        d = fmax(d, slot[g].dmax);
         if (better(slot[g].val, slot[g].pos, b.val, b.pos)) b = slot[g];
+      }
+      b.dmax = d;
+      s_best = b;
+    }
+    __syncthreads();
+    return s_best;
+  };
+
+  for (int j = 0; j < k; ++j) {
+    BestRec* slot0 = bb + (size_t)((j & 1) * 2) * gridDim.x;
+    publish(slot0);
+    grid.sync();
+    BestRec b = global_best(slot0);
+    if (j == 0 && tid == 0) s_gmax0 = b.val;
+    if (b.dmax >= b.val || b.col < 0) {
+      // resolve deferred columns whose bound reaches the best exact candidate
+      const double thr = b.col < 0 ? -1.0 : b.val;
+      for (int li = grp; li < cnt; li += NGRP) {
+        const int c = c_lo + li;
+        const int s0 = dirty[c];
+        if (s0 < 0 || pos[c] < j || !(vn[c].x >= thr)) continue;
+        const T* x = X + (int64_t)c * ldx;
+        double v1 = recompute_group(qs, x, k, s0, gl, gmask), v2 = v1;
+        for (int st = s0 + 1; st < j; ++st) {
+          if (v1 == 0.0) continue;
+          const double d = dot_group(qs + (size_t)st * k, x, k, gl, gmask);
+          double temp = fabs(d) / v1;
+          temp = fmax(0.0, (1.0 + temp) * (1.0 - temp));
+          if (temp * v1 * v1 <= tol3z * v2 * v2) {
+            v1 = recompute_group(qs, x, k, st, gl, gmask);
+            v2 = v1;
+          } else {
+            v1 = v1 * sqrt(temp);
+          }
+        }
+        if (gl == 0) {
+          vn[c] = make_double2(v1, v2);
+          dirty[c] = -1;
+          atomicOr(&amask[li >> 5], 1u << (li & 31));
+        }
+      }
+      __syncthreads();
+      // fresh candidates and deferred bound over this CTA's columns
+      if (tid == 0) s_dpersist = -1.0;
+      for (int li = tid; li < cnt; li += QT) {
+        const int c = c_lo + li;
+        if (pos[c] < j) continue;
+        const double v = vn[c].x;
+        if ((amask[li >> 5] >> (li & 31)) & 1u) offer(v, pos[c], c);
+        else if (dirty[c] >= 0) dm = fmax(dm, v);
+      }
+      __syncthreads();
+      BestRec* slot1 = slot0 + gridDim.x;
+      publish(slot1);
+      grid.sync();
+      b = global_best(slot1);
+    }
+    // ---- every CTA: swap replay, q_j
+    if (tid == 0) {
       // perm[j]: column currently at position j = column moved there by the latest
       // earlier swap whose pivot came from position j, else j itself
       int cj = j;
@@ -123,7 +303,11 @@ qrcp_pivots(const T* __restrict__ X, int64_t ldx, int n, int k, double* __restri
     }
     __syncthreads();
     const int p = s_p, pp = s_pp, cj = s_cj;
-    if (p >= c_lo && p < c_hi && tid == 0) { pos[p] = j; vn1[p] = 0.0; }
+    if (p >= c_lo && p < c_hi && tid == 0) {
+      pos[p] = j;
+      vn[p].x = 0.0;
+      amask[(p - c_lo) >> 5] &= ~(1u << ((p - c_lo) & 31));
+    }
     if (cj != p && cj >= c_lo && cj < c_hi && tid == 0) pos[cj] = pp;
     // q_j = normalize((I - Q Q')^2 x_p): CGS2 with thread-parallel dots and updates
     for (int t = tid; t < k; t += QT) xp[t] = (double)X[(int64_t)p * ldx + t];
@@ -152,51 +336,53 @@ qrcp_pivots(const T* __restrict__ X, int64_t ldx, int n, int k, double* __restri
       for (int t = lane; t < k; t += 32) qj[t] = xp[t] * inv;
     }
     __syncthreads();
-    // ---- downdate my remaining columns (dlaqp2: recompute when |q_j'x|/vn1 loses digits)
-    for (int c = c_lo + warp; c < c_hi; c += QT / 32) {
-      if (pos[c] <= j) continue;
-      const double v1 = vn1[c];
-      if (v1 == 0.0) continue;
-      double s = 0.0;
-      for (int t = lane; t < k; t += 32) s += qj[t] * (double)X[(int64_t)c * ldx + t];
-      s = warp_sum(s);
-      double temp = fabs(s) / v1;
-      temp = fmax(0.0, (1.0 + temp) * (1.0 - temp));
-      const double r = v1 / vn2[c];
-      if (temp * r * r <= tol3z) {
-        double nn = 0.0;
-        if (j + 1 < k) {
-          double acc[8];
+    if (j + 1 == k) break;
+    // ---- one pass: downdate the exact columns, defer the ones dlaqp2 recomputes,
+    //      and track the next step's candidates
+    for (int base = grp; base < cnt; base += NGRP * QU) {
+      bool act[QU];
+      double2 st[QU];
+      int ps[QU];
 #pragma unroll
-          for (int tt = 0; tt < 8; ++tt) {
-            const int t = lane + 32 * tt;
-            acc[tt] = t < k ? (double)X[(int64_t)c * ldx + t] : 0.0;
-          }
-          for (int t0 = 0; t0 <= j; ++t0) {
-            const double* qt = qs + (size_t)t0 * k;
-            double d = 0.0;
-#pragma unroll
-            for (int tt = 0; tt < 8; ++tt) {
-              const int t = lane + 32 * tt;
-              if (t < k) d += qt[t] * acc[tt];
-            }
-            d = warp_sum(d);
-#pragma unroll
-            for (int tt = 0; tt < 8; ++tt) {
-              const int t = lane + 32 * tt;
-              if (t < k) acc[tt] -= d * qt[t];
-            }
-          }
-#pragma unroll
-          for (int tt = 0; tt < 8; ++tt) nn += acc[tt] * acc[tt];
-          nn = sqrt(warp_sum(nn));
+      for (int u = 0; u < QU; ++u) {
+        const int li = base + u * NGRP;
+        act[u] = li < cnt && ((amask[li >> 5] >> (li & 31)) & 1u);
+        if (act[u]) {
+          st[u] = vn[c_lo + li];
+          ps[u] = pos[c_lo + li];
         }
-        if (lane == 0) {
-          vn1[c] = nn;
-          vn2[c] = nn;
+      }
+      double dots[QU];
+#pragma unroll
+      for (int u = 0; u < QU; ++u)
+        dots[u] = act[u] ? dot_group(qj, X + (int64_t)(c_lo + base + u * NGRP) * ldx, k, gl, gmask)
+                         : 0.0;
+#pragma unroll
+      for (int u = 0; u < QU; ++u) {
+        if (!act[u]) continue;
+        const int li = base + u * NGRP, c = c_lo + li;
+        double v1 = st[u].x;
+        const double v2 = st[u].y;
+        if (v1 != 0.0) {
+          double temp = fabs(dots[u]) / v1;
+          temp = fmax(0.0, (1.0 + temp) * (1.0 - temp));
+          if (temp * v1 * v1 <= tol3z * v2 * v2) {  // dlaqp2: temp * (vn1/vn2)^2 <= tol3z
+            // Bound on the norm dlaqp2 would recompute: the downdated estimate is
+            // <= sqrt(tol3z) vn2 here and its accumulated rounding is O(k eps)
+            // relative to vn2 (and to the column's initial norm <= gmax0).
+            const double bound = 2e-4 * v2 + 1e-10 * s_gmax0;
+            dm = fmax(dm, bound);
+            if (gl == 0) {
+              dirty[c] = j;
+              vn[c].x = bound;
+              atomicAnd(&amask[li >> 5], ~(1u << (li & 31)));
+            }
+            continue;
+          }
+          v1 = v1 * sqrt(temp);
+          if (gl == 0) vn[c].x = v1;
         }
-      } else if (lane == 0) {
-        vn1[c] = v1 * sqrt(temp);
+        offer(v1, ps[u], c);
       }
     }
     __syncthreads();
@@ -317,8 +503,8 @@ struct AssignWs {
 
 AssignWs carve_assign(Arena& a, int n, int k) {
   AssignWs w;
-  w.vn1 = a.take<double>(n);
-  w.vn2 = a.take<double>(n);
+  w.vn1 = a.take<double>(2 * (size_t)n);  // (vn1, vn2) records
+  w.vn2 = nullptr;
   w.pos = a.take<int>(n);
   w.perm = a.take<int>(n);
   w.raw = a.take<int>(n);
@@ -338,7 +524,7 @@ AssignWs carve_assign(Arena& a, int n, int k) {
   w.remap = a.take<int>(k);
   w.kfound = a.take<int>(4);
   w.zero_rows = a.take<unsigned long long>(2);
-  w.bb = a.take<BestRec>(4096);
+  w.bb = a.take<BestRec>(4 * 2048);
   w.status = a.take<SmallStatus>(1);
   return w;
 }
@@ -366,8 +552,11 @@ int assign_t(const void* xv, int64_t ldx, int n, int k, const AssignWs& w, int* 
     return SPB_ERR_CONTRACT;
   }
   // ---- pivots (cooperative: all CTAs co-resident)
-  const size_t qsmem = sizeof(double) * ((size_t)k * k + 2 * (size_t)k);
-  if (qsmem > 200 * 1024) {
+  int grid0 = num_sms();
+  grid0 = (int)std::min<int64_t>(grid0, std::max<int64_t>(1, ceil_div(n, 64)));
+  const int per0 = (int)ceil_div(n, grid0);
+  const size_t qsmem = sizeof(double) * ((size_t)k * k + 2 * (size_t)k) + 4 * (size_t)ceil_div(per0, 32);
+  if (qsmem + 9 * 1024 > 227 * 1024 || k > QKMAX) {
     set_error("QRCP supports k <= 160 columns in this build (got %d)", k);
     return SPB_ERR_CONTRACT;
   }
@@ -375,15 +564,17 @@ int assign_t(const void* xv, int64_t ldx, int n, int k, const AssignWs& w, int* 
                                 (int)qsmem));
   int per_sm = 0;
   SPB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, qrcp_pivots<T>, QT, qsmem));
-  int grid = std::max(1, std::min(per_sm, 1)) * num_sms();
-  grid = (int)std::min<int64_t>(grid, std::max<int64_t>(1, ceil_div(n, 64)));
-  grid = std::min(grid, 2048);
+  if (per_sm < 1) {
+    set_error("QRCP pivot kernel cannot be resident (k = %d)", k);
+    return SPB_ERR_CONTRACT;
+  }
+  const int grid = grid0;
   const T* Xa = X;
   int64_t ldxa = ldx;
   int na = n, ka = k;
-  void* args[] = {(void*)&Xa, (void*)&ldxa, (void*)&na, (void*)&ka, (void*)&w.vn1,
-                  (void*)&w.vn2, (void*)&w.pos, (void*)&w.perm, (void*)&w.Q, (void*)&w.bb,
-                  (void*)&w.piv};
+  double2* vnp = reinterpret_cast<double2*>(w.vn1);
+  void* args[] = {(void*)&Xa, (void*)&ldxa, (void*)&na, (void*)&ka, (void*)&vnp,
+                  (void*)&w.pos, (void*)&w.perm, (void*)&w.bb, (void*)&w.piv};
   SPB_CUDA(cudaLaunchCooperativeKernel((void*)qrcp_pivots<T>, grid, QT, args, qsmem, st));
   if (pivots_out)
     SPB_CUDA(cudaMemcpyAsync(pivots_out, w.piv, sizeof(int) * k, cudaMemcpyDeviceToDevice, st));
