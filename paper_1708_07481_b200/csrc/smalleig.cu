@@ -738,6 +738,161 @@ tridiag_cluster(const double* __restrict__ Asrc, int m, int symmetrize, double* 
   }
 }
 
+// Cholesky + inverse for kCholLdlMax < m <= kCholClusterMax: the packed
+// array of chol_ldl (L' in the lower triangle, the unit-lower inverse
+// transposed in the upper one) is split by columns over the CTAs of a cluster.
+// Iteration c needs only packed column c (L' column c below the diagonal, row c
+// of L'^-1 above it, d_c on it): its owner pushes it to every CTA while
+// finishing iteration c-1, so a column costs one cluster barrier. The cond
+// bracket / CholQR tests run afterwards in chol_finish.
+constexpr int CCT = 512;
+constexpr int kCholClusterMax = 560;
+
+__global__ void __launch_bounds__(CCT)
+chol_cluster(const double* __restrict__ Bsrc, int m, double* __restrict__ Lg,
+             double* __restrict__ Linv, int mode, SmallStatus* status) {
+  if (status->nonfinite) return;  // uniform over the cluster
+  unsigned rank_u, csize_u;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;\n" : "=r"(rank_u));
+  asm volatile("mov.u32 %0, %%cluster_nctarank;\n" : "=r"(csize_u));
+  const int rank = (int)rank_u, C = (int)csize_u;
+  const int nc = (m + C - 1) / C;
+  const int c0 = rank * nc;
+  const int ncl = max(0, min(m, c0 + nc) - c0);
+  extern __shared__ double csm[];
+  double* P = csm;                    // m x nc packed columns
+  double* colbuf = P + (size_t)m * nc;  // [2][m] broadcast column
+  __shared__ int s_fail;
+  const int tid = threadIdx.x;
+  const int G = CCT / nc;
+  const int g = tid / nc, lc = tid - (tid / nc) * nc;
+  const bool active = g < G && lc < ncl;
+  const int q = c0 + lc;
+  if (tid == 0) {
+    s_fail = 0;
+    if (mode == 1) {  // diag > 0 and min diag > (eps na)^2 max diag (lobpcg.py:229-231)
+      double dmin = DBL_MAX, dmax = -DBL_MAX;
+      for (int i = 0; i < m; ++i) {
+        dmin = fmin(dmin, Bsrc[(int64_t)i * m + i]);
+        dmax = fmax(dmax, Bsrc[(int64_t)i * m + i]);
+      }
+      if (rank == 0) {
+        status->dmin = dmin;
+        status->dmax = dmax;
+      }
+      const double t = kEps64 * m;
+      if (!(dmin > 0.0) || !(dmin > t * t * dmax)) s_fail = 1;
+    }
+  }
+  for (int x = tid; x < m * ncl; x += CCT) {
+    const int i = x / ncl, c = x - (x / ncl) * ncl;
+    P[i * nc + c] = i >= c0 + c ? Bsrc[(int64_t)i * m + c0 + c] : 0.0;
+  }
+  __syncthreads();
+  if (s_fail) {
+    if (rank == 0 && tid == 0) status->fallback = 1;
+    return;
+  }
+  if (c0 == 0 && ncl > 0)
+    for (int i = tid; i < m; i += CCT) {
+      const double v = P[i * nc];
+      for (int r = 0; r < C; ++r) dsmem_store(colbuf + i, r, v);
+    }
+  cluster_sync_all();
+  int fail = 0;
+  for (int c = 0; c < m; ++c) {
+    const double* col = colbuf + (c & 1) * m;
+    double* nxt = colbuf + ((c + 1) & 1) * m;
+    const double dc = col[c];
+    if (!(dc > 0.0)) {
+      fail = 1;
+      break;
+    }
+    if (active && q > c) {
+      const double rc = 1.0 / dc;
+      const double lqc = col[q] * rc;  // L'[q][c]
+      double* Pq = P + lc;
+      for (int i = q + g; i < m; i += G)  // factor: A[i][q] -= A[i][c] L'[q][c]
+        Pq[i * nc] = fma(-col[i], lqc, Pq[i * nc]);
+      for (int j = g; j < c; j += G)  // inverse: L'^-1[q][j] -= L'[q][c] L'^-1[c][j]
+        Pq[j * nc] = fma(-lqc, col[j], Pq[j * nc]);
+      if (g == 0) Pq[c * nc] = -lqc;
+    }
+    const int cn = c + 1;
+    if (cn < m && cn >= c0 && cn < c0 + ncl) {  // owner of the next column: push it
+      __syncthreads();
+      const double* Pn = P + (cn - c0);
+      for (int x = tid; x < m * C; x += CCT) {
+        const int r = x / m, i = x - (x / m) * m;
+        dsmem_store(nxt + i, r, Pn[i * nc]);
+      }
+    }
+    cluster_sync_all();
+  }
+  if (fail) {
+    if (rank == 0 && tid == 0) {
+      if (mode == 0) status->not_pd = 1;
+      else status->fallback = 1;
+    }
+    return;
+  }
+  // L = L' D^1/2 (own columns), L^-1 = D^-1/2 L'^-1 (own rows)
+  for (int x = tid; x < m * ncl; x += CCT) {
+    const int c = x / m, i = x - (x / m) * m;
+    const int qq = c0 + c;
+    const double dq = P[qq * nc + c];
+    const double rs = 1.0 / sqrt(dq);
+    double l = 0.0, v = 0.0;
+    if (i > qq) l = P[i * nc + c] * rs;
+    else if (i == qq) l = sqrt(dq);
+    if (i < qq) v = P[i * nc + c] * rs;
+    else if (i == qq) v = rs;
+    Lg[(int64_t)i * m + qq] = l;
+    Linv[(int64_t)qq * m + i] = v;
+  }
+}
+
+// Frobenius norms, cond bracket / CholQR diagonal test and Rinv layout after chol_cluster.
+__global__ void __launch_bounds__(ET)
+chol_finish(const double* __restrict__ Bsrc, int m, const double* __restrict__ Lg,
+            double* __restrict__ Linv, int mode, SmallStatus* status) {
+  __shared__ double red[33];
+  __shared__ int fail;
+  if (status->nonfinite || status->not_pd || status->fallback) return;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  double fb = 0.0;
+  for (int i = warp; i < m; i += ET / 32)
+    for (int j = lane; j < m; j += 32) {
+      const double v = Bsrc[(int64_t)i * m + j];
+      fb += v * v;
+    }
+  fb = block_sum(fb, red);
+  if (tid == 0) {
+    fail = 0;
+    if (mode == 1) {
+      double rmin = DBL_MAX, rmax = -DBL_MAX;
+      for (int i = 0; i < m; ++i) {
+        rmin = fmin(rmin, Lg[(int64_t)i * m + i]);
+        rmax = fmax(rmax, Lg[(int64_t)i * m + i]);
+      }
+      status->rmin = rmin;
+      status->rmax = rmax;
+      if (!(rmin > sqrt(kEps64) * rmax)) fail = 1;  // lobpcg.py:235
+    }
+  }
+  __syncthreads();
+  if (fail) {
+    if (tid == 0) status->fallback = 1;
+    return;
+  }
+  chol_epilogue(m, fb, Linv, mode, status, red);
+}
+
+size_t chol_cluster_smem(int m, int C) {
+  const int nc = (m + C - 1) / C;
+  return sizeof(double) * ((size_t)m * nc + 2 * (size_t)m);
+}
+
 size_t tridiag_cluster_smem(int m, int C);
 
 int tridiag_cluster_size(int m) {
@@ -1305,10 +1460,33 @@ size_t tridiag_smem(int m) {
 void launch_chol(const double* B, int m, double* L, double* Linv, int mode, SmallStatus* status,
                  cudaStream_t st) {
   static const bool old = getenv("SPB_CHOL_BLOCKED") != nullptr;  // A/B switch
-  if (!old && m <= kCholLdlMax && chol_ldl_smem(m) <= 224 * 1024)
+  if (!old && m <= kCholLdlMax && chol_ldl_smem(m) <= 224 * 1024) {
     chol_ldl<<<1, ET, chol_ldl_smem(m), st>>>(B, m, L, Linv, mode, status);
-  else
+  } else if (!old && m <= kCholClusterMax) {
+    const int C = m <= 400 ? 8 : 16;
+    static bool attr = false;
+    if (!attr) {
+      cudaFuncSetAttribute(chol_cluster, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+      cudaFuncSetAttribute(chol_cluster, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+      attr = true;
+    }
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(C);
+    cfg.blockDim = dim3(CCT);
+    cfg.dynamicSmemBytes = chol_cluster_smem(m, C);
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = C;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    cudaLaunchKernelEx(&cfg, chol_cluster, B, m, L, Linv, mode, status);
+    chol_finish<<<1, ET, 0, st>>>(B, m, L, Linv, mode, status);
+  } else {
     chol_linv<<<1, ET, chol_smem(m), st>>>(B, m, L, Linv, mode, status);
+  }
 }
 
 int set_smem_attrs() {

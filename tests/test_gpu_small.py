@@ -24,7 +24,7 @@ def _spd_pair(m, seed, cond_b=10.0):
     return a, b
 
 
-@pytest.mark.parametrize("m", [1, 2, 3, 7, 21, 63, 147, 170, 324])
+@pytest.mark.parametrize("m", [1, 2, 3, 7, 21, 47, 63, 147, 164, 165, 170, 324, 401, 528])
 def test_sygv_matches_lapack(spb, m):
     from paper_1708_07481_b200.lobpcg import _solve_small
 
@@ -103,3 +103,22 @@ def test_rayleigh_ritz_full_basis(spb):
     assert np.allclose(vals, np.linalg.eigvalsh(a), atol=1e-8)
     ritz = basis @ coeff
     assert np.allclose(ritz.T @ (a @ ritz), np.diag(vals), atol=1e-7)
+
+
+@pytest.mark.parametrize("w", [49, 108, 176, 256])
+def test_orthonormalize_wide_blocks(spb, w):
+    # CholQR widths of C2..C4 (l = 49, 108, 176) and beyond: single-CTA LDL'
+    # and cluster Cholesky paths
+    rng = np.random.default_rng(w)
+    x = rng.standard_normal((4 * w + 100, w)) * np.geomspace(1.0, 1e3, w)[None, :]
+    spb.orthonormalize(x)
+    assert np.allclose(x.T @ x, np.eye(w), atol=1e-11)
+
+
+def test_sygv_not_pd_cluster(spb):
+    from paper_1708_07481_b200.lobpcg import _solve_small
+
+    a, b = _spd_pair(300, 5)
+    b[150, 150] = -50.0  # indefinite B in the cluster Cholesky range
+    with pytest.raises(spb.ConditioningError):
+        _solve_small(a, b, 10)
