@@ -313,6 +313,167 @@ update_kernel(UpdParams P, int64_t n) {
   }
 }
 
+// fp32 block update with an 8x8 register tile per thread: CTA = RG row groups x
+// NCG column groups (8 rows interleaved by RG, 8 contiguous columns each), so a
+// k-step costs 2.5 shared float4 loads per 64 FMAs. The coefficients are first
+// rounded to fp32 (exactly as update_kernel does) into a staging buffer laid out
+// per 16-row k tile as [k][half][column group][4], so both operands arrive by
+// cp.async (A zero-filled past n / w) through a 3-stage pipeline with one
+// barrier per tile and the column-group reads are bank-conflict free. The
+// per-element FMA order is update_kernel's, so results are identical.
+constexpr int UKT = 16;       // k per stage
+constexpr int UAP = UKT + 4;  // padded A row (floats)
+constexpr int UNS = 3;        // pipeline stages
+
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem, int src_bytes) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(sa), "l"(gmem), "r"(src_bytes));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory");
+}
+
+int update_cols(int q) { return q <= 32 ? 32 : q <= 64 ? 64 : q <= 128 ? 128 : q <= 192 ? 192 : 256; }
+
+// cst[s] = fp32(scale_s * C_s) in the tile layout above, zero padded.
+__global__ void stage_coeffs(UpdParams P, int cols) {
+  const int ncg = cols / 8;
+  int off = 0;
+  for (int s = 0; s < P.nseg; ++s) {
+    const UpdSeg sg = P.seg[s];
+    const int wr = (int)round_up(sg.w, UKT);
+    float* dst = P.cstage + off;
+    const int total = wr * cols;
+    for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < total; e += gridDim.x * blockDim.x) {
+      const int k = e / cols, r = e % cols;
+      const int h = r / (4 * ncg), cg = (r / 4) % ncg, x = r % 4;
+      const int c = cg * 8 + h * 4 + x;
+      float v = 0.0f;
+      if (k < sg.w && c < P.q) v = (float)(sg.scale * sg.C[(int64_t)k * sg.ldc + c]);
+      dst[e] = v;
+    }
+    off += total;
+  }
+}
+
+template <int NCG, int RG>
+__global__ void __launch_bounds__(NCG * RG, NCG * RG <= 128 ? 4 : 2)
+update_f32(UpdParams P, int64_t n) {
+  constexpr int NT = NCG * RG, ROWS = RG * 8, COLS = NCG * 8;
+  extern __shared__ __align__(16) float usm[];
+  float* As = usm;                          // [UNS][ROWS][UAP]
+  float* Cs = usm + UNS * ROWS * UAP;       // [UNS][UKT][COLS]
+  const int tid = threadIdx.x, cg = tid % NCG, rg = tid / NCG;
+  const int64_t r0 = (int64_t)blockIdx.x * ROWS;
+  const int q = P.q;
+  const int c0 = cg * 8;
+  float acc[8][8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    const int64_t r = r0 + rg + RG * i;
+#pragma unroll
+    for (int jj = 0; jj < 8; ++jj) {
+      const int col = c0 + jj;
+      acc[i][jj] = (P.init && col < q && r < n) ? ((const float*)P.init)[r * P.ldi + col] : 0.0f;
+    }
+  }
+  int coff = 0;
+  for (int s = 0; s < P.nseg; ++s) {
+    const UpdSeg sg = P.seg[s];
+    const float* A = (const float*)sg.A;
+    const float* Cg = P.cstage + coff;
+    const int ntiles = (sg.w + UKT - 1) / UKT;
+    coff += ntiles * UKT * COLS;
+    auto stage = [&](int t) {
+      if (t < ntiles) {
+        const int buf = t % UNS;
+        const int k0 = t * UKT;
+        for (int e = tid; e < ROWS * (UKT / 4); e += NT) {
+          const int r = e / (UKT / 4), ch = e % (UKT / 4);
+          const int64_t gr = r0 + r;
+          const int k = k0 + ch * 4;
+          int bytes = 0;
+          if (gr < n && k < sg.w) bytes = min(4, sg.w - k) * 4;
+          const float* src = bytes ? A + gr * sg.lda + k : A;
+          cp_async16(As + (buf * ROWS + r) * UAP + ch * 4, src, bytes);
+        }
+        const float* cs = Cg + (size_t)t * UKT * COLS;
+        for (int e = tid; e < UKT * COLS / 4; e += NT)
+          cp_async16(Cs + buf * UKT * COLS + e * 4, cs + e * 4, 16);
+      }
+      cp_async_commit();
+    };
+    for (int t = 0; t < UNS - 1; ++t) stage(t);
+    for (int t = 0; t < ntiles; ++t) {
+      cp_async_wait<UNS - 2>();
+      __syncthreads();
+      stage(t + UNS - 1);
+      const int buf = t % UNS;
+      const float* Ab = As + buf * ROWS * UAP;
+      const float* Cb = Cs + buf * UKT * COLS;
+#pragma unroll
+      for (int kk = 0; kk < UKT; kk += 4) {
+        float4 a4[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) a4[i] = *reinterpret_cast<const float4*>(Ab + (rg + RG * i) * UAP + kk);
+#pragma unroll
+        for (int k4 = 0; k4 < 4; ++k4) {
+          const float4 cA = *reinterpret_cast<const float4*>(Cb + (kk + k4) * COLS + cg * 4);
+          const float4 cB = *reinterpret_cast<const float4*>(Cb + (kk + k4) * COLS + (NCG + cg) * 4);
+          const float cv[8] = {cA.x, cA.y, cA.z, cA.w, cB.x, cB.y, cB.z, cB.w};
+#pragma unroll
+          for (int i = 0; i < 8; ++i) {
+            const float a = k4 == 0 ? a4[i].x : (k4 == 1 ? a4[i].y : (k4 == 2 ? a4[i].z : a4[i].w));
+#pragma unroll
+            for (int jj = 0; jj < 8; ++jj) acc[i][jj] = fmaf(a, cv[jj], acc[i][jj]);
+          }
+        }
+      }
+    }
+    cp_async_wait<0>();
+    __syncthreads();  // buffers free before the next segment's prologue
+    if (sg.emit) {
+      float* O = (float*)sg.out;
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const int64_t r = r0 + rg + RG * i;
+        if (r >= n) continue;
+#pragma unroll
+        for (int jj = 0; jj < 8; ++jj) {
+          const int col = c0 + jj;
+          if (col < q) O[r * sg.ldo + col] = acc[i][jj];
+        }
+      }
+    }
+  }
+}
+
+template <int NCG, int RG>
+void launch_update_f32(const UpdParams& p, int64_t n, cudaStream_t st) {
+  constexpr int ROWS = RG * 8, COLS = NCG * 8;
+  const size_t smem = sizeof(float) * (UNS * ROWS * UAP + UNS * UKT * COLS);
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(update_f32<NCG, RG>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    attr = true;
+  }
+  stage_coeffs<<<32, 256, 0, st>>>(p, COLS);
+  update_f32<NCG, RG><<<(unsigned)ceil_div(n, ROWS), NCG * RG, smem, st>>>(p, n);
+}
+
+bool update_f32_ok(const UpdParams& p) {
+  if (!p.cstage) return false;
+  size_t need = 0;
+  for (int s = 0; s < p.nseg; ++s) {
+    const UpdSeg& g = p.seg[s];
+    if ((reinterpret_cast<uintptr_t>(g.A) & 15) || (g.lda & 3)) return false;
+    need += (size_t)round_up(g.w, UKT) * update_cols(p.q);
+  }
+  return need <= p.cstage_cap && (reinterpret_cast<uintptr_t>(p.cstage) & 15) == 0;
+}
+
 template <typename T, int QV>
 void launch_update_qv(const UpdParams& p, int64_t n, cudaStream_t st) {
   constexpr int RPT = QV <= 2 ? 8 : (QV <= 4 ? 4 : 2);
@@ -322,6 +483,15 @@ void launch_update_qv(const UpdParams& p, int64_t n, cudaStream_t st) {
 
 template <typename T>
 void launch_update(const UpdParams& p, int64_t n, cudaStream_t st) {
+  static const bool generic = getenv("SPB_UPDATE_GENERIC") != nullptr;  // A/B switch
+  if (sizeof(T) == 4 && !generic && update_f32_ok(p)) {
+    if (p.q <= 32) launch_update_f32<4, 32>(p, n, st);
+    else if (p.q <= 64) launch_update_f32<8, 16>(p, n, st);
+    else if (p.q <= 128) launch_update_f32<16, 8>(p, n, st);
+    else if (p.q <= 192) launch_update_f32<24, 8>(p, n, st);
+    else launch_update_f32<32, 8>(p, n, st);
+    return;
+  }
   const int qv = (p.q + 31) / 32;
   switch (qv) {
     case 1: launch_update_qv<T, 1>(p, n, st); break;
@@ -511,6 +681,10 @@ int block_update(int dtype, const UpdParams& p, int64_t n, cudaStream_t st) {
     launch_update<double>(p, n, st);
   SPB_LAUNCH_CHECK();
   return SPB_OK;
+}
+
+size_t update_cstage_floats(int w_total, int nseg) {
+  return (size_t)(w_total + nseg * UKT) * 256;
 }
 
 size_t colreduce_partial_doubles(int64_t n, int cols) {

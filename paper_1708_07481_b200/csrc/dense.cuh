@@ -41,7 +41,12 @@ struct UpdParams {
   int64_t ldi;
   int nseg;
   int q;
+  float* cstage;        // optional fp32 coefficient staging (fast fp32 path)
+  size_t cstage_cap;    // floats; see update_cstage_floats()
 };
+
+// Staging floats the fp32 update needs for segments of total width w_total.
+size_t update_cstage_floats(int w_total, int nseg);
 
 // Column-reduction kinds.
 enum ColReduce { CR_SUMSQ = 0, CR_SUM = 1, CR_RESIDUAL = 2 };

@@ -40,6 +40,8 @@ struct SolveWs {
   double *Gs;         // small Gram (lp x lp)
   double *coef;       // coupling / Rinv (lp x lp)
   double *Cm;         // Ritz coefficients (mmax x l)
+  float *cstage;      // fp32 coefficient staging of the block updates
+  size_t cstage_cap;
   double *theta, *theta_new;
   double *sygv_ws;
   size_t sygv_cap;
@@ -90,6 +92,8 @@ SolveWs carve(Arena& a, int dtype, int n, int l, int nranks = 1, int n_max = 0) 
   w.Gs = a.take<double>((size_t)w.lp * w.lp);
   w.coef = a.take<double>((size_t)w.lp * w.lp);
   w.Cm = a.take<double>((size_t)mm * l);
+  w.cstage_cap = update_cstage_floats(3 * w.lp, 3);
+  w.cstage = a.take<float>(w.cstage_cap);
   w.theta = a.take<double>(mm + 8);
   w.theta_new = a.take<double>(mm + 8);
   w.sygv_cap = sygv_ws_doubles(mm, l);
@@ -276,6 +280,8 @@ struct Driver {
     p.nseg = 1;
     p.q = q;
     p.seg[0] = {B, w.ld, C, ldc, B, w.ld, scale, wcols, 1};
+    p.cstage = w.cstage;
+    p.cstage_cap = w.cstage_cap;
     return block_update(w.dtype, p, w.n, st);
   }
 
@@ -288,6 +294,8 @@ struct Driver {
     p.init = w.R;
     p.ldi = w.ld;
     p.seg[0] = {w.X, w.ld, w.coef, w.lp, w.R, w.ld, -1.0, w.l, 1};
+    p.cstage = w.cstage;
+    p.cstage_cap = w.cstage_cap;
     return block_update(w.dtype, p, w.n, st);
   }
 
@@ -487,6 +495,8 @@ struct Driver {
       if (pw) p.seg[s++] = {P, w.ld, Cp, l, P, w.ld, 1.0, pw, 1};
       p.seg[s++] = {X, w.ld, Cx, l, X, w.ld, 1.0, l, 1};
       p.nseg = s;
+      p.cstage = w.cstage;
+      p.cstage_cap = w.cstage_cap;
       SPB_TRY(block_update(w.dtype, p, w.n, st));
     }
     return SPB_OK;
