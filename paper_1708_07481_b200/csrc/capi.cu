@@ -2,6 +2,8 @@
 #include <cstdarg>
 #include <cstring>
 
+#include <mutex>
+
 #include "common.cuh"
 
 namespace spb {
@@ -106,13 +108,21 @@ extern "C" int spb_max_f64(const double* v, int64_t count, double* out_host, voi
     return SPB_OK;
   }
   const int blocks = (int)std::min<int64_t>(ceil_div(count, 256), 256);
+  // per-device scratch allocated once (a stream-ordered allocation per call
+  // occasionally stalled the caller for hundreds of ms while the pool remapped)
+  static std::mutex mu;
+  static double* scratch[64] = {nullptr};
+  int dev = 0;
+  SPB_CUDA(cudaGetDevice(&dev));
   double* part = nullptr;
-  SPB_CUDA(cudaMallocAsync((void**)&part, sizeof(double) * (blocks + 1), st));
-  max_partial<<<blocks, 256, 0, st>>>(v, count, part);
-  max_partial<<<1, 256, 0, st>>>(part, blocks, part + blocks);
-  cudaError_t e = cudaMemcpyAsync(out_host, part + blocks, sizeof(double), cudaMemcpyDeviceToHost, st);
-  cudaFreeAsync(part, st);
-  SPB_CUDA(e);
-  SPB_CUDA(cudaStreamSynchronize(st));
+  {
+    std::lock_guard<std::mutex> lock(mu);
+    if (!scratch[dev & 63]) SPB_CUDA(cudaMalloc((void**)&scratch[dev & 63], sizeof(double) * 320));
+    part = scratch[dev & 63];
+    max_partial<<<blocks, 256, 0, st>>>(v, count, part);
+    max_partial<<<1, 256, 0, st>>>(part, blocks, part + blocks);
+    SPB_CUDA(cudaMemcpyAsync(out_host, part + blocks, sizeof(double), cudaMemcpyDeviceToHost, st));
+    SPB_CUDA(cudaStreamSynchronize(st));
+  }
   return SPB_OK;
 }

@@ -144,13 +144,15 @@ struct Driver {
   cudaStream_t st;
   int64_t stats[16] = {0};
   // optional CUDA-event timing of every operator apply (cfg->reserved & 1)
+  // (events come from a process-wide pool: creating/destroying them per solve
+  // perturbed the timed steps)
   bool profile = false;
-  std::vector<cudaEvent_t> ev;
   size_t ev_used = 0;
   double spmm_bytes = 0.0;
   int64_t nnz = 0;
-  ~Driver() {
-    for (auto e : ev) cudaEventDestroy(e);
+  static std::vector<cudaEvent_t>& event_pool() {
+    static std::vector<cudaEvent_t> pool;
+    return pool;
   }
   std::vector<double> h_theta, h_norms;  // last residual step
   double h_scale = 0.0;
@@ -160,6 +162,7 @@ struct Driver {
     stats[1]++;
     if (op->kind != SPB_OP_LAPLACIAN)
       return dense_apply(op->dense, op->n, src, w.ld, cols, dst, w.ld, w.dtype, nullptr, st);
+    std::vector<cudaEvent_t>& ev = event_pool();
     if (profile) {
       while (ev.size() < ev_used + 2) {
         cudaEvent_t e;
@@ -193,6 +196,7 @@ struct Driver {
 
   int finish_profile() {
     if (!profile || ev_used == 0) return SPB_OK;
+    std::vector<cudaEvent_t>& ev = event_pool();
     SPB_CUDA(cudaStreamSynchronize(st));
     double ms = 0.0;
     for (size_t i = 0; i < ev_used; i += 2) {

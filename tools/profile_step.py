@@ -21,6 +21,7 @@ ap = argparse.ArgumentParser()
 ap.add_argument("--config", default="c2")
 ap.add_argument("--precision", default="float32")
 ap.add_argument("--iters", type=int, default=20)
+ap.add_argument("--tol", type=float, default=1e-12)
 a = ap.parse_args()
 spec = CONFIGS[a.config]
 edges, truth = generate_dcsbm(spec)
@@ -31,7 +32,7 @@ dev = torch.device("cuda", 0)
 src = torch.from_numpy(np.ascontiguousarray(edges[:, 0])).to(dev)
 dst = torch.from_numpy(np.ascontiguousarray(edges[:, 1])).to(dev)
 x0_d = torch.from_numpy(x0).to(dev)
-cfg = spb.SolverConfig(block_size=l, tol=1e-12, max_iter=a.iters, seed=0)
+cfg = spb.SolverConfig(block_size=l, tol=a.tol, max_iter=a.iters, seed=0)
 
 
 def step():
