@@ -208,6 +208,44 @@ def ten_x_tol(spb, g, x0, l, k, precision):
     return 0.1 * float(np.max(r0[: k + 1])) / max(abs(float(t0[l - 1])), op.scale_hint)
 
 
+def gram_roofline(n, l, precision):
+    """Rayleigh-Ritz Gram [X R P]'[X R P] (n x 3l, solver layout) timed alone with
+    CUDA events on the launching stream: float64 products on the DMMA pipe."""
+    import torch
+
+    from paper_1708_07481_b200 import _native as N
+
+    tdt = torch.float32 if precision == "float32" else torch.float64
+    code = N.F32 if precision == "float32" else N.F64
+    m = 3 * l
+    ld = 3 * ((l + 7) // 8 * 8)
+    u = torch.randn((n, ld), dtype=tdt, device="cuda")
+    out = torch.empty((m, m), dtype=torch.float64, device="cuda")
+    L = N.lib()
+    wsb = L.spb_gram_workspace(m, m, n)
+    ws = torch.empty(wsb, dtype=torch.uint8, device="cuda")
+
+    def run():
+        N.check(L.spb_gram(code, 0, N.ptr(u), ld, m, N.ptr(u), ld, m, n, N.ptr(out), m,
+                           N.ptr(ws), wsb, N.stream()))
+
+    for _ in range(3):
+        run()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    reps = 10
+    e0.record()
+    for _ in range(reps):
+        run()
+    e1.record()
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / reps
+    tflops = 2.0 * n * m * m / (ms * 1e-3) / 1e12
+    peak = 37.0  # B200 FP64 tensor (DMMA) spec per GPU; no measured FP64 peak in MEASURED_PEAKS.json
+    return {"bound": "tensor (fp64 DMMA)", "achieved": tflops, "peak": peak, "unit": "TFLOP/s",
+            "frac": tflops / peak, "peak_kind": "spec", "shape": f"{n}x{m} -> {m}x{m}",
+            "ms_per_launch": ms, "kernel": "spb::gram_dmma"}
+
+
 def run_ours(args):
     import torch
 
@@ -290,6 +328,12 @@ def run_ours(args):
     spmm_calls = sum(s["spmm_calls"] for s in stats)
     peak, peak_kind = load_peaks()
     achieved = (spmm_bytes / (spmm_us * 1e-6)) / 1e9 if spmm_us else None
+    # gather model: + 4 bytes per (nonzero, column) of the gathered X rows
+    esz = 4 if args.precision == "float32" else 8
+    nnz_w = int(spb.from_edges((src, dst), spec.n).device_csr()[3])
+    gather_bytes = spmm_bytes + esz * nnz_w * sum(s["spmm_cols"] for s in stats)
+    gather_achieved = (gather_bytes / (spmm_us * 1e-6)) / 1e9 if spmm_us else None
+    gram = gram_roofline(spec.n, l, args.precision)
     traffic = None
     tf = ROOT / "profiles" / "spmm_traffic.json"
     if tf.exists():
@@ -344,7 +388,12 @@ def run_ours(args):
                          "frac": (achieved / peak) if achieved else None, "traffic": traffic,
                          "kernel": "spb::spmm_vec (Laplacian SpMM)", "peak_kind": peak_kind,
                          "launches": spmm_calls,
-                         "avg_launch_us": spmm_us / max(spmm_calls, 1)},
+                         "avg_launch_us": spmm_us / max(spmm_calls, 1),
+                         "bytes_model": "compulsory 4(n+1)+(4+esz)nnz+esz*n+2*esz*n*cols per apply",
+                         "gather_model": {"achieved": gather_achieved,
+                                          "frac": (gather_achieved / peak) if gather_achieved else None,
+                                          "bytes_model": "compulsory + esz*nnz*cols"},
+                         "gram": gram},
             "cpu_baseline": cpu,
             "e2e": {"value": e2e_value, "unit": UNIT,
                     "h2d_bytes_per_step": int(edges.nbytes + x0.nbytes),
