@@ -44,7 +44,8 @@ enum {
   SPB_ERR_ASSIGNMENT = 6,     /* AssignmentError (spectral.py:156-161)            */
   SPB_ERR_CUDA = 7,           /* CUDA runtime failure                             */
   SPB_ERR_WORKSPACE = 8,      /* workspace smaller than the size query returned   */
-  SPB_ERR_CALLBACK = 9        /* a host callback reported failure                 */
+  SPB_ERR_CALLBACK = 9,       /* a host callback reported failure                 */
+  SPB_ERR_PARSE = 10          /* edge-list line outside the fast-path syntax      */
 };
 
 /* Storage type of the n-row dense blocks and of the operator values. */
@@ -218,6 +219,21 @@ SPB_API size_t spb_assign_workspace(int32_t n, int32_t k);
 SPB_API int spb_assign_qrcp(int dtype, const void* x, int64_t ldx, int32_t n, int32_t k, void* ws,
                     size_t ws_bytes, int32_t* labels_out, int32_t* pivots_out,
                     double* info_out, void* stream);
+
+/* ---------------- (f.2) edge-list ingestion ---------------------------------
+ * load_edge_list (graph.py:152-209): tab-separated "src dst [weight]" text in a
+ * host buffer, parsed by nthreads host threads (<= 0: all cores) into arcs in
+ * file order (ids minus base). On success *handle_out owns the arrays:
+ * spb_edge_list_fetch copies them into caller buffers of *m_out entries (w may
+ * be null) and releases the handle. SPB_ERR_PARSE with *bad_line_out = the
+ * first line (1-based) outside the accepted syntax or breaking a rule (field
+ * count, negative id after base, negative weight): the caller re-reads it with
+ * the reference's rules to raise the exact ParseError / DomainError. */
+SPB_API int spb_edge_list_parse(const char* data, size_t len, int32_t base, int32_t nthreads,
+                                int64_t* m_out, int64_t* max_idx_out, int32_t* has_weights_out,
+                                int64_t* bad_line_out, void** handle_out);
+SPB_API int spb_edge_list_fetch(void* handle, int64_t* src, int64_t* dst, double* w);
+SPB_API void spb_edge_list_free(void* handle);
 
 /* Optional k-means mode (north star (e); the reference has none, so parity is
  * unpinned): Lloyd iterations on the rows of x (n x d, dtype, row stride ldx),

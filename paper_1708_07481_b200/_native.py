@@ -20,7 +20,7 @@ from .errors import (
 
 LIB_PATH = Path(__file__).resolve().parent / "_lib" / "libspb200.so"
 
-OK, E_CONTRACT, E_DOMAIN, E_COND, E_SOLVER, E_SOLVER_NOSTATE, E_ASSIGN, E_CUDA, E_WS, E_CB = range(10)
+OK, E_CONTRACT, E_DOMAIN, E_COND, E_SOLVER, E_SOLVER_NOSTATE, E_ASSIGN, E_CUDA, E_WS, E_CB, E_PARSE = range(11)
 F32, F64 = 0, 1
 CSR_DIRECTED, CSR_SYMMETRIZED, CSR_AS_SYMMETRIC = 0, 1, 2
 OP_LAPLACIAN, OP_DENSE = 0, 1
@@ -81,6 +81,10 @@ _SIGS = {
     "spb_orthonormalize": (C.c_int, [C.c_int, vp, i64, i32, i32, REFILL_CB, vp, vp, sz, vp]),
     "spb_sygv_workspace": (sz, [i32]),
     "spb_sygv": (C.c_int, [vp, vp, i32, i32, vp, vp, vp, sz, vp]),
+    "spb_edge_list_parse": (C.c_int, [C.c_char_p, sz, i32, i32, C.POINTER(i64), C.POINTER(i64),
+                                      C.POINTER(i32), C.POINTER(i64), C.POINTER(vp)]),
+    "spb_edge_list_fetch": (C.c_int, [vp, vp, vp, vp]),
+    "spb_edge_list_free": (None, [vp]),
     "spb_kmeans_workspace": (sz, [i32, i32]),
     "spb_kmeans": (C.c_int, [C.c_int, vp, i64, i32, i32, i32, vp, i32, i32, vp, sz, vp, vp,
                              C.POINTER(i32), vp]),

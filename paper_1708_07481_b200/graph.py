@@ -237,56 +237,89 @@ def empty_graph(n: int = 0) -> SparseGraph:
     return SparseGraph(n, z, z.clone(), None)
 
 
-def load_edge_list(source, base: int = 1, num_vertices: int | None = None) -> SparseGraph:
-    """Tab-separated ``src dst [weight]`` reader (graph.py:152-209 semantics)."""
-    if base not in (0, 1):
-        raise DomainError("base must be 0 or 1")
-    close = False
+def _read_all(source) -> bytes:
     if isinstance(source, (str, Path)):
-        fh = open(source, "rb")
-        close = True
-    elif isinstance(source, bytes):
-        fh = io.BytesIO(source)
-    else:
-        fh = source
+        with open(source, "rb") as fh:
+            return fh.read()
+    if isinstance(source, (bytes, bytearray, memoryview)):
+        return bytes(source)
+    data = source.read()
+    return data.encode("utf-8") if isinstance(data, str) else bytes(data)
+
+
+def _parse_native(data: bytes, base: int, threads: int = 0):
+    """Native multithreaded parse (csrc/ingest.cu); None when a line needs the
+    reference's own rules (errors, or syntax outside the fast path)."""
+    L = N.lib()
+    m, mx, hw, bad = N.C.c_int64(0), N.C.c_int64(0), N.C.c_int32(0), N.C.c_int64(0)
+    h = N.C.c_void_p()
+    st = L.spb_edge_list_parse(data, len(data), base, threads, N.C.byref(m), N.C.byref(mx),
+                               N.C.byref(hw), N.C.byref(bad), N.C.byref(h))
+    if st == N.E_PARSE:
+        return None
+    N.check(st)
+    src = np.empty(m.value, dtype=np.int64)
+    dst = np.empty(m.value, dtype=np.int64)
+    w = np.empty(m.value, dtype=np.float64) if hw.value else None
+    N.check(L.spb_edge_list_fetch(h, src.ctypes.data, dst.ctypes.data,
+                                  w.ctypes.data if w is not None else None))
+    return src, dst, w, int(mx.value)
+
+
+def _parse_python(fh, base: int):
+    """The reference's line loop (graph.py:171-198): exact errors for any input."""
     src, dst, wts = [], [], []
     any_w = False
     max_idx = -1
-    try:
-        for line_no, raw in enumerate(fh, start=1):
-            if isinstance(raw, bytes):
-                raw = raw.decode("utf-8")
-            line = raw.strip()
-            if not line or line.startswith("#"):
-                continue
-            parts = line.split()
-            if len(parts) not in (2, 3):
-                raise ParseError(f"expected 2 or 3 fields, got {len(parts)}", line_no)
-            try:
-                u = int(parts[0]) - base
-                v = int(parts[1]) - base
-                w = float(parts[2]) if len(parts) == 3 else 1.0
-            except ValueError as exc:
-                raise ParseError(str(exc), line_no) from None
-            if u < 0 or v < 0:
-                raise ParseError(f"vertex index below base {base}", line_no)
-            if w < 0:
-                raise DomainError(f"line {line_no}: negative weight {w}")
-            any_w |= len(parts) == 3
-            src.append(u)
-            dst.append(v)
-            wts.append(w)
-            max_idx = max(max_idx, u, v)
-    finally:
-        if close:
-            fh.close()
+    for line_no, raw in enumerate(fh, start=1):
+        if isinstance(raw, bytes):
+            raw = raw.decode("utf-8")
+        line = raw.strip()
+        if not line or line.startswith("#"):
+            continue
+        parts = line.split()
+        if len(parts) not in (2, 3):
+            raise ParseError(f"expected 2 or 3 fields, got {len(parts)}", line_no)
+        try:
+            u = int(parts[0]) - base
+            v = int(parts[1]) - base
+            w = float(parts[2]) if len(parts) == 3 else 1.0
+        except ValueError as exc:
+            raise ParseError(str(exc), line_no) from None
+        if u < 0 or v < 0:
+            raise ParseError(f"vertex index below base {base}", line_no)
+        if w < 0:
+            raise DomainError(f"line {line_no}: negative weight {w}")
+        any_w |= len(parts) == 3
+        src.append(u)
+        dst.append(v)
+        wts.append(w)
+        max_idx = max(max_idx, u, v)
+    return (np.asarray(src, dtype=np.int64), np.asarray(dst, dtype=np.int64),
+            np.asarray(wts, dtype=np.float64) if (wts and any_w) else None, max_idx)
+
+
+def load_edge_list(source, base: int = 1, num_vertices: int | None = None) -> SparseGraph:
+    """Tab-separated ``src dst [weight]`` reader (graph.py:152-209 semantics).
+
+    Parsed by the native multithreaded reader; a file containing a line it does
+    not accept is re-read with the reference's loop, which raises the same
+    ParseError / DomainError (with line number) the reference raises.
+    """
+    if base not in (0, 1):
+        raise DomainError("base must be 0 or 1")
+    data = _read_all(source)
+    parsed = _parse_native(data, base)
+    if parsed is None:
+        parsed = _parse_python(io.BytesIO(data), base)
+    src, dst, w, max_idx = parsed
     n = max_idx + 1
     if num_vertices is not None:
         if num_vertices < n:
             raise DomainError(f"num_vertices={num_vertices} below max index {max_idx}")
         n = num_vertices
-    edges = np.column_stack([src, dst]) if src else np.empty((0, 2), dtype=np.int64)
-    return from_edges(edges, n, weights=np.asarray(wts) if (wts and any_w) else None)
+    edges = np.column_stack([src, dst]) if src.size else np.empty((0, 2), dtype=np.int64)
+    return from_edges(edges, n, weights=w if src.size else None)
 
 
 def write_edge_list(g: SparseGraph, path, base: int = 1) -> None:

@@ -94,3 +94,29 @@ def test_apply_delta_matches_bulk(spb):
     assert np.array_equal(g.col_indices, h.col_indices)
     assert np.allclose(g.weights, h.weights)
     assert spb.degrees(g).tolist() == [4.0, 3.0, 2.0, 1.0]
+
+
+def test_load_edge_list_native_matches_from_edges(spb, tmp_path):
+    spec, edges, _ = config_input("c1", seed=0)
+    rng = np.random.default_rng(5)
+    # integer-valued weights: duplicate sums are exact in any order (the reference's
+    # order of summing duplicates is scipy's unstable per-row sort)
+    w = rng.integers(1, 5, len(edges)).astype(np.float64)
+    path = tmp_path / "c1.tsv"
+    with open(path, "w") as fh:
+        fh.write("# DC-SBM c1\n")
+        for (a, b), x in zip(edges, w):
+            fh.write(f"{a + 1}\t{b + 1}\t{float(x)!r}\n")
+    g = spb.load_edge_list(path, base=1, num_vertices=spec.n)
+    dref = oracle.directed_csr(edges, spec.n, w)
+    assert np.array_equal(g.row_offsets, dref[0]) and np.array_equal(g.col_indices, dref[1])
+    assert np.array_equal(g.weights, dref[2])
+    ref = oracle.symmetrize_csr(*dref, spec.n)
+    sym = spb.symmetrize(g)
+    assert np.array_equal(sym.row_offsets, ref[0]) and np.array_equal(sym.col_indices, ref[1])
+    assert np.array_equal(sym.weights, ref[2])
+    # errors keep the reference's types and line numbers
+    bad = tmp_path / "bad.tsv"
+    bad.write_text("1 2\n2 3\n3 x\n")
+    with pytest.raises(spb.ParseError, match="line 3"):
+        spb.load_edge_list(bad)
