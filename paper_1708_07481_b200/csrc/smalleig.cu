@@ -948,10 +948,20 @@ void launch_tridiag(const double* Asrc, int m, int symmetrize, double* Wg, doubl
 }
 
 // One warp per eigenvalue index (first + t): 33-section of the Gershgorin interval.
+// d and e^2 are staged in shared memory once per CTA (dynamic, 2m doubles); the
+// Sturm count is the LDL' pivot recurrence of dstebz.
 __global__ void bisect(const double* __restrict__ d, const double* __restrict__ e, int m,
-                       int first, int count, double* __restrict__ theta, double* __restrict__ e2,
-                       const SmallStatus* status) {
+                       int first, int count, double* __restrict__ theta, double* __restrict__ e2unused,
+                       const SmallStatus* status, int use_div) {
+  extern __shared__ double bsd[];  // d[m], e2[m]
   if (status && (status->nonfinite || status->not_pd)) return;
+  double* sd = bsd;
+  double* se2 = bsd + m;
+  for (int i = threadIdx.x; i < m; i += blockDim.x) {
+    sd[i] = d[i];
+    se2[i] = i + 1 < m ? e[i] * e[i] : 0.0;
+  }
+  __syncthreads();
   const int lane = threadIdx.x & 31;
   const int t = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   if (t >= count) return;
@@ -959,9 +969,9 @@ __global__ void bisect(const double* __restrict__ d, const double* __restrict__ 
   double lo = DBL_MAX, hi = -DBL_MAX, emax = 0.0;
   for (int i = lane; i < m; i += 32) {
     const double r = (i > 0 ? fabs(e[i - 1]) : 0.0) + (i + 1 < m ? fabs(e[i]) : 0.0);
-    lo = fmin(lo, d[i] - r);
-    hi = fmax(hi, d[i] + r);
-    if (i + 1 < m) emax = fmax(emax, e[i] * e[i]);
+    lo = fmin(lo, sd[i] - r);
+    hi = fmax(hi, sd[i] + r);
+    if (i + 1 < m) emax = fmax(emax, se2[i]);
   }
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) {
@@ -973,20 +983,17 @@ __global__ void bisect(const double* __restrict__ d, const double* __restrict__ 
   const double tnorm = fmax(fabs(lo), fabs(hi));
   lo -= 2.0 * kEps64 * tnorm + 2.0 * pivmin;
   hi += 2.0 * kEps64 * tnorm + 2.0 * pivmin;
-  // e2 computed per warp into a private view (all warps write identical values)
   double a = lo, b = hi;
   for (int round = 0; round < 64; ++round) {
     const double w = b - a;
     const double tol = fmax(2.0 * kEps64 * fmax(fabs(a), fabs(b)), kEps64 * tnorm) + pivmin;
     if (w <= tol) break;
     const double x = a + w * (double)(lane + 1) / 33.0;
-    // Sturm count with e^2 on the fly
-    double q = d[0] - x;
+    double q = sd[0] - x;
     if (fabs(q) < pivmin) q = -pivmin;
     int c = q < 0.0;
     for (int i = 1; i < m; ++i) {
-      const double ei = e[i - 1];
-      q = d[i] - x - (ei * ei) / q;
+      q = use_div ? (sd[i] - x) - se2[i - 1] / q : (sd[i] - x) - se2[i - 1] * __drcp_rn(q);
       if (fabs(q) < pivmin) q = -pivmin;
       c += q < 0.0;
     }
@@ -1002,8 +1009,15 @@ __global__ void bisect(const double* __restrict__ d, const double* __restrict__ 
       if (f > 0) a = xp;
     }
   }
-  (void)e2;
   if (lane == 0) theta[t] = 0.5 * (a + b);
+}
+
+// Sturm pivots by true division (dstebz's arithmetic) unless SPB_BISECT_RCP is
+// set: the reciprocal variant is faster but its last-bit differences measurably
+// change long LOBPCG trajectories (tests/test_gpu_lobpcg.py rand150).
+int bisect_div() {
+  static const int v = getenv("SPB_BISECT_RCP") ? 0 : 1;
+  return v;
 }
 
 __device__ __forceinline__ double hash_uniform(uint32_t a, uint32_t b) {
@@ -1134,83 +1148,144 @@ __global__ void invit(const double* __restrict__ d, const double* __restrict__ e
 
 // Z = Q Y with Q = H_0 H_1 ... H_{m-3}, applied in blocks of 32 reflectors
 // (compact WY, as LAPACK dormtr/dlarft): B_b = I - V_b T_b V_b', Z = B_0 (B_1 (... (B_last Y))).
-// Per block: G = V_b'V_b, T_b by the forward column recurrence (one warp),
-// W = T_b (V_b' Y), Y -= V_b W  -> four CTA barriers per 32 reflectors.
-__global__ void __launch_bounds__(ET)
-backtransform(const double* __restrict__ V, const double* __restrict__ tau, int m, double* Y,
-              int ldy, int nev, const SmallStatus* status) {
-  extern __shared__ double bsm[];  // W1 [32][nev], W2 [32][nev]
+// wy_tfactors: one CTA per block stages V_b in shared memory and forms
+// G = V_b'V_b and T_b (forward column recurrence), all blocks at once.
+// wy_apply: the columns of Y are independent, so each CTA owns BCW of them in
+// shared memory and runs the block loop W1 = V_b' Y, W2 = T_b W1, Y -= V_b W2
+// with V_b staged per block.
+constexpr int BCW = 8;     // Y columns per CTA
+constexpr int BAT = 256;   // threads of wy_apply (= 32 reflectors x BCW columns)
+
+__global__ void __launch_bounds__(256)
+wy_tfactors(const double* __restrict__ V, const double* __restrict__ tau, int m,
+            double* __restrict__ Tall, const SmallStatus* status) {
+  extern __shared__ double tvb[];  // V_b rows [32][m | 1]
   __shared__ double G[32][33];
   __shared__ double Tm[32][33];
   if (status && (status->nonfinite || status->not_pd)) return;
-  double* W1 = bsm;
-  double* W2 = bsm + 32 * (size_t)nev;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int nrefl = m - 2;
-  if (nrefl <= 0) return;
+  const int kb = blockIdx.x * 32;
+  const int nb = min(32, nrefl - kb);
+  const int r0 = kb + 1;
+  const int vld = m | 1;
+  for (int x = tid; x < nb * m; x += 256) {
+    const int j = x / m, r = x - (x / m) * m;
+    tvb[j * vld + r] = V[(size_t)(kb + j) * m + r];
+  }
+  __syncthreads();
+  for (int x = warp; x < nb * nb; x += 8) {
+    const int i = x / nb, j = x % nb;
+    double acc = 0.0;
+    if (i <= j) {
+      const double* vi = tvb + i * vld;
+      const double* vj = tvb + j * vld;
+      for (int r = r0 + lane; r < m; r += 32) acc += vi[r] * vj[r];
+      acc = warp_sum(acc);
+    }
+    if (lane == 0) G[i][j] = acc;
+  }
+  __syncthreads();
+  if (warp == 0) {
+    for (int j = 0; j < nb; ++j) {
+      const double tj = tau[kb + j];
+      double x = 0.0;
+      if (lane < j) {
+        for (int q = lane; q < j; ++q) x += Tm[lane][q] * G[q][j];
+        x = -tj * x;
+      }
+      __syncwarp();
+      if (lane < j) Tm[lane][j] = x;
+      if (lane == j) Tm[j][j] = tj;
+      if (lane > j) Tm[lane][j] = 0.0;
+      __syncwarp();
+    }
+  }
+  __syncthreads();
+  double* T = Tall + (size_t)blockIdx.x * 1024;
+  for (int x = tid; x < 1024; x += 256) {
+    const int i = x >> 5, j = x & 31;
+    T[x] = (i < nb && j < nb) ? Tm[i][j] : 0.0;
+  }
+}
+
+__global__ void __launch_bounds__(BAT)
+wy_apply(const double* __restrict__ V, int m, const double* __restrict__ Tall, double* Y,
+         int ldy, int nev, const SmallStatus* status) {
+  extern __shared__ double wsm[];
+  if (status && (status->nonfinite || status->not_pd)) return;
+  const int vld = m | 1;                       // odd row stride: conflict-free column reads
+  double* Ys = wsm;                            // [m][BCW]
+  double* Vb = Ys + (size_t)m * BCW;           // [32][vld]
+  double* W1 = Vb + 32 * (size_t)vld;          // [32][BCW]
+  double* W2 = W1 + 32 * BCW;                  // [32][BCW]
+  double* Tb = W2 + 32 * BCW;                  // [32][33]
+  const int tid = threadIdx.x;
+  const int c0 = blockIdx.x * BCW;
+  const int nc = min(BCW, nev - c0);
+  for (int x = tid; x < m * BCW; x += BAT) {
+    const int r = x / BCW, c = x % BCW;
+    Ys[x] = c < nc ? Y[(size_t)r * ldy + c0 + c] : 0.0;
+  }
+  const int nrefl = m - 2;
+  const int jj = tid / BCW, cc = tid % BCW;  // (reflector, column) of this thread
   for (int kb = ((nrefl - 1) / 32) * 32; kb >= 0; kb -= 32) {
     const int nb = min(32, nrefl - kb);
-    const int r0 = kb + 1;  // first row touched by the block
-    // (1) G = V_b' V_b (upper part used)
-    for (int x = warp; x < nb * nb; x += ET / 32) {
-      const int i = x / nb, j = x % nb;
+    const double* T = Tall + (size_t)(kb / 32) * 1024;
+    for (int x = tid; x < nb * m; x += BAT) {
+      const int j = x / m, r = x - (x / m) * m;
+      Vb[j * vld + r] = V[(size_t)(kb + j) * m + r];
+    }
+    for (int x = tid; x < 1024; x += BAT) Tb[(x >> 5) * 33 + (x & 31)] = T[x];
+    __syncthreads();
+    // W1 = V_b' Y (v_{kb+j}[r] = 0 for r <= kb + j)
+    if (jj < nb) {
+      double a0 = 0.0, a1 = 0.0;
+      const double* vr = Vb + jj * vld;
+      int r = kb + jj + 1;
+      for (; r + 1 < m; r += 2) {
+        a0 = fma(vr[r], Ys[r * BCW + cc], a0);
+        a1 = fma(vr[r + 1], Ys[(r + 1) * BCW + cc], a1);
+      }
+      if (r < m) a0 = fma(vr[r], Ys[r * BCW + cc], a0);
+      W1[jj * BCW + cc] = a0 + a1;
+    }
+    __syncthreads();
+    // W2 = T_b W1 (upper triangular)
+    if (jj < nb) {
       double acc = 0.0;
-      if (i <= j) {
-        const double* vi = V + (size_t)(kb + i) * m;
-        const double* vj = V + (size_t)(kb + j) * m;
-        for (int r = r0 + lane; r < m; r += 32) acc += vi[r] * vj[r];
-        acc = warp_sum(acc);
-      }
-      if (lane == 0) G[i][j] = acc;
+      for (int q = jj; q < nb; ++q) acc = fma(Tb[jj * 33 + q], W1[q * BCW + cc], acc);
+      W2[jj * BCW + cc] = acc;
     }
     __syncthreads();
-    // (2) T (forward, columnwise): T[j][j] = tau_j; T[0:j, j] = -tau_j T[0:j,0:j] G[0:j, j]
-    if (warp == 0) {
-      for (int j = 0; j < nb; ++j) {
-        const double tj = tau[kb + j];
-        double x = 0.0;
-        if (lane < j) {
-          for (int q = lane; q < j; ++q) x += Tm[lane][q] * G[q][j];
-          x = -tj * x;
-        }
-        __syncwarp();
-        if (lane < j) Tm[lane][j] = x;
-        if (lane == j) Tm[j][j] = tj;
-        if (lane > j && lane < 32) Tm[lane][j] = 0.0;
-        __syncwarp();
-      }
-    }
-    // (3) W1 = V_b' Y  (warp j, lanes over columns)
-    for (int j = warp; j < nb; j += ET / 32) {
-      const double* vj = V + (size_t)(kb + j) * m;
-      for (int c0 = 0; c0 < nev; c0 += 32) {
-        const int c = c0 + lane;
-        double acc = 0.0;
-        if (c < nev)
-          for (int r = kb + j + 1; r < m; ++r) acc += vj[r] * Y[(size_t)r * ldy + c];
-        if (c < nev) W1[(size_t)j * nev + c] = acc;
-      }
-    }
-    __syncthreads();
-    // (4) W2 = T W1
-    for (int j = warp; j < nb; j += ET / 32)
-      for (int c = lane; c < nev; c += 32) {
-        double acc = 0.0;
-        for (int q = j; q < nb; ++q) acc += Tm[j][q] * W1[(size_t)q * nev + c];
-        W2[(size_t)j * nev + c] = acc;
-      }
-    __syncthreads();
-    // (5) Y -= V_b W2
-    for (int r = r0 + warp; r < m; r += ET / 32) {
-      const int jmax = min(nb, r - kb);  // v_{kb+j}[r] = 0 for r <= kb + j
-      for (int c = lane; c < nev; c += 32) {
-        double acc = 0.0;
-        for (int j = 0; j < jmax; ++j) acc += V[(size_t)(kb + j) * m + r] * W2[(size_t)j * nev + c];
-        Y[(size_t)r * ldy + c] -= acc;
-      }
+    // Y -= V_b W2
+    for (int x = tid; x < (m - kb - 1) * BCW; x += BAT) {
+      const int r = kb + 1 + x / BCW, c = x % BCW;
+      const int jmax = min(nb, r - kb);
+      double acc = 0.0;
+      for (int j = 0; j < jmax; ++j) acc = fma(Vb[j * vld + r], W2[j * BCW + c], acc);
+      Ys[r * BCW + c] -= acc;
     }
     __syncthreads();
   }
+  for (int x = tid; x < m * BCW; x += BAT) {
+    const int r = x / BCW, c = x % BCW;
+    if (c < nc) Y[(size_t)r * ldy + c0 + c] = Ys[x];
+  }
+}
+
+size_t wy_apply_smem(int m) {
+  return sizeof(double) * ((size_t)m * BCW + 32 * (size_t)(m | 1) + 64 * BCW + 32 * 33);
+}
+
+void launch_backtransform(const double* V, const double* tau, int m, double* Y, int nev,
+                          double* Tscratch, const SmallStatus* status, cudaStream_t st) {
+  const int nrefl = m - 2;
+  if (nrefl <= 0 || nev <= 0) return;
+  const int nblk = (nrefl + 31) / 32;
+  wy_tfactors<<<nblk, 256, sizeof(double) * 32 * (size_t)(m | 1), st>>>(V, tau, m, Tscratch, status);
+  wy_apply<<<(nev + BCW - 1) / BCW, BAT, wy_apply_smem(m), st>>>(V, m, Tscratch, Y, nev, nev,
+                                                                  status);
 }
 
 __global__ void copy_cols(const double* __restrict__ Y, int ldy, int m, int nev,
@@ -1501,7 +1576,8 @@ int set_smem_attrs() {
   SPB_CUDA(cudaFuncSetAttribute(tridiag<5>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
   SPB_CUDA(cudaFuncSetAttribute(tridiag<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
   SPB_CUDA(cudaFuncSetAttribute(invit, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-  SPB_CUDA(cudaFuncSetAttribute(backtransform, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+  SPB_CUDA(cudaFuncSetAttribute(wy_apply, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
+  SPB_CUDA(cudaFuncSetAttribute(wy_tfactors, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
   done = true;
   return SPB_OK;
 }
@@ -1511,8 +1587,8 @@ int tri_eigs(const double* Asrc, int m, int symmetrize, const SygvWs& w, int fir
   launch_tridiag(Asrc, m, symmetrize, w.W, w.V, w.tau, w.d, w.e, status, tridiag_smem(m), st);
   SPB_LAUNCH_CHECK();
   const int warps = 8;
-  bisect<<<(int)ceil_div(count, warps), warps * 32, 0, st>>>(w.d, w.e, m, first, count, theta,
-                                                             nullptr, status);
+  bisect<<<(int)ceil_div(count, warps), warps * 32, 2 * sizeof(double) * (size_t)m, st>>>(
+      w.d, w.e, m, first, count, theta, nullptr, status, bisect_div());
   SPB_LAUNCH_CHECK();
   return SPB_OK;
 }
@@ -1559,8 +1635,7 @@ int sygv_enqueue(const double* ga, const double* gb, int ldg, int m, int nev, do
     }
   }
   SPB_LAUNCH_CHECK();
-  backtransform<<<1, ET, 2 * 32 * sizeof(double) * (size_t)nev, st>>>(w.V, w.tau, m, w.Y, nev,
-                                                                     nev, status);
+  launch_backtransform(w.V, w.tau, m, w.Y, nev, w.scratch, status, st);
   SPB_LAUNCH_CHECK();
   if (!ident) {
     dim3 grid((unsigned)ceil_div(nev, 32), (unsigned)ceil_div(m, 32));
@@ -1584,8 +1659,10 @@ int exact_cond_spd(const double* gb, int ldg, int m, double* ws, size_t ws_doubl
   const int g1 = (int)std::min<int64_t>(ceil_div((int64_t)m * m, 256), 1024);
   sym_prep<<<g1, 256, 0, st>>>(gb, nullptr, ldg, m, w.A, nullptr, nullptr, seg1, seg2);
   launch_tridiag(w.A, m, 0, w.W, w.V, w.tau, w.d, w.e, nullptr, tridiag_smem(m), st);
-  bisect<<<1, 32, 0, st>>>(w.d, w.e, m, 0, 1, ext, nullptr, nullptr);
-  bisect<<<1, 32, 0, st>>>(w.d, w.e, m, m - 1, 1, ext + 1, nullptr, nullptr);
+  bisect<<<1, 32, 2 * sizeof(double) * (size_t)m, st>>>(w.d, w.e, m, 0, 1, ext, nullptr, nullptr,
+                                                          bisect_div());
+  bisect<<<1, 32, 2 * sizeof(double) * (size_t)m, st>>>(w.d, w.e, m, m - 1, 1, ext + 1, nullptr,
+                                                          nullptr, bisect_div());
   SPB_LAUNCH_CHECK();
   double h[2];
   SPB_CUDA(cudaMemcpyAsync(h, ext, sizeof(h), cudaMemcpyDeviceToHost, st));

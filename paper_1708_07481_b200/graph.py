@@ -222,6 +222,17 @@ def from_edges(edges, n: int, weights=None, *, symmetric: bool = False) -> Spars
         w = None if weights is None else torch.as_tensor(weights, dtype=torch.float64, device=_device())
         if w is not None and w.numel() and bool((w < 0).any()):
             raise DomainError("negative edge weight")
+    elif (weights is None and isinstance(edges, np.ndarray) and edges.ndim == 2
+          and edges.shape[1] == 2 and edges.dtype == np.int64 and edges.flags.c_contiguous
+          and edges.shape[0] > 0):
+        # fast path: one (pinned) H2D copy of the arc block, columns split on the
+        # device; the endpoint range check happens in the CSR build's validation
+        # pass (same DomainError)
+        t = torch.from_numpy(edges)
+        if t.numel() * 8 >= (1 << 20) and torch.cuda.is_available() and not t.is_pinned():
+            t = t.pin_memory()
+        dev = t.to(device=_device(), non_blocking=True)
+        src, dst, w = dev[:, 0].contiguous(), dev[:, 1].contiguous(), None
     else:
         hs, hd, hw = _coerce_edges(edges, weights)
         if hs.size and (min(hs.min(), hd.min()) < 0 or max(hs.max(), hd.max()) >= n):

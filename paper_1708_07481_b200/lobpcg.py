@@ -247,7 +247,7 @@ def _x0_device(x0, n, l):
         return t.contiguous()
     arr = np.ascontiguousarray(x0, dtype=np.float64)
     t = torch.from_numpy(arr)
-    if arr.nbytes >= (1 << 20):
+    if arr.nbytes >= (1 << 20) and not t.is_pinned():
         t = t.pin_memory()
     return t.to(_device(), non_blocking=True)
 

@@ -1,0 +1,47 @@
+"""cProfile of the public-API end-to-end call (host arcs + x0 -> host labels).
+
+    python tools/e2e_profile.py [--config c2]
+"""
+import argparse
+import cProfile
+import pstats
+import sys
+import time
+from pathlib import Path
+
+import numpy as np
+import torch
+
+sys.path.insert(0, str(Path(__file__).resolve().parent.parent))
+import paper_1708_07481_b200 as spb  # noqa: E402
+from paper_1708_07481_b200.dcsbm import CONFIGS, generate_dcsbm  # noqa: E402
+
+ap = argparse.ArgumentParser()
+ap.add_argument("--config", default="c2")
+ap.add_argument("--iters", type=int, default=20)
+a = ap.parse_args()
+spec = CONFIGS[a.config]
+edges, _ = generate_dcsbm(spec)
+k = spec.blocks
+l = spb.block_size_for(k)
+x0 = np.random.default_rng(0).standard_normal((spec.n, l))
+edges_pinned = torch.from_numpy(np.ascontiguousarray(edges)).pin_memory().numpy()
+cfg = spb.SolverConfig(block_size=l, tol=1e-12, max_iter=a.iters, seed=0)
+
+
+def step():
+    g = spb.from_edges(edges_pinned, spec.n)
+    part, st, gap = spb.partition_static(g, cfg, k, fix_k=True, x0=x0)
+    torch.cuda.synchronize()
+    return part
+
+
+step()
+t0 = time.perf_counter()
+step()
+print(f"e2e wall {1e3 * (time.perf_counter() - t0):.1f} ms")
+pr = cProfile.Profile()
+pr.enable()
+step()
+pr.disable()
+pstats.Stats(pr).sort_stats("tottime").print_stats(15)
