@@ -1535,10 +1535,15 @@ size_t tridiag_smem(int m) {
 void launch_chol(const double* B, int m, double* L, double* Linv, int mode, SmallStatus* status,
                  cudaStream_t st) {
   static const bool old = getenv("SPB_CHOL_BLOCKED") != nullptr;  // A/B switch
-  if (!old && m <= kCholLdlMax && chol_ldl_smem(m) <= 224 * 1024) {
+  static const int cmin = getenv("SPB_CHOL_CLUSTER_MIN") ? atoi(getenv("SPB_CHOL_CLUSTER_MIN"))
+                                                         : kCholLdlMax + 1;
+  static const int cfix = getenv("SPB_CHOL_CLUSTER_C") ? atoi(getenv("SPB_CHOL_CLUSTER_C")) : 0;
+  if (!old && m < cmin && m <= kCholLdlMax && chol_ldl_smem(m) <= 224 * 1024) {
     chol_ldl<<<1, ET, chol_ldl_smem(m), st>>>(B, m, L, Linv, mode, status);
   } else if (!old && m <= kCholClusterMax) {
-    const int C = m <= 400 ? 8 : 16;
+    int C = m <= 400 ? 8 : 16;
+    if ((cfix == 2 || cfix == 4 || cfix == 8 || cfix == 16) && (m + cfix - 1) / cfix * 8 <= CCT)
+      C = cfix;
     static bool attr = false;
     if (!attr) {
       cudaFuncSetAttribute(chol_cluster, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);

@@ -1,0 +1,100 @@
+// Latency microbenchmarks for the single-CTA / cluster kernels' building blocks.
+//   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o /tmp/lat latency.cu && /tmp/lat
+#include <cstdio>
+#include <cuda_runtime.h>
+
+__global__ void k_sync(int iters, long long* out) {
+  long long t0 = clock64();
+  for (int i = 0; i < iters; ++i) __syncthreads();
+  long long t1 = clock64();
+  if (threadIdx.x == 0) out[0] = (t1 - t0) / iters;
+}
+
+__global__ void k_ddiv(int iters, double x, long long* out, double* sink) {
+  double a = x;
+  long long t0 = clock64();
+  for (int i = 0; i < iters; ++i) a = 1.0 / (a + 1.0);
+  long long t1 = clock64();
+  if (threadIdx.x == 0) { out[0] = (t1 - t0) / iters; sink[0] = a; }
+}
+
+__global__ void k_drcp(int iters, double x, long long* out, double* sink) {
+  double a = x;
+  long long t0 = clock64();
+  for (int i = 0; i < iters; ++i) a = __drcp_rn(a + 1.0);
+  long long t1 = clock64();
+  if (threadIdx.x == 0) { out[0] = (t1 - t0) / iters; sink[0] = a; }
+}
+
+__global__ void k_dsqrt(int iters, double x, long long* out, double* sink) {
+  double a = x;
+  long long t0 = clock64();
+  for (int i = 0; i < iters; ++i) a = sqrt(a + 1.0);
+  long long t1 = clock64();
+  if (threadIdx.x == 0) { out[0] = (t1 - t0) / iters; sink[0] = a; }
+}
+
+__global__ void k_smem_chain(int iters, long long* out) {
+  __shared__ double s[1024];
+  s[threadIdx.x] = threadIdx.x;
+  __syncthreads();
+  int idx = threadIdx.x;
+  long long t0 = clock64();
+  for (int i = 0; i < iters; ++i) {
+    double v = s[idx];
+    s[idx] = v * 1.0000001 + 1.0;
+    idx = (idx + 33) & 1023;
+  }
+  long long t1 = clock64();
+  if (threadIdx.x == 0) out[0] = (t1 - t0) / iters;
+}
+
+__global__ void k_cluster(int iters, long long* out) {
+  long long t0 = clock64();
+  for (int i = 0; i < iters; ++i)
+    asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;\n" ::: "memory");
+  long long t1 = clock64();
+  unsigned r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;\n" : "=r"(r));
+  if (threadIdx.x == 0 && r == 0) out[0] = (t1 - t0) / iters;
+}
+
+int main() {
+  long long* d;
+  double* sink;
+  cudaMalloc(&d, 64);
+  cudaMalloc(&sink, 64);
+  long long h;
+  int clk;
+  cudaDeviceGetAttribute(&clk, cudaDevAttrClockRate, 0);
+  printf("clock rate attr %d kHz\n", clk);
+  for (int nt : {64, 256, 512, 1024}) {
+    k_sync<<<1, nt>>>(10000, d);
+    cudaMemcpy(&h, d, 8, cudaMemcpyDeviceToHost);
+    printf("__syncthreads %4d threads: %lld cycles\n", nt, h);
+  }
+  k_ddiv<<<1, 32>>>(10000, 0.5, d, sink); cudaMemcpy(&h, d, 8, cudaMemcpyDeviceToHost); printf("dependent 1/x (DDIV): %lld cycles\n", h);
+  k_drcp<<<1, 32>>>(10000, 0.5, d, sink); cudaMemcpy(&h, d, 8, cudaMemcpyDeviceToHost); printf("dependent __drcp_rn: %lld cycles\n", h);
+  k_dsqrt<<<1, 32>>>(10000, 0.5, d, sink); cudaMemcpy(&h, d, 8, cudaMemcpyDeviceToHost); printf("dependent sqrt: %lld cycles\n", h);
+  for (int nt : {32, 1024}) {
+    k_smem_chain<<<1, nt>>>(10000, d); cudaMemcpy(&h, d, 8, cudaMemcpyDeviceToHost);
+    printf("smem load->fma->store chain (%d thr): %lld cycles\n", nt, h);
+  }
+  for (int C : {2, 4, 8, 16}) {
+    cudaFuncSetAttribute(k_cluster, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    for (int nt : {256, 512}) {
+      cudaLaunchConfig_t cfg = {};
+      cfg.gridDim = dim3(C);
+      cfg.blockDim = dim3(nt);
+      cudaLaunchAttribute at[1];
+      at[0].id = cudaLaunchAttributeClusterDimension;
+      at[0].val.clusterDim.x = C; at[0].val.clusterDim.y = 1; at[0].val.clusterDim.z = 1;
+      cfg.attrs = at; cfg.numAttrs = 1;
+      cudaError_t e = cudaLaunchKernelEx(&cfg, k_cluster, 10000, d);
+      cudaDeviceSynchronize();
+      cudaMemcpy(&h, d, 8, cudaMemcpyDeviceToHost);
+      printf("cluster barrier C=%2d %d thr: %lld cycles (%s)\n", C, nt, h, cudaGetErrorString(e));
+    }
+  }
+  return 0;
+}
