@@ -235,6 +235,12 @@ SPB_API int spb_edge_list_parse(const char* data, size_t len, int32_t base, int3
 SPB_API int spb_edge_list_fetch(void* handle, int64_t* src, int64_t* dst, double* w);
 SPB_API void spb_edge_list_free(void* handle);
 
+/* (f.4) Contingency table of two device label arrays (int32, values in
+ * [0, kt) and [0, kf)) into device int64 counts[kt * kf] (metrics.py:65-75).
+ * ws: >= 4 bytes of device scratch. SPB_ERR_CONTRACT for a label outside range. */
+SPB_API int spb_contingency(const int32_t* truth, const int32_t* found, int64_t n, int32_t kt,
+                            int32_t kf, int64_t* counts, void* ws, size_t ws_bytes, void* stream);
+
 /* Optional k-means mode (north star (e); the reference has none, so parity is
  * unpinned): Lloyd iterations on the rows of x (n x d, dtype, row stride ldx),
  * optionally row-normalised, from the rows ``seeds`` (device int32[k], e.g.

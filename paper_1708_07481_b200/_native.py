@@ -85,6 +85,7 @@ _SIGS = {
                                       C.POINTER(i32), C.POINTER(i64), C.POINTER(vp)]),
     "spb_edge_list_fetch": (C.c_int, [vp, vp, vp, vp]),
     "spb_edge_list_free": (None, [vp]),
+    "spb_contingency": (C.c_int, [vp, vp, i64, i32, i32, vp, vp, sz, vp]),
     "spb_kmeans_workspace": (sz, [i32, i32]),
     "spb_kmeans": (C.c_int, [C.c_int, vp, i64, i32, i32, i32, vp, i32, i32, vp, sz, vp, vp,
                              C.POINTER(i32), vp]),

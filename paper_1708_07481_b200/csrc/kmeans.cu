@@ -210,3 +210,70 @@ extern "C" int spb_kmeans(int dtype, const void* x, int64_t ldx, int32_t n, int3
   *iterations_out = it;
   return s;
 }
+
+// ---------------------------------------------------------------------------
+// (f.4) Contingency table on the device (metrics.py:65-75): counts[t * kf + f]
+// of (truth, found) label pairs, a shared-memory histogram per CTA when the
+// table fits (integer atomics: order-independent, so deterministic), global
+// 64-bit atomics otherwise.
+namespace spb {
+namespace {
+__global__ void contingency_kernel(const int32_t* __restrict__ t, const int32_t* __restrict__ f,
+                                   int64_t n, int kt, int kf, unsigned long long* __restrict__ counts,
+                                   int use_smem, int* __restrict__ bad) {
+  extern __shared__ unsigned int hist[];
+  const int cells = kt * kf;
+  if (use_smem) {
+    for (int x = threadIdx.x; x < cells; x += blockDim.x) hist[x] = 0u;
+    __syncthreads();
+  }
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int a = t[i], b = f[i];
+    if (a < 0 || a >= kt || b < 0 || b >= kf) {
+      atomicOr(bad, 1);
+      continue;
+    }
+    if (use_smem) atomicAdd(&hist[a * kf + b], 1u);
+    else atomicAdd(&counts[(int64_t)a * kf + b], 1ull);
+  }
+  if (use_smem) {
+    __syncthreads();
+    for (int x = threadIdx.x; x < cells; x += blockDim.x)
+      if (hist[x]) atomicAdd(&counts[x], (unsigned long long)hist[x]);
+  }
+}
+}  // namespace
+}  // namespace spb
+
+extern "C" int spb_contingency(const int32_t* truth, const int32_t* found, int64_t n, int32_t kt,
+                               int32_t kf, int64_t* counts, void* ws, size_t ws_bytes,
+                               void* stream) {
+  if (n < 0 || kt < 1 || kf < 1) {
+    set_error("contingency needs n >= 0 and label ranges >= 1");
+    return SPB_ERR_CONTRACT;
+  }
+  if (ws_bytes < sizeof(int) || !ws) {
+    set_error("contingency workspace too small");
+    return SPB_ERR_WORKSPACE;
+  }
+  cudaStream_t st = (cudaStream_t)stream;
+  int* bad = (int*)ws;
+  SPB_CUDA(cudaMemsetAsync(counts, 0, sizeof(int64_t) * (size_t)kt * kf, st));
+  SPB_CUDA(cudaMemsetAsync(bad, 0, sizeof(int), st));
+  const size_t smem = sizeof(unsigned int) * (size_t)kt * kf;
+  const int use_smem = smem <= 48 * 1024;
+  const int blocks = (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(std::max<int64_t>(n, 1), 1024),
+                                                                 4 * num_sms()));
+  contingency_kernel<<<blocks, 256, use_smem ? smem : 0, st>>>(
+      truth, found, n, kt, kf, (unsigned long long*)counts, use_smem, bad);
+  SPB_LAUNCH_CHECK();
+  int hb = 0;
+  SPB_CUDA(cudaMemcpyAsync(&hb, bad, sizeof(int), cudaMemcpyDeviceToHost, st));
+  SPB_CUDA(cudaStreamSynchronize(st));
+  if (hb) {
+    set_error("label outside [0, k)");
+    return SPB_ERR_CONTRACT;
+  }
+  return SPB_OK;
+}

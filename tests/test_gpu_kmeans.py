@@ -84,3 +84,20 @@ def test_kmeans_contract_errors():
         spb.assign_clusters_kmeans(np.zeros((3, 2)), 4)
     with pytest.raises(spb.ContractError):
         spb.assign_clusters_kmeans(np.zeros((10, 2)), 3)  # k > width with default seeds
+
+
+def test_contingency_device_matches_host():
+    import torch
+
+    import paper_1708_07481_b200 as spb
+    from paper_1708_07481_b200.metrics import contingency_device
+
+    rng = np.random.default_rng(3)
+    for n, kt, kf in [(1000, 5, 7), (200_000, 44, 44), (50_000, 160, 300)]:
+        t = rng.integers(0, kt, n)
+        f = rng.integers(0, kf, n)
+        t[0], f[0] = kt - 1, kf - 1
+        dev = contingency_device(torch.tensor(t, device="cuda"), torch.tensor(f, device="cuda"))
+        host = spb.contingency(t, f)
+        assert np.array_equal(dev.counts, host.counts) and dev.n == host.n
+        assert spb.partition_match(dev) == spb.partition_match(host)
