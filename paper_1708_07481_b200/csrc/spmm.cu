@@ -8,8 +8,9 @@
 // neighbour's row of X is one contiguous run of ncols values, read as 128-bit
 // vectors (float4 / double2). When the row is narrower than a warp's vector
 // width the warp splits into lane groups that walk different neighbours and
-// are combined with xor-shuffles at the end. Wide blocks are processed in
-// column panels sized so the gathered panel of X stays L2-resident.
+// are combined with xor-shuffles at the end.
+#include <cstdlib>
+
 #include "common.cuh"
 
 namespace spb {
@@ -152,16 +153,13 @@ int launch_spmm(int32_t r0, int32_t r1, const int32_t* rp, const int32_t* ci, co
     SPB_LAUNCH_CHECK();
     return SPB_OK;
   }
-  // column panels: keep the gathered panel of X within ~half of L2
-  static int l2 = -1;
-  if (l2 < 0) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    if (cudaDeviceGetAttribute(&l2, cudaDevAttrL2CacheSize, dev) != cudaSuccess) l2 = 64 << 20;
-  }
-  int64_t n_all = x_rows > 0 ? x_rows : (int64_t)r1;  // rows the gathers can touch
-  int64_t panel = ((int64_t)l2 / 2) / std::max<int64_t>(1, n_all * (int64_t)sizeof(T));
-  panel = std::max<int64_t>(panel / (8 * VN) * (8 * VN), 8 * VN);
+  // Full-width rows by default: each gathered neighbour row is one contiguous
+  // run (432 B at C3), and the CSR is read once. L2-sized column panels (the
+  // earlier design) re-read the CSR per panel and measured 28 % slower at C3
+  // (X = 216 MB); SPB_SPMM_PANEL=<cols> restores them for experiments.
+  static const int forced = getenv("SPB_SPMM_PANEL") ? atoi(getenv("SPB_SPMM_PANEL")) : 0;
+  (void)x_rows;
+  int64_t panel = forced > 0 ? forced : ncols;
   if (panel >= ncols) panel = ncols;
   for (int c0 = 0; c0 < ncols; c0 += (int)panel) {
     const int pc = (int)std::min<int64_t>(panel, ncols - c0);
