@@ -1627,8 +1627,13 @@ int sygv_enqueue(const double* ga, const double* gb, int ldg, int m, int nev, do
   }
   SPB_TRY(tri_eigs(Atri, m, 1, w, 0, nev, theta, status, st));
   {
+    // a few eigenvectors per CTA: each thread's recurrences are serial and
+    // divergent (pivoting), so spreading them over SMs beats packing a warp;
+    // the scratch (6 m doubles per thread) must stay in shared memory
     const size_t per_thread = 6 * (size_t)m * sizeof(double);
-    const int tpb = 16;
+    static const int tpb_env = getenv("SPB_INVIT_TPB") ? atoi(getenv("SPB_INVIT_TPB")) : 0;
+    int tpb = tpb_env > 0 ? tpb_env : 1;
+    while (tpb > 1 && per_thread * tpb > 200 * 1024) tpb >>= 1;
     if (per_thread * tpb <= 200 * 1024) {
       invit<<<(int)ceil_div(nev, tpb), tpb, per_thread * tpb, st>>>(w.d, w.e, m, nev, theta, w.Y,
                                                                     nev, w.scratch, 1, status);
