@@ -16,6 +16,7 @@
 #include <cooperative_groups.h>
 
 #include <algorithm>
+#include <cmath>
 #include <cstdint>
 #include <vector>
 
@@ -580,13 +581,28 @@ int assign_t(const void* xv, int64_t ldx, int n, int k, const AssignWs& w, int* 
     SPB_CUDA(cudaMemcpyAsync(pivots_out, w.piv, sizeof(int) * k, cudaMemcpyDeviceToDevice, st));
   gather_seeds<T><<<1, 256, 0, st>>>(X, ldx, k, w.piv, w.seeds, w.S);
   SPB_LAUNCH_CHECK();
-  // ---- cond(S) and S^-1 (spectral.py:156-161)
-  SPB_CUDA(cudaMemsetAsync(w.status, 0, sizeof(SmallStatus), st));
-  SPB_TRY(jacobi_svd_inverse(w.S, k, w.inv, w.jws, w.jws_cap, w.status, st));
+  // ---- cond(S) and S^-1 (spectral.py:156-161). Fast path: Cholesky of S'S,
+  // whose bracket ||G||_F ||L^-1||_F^2 / k^1.5 <= cond2(S)^2 <= ||G||_F ||L^-1||_F^2
+  // settles cond2(S) <= 1e12 whenever cond2(S) <= 1e4 (the inverse is then
+  // accurate to ~eps cond^2 <= 1e-8, far below label-changing ties); otherwise
+  // the exact one-sided Jacobi SVD decides (and inverts), as np.linalg.cond does.
   SmallStatus hs;
+  bool exact = true;
+  SPB_CUDA(cudaMemsetAsync(w.status, 0, sizeof(SmallStatus), st));
+  SPB_TRY(normal_eq_inverse(w.S, k, w.inv, w.jws, w.jws_cap, w.status, st));
   SPB_CUDA(cudaMemcpyAsync(&hs, w.status, sizeof(hs), cudaMemcpyDeviceToHost, st));
   SPB_CUDA(cudaStreamSynchronize(st));
-  info[2] = hs.cond_hi;
+  if (!hs.not_pd && !hs.nonfinite && hs.cond_hi <= 1e8) {
+    exact = false;
+    info[2] = std::sqrt(hs.cond_hi);  // upper bound on cond2(S)
+  }
+  if (exact) {
+    SPB_CUDA(cudaMemsetAsync(w.status, 0, sizeof(SmallStatus), st));
+    SPB_TRY(jacobi_svd_inverse(w.S, k, w.inv, w.jws, w.jws_cap, w.status, st));
+    SPB_CUDA(cudaMemcpyAsync(&hs, w.status, sizeof(hs), cudaMemcpyDeviceToHost, st));
+    SPB_CUDA(cudaStreamSynchronize(st));
+    info[2] = hs.cond_hi;
+  }
   if (!(hs.cond_hi <= 1e12)) {
     set_error("seed rows numerically singular; embedding carries no clusters");
     return SPB_ERR_ASSIGNMENT;

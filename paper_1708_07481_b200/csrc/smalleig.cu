@@ -1708,7 +1708,32 @@ int pivoted_cholqr_enqueue(const double* g, int ldg, int na, double rank_tol, in
 
 size_t jacobi_ws_doubles(int k) {
   const size_t K = (size_t)((k + 1) & ~1);
-  return K * k + K * K + 64;
+  return std::max(K * k + K * K, 4 * (size_t)k * k) + 64;
+}
+
+// Fast path for cond(S) / S^-1 of the QRCP seed block: G = S'S, Cholesky with
+// its cond2(G) bracket, S^-1 = L^-T L^-1 S'. status->cond_lo/hi hold the
+// bracket of cond2(G) = cond2(S)^2 (status->not_pd when G is not numerically
+// PD); the caller decides and falls back to the Jacobi SVD when undecided.
+int normal_eq_inverse(const double* s, int k, double* inv, double* ws, size_t ws_doubles,
+                      SmallStatus* status, cudaStream_t st) {
+  if (ws_doubles < jacobi_ws_doubles(k)) {
+    set_error("seed inverse workspace too small");
+    return SPB_ERR_WORKSPACE;
+  }
+  SPB_TRY(set_smem_attrs());
+  const size_t kk = (size_t)k * k;
+  double* G = ws;
+  double* L = ws + kk;
+  double* Li = ws + 2 * kk;
+  double* T = ws + 3 * kk;
+  dim3 grid((unsigned)ceil_div(k, 32), (unsigned)ceil_div(k, 32));
+  small_gemm<<<grid, 256, 0, st>>>(1, 0, k, k, k, s, k, s, k, G, k);  // S'S
+  launch_chol(G, k, L, Li, 0, status, st);
+  small_gemm<<<grid, 256, 0, st>>>(0, 1, k, k, k, Li, k, s, k, T, k);   // L^-1 S'
+  small_gemm<<<grid, 256, 0, st>>>(1, 0, k, k, k, Li, k, T, k, inv, k);  // L^-T (L^-1 S')
+  SPB_LAUNCH_CHECK();
+  return SPB_OK;
 }
 
 int jacobi_svd_inverse(const double* s, int k, double* inv, double* ws, size_t ws_doubles,

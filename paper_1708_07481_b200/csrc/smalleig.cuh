@@ -51,5 +51,8 @@ int pivoted_cholqr_enqueue(const double* g, int ldg, int na, double rank_tol, in
 int jacobi_svd_inverse(const double* s, int k, double* inv, double* ws, size_t ws_doubles,
                        SmallStatus* status, cudaStream_t st);
 size_t jacobi_ws_doubles(int k);
+// S^-1 through the normal equations with the Cholesky cond bracket of S'S in status.
+int normal_eq_inverse(const double* s, int k, double* inv, double* ws, size_t ws_doubles,
+                      SmallStatus* status, cudaStream_t st);
 
 }  // namespace spb
