@@ -221,6 +221,167 @@ gram_dmma(GramBatch b, int64_t n, int64_t kchunk, int ldo, int64_t split_stride,
   }
 }
 
+// Same DMMA Gram with a configurable CTA tile, so the tile matches the block
+// widths of the solver (l = 108 at C3 -> 112x112 tiles instead of 2x2 tiles of
+// 64 = 1.4x wasted MMAs). Warp grid WM x WN, each warp
+// MT x NT m8n8 tiles; DKT rows per staged chunk; row pitch TM+4 / TN+4 doubles
+// (== 4 mod 16: the four k-rows of a fragment load hit disjoint bank groups).
+template <typename T, int MT, int NT, int WM, int WN, int DKT>
+__global__ void __launch_bounds__(32 * WM * WN)
+gram_dmma_t(GramBatch b, int64_t n, int64_t kchunk, int ldo, int64_t split_stride,
+            double* __restrict__ part) {
+  constexpr int TM = WM * MT * 8, TN = WN * NT * 8, NTHR = 32 * WM * WN;
+  constexpr int LDM = TM + 4, LDN = TN + 4;
+  constexpr int PERU = (DKT * TM + NTHR - 1) / NTHR, PERV = (DKT * TN + NTHR - 1) / NTHR;
+  extern __shared__ double dsm[];
+  double* Us = dsm;                  // [2][DKT][LDM]
+  double* Vs = dsm + 2 * DKT * LDM;  // [2][DKT][LDN]
+  const int tile = blockIdx.x;
+  int j = 0;
+  while (j + 1 < b.njobs && tile >= b.tile_start[j + 1]) ++j;
+  const GramJob jb = b.job[j];
+  const int local = tile - b.tile_start[j];
+  const int tq_count = (jb.q + TN - 1) / TN;
+  const int tp = local / tq_count, tq = local % tq_count;
+  const int p0 = tp * TM, q0 = tq * TN;
+  const int64_t k0 = (int64_t)blockIdx.y * kchunk;
+  const int64_t k1 = min(n, k0 + kchunk);
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int wm = warp / WN, wn = warp % WN;
+  const T* U = (const T*)jb.U;
+  const T* V = (const T*)jb.V;
+  T ru[PERU], rv[PERV];
+  double acc[MT][NT][2];
+#pragma unroll
+  for (int a = 0; a < MT; ++a)
+#pragma unroll
+    for (int c = 0; c < NT; ++c) acc[a][c][0] = acc[a][c][1] = 0.0;
+  const int fr = lane & 3, fc = lane >> 2;
+  int buf = 0;
+#define SPB_GT_LOAD(KB)                                                                     \
+  {                                                                                         \
+    _Pragma("unroll") for (int t = 0; t < PERU; ++t) {                                      \
+      const int e = tid + NTHR * t;                                                         \
+      const int r = e / TM, c = e % TM;                                                     \
+      const int64_t k = (KB) + r;                                                           \
+      ru[t] = (e < DKT * TM && k < k1 && p0 + c < jb.p) ? U[k * jb.ldu + p0 + c] : T(0);     \
+    }                                                                                       \
+    _Pragma("unroll") for (int t = 0; t < PERV; ++t) {                                      \
+      const int e = tid + NTHR * t;                                                         \
+      const int r = e / TN, c = e % TN;                                                     \
+      const int64_t k = (KB) + r;                                                           \
+      rv[t] = (e < DKT * TN && k < k1 && q0 + c < jb.q) ? V[k * jb.ldv + q0 + c] : T(0);     \
+    }                                                                                       \
+  }
+#define SPB_GT_STORE(BUF)                                                                   \
+  {                                                                                         \
+    _Pragma("unroll") for (int t = 0; t < PERU; ++t) {                                      \
+      const int e = tid + NTHR * t;                                                         \
+      if (e < DKT * TM) Us[((BUF) * DKT + e / TM) * LDM + e % TM] = (double)ru[t];           \
+    }                                                                                       \
+    _Pragma("unroll") for (int t = 0; t < PERV; ++t) {                                      \
+      const int e = tid + NTHR * t;                                                         \
+      if (e < DKT * TN) Vs[((BUF) * DKT + e / TN) * LDN + e % TN] = (double)rv[t];           \
+    }                                                                                       \
+  }
+  if (k0 < k1) {
+    SPB_GT_LOAD(k0);
+    SPB_GT_STORE(0);
+  }
+  __syncthreads();
+  for (int64_t kb = k0; kb < k1; kb += DKT) {
+    const bool more = kb + DKT < k1;
+    if (more) SPB_GT_LOAD(kb + DKT);
+    const double* ub = Us + buf * DKT * LDM + wm * (MT * 8) + fc;
+    const double* vb = Vs + buf * DKT * LDN + wn * (NT * 8) + fc;
+#pragma unroll
+    for (int k4 = 0; k4 < DKT; k4 += 4) {
+      double af[MT], bf[NT];
+#pragma unroll
+      for (int t = 0; t < MT; ++t) af[t] = ub[(k4 + fr) * LDM + t * 8];
+#pragma unroll
+      for (int t = 0; t < NT; ++t) bf[t] = vb[(k4 + fr) * LDN + t * 8];
+#pragma unroll
+      for (int mt = 0; mt < MT; ++mt)
+#pragma unroll
+        for (int nt = 0; nt < NT; ++nt)
+          asm volatile(
+              "mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+              : "+d"(acc[mt][nt][0]), "+d"(acc[mt][nt][1])
+              : "d"(af[mt]), "d"(bf[nt]));
+    }
+    if (more) SPB_GT_STORE(buf ^ 1);
+    __syncthreads();
+    buf ^= 1;
+  }
+  double* out = part + (int64_t)blockIdx.y * split_stride;
+#pragma unroll
+  for (int mt = 0; mt < MT; ++mt) {
+    const int i = p0 + wm * (MT * 8) + mt * 8 + fc;
+    if (i >= jb.p) continue;
+#pragma unroll
+    for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int c = q0 + wn * (NT * 8) + nt * 8 + fr * 2 + h;
+        if (c < jb.q) out[(int64_t)(jb.out_r + i) * ldo + jb.out_c + c] = acc[mt][nt][h];
+      }
+  }
+#undef SPB_GT_LOAD
+#undef SPB_GT_STORE
+}
+
+// Launch one tile configuration: recompute the batch's tile starts for its
+// tile shape and pick the split-K so tiles * ks fills the GPU.
+template <typename T, int MT, int NT, int WM, int WN, int DKT>
+int launch_gram_cfg(GramBatch bb, int64_t n, int out_rows, int out_cols, double* partial,
+                    size_t partial_cap, int ctas_per_sm, int* ks_out, cudaStream_t st) {
+  constexpr int TM = WM * MT * 8, TN = WN * NT * 8, NTHR = 32 * WM * WN;
+  constexpr size_t smem = sizeof(double) * 2 * DKT * ((size_t)(TM + 4) + (TN + 4));
+  int tiles = 0;
+  for (int j = 0; j < bb.njobs; ++j) {
+    bb.tile_start[j] = tiles;
+    tiles += (int)(ceil_div(bb.job[j].p, TM) * ceil_div(bb.job[j].q, TN));
+  }
+  bb.tile_start[bb.njobs] = tiles;
+  int64_t ks = std::max<int64_t>(1, (int64_t)ctas_per_sm * num_sms() / std::max(tiles, 1));
+  ks = std::min<int64_t>(ks, ceil_div(n, 512));
+  ks = std::max<int64_t>(ks, 1);
+  while (ks > 1 && (size_t)ks * out_rows * out_cols > partial_cap) --ks;
+  if ((size_t)ks * out_rows * out_cols > partial_cap) {
+    set_error("gram partial workspace too small");
+    return SPB_ERR_WORKSPACE;
+  }
+  const int64_t kchunk = round_up(ceil_div(std::max<int64_t>(n, 1), ks), DKT);
+  static bool attr = false;
+  if (!attr) {
+    SPB_CUDA(cudaFuncSetAttribute(gram_dmma_t<T, MT, NT, WM, WN, DKT>,
+                                  cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    attr = true;
+  }
+  dim3 grid(tiles, (unsigned)ks);
+  gram_dmma_t<T, MT, NT, WM, WN, DKT><<<grid, NTHR, smem, st>>>(
+      bb, n, kchunk, out_cols, (int64_t)out_rows * out_cols, partial);
+  SPB_LAUNCH_CHECK();
+  *ks_out = (int)ks;
+  return SPB_OK;
+}
+
+// Tile shape for a batch: 112 x 112 when every job is 65..112 wide (C3's
+// l = 108 blocks: 1.075x padding instead of 1.4x with 64-tiles), else 64.
+// (A 176-wide tile for C4 needs more accumulator registers than a warp grid
+// of <= 32 warps can hold; 64-tiles pad 176 -> 192, 1.19x.)
+int gram_tile_for(const GramBatch& b) {
+  static const int forced = getenv("SPB_GRAM_TILE") ? atoi(getenv("SPB_GRAM_TILE")) : 0;
+  if (forced == 64 || forced == 112) return forced;
+  int wmin = 1 << 30, wmax = 0;
+  for (int j = 0; j < b.njobs; ++j) {
+    wmax = std::max(wmax, std::max(b.job[j].p, b.job[j].q));
+    wmin = std::min(wmin, std::max(b.job[j].p, b.job[j].q));
+  }
+  return (wmax > 64 && wmax <= 112 && wmin > 64) ? 112 : 64;
+}
+
 __global__ void sum_splits(const double* __restrict__ part, int ksplit, int64_t split_stride,
                            int rows, int cols, int ldp, double* __restrict__ out, int ldo) {
   const int64_t total = (int64_t)rows * cols;
@@ -645,6 +806,16 @@ int gram_batched(int dtype, const GramBatch& b, int64_t n, int out_rows, int out
     else
       gram_kernel<double><<<grid, 128, 0, st>>>(b, n, kchunk, out_cols, stride, partial);
     SPB_LAUNCH_CHECK();
+  } else if (n > 0 && gram_tile_for(b) != 64) {
+    const int tw = gram_tile_for(b);
+    (void)tw;  // 112 x 112: 7 x 2 warps of 16 x 56 (2 x 7 m8n8 tiles each)
+    const int rc =
+        dtype == SPB_F32
+            ? launch_gram_cfg<float, 2, 7, 7, 2, 16>(b, n, out_rows, out_cols, partial, partial_cap, 1,
+                                                     &ks, st)
+            : launch_gram_cfg<double, 2, 7, 7, 2, 16>(b, n, out_rows, out_cols, partial, partial_cap,
+                                                      1, &ks, st);
+    if (rc != SPB_OK) return rc;
   } else if (n > 0) {
     static bool attr = false;
     if (!attr) {

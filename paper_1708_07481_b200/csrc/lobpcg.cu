@@ -75,7 +75,9 @@ SolveWs carve(Arena& a, int dtype, int n, int l, int nranks = 1, int n_max = 0) 
   const int mm = w.mmax;
   w.G = a.take<double>((size_t)mm * 2 * mm);
   const int seg_tiles = (int)ceil_div(l, 64) * (int)ceil_div(l, 64);
-  w.gpart_cap = gram_partial_doubles(n, 18 * seg_tiles, mm, 2 * mm, nullptr);
+  // 12 jobs of one 112-tile each is the fewest tiles an RR Gram can have: the
+  // split-K (and so the partial buffer) is largest then
+  w.gpart_cap = gram_partial_doubles(n, std::min(12, 18 * seg_tiles), mm, 2 * mm, nullptr);
   w.gpart_cap = std::max(w.gpart_cap, gram_partial_doubles(n, seg_tiles, w.lp, w.lp, nullptr));
   w.use_tc = false;
   if (dtype == SPB_F32) {
