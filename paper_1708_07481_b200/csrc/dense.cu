@@ -689,6 +689,7 @@ colreduce_kernel(int kind, const T* __restrict__ A, int64_t lda, int cols, int64
     if (ry < nry && c < cols) {
       T th = T(0);
       if (kind == CR_RESIDUAL) th = (T)theta[c];
+#pragma unroll 4
       for (int64_t r = rb + ry; r < re; r += nry) {
         T v = A[r * lda + c];
         if (kind == CR_RESIDUAL) {
@@ -724,7 +725,8 @@ __global__ void colreduce_final(const double* __restrict__ part, int blocks, int
 }
 
 int colreduce_blocks(int64_t n) {
-  return (int)std::max<int64_t>(1, std::min<int64_t>(2 * num_sms(), ceil_div(n, 64)));
+  // 8 CTAs of 256 threads per SM: enough loads in flight for HBM bandwidth
+  return (int)std::max<int64_t>(1, std::min<int64_t>(8 * num_sms(), ceil_div(n, 64)));
 }
 
 // ----------------------------------------------------------------------------
