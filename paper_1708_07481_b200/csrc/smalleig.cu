@@ -738,6 +738,212 @@ tridiag_cluster(const double* __restrict__ Asrc, int m, int symmetrize, double* 
   }
 }
 
+// Same reduction with the two per-step exchanges carried by st.async stores that
+// complete transactions on the receiver's mbarrier (one barrier per buffer
+// parity for the p / p'v exchange and one for row k+1): a CTA waits only for the
+// bytes it needs, with no release fence or cluster-wide barrier per step. WAR
+// safety of the double-buffered slots follows from the data dependencies (a
+// producer can only reach step k+2 after every CTA has finished step k), plus
+// one CTA barrier per step before vbuf / sc are rewritten.
+__device__ __forceinline__ uint32_t sm_u32(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mb_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(sm_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mb_expect(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(sm_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mb_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred P;\n"
+      "MBW_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P, [%0], %1;\n\t"
+      "@!P bra MBW_%=;\n}" ::"r"(sm_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void st_async_f64(double* local_addr, uint64_t* local_bar, int rank,
+                                             double v) {
+  uint32_t ra, rb;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;\n" : "=r"(ra) : "r"(sm_u32(local_addr)), "r"(rank));
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;\n" : "=r"(rb) : "r"(sm_u32(local_bar)), "r"(rank));
+  asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.b64 [%0], %1, [%2];\n" ::"r"(ra),
+               "l"(__double_as_longlong(v)), "r"(rb)
+               : "memory");
+}
+
+__global__ void __launch_bounds__(TCT)
+tridiag_cluster_mb(const double* __restrict__ Asrc, int m, int symmetrize, double* __restrict__ V,
+                   double* __restrict__ tau, double* __restrict__ d, double* __restrict__ e,
+                   const SmallStatus* status) {
+  if (status && (status->nonfinite || status->not_pd)) return;  // uniform over the cluster
+  unsigned rank_u, csize_u;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;\n" : "=r"(rank_u));
+  asm volatile("mov.u32 %0, %%cluster_nctarank;\n" : "=r"(csize_u));
+  const int rank = (int)rank_u, C = (int)csize_u;
+  const int nc = (m + C - 1) / C;
+  const int c0 = rank * nc;
+  const int ncl = max(0, min(m, c0 + nc) - c0);
+  extern __shared__ double tsm[];
+  double* Wl = tsm;                        // m x nc, row j / local column c
+  double* rowbuf = Wl + (size_t)m * nc;    // [2][m]  row k (all-gathered)
+  double* pbuf = rowbuf + 2 * m;           // [2][m]  p (all-gathered)
+  double* vbuf = pbuf + 2 * m;             // [m]     v of the current step
+  double* dotbuf = vbuf + m;               // [2][16] per-CTA shares of p'v
+  double* red = dotbuf + 32;               // [G][nc]
+  __shared__ double wdot[2];
+  __shared__ double sc[2];
+  __shared__ __align__(8) uint64_t mbA[2], mbB[2];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int G = TCT / nc;
+  const int g = tid / nc, lc = tid - (tid / nc) * nc;
+  const bool active = g < G && lc < ncl;
+  const int icol = c0 + lc;
+  if (tid == 0) {
+    mb_init(&mbA[0], 1);
+    mb_init(&mbA[1], 1);
+    mb_init(&mbB[0], 1);
+    mb_init(&mbB[1], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  for (int x = tid; x < m * ncl; x += TCT) {
+    const int j = x / ncl, c = x - (x / ncl) * ncl, i = c0 + c;
+    const double a = Asrc[(int64_t)j * m + i];
+    Wl[j * nc + c] = symmetrize ? 0.5 * (a + Asrc[(int64_t)i * m + j]) : a;
+    V[(int64_t)j * m + i] = 0.0;
+  }
+  cluster_sync_all();  // barriers initialised everywhere before any remote transaction
+  for (int x = tid; x < ncl * C; x += TCT) {
+    const int r = x / ncl, c = x - (x / ncl) * ncl;
+    st_async_f64(rowbuf + c0 + c, &mbB[0], r, Wl[c]);
+  }
+  uint32_t useA0 = 0, useA1 = 0;
+  for (int k = 0; k + 2 < m; ++k) {
+    const int b = k & 1;
+    const double* row = rowbuf + b * m;
+    double* pb = pbuf + b * m;
+    double* nextrow = rowbuf + (b ^ 1) * m;
+    __syncthreads();  // every thread is done with vbuf / sc of step k-1
+    if (tid == 0) mb_expect(&mbB[b], 8u * (uint32_t)(m - k));
+    mb_wait(&mbB[b], (uint32_t)((k >> 1) & 1));  // row k has arrived
+    // (1) reflector of row k (warp 0), v into vbuf
+    if (warp == 0) {
+      double ss = 0.0;
+      for (int i = k + 2 + lane; i < m; i += 32) ss = fma(row[i], row[i], ss);
+      ss = warp_sum(ss);
+      const double alpha = row[k + 1];
+      double tk = 0.0, scale = 0.0, beta = alpha;
+      if (ss != 0.0) {
+        beta = -copysign(sqrt(alpha * alpha + ss), alpha);
+        tk = (beta - alpha) / beta;
+        scale = 1.0 / (alpha - beta);
+      }
+      for (int i = k + 1 + lane; i < m; i += 32) vbuf[i] = i == k + 1 ? 1.0 : row[i] * scale;
+      if (lane == 0) {
+        sc[0] = tk;
+        if (rank == 0) {
+          d[k] = row[k];
+          e[k] = beta;
+          tau[k] = tk;
+        }
+      }
+    }
+    __syncthreads();
+    const double tk = sc[0];
+    const int j0 = k + 1 + g;
+    const bool own = active && icol > k;
+    if (tid < ncl && icol > k) V[(int64_t)k * m + icol] = vbuf[icol];
+    if (tk == 0.0) {  // identity reflector: row k+1 is unchanged, pass it on
+      if (tid < ncl && icol > k) {
+        const double wv = Wl[(k + 1) * nc + tid];
+        for (int r = 0; r < C; ++r) st_async_f64(nextrow + icol, &mbB[b ^ 1], r, wv);
+      }
+      continue;
+    }
+    // (2) p = tau W v on own columns
+    if (own) {
+      double a0 = 0.0, a1 = 0.0;
+      const double* wp = Wl + j0 * nc + lc;
+      const double* vp = vbuf + j0;
+      const int step = G * nc;
+      int j = j0;
+      for (; j + G < m; j += 2 * G, wp += 2 * step, vp += 2 * G) {
+        a0 = fma(wp[0], vp[0], a0);
+        a1 = fma(wp[step], vp[G], a1);
+      }
+      if (j < m) a0 = fma(wp[0], vp[0], a0);
+      red[g * nc + lc] = a0 + a1;
+    }
+    __syncthreads();
+    if (tid < 64) {
+      double pv = 0.0;
+      if (tid < ncl && icol > k) {
+        double sacc = 0.0;
+        const int gmax = min(G, m - (k + 1));  // groups that saw a row
+        for (int q = 0; q < gmax; ++q) sacc += red[q * nc + tid];
+        const double p = tk * sacc;
+        pv = p * vbuf[icol];
+        for (int r = 0; r < C; ++r) st_async_f64(pb + icol, &mbA[b], r, p);
+      }
+      pv = warp_sum(pv);
+      if (lane == 0) wdot[tid >> 5] = pv;
+      asm volatile("bar.sync 1, 64;\n" ::: "memory");
+      if (tid < C) st_async_f64(dotbuf + b * 16 + rank, &mbA[b], tid, wdot[0] + wdot[1]);
+    }
+    if (tid == 0) mb_expect(&mbA[b], 8u * (uint32_t)(m - k - 1 + C));
+    {
+      const uint32_t u = b ? useA1 : useA0;
+      mb_wait(&mbA[b], u & 1u);
+      if (b) ++useA1; else ++useA0;
+    }
+    // (3) rank-2 update of own columns, push row k+1
+    if (own) {
+      double tot = 0.0;
+      for (int r = 0; r < C; ++r) tot += dotbuf[b * 16 + r];
+      const double K = 0.5 * tk * tot;
+      const double vi = vbuf[icol];
+      const double wi = fma(-K, vi, pb[icol]);
+      double* wp = Wl + j0 * nc + lc;
+      const double* vp = vbuf + j0;
+      const double* pp = pb + j0;
+      const int step = G * nc;
+      int j = j0;
+      if (g == 0) {  // row k+1 goes to every CTA for the next reflector
+        const double wj = fma(-K, vp[0], pp[0]);
+        const double wv = fma(-vp[0], wi, fma(-wj, vi, wp[0]));
+        wp[0] = wv;
+        for (int r = 0; r < C; ++r) st_async_f64(nextrow + icol, &mbB[b ^ 1], r, wv);
+        j += G, wp += step, vp += G, pp += G;
+      }
+#pragma unroll 2
+      for (; j < m; j += G, wp += step, vp += G, pp += G) {
+        const double vj = vp[0];
+        const double wj = fma(-K, vj, pp[0]);
+        wp[0] = fma(-vj, wi, fma(-wj, vi, wp[0]));
+      }
+    }
+  }
+  if (m >= 2) {
+    const int kk = m - 2;  // row m-2 was pushed at step m-3 (or at init when m == 2)
+    __syncthreads();
+    if (tid == 0) mb_expect(&mbB[kk & 1], 8u * (uint32_t)(m - kk));
+    mb_wait(&mbB[kk & 1], (uint32_t)((kk >> 1) & 1));
+    const double* row = rowbuf + (kk & 1) * m;
+    if (rank == 0 && tid == 0) {
+      d[m - 2] = row[m - 2];
+      e[m - 2] = row[m - 1];
+      tau[m - 2] = 0.0;
+      tau[m - 1] = 0.0;
+      e[m - 1] = 0.0;
+    }
+    if (tid == 0 && m - 1 >= c0 && m - 1 < c0 + ncl) d[m - 1] = Wl[(m - 1) * nc + (m - 1 - c0)];
+  }
+  cluster_sync_all();  // no CTA leaves while its shared memory can still be written
+}
+
 // Cholesky + inverse for kCholLdlMax < m <= kCholClusterMax: the packed
 // array of chol_ldl (L' in the lower triangle, the unit-lower inverse
 // transposed in the upper one) is split by columns over the CTAs of a cluster.
@@ -915,6 +1121,8 @@ void launch_tridiag(const double* Asrc, int m, int symmetrize, double* Wg, doubl
     if (!attr) {
       cudaFuncSetAttribute(tridiag_cluster, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
       cudaFuncSetAttribute(tridiag_cluster, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+      cudaFuncSetAttribute(tridiag_cluster_mb, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+      cudaFuncSetAttribute(tridiag_cluster_mb, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
       attr = true;
     }
     cudaLaunchConfig_t cfg = {};
@@ -929,7 +1137,11 @@ void launch_tridiag(const double* Asrc, int m, int symmetrize, double* Wg, doubl
     at[0].val.clusterDim.z = 1;
     cfg.attrs = at;
     cfg.numAttrs = 1;
-    cudaLaunchKernelEx(&cfg, tridiag_cluster, Asrc, m, symmetrize, V, tau, d, e, status);
+    static const bool sync_variant = getenv("SPB_TRI_SYNC") != nullptr;  // A/B switch
+    if (sync_variant)
+      cudaLaunchKernelEx(&cfg, tridiag_cluster, Asrc, m, symmetrize, V, tau, d, e, status);
+    else
+      cudaLaunchKernelEx(&cfg, tridiag_cluster_mb, Asrc, m, symmetrize, V, tau, d, e, status);
     return;
   }
   const int rows = (m + 31) / 32;
