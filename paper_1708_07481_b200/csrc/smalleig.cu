@@ -89,7 +89,7 @@ __device__ void chol_epilogue(int m, double fb, double* __restrict__ Linv, int m
                               SmallStatus* status, double* red) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   double fl = 0.0;
-  for (int i = warp; i < m; i += ET / 32)
+  for (int i = warp; i < m; i += (int)(blockDim.x >> 5))
     for (int j = lane; j <= i; j += 32) {
       const double v = Linv[(int64_t)i * m + j];
       fl += v * v;
@@ -108,7 +108,7 @@ __device__ void chol_epilogue(int m, double fb, double* __restrict__ Linv, int m
     }
   } else {
     // Rinv = (L^-1)' in place of Linv (upper triangular)
-    for (int i = warp; i < m; i += ET / 32)
+    for (int i = warp; i < m; i += (int)(blockDim.x >> 5))
       for (int j = i + 1 + lane; j < m; j += 32) {
         const double a = Linv[(int64_t)i * m + j], b = Linv[(int64_t)j * m + i];
         Linv[(int64_t)i * m + j] = b;
@@ -407,6 +407,243 @@ chol_ldl(const double* __restrict__ Bsrc, int m, double* __restrict__ Lg, double
   }
   __syncthreads();
   chol_epilogue(m, fb, Linv, mode, status, red);
+}
+
+__device__ __forceinline__ void tri_index(int t, int* ti, int* tq) {
+  int r = (int)((sqrtf(8.0f * (float)t + 1.0f) - 1.0f) * 0.5f);
+  while ((r + 1) * (r + 2) / 2 <= t) ++r;
+  while (r * (r + 1) / 2 > t) --r;
+  *ti = r;
+  *tq = t - r * (r + 1) / 2;
+}
+
+// Blocked Cholesky + inverse for m <= kCholLdlMax with warp-synchronous
+// panels (same packed layout, outputs and status protocol as chol_ldl):
+//  P1  the 32x32 diagonal block is factored (LDL') by warp 0 in registers,
+//      lane i = row i, columns broadcast by shuffles: no CTA barrier per column;
+//  P2  the rows below the block solve against it, one thread per row, right-
+//      looking inside the row (independent FMAs);
+//  P3  one rank-32 update of the trailing lower triangle in 4x4 register tiles
+//      against a D^-1-scaled copy of the panel.
+// The unit-lower inverse is formed by blocks as in chol_blk (diagonal blocks by
+// one warp each in registers, then block rows). Three CTA barriers per panel.
+constexpr int CWT = 512;  // threads of chol_wsync
+
+__global__ void __launch_bounds__(CWT)
+chol_wsync(const double* __restrict__ Bsrc, int m, double* __restrict__ Lg, double* __restrict__ Linv,
+           int mode, SmallStatus* status) {
+  extern __shared__ double smem[];
+  __shared__ double red[33];
+  __shared__ int fail;
+  __shared__ double Lp[32][33];  // L' of the current diagonal block (unit lower, scaled)
+  const int ld = m | 1;
+  double* A = smem;                          // m x ld packed: L' d below, X' above
+  double* S = A + (size_t)m * ld;            // m x 33: D^-1 scaled panel / block scratch
+  double* dinv = S + (size_t)m * 33;         // m
+  const int sld = 33;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  if (status->nonfinite) return;
+  double fb = 0.0;
+  for (int i = warp; i < m; i += CWT / 32)
+    for (int j = lane; j < m; j += 32) {
+      const double v = Bsrc[(int64_t)i * m + j];
+      A[i * ld + j] = v;
+      fb += v * v;
+    }
+  fb = block_sum(fb, red);
+  if (tid == 0) {
+    fail = 0;
+    if (mode == 1) {  // diag > 0 and min diag > (eps na)^2 max diag (lobpcg.py:229-231)
+      double dmin = DBL_MAX, dmax = -DBL_MAX;
+      for (int i = 0; i < m; ++i) {
+        dmin = fmin(dmin, A[i * ld + i]);
+        dmax = fmax(dmax, A[i * ld + i]);
+      }
+      status->dmin = dmin;
+      status->dmax = dmax;
+      const double t = kEps64 * m;
+      if (!(dmin > 0.0) || !(dmin > t * t * dmax)) fail = 1;
+    }
+  }
+  __syncthreads();
+  if (fail == 1) {
+    if (tid == 0) status->fallback = 1;
+    return;
+  }
+  for (int kb = 0; kb < m; kb += 32) {
+    const int nb = min(32, m - kb);
+    const int ke = kb + nb;
+    // ---- P1: diagonal block, right-looking; one element of the block's
+    // trailing triangle per thread and one CTA barrier per column
+    for (int c = 0; c < nb; ++c) {
+      const double dc = A[(kb + c) * ld + kb + c];
+      if (!(dc > 0.0)) {
+        if (tid == 0) fail = 2;
+        break;  // uniform: every thread read the same pivot
+      }
+      const double rc = 1.0 / dc;
+      const int rem = nb - 1 - c;
+      if (tid < rem * (rem + 1) / 2) {
+        int ti, tq;
+        tri_index(tid, &ti, &tq);
+        const int i = kb + c + 1 + ti, q = kb + c + 1 + tq;
+        A[i * ld + q] = fma(-A[i * ld + kb + c] * rc, A[q * ld + kb + c], A[i * ld + q]);
+      }
+      if (tid == 0) dinv[kb + c] = rc;
+      __syncthreads();
+    }
+    __syncthreads();
+    if (fail) break;
+    // scaled unit-lower L' of the block for P2
+    for (int x = tid; x < 32 * 32; x += CWT) {
+      const int i = x >> 5, c = x & 31;
+      Lp[i][c] = (i < nb && c < i) ? A[(kb + i) * ld + kb + c] * dinv[kb + c] : (i == c ? 1.0 : 0.0);
+    }
+    __syncthreads();
+    if (fail) break;
+    if (ke >= m) break;
+    // ---- P2: rows below the block, one thread per row
+    for (int i = ke + tid; i < m; i += CWT) {
+      double x[32];
+#pragma unroll
+      for (int t = 0; t < 32; ++t) x[t] = t < nb ? A[i * ld + kb + t] : 0.0;
+#pragma unroll
+      for (int t = 0; t < 32; ++t) {
+#pragma unroll
+        for (int c = t + 1; c < 32; ++c) x[c] = fma(-x[t], Lp[c][t], x[c]);
+      }
+#pragma unroll
+      for (int t = 0; t < 32; ++t)
+        if (t < nb) {
+          A[i * ld + kb + t] = x[t];
+          S[i * sld + t] = x[t] * dinv[kb + t];
+        }
+    }
+    __syncthreads();
+    // ---- P3: trailing update A[i][q] -= sum_t A[i][kb+t] S[q][t], i >= q >= ke, 4x4 tiles
+    const int T = m - ke;
+    const int TT = (T + 3) / 4;
+    const int ntile = TT * (TT + 1) / 2;
+    for (int t = tid; t < ntile; t += CWT) {
+      int ti, tq;
+      tri_index(t, &ti, &tq);
+      const int i0 = ke + 4 * ti, q0 = ke + 4 * tq;
+      double acc[4][4];
+#pragma unroll
+      for (int a2 = 0; a2 < 4; ++a2)
+#pragma unroll
+        for (int b2 = 0; b2 < 4; ++b2) acc[a2][b2] = 0.0;
+      for (int c = 0; c < nb; ++c) {
+        double av[4], sv[4];
+#pragma unroll
+        for (int a2 = 0; a2 < 4; ++a2) {
+          av[a2] = i0 + a2 < m ? A[(i0 + a2) * ld + kb + c] : 0.0;
+          sv[a2] = q0 + a2 < m ? S[(q0 + a2) * sld + c] : 0.0;
+        }
+#pragma unroll
+        for (int a2 = 0; a2 < 4; ++a2)
+#pragma unroll
+          for (int b2 = 0; b2 < 4; ++b2) acc[a2][b2] = fma(av[a2], sv[b2], acc[a2][b2]);
+      }
+#pragma unroll
+      for (int a2 = 0; a2 < 4; ++a2)
+#pragma unroll
+        for (int b2 = 0; b2 < 4; ++b2) {
+          const int i = i0 + a2, qq = q0 + b2;
+          if (i < m && qq <= i) A[i * ld + qq] -= acc[a2][b2];
+        }
+    }
+    __syncthreads();
+  }
+  if (fail) {
+    if (tid == 0) {
+      if (mode == 0) status->not_pd = 1;
+      else status->fallback = 1;
+    }
+    return;
+  }
+  if (mode == 1 && tid == 0) {
+    double rmin = DBL_MAX, rmax = -DBL_MAX;
+    for (int i = 0; i < m; ++i) {
+      const double r = sqrt(A[i * ld + i]);
+      rmin = fmin(rmin, r);
+      rmax = fmax(rmax, r);
+    }
+    status->rmin = rmin;
+    status->rmax = rmax;
+    if (!(rmin > sqrt(kEps64) * rmax)) fail = 1;  // lobpcg.py:235
+  }
+  for (int i = tid; i < m; i += CWT) dinv[i] = 1.0 / sqrt(A[i * ld + i]);
+  __syncthreads();
+  if (fail) {
+    if (tid == 0) status->fallback = 1;
+    return;
+  }
+  // ---- L' = A / d (strictly lower, in place); X = L'^-1 transposed into the upper triangle
+  for (int i = warp; i < m; i += CWT / 32)
+    for (int j = lane; j < i; j += 32) A[i * ld + j] *= dinv[j] * dinv[j];
+  __syncthreads();
+  const int nblk = (m + 31) / 32;
+  for (int bI = warp; bI < nblk; bI += CWT / 32) {  // diagonal blocks: lane = column j
+    const int b0 = bI * 32, bn = min(32, m - b0);
+    const int j = lane;
+    double x[32];
+#pragma unroll
+    for (int i = 0; i < 32; ++i) x[i] = (i == j) ? 1.0 : 0.0;
+#pragma unroll
+    for (int t = 0; t < 32; ++t) {
+      if (t >= j && t < bn) {
+#pragma unroll
+        for (int i = t + 1; i < 32; ++i)
+          if (i < bn) x[i] = fma(-A[(b0 + i) * ld + b0 + t], x[t], x[i]);
+      }
+    }
+    if (j < bn)
+#pragma unroll
+      for (int i = 0; i < 32; ++i)
+        if (i > j && i < bn) A[(b0 + j) * ld + b0 + i] = x[i];
+  }
+  __syncthreads();
+  for (int bI = 1; bI < nblk; ++bI) {  // block rows: X_IJ = -X_II (sum_K L_IK X_KJ)
+    const int i0 = bI * 32, ni = min(32, m - i0);
+    double* R = S;  // ni x i0
+    for (int x = tid; x < ni * i0; x += CWT) {
+      const int r = x / i0, j = x % i0;
+      const double* Lr = A + (i0 + r) * ld;
+      double acc = Lr[j];  // k = j (X_jj = 1)
+      for (int k = j + 1; k < i0; ++k) acc = fma(Lr[k], A[j * ld + k], acc);
+      R[x] = acc;
+    }
+    __syncthreads();
+    for (int x = tid; x < ni * i0; x += CWT) {
+      const int r = x / i0, j = x % i0;
+      double acc = R[r * i0 + j];  // q = r (X_rr = 1)
+      for (int q = 0; q < r; ++q) acc = fma(A[(i0 + q) * ld + i0 + r], R[q * i0 + j], acc);
+      A[j * ld + i0 + r] = -acc;
+    }
+    __syncthreads();
+  }
+  for (int i = warp; i < m; i += CWT / 32) {
+    const double ri = dinv[i];
+    for (int j = lane; j < m; j += 32) {
+      double l = 0.0, v = 0.0;
+      if (j < i) {
+        l = A[i * ld + j] / dinv[j];
+        v = A[j * ld + i] * ri;
+      } else if (j == i) {
+        l = 1.0 / ri;
+        v = ri;
+      }
+      Lg[(int64_t)i * m + j] = l;
+      Linv[(int64_t)i * m + j] = v;
+    }
+  }
+  __syncthreads();
+  chol_epilogue(m, fb, Linv, mode, status, red);
+}
+
+size_t chol_wsync_smem(int m) {
+  return sizeof(double) * ((size_t)m * (m | 1) + (size_t)m * 33 + m);
 }
 
 // C = op(A) op(B) for small float64 matrices, 32x32 tiles, 256 threads.
@@ -1750,7 +1987,10 @@ void launch_chol(const double* B, int m, double* L, double* Linv, int mode, Smal
   static const int cmin = getenv("SPB_CHOL_CLUSTER_MIN") ? atoi(getenv("SPB_CHOL_CLUSTER_MIN"))
                                                          : kCholLdlMax + 1;
   static const int cfix = getenv("SPB_CHOL_CLUSTER_C") ? atoi(getenv("SPB_CHOL_CLUSTER_C")) : 0;
-  if (!old && m < cmin && m <= kCholLdlMax && chol_ldl_smem(m) <= 224 * 1024) {
+  static const bool unblocked = getenv("SPB_CHOL_LDL") != nullptr;  // A/B switch
+  if (!old && !unblocked && m < cmin && m <= kCholLdlMax && chol_wsync_smem(m) <= 217 * 1024) {
+    chol_wsync<<<1, CWT, chol_wsync_smem(m), st>>>(B, m, L, Linv, mode, status);
+  } else if (!old && m < cmin && m <= kCholLdlMax && chol_ldl_smem(m) <= 224 * 1024) {
     chol_ldl<<<1, ET, chol_ldl_smem(m), st>>>(B, m, L, Linv, mode, status);
   } else if (!old && m <= kCholClusterMax) {
     int C = m <= 400 ? 8 : 16;
@@ -1786,6 +2026,7 @@ int set_smem_attrs() {
   if (done) return SPB_OK;
   SPB_CUDA(cudaFuncSetAttribute(chol_linv, cudaFuncAttributeMaxDynamicSharedMemorySize, 224 * 1024));
   SPB_CUDA(cudaFuncSetAttribute(chol_ldl, cudaFuncAttributeMaxDynamicSharedMemorySize, 224 * 1024));
+  SPB_CUDA(cudaFuncSetAttribute(chol_wsync, cudaFuncAttributeMaxDynamicSharedMemorySize, 217 * 1024));
   SPB_CUDA(cudaFuncSetAttribute(tridiag<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
   SPB_CUDA(cudaFuncSetAttribute(tridiag<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
   SPB_CUDA(cudaFuncSetAttribute(tridiag<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
