@@ -1727,14 +1727,39 @@ size_t wy_apply_smem(int m) {
   return sizeof(double) * ((size_t)m * BCW + 32 * (size_t)(m | 1) + 64 * BCW + 32 * 33);
 }
 
-void launch_backtransform(const double* V, const double* tau, int m, double* Y, int nev,
-                          double* Tscratch, const SmallStatus* status, cudaStream_t st) {
+void launch_wy_tfactors(const double* V, const double* tau, int m, double* Tscratch,
+                        const SmallStatus* status, cudaStream_t st) {
   const int nrefl = m - 2;
-  if (nrefl <= 0 || nev <= 0) return;
+  if (nrefl <= 0) return;
   const int nblk = (nrefl + 31) / 32;
   wy_tfactors<<<nblk, 256, sizeof(double) * 32 * (size_t)(m | 1), st>>>(V, tau, m, Tscratch, status);
+}
+
+void launch_wy_apply(const double* V, int m, const double* Tscratch, double* Y, int nev,
+                     const SmallStatus* status, cudaStream_t st) {
+  if (m - 2 <= 0 || nev <= 0) return;
   wy_apply<<<(nev + BCW - 1) / BCW, BAT, wy_apply_smem(m), st>>>(V, m, Tscratch, Y, nev, nev,
                                                                   status);
+}
+
+// Side stream (per device) on which the compact-WY T factors are formed while
+// the main stream runs bisection and inverse iteration: both only need the
+// tridiagonalisation, so they overlap.
+struct SideStream {
+  cudaStream_t s = nullptr;
+  cudaEvent_t fork = nullptr, join = nullptr;
+};
+SideStream* side_stream() {
+  static SideStream ss[16];
+  int dev = 0;
+  cudaGetDevice(&dev);
+  SideStream& x = ss[dev & 15];
+  if (!x.s) {
+    cudaStreamCreateWithFlags(&x.s, cudaStreamNonBlocking);
+    cudaEventCreateWithFlags(&x.fork, cudaEventDisableTiming);
+    cudaEventCreateWithFlags(&x.join, cudaEventDisableTiming);
+  }
+  return &x;
 }
 
 __global__ void copy_cols(const double* __restrict__ Y, int ldy, int m, int nev,
@@ -2040,17 +2065,6 @@ int set_smem_attrs() {
   return SPB_OK;
 }
 
-int tri_eigs(const double* Asrc, int m, int symmetrize, const SygvWs& w, int first, int count,
-             double* theta, const SmallStatus* status, cudaStream_t st) {
-  launch_tridiag(Asrc, m, symmetrize, w.W, w.V, w.tau, w.d, w.e, status, tridiag_smem(m), st);
-  SPB_LAUNCH_CHECK();
-  const int warps = 8;
-  bisect<<<(int)ceil_div(count, warps), warps * 32, 2 * sizeof(double) * (size_t)m, st>>>(
-      w.d, w.e, m, first, count, theta, nullptr, status, bisect_div());
-  SPB_LAUNCH_CHECK();
-  return SPB_OK;
-}
-
 }  // namespace
 
 size_t sygv_ws_doubles(int m, int nev) { return sygv_ws_count(m, nev); }
@@ -2078,7 +2092,19 @@ int sygv_enqueue(const double* ga, const double* gb, int ldg, int m, int nev, do
     SPB_LAUNCH_CHECK();
     Atri = w.Ap;
   }
-  SPB_TRY(tri_eigs(Atri, m, 1, w, 0, nev, theta, status, st));
+  launch_tridiag(Atri, m, 1, w.W, w.V, w.tau, w.d, w.e, status, tridiag_smem(m), st);
+  SPB_LAUNCH_CHECK();
+  SideStream* side = side_stream();
+  SPB_CUDA(cudaEventRecord(side->fork, st));
+  SPB_CUDA(cudaStreamWaitEvent(side->s, side->fork, 0));
+  launch_wy_tfactors(w.V, w.tau, m, w.scratch, status, side->s);  // overlaps bisect + invit
+  SPB_CUDA(cudaEventRecord(side->join, side->s));
+  {
+    const int warps = 8;
+    bisect<<<(int)ceil_div(nev, warps), warps * 32, 2 * sizeof(double) * (size_t)m, st>>>(
+        w.d, w.e, m, 0, nev, theta, nullptr, status, bisect_div());
+    SPB_LAUNCH_CHECK();
+  }
   {
     // a few eigenvectors per CTA: each thread's recurrences are serial and
     // divergent (pivoting), so spreading them over SMs beats packing a warp;
@@ -2098,7 +2124,8 @@ int sygv_enqueue(const double* ga, const double* gb, int ldg, int m, int nev, do
     }
   }
   SPB_LAUNCH_CHECK();
-  launch_backtransform(w.V, w.tau, m, w.Y, nev, w.scratch, status, st);
+  SPB_CUDA(cudaStreamWaitEvent(st, side->join, 0));
+  launch_wy_apply(w.V, m, w.scratch, w.Y, nev, status, st);
   SPB_LAUNCH_CHECK();
   if (!ident) {
     dim3 grid((unsigned)ceil_div(nev, 32), (unsigned)ceil_div(m, 32));
