@@ -645,10 +645,9 @@ void launch_update_qv(const UpdParams& p, int64_t n, cudaStream_t st) {
 template <typename T>
 void launch_update(const UpdParams& p, int64_t n, cudaStream_t st) {
   static const bool generic = getenv("SPB_UPDATE_GENERIC") != nullptr;  // A/B switch
-  if (sizeof(T) == 4 && !generic && update_f32_ok(p)) {
-    if (p.q <= 32) launch_update_f32<4, 32>(p, n, st);
-    else if (p.q <= 64) launch_update_f32<8, 16>(p, n, st);
-    else if (p.q <= 128) launch_update_f32<16, 8>(p, n, st);
+  // narrow blocks (q <= 64, C1/C2) measure faster on the generic kernel
+  if (sizeof(T) == 4 && !generic && p.q > 64 && update_f32_ok(p)) {
+    if (p.q <= 128) launch_update_f32<16, 8>(p, n, st);
     else if (p.q <= 192) launch_update_f32<24, 8>(p, n, st);
     else launch_update_f32<32, 8>(p, n, st);
     return;

@@ -1028,8 +1028,8 @@ tridiag_cluster_mb(const double* __restrict__ Asrc, int m, int symmetrize, doubl
   double* Wl = tsm;                        // m x nc, row j / local column c
   double* rowbuf = Wl + (size_t)m * nc;    // [2][m]  row k (all-gathered)
   double* pbuf = rowbuf + 2 * m;           // [2][m]  p (all-gathered)
-  double* vbuf = pbuf + 2 * m;             // [m]     v of the current step
-  double* dotbuf = vbuf + m;               // [2][16] per-CTA shares of p'v
+  double* vbufs = pbuf + 2 * m;            // [2][m]  v of steps k (parity)
+  double* dotbuf = vbufs + 2 * m;          // [2][16] per-CTA shares of p'v
   double* red = dotbuf + 32;               // [G][nc]
   __shared__ double wdot[2];
   __shared__ double sc[2];
@@ -1057,124 +1057,129 @@ tridiag_cluster_mb(const double* __restrict__ Asrc, int m, int symmetrize, doubl
     const int r = x / ncl, c = x - (x / ncl) * ncl;
     st_async_f64(rowbuf + c0 + c, &mbB[0], r, Wl[c]);
   }
+  // warp 0: wait for row kk, form its reflector into vbufs[kk & 1], sc[kk & 1]
+  auto reflect = [&](int kk) {
+    const int bb = kk & 1;
+    if (lane == 0) mb_expect(&mbB[bb], 8u * (uint32_t)(m - kk));
+    mb_wait(&mbB[bb], (uint32_t)((kk >> 1) & 1));
+    const double* row = rowbuf + bb * m;
+    double* vb = vbufs + bb * m;
+    double ss = 0.0;
+    for (int i = kk + 2 + lane; i < m; i += 32) ss = fma(row[i], row[i], ss);
+    ss = warp_sum(ss);
+    const double alpha = row[kk + 1];
+    double tk = 0.0, scale = 0.0, beta = alpha;
+    if (ss != 0.0) {
+      beta = -copysign(sqrt(alpha * alpha + ss), alpha);
+      tk = (beta - alpha) / beta;
+      scale = 1.0 / (alpha - beta);
+    }
+    for (int i = kk + 1 + lane; i < m; i += 32) vb[i] = i == kk + 1 ? 1.0 : row[i] * scale;
+    if (lane == 0) {
+      sc[bb] = tk;
+      if (rank == 0) {
+        d[kk] = row[kk];
+        e[kk] = beta;
+        tau[kk] = tk;
+      }
+    }
+  };
+  if (warp == 0 && m > 2) reflect(0);
   uint32_t useA0 = 0, useA1 = 0;
   for (int k = 0; k + 2 < m; ++k) {
     const int b = k & 1;
-    const double* row = rowbuf + b * m;
     double* pb = pbuf + b * m;
     double* nextrow = rowbuf + (b ^ 1) * m;
-    __syncthreads();  // every thread is done with vbuf / sc of step k-1
-    if (tid == 0) mb_expect(&mbB[b], 8u * (uint32_t)(m - k));
-    mb_wait(&mbB[b], (uint32_t)((k >> 1) & 1));  // row k has arrived
-    // (1) reflector of row k (warp 0), v into vbuf
-    if (warp == 0) {
-      double ss = 0.0;
-      for (int i = k + 2 + lane; i < m; i += 32) ss = fma(row[i], row[i], ss);
-      ss = warp_sum(ss);
-      const double alpha = row[k + 1];
-      double tk = 0.0, scale = 0.0, beta = alpha;
-      if (ss != 0.0) {
-        beta = -copysign(sqrt(alpha * alpha + ss), alpha);
-        tk = (beta - alpha) / beta;
-        scale = 1.0 / (alpha - beta);
-      }
-      for (int i = k + 1 + lane; i < m; i += 32) vbuf[i] = i == k + 1 ? 1.0 : row[i] * scale;
-      if (lane == 0) {
-        sc[0] = tk;
-        if (rank == 0) {
-          d[k] = row[k];
-          e[k] = beta;
-          tau[k] = tk;
-        }
-      }
-    }
-    __syncthreads();
-    const double tk = sc[0];
+    const double* vbuf = vbufs + b * m;
+    __syncthreads();  // reflector k in vbufs[b]; every update of step k-1 is done
+    const double tk = sc[b];
     const int j0 = k + 1 + g;
     const bool own = active && icol > k;
     if (tid < ncl && icol > k) V[(int64_t)k * m + icol] = vbuf[icol];
-    if (tk == 0.0) {  // identity reflector: row k+1 is unchanged, pass it on
-      if (tid < ncl && icol > k) {
-        const double wv = Wl[(k + 1) * nc + tid];
-        for (int r = 0; r < C; ++r) st_async_f64(nextrow + icol, &mbB[b ^ 1], r, wv);
+    if (tk != 0.0) {
+      // (2) p = tau W v on own columns
+      if (own) {
+        double a0 = 0.0, a1 = 0.0;
+        const double* wp = Wl + j0 * nc + lc;
+        const double* vp = vbuf + j0;
+        const int step = G * nc;
+        int j = j0;
+        for (; j + G < m; j += 2 * G, wp += 2 * step, vp += 2 * G) {
+          a0 = fma(wp[0], vp[0], a0);
+          a1 = fma(wp[step], vp[G], a1);
+        }
+        if (j < m) a0 = fma(wp[0], vp[0], a0);
+        red[g * nc + lc] = a0 + a1;
       }
-      continue;
-    }
-    // (2) p = tau W v on own columns
-    if (own) {
-      double a0 = 0.0, a1 = 0.0;
-      const double* wp = Wl + j0 * nc + lc;
-      const double* vp = vbuf + j0;
-      const int step = G * nc;
-      int j = j0;
-      for (; j + G < m; j += 2 * G, wp += 2 * step, vp += 2 * G) {
-        a0 = fma(wp[0], vp[0], a0);
-        a1 = fma(wp[step], vp[G], a1);
+      __syncthreads();
+      if (tid < 64) {
+        double pv = 0.0;
+        if (tid < ncl && icol > k) {
+          double sacc = 0.0;
+          const int gmax = min(G, m - (k + 1));  // groups that saw a row
+          for (int q = 0; q < gmax; ++q) sacc += red[q * nc + tid];
+          const double p = tk * sacc;
+          pv = p * vbuf[icol];
+          for (int r = 0; r < C; ++r) st_async_f64(pb + icol, &mbA[b], r, p);
+        }
+        pv = warp_sum(pv);
+        if (lane == 0) wdot[tid >> 5] = pv;
+        asm volatile("bar.sync 1, 64;\n" ::: "memory");
+        if (tid < C) st_async_f64(dotbuf + b * 16 + rank, &mbA[b], tid, wdot[0] + wdot[1]);
       }
-      if (j < m) a0 = fma(wp[0], vp[0], a0);
-      red[g * nc + lc] = a0 + a1;
-    }
-    __syncthreads();
-    if (tid < 64) {
-      double pv = 0.0;
-      if (tid < ncl && icol > k) {
-        double sacc = 0.0;
-        const int gmax = min(G, m - (k + 1));  // groups that saw a row
-        for (int q = 0; q < gmax; ++q) sacc += red[q * nc + tid];
-        const double p = tk * sacc;
-        pv = p * vbuf[icol];
-        for (int r = 0; r < C; ++r) st_async_f64(pb + icol, &mbA[b], r, p);
+      if (tid == 0) mb_expect(&mbA[b], 8u * (uint32_t)(m - k - 1 + C));
+      {
+        const uint32_t u = b ? useA1 : useA0;
+        mb_wait(&mbA[b], u & 1u);
+        if (b) ++useA1; else ++useA0;
       }
-      pv = warp_sum(pv);
-      if (lane == 0) wdot[tid >> 5] = pv;
-      asm volatile("bar.sync 1, 64;\n" ::: "memory");
-      if (tid < C) st_async_f64(dotbuf + b * 16 + rank, &mbA[b], tid, wdot[0] + wdot[1]);
-    }
-    if (tid == 0) mb_expect(&mbA[b], 8u * (uint32_t)(m - k - 1 + C));
-    {
-      const uint32_t u = b ? useA1 : useA0;
-      mb_wait(&mbA[b], u & 1u);
-      if (b) ++useA1; else ++useA0;
-    }
-    // (3) rank-2 update of own columns, push row k+1
-    if (own) {
-      double tot = 0.0;
-      for (int r = 0; r < C; ++r) tot += dotbuf[b * 16 + r];
-      const double K = 0.5 * tk * tot;
-      const double vi = vbuf[icol];
-      const double wi = fma(-K, vi, pb[icol]);
-      double* wp = Wl + j0 * nc + lc;
-      const double* vp = vbuf + j0;
-      const double* pp = pb + j0;
-      const int step = G * nc;
-      int j = j0;
-      if (g == 0) {  // row k+1 goes to every CTA for the next reflector
-        const double wj = fma(-K, vp[0], pp[0]);
-        const double wv = fma(-vp[0], wi, fma(-wj, vi, wp[0]));
-        wp[0] = wv;
-        for (int r = 0; r < C; ++r) st_async_f64(nextrow + icol, &mbB[b ^ 1], r, wv);
-        j += G, wp += step, vp += G, pp += G;
-      }
+      // (3) rank-2 update of own columns; row k+1 first, pushed to every CTA
+      if (own) {
+        double tot = 0.0;
+        for (int r = 0; r < C; ++r) tot += dotbuf[b * 16 + r];
+        const double K = 0.5 * tk * tot;
+        const double vi = vbuf[icol];
+        const double wi = fma(-K, vi, pb[icol]);
+        double* wp = Wl + j0 * nc + lc;
+        const double* vp = vbuf + j0;
+        const double* pp = pb + j0;
+        const int step = G * nc;
+        int j = j0;
+        if (g == 0) {
+          const double wj = fma(-K, vp[0], pp[0]);
+          const double wv = fma(-vp[0], wi, fma(-wj, vi, wp[0]));
+          wp[0] = wv;
+          for (int r = 0; r < C; ++r) st_async_f64(nextrow + icol, &mbB[b ^ 1], r, wv);
+          j += G, wp += step, vp += G, pp += G;
+        }
 #pragma unroll 2
-      for (; j < m; j += G, wp += step, vp += G, pp += G) {
-        const double vj = vp[0];
-        const double wj = fma(-K, vj, pp[0]);
-        wp[0] = fma(-vj, wi, fma(-wj, vi, wp[0]));
+        for (; j < m; j += G, wp += step, vp += G, pp += G) {
+          const double vj = vp[0];
+          const double wj = fma(-K, vj, pp[0]);
+          wp[0] = fma(-vj, wi, fma(-wj, vi, wp[0]));
+        }
       }
+    } else if (tid < ncl && icol > k) {  // identity reflector: row k+1 is unchanged, pass it on
+      const double wv = Wl[(k + 1) * nc + tid];
+      for (int r = 0; r < C; ++r) st_async_f64(nextrow + icol, &mbB[b ^ 1], r, wv);
     }
+    // warp 0 forms the next reflector while the other warps finish their updates
+    if (warp == 0 && k + 3 < m) reflect(k + 1);
   }
   if (m >= 2) {
     const int kk = m - 2;  // row m-2 was pushed at step m-3 (or at init when m == 2)
     __syncthreads();
-    if (tid == 0) mb_expect(&mbB[kk & 1], 8u * (uint32_t)(m - kk));
-    mb_wait(&mbB[kk & 1], (uint32_t)((kk >> 1) & 1));
-    const double* row = rowbuf + (kk & 1) * m;
-    if (rank == 0 && tid == 0) {
-      d[m - 2] = row[m - 2];
-      e[m - 2] = row[m - 1];
-      tau[m - 2] = 0.0;
-      tau[m - 1] = 0.0;
-      e[m - 1] = 0.0;
+    if (warp == 0) {
+      if (lane == 0) mb_expect(&mbB[kk & 1], 8u * (uint32_t)(m - kk));
+      mb_wait(&mbB[kk & 1], (uint32_t)((kk >> 1) & 1));
+      const double* row = rowbuf + (kk & 1) * m;
+      if (rank == 0 && lane == 0) {
+        d[m - 2] = row[m - 2];
+        e[m - 2] = row[m - 1];
+        tau[m - 2] = 0.0;
+        tau[m - 1] = 0.0;
+        e[m - 1] = 0.0;
+      }
     }
     if (tid == 0 && m - 1 >= c0 && m - 1 < c0 + ncl) d[m - 1] = Wl[(m - 1) * nc + (m - 1 - c0)];
   }
@@ -1348,7 +1353,7 @@ int tridiag_cluster_size(int m) {
 
 size_t tridiag_cluster_smem(int m, int C) {
   const int nc = (m + C - 1) / C;
-  return sizeof(double) * ((size_t)m * nc + 5 * (size_t)m + 32 + (size_t)(TCT / nc) * nc);
+  return sizeof(double) * ((size_t)m * nc + 6 * (size_t)m + 32 + (size_t)(TCT / nc) * nc);
 }
 
 void launch_tridiag(const double* Asrc, int m, int symmetrize, double* Wg, double* V, double* tau,
