@@ -1186,6 +1186,189 @@ tridiag_cluster_mb(const double* __restrict__ Asrc, int m, int symmetrize, doubl
   cluster_sync_all();  // no CTA leaves while its shared memory can still be written
 }
 
+// One exchange per step. Exchange E_k carries p_k = tau_k W v_k (own columns),
+// each CTA's share of p_k'v_k, and each CTA's slice of row k+1 BEFORE update k.
+// Every CTA then forms w_k = p_k - K v_k for all indices, applies update k to
+// the gathered row k+1 itself (the same fma the owner uses, so the copies agree
+// bit for bit) and computes reflector k+1 redundantly; one fused pass over its
+// own columns applies update k and accumulates p_{k+1} with v_{k+1}; the row
+// k+2 slice falls out of the same pass. The exchange parity buffers are safe to
+// reuse because E_{k+1} can only be sent after every CTA sent E_k.
+__global__ void __launch_bounds__(TCT)
+tridiag_fused(const double* __restrict__ Asrc, int m, int symmetrize, double* __restrict__ V,
+              double* __restrict__ tau, double* __restrict__ d, double* __restrict__ e,
+              const SmallStatus* status) {
+  if (status && (status->nonfinite || status->not_pd)) return;  // uniform over the cluster
+  unsigned rank_u, csize_u;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;\n" : "=r"(rank_u));
+  asm volatile("mov.u32 %0, %%cluster_nctarank;\n" : "=r"(csize_u));
+  const int rank = (int)rank_u, C = (int)csize_u;
+  const int nc = (m + C - 1) / C;
+  const int c0 = rank * nc;
+  const int ncl = max(0, min(m, c0 + nc) - c0);
+  extern __shared__ double tsm[];
+  double* Wl = tsm;                        // m x nc, row j / local column c
+  double* xrow = Wl + (size_t)m * nc;      // [2][m] gathered row slices (row k+1 before update k)
+  double* xp = xrow + 2 * m;               // [2][m] gathered p
+  double* vb = xp + 2 * m;                 // [2][m] v_k by parity
+  double* wv = vb + 2 * m;                 // [m]    w_k
+  double* xdot = wv + m;                   // [2][16]
+  double* red = xdot + 32;                 // [G][nc]
+  __shared__ double wdot[2];
+  __shared__ double sc[4];  // tau by parity
+  __shared__ __align__(8) uint64_t mbE[2], mbI;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int G = TCT / nc;
+  const int g = tid / nc, lc = tid - (tid / nc) * nc;
+  const bool active = g < G && lc < ncl;
+  const int icol = c0 + lc;
+  if (tid == 0) {
+    mb_init(&mbE[0], 1);
+    mb_init(&mbE[1], 1);
+    mb_init(&mbI, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  for (int x = tid; x < m * ncl; x += TCT) {
+    const int j = x / ncl, c = x - (x / ncl) * ncl, i = c0 + c;
+    const double a = Asrc[(int64_t)j * m + i];
+    Wl[j * nc + c] = symmetrize ? 0.5 * (a + Asrc[(int64_t)i * m + j]) : a;
+    V[(int64_t)j * m + i] = 0.0;
+  }
+  cluster_sync_all();
+  // row 0 to everyone (reflector 0), into xrow[1] (free until E_1)
+  for (int x = tid; x < ncl * C; x += TCT) {
+    const int r = x / ncl, c = x - (x / ncl) * ncl;
+    st_async_f64(xrow + m + c0 + c, &mbI, r, Wl[c]);
+  }
+  // warp 0: Householder reflector of a gathered row `row` at step kk -> vb[kk&1], sc
+  auto reflect = [&](const double* row, int kk) {
+    double ss = 0.0;
+    for (int i = kk + 2 + lane; i < m; i += 32) ss = fma(row[i], row[i], ss);
+    ss = warp_sum(ss);
+    const double alpha = row[kk + 1];
+    double tk = 0.0, scale = 0.0, beta = alpha;
+    if (ss != 0.0) {
+      beta = -copysign(sqrt(alpha * alpha + ss), alpha);
+      tk = (beta - alpha) / beta;
+      scale = 1.0 / (alpha - beta);
+    }
+    double* v = vb + (kk & 1) * m;
+    for (int i = kk + 1 + lane; i < m; i += 32) v[i] = i == kk + 1 ? 1.0 : row[i] * scale;
+    if (lane == 0) {
+      sc[kk & 1] = tk;
+      if (rank == 0) {
+        d[kk] = row[kk];
+        e[kk] = beta;
+        tau[kk] = tk;
+      }
+    }
+  };
+  // p_kk partial over own columns i > kk with v = vb[kk&1]; red + push E_kk (p, dot, row kk+1 slice)
+  auto push_exchange = [&](int kk, double acc, double rowslice) {
+    const int bb = kk & 1;
+    if (active && icol > kk) red[g * nc + lc] = acc;
+    __syncthreads();
+    if (tid < 64) {
+      double pv = 0.0;
+      if (tid < ncl && icol > kk) {
+        double sacc = 0.0;  // every group wrote its slot (zero when it saw no row)
+        for (int q = 0; q < G; ++q) sacc += red[q * nc + tid];
+        const double p = sc[bb] * sacc;
+        pv = p * vb[bb * m + icol];
+        for (int r = 0; r < C; ++r) st_async_f64(xp + bb * m + icol, &mbE[bb], r, p);
+      }
+      pv = warp_sum(pv);
+      if (lane == 0) wdot[tid >> 5] = pv;
+      asm volatile("bar.sync 1, 64;\n" ::: "memory");
+      if (tid < C) st_async_f64(xdot + bb * 16 + rank, &mbE[bb], tid, wdot[0] + wdot[1]);
+    }
+    // row kk+1 slice (before update kk) from the g == 0 thread of each own column i > kk
+    if (active && g == 0 && icol > kk)
+      for (int r = 0; r < C; ++r) st_async_f64(xrow + bb * m + icol, &mbE[bb], r, rowslice);
+  };
+  if (m > 2) {
+    if (warp == 0) {
+      if (lane == 0) mb_expect(&mbI, 8u * (uint32_t)m);
+      mb_wait(&mbI, 0);
+      reflect(xrow + m, 0);
+    }
+    __syncthreads();
+    // pass 0: p_0 = tau_0 A v_0 on own columns, row 1 slice
+    double acc = 0.0, rs = 0.0;
+    if (active && icol > 0) {
+      const double* v = vb;
+      for (int j = 1 + g; j < m; j += G) acc = fma(Wl[j * nc + lc], v[j], acc);
+      rs = Wl[1 * nc + lc];
+      if (icol >= 1 && tid < ncl) V[icol] = v[icol];
+    }
+    push_exchange(0, acc, rs);
+  }
+  for (int k = 0; k + 2 < m; ++k) {
+    const int b = k & 1;
+    if (tid == 0) mb_expect(&mbE[b], 8u * (uint32_t)(2 * (m - k - 1) + C));
+    mb_wait(&mbE[b], (uint32_t)((k >> 1) & 1));
+    const double tk = sc[b];
+    const double* v = vb + b * m;
+    const double* pk = xp + b * m;
+    double tot = 0.0;
+    for (int r = 0; r < C; ++r) tot += xdot[b * 16 + r];
+    const double K = 0.5 * tk * tot;
+    for (int j = k + 1 + tid; j < m; j += TCT) wv[j] = fma(-K, v[j], pk[j]);
+    __syncthreads();
+    const bool more = k + 3 < m;  // a reflector k+1 exists
+    if (warp == 0) {
+      // updated row k+1 (entries i >= k+1), as the owner's fused pass computes them
+      double* row = xrow + b * m;
+      const double wk1 = wv[k + 1];
+      for (int i = k + 1 + lane; i < m; i += 32)
+        row[i] = fma(-1.0, wv[i], fma(-wk1, v[i], row[i]));
+      __syncwarp();
+      if (more) {
+        reflect(row, k + 1);
+      } else if (rank == 0 && lane == 0) {  // k + 1 == m - 2: the last 2x2 block
+        d[m - 2] = row[m - 2];
+        e[m - 2] = row[m - 1];
+        tau[m - 2] = 0.0;
+        tau[m - 1] = 0.0;
+        e[m - 1] = 0.0;
+      }
+    }
+    __syncthreads();
+    // fused pass: update k on own columns i > k, p_{k+1} with v_{k+1}, row k+2 slice
+    const double* vn = vb + (b ^ 1) * m;
+    double acc = 0.0, rs = 0.0;
+    if (active && icol > k) {
+      const double vi = v[icol], wi = wv[icol];
+      const bool pcol = more && icol > k + 1;
+      for (int j = k + 1 + g; j < m; j += G) {
+        double* wp = Wl + j * nc + lc;
+        const double nw = fma(-v[j], wi, fma(-wv[j], vi, wp[0]));
+        wp[0] = nw;
+        if (pcol && j > k + 1) acc = fma(nw, vn[j], acc);
+        if (j == k + 2) rs = nw;
+      }
+      if (more && tid < ncl && icol > k + 1) V[(int64_t)(k + 1) * m + icol] = vn[icol];
+    }
+    if (more) {
+      // the row k+2 slice is produced by the thread whose j loop visited j = k+2;
+      // route it to the g == 0 thread of the column through red's last slot use
+      // (the (j - k - 1) % G == 1 group): stage it in wv-free scratch via red
+      __syncthreads();
+      const int gsrc = 1 % G;  // j = k + 2 is visited by group (k+2 - (k+1)) % G
+      if (active && g == gsrc && icol > k + 1) red[lc] = rs;
+      __syncthreads();
+      const double row2 = (active && g == 0 && icol > k + 1) ? red[lc] : 0.0;
+      __syncthreads();
+      push_exchange(k + 1, (active && icol > k + 1) ? acc : 0.0, row2);
+    }
+  }
+  if (m >= 2 && tid == 0 && m - 1 >= c0 && m - 1 < c0 + ncl) d[m - 1] = Wl[(m - 1) * nc + (m - 1 - c0)];
+  if (m == 2 && rank == 0 && tid == 0) {
+    d[0] = Wl[0];
+  }
+  cluster_sync_all();  // no CTA leaves while its shared memory can still be written
+}
+
 // Cholesky + inverse for kCholLdlMax < m <= kCholClusterMax: the packed
 // array of chol_ldl (L' in the lower triangle, the unit-lower inverse
 // transposed in the upper one) is split by columns over the CTAs of a cluster.
@@ -1353,7 +1536,7 @@ int tridiag_cluster_size(int m) {
 
 size_t tridiag_cluster_smem(int m, int C) {
   const int nc = (m + C - 1) / C;
-  return sizeof(double) * ((size_t)m * nc + 6 * (size_t)m + 32 + (size_t)(TCT / nc) * nc);
+  return sizeof(double) * ((size_t)m * nc + 7 * (size_t)m + 32 + (size_t)(TCT / nc) * nc);
 }
 
 void launch_tridiag(const double* Asrc, int m, int symmetrize, double* Wg, double* V, double* tau,
@@ -1365,6 +1548,8 @@ void launch_tridiag(const double* Asrc, int m, int symmetrize, double* Wg, doubl
       cudaFuncSetAttribute(tridiag_cluster, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
       cudaFuncSetAttribute(tridiag_cluster_mb, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
       cudaFuncSetAttribute(tridiag_cluster_mb, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+      cudaFuncSetAttribute(tridiag_fused, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+      cudaFuncSetAttribute(tridiag_fused, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
       attr = true;
     }
     cudaLaunchConfig_t cfg = {};
@@ -1379,11 +1564,13 @@ void launch_tridiag(const double* Asrc, int m, int symmetrize, double* Wg, doubl
     at[0].val.clusterDim.z = 1;
     cfg.attrs = at;
     cfg.numAttrs = 1;
-    static const bool sync_variant = getenv("SPB_TRI_SYNC") != nullptr;  // A/B switch
-    if (sync_variant)
+    static const int variant = getenv("SPB_TRI_VARIANT") ? atoi(getenv("SPB_TRI_VARIANT")) : 1;
+    if (variant == 0)
       cudaLaunchKernelEx(&cfg, tridiag_cluster, Asrc, m, symmetrize, V, tau, d, e, status);
-    else
+    else if (variant == 1)
       cudaLaunchKernelEx(&cfg, tridiag_cluster_mb, Asrc, m, symmetrize, V, tau, d, e, status);
+    else
+      cudaLaunchKernelEx(&cfg, tridiag_fused, Asrc, m, symmetrize, V, tau, d, e, status);
     return;
   }
   const int rows = (m + 31) / 32;
