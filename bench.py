@@ -189,12 +189,24 @@ def count_launches(step_fn):
         torch.cuda.synchronize()
     ours = 0
     total = 0
+    per = {}
     for ev in prof.events():
         if ev.device_type is not None and str(ev.device_type).endswith("CUDA"):
             total += 1
             if "spb::" in ev.name:
                 ours += 1
-    return ours, total
+                name = ev.name.replace("(anonymous namespace)::", "").split("(")[0]
+                name = name.replace("void ", "").replace("spb::", "")
+                t = getattr(ev, "device_time_total", None)
+                if t is None:
+                    t = ev.cuda_time_total
+                a = per.setdefault(name, [0.0, 0])
+                a[0] += t
+                a[1] += 1
+    tot = sum(v[0] for v in per.values()) or 1.0
+    shares = {k: {"share": round(v[0] / tot, 4), "launches": v[1], "us": round(v[0], 1)}
+              for k, v in sorted(per.items(), key=lambda kv: -kv[1][0])[:10]}
+    return ours, total, shares
 
 
 def ten_x_tol(spb, g, x0, l, k, precision):
@@ -361,7 +373,9 @@ def run_ours(args):
         t = torch.tensor([sum(e2e_times)], dtype=torch.float64, device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         e2e_value = e2e_iters * (1 if sharded else world) / float(t.item())
-    launches_per_step = count_launches(step_device)[0] if not sharded else None
+    launches_per_step, shares = None, None
+    if not sharded:
+        launches_per_step, _, shares = count_launches(step_device)
     out = None
     if rank == 0:
         pm = spb.partition_match(spb.contingency(truth, part.labels if hasattr(part, "labels") else part))
@@ -393,12 +407,16 @@ def run_ours(args):
                          "gather_model": {"achieved": gather_achieved,
                                           "frac": (gather_achieved / peak) if gather_achieved else None,
                                           "bytes_model": "compulsory + esz*nnz*cols"},
-                         "gram": gram},
+                         "gram": gram,
+                         "note": ("roofline of the path's HBM-streaming kernel (SpMM) and of the "
+                                  "Rayleigh-Ritz Gram (DMMA); the step's time split by kernel is "
+                                  "kernel_shares (latency-bound small dense solves dominate at C1/C2)")},
             "cpu_baseline": cpu,
             "e2e": {"value": e2e_value, "unit": UNIT,
                     "h2d_bytes_per_step": int(edges.nbytes + x0.nbytes),
                     "d2h_bytes_per_step": int(4 * spec.n + 16 * l)},
             "gpu_launches": int(launches_per_step * args.steps) if launches_per_step is not None else None,
+            "kernel_shares": shares,
             "clocks": clk.summary(),
             "partition_seconds": t_ms / args.steps / 1e3,
             "e2e_partition_seconds": sum(e2e_times) / args.steps,

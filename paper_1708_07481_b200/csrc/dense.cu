@@ -395,8 +395,11 @@ __global__ void sum_splits(const double* __restrict__ part, int ksplit, int64_t 
 }
 
 int choose_ksplit(int64_t n, int tiles) {
-  // one full wave of the DMMA Gram (3 CTAs per SM): tiles * ks <= 3 * SMs
-  const int target = 3 * num_sms();
+  // one full wave of the DMMA Gram (3 CTAs per SM): tiles * ks <= 3 * SMs; the
+  // per-SM work is the same for fewer, longer splits, but the fixed-order
+  // reduction reads ks partial tiles, so SPB_GRAM_WAVE can trade the two
+  static const int per_sm = getenv("SPB_GRAM_WAVE") ? atoi(getenv("SPB_GRAM_WAVE")) : 3;
+  const int target = std::max(1, per_sm) * num_sms();
   int64_t ks = std::max<int64_t>(1, target / std::max(tiles, 1));
   ks = std::min<int64_t>(ks, ceil_div(n, 512));
   return (int)std::max<int64_t>(ks, 1);
