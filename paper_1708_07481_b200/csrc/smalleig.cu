@@ -1630,13 +1630,40 @@ __global__ void bisect(const double* __restrict__ d, const double* __restrict__ 
     const double tol = fmax(2.0 * kEps64 * fmax(fabs(a), fabs(b)), kEps64 * tnorm) + pivmin;
     if (w <= tol) break;
     const double x = a + w * (double)(lane + 1) / 33.0;
-    double q = sd[0] - x;
-    if (fabs(q) < pivmin) q = -pivmin;
-    int c = q < 0.0;
-    for (int i = 1; i < m; ++i) {
-      q = use_div ? (sd[i] - x) - se2[i - 1] / q : (sd[i] - x) - se2[i - 1] * __drcp_rn(q);
+    int c;
+    if (use_div == 2) {
+      // division-free three-term Sturm sequence p_i = (d_i - x) p_{i-1} - e_{i-1}^2 p_{i-2}
+      // with exact power-of-two rescaling; a pivot p_i / p_{i-1} below pivmin in
+      // magnitude is taken as -pivmin, as in the ratio form
+      double p0 = 1.0, p1 = sd[0] - x;
+      if (fabs(p1) < pivmin) p1 = -pivmin;
+      c = p1 < 0.0;
+#pragma unroll 8
+      for (int i = 1; i < m; ++i) {
+        double p2 = fma(sd[i] - x, p1, -se2[i - 1] * p0);
+        if (fabs(p2) < pivmin * fabs(p1)) p2 = -pivmin * p1;
+        c += (p2 < 0.0) != (p1 < 0.0);
+        p0 = p1;
+        p1 = p2;
+        if (fabs(p1) > 0x1p500 || fabs(p1) < 0x1p-500) {
+          int ex;
+          frexp(p1, &ex);
+          p1 = ldexp(p1, -ex);
+          p0 = ldexp(p0, -ex);
+        }
+      }
+    } else {
+      double q = sd[0] - x;
       if (fabs(q) < pivmin) q = -pivmin;
-      c += q < 0.0;
+      c = q < 0.0;
+      // unrolled so the shared-memory loads of later steps issue ahead of the
+      // division chain (warps issue in order)
+#pragma unroll 8
+      for (int i = 1; i < m; ++i) {
+        q = use_div ? (sd[i] - x) - se2[i - 1] / q : (sd[i] - x) - se2[i - 1] * __drcp_rn(q);
+        if (fabs(q) < pivmin) q = -pivmin;
+        c += q < 0.0;
+      }
     }
     const unsigned bal = __ballot_sync(0xffffffffu, c > idx);
     const double x31 = __shfl_sync(0xffffffffu, x, 31);
@@ -1653,11 +1680,126 @@ __global__ void bisect(const double* __restrict__ d, const double* __restrict__ 
   if (lane == 0) theta[t] = 0.5 * (a + b);
 }
 
+// Sturm count of T - x I: the number of eigenvalues below x.
+__device__ __forceinline__ int sturm_count(const double* sd, const double* se2, int m, double x,
+                                           double pivmin, int mode) {
+  int c;
+  if (mode == 2) {
+    // division-free three-term recurrence p_i = (d_i - x) p_{i-1} - e_{i-1}^2 p_{i-2},
+    // exact power-of-two rescaling; a pivot p_i / p_{i-1} below pivmin in magnitude
+    // is taken as -pivmin, as in the ratio form
+    double p0 = 1.0, p1 = sd[0] - x;
+    if (fabs(p1) < pivmin) p1 = -pivmin;
+    c = p1 < 0.0;
+#pragma unroll 8
+    for (int i = 1; i < m; ++i) {
+      double p2 = fma(sd[i] - x, p1, -se2[i - 1] * p0);
+      if (fabs(p2) < pivmin * fabs(p1)) p2 = -pivmin * p1;
+      c += (p2 < 0.0) != (p1 < 0.0);
+      p0 = p1;
+      p1 = p2;
+      if (fabs(p1) > 0x1p500 || fabs(p1) < 0x1p-500) {
+        int ex;
+        frexp(p1, &ex);
+        p1 = ldexp(p1, -ex);
+        p0 = ldexp(p0, -ex);
+      }
+    }
+  } else {
+    double q = sd[0] - x;
+    if (fabs(q) < pivmin) q = -pivmin;
+    c = q < 0.0;
+#pragma unroll 8
+    for (int i = 1; i < m; ++i) {
+      q = mode ? (sd[i] - x) - se2[i - 1] / q : (sd[i] - x) - se2[i - 1] * __drcp_rn(q);
+      if (fabs(q) < pivmin) q = -pivmin;
+      c += q < 0.0;
+    }
+  }
+  return c;
+}
+
+// One CTA of BSW warps per eigenvalue index (first + blockIdx.x): (32 BSW + 1)-
+// section of the Gershgorin interval, so a round narrows the bracket 257-fold at
+// BSW = 8 (about 7 rounds to full precision instead of 11 with one warp).
+constexpr int BSW = 8;
+
+__global__ void __launch_bounds__(32 * BSW)
+bisect_cta(const double* __restrict__ d, const double* __restrict__ e, int m, int first,
+           int count, double* __restrict__ theta, const SmallStatus* status, int mode) {
+  extern __shared__ double bsd[];  // d[m], e2[m]
+  __shared__ int wfirst[2][BSW];
+  __shared__ double red3[3][BSW];
+  if (status && (status->nonfinite || status->not_pd)) return;
+  double* sd = bsd;
+  double* se2 = bsd + m;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  constexpr int P = 32 * BSW;
+  double lo = DBL_MAX, hi = -DBL_MAX, emax = 0.0;
+  for (int i = tid; i < m; i += P) {
+    const double di = d[i];
+    sd[i] = di;
+    se2[i] = i + 1 < m ? e[i] * e[i] : 0.0;
+    const double r = (i > 0 ? fabs(e[i - 1]) : 0.0) + (i + 1 < m ? fabs(e[i]) : 0.0);
+    lo = fmin(lo, di - r);
+    hi = fmax(hi, di + r);
+    if (i + 1 < m) emax = fmax(emax, e[i] * e[i]);
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    lo = fmin(lo, __shfl_xor_sync(0xffffffffu, lo, o));
+    hi = fmax(hi, __shfl_xor_sync(0xffffffffu, hi, o));
+    emax = fmax(emax, __shfl_xor_sync(0xffffffffu, emax, o));
+  }
+  if (lane == 0) {
+    red3[0][warp] = lo;
+    red3[1][warp] = hi;
+    red3[2][warp] = emax;
+  }
+  __syncthreads();
+  lo = red3[0][0];
+  hi = red3[1][0];
+  emax = red3[2][0];
+  for (int w2 = 1; w2 < BSW; ++w2) {
+    lo = fmin(lo, red3[0][w2]);
+    hi = fmax(hi, red3[1][w2]);
+    emax = fmax(emax, red3[2][w2]);
+  }
+  const int idx = first + blockIdx.x;
+  if (blockIdx.x >= count) return;
+  const double pivmin = DBL_MIN * fmax(1.0, emax);
+  const double tnorm = fmax(fabs(lo), fabs(hi));
+  lo -= 2.0 * kEps64 * tnorm + 2.0 * pivmin;
+  hi += 2.0 * kEps64 * tnorm + 2.0 * pivmin;
+  double a = lo, b = hi;
+  for (int round = 0; round < 64; ++round) {
+    const double w = b - a;
+    const double tol = fmax(2.0 * kEps64 * fmax(fabs(a), fabs(b)), kEps64 * tnorm) + pivmin;
+    if (w <= tol) break;
+    const double x = a + w * (double)(tid + 1) / (double)(P + 1);
+    const int c = sturm_count(sd, se2, m, x, pivmin, mode);
+    const unsigned bal = __ballot_sync(0xffffffffu, c > idx);
+    if (lane == 0) wfirst[round & 1][warp] = bal ? warp * 32 + __ffs(bal) - 1 : INT_MAX;
+    __syncthreads();
+    int f = INT_MAX;
+    for (int w2 = 0; w2 < BSW; ++w2) f = min(f, wfirst[round & 1][w2]);
+    if (f == INT_MAX) {
+      a = a + w * (double)P / (double)(P + 1);
+    } else {
+      const double xf = a + w * (double)(f + 1) / (double)(P + 1);
+      const double xp = a + w * (double)f / (double)(P + 1);
+      b = xf;
+      if (f > 0) a = xp;
+    }
+  }
+  if (tid == 0) theta[blockIdx.x] = 0.5 * (a + b);
+}
+
 // Sturm pivots by true division (dstebz's arithmetic) unless SPB_BISECT_RCP is
 // set: the reciprocal variant is faster but its last-bit differences measurably
 // change long LOBPCG trajectories (tests/test_gpu_lobpcg.py rand150).
 int bisect_div() {
-  static const int v = getenv("SPB_BISECT_RCP") ? 0 : 1;
+  static const int v = getenv("SPB_BISECT_RCP") ? 0 : (getenv("SPB_BISECT_DIV") ? 1 : 2);
   return v;
 }
 
@@ -2292,9 +2434,8 @@ int sygv_enqueue(const double* ga, const double* gb, int ldg, int m, int nev, do
   launch_wy_tfactors(w.V, w.tau, m, w.scratch, status, side->s);  // overlaps bisect + invit
   SPB_CUDA(cudaEventRecord(side->join, side->s));
   {
-    const int warps = 8;
-    bisect<<<(int)ceil_div(nev, warps), warps * 32, 2 * sizeof(double) * (size_t)m, st>>>(
-        w.d, w.e, m, 0, nev, theta, nullptr, status, bisect_div());
+    bisect_cta<<<nev, 32 * BSW, 2 * sizeof(double) * (size_t)m, st>>>(w.d, w.e, m, 0, nev, theta,
+                                                                      status, bisect_div());
     SPB_LAUNCH_CHECK();
   }
   {
