@@ -1876,12 +1876,14 @@ __global__ void invit(const double* __restrict__ d, const double* __restrict__ e
         at(5, i) = 1.0;
       }
     }
-    for (int i = 0; i < m; ++i) {
-      const double v = at(1, i);
-      if (fabs(v) < pert) at(1, i) = copysign(pert, v == 0.0 ? 1.0 : v);
+    for (int i = 0; i < m; ++i) {  // tiny pivots perturbed; array 1 then holds 1/pivot
+      double v = at(1, i);
+      if (fabs(v) < pert) v = copysign(pert, v == 0.0 ? 1.0 : v);
+      at(1, i) = 1.0 / v;
     }
     for (int i = 0; i < m; ++i) at(4, i) = hash_uniform((uint32_t)j, (uint32_t)i);
     for (int it = 0; it < 2; ++it) {
+#pragma unroll 4
       for (int i = 0; i + 1 < m; ++i) {
         const double yi = at(4, i), yn = at(4, i + 1), f = at(0, i);
         if (at(5, i) != 0.0) {
@@ -1891,15 +1893,16 @@ __global__ void invit(const double* __restrict__ d, const double* __restrict__ e
           at(4, i + 1) = yn - f * yi;
         }
       }
-      double y2 = at(4, m - 1) / at(1, m - 1);
+      double y2 = at(4, m - 1) * at(1, m - 1);
       at(4, m - 1) = y2;
       double y1 = y2;
       if (m >= 2) {
-        y1 = (at(4, m - 2) - at(2, m - 2) * y2) / at(1, m - 2);
+        y1 = (at(4, m - 2) - at(2, m - 2) * y2) * at(1, m - 2);
         at(4, m - 2) = y1;
       }
+#pragma unroll 4
       for (int i = m - 3; i >= 0; --i) {
-        const double yi = (at(4, i) - at(2, i) * y1 - at(3, i) * y2) / at(1, i);
+        const double yi = (at(4, i) - at(2, i) * y1 - at(3, i) * y2) * at(1, i);
         at(4, i) = yi;
         y2 = y1;
         y1 = yi;
