@@ -1845,36 +1845,43 @@ __global__ void invit(const double* __restrict__ d, const double* __restrict__ e
     double lam = theta[j];
     if (j > j0 && lam - lam_prev < 10.0 * kEps64 * fabs(lam)) lam = lam_prev + 10.0 * kEps64 * fabs(lam);
     lam_prev = lam;
-    // LU with partial pivoting of T - lam I (dgttrf): 0 dl, 1 dd, 2 du, 3 du2, 4 y, 5 swap
-    for (int i = 0; i < m; ++i) {
-      at(1, i) = d[i] - lam;
-      at(0, i) = i + 1 < m ? e[i] : 0.0;
-      at(2, i) = i + 1 < m ? e[i] : 0.0;
-      at(3, i) = 0.0;
-      at(5, i) = 0.0;
-    }
-    for (int i = 0; i + 1 < m; ++i) {
-      double di = at(1, i);
-      const double li = at(0, i);
-      if (fabs(di) >= fabs(li)) {
-        if (di == 0.0) { di = pert; at(1, i) = di; }
-        const double f = li / di;
-        at(0, i) = f;
-        at(1, i + 1) -= f * at(2, i);
-      } else {
-        const double f = di / li;
-        at(1, i) = li;
-        at(0, i) = f;
-        const double tmp = at(2, i);
-        const double dn = at(1, i + 1);
-        at(2, i) = dn;
-        at(1, i + 1) = tmp - f * dn;
-        if (i + 2 < m) {
-          at(3, i) = at(2, i + 1);
-          at(2, i + 1) = -f * at(2, i + 1);
+    // LU with partial pivoting of T - lam I (dgttrf): 0 dl, 1 dd (then 1/dd), 2 du,
+    // 3 du2, 4 y, 5 swap. The running pivot and super-diagonal are carried in
+    // registers (the shared-memory round trip per step was the critical path).
+    {
+      double dcur = d[0] - lam;
+      double ucur = m > 1 ? e[0] : 0.0;
+#pragma unroll 2
+      for (int i = 0; i + 1 < m; ++i) {
+        const double li = e[i];
+        const double dn0 = d[i + 1] - lam;
+        const double un0 = i + 2 < m ? e[i + 1] : 0.0;
+        double di = dcur;
+        if (fabs(di) >= fabs(li)) {
+          if (di == 0.0) di = pert;
+          const double f = li / di;
+          at(0, i) = f;
+          at(1, i) = di;
+          at(2, i) = ucur;
+          at(3, i) = 0.0;
+          at(5, i) = 0.0;
+          dcur = dn0 - f * ucur;
+          ucur = un0;
+        } else {
+          const double f = di / li;
+          at(0, i) = f;
+          at(1, i) = li;
+          at(2, i) = dn0;
+          at(3, i) = un0;
+          at(5, i) = 1.0;
+          dcur = ucur - f * dn0;
+          ucur = -f * un0;
         }
-        at(5, i) = 1.0;
       }
+      at(1, m - 1) = dcur;
+      at(2, m - 1) = 0.0;
+      at(3, m - 1) = 0.0;
+      at(5, m - 1) = 0.0;
     }
     for (int i = 0; i < m; ++i) {  // tiny pivots perturbed; array 1 then holds 1/pivot
       double v = at(1, i);
@@ -1883,15 +1890,20 @@ __global__ void invit(const double* __restrict__ d, const double* __restrict__ e
     }
     for (int i = 0; i < m; ++i) at(4, i) = hash_uniform((uint32_t)j, (uint32_t)i);
     for (int it = 0; it < 2; ++it) {
+      {  // forward: row interchanges and L, running value in a register
+        double ycar = at(4, 0);
 #pragma unroll 4
-      for (int i = 0; i + 1 < m; ++i) {
-        const double yi = at(4, i), yn = at(4, i + 1), f = at(0, i);
-        if (at(5, i) != 0.0) {
-          at(4, i) = yn;
-          at(4, i + 1) = yi - f * yn;
-        } else {
-          at(4, i + 1) = yn - f * yi;
+        for (int i = 0; i + 1 < m; ++i) {
+          const double yn = at(4, i + 1), f = at(0, i);
+          if (at(5, i) != 0.0) {
+            at(4, i) = yn;
+            ycar = ycar - f * yn;
+          } else {
+            at(4, i) = ycar;
+            ycar = yn - f * ycar;
+          }
         }
+        at(4, m - 1) = ycar;
       }
       double y2 = at(4, m - 1) * at(1, m - 1);
       at(4, m - 1) = y2;
@@ -1913,6 +1925,7 @@ __global__ void invit(const double* __restrict__ d, const double* __restrict__ e
         for (int i = 0; i < m; ++i) at(4, i) -= sdot * Y[(size_t)i * ldy + q];
       }
       double amax = 0.0;
+#pragma unroll 4
       for (int i = 0; i < m; ++i) amax = fmax(amax, fabs(at(4, i)));
       if (amax == 0.0) {
         for (int i = 0; i < m; ++i) at(4, i) = hash_uniform((uint32_t)j + 7919u * (it + 1), (uint32_t)i);
@@ -1920,13 +1933,14 @@ __global__ void invit(const double* __restrict__ d, const double* __restrict__ e
       }
       const double ia = 1.0 / amax;
       double nrm = 0.0;
+#pragma unroll 4
       for (int i = 0; i < m; ++i) {
         const double v = at(4, i) * ia;
-        at(4, i) = v;
-        nrm += v * v;
+        nrm = fma(v, v, nrm);
       }
-      nrm = 1.0 / sqrt(nrm);
-      for (int i = 0; i < m; ++i) at(4, i) *= nrm;
+      const double sc2 = ia / sqrt(nrm);  // scale by 1/amax then by 1/norm, in one pass
+#pragma unroll 4
+      for (int i = 0; i < m; ++i) at(4, i) *= sc2;
     }
     for (int i = 0; i < m; ++i) Y[(size_t)i * ldy + j] = at(4, i);
   }
