@@ -1819,25 +1819,36 @@ __device__ __forceinline__ double hash_uniform(uint32_t a, uint32_t b) {
 // handled by its first thread, which orthogonalises later members against
 // earlier ones (MGS), as LAPACK dstein does with its (wider) 1e-3 ||T||; for
 // gaps above ctol inverse iteration alone gives orthogonality eps ||T|| / gap.
-__global__ void invit(const double* __restrict__ d, const double* __restrict__ e, int m, int nev,
+__global__ void invit(const double* __restrict__ d_g, const double* __restrict__ e_g, int m, int nev,
                       const double* __restrict__ theta, double* __restrict__ Y, int ldy,
                       double* __restrict__ gscratch, int use_smem, const SmallStatus* status) {
+  // One eigenvector (cluster head) per CTA of one warp: the lanes stage d, e in
+  // shared memory and reduce ||T||; lane 0 runs the serial recurrences.
   extern __shared__ double ssc[];
   if (status && (status->nonfinite || status->not_pd)) return;
-  const int j0 = blockIdx.x * blockDim.x + threadIdx.x;
+  const int j0 = blockIdx.x;
   if (j0 >= nev) return;
-  // scratch: shared memory [array][i][thread-in-block] when it fits, else global
-  double* scratch = use_smem ? ssc : gscratch;
-  const int NT = use_smem ? blockDim.x : gridDim.x * blockDim.x;
-  const int tsl = use_smem ? threadIdx.x : j0;
-  double tnorm = 0.0;
-  for (int i = 0; i < m; ++i)
-    tnorm = fmax(tnorm, fabs(d[i]) + (i > 0 ? fabs(e[i - 1]) : 0.0) + (i + 1 < m ? fabs(e[i]) : 0.0));
-  tnorm = fmax(tnorm, DBL_MIN);
+  const int lane = threadIdx.x & 31;
+  double* d = ssc;                 // m
+  double* e = ssc + m;             // m
+  double* scratch = ssc + 2 * m;   // 6 m
+  (void)gscratch;
+  (void)use_smem;
+  double tn = 0.0;
+  for (int i = lane; i < m; i += 32) {
+    const double di = d_g[i], ei = i + 1 < m ? e_g[i] : 0.0;
+    d[i] = di;
+    e[i] = ei;
+    tn = fmax(tn, fabs(di) + (i > 0 ? fabs(e_g[i - 1]) : 0.0) + fabs(ei));
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) tn = fmax(tn, __shfl_xor_sync(0xffffffffu, tn, o));
+  __syncwarp();
+  if (lane != 0) return;
+  const double tnorm = fmax(tn, DBL_MIN);
   const double ctol = 1e-8 * tnorm;
   if (j0 > 0 && theta[j0] - theta[j0 - 1] <= ctol) return;  // not a cluster head
-  // strided scratch: element i of array a for this thread at (a*m + i)*NT + j0
-  auto at = [&](int a, int i) -> double& { return scratch[((size_t)a * m + i) * NT + tsl]; };
+  auto at = [&](int a2, int i) -> double& { return scratch[a2 * m + i]; };
   const double pert = kEps64 * tnorm;
   double lam_prev = -DBL_MAX;
   for (int j = j0; j < nev; ++j) {
@@ -2456,22 +2467,8 @@ int sygv_enqueue(const double* ga, const double* gb, int ldg, int m, int nev, do
     SPB_LAUNCH_CHECK();
   }
   {
-    // a few eigenvectors per CTA: each thread's recurrences are serial and
-    // divergent (pivoting), so spreading them over SMs beats packing a warp;
-    // the scratch (6 m doubles per thread) must stay in shared memory
-    const size_t per_thread = 6 * (size_t)m * sizeof(double);
-    static const int tpb_env = getenv("SPB_INVIT_TPB") ? atoi(getenv("SPB_INVIT_TPB")) : 0;
-    int tpb = tpb_env > 0 ? tpb_env : 1;
-    while (tpb > 1 && per_thread * tpb > 200 * 1024) tpb >>= 1;
-    if (per_thread * tpb <= 200 * 1024) {
-      invit<<<(int)ceil_div(nev, tpb), tpb, per_thread * tpb, st>>>(w.d, w.e, m, nev, theta, w.Y,
-                                                                    nev, w.scratch, 1, status);
-    } else {
-      const int nt = (int)round_up(nev, 32);
-      const int blocks = (int)ceil_div(nt, 128);
-      invit<<<blocks, nt < 128 ? nt : 128, 0, st>>>(w.d, w.e, m, nev, theta, w.Y, nev, w.scratch,
-                                                   0, status);
-    }
+    invit<<<nev, 32, 8 * sizeof(double) * (size_t)m, st>>>(w.d, w.e, m, nev, theta, w.Y, nev,
+                                                           nullptr, 1, status);
   }
   SPB_LAUNCH_CHECK();
   SPB_CUDA(cudaStreamWaitEvent(st, side->join, 0));
