@@ -345,7 +345,7 @@ int launch_gram_cfg(GramBatch bb, int64_t n, int out_rows, int out_cols, double*
   }
   bb.tile_start[bb.njobs] = tiles;
   int64_t ks = std::max<int64_t>(1, (int64_t)ctas_per_sm * num_sms() / std::max(tiles, 1));
-  ks = std::min<int64_t>(ks, ceil_div(n, 512));
+  ks = std::min<int64_t>(ks, ceil_div(n, 128));
   ks = std::max<int64_t>(ks, 1);
   while (ks > 1 && (size_t)ks * out_rows * out_cols > partial_cap) --ks;
   if ((size_t)ks * out_rows * out_cols > partial_cap) {
@@ -382,16 +382,41 @@ int gram_tile_for(const GramBatch& b) {
   return (wmax > 64 && wmax <= 112 && wmin > 64) ? 112 : 64;
 }
 
-__global__ void sum_splits(const double* __restrict__ part, int ksplit, int64_t split_stride,
-                           int rows, int cols, int ldp, double* __restrict__ out, int ldo) {
+// Fixed-order reduction of the split-K partials: a CTA owns 32 consecutive
+// outputs (one per lane, coalesced); its 8 warps each sum a contiguous range of
+// splits and the 8 warp sums are added in warp order (deterministic).
+__global__ void __launch_bounds__(256)
+sum_splits(const double* __restrict__ part, int ksplit, int64_t split_stride, int rows, int cols,
+           int ldp, double* __restrict__ out, int ldo) {
+  __shared__ double ws[8][33];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int64_t total = (int64_t)rows * cols;
-  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
-       e += (int64_t)gridDim.x * blockDim.x) {
-    const int r = (int)(e / cols), c = (int)(e % cols);
+  const int kc = (ksplit + 7) / 8;
+  const int k0 = warp * kc, k1 = min(ksplit, k0 + kc);
+  for (int64_t base = (int64_t)blockIdx.x * 32; base < total; base += (int64_t)gridDim.x * 32) {
+    const int64_t e = base + lane;
     double s = 0.0;
-    for (int k = 0; k < ksplit; ++k) s += part[k * split_stride + (int64_t)r * ldp + c];
-    out[(int64_t)r * ldo + c] = s;
+    if (e < total) {
+      const int r = (int)(e / cols), c = (int)(e % cols);
+      const double* p = part + (int64_t)r * ldp + c;
+#pragma unroll 4
+      for (int k = k0; k < k1; ++k) s += p[(int64_t)k * split_stride];
+    }
+    ws[warp][lane] = s;
+    __syncthreads();
+    if (warp == 0 && e < total) {
+      double t = ws[0][lane];
+#pragma unroll
+      for (int w = 1; w < 8; ++w) t += ws[w][lane];
+      const int r = (int)(e / cols), c = (int)(e % cols);
+      out[(int64_t)r * ldo + c] = t;
+    }
+    __syncthreads();
   }
+}
+
+int sum_splits_grid(int64_t total) {
+  return (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(total, 32), (int64_t)num_sms() * 16));
 }
 
 int choose_ksplit(int64_t n, int tiles) {
@@ -401,7 +426,7 @@ int choose_ksplit(int64_t n, int tiles) {
   static const int per_sm = getenv("SPB_GRAM_WAVE") ? atoi(getenv("SPB_GRAM_WAVE")) : 3;
   const int target = std::max(1, per_sm) * num_sms();
   int64_t ks = std::max<int64_t>(1, target / std::max(tiles, 1));
-  ks = std::min<int64_t>(ks, ceil_div(n, 512));
+  ks = std::min<int64_t>(ks, ceil_div(n, 128));
   return (int)std::max<int64_t>(ks, 1);
 }
 
@@ -838,8 +863,8 @@ int gram_batched(int dtype, const GramBatch& b, int64_t n, int out_rows, int out
     SPB_CUDA(cudaMemsetAsync(partial, 0, sizeof(double) * stride, st));
     ks = 1;
   }
-  sum_splits<<<grid_1d(stride), 256, 0, st>>>(partial, ks, stride, out_rows, out_cols, out_cols,
-                                               out, ldo);
+  sum_splits<<<sum_splits_grid(stride), 256, 0, st>>>(partial, ks, stride, out_rows, out_cols,
+                                                        out_cols, out, ldo);
   SPB_LAUNCH_CHECK();
   return SPB_OK;
 }
