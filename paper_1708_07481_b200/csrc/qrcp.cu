@@ -224,16 +224,27 @@ qrcp_pivots(const T* __restrict__ X, int64_t ldx, int n, int k, double2* __restr
     bp = INT_MAX;
     bc = -1;
   };
+  // global maximum over the per-CTA records: warp 0, lane-strided loads then a
+  // shuffle tree ((value, position) is a total order, so any order gives the
+  // same winner)
   auto global_best = [&](const BestRec* slot) {
-    if (tid == 0) {
-      BestRec b = slot[0];
-      double d = b.dmax;
-      for (int g = 1; g < (int)gridDim.x; ++g) {
-        d = fmax(d, slot[g].dmax);
-        if (better(slot[g].val, slot[g].pos, b.val, b.pos)) b = slot[g];
+    if (warp == 0) {
+      double bv2 = -1.0, d = -1.0;
+      int bp2 = INT_MAX, bc2 = -1;
+      for (int g = lane; g < (int)gridDim.x; g += 32) {
+        const BestRec r = slot[g];
+        d = fmax(d, r.dmax);
+        if (better(r.val, r.pos, bv2, bp2)) { bv2 = r.val; bp2 = r.pos; bc2 = r.col; }
       }
-      b.dmax = d;
-      s_best = b;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        const double ov = __shfl_xor_sync(0xffffffffu, bv2, o);
+        const int op = __shfl_xor_sync(0xffffffffu, bp2, o);
+        const int oc = __shfl_xor_sync(0xffffffffu, bc2, o);
+        d = fmax(d, __shfl_xor_sync(0xffffffffu, d, o));
+        if (better(ov, op, bv2, bp2)) { bv2 = ov; bp2 = op; bc2 = oc; }
+      }
+      if (lane == 0) s_best = {bv2, bp2, bc2, d};
     }
     __syncthreads();
     return s_best;
