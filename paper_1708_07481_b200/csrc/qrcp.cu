@@ -405,15 +405,15 @@ template <typename T>
 __global__ void gather_seeds(const T* __restrict__ X, int64_t ldx, int k, const int* __restrict__ piv,
                              int* __restrict__ seeds, double* __restrict__ S) {
   __shared__ int sd[1024];
-  if (threadIdx.x == 0) {
-    for (int i = 0; i < k; ++i) sd[i] = piv[i];
-    for (int i = 1; i < k; ++i) {  // insertion sort (k small)
-      const int v = sd[i];
-      int j = i - 1;
-      while (j >= 0 && sd[j] > v) { sd[j + 1] = sd[j]; --j; }
-      sd[j + 1] = v;
-    }
-    for (int i = 0; i < k; ++i) seeds[i] = sd[i];
+  __shared__ int pv[1024];
+  for (int i = threadIdx.x; i < k; i += blockDim.x) pv[i] = piv[i];
+  __syncthreads();
+  for (int i = threadIdx.x; i < k; i += blockDim.x) {  // sort by rank (pivots are distinct)
+    const int v = pv[i];
+    int r = 0;
+    for (int j = 0; j < k; ++j) r += pv[j] < v;
+    sd[r] = v;
+    seeds[r] = v;
   }
   __syncthreads();
   for (int x = threadIdx.x; x < k * k; x += blockDim.x) {

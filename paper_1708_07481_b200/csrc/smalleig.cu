@@ -417,6 +417,26 @@ __device__ __forceinline__ void tri_index(int t, int* ti, int* tq) {
   *tq = t - r * (r + 1) / 2;
 }
 
+// min / max over m strided doubles (optionally their square roots) by one warp;
+// every lane returns the result.
+__device__ __forceinline__ void warp_minmax(const double* base, int64_t stride, int m, bool root,
+                                            double* mn, double* mx) {
+  const int lane = threadIdx.x & 31;
+  double a = DBL_MAX, b = -DBL_MAX;
+  for (int i = lane; i < m; i += 32) {
+    const double v = root ? sqrt(base[(int64_t)i * stride]) : base[(int64_t)i * stride];
+    a = fmin(a, v);
+    b = fmax(b, v);
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    a = fmin(a, __shfl_xor_sync(0xffffffffu, a, o));
+    b = fmax(b, __shfl_xor_sync(0xffffffffu, b, o));
+  }
+  *mn = a;
+  *mx = b;
+}
+
 // Blocked Cholesky + inverse for m <= kCholLdlMax with warp-synchronous
 // panels (same packed layout, outputs and status protocol as chol_ldl):
 //  P1  the 32x32 diagonal block is factored (LDL') by warp 0 in registers,
@@ -451,19 +471,19 @@ chol_wsync(const double* __restrict__ Bsrc, int m, double* __restrict__ Lg, doub
       fb += v * v;
     }
   fb = block_sum(fb, red);
-  if (tid == 0) {
-    fail = 0;
+  if (warp == 0) {
+    int f0 = 0;
     if (mode == 1) {  // diag > 0 and min diag > (eps na)^2 max diag (lobpcg.py:229-231)
-      double dmin = DBL_MAX, dmax = -DBL_MAX;
-      for (int i = 0; i < m; ++i) {
-        dmin = fmin(dmin, A[i * ld + i]);
-        dmax = fmax(dmax, A[i * ld + i]);
-      }
-      status->dmin = dmin;
-      status->dmax = dmax;
+      double dmin, dmax;
+      warp_minmax(A, ld + 1, m, false, &dmin, &dmax);
       const double t = kEps64 * m;
-      if (!(dmin > 0.0) || !(dmin > t * t * dmax)) fail = 1;
+      if (!(dmin > 0.0) || !(dmin > t * t * dmax)) f0 = 1;
+      if (lane == 0) {
+        status->dmin = dmin;
+        status->dmax = dmax;
+      }
     }
+    if (lane == 0) fail = f0;
   }
   __syncthreads();
   if (fail == 1) {
@@ -562,16 +582,14 @@ chol_wsync(const double* __restrict__ Bsrc, int m, double* __restrict__ Lg, doub
     }
     return;
   }
-  if (mode == 1 && tid == 0) {
-    double rmin = DBL_MAX, rmax = -DBL_MAX;
-    for (int i = 0; i < m; ++i) {
-      const double r = sqrt(A[i * ld + i]);
-      rmin = fmin(rmin, r);
-      rmax = fmax(rmax, r);
+  if (mode == 1 && warp == 0) {
+    double rmin, rmax;
+    warp_minmax(A, ld + 1, m, true, &rmin, &rmax);
+    if (lane == 0) {
+      status->rmin = rmin;
+      status->rmax = rmax;
+      if (!(rmin > sqrt(kEps64) * rmax)) fail = 1;  // lobpcg.py:235
     }
-    status->rmin = rmin;
-    status->rmax = rmax;
-    if (!(rmin > sqrt(kEps64) * rmax)) fail = 1;  // lobpcg.py:235
   }
   for (int i = tid; i < m; i += CWT) dinv[i] = 1.0 / sqrt(A[i * ld + i]);
   __syncthreads();
@@ -1399,21 +1417,19 @@ chol_cluster(const double* __restrict__ Bsrc, int m, double* __restrict__ Lg,
   const int g = tid / nc, lc = tid - (tid / nc) * nc;
   const bool active = g < G && lc < ncl;
   const int q = c0 + lc;
-  if (tid == 0) {
-    s_fail = 0;
+  if (tid < 32) {
+    int f0 = 0;
     if (mode == 1) {  // diag > 0 and min diag > (eps na)^2 max diag (lobpcg.py:229-231)
-      double dmin = DBL_MAX, dmax = -DBL_MAX;
-      for (int i = 0; i < m; ++i) {
-        dmin = fmin(dmin, Bsrc[(int64_t)i * m + i]);
-        dmax = fmax(dmax, Bsrc[(int64_t)i * m + i]);
-      }
-      if (rank == 0) {
+      double dmin, dmax;
+      warp_minmax(Bsrc, (int64_t)m + 1, m, false, &dmin, &dmax);
+      if (rank == 0 && tid == 0) {
         status->dmin = dmin;
         status->dmax = dmax;
       }
       const double t = kEps64 * m;
-      if (!(dmin > 0.0) || !(dmin > t * t * dmax)) s_fail = 1;
+      if (!(dmin > 0.0) || !(dmin > t * t * dmax)) f0 = 1;
     }
+    if (tid == 0) s_fail = f0;
   }
   for (int x = tid; x < m * ncl; x += CCT) {
     const int i = x / ncl, c = x - (x / ncl) * ncl;
@@ -1498,18 +1514,18 @@ chol_finish(const double* __restrict__ Bsrc, int m, const double* __restrict__ L
       fb += v * v;
     }
   fb = block_sum(fb, red);
-  if (tid == 0) {
-    fail = 0;
+  if (warp == 0) {
+    int f0 = 0;
     if (mode == 1) {
-      double rmin = DBL_MAX, rmax = -DBL_MAX;
-      for (int i = 0; i < m; ++i) {
-        rmin = fmin(rmin, Lg[(int64_t)i * m + i]);
-        rmax = fmax(rmax, Lg[(int64_t)i * m + i]);
+      double rmin, rmax;
+      warp_minmax(Lg, (int64_t)m + 1, m, false, &rmin, &rmax);
+      if (lane == 0) {
+        status->rmin = rmin;
+        status->rmax = rmax;
       }
-      status->rmin = rmin;
-      status->rmax = rmax;
-      if (!(rmin > sqrt(kEps64) * rmax)) fail = 1;  // lobpcg.py:235
+      if (!(rmin > sqrt(kEps64) * rmax)) f0 = 1;  // lobpcg.py:235
     }
+    if (lane == 0) fail = f0;
   }
   __syncthreads();
   if (fail) {
