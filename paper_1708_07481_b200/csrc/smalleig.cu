@@ -622,22 +622,50 @@ chol_wsync(const double* __restrict__ Bsrc, int m, double* __restrict__ Lg, doub
         if (i > j && i < bn) A[(b0 + j) * ld + b0 + i] = x[i];
   }
   __syncthreads();
-  for (int bI = 1; bI < nblk; ++bI) {  // block rows: X_IJ = -X_II (sum_K L_IK X_KJ)
+  // block rows on the FP64 tensor pipe (mma.sync m8n8k4): R = L'_{I,<I} X_{<I,<I},
+  // then X_{I,<I} = -X_II R; every warp owns 8 x 8 output tiles
+  for (int bI = 1; bI < nblk; ++bI) {
     const int i0 = bI * 32, ni = min(32, m - i0);
-    double* R = S;  // ni x i0
-    for (int x = tid; x < ni * i0; x += CWT) {
-      const int r = x / i0, j = x % i0;
-      const double* Lr = A + (i0 + r) * ld;
-      double acc = Lr[j];  // k = j (X_jj = 1)
-      for (int k = j + 1; k < i0; ++k) acc = fma(Lr[k], A[j * ld + k], acc);
-      R[x] = acc;
+    double* R = S;  // ni x i0, row pitch i0
+    const int mtiles = (ni + 7) / 8, ntiles = i0 / 8;
+    const int fr = lane >> 2, fk = lane & 3;  // fragment row / k index
+    for (int t = warp; t < mtiles * ntiles; t += CWT / 32) {
+      const int mt = t / ntiles, nt = t % ntiles;
+      const int r = mt * 8 + fr, j0 = nt * 8, jb = j0 + fr;  // A row; B column for this lane
+      double c0 = 0.0, c1 = 0.0;
+      for (int k0 = j0 & ~3; k0 < i0; k0 += 4) {
+        const int k = k0 + fk;
+        const double av = r < ni ? A[(i0 + r) * ld + k] : 0.0;               // L'[i0+r][k]
+        const double bv = k > jb ? A[jb * ld + k] : (k == jb ? 1.0 : 0.0);   // X[k][jb]
+        asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+                     : "+d"(c0), "+d"(c1)
+                     : "d"(av), "d"(bv));
+      }
+      const int rr = mt * 8 + fr, cc = j0 + 2 * fk;
+      if (rr < ni) {
+        R[rr * i0 + cc] = c0;
+        R[rr * i0 + cc + 1] = c1;
+      }
     }
     __syncthreads();
-    for (int x = tid; x < ni * i0; x += CWT) {
-      const int r = x / i0, j = x % i0;
-      double acc = R[r * i0 + j];  // q = r (X_rr = 1)
-      for (int q = 0; q < r; ++q) acc = fma(A[(i0 + q) * ld + i0 + r], R[q * i0 + j], acc);
-      A[j * ld + i0 + r] = -acc;
+    for (int t = warp; t < mtiles * ntiles; t += CWT / 32) {
+      const int mt = t / ntiles, nt = t % ntiles;
+      const int r = mt * 8 + fr, jb = nt * 8 + fr;
+      double c0 = 0.0, c1 = 0.0;
+      for (int q0 = 0; q0 < ni; q0 += 4) {
+        const int q = q0 + fk;
+        // X_II[r][q] (unit lower, stored transposed) and R[q][jb]
+        const double av = (r < ni && q < ni) ? (r > q ? A[(i0 + q) * ld + i0 + r] : (r == q ? 1.0 : 0.0)) : 0.0;
+        const double bv = q < ni ? R[q * i0 + jb] : 0.0;
+        asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+                     : "+d"(c0), "+d"(c1)
+                     : "d"(av), "d"(bv));
+      }
+      const int rr = mt * 8 + fr, cc = nt * 8 + 2 * fk;
+      if (rr < ni) {
+        A[cc * ld + i0 + rr] = -c0;
+        A[(cc + 1) * ld + i0 + rr] = -c1;
+      }
     }
     __syncthreads();
   }
