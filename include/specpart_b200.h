@@ -95,9 +95,10 @@ SPB_API int spb_laplacian_spmm(int dtype, int32_t row_begin, int32_t row_end, co
 
 /* ---------------- (c) tall-skinny Gram ---------------------------------------
  * out[p x q] (float64, row stride ldo) = U' V for vertex-major blocks U (n x p),
- * V (n x q): the Gram products of lobpcg.py:228, :366, :418. mode 0: CUDA-core
- * float64 products (any dtype); mode 1: tcgen05 tensor cores, 3xTF32 split,
- * TMA-fed (SPB_F32 only, sm_100; 16-byte aligned rows). Split-K partials are
+ * V (n x q): the Gram products of lobpcg.py:228, :366, :418. mode 0: float64
+ * products on the FP64 tensor pipe (DMMA; any dtype); mode 1: tcgen05, 3xTF32
+ * split, TMA-fed (SPB_F32 only, sm_100; 16-byte aligned rows); mode 2: tcgen05
+ * int8 Ozaki splitting (6 digits, exact int32 sums; SPB_F32 only, sm_100). Split-K partials are
  * reduced in float64 in a fixed order. ws: spb_gram_workspace(p, q, n) bytes. */
 SPB_API size_t spb_gram_workspace(int32_t p, int32_t q, int64_t n);
 SPB_API int spb_gram(int dtype, int mode, const void* u, int64_t ldu, int32_t p, const void* v,

@@ -883,6 +883,13 @@ int block_update(int dtype, const UpdParams& p, int64_t n, cudaStream_t st) {
   return SPB_OK;
 }
 
+int oz_sum_splits(const double* part, int ks, int64_t stride, int rows, int cols, double* out,
+                  int ldo, cudaStream_t st) {
+  sum_splits<<<sum_splits_grid(stride), 256, 0, st>>>(part, ks, stride, rows, cols, cols, out, ldo);
+  SPB_LAUNCH_CHECK();
+  return SPB_OK;
+}
+
 size_t update_cstage_floats(int w_total, int nseg) {
   return (size_t)(w_total + nseg * UKT) * 256;
 }

@@ -1,0 +1,399 @@
+// (c) Tall-skinny Gram products on the 5th-generation tensor cores with the
+// Ozaki splitting: float64-accurate G = U'V from int8 tcgen05 MMAs.
+//
+//   G[p x q] = U' V,   U: n x p, V: n x q (float32, vertex-major, row stride ld)
+//
+// Every column c of U (and of V) gets a power-of-two scale 2^e_c > max|x|; the
+// scaled entries r in (-1, 1) are written as S = 6 signed 7-bit digits,
+// r = sum_t a_t 2^(-7t) + eps, |eps| < 2^-42 (exact digit extraction in fp32).
+// Then G_cd = 2^(e_c + e_d) sum_{t+u <= S+1} 2^(-7(t+u)) (A_t' B_u)_cd: 21 int8
+// GEMMs with exact int32 accumulation, grouped by the level t+u into six TMEM
+// accumulators, converted to fp64 and combined smallest level first. The
+// per-product truncation error is O(2^-42) relative to the column maxima, far
+// below the fp32 storage rounding of the operands.
+//
+// Operands are pre-packed by oz_pack into the UMMA canonical K-major layout
+// (8 columns x 16 rows core matrices), one plane per digit:
+//   plane[kblock (32 rows)][column group (8 cols)][k half][8 cols][16 rows]
+// so a CTA's operand tile for one 32-row k-block is one contiguous bulk copy.
+//
+// Per CTA: a 128 x 80 output tile over a range of k-blocks (split-K, at most
+// 16384 rows so the int32 sums cannot overflow). Warp 0 issues the bulk copies
+// (mbarrier pipeline, OZ_KS stages), warp 1 one thread issues the 21 MMAs per
+// k-block, warps 2-5 the epilogue (tcgen05.ld -> fp64 partial tile); the split-K
+// partials are reduced in a fixed order (sum_splits).
+#include "dense.cuh"
+
+namespace spb {
+
+int oz_sum_splits(const double* part, int ks, int64_t stride, int rows, int cols, double* out,
+                  int ldo, cudaStream_t st);
+
+namespace {
+
+constexpr int OZ_S = 6;          // digits per value
+constexpr int OZ_M = 128;        // UMMA M (columns of U per tile)
+constexpr int OZ_N = 80;         // UMMA N (columns of V per tile); OZ_S * OZ_N <= 512 TMEM columns
+constexpr int OZ_KB = 32;        // rows per k-block (one UMMA K step for 8-bit operands)
+constexpr int OZ_KS = 4;         // pipeline stages
+constexpr int OZ_MAXROWS = 16384;  // rows per CTA: 6 pairs x 127^2 x 16384 < 2^31
+constexpr int kOzA = OZ_S * (OZ_M / 8) * 256;  // bytes of the A planes per stage (24 KB)
+constexpr int kOzB = OZ_S * (OZ_N / 8) * 256;  // bytes of the B planes per stage (15 KB)
+constexpr int kOzStage = kOzA + kOzB;
+constexpr int kOzSmem = OZ_KS * kOzStage + 1024 + 256;
+
+__device__ __forceinline__ uint32_t s_u32(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void oz_mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(s_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void oz_mbar_expect(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(s_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void oz_mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred P;\n"
+      "OZW_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P, [%0], %1;\n\t"
+      "@!P bra OZW_%=;\n}" ::"r"(s_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          s_u32(dst)),
+      "l"(src), "r"(bytes), "r"(s_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ uint64_t oz_desc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
+  uint64_t d = 0;
+  d |= (uint64_t)((saddr >> 4) & 0x3FFF);
+  d |= (uint64_t)((lbo >> 4) & 0x3FFF) << 16;
+  d |= (uint64_t)((sbo >> 4) & 0x3FFF) << 32;
+  d |= (uint64_t)1 << 46;  // descriptor version (Blackwell); layout SWIZZLE_NONE
+  return d;
+}
+__device__ __forceinline__ void umma_i8(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t idesc,
+                                        uint32_t accum) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+      "l"(a), "l"(b), "r"(idesc), "r"(accum));
+}
+__device__ __forceinline__ void oz_commit(uint64_t* bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                   s_u32(bar))
+               : "memory");
+}
+
+// Column maxima |x| (as float bits; non-negative floats order like their bits).
+__global__ void oz_colmax(const float* __restrict__ X, int64_t ldx, int64_t n, int cols,
+                          unsigned* __restrict__ cmax) {
+  const int c = blockIdx.y * 32 + (threadIdx.x & 31);
+  if (c >= cols) return;
+  unsigned m = 0;
+  for (int64_t r = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); r < n;
+       r += (int64_t)gridDim.x * (blockDim.x >> 5))
+    m = max(m, __float_as_uint(fabsf(X[r * ldx + c])));
+  atomicMax(&cmax[c], m);
+}
+
+// Digits of x / 2^e_c into the packed planes (see the header comment).
+__global__ void oz_pack(const float* __restrict__ X, int64_t ldx, int64_t n, int cols, int ncg,
+                        int64_t nkb, const unsigned* __restrict__ cmax, int8_t* __restrict__ planes,
+                        int64_t plane_bytes) {
+  // one thread per (k-block, column group, k half, column, 16 rows) = 16 values
+  const int64_t total = nkb * ncg * 2 * 8;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    const int cl = (int)(t & 7);
+    const int h = (int)((t >> 3) & 1);
+    const int64_t rest = t >> 4;
+    const int g = (int)(rest % ncg);
+    const int64_t kb = rest / ncg;
+    const int c = g * 8 + cl;
+    int e = 0;
+    if (c < cols) {
+      const float mx = __uint_as_float(cmax[c]);
+      if (mx > 0.f) frexpf(mx, &e);  // mx < 2^e
+    }
+    uint32_t w[OZ_S][4];
+#pragma unroll
+    for (int s = 0; s < OZ_S; ++s)
+#pragma unroll
+      for (int q = 0; q < 4; ++q) w[s][q] = 0u;
+#pragma unroll
+    for (int i = 0; i < 16; ++i) {
+      const int64_t r = kb * OZ_KB + h * 16 + i;
+      float v = 0.f;
+      if (c < cols && r < n) v = ldexpf(X[r * ldx + c], -e);  // exact: power-of-two scaling
+#pragma unroll
+      for (int s = 0; s < OZ_S; ++s) {
+        const float y = v * 128.f;
+        const float a = truncf(y);  // |a| <= 127 since |v| < 1
+        v = y - a;                  // exact
+        w[s][i >> 2] |= ((uint32_t)(uint8_t)(int8_t)(int)a) << (8 * (i & 3));
+      }
+    }
+    const int64_t off = (((kb * ncg + g) * 2 + h) * 8 + cl) * 16;
+#pragma unroll
+    for (int s = 0; s < OZ_S; ++s)
+      *reinterpret_cast<uint4*>(planes + s * plane_bytes + off) =
+          make_uint4(w[s][0], w[s][1], w[s][2], w[s][3]);
+  }
+}
+
+struct OzParams {
+  int p, q;          // output rows (U columns), columns (V columns)
+  int mtiles, ntiles;
+  int ncgA, ncgB;    // column groups of the packed planes
+  int64_t nkb;       // k-blocks
+  int64_t kbchunk;   // k-blocks per split
+  int64_t planeA, planeB;  // bytes per plane
+  int64_t split_stride;
+};
+
+__global__ void __launch_bounds__(192, 1)
+gram_oz_kernel(const int8_t* __restrict__ PA, const int8_t* __restrict__ PB,
+               const unsigned* __restrict__ cmaxA, const unsigned* __restrict__ cmaxB, OzParams P,
+               double* __restrict__ part) {
+  extern __shared__ __align__(1024) uint8_t osm[];
+  uint8_t* base = (uint8_t*)(((uintptr_t)osm + 1023) & ~(uintptr_t)1023);
+  uint64_t* full = (uint64_t*)(base + OZ_KS * kOzStage);
+  uint64_t* empty = full + OZ_KS;
+  uint64_t* accb = empty + OZ_KS;
+  uint32_t* tmem_slot = (uint32_t*)(accb + 1);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int mt = blockIdx.x % P.mtiles, nt = blockIdx.x / P.mtiles;
+  const int m0 = mt * OZ_M, n0 = nt * OZ_N;
+  const int64_t kb0 = (int64_t)blockIdx.y * P.kbchunk;
+  const int64_t kb1 = min(P.nkb, kb0 + P.kbchunk);
+  const int nk = kb1 > kb0 ? (int)(kb1 - kb0) : 0;
+  const int gA = m0 / 8, gB = n0 / 8;
+  const int cgA = min(OZ_M / 8, P.ncgA - gA);  // column groups present in this tile
+  const int cgB = min(OZ_N / 8, P.ncgB - gB);
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < OZ_KS; ++s) {
+      oz_mbar_init(&full[s], 1);
+      oz_mbar_init(&empty[s], 1);
+    }
+    oz_mbar_init(accb, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     s_u32(tmem_slot)),
+                 "r"(512));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  // zero the operand buffers once: column groups absent from a tile stay zero
+  for (int i = threadIdx.x; i < OZ_KS * kOzStage / 16; i += blockDim.x)
+    reinterpret_cast<uint4*>(base)[i] = make_uint4(0, 0, 0, 0);
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;");
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0 && nk > 0) {
+      const uint32_t bytesA = (uint32_t)cgA * 256, bytesB = (uint32_t)cgB * 256;
+      for (int kc = 0; kc < nk; ++kc) {
+        const int s = kc % OZ_KS, u = kc / OZ_KS;
+        if (u > 0) oz_mbar_wait(&empty[s], (u - 1) & 1);
+        uint8_t* st = base + s * kOzStage;
+        oz_mbar_expect(&full[s], OZ_S * (bytesA + bytesB));
+        const int64_t kb = kb0 + kc;
+#pragma unroll
+        for (int d = 0; d < OZ_S; ++d) {
+          bulk_g2s(st + d * (OZ_M / 8) * 256, PA + d * P.planeA + (kb * P.ncgA + gA) * 256, bytesA,
+                   &full[s]);
+          bulk_g2s(st + kOzA + d * (OZ_N / 8) * 256, PB + d * P.planeB + (kb * P.ncgB + gB) * 256,
+                   bytesB, &full[s]);
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0 && nk > 0) {
+      const uint32_t idesc = (2u << 4) | (1u << 7) | (1u << 10) |  // S32 acc, s8 A/B, K-major
+                             ((uint32_t)(OZ_N >> 3) << 17) | ((uint32_t)(OZ_M >> 4) << 24);
+      for (int kc = 0; kc < nk; ++kc) {
+        const int s = kc % OZ_KS, u = kc / OZ_KS;
+        oz_mbar_wait(&full[s], u & 1);
+        asm volatile("tcgen05.fence::after_thread_sync;");
+        const uint32_t sa = s_u32(base + s * kOzStage), sb = sa + kOzA;
+        // level L = t + u - 2 accumulates digit pairs (t, u), t + u <= S + 1
+#pragma unroll
+        for (int t = 1; t <= OZ_S; ++t)
+#pragma unroll
+          for (int uu = 1; uu <= OZ_S; ++uu) {
+            if (t + uu > OZ_S + 1) continue;
+            const int L = t + uu - 2;
+            const uint64_t da = oz_desc(sa + (t - 1) * (OZ_M / 8) * 256, 128, 256);
+            const uint64_t db = oz_desc(sb + (uu - 1) * (OZ_N / 8) * 256, 128, 256);
+            // first write of level L in this CTA: the (1, L+1) pair at kc == 0
+            const uint32_t acc = (kc > 0 || t > 1) ? 1u : 0u;
+            umma_i8(tmem + (uint32_t)(L * OZ_N), da, db, idesc, acc);
+          }
+        oz_commit(&empty[s]);
+      }
+      oz_commit(accb);
+    }
+  } else {
+    // epilogue: warps 2..5 -> TMEM lanes 32*(warp & 3) .. +31 = tile rows
+    if (nk > 0) {
+      oz_mbar_wait(accb, 0);
+      asm volatile("tcgen05.fence::after_thread_sync;");
+    }
+    const int quarter = warp & 3;
+    const int row = m0 + quarter * 32 + lane;
+    int eA = 0;
+    if (row < P.p) {
+      const float mx = __uint_as_float(cmaxA[row]);
+      if (mx > 0.f) frexpf(mx, &eA);
+    }
+    double* out = part + (int64_t)blockIdx.y * P.split_stride;
+    for (int c0 = 0; c0 < OZ_N; c0 += 16) {
+      double acc[16];
+#pragma unroll
+      for (int i = 0; i < 16; ++i) acc[i] = 0.0;
+      if (nk > 0) {
+#pragma unroll
+        for (int L = OZ_S - 1; L >= 0; --L) {  // smallest level first
+          uint32_t r[16];
+          const uint32_t taddr = tmem + ((uint32_t)(quarter * 32) << 16) + (uint32_t)(L * OZ_N + c0);
+          asm volatile(
+              "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, "
+              "%10, %11, %12, %13, %14, %15}, [%16];"
+              : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]),
+                "=r"(r[6]), "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]),
+                "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+              : "r"(taddr));
+          asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+          const double sc = ldexp(1.0, -7 * (L + 2));
+#pragma unroll
+          for (int i = 0; i < 16; ++i) acc[i] = fma((double)(int)r[i], sc, acc[i]);
+        }
+      }
+      if (row < P.p) {
+#pragma unroll
+        for (int i = 0; i < 16; ++i) {
+          const int col = n0 + c0 + i;
+          if (col < P.q) {
+            int eB = 0;
+            const float mx = __uint_as_float(cmaxB[col]);
+            if (mx > 0.f) frexpf(mx, &eB);
+            out[(int64_t)row * P.q + col] = ldexp(acc[i], eA + eB);
+          }
+        }
+      }
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  if (warp == 0) {
+    asm volatile("tcgen05.fence::after_thread_sync;");
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512));
+  }
+}
+
+// Device scratch for the packed planes (grown on demand, never shrunk).
+struct OzScratch {
+  void* p = nullptr;
+  size_t cap = 0;
+};
+void* oz_scratch(size_t bytes) {
+  static OzScratch s[16];
+  int dev = 0;
+  cudaGetDevice(&dev);
+  OzScratch& x = s[dev & 15];
+  if (x.cap < bytes) {
+    if (x.p) cudaFree(x.p);
+    x.p = nullptr;
+    if (cudaMalloc(&x.p, bytes) != cudaSuccess) {
+      x.cap = 0;
+      return nullptr;
+    }
+    x.cap = bytes;
+  }
+  return x.p;
+}
+
+}  // namespace
+
+size_t gram_oz_partial_doubles(int64_t n, int p, int q) {
+  const int tiles = (int)(ceil_div(p, OZ_M) * ceil_div(q, OZ_N));
+  const int64_t nkb = ceil_div(std::max<int64_t>(n, 1), OZ_KB);
+  int64_t ks = std::max<int64_t>(ceil_div(2 * num_sms(), tiles), ceil_div(nkb, OZ_MAXROWS / OZ_KB));
+  ks = std::min<int64_t>(ks, nkb);
+  return (size_t)std::max<int64_t>(ks, 1) * p * q;
+}
+
+// out[p x q] (ld ldo) = U' V with float32 operands, float64-accurate.
+int gram_oz(const float* U, int64_t ldu, int p, const float* V, int64_t ldv, int q, int64_t n,
+            double* partial, size_t partial_cap, double* out, int ldo, cudaStream_t st) {
+  if (p <= 0 || q <= 0) return SPB_OK;
+  static bool attr = false;
+  if (!attr) {
+    SPB_CUDA(cudaFuncSetAttribute(gram_oz_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  kOzSmem));
+    attr = true;
+  }
+  const int64_t nkb = ceil_div(std::max<int64_t>(n, 1), OZ_KB);
+  const int ncgA = (int)ceil_div(p, 8), ncgB = (int)ceil_div(q, 8);
+  const int64_t planeA = nkb * ncgA * 256, planeB = nkb * ncgB * 256;
+  const size_t need = (size_t)OZ_S * (planeA + planeB) + sizeof(unsigned) * (size_t)(p + q) + 256;
+  uint8_t* scr = (uint8_t*)oz_scratch(need);
+  if (!scr) {
+    set_error("Ozaki Gram scratch allocation failed (%zu bytes)", need);
+    return SPB_ERR_CUDA;
+  }
+  int8_t* PA = (int8_t*)scr;
+  int8_t* PB = PA + OZ_S * planeA;
+  unsigned* cmA = (unsigned*)(PB + OZ_S * planeB);
+  unsigned* cmB = cmA + p;
+  SPB_CUDA(cudaMemsetAsync(cmA, 0, sizeof(unsigned) * (size_t)(p + q), st));
+  {
+    const int gx = (int)std::min<int64_t>(ceil_div(n, 8), 4 * num_sms());
+    oz_colmax<<<dim3(gx, (unsigned)ceil_div(p, 32)), 256, 0, st>>>(U, ldu, n, p, cmA);
+    oz_colmax<<<dim3(gx, (unsigned)ceil_div(q, 32)), 256, 0, st>>>(V, ldv, n, q, cmB);
+    const int64_t ta = nkb * ncgA * 16, tb = nkb * ncgB * 16;
+    oz_pack<<<(int)std::min<int64_t>(ceil_div(ta, 256), 8 * num_sms()), 256, 0, st>>>(
+        U, ldu, n, p, ncgA, nkb, cmA, PA, planeA);
+    oz_pack<<<(int)std::min<int64_t>(ceil_div(tb, 256), 8 * num_sms()), 256, 0, st>>>(
+        V, ldv, n, q, ncgB, nkb, cmB, PB, planeB);
+    SPB_LAUNCH_CHECK();
+  }
+  OzParams P{};
+  P.p = p;
+  P.q = q;
+  P.mtiles = (int)ceil_div(p, OZ_M);
+  P.ntiles = (int)ceil_div(q, OZ_N);
+  P.ncgA = ncgA;
+  P.ncgB = ncgB;
+  P.nkb = nkb;
+  P.planeA = planeA;
+  P.planeB = planeB;
+  const int tiles = P.mtiles * P.ntiles;
+  int64_t ks = std::max<int64_t>(ceil_div(2 * num_sms(), tiles), ceil_div(nkb, OZ_MAXROWS / OZ_KB));
+  ks = std::min<int64_t>(ks, nkb);
+  while (ks > 1 && (size_t)ks * p * q > partial_cap) --ks;
+  P.kbchunk = ceil_div(nkb, ks);
+  ks = ceil_div(nkb, P.kbchunk);
+  if ((size_t)ks * p * q > partial_cap || P.kbchunk * OZ_KB > OZ_MAXROWS) {
+    set_error("Ozaki Gram partial workspace too small");
+    return SPB_ERR_WORKSPACE;
+  }
+  P.split_stride = (int64_t)p * q;
+  gram_oz_kernel<<<dim3(tiles, (unsigned)ks), 192, kOzSmem, st>>>(PA, PB, cmA, cmB, P, partial);
+  SPB_LAUNCH_CHECK();
+  return oz_sum_splits(partial, (int)ks, P.split_stride, p, q, out, ldo, st);
+}
+
+}  // namespace spb
