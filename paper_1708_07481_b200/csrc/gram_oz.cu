@@ -97,54 +97,61 @@ __global__ void oz_colmax(const float* __restrict__ X, int64_t ldx, int64_t n, i
   const int c = blockIdx.y * 32 + (threadIdx.x & 31);
   if (c >= cols) return;
   unsigned m = 0;
-  for (int64_t r = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); r < n;
-       r += (int64_t)gridDim.x * (blockDim.x >> 5))
-    m = max(m, __float_as_uint(fabsf(X[r * ldx + c])));
+  const int64_t step = (int64_t)gridDim.x * (blockDim.x >> 5);
+#pragma unroll 8
+  for (int64_t r = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); r < n; r += step)
+    m = max(m, __float_as_uint(fabsf(__ldg(X + r * ldx + c))));
   atomicMax(&cmax[c], m);
 }
 
-// Digits of x / 2^e_c into the packed planes (see the header comment).
-__global__ void oz_pack(const float* __restrict__ X, int64_t ldx, int64_t n, int cols, int ncg,
-                        int64_t nkb, const unsigned* __restrict__ cmax, int8_t* __restrict__ planes,
-                        int64_t plane_bytes) {
-  // one thread per (k-block, column group, k half, column, 16 rows) = 16 values
-  const int64_t total = nkb * ncg * 2 * 8;
+// Digits of x / 2^e_c into the packed planes (see the header comment). One
+// thread per (k-block, k half, column): 16 consecutive rows of one column, the
+// lanes of a warp on 32 consecutive columns (coalesced row reads); the 16 digit
+// bytes of each plane are packed in registers and stored as one 16-byte vector
+// (a warp's stores form contiguous 128-byte runs).
+__global__ void __launch_bounds__(256)
+oz_pack(const float* __restrict__ X, int64_t ldx, int64_t n, int cols, int ncg, int64_t nkb,
+        const unsigned* __restrict__ cmax, int8_t* __restrict__ planes, int64_t plane_bytes) {
+  const int cpad = ncg * 8;
+  const int64_t total = nkb * 2 * cpad;
   for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total;
        t += (int64_t)gridDim.x * blockDim.x) {
-    const int cl = (int)(t & 7);
-    const int h = (int)((t >> 3) & 1);
-    const int64_t rest = t >> 4;
-    const int g = (int)(rest % ncg);
-    const int64_t kb = rest / ncg;
-    const int c = g * 8 + cl;
+    const int c = (int)(t % cpad);
+    const int64_t kh = t / cpad;
+    const int h = (int)(kh & 1);
+    const int64_t kb = kh >> 1;
     int e = 0;
     if (c < cols) {
       const float mx = __uint_as_float(cmax[c]);
       if (mx > 0.f) frexpf(mx, &e);  // mx < 2^e
     }
-    uint32_t w[OZ_S][4];
-#pragma unroll
-    for (int s = 0; s < OZ_S; ++s)
-#pragma unroll
-      for (int q = 0; q < 4; ++q) w[s][q] = 0u;
+    float xv[16];
 #pragma unroll
     for (int i = 0; i < 16; ++i) {
       const int64_t r = kb * OZ_KB + h * 16 + i;
-      float v = 0.f;
-      if (c < cols && r < n) v = ldexpf(X[r * ldx + c], -e);  // exact: power-of-two scaling
+      xv[i] = (c < cols && r < n) ? __ldg(X + r * ldx + c) : 0.f;
+    }
+    uint32_t w[OZ_S][4];
 #pragma unroll
-      for (int s = 0; s < OZ_S; ++s) {
+    for (int sd = 0; sd < OZ_S; ++sd)
+#pragma unroll
+      for (int q = 0; q < 4; ++q) w[sd][q] = 0u;
+#pragma unroll
+    for (int i = 0; i < 16; ++i) {
+      float v = ldexpf(xv[i], -e);  // exact: power-of-two scaling
+#pragma unroll
+      for (int sd = 0; sd < OZ_S; ++sd) {
         const float y = v * 128.f;
         const float a = truncf(y);  // |a| <= 127 since |v| < 1
         v = y - a;                  // exact
-        w[s][i >> 2] |= ((uint32_t)(uint8_t)(int8_t)(int)a) << (8 * (i & 3));
+        w[sd][i >> 2] |= ((uint32_t)(uint8_t)(int8_t)(int)a) << (8 * (i & 3));
       }
     }
-    const int64_t off = (((kb * ncg + g) * 2 + h) * 8 + cl) * 16;
+    const int64_t off = (((kb * ncg + (c >> 3)) * 2 + h) * 8 + (c & 7)) * 16;
 #pragma unroll
-    for (int s = 0; s < OZ_S; ++s)
-      *reinterpret_cast<uint4*>(planes + s * plane_bytes + off) =
-          make_uint4(w[s][0], w[s][1], w[s][2], w[s][3]);
+    for (int sd = 0; sd < OZ_S; ++sd)
+      *reinterpret_cast<uint4*>(planes + sd * plane_bytes + off) =
+          make_uint4(w[sd][0], w[sd][1], w[sd][2], w[sd][3]);
   }
 }
 
@@ -363,10 +370,10 @@ int gram_oz(const float* U, int64_t ldu, int p, const float* V, int64_t ldv, int
     const int gx = (int)std::min<int64_t>(ceil_div(n, 8), 4 * num_sms());
     oz_colmax<<<dim3(gx, (unsigned)ceil_div(p, 32)), 256, 0, st>>>(U, ldu, n, p, cmA);
     oz_colmax<<<dim3(gx, (unsigned)ceil_div(q, 32)), 256, 0, st>>>(V, ldv, n, q, cmB);
-    const int64_t ta = nkb * ncgA * 16, tb = nkb * ncgB * 16;
-    oz_pack<<<(int)std::min<int64_t>(ceil_div(ta, 256), 8 * num_sms()), 256, 0, st>>>(
+    const int64_t ta = nkb * 2 * ncgA * 8, tb = nkb * 2 * ncgB * 8;
+    oz_pack<<<(int)std::min<int64_t>(ceil_div(ta, 256), 16 * num_sms()), 256, 0, st>>>(
         U, ldu, n, p, ncgA, nkb, cmA, PA, planeA);
-    oz_pack<<<(int)std::min<int64_t>(ceil_div(tb, 256), 8 * num_sms()), 256, 0, st>>>(
+    oz_pack<<<(int)std::min<int64_t>(ceil_div(tb, 256), 16 * num_sms()), 256, 0, st>>>(
         V, ldv, n, q, ncgB, nkb, cmB, PB, planeB);
     SPB_LAUNCH_CHECK();
   }

@@ -53,3 +53,28 @@ def test_fp64_mode_gram():
     v = rng.standard_normal((999, 7))
     g = _gram(u, v, 0, dtype="float64")
     assert np.allclose(g, u.T @ v, rtol=1e-13, atol=1e-12)
+
+
+@pytest.mark.parametrize("n,p,q", [(1000, 21, 63), (5003, 49, 147), (50000, 147, 294),
+                                   (40000, 176, 352), (70000, 324, 324), (300, 8, 8), (77, 3, 5),
+                                   (33000, 130, 90)])
+def test_ozaki_int8_gram_accuracy(n, p, q):
+    """spb_gram mode 2: int8 tcgen05 with six 7-bit digits per value and exact int32
+    sums (error O(2^-42) of the column maxima per product)."""
+    rng = np.random.default_rng(n + 7 * p + q)
+    u = rng.standard_normal((n, p)).astype(np.float32)
+    v = rng.standard_normal((n, q)).astype(np.float32)
+    v[:, 0] = 0.0  # an all-zero column
+
+    def rel_err(u, v):
+        exact = u.astype(np.float64).T @ v.astype(np.float64)
+        scale = np.abs(u.astype(np.float64)).T @ np.abs(v.astype(np.float64))
+        g = _gram(u, v, 2)
+        assert np.all(np.isfinite(g)) and np.all(g[:, 0] == 0.0)
+        return (np.abs(g - exact) / np.maximum(scale, 1e-300)).max()
+
+    assert rel_err(u, v) < 1e-12
+    # one entry 1e3 x larger per column of U: the shared column scale costs
+    # ~10 bits of the other entries' digits (the scheme's known dynamic-range cost)
+    u[5, :] *= 1e3
+    assert rel_err(u, v) < 1e-9
