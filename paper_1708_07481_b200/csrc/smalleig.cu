@@ -1077,11 +1077,12 @@ tridiag_cluster_mb(const double* __restrict__ Asrc, int m, int symmetrize, doubl
   double* vbufs = pbuf + 2 * m;            // [2][m]  v of steps k (parity)
   double* dotbuf = vbufs + 2 * m;          // [2][16] per-CTA shares of p'v
   double* red = dotbuf + 32;               // [G][nc]
-  __shared__ double wdot[2];
+  __shared__ double wdot[4];
   __shared__ double sc[2];
   __shared__ __align__(8) uint64_t mbA[2], mbB[2];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int G = TCT / nc;
+  const int nwt = ((nc + 31) >> 5) << 5;  // warps covering the local columns (nc <= 128)
   const int g = tid / nc, lc = tid - (tid / nc) * nc;
   const bool active = g < G && lc < ncl;
   const int icol = c0 + lc;
@@ -1158,7 +1159,7 @@ tridiag_cluster_mb(const double* __restrict__ Asrc, int m, int symmetrize, doubl
         red[g * nc + lc] = a0 + a1;
       }
       __syncthreads();
-      if (tid < 64) {
+      if (tid < nwt) {
         double pv = 0.0;
         if (tid < ncl && icol > k) {
           double sacc = 0.0;
@@ -1170,8 +1171,10 @@ tridiag_cluster_mb(const double* __restrict__ Asrc, int m, int symmetrize, doubl
         }
         pv = warp_sum(pv);
         if (lane == 0) wdot[tid >> 5] = pv;
-        asm volatile("bar.sync 1, 64;\n" ::: "memory");
-        if (tid < C) st_async_f64(dotbuf + b * 16 + rank, &mbA[b], tid, wdot[0] + wdot[1]);
+        asm volatile("bar.sync 1, %0;\n" ::"r"(nwt) : "memory");
+        double wsum = wdot[0];
+        for (int q = 1; q < (nwt >> 5); ++q) wsum += wdot[q];
+        if (tid < C) st_async_f64(dotbuf + b * 16 + rank, &mbA[b], tid, wsum);
       }
       if (tid == 0) mb_expect(&mbA[b], 8u * (uint32_t)(m - k - 1 + C));
       {
@@ -1574,7 +1577,9 @@ int tridiag_cluster_size(int m) {
   static const int forced = getenv("SPB_TRI_CLUSTER") ? atoi(getenv("SPB_TRI_CLUSTER")) : 0;
   if (m < kTriClusterMin || m > kTriClusterMax) return 0;
   if (forced == 2 || forced == 4 || forced == 8 || forced == 16)
-    if ((m + forced - 1) / forced <= 64 && tridiag_cluster_smem(m, forced) <= 200 * 1024) return forced;
+    if ((m + forced - 1) / forced <= (forced == 2 ? 128 : 64) &&
+        tridiag_cluster_smem(m, forced) <= 200 * 1024)
+      return forced;  // C == 2 (nc up to 128) only for the default mbarrier variant
   return m <= 160 ? 4 : (m <= 400 ? 8 : 16);
 }
 
