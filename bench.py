@@ -354,6 +354,8 @@ def run_ours(args):
     e2e_times = []
     part = None
     edges_pinned = torch.from_numpy(np.ascontiguousarray(edges)).pin_memory().numpy()
+    x0_host = x0.numpy() if isinstance(x0, torch.Tensor) else x0
+    x0 = torch.from_numpy(np.ascontiguousarray(x0_host)).pin_memory().numpy()  # pinned host input
     for i in range(args.steps):
         torch.cuda.synchronize()
         t0 = time.perf_counter()

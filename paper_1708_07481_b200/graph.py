@@ -225,13 +225,12 @@ def from_edges(edges, n: int, weights=None, *, symmetric: bool = False) -> Spars
     elif (weights is None and isinstance(edges, np.ndarray) and edges.ndim == 2
           and edges.shape[1] == 2 and edges.dtype == np.int64 and edges.flags.c_contiguous
           and edges.shape[0] > 0):
-        # fast path: one (pinned) H2D copy of the arc block, columns split on the
-        # device; the endpoint range check happens in the CSR build's validation
-        # pass (same DomainError)
-        t = torch.from_numpy(edges)
-        if t.numel() * 8 >= (1 << 20) and torch.cuda.is_available() and not t.is_pinned():
-            t = t.pin_memory()
-        dev = t.to(device=_device(), non_blocking=True)
+        # fast path: one H2D copy of the arc block (asynchronous from pinned
+        # memory; pageable blocks go through the driver's staged copy, which is
+        # steadier than a per-call pin_memory), columns split on the device; the
+        # endpoint range check happens in the CSR build's validation pass (same
+        # DomainError)
+        dev = torch.from_numpy(edges).to(device=_device(), non_blocking=True)
         src, dst, w = dev[:, 0].contiguous(), dev[:, 1].contiguous(), None
     else:
         hs, hd, hw = _coerce_edges(edges, weights)

@@ -246,10 +246,8 @@ def _x0_device(x0, n, l):
         t = x0.to(device=_device(), dtype=torch.float64)
         return t.contiguous()
     arr = np.ascontiguousarray(x0, dtype=np.float64)
-    t = torch.from_numpy(arr)
-    if arr.nbytes >= (1 << 20) and not t.is_pinned():
-        t = t.pin_memory()
-    return t.to(_device(), non_blocking=True)
+    # asynchronous from pinned memory; pageable arrays take the driver's staged copy
+    return torch.from_numpy(arr).to(_device(), non_blocking=True)
 
 
 def lobpcg_solve(operator, x0, config: SolverConfig, precond=None, n_converge: int | None = None,

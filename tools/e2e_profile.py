@@ -45,3 +45,28 @@ pr.enable()
 step()
 pr.disable()
 pstats.Stats(pr).sort_stats("tottime").print_stats(15)
+
+# per-phase wall times (synchronised): host arcs -> graph, x0 staging, solve, assignment
+from paper_1708_07481_b200.graph import LaplacianOperator  # noqa: E402
+from paper_1708_07481_b200.lobpcg import _x0_device  # noqa: E402
+
+for rep in range(10):
+    ts = []
+    torch.cuda.synchronize()
+    t = time.perf_counter()
+    g = spb.from_edges(edges_pinned, spec.n)
+    torch.cuda.synchronize()
+    ts.append(("from_edges", time.perf_counter() - t))
+    t = time.perf_counter()
+    xd = _x0_device(x0, spec.n, l)
+    torch.cuda.synchronize()
+    ts.append(("x0_stage", time.perf_counter() - t))
+    t = time.perf_counter()
+    xd = torch.from_numpy(x0).to("cuda")
+    torch.cuda.synchronize()
+    ts.append(("x0_pageable", time.perf_counter() - t))
+    t = time.perf_counter()
+    part, st, gap = spb.partition_static(g, cfg, k, fix_k=True, x0=x0)
+    torch.cuda.synchronize()
+    ts.append(("partition_static(host x0)", time.perf_counter() - t))
+    print("  ".join(f"{nm} {1e3 * v:.1f} ms" for nm, v in ts))
