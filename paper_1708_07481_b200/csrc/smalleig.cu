@@ -17,7 +17,9 @@
 // (eigenvalues of G_B by the same tridiagonal + bisection kernels), so the
 // ladder takes the reference's branch in every case.
 #include <cfloat>
+#include <cstdio>
 #include <cstdlib>
+#include <vector>
 
 #include "smalleig.cuh"
 
@@ -1061,7 +1063,7 @@ __device__ __forceinline__ void st_async_f64(double* local_addr, uint64_t* local
 __global__ void __launch_bounds__(TCT)
 tridiag_cluster_mb(const double* __restrict__ Asrc, int m, int symmetrize, double* __restrict__ V,
                    double* __restrict__ tau, double* __restrict__ d, double* __restrict__ e,
-                   const SmallStatus* status) {
+                   const SmallStatus* status, long long* trace) {
   if (status && (status->nonfinite || status->not_pd)) return;  // uniform over the cluster
   unsigned rank_u, csize_u;
   asm volatile("mov.u32 %0, %%cluster_ctarank;\n" : "=r"(rank_u));
@@ -1139,6 +1141,8 @@ tridiag_cluster_mb(const double* __restrict__ Asrc, int m, int symmetrize, doubl
     double* nextrow = rowbuf + (b ^ 1) * m;
     const double* vbuf = vbufs + b * m;
     __syncthreads();  // reflector k in vbufs[b]; every update of step k-1 is done
+    const bool tr = trace && rank == C - 1 && tid == 0;  // the CTA owning the last columns
+    if (tr) trace[k * 8 + 0] = clock64();
     const double tk = sc[b];
     const int j0 = k + 1 + g;
     const bool own = active && icol > k;
@@ -1158,7 +1162,9 @@ tridiag_cluster_mb(const double* __restrict__ Asrc, int m, int symmetrize, doubl
         if (j < m) a0 = fma(wp[0], vp[0], a0);
         red[g * nc + lc] = a0 + a1;
       }
+      if (tr) trace[k * 8 + 1] = clock64();
       __syncthreads();
+      if (tr) trace[k * 8 + 2] = clock64();
       if (tid < nwt) {
         double pv = 0.0;
         if (tid < ncl && icol > k) {
@@ -1167,6 +1173,7 @@ tridiag_cluster_mb(const double* __restrict__ Asrc, int m, int symmetrize, doubl
           for (int q = 0; q < gmax; ++q) sacc += red[q * nc + tid];
           const double p = tk * sacc;
           pv = p * vbuf[icol];
+          if (tr) trace[k * 8 + 7] = clock64();
           for (int r = 0; r < C; ++r) st_async_f64(pb + icol, &mbA[b], r, p);
         }
         pv = warp_sum(pv);
@@ -1176,12 +1183,14 @@ tridiag_cluster_mb(const double* __restrict__ Asrc, int m, int symmetrize, doubl
         for (int q = 1; q < (nwt >> 5); ++q) wsum += wdot[q];
         if (tid < C) st_async_f64(dotbuf + b * 16 + rank, &mbA[b], tid, wsum);
       }
+      if (tr) trace[k * 8 + 3] = clock64();
       if (tid == 0) mb_expect(&mbA[b], 8u * (uint32_t)(m - k - 1 + C));
       {
         const uint32_t u = b ? useA1 : useA0;
         mb_wait(&mbA[b], u & 1u);
         if (b) ++useA1; else ++useA0;
       }
+      if (tr) trace[k * 8 + 4] = clock64();
       // (3) rank-2 update of own columns; row k+1 first, pushed to every CTA
       if (own) {
         double tot = 0.0;
@@ -1212,8 +1221,10 @@ tridiag_cluster_mb(const double* __restrict__ Asrc, int m, int symmetrize, doubl
       const double wv = Wl[(k + 1) * nc + tid];
       for (int r = 0; r < C; ++r) st_async_f64(nextrow + icol, &mbB[b ^ 1], r, wv);
     }
+    if (tr) trace[k * 8 + 5] = clock64();
     // warp 0 forms the next reflector while the other warps finish their updates
     if (warp == 0 && k + 3 < m) reflect(k + 1);
+    if (tr) trace[k * 8 + 6] = clock64();
   }
   if (m >= 2) {
     const int kk = m - 2;  // row m-2 was pushed at step m-3 (or at init when m == 2)
@@ -1617,7 +1628,28 @@ void launch_tridiag(const double* Asrc, int m, int symmetrize, double* Wg, doubl
     if (variant == 0)
       cudaLaunchKernelEx(&cfg, tridiag_cluster, Asrc, m, symmetrize, V, tau, d, e, status);
     else if (variant == 1)
-      cudaLaunchKernelEx(&cfg, tridiag_cluster_mb, Asrc, m, symmetrize, V, tau, d, e, status);
+    {
+      // SPB_TRI_TRACE=<file>: per-step clock64 phase stamps of the last CTA's
+      // thread 0 appended to <file> (diagnostics only; synchronises the stream)
+      static const char* tf = getenv("SPB_TRI_TRACE");
+      static long long* tbuf = nullptr;
+      if (tf && !tbuf) cudaMalloc(&tbuf, sizeof(long long) * 8 * 4096);
+      long long* trace = (tf && m <= 4096) ? tbuf : nullptr;
+      cudaLaunchKernelEx(&cfg, tridiag_cluster_mb, Asrc, m, symmetrize, V, tau, d, e, status, trace);
+      if (trace) {
+        std::vector<long long> h((size_t)8 * m);
+        cudaMemcpyAsync(h.data(), trace, sizeof(long long) * 8 * m, cudaMemcpyDeviceToHost, st);
+        cudaStreamSynchronize(st);
+        if (FILE* f = fopen(tf, "a")) {
+          fprintf(f, "m %d C %d\n", m, C);
+          for (int k = 0; k + 2 < m; ++k) {
+            for (int j = 0; j < 8; ++j) fprintf(f, "%lld ", h[(size_t)k * 8 + j]);
+            fprintf(f, "\n");
+          }
+          fclose(f);
+        }
+      }
+    }
     else
       cudaLaunchKernelEx(&cfg, tridiag_fused, Asrc, m, symmetrize, V, tau, d, e, status);
     return;

@@ -15,6 +15,7 @@ ap = argparse.ArgumentParser()
 ap.add_argument("--mode", type=int, default=0)
 ap.add_argument("--reps", type=int, default=10)
 ap.add_argument("--dtype", default="float32")
+ap.add_argument("--profile", action="store_true")
 ap.add_argument("--shapes", default="500000x108x108,500000x324x324,50000x147x147,50000x49x49,2000000x176x176")
 a = ap.parse_args()
 tdt = torch.float32 if a.dtype == "float32" else torch.float64
@@ -46,3 +47,11 @@ for sh in a.shapes.split(","):
     ref = (u[:, :p].double().T @ v[:, :q].double())
     err = ((out - ref).abs().max() / (u[:, :p].abs().double().T @ v[:, :q].abs().double()).max()).item()
     print(f"{sh:>20s}  {ms:8.3f} ms  {2.0*n*p*q/ms/1e9:7.2f} TFLOP/s  relerr {err:.2e}", flush=True)
+    if a.profile:
+        from torch.profiler import ProfilerActivity, profile
+        with profile(activities=[ProfilerActivity.CUDA]) as prof:
+            run()
+            torch.cuda.synchronize()
+        for ev in prof.key_averages():
+            if ev.device_time_total > 0:
+                print(f"      {ev.key[:70]:70s} {ev.device_time_total:9.1f} us  x{ev.count}")
