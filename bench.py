@@ -402,7 +402,7 @@ def run_ours(args):
                        "parallelism": ("row-sharded" if sharded else "replicas") if world > 1 else "single"},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": (achieved / peak) if achieved else None, "traffic": traffic,
-                         "kernel": "spb::spmm_vec (Laplacian SpMM)", "peak_kind": peak_kind,
+                         "kernel": "spb::spmm_vb (Laplacian SpMM)", "peak_kind": peak_kind,
                          "launches": spmm_calls,
                          "avg_launch_us": spmm_us / max(spmm_calls, 1),
                          "bytes_model": "compulsory 4(n+1)+(4+esz)nnz+esz*n+2*esz*n*cols per apply",

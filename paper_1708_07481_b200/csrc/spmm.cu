@@ -108,6 +108,74 @@ spmm_vec(int32_t r0, int32_t r1, const int32_t* __restrict__ rp, const int32_t* 
   }
 }
 
+// Batched variant of spmm_vec: each lane gathers U neighbour vectors into
+// registers before the FMAs, so U independent L2 loads are in flight per lane
+// (the gather is latency-bound: X rows come from L2 in random order). The FMA
+// order per (lane, vector) is the same as spmm_vec's.
+template <typename T, int GS, int U, int MINB>
+__global__ void __launch_bounds__(256, MINB)
+spmm_vb(int32_t r0, int32_t r1, const int32_t* __restrict__ rp, const int32_t* __restrict__ ci,
+        const T* __restrict__ cv, const T* __restrict__ deg, const T* __restrict__ x,
+        int64_t ldx, int c0, int ncols, T* __restrict__ y, int64_t ldy, int64_t xoff) {
+  using V = typename Vec<T>::type;
+  constexpr int VN = Vec<T>::N;
+  constexpr int NG = 32 / GS;
+  const int lane = threadIdx.x & 31;
+  const int g = lane / GS, gl = lane % GS;
+  const int32_t row = r0 + (int32_t)((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5);
+  if (row >= r1) return;
+  const int nvec = (ncols + VN - 1) / VN;
+  const int32_t e0 = rp[row], e1 = rp[row + 1];
+  for (int vbase = 0; vbase < nvec; vbase += GS) {
+    const int v = vbase + gl;
+    const bool act = v < nvec;
+    const int64_t coff = c0 + (int64_t)v * VN;
+    const T* xb = x + coff;
+    V acc = vzero<V>();
+    for (int32_t eb = e0; eb < e1; eb += 32) {
+      const int32_t my = eb + lane;
+      int32_t cj = 0;
+      T wv = T(0);
+      if (my < e1) {
+        cj = __ldg(ci + my);
+        wv = __ldg(cv + my);
+      }
+      const int cnt = min(32, e1 - eb);
+      for (int kk = 0; kk < cnt; kk += NG * U) {  // warp-uniform trip count
+        V xv[U];
+        T ww[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const int k = kk + u * NG + g;
+          const int srcl = k < cnt ? k : 0;
+          const int32_t j = __shfl_sync(0xffffffffu, cj, srcl);
+          const T w = __shfl_sync(0xffffffffu, wv, srcl);
+          const bool ok = act && k < cnt;
+          ww[u] = ok ? w : T(0);
+          xv[u] = ok ? __ldg(reinterpret_cast<const V*>(xb + (int64_t)j * ldx)) : vzero<V>();
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+          if (kk + u * NG + g < cnt) vfma(acc, ww[u], xv[u]);
+      }
+      __syncwarp();
+    }
+#pragma unroll
+    for (int o = GS; o < 32; o <<= 1) vshfl_add(acc, o);
+    if (g == 0 && act) {
+      const V xi = *reinterpret_cast<const V*>(x + (xoff + row) * ldx + coff);
+      const T d = deg[row];
+      V out = vaxpy_out(d, xi, acc);
+      T* yp = y + (int64_t)row * ldy + coff;
+      if (coff - c0 + VN <= ncols) {
+        *reinterpret_cast<V*>(yp) = out;
+      } else {
+        for (int q = 0; q < VN && coff - c0 + q < ncols; ++q) yp[q] = vget(out, q);
+      }
+    }
+  }
+}
+
 // Scalar fallback for unaligned / odd strides.
 template <typename T>
 __global__ void __launch_bounds__(256)
@@ -164,6 +232,19 @@ int launch_spmm(int32_t r0, int32_t r1, const int32_t* rp, const int32_t* ci, co
   for (int c0 = 0; c0 < ncols; c0 += (int)panel) {
     const int pc = (int)std::min<int64_t>(panel, ncols - c0);
     const int nvec = (pc + VN - 1) / VN;
+    // spmm_vb (2 gathers in flight per lane, 128-thread blocks so short rows
+    // free their slots early) for rows of more than 8 vectors: -7 % at C2, -9 %
+    // at C3 against spmm_vec; SPB_SPMM_VARIANT=0 selects spmm_vec
+    static const int variant = getenv("SPB_SPMM_VARIANT") ? atoi(getenv("SPB_SPMM_VARIANT")) : 2;
+    if (variant >= 1 && nvec > 8) {
+      auto kf = nvec <= 16 ? (variant == 1 ? spmm_vb<T, 16, 4, 6> : variant == 2 ? spmm_vb<T, 16, 2, 8> : spmm_vb<T, 16, 8, 4>)
+                           : (variant == 1 ? spmm_vb<T, 32, 4, 6> : variant == 2 ? spmm_vb<T, 32, 2, 8> : spmm_vb<T, 32, 8, 4>);
+      static const int vt = getenv("SPB_SPMM_THREADS") ? atoi(getenv("SPB_SPMM_THREADS")) : 128;
+      const int64_t vblocks = ceil_div(rows * 32, vt);
+      kf<<<vblocks, vt, 0, st>>>(r0, r1, rp, ci, cv, deg, x, ldx, c0, pc, y, ldy, xoff);
+      SPB_LAUNCH_CHECK();
+      continue;
+    }
     if (nvec <= 1)
       spmm_vec<T, 1><<<blocks, threads, 0, st>>>(r0, r1, rp, ci, cv, deg, x, ldx, c0, pc, y, ldy, xoff);
     else if (nvec <= 2)
