@@ -200,6 +200,18 @@ SPB_API int spb_orthonormalize(int dtype, void* b, int64_t ldb, int32_t n, int32
                                spb_refill_cb refill, void* user, void* ws, size_t ws_bytes,
                                void* stream);
 
+/* Block update out = init + scale * A C (the basis update of lobpcg.py:436-439
+ * and the right-multiplications of :228, :366, one segment): A device n x w
+ * (row stride lda), c device float64 w x q (row stride ldc), init NULL or
+ * n x q; out may alias init or A (in place). mode 0: float32 CUDA-core FMA,
+ * 1: 3xTF32 tensor cores (float32 only), -1: the solver's default.
+ * ws: spb_block_update_workspace(w, q) bytes. */
+SPB_API size_t spb_block_update_workspace(int32_t w, int32_t q);
+SPB_API int spb_block_update(int dtype, int mode, const void* a, int64_t lda, int32_t w,
+                             const double* c, int64_t ldc, int32_t q, double scale,
+                             const void* init, int64_t ldi, void* out, int64_t ldo, int64_t n,
+                             void* ws, size_t ws_bytes, void* stream);
+
 /* Small projected problem (lobpcg.py:168-177): ga, gb are device float64
  * m x m (symmetrised inside); gb may be NULL for B = I. Outputs: theta
  * (device, nev smallest, ascending) and c (device m x nev row-major,

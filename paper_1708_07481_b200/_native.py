@@ -62,6 +62,9 @@ _SIGS = {
     "spb_laplacian_spmm": (C.c_int, [C.c_int, i32, i32, vp, vp, vp, vp, vp, i64, i32, vp, i64, vp]),
     "spb_gram_workspace": (sz, [i32, i32, i64]),
     "spb_gram": (C.c_int, [C.c_int, C.c_int, vp, i64, i32, vp, i64, i32, i64, vp, i64, vp, sz, vp]),
+    "spb_block_update_workspace": (sz, [i32, i32]),
+    "spb_block_update": (C.c_int, [C.c_int, C.c_int, vp, i64, i32, vp, i64, i32, f64, vp, i64, vp,
+                                   i64, i64, vp, sz, vp]),
     "spb_lobpcg_workspace": (sz, [C.c_int, i32, i32]),
     "spb_lobpcg_solve": (C.c_int, [C.POINTER(Operator), C.c_int, vp, C.POINTER(SolverConfigC),
                                    ITER_CB, REFILL_CB, PRECOND_CB, vp, vp, sz, vp,

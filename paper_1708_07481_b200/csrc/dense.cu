@@ -345,7 +345,8 @@ int launch_gram_cfg(GramBatch bb, int64_t n, int out_rows, int out_cols, double*
   }
   bb.tile_start[bb.njobs] = tiles;
   int64_t ks = std::max<int64_t>(1, (int64_t)ctas_per_sm * num_sms() / std::max(tiles, 1));
-  ks = std::min<int64_t>(ks, ceil_div(n, 128));
+  static const int minrows = getenv("SPB_GRAM_MINROWS") ? atoi(getenv("SPB_GRAM_MINROWS")) : 128;
+  ks = std::min<int64_t>(ks, ceil_div(n, std::max(32, minrows)));
   ks = std::max<int64_t>(ks, 1);
   while (ks > 1 && (size_t)ks * out_rows * out_cols > partial_cap) --ks;
   if ((size_t)ks * out_rows * out_cols > partial_cap) {
@@ -426,7 +427,8 @@ int choose_ksplit(int64_t n, int tiles) {
   static const int per_sm = getenv("SPB_GRAM_WAVE") ? atoi(getenv("SPB_GRAM_WAVE")) : 3;
   const int target = std::max(1, per_sm) * num_sms();
   int64_t ks = std::max<int64_t>(1, target / std::max(tiles, 1));
-  ks = std::min<int64_t>(ks, ceil_div(n, 128));
+  static const int minrows = getenv("SPB_GRAM_MINROWS") ? atoi(getenv("SPB_GRAM_MINROWS")) : 128;
+  ks = std::min<int64_t>(ks, ceil_div(n, std::max(32, minrows)));
   return (int)std::max<int64_t>(ks, 1);
 }
 
@@ -670,10 +672,22 @@ void launch_update_qv(const UpdParams& p, int64_t n, cudaStream_t st) {
   update_kernel<T, QV, RPT><<<blocks, 256, 0, st>>>(p, n);
 }
 
+static int g_update_mode = -1;  // spb_block_update's override (-1: default)
+
 template <typename T>
 void launch_update(const UpdParams& p, int64_t n, cudaStream_t st) {
   static const bool generic = getenv("SPB_UPDATE_GENERIC") != nullptr;  // A/B switch
+  // float32: 3xTF32 on the tensor cores (update_tc.cu) unless SPB_UPDATE_TC=0
+  static const bool tc_env = !getenv("SPB_UPDATE_TC") || atoi(getenv("SPB_UPDATE_TC")) != 0;
+  const bool tc = g_update_mode < 0 ? tc_env : g_update_mode == 1;
+  if (sizeof(T) == 4 && tc && !generic && update_tc(p, n, st)) return;
   // narrow blocks (q <= 64, C1/C2) measure faster on the generic kernel
+  static const int narrow = getenv("SPB_UPDATE_NARROW") ? atoi(getenv("SPB_UPDATE_NARROW")) : 0;
+  if (sizeof(T) == 4 && !generic && narrow && p.q > 32 && p.q <= 64 && update_f32_ok(p)) {
+    if (narrow == 1) launch_update_f32<8, 16>(p, n, st);
+    else launch_update_f32<8, 32>(p, n, st);
+    return;
+  }
   if (sizeof(T) == 4 && !generic && p.q > 64 && update_f32_ok(p)) {
     if (p.q <= 128) launch_update_f32<16, 8>(p, n, st);
     else if (p.q <= 192) launch_update_f32<24, 8>(p, n, st);
@@ -891,7 +905,7 @@ int oz_sum_splits(const double* part, int ks, int64_t stride, int rows, int cols
 }
 
 size_t update_cstage_floats(int w_total, int nseg) {
-  return (size_t)(w_total + nseg * UKT) * 256;
+  return std::max((size_t)(w_total + nseg * UKT) * 256, update_tc_cstage_floats(w_total, nseg, 256));
 }
 
 size_t colreduce_partial_doubles(int64_t n, int cols) {
@@ -981,3 +995,47 @@ int dense_apply(const double* Adense, int64_t n, const void* X, int64_t ldx, int
 }
 
 }  // namespace spb
+
+extern "C" size_t spb_block_update_workspace(int32_t w, int32_t q) {
+  (void)q;
+  return sizeof(float) * spb::update_cstage_floats(std::max(w, 1), 1) + 256;
+}
+
+extern "C" int spb_block_update(int dtype, int mode, const void* a, int64_t lda, int32_t w,
+                                const double* c, int64_t ldc, int32_t q, double scale,
+                                const void* init, int64_t ldi, void* out, int64_t ldo, int64_t n,
+                                void* ws, size_t ws_bytes, void* stream) {
+  using namespace spb;
+  if (dtype != SPB_F32 && dtype != SPB_F64) {
+    set_error("unknown dtype %d", dtype);
+    return SPB_ERR_DOMAIN;
+  }
+  if (w < 1 || q < 1 || q > 256 || n < 0 || lda < w || ldc < q || ldo < q || (init && ldi < q)) {
+    set_error("block update shape contract violated");
+    return SPB_ERR_CONTRACT;
+  }
+  if (mode == 1 && dtype != SPB_F32) {
+    set_error("tensor-core update needs float32 storage");
+    return SPB_ERR_DOMAIN;
+  }
+  if (ws_bytes < spb_block_update_workspace(w, q)) {
+    set_error("block update workspace too small");
+    return SPB_ERR_WORKSPACE;
+  }
+  if (n == 0) return SPB_OK;
+  UpdParams p{};
+  p.nseg = 1;
+  p.q = q;
+  p.init = init;
+  p.ldi = ldi;
+  p.seg[0] = {a, lda, c, ldc, out, ldo, scale, w, 1};
+  p.cstage = (float*)(((uintptr_t)ws + 255) & ~(uintptr_t)255);
+  p.cstage_cap = (ws_bytes - 256) / sizeof(float);
+  const int saved = g_update_mode;
+  g_update_mode = mode;
+  const int rc = block_update(dtype, p, n, (cudaStream_t)stream);
+  g_update_mode = saved;
+  if (rc != SPB_OK) return rc;
+  SPB_LAUNCH_CHECK();
+  return SPB_OK;
+}

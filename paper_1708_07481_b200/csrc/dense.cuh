@@ -47,6 +47,9 @@ struct UpdParams {
 
 // Staging floats the fp32 update needs for segments of total width w_total.
 size_t update_cstage_floats(int w_total, int nseg);
+// Tensor-core (3xTF32) float32 update (update_tc.cu): false = not launched.
+bool update_tc(const UpdParams& p, int64_t n, cudaStream_t st);
+size_t update_tc_cstage_floats(int w_total, int nseg, int q);
 
 // Column-reduction kinds.
 enum ColReduce { CR_SUMSQ = 0, CR_SUM = 1, CR_RESIDUAL = 2 };

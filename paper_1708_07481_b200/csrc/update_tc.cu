@@ -1,0 +1,451 @@
+// (c) Block update on the 5th-generation tensor cores: 3xTF32 split, TMA-fed.
+//
+//   acc = init + sum_s A_s (scale_s C_s),  written to seg.out after every
+//   segment with emit set (the running sum, as block_update's other kernels).
+//
+// This is the LOBPCG basis update X' = X Cx + R Cr + P Cp, P' = R Cr + P Cp of
+// lobpcg.py:436-439 (and the in-place right-multiplications of :228, :366) as a
+// GEMM with M = 128 rows (vertices) per CTA, N = q (block width, padded to 16),
+// K = the segment widths. The float32 operands are split as x = hi + lo with
+// hi = x rounded to the nearest TF32 value and lo = (x - hi) rounded likewise
+// (split error 2^-24 |x|); three tcgen05.mma.kind::tf32 per K step (hi*lo +
+// lo*hi + hi*hi) into one fp32 TMEM accumulator give float32-accurate products.
+//
+// Warp roles (320 threads):
+//   warp 0    TMA producer: {32 columns x 128 rows} boxes of A_s, 128-byte
+//             swizzled, plus one bulk copy of the pre-split coefficient chunk
+//             (hi | lo, same swizzled K-major layout, staged once per launch by
+//             tc_stage_coeffs);
+//   warp 1    MMA issuer (one thread); each 32-deep chunk into one of two TMEM
+//             regions (double-buffered);
+//   warps 2-5 splitters: hi written in place over the staged tile, lo into its
+//             own buffer (elementwise, so the swizzled layout is preserved);
+//   warps 6-9 epilogue: per chunk, tcgen05.ld the region and add it into
+//             float32 registers (round-to-nearest: the tensor cores' own
+//             accumulation, which is not, then spans 12 MMAs only); at every
+//             emit, store the running sum (+ init) as float32 rows.
+#include <cuda.h>
+
+#include "dense.cuh"
+
+namespace spb {
+namespace {
+
+constexpr int UTM = 128;             // rows per CTA (UMMA M)
+constexpr int UTK = 32;              // K per chunk (one 128-byte swizzle atom of fp32)
+constexpr int UTS_MAX = 4;           // pipeline stages (runtime: 2 when two CTAs fit per SM)
+constexpr int kUtA = UTM * UTK * 4;  // A tile bytes (16 KB)
+constexpr int kUtThreads = 320;
+
+__device__ __forceinline__ uint32_t ut_smem(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void ut_mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(ut_smem(bar)), "r"(count));
+}
+__device__ __forceinline__ void ut_expect(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(ut_smem(bar)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void ut_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(ut_smem(bar)) : "memory");
+}
+__device__ __forceinline__ void ut_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred P;\n"
+      "UTW_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P, [%0], %1;\n\t"
+      "@!P bra UTW_%=;\n}" ::"r"(ut_smem(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void ut_tma2d(void* dst, const CUtensorMap* map, uint64_t* bar, int c0,
+                                         int c1) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, "
+      "%3}], [%4];" ::"r"(ut_smem(dst)),
+      "l"(map), "r"(c0), "r"(c1), "r"(ut_smem(bar))
+      : "memory");
+}
+__device__ __forceinline__ void ut_bulk(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          ut_smem(dst)),
+      "l"(src), "r"(bytes), "r"(ut_smem(bar))
+      : "memory");
+}
+// K-major, 128-byte swizzle: 8-row x 128-byte atoms, SBO = 1024 B between atoms
+// along M/N; a K step of 8 tf32 advances the start address by 32 bytes.
+__device__ __forceinline__ uint64_t ut_desc_sw128(uint32_t saddr) {
+  uint64_t d = 0;
+  d |= (uint64_t)((saddr >> 4) & 0x3FFF);
+  d |= (uint64_t)1 << 16;                   // LBO (unused for swizzled K-major)
+  d |= (uint64_t)(1024 >> 4) << 32;         // SBO
+  d |= (uint64_t)1 << 46;                   // descriptor version (Blackwell)
+  d |= (uint64_t)2 << 61;                   // layout: SWIZZLE_128B
+  return d;
+}
+__device__ __forceinline__ void ut_mma(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t idesc,
+                                       uint32_t accum) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+      "l"(a), "l"(b), "r"(idesc), "r"(accum));
+}
+__device__ __forceinline__ void ut_commit(uint64_t* bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                   ut_smem(bar))
+               : "memory");
+}
+// Round to the nearest TF32 value (a float32 container with 13 zero low bits).
+__device__ __forceinline__ float tf32_rna(float x) {
+  uint32_t r;
+  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
+  return __uint_as_float(r);
+}
+// x = hi + lo with both parts TF32 values rounded to nearest: the split error is
+// 2^-24 |x| (the lo part's own rounding), not the 2^-22 of truncated parts.
+__device__ __forceinline__ void tf32_split(float x, float& hi, float& lo) {
+  hi = tf32_rna(x);
+  lo = tf32_rna(x - hi);  // x - hi is exact in float32
+}
+
+struct UtSeg {
+  int chunks;      // ceil(w / UTK)
+  int emit;
+  float* out;
+  int64_t ldo;
+};
+
+struct UtParams {
+  UtSeg seg[3];
+  int nseg;
+  int q, npad;              // output columns, UMMA N (multiple of 16)
+  int nemit;
+  const float* init;
+  int64_t ldi;
+  const float* coef;        // staged chunks: [chunk][hi | lo][npad rows x 128 B, swizzled]
+  int64_t n;
+  uint32_t tmem_cols;
+  int stages;
+};
+
+// Coefficient chunks: element (output column j, k) of chunk c of segment s is
+// scale_s C_s[32 c + k][j], stored at the 128-byte-swizzled K-major position.
+__global__ void tc_stage_coeffs(UpdParams P, int npad, float* __restrict__ dst) {
+  int cbase = 0;
+  for (int s = 0; s < P.nseg; ++s) {
+    const UpdSeg sg = P.seg[s];
+    const int chunks = (sg.w + UTK - 1) / UTK;
+    const int total = chunks * npad * UTK;
+    for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < total; e += gridDim.x * blockDim.x) {
+      const int c = e / (npad * UTK), r = e % (npad * UTK);
+      const int j = r / UTK, k = r % UTK;
+      const int kg = c * UTK + k;
+      float x = 0.0f;
+      if (kg < sg.w && j < P.q) x = (float)(sg.scale * sg.C[(int64_t)kg * sg.ldc + j]);
+      float h, l;
+      tf32_split(x, h, l);
+      const int off = (j >> 3) * 256 + (j & 7) * 32 + (((k >> 2) ^ (j & 7)) << 2) + (k & 3);
+      float* chunk = dst + (size_t)(cbase + c) * 2 * npad * UTK;
+      chunk[off] = h;
+      chunk[npad * UTK + off] = l;
+    }
+    cbase += chunks;
+  }
+}
+
+template <int NPMAX>
+__global__ void __launch_bounds__(kUtThreads, 1)
+update_tc_kernel(const __grid_constant__ CUtensorMap map0, const __grid_constant__ CUtensorMap map1,
+                 const __grid_constant__ CUtensorMap map2, UtParams P) {
+  extern __shared__ __align__(1024) uint8_t usm_raw[];
+  uint8_t* base = (uint8_t*)(((uintptr_t)usm_raw + 1023) & ~(uintptr_t)1023);
+  const int kB = 2 * P.npad * UTK * 4;              // coefficient chunk bytes (hi | lo)
+  const int kStage = 2 * kUtA + kB;                 // [A hi (staged in place)][A lo][B hi|lo]
+  const int UTS = P.stages;
+  uint64_t* full = (uint64_t*)(base + UTS * kStage);
+  uint64_t* split = full + UTS_MAX;
+  uint64_t* empty = split + UTS_MAX;
+  uint64_t* rdone = empty + UTS_MAX;                // [2] chunk partial ready in TMEM
+  uint64_t* rfree = rdone + 2;                      // [2] region read by the epilogue
+  uint32_t* tmem_slot = (uint32_t*)(rfree + 2);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int ntiles = (int)((P.n + UTM - 1) / UTM);
+  // persistent: tiles blockIdx.x, blockIdx.x + gridDim.x, ...; chunk counters
+  // run on across tiles so the stage ring and TMEM regions never drain
+  int nk = 0;
+  for (int s = 0; s < P.nseg; ++s) nk += P.seg[s].chunks;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < UTS; ++s) {
+      ut_mbar_init(&full[s], 1);
+      ut_mbar_init(&split[s], 128);
+      ut_mbar_init(&empty[s], 1);
+    }
+    for (int e = 0; e < 2; ++e) {
+      ut_mbar_init(&rdone[e], 1);
+      ut_mbar_init(&rfree[e], 128);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     ut_smem(tmem_slot)),
+                 "r"(P.tmem_cols));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;");
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      int g = 0;
+      for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+        int kc = 0;
+        for (int s = 0; s < P.nseg; ++s) {
+          const CUtensorMap* map = s == 0 ? &map0 : (s == 1 ? &map1 : &map2);
+          for (int c = 0; c < P.seg[s].chunks; ++c, ++kc, ++g) {
+            const int st = g % UTS, u = g / UTS;
+            if (u > 0) ut_wait(&empty[st], (u - 1) & 1);
+            uint8_t* sb = base + st * kStage;
+            ut_expect(&full[st], (uint32_t)(kUtA + kB));
+            ut_tma2d(sb, map, &full[st], c * UTK, tile * UTM);
+            ut_bulk(sb + 2 * kUtA, P.coef + (size_t)kc * 2 * P.npad * UTK, (uint32_t)kB, &full[st]);
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      const uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) |  // F32 acc, TF32 A/B, K-major
+                             ((uint32_t)(P.npad >> 3) << 17) | ((uint32_t)(UTM >> 4) << 24);
+      const int total = ((ntiles - (int)blockIdx.x + (int)gridDim.x - 1) / (int)gridDim.x) * nk;
+      for (int kc = 0; kc < total; ++kc) {
+        const int st = kc % UTS, u = kc / UTS;
+        const int rg = kc & 1;  // TMEM region of this chunk (double-buffered)
+        if (kc >= 2) ut_wait(&rfree[rg], ((kc >> 1) - 1) & 1);
+        ut_wait(&split[st], u & 1);
+        asm volatile("tcgen05.fence::after_thread_sync;");
+        uint8_t* sb = base + st * kStage;
+        const uint32_t ahi = ut_smem(sb), alo = ut_smem(sb + kUtA);
+        const uint32_t bhi = ut_smem(sb + 2 * kUtA), blo = bhi + (uint32_t)(P.npad * UTK * 4);
+        const uint32_t dacc = tmem + (uint32_t)(rg * P.npad);
+#pragma unroll
+        for (int kk = 0; kk < UTK / 8; ++kk) {
+          const uint32_t off = (uint32_t)kk * 32;
+          const uint64_t dah = ut_desc_sw128(ahi + off), dal = ut_desc_sw128(alo + off);
+          const uint64_t dbh = ut_desc_sw128(bhi + off), dbl = ut_desc_sw128(blo + off);
+          ut_mma(dacc, dah, dbl, idesc, kk == 0 ? 0u : 1u);  // small terms first
+          ut_mma(dacc, dal, dbh, idesc, 1u);
+          ut_mma(dacc, dah, dbh, idesc, 1u);
+        }
+        ut_commit(&empty[st]);
+        ut_commit(&rdone[rg]);
+      }
+    }
+  } else if (warp < 6) {
+    // splitters: hi in place, lo to its own buffer (elementwise: layout preserved)
+    const int t = threadIdx.x - 64;
+    const int total = ((ntiles - (int)blockIdx.x + (int)gridDim.x - 1) / (int)gridDim.x) * nk;
+    for (int kc = 0; kc < total; ++kc) {
+      const int st = kc % UTS, u = kc / UTS;
+      ut_wait(&full[st], u & 1);
+      float4* a = reinterpret_cast<float4*>(base + st * kStage);
+      float4* lo = reinterpret_cast<float4*>(base + st * kStage + kUtA);
+#pragma unroll
+      for (int i = 0; i < kUtA / 16 / 128; ++i) {
+        const int e = i * 128 + t;
+        const float4 x = a[e];
+        float4 h, l;
+        tf32_split(x.x, h.x, l.x);
+        tf32_split(x.y, h.y, l.y);
+        tf32_split(x.z, h.z, l.z);
+        tf32_split(x.w, h.w, l.w);
+        a[e] = h;
+        lo[e] = l;
+      }
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      ut_arrive(&split[st]);
+    }
+  } else {
+    // epilogue: warps 6..9 -> TMEM lane quarter (warp & 3) = tile rows. Every
+    // chunk's 32-deep partial product is added into float32 registers
+    // (round-to-nearest), so the tensor cores' accumulation covers only 12
+    // MMAs; the running sum is written at every emit.
+    const int quarter = warp & 3;
+    int kc = 0;
+    for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    const int64_t row = (int64_t)tile * UTM + quarter * 32 + lane;
+    float acc[NPMAX];
+#pragma unroll
+    for (int i = 0; i < NPMAX; ++i) acc[i] = 0.0f;
+    if (P.init && row < P.n) {
+      const float* irow = P.init + row * P.ldi;
+#pragma unroll
+      for (int i = 0; i < NPMAX; ++i)
+        if (i < P.q) acc[i] = irow[i];
+    }
+    for (int s = 0; s < P.nseg; ++s) {
+      for (int c = 0; c < P.seg[s].chunks; ++c, ++kc) {
+        const int rg = kc & 1;
+        ut_wait(&rdone[rg], (kc >> 1) & 1);
+        asm volatile("tcgen05.fence::after_thread_sync;");
+#pragma unroll
+        for (int c0 = 0; c0 < NPMAX; c0 += 16) {
+          if (c0 < P.npad) {
+            uint32_t r[16];
+            const uint32_t taddr =
+                tmem + ((uint32_t)(quarter * 32) << 16) + (uint32_t)(rg * P.npad + c0);
+            asm volatile(
+                "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, "
+                "%10, %11, %12, %13, %14, %15}, [%16];"
+                : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]),
+                  "=r"(r[6]), "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]),
+                  "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+                : "r"(taddr));
+            asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+            for (int i = 0; i < 16; ++i) acc[c0 + i] += __uint_as_float(r[i]);
+          }
+        }
+        asm volatile("tcgen05.fence::before_thread_sync;");
+        ut_arrive(&rfree[rg]);
+      }
+      if (P.seg[s].emit && row < P.n) {
+        float* orow = P.seg[s].out + row * P.seg[s].ldo;
+        const bool vec = (reinterpret_cast<uintptr_t>(orow) & 15) == 0;
+#pragma unroll
+        for (int c0 = 0; c0 < NPMAX; c0 += 4) {
+          if (vec && c0 + 4 <= P.q)
+            *reinterpret_cast<float4*>(orow + c0) =
+                make_float4(acc[c0], acc[c0 + 1], acc[c0 + 2], acc[c0 + 3]);
+          else
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+              if (c0 + i < P.q) orow[c0 + i] = acc[c0 + i];
+        }
+      }
+    }
+    }  // tile
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  if (warp == 0) {
+    asm volatile("tcgen05.fence::after_thread_sync;");
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(P.tmem_cols));
+  }
+}
+
+typedef CUresult (*UtEncodeFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                               const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                               const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                               CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+UtEncodeFn ut_encode() {
+  static UtEncodeFn fn = nullptr;
+  static bool tried = false;
+  if (!tried) {
+    tried = true;
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) ==
+            cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = (UtEncodeFn)p;
+  }
+  return fn;
+}
+
+// {cols (K, inner) x rows} float32 view with row pitch ld, 32 x 128 boxes, 128B swizzle
+bool ut_map(CUtensorMap* m, const void* ptr, int64_t rows, int cols, int64_t ld) {
+  UtEncodeFn fn = ut_encode();
+  if (!fn) return false;
+  const cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
+  const cuuint64_t strides[1] = {(cuuint64_t)ld * 4};
+  const cuuint32_t box[2] = {(cuuint32_t)UTK, (cuuint32_t)UTM};
+  const cuuint32_t estr[2] = {1, 1};
+  return fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<void*>(ptr), dims, strides, box, estr,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+            CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+}  // namespace
+
+size_t update_tc_cstage_floats(int w_total, int nseg, int q) {
+  const int npad = (q + 15) / 16 * 16;
+  return (size_t)((w_total + UTK - 1) / UTK + nseg) * 2 * npad * UTK;
+}
+
+// Float32 block update on the tensor cores; returns false (nothing launched)
+// when the shape is outside the kernel's envelope, so the caller falls back.
+bool update_tc(const UpdParams& p, int64_t n, cudaStream_t st) {
+  if (p.nseg < 1 || p.nseg > 3 || p.q < 1 || p.q > 256 || n < 1 || n > INT32_MAX) return false;
+  const int npad = (p.q + 15) / 16 * 16;
+  int nemit = 0, chunks = 0, wtot = 0;
+  for (int s = 0; s < p.nseg; ++s) {
+    const UpdSeg& g = p.seg[s];
+    if (g.w < 1) return false;
+    if ((reinterpret_cast<uintptr_t>(g.A) & 15) || (g.lda & 3)) return false;
+    nemit += g.emit ? 1 : 0;
+    chunks += (g.w + UTK - 1) / UTK;
+    wtot += g.w;
+  }
+  if (nemit < 1 || !p.seg[p.nseg - 1].emit || npad > 128) return false;
+  uint32_t cols = 32;
+  while (cols < (uint32_t)(2 * npad)) cols <<= 1;
+  const size_t need = (size_t)chunks * 2 * npad * UTK;
+  if (!p.cstage || need > p.cstage_cap || need > update_tc_cstage_floats(wtot, p.nseg, p.q) ||
+      (reinterpret_cast<uintptr_t>(p.cstage) & 15))
+    return false;
+  CUtensorMap maps[3];
+  for (int s = 0; s < 3; ++s) {
+    const UpdSeg& g = p.seg[s < p.nseg ? s : 0];
+    if (!ut_map(&maps[s], g.A, n, g.w, g.lda)) return false;
+  }
+  UtParams P{};
+  for (int s = 0; s < p.nseg; ++s) {
+    P.seg[s].chunks = (p.seg[s].w + UTK - 1) / UTK;
+    P.seg[s].emit = p.seg[s].emit;
+    P.seg[s].out = (float*)p.seg[s].out;
+    P.seg[s].ldo = p.seg[s].ldo;
+  }
+  P.nseg = p.nseg;
+  P.q = p.q;
+  P.npad = npad;
+  P.nemit = nemit;
+  P.init = (const float*)p.init;
+  P.ldi = p.ldi;
+  P.coef = p.cstage;
+  P.n = n;
+  P.tmem_cols = cols;
+  const int kB = 2 * npad * UTK * 4;
+  const size_t kStage = 2 * kUtA + kB;
+  // two stages when two CTAs fit per SM (one CTA's epilogue overlaps the other's
+  // MMAs), else three
+  int stages = 2 * (2 * kStage + 1280) <= 227 * 1024 ? 2 : 3;
+  if ((size_t)stages * kStage + 1280 > 227 * 1024) stages = 2;
+  P.stages = stages;
+  const size_t smem = (size_t)stages * kStage + 1024 + 256;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(update_tc_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    cudaFuncSetAttribute(update_tc_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    attr = true;
+  }
+  if (smem > 227 * 1024) return false;
+  tc_stage_coeffs<<<64, 256, 0, st>>>(p, npad, p.cstage);
+  const int per_sm = 2 * (smem + 2048) <= 228 * 1024 ? 2 : 1;
+  const unsigned grid = (unsigned)std::min<int64_t>(ceil_div(n, UTM), (int64_t)per_sm * num_sms());
+  if (npad <= 64)
+    update_tc_kernel<64><<<grid, kUtThreads, smem, st>>>(maps[0], maps[1], maps[2], P);
+  else
+    update_tc_kernel<128><<<grid, kUtThreads, smem, st>>>(maps[0], maps[1], maps[2], P);
+  return true;
+}
+
+}  // namespace spb
