@@ -453,7 +453,7 @@ constexpr int CWT = 512;  // threads of chol_wsync
 
 __global__ void __launch_bounds__(CWT)
 chol_wsync(const double* __restrict__ Bsrc, int m, double* __restrict__ Lg, double* __restrict__ Linv,
-           int mode, SmallStatus* status) {
+           int mode, SmallStatus* status, long long* trace) {
   extern __shared__ double smem[];
   __shared__ double red[33];
   __shared__ int fail;
@@ -473,6 +473,8 @@ chol_wsync(const double* __restrict__ Bsrc, int m, double* __restrict__ Lg, doub
       fb += v * v;
     }
   fb = block_sum(fb, red);
+  const bool tr = trace && threadIdx.x == 0;
+  if (tr) trace[0] = clock64();
   if (warp == 0) {
     int f0 = 0;
     if (mode == 1) {  // diag > 0 and min diag > (eps na)^2 max diag (lobpcg.py:229-231)
@@ -492,27 +494,65 @@ chol_wsync(const double* __restrict__ Bsrc, int m, double* __restrict__ Lg, doub
     if (tid == 0) status->fallback = 1;
     return;
   }
+  int hti = 0, htq = 0;
+  tri_index(tid, &hti, &htq);  // this thread's (row, col) in any trailing triangle
   for (int kb = 0; kb < m; kb += 32) {
     const int nb = min(32, m - kb);
     const int ke = kb + nb;
+    if (tr) trace[1 + (kb >> 5) * 4] = clock64();
     // ---- P1: diagonal block, right-looking; one element of the block's
-    // trailing triangle per thread and one CTA barrier per column
-    for (int c = 0; c < nb; ++c) {
-      const double dc = A[(kb + c) * ld + kb + c];
+    // trailing triangle per thread. Two columns per CTA barrier: every thread
+    // forms column c+1's update by column c on the fly (same operations as a
+    // separate step), then applies both rank-1 updates to its element.
+    int c = 0;
+    bool bad = false;  // uniform
+    for (; c + 1 < nb; c += 2) {
+      const int kc = kb + c;
+      const double dc = A[kc * ld + kc];
+      const double a10 = A[(kc + 1) * ld + kc];
       if (!(dc > 0.0)) {
         if (tid == 0) fail = 2;
+        bad = true;
         break;  // uniform: every thread read the same pivot
       }
       const double rc = 1.0 / dc;
-      const int rem = nb - 1 - c;
-      if (tid < rem * (rem + 1) / 2) {
-        int ti, tq;
-        tri_index(tid, &ti, &tq);
-        const int i = kb + c + 1 + ti, q = kb + c + 1 + tq;
-        A[i * ld + q] = fma(-A[i * ld + kb + c] * rc, A[q * ld + kb + c], A[i * ld + q]);
+      const double d1 = fma(-a10 * rc, a10, A[(kc + 1) * ld + kc + 1]);
+      if (!(d1 > 0.0)) {
+        if (tid == 0) fail = 2;
+        bad = true;
+        break;
       }
-      if (tid == 0) dinv[kb + c] = rc;
+      const double r1 = 1.0 / d1;
+      const int rem = nb - 1 - c;  // rows/cols kc+1 .. kb+nb-1
+      int paddr = -1;              // column c+1 result: written after the barrier,
+      double pval = 0.0;           // as other threads read the old value this step
+      if (tid < rem * (rem + 1) / 2) {
+        const int i = kc + 1 + hti, q = kc + 1 + htq;
+        const double aic = A[i * ld + kc], aqc = A[q * ld + kc];
+        const double ai1 = fma(-aic * rc, a10, A[i * ld + kc + 1]);  // column c+1 after step c
+        if (q == kc + 1) {
+          paddr = i * ld + q;
+          pval = i > kc + 1 ? ai1 : d1;
+        } else {
+          const double aq1 = fma(-aqc * rc, a10, A[q * ld + kc + 1]);
+          const double t = fma(-aic * rc, aqc, A[i * ld + q]);
+          A[i * ld + q] = fma(-ai1 * r1, aq1, t);
+        }
+      }
+      if (tid == 0) {
+        dinv[kc] = rc;
+        dinv[kc + 1] = r1;
+      }
       __syncthreads();
+      if (paddr >= 0) A[paddr] = pval;  // next step reads columns c+2, c+3 only
+    }
+    if (!bad && c < nb) {  // odd last column
+      const double dc = A[(kb + c) * ld + kb + c];
+      if (!(dc > 0.0)) {
+        if (tid == 0) fail = 2;
+      } else if (tid == 0) {
+        dinv[kb + c] = 1.0 / dc;
+      }
     }
     __syncthreads();
     if (fail) break;
@@ -522,6 +562,7 @@ chol_wsync(const double* __restrict__ Bsrc, int m, double* __restrict__ Lg, doub
       Lp[i][c] = (i < nb && c < i) ? A[(kb + i) * ld + kb + c] * dinv[kb + c] : (i == c ? 1.0 : 0.0);
     }
     __syncthreads();
+    if (tr) trace[2 + (kb >> 5) * 4] = clock64();
     if (fail) break;
     if (ke >= m) break;
     // ---- P2: rows below the block, one thread per row
@@ -542,6 +583,7 @@ chol_wsync(const double* __restrict__ Bsrc, int m, double* __restrict__ Lg, doub
         }
     }
     __syncthreads();
+    if (tr) trace[3 + (kb >> 5) * 4] = clock64();
     // ---- P3: trailing update A[i][q] -= sum_t A[i][kb+t] S[q][t], i >= q >= ke, 4x4 tiles
     const int T = m - ke;
     const int TT = (T + 3) / 4;
@@ -576,7 +618,9 @@ chol_wsync(const double* __restrict__ Bsrc, int m, double* __restrict__ Lg, doub
         }
     }
     __syncthreads();
+    if (tr) trace[4 + (kb >> 5) * 4] = clock64();
   }
+  if (tr) trace[40] = clock64();
   if (fail) {
     if (tid == 0) {
       if (mode == 0) status->not_pd = 1;
@@ -603,6 +647,7 @@ chol_wsync(const double* __restrict__ Bsrc, int m, double* __restrict__ Lg, doub
   for (int i = warp; i < m; i += CWT / 32)
     for (int j = lane; j < i; j += 32) A[i * ld + j] *= dinv[j] * dinv[j];
   __syncthreads();
+  if (tr) trace[41] = clock64();
   const int nblk = (m + 31) / 32;
   for (int bI = warp; bI < nblk; bI += CWT / 32) {  // diagonal blocks: lane = column j
     const int b0 = bI * 32, bn = min(32, m - b0);
@@ -624,6 +669,7 @@ chol_wsync(const double* __restrict__ Bsrc, int m, double* __restrict__ Lg, doub
         if (i > j && i < bn) A[(b0 + j) * ld + b0 + i] = x[i];
   }
   __syncthreads();
+  if (tr) trace[42] = clock64();
   // block rows on the FP64 tensor pipe (mma.sync m8n8k4): R = L'_{I,<I} X_{<I,<I},
   // then X_{I,<I} = -X_II R; every warp owns 8 x 8 output tiles
   for (int bI = 1; bI < nblk; ++bI) {
@@ -671,6 +717,7 @@ chol_wsync(const double* __restrict__ Bsrc, int m, double* __restrict__ Lg, doub
     }
     __syncthreads();
   }
+  if (tr) trace[43] = clock64();
   for (int i = warp; i < m; i += CWT / 32) {
     const double ri = dinv[i];
     for (int j = lane; j < m; j += 32) {
@@ -687,7 +734,9 @@ chol_wsync(const double* __restrict__ Bsrc, int m, double* __restrict__ Lg, doub
     }
   }
   __syncthreads();
+  if (tr) trace[44] = clock64();
   chol_epilogue(m, fb, Linv, mode, status, red);
+  if (tr) trace[45] = clock64();
 }
 
 size_t chol_wsync_smem(int m) {
@@ -2457,7 +2506,22 @@ void launch_chol(const double* B, int m, double* L, double* Linv, int mode, Smal
   static const int cfix = getenv("SPB_CHOL_CLUSTER_C") ? atoi(getenv("SPB_CHOL_CLUSTER_C")) : 0;
   static const bool unblocked = getenv("SPB_CHOL_LDL") != nullptr;  // A/B switch
   if (!old && !unblocked && m < cmin && m <= kCholLdlMax && chol_wsync_smem(m) <= 217 * 1024) {
-    chol_wsync<<<1, CWT, chol_wsync_smem(m), st>>>(B, m, L, Linv, mode, status);
+    // SPB_CHOL_TRACE=<file>: clock64 phase stamps appended to <file> (diagnostics)
+    static const char* tf = getenv("SPB_CHOL_TRACE");
+    static long long* tbuf = nullptr;
+    if (tf && !tbuf) cudaMalloc(&tbuf, sizeof(long long) * 48);
+    chol_wsync<<<1, CWT, chol_wsync_smem(m), st>>>(B, m, L, Linv, mode, status, tf ? tbuf : nullptr);
+    if (tf) {
+      long long h[48];
+      cudaMemcpyAsync(h, tbuf, sizeof(h), cudaMemcpyDeviceToHost, st);
+      cudaStreamSynchronize(st);
+      if (FILE* f = fopen(tf, "a")) {
+        fprintf(f, "m %d\n", m);
+        for (int j = 0; j < 46; ++j) fprintf(f, "%lld ", h[j]);
+        fprintf(f, "\n");
+        fclose(f);
+      }
+    }
   } else if (!old && m < cmin && m <= kCholLdlMax && chol_ldl_smem(m) <= 224 * 1024) {
     chol_ldl<<<1, ET, chol_ldl_smem(m), st>>>(B, m, L, Linv, mode, status);
   } else if (!old && m <= kCholClusterMax) {

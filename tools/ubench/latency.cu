@@ -59,6 +59,48 @@ __global__ void k_cluster(int iters, long long* out) {
   if (threadIdx.x == 0 && r == 0) out[0] = (t1 - t0) / iters;
 }
 
+
+__device__ __forceinline__ void tri_index(int t, int* ti, int* tq) {
+  int r = (int)((sqrtf(8.0f * (float)t + 1.0f) - 1.0f) * 0.5f);
+  while ((r + 1) * (r + 2) / 2 <= t) ++r;
+  while (r * (r + 1) / 2 > t) --r;
+  *ti = r;
+  *tq = t - r * (r + 1) / 2;
+}
+
+// The Cholesky P1 column step (chol_wsync): pivot read, reciprocal, one
+// trailing-triangle element per thread, CTA barrier. variant 0: as written;
+// 1: tri_index hoisted; 2: hoisted + no division (reciprocal precomputed)
+__global__ void k_p1(int reps, int variant, long long* out) {
+  extern __shared__ double A[];
+  __shared__ double dinv[32];
+  const int ld = 147, tid = threadIdx.x;
+  for (int x = tid; x < 147 * 147; x += blockDim.x) A[x] = (x % 148 == 0) ? 100.0 : 0.01;
+  __syncthreads();
+  int hti, htq;
+  tri_index(tid, &hti, &htq);
+  long long t0 = clock64();
+  for (int r = 0; r < reps; ++r) {
+    const int kb = 32 * (r % 4);
+    for (int c = 0; c < 32; ++c) {
+      const double dc = A[(kb + c) * ld + kb + c];
+      const double rc = variant == 2 ? 0.01 : 1.0 / dc;
+      const int rem = 31 - c;
+      if (tid < rem * (rem + 1) / 2) {
+        int ti, tq;
+        if (variant == 0) tri_index(tid, &ti, &tq);
+        else { ti = hti; tq = htq; }
+        const int i = kb + c + 1 + ti, q = kb + c + 1 + tq;
+        A[i * ld + q] = fma(-A[i * ld + kb + c] * rc, A[q * ld + kb + c], A[i * ld + q]);
+      }
+      if (tid == 0) dinv[c] = rc;
+      __syncthreads();
+    }
+  }
+  long long t1 = clock64();
+  if (tid == 0) out[0] = (t1 - t0) / (reps * 32);
+}
+
 int main() {
   long long* d;
   double* sink;
@@ -79,6 +121,15 @@ int main() {
   for (int nt : {32, 1024}) {
     k_smem_chain<<<1, nt>>>(10000, d); cudaMemcpy(&h, d, 8, cudaMemcpyDeviceToHost);
     printf("smem load->fma->store chain (%d thr): %lld cycles\n", nt, h);
+  }
+  cudaFuncSetAttribute(k_p1, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+  for (int v : {0, 1, 2}) {
+    for (int nt : {512, 1024}) {
+      k_p1<<<1, nt, 147 * 147 * 8>>>(100, v, d);
+      cudaError_t e = cudaDeviceSynchronize();
+      cudaMemcpy(&h, d, 8, cudaMemcpyDeviceToHost);
+      printf("chol P1 column step variant %d, %d thr: %lld cycles (%s)\n", v, nt, h, cudaGetErrorString(e));
+    }
   }
   for (int C : {2, 4, 8, 16}) {
     cudaFuncSetAttribute(k_cluster, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
