@@ -87,6 +87,23 @@ __global__ void sym_prep(const double* __restrict__ ga, const double* __restrict
 constexpr int CB = 32;
 
 // ||L^-1||_F and the cond2 bracket (mode 0), or Rinv = (L^-1)' in place (mode 1).
+// chol_epilogue with ||L^-1||_F^2 partials already accumulated by the caller
+// and L^-1 already written in the mode's orientation.
+__device__ void chol_epilogue_fl(int m, double fb, double fl, int mode, SmallStatus* status,
+                                 double* red) {
+  const int tid = threadIdx.x;
+  fl = block_sum(fl, red);
+  if (mode == 0 && tid == 0) {
+    const double upper = sqrt(fb) * fl;
+    const double lower = upper / (m * sqrt((double)m));
+    status->fro_b = sqrt(fb);
+    status->fro_linv = sqrt(fl);
+    status->cond_hi = upper;
+    status->cond_lo = lower;
+    status->cond_state = upper <= kCondMax ? 0 : (lower > kCondMax ? 1 : 2);
+  }
+}
+
 __device__ void chol_epilogue(int m, double fb, double* __restrict__ Linv, int mode,
                               SmallStatus* status, double* red) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -718,24 +735,31 @@ chol_wsync(const double* __restrict__ Bsrc, int m, double* __restrict__ Lg, doub
     __syncthreads();
   }
   if (tr) trace[43] = clock64();
+  // L = L' D^1/2 and L^-1 (mode 1: its transpose, the R^-1 of the QR view),
+  // row-major coalesced stores; ||L^-1||_F^2 accumulated on the way
+  double* sq = S;  // sqrt(d_j) (S is free after the block rows)
+  for (int j = tid; j < m; j += CWT) sq[j] = 1.0 / dinv[j];
+  __syncthreads();
+  double fl = 0.0;
   for (int i = warp; i < m; i += CWT / 32) {
     const double ri = dinv[i];
     for (int j = lane; j < m; j += 32) {
-      double l = 0.0, v = 0.0;
-      if (j < i) {
-        l = A[i * ld + j] / dinv[j];
-        v = A[j * ld + i] * ri;
-      } else if (j == i) {
-        l = 1.0 / ri;
-        v = ri;
-      }
+      const double l = j < i ? A[i * ld + j] * sq[j] : (j == i ? sq[i] : 0.0);
       Lg[(int64_t)i * m + j] = l;
-      Linv[(int64_t)i * m + j] = v;
+      if (mode == 0) {
+        const double v = j < i ? A[j * ld + i] * ri : (j == i ? ri : 0.0);
+        Linv[(int64_t)i * m + j] = v;
+        fl = fma(v, v, fl);
+      } else {
+        // row i of (L^-1)' = column i of L^-1: element (i, j) = L^-1[j][i], j >= i
+        const double v = j > i ? A[i * ld + j] * dinv[j] : (j == i ? ri : 0.0);
+        Linv[(int64_t)i * m + j] = v;
+        fl = fma(v, v, fl);
+      }
     }
   }
-  __syncthreads();
   if (tr) trace[44] = clock64();
-  chol_epilogue(m, fb, Linv, mode, status, red);
+  chol_epilogue_fl(m, fb, fl, mode, status, red);
   if (tr) trace[45] = clock64();
 }
 
