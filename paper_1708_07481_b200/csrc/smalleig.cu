@@ -1123,6 +1123,42 @@ __device__ __forceinline__ void mb_wait(uint64_t* bar, uint32_t parity) {
       "r"(parity)
       : "memory");
 }
+// Bulk copy of `bytes` (multiple of 16, 16-byte aligned) from this CTA's shared memory
+// into the same offset of `local_dst` in CTA `rank`, completing on its mbarrier.
+__device__ __forceinline__ void bulk_s2cluster(double* local_dst, const double* src, uint32_t bytes,
+                                               uint64_t* local_bar, int rank) {
+  uint32_t ra, rb;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;\n" : "=r"(ra) : "r"(sm_u32(local_dst)), "r"(rank));
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;\n" : "=r"(rb) : "r"(sm_u32(local_bar)), "r"(rank));
+  asm volatile(
+      "cp.async.bulk.shared::cluster.shared::cta.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(ra),
+      "r"(sm_u32(src)), "r"(bytes), "r"(rb)
+      : "memory");
+}
+
+// mb_wait with a spin bound: a protocol error reports and traps instead of hanging the GPU.
+__device__ __forceinline__ bool mb_try(uint64_t* bar, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n\t.reg .pred P;\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P, [%1], %2;\n\t"
+      "selp.u32 %0, 1, 0, P;\n}"
+      : "=r"(ok)
+      : "r"(sm_u32(bar)), "r"(parity)
+      : "memory");
+  return ok != 0;
+}
+__device__ __noinline__ void mb_stuck(int tag, int k) {
+  unsigned r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;\n" : "=r"(r));
+  printf("spb: mbarrier wait stuck (tag %d step %d cta %u warp %d)\n", tag, k, r,
+         (int)(threadIdx.x >> 5));
+  __trap();
+}
+__device__ __forceinline__ void mb_wait_bounded(uint64_t* bar, uint32_t parity, int tag, int k) {
+  for (uint32_t spin = 0; !mb_try(bar, parity); ++spin)
+    if (spin == (1u << 20)) mb_stuck(tag, k);
+}
 __device__ __forceinline__ void st_async_f64(double* local_addr, uint64_t* local_bar, int rank,
                                              double v) {
   uint32_t ra, rb;
@@ -1650,6 +1686,343 @@ chol_finish(const double* __restrict__ Bsrc, int m, const double* __restrict__ L
   chol_epilogue(m, fb, Linv, mode, status, red);
 }
 
+// Lane-group-per-column tridiagonalisation (default for kTriClusterMin <= m <= 320).
+// The columns are split over a cluster of C CTAs; a group of LPC lanes owns one
+// column i and keeps ALL its rows in registers (lane g of the group holds rows
+// g + LPC t), so the matvec p_i = tau W(:,i)'v and the rank-2 update of column i
+// are register FMAs plus an LPC-lane reduction -- no shared-memory sweep of the
+// matrix and no CTA barrier per step. Per step k every participating group
+//   (1) waits for row k (all-gathered by st.async into every consumer CTA), completes
+//       it with the previous step's 2K v v' term (its own v_j), and forms reflector k
+//       redundantly (same inputs and order => the same v, tau everywhere) together with
+//       p_i = ((beta - alpha) W_{k+1,i} - sum_{j>k+1} W_ji x_j) / beta: one rsqrt on
+//       the path from the row's arrival to the push of p_i,
+//   (2) pushes p_i into every consumer CTA's p buffer,
+//   (3) waits for p_k, applies W -= v p' + p v' to column i, pushes its element of
+//       row k+1 (without the 2K v v' term, which every receiver adds itself) and then
+//       applies the 2K v v' term (K = tau/2 p'v) to its column.
+// A column leaves after step i-1. A controller warp per CTA arms the expected byte
+// counts of the double-buffered row / p mbarriers. WAR safety of the parity buffers
+// follows from the data dependencies: data of step k+2 can only be produced after
+// every consumer finished reading step k's buffers (its contribution to row k+1 or
+// p_{k+1} is issued after those reads).
+constexpr int kWcWarps = 19;  // column warps per CTA (upper bound; + 1 controller warp)
+constexpr int kWcThreads = 32 * (kWcWarps + 1);
+
+template <int R, int LPC, bool BULK>
+__global__ void __launch_bounds__(kWcThreads)
+tridiag_warpcol(const double* __restrict__ Asrc, int m, int symmetrize, double* __restrict__ V,
+                double* __restrict__ tau, double* __restrict__ d, double* __restrict__ e,
+                const SmallStatus* status, long long* trace) {
+  if (status && (status->nonfinite || status->not_pd)) return;  // uniform over the cluster
+  constexpr int G = 32 / LPC;  // columns per warp
+  unsigned rank_u, csize_u;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;\n" : "=r"(rank_u));
+  asm volatile("mov.u32 %0, %%cluster_nctarank;\n" : "=r"(csize_u));
+  const int rank = (int)rank_u, C = (int)csize_u;
+  // BULK: each exchange is gathered in a local stage and sent as one bulk copy per
+  // consumer CTA (16-byte aligned chunks: nc even) instead of one st.async per value
+  const int nc = BULK ? (((m + C - 1) / C + 1) & ~1) : (m + C - 1) / C;
+  const int Mp = BULK ? C * nc : m;          // exchange buffer stride
+  const int nne = (m + nc - 1) / nc;         // CTAs holding columns
+  const int c0 = rank * nc;
+  const int ncl = max(0, min(m, c0 + nc) - c0);
+  const int cmax = ncl > 0 ? c0 + ncl - 1 : -1;  // last column held by this CTA (-1: none)
+  const int nw = (nc + G - 1) / G;                 // column warps per CTA
+  extern __shared__ __align__(16) double wsm[];
+  double* rowb = wsm;           // [2][Mp] rows k (parity k & 1), entries k..m-1
+  double* pbuf = wsm + 2 * Mp;  // [2][Mp] p_k, entries k+1..m-1
+  double* stR = wsm + 4 * Mp;   // BULK: [2][nc] local slice of the next row
+  double* stP = stR + 2 * nc;   // BULK: [2][nc] local slice of p
+  __shared__ __align__(8) uint64_t mbR[2], mbP[2];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int gl = lane % LPC, q = lane / LPC, gb = q * LPC;  // lane in group, group, base lane
+  const unsigned full = 0xffffffffu;
+  // last column of CTA r: consumers of step-k data are the CTAs with a column > k
+#define cmax_of(r) ((r) * nc < m ? min(m, ((r) + 1) * nc) - 1 : -1)
+  // bytes of row r / p_k landing in a consumer (BULK: whole slices of the senders)
+#define RBYTES(r) (BULK ? 8u * (uint32_t)(nc * (nne - (r) / nc)) : 8u * (uint32_t)(m - (r)))
+#define PBYTES(k) (BULK ? 8u * (uint32_t)(nc * (nne - ((k) + 1) / nc)) : 8u * (uint32_t)(m - (k) - 1))
+  if (threadIdx.x == 0) {
+    mb_init(&mbR[0], 1);
+    mb_init(&mbR[1], 1);
+    mb_init(&mbP[0], 1);
+    mb_init(&mbP[1], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  cluster_sync_all();
+  if (warp == nw) {
+    // controller: arm row r (8(m-r) bytes) and p_k (8(m-k-1) bytes) phases in order
+    if (lane == 0 && cmax >= 0) {
+      if (cmax > 0) mb_expect(&mbR[0], RBYTES(0));
+      if (cmax > 1) mb_expect(&mbR[1], RBYTES(1));
+      if (cmax > 0) mb_expect(&mbP[0], PBYTES(0));
+      if (cmax > 1 && m >= 4) mb_expect(&mbP[1], PBYTES(1));
+      for (int k = 0; k + 2 < m && cmax > k; ++k) {
+        const int b = k & 1;
+        const uint32_t par = (uint32_t)((k >> 1) & 1);
+        mb_wait_bounded(&mbR[b], par, 1, k);
+        if (k + 2 <= m - 2 && cmax > k + 2) mb_expect(&mbR[b], RBYTES(k + 2));
+        mb_wait_bounded(&mbP[b], par, 2, k);
+        if (k + 2 <= m - 3 && cmax > k + 2) mb_expect(&mbP[b], PBYTES(k + 2));
+      }
+    }
+  } else if (warp < nw) {
+    const int lc = warp * G + q;  // local column of this lane group
+    const bool valid = lc < ncl;
+    const int i = c0 + lc;
+    const int kend = valid ? min(i - 1, m - 3) : -1;  // last step this column takes part in
+    // the warp runs until its last valid column is done (shuffles need every lane)
+    const int lcw = min(warp * G + G, ncl) - 1;
+    const int kwarp = warp * G < ncl ? min(c0 + lcw - 1, m - 3) : -1;
+    double w[R];  // column i, rows gl + LPC t
+    double v[R];  // reflector of the previous step on the same rows (0 before step 0)
+    double Kp = 0.0;  // K of the previous step
+#pragma unroll
+    for (int t = 0; t < R; ++t) {
+      const int j = gl + LPC * t;
+      double a = 0.0;
+      if (valid && j < m) {
+        a = Asrc[(int64_t)j * m + i];
+        if (symmetrize) a = 0.5 * (a + Asrc[(int64_t)i * m + j]);
+      }
+      w[t] = a;
+      v[t] = 0.0;
+    }
+    if (valid) {
+      for (int k = max(kend + 1, 0) + gl; k < m; k += LPC) V[(int64_t)k * m + i] = 0.0;
+      const double r0 = __shfl_sync(full, w[0], gb);
+      if (BULK) {
+        if (lane == 0) stR[lc] = r0;
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        asm volatile("bar.sync 2, %0;" ::"r"(32 * ncl) : "memory");
+        if (lc == ncl - 1 && lane < C && cmax_of(lane) > 0)
+          bulk_s2cluster(rowb + c0, stR, 8u * nc, &mbR[0], lane);
+      } else {
+        for (int r = gl; r < C; r += LPC)
+          if (cmax_of(r) > 0) st_async_f64(rowb + i, &mbR[0], r, r0);
+      }
+    } else {
+      __shfl_sync(full, 0.0, gb);
+    }
+    const bool tr = trace && i == m - 1 && gl == 0;
+#define SPB_TS(qq) \
+  if (tr) trace[k * 8 + (qq)] = clock64();
+    for (int k = 0; k <= kwarp; ++k) {
+      const bool act = k <= kend;
+      const int b = k & 1;
+      const uint32_t par = (uint32_t)((k >> 1) & 1);
+      SPB_TS(0)
+      mb_wait_bounded(&mbR[b], par, 3, k);
+      SPB_TS(1)
+      const double* row = rowb + b * Mp;
+      const double twoK = 2.0 * Kp;
+      double ss = 0.0, s2 = 0.0, cal = 0.0, s1 = 0.0, cii = 0.0;
+      // BULK: column warps still in the loop at step k (columns > k), the last one sends
+      const int nact = ncl - max(0, min(ncl, k + 1 - c0));
+#pragma unroll
+      for (int t = 0; t < R; ++t) {
+        const int j = gl + LPC * t;
+        const double c = (j >= k && j < m) ? fma(twoK, v[t], row[j]) : 0.0;
+        if (j == k + 1) {
+          cal = c;
+          s1 = w[t];
+        }
+        if (j == i) cii = c;
+        if (j == k && i == k + 1) d[k] = c;
+        const double x = j >= k + 2 ? c : 0.0;
+        v[t] = x;
+        ss = fma(x, x, ss);
+        s2 = fma(w[t], x, s2);
+      }
+#pragma unroll
+      for (int o = LPC / 2; o > 0; o >>= 1) {
+        ss += __shfl_xor_sync(full, ss, o);
+        s2 += __shfl_xor_sync(full, s2, o);
+      }
+      const double alpha = __shfl_sync(full, cal, gb + (k + 1) % LPC);
+      s1 = __shfl_sync(full, s1, gb + (k + 1) % LPC);
+      cii = __shfl_sync(full, cii, gb + (valid ? i % LPC : 0));
+      SPB_TS(5)
+      double beta = alpha, rbeta = 0.0, pi = 0.0;
+      if (ss != 0.0) {
+        const double a2 = fma(alpha, alpha, ss);
+        const double r = rsqrt(a2);
+        beta = -copysign(a2 * r, alpha);
+        rbeta = -copysign(r, alpha);  // 1 / beta
+        pi = fma(beta - alpha, s1, -s2) * rbeta;
+      }
+      SPB_TS(6)
+      if (BULK) {
+        if (lane == 0) stP[b * nc + lc] = pi;
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        asm volatile("bar.sync 1, %0;" ::"r"(32 * nact) : "memory");
+        if (lc == ncl - 1 && lane < C && cmax_of(lane) > k)
+          bulk_s2cluster(pbuf + b * Mp + c0, stP + b * nc, 8u * nc, &mbP[b], lane);
+      } else if (act) {
+        for (int r = gl; r < C; r += LPC)
+          if (cmax_of(r) > k) st_async_f64(pbuf + b * m + i, &mbP[b], r, pi);
+      }
+      SPB_TS(2)
+      double tk = 0.0, scale = 0.0;
+      if (ss != 0.0) {
+        tk = (beta - alpha) * rbeta;
+        scale = 1.0 / (alpha - beta);
+      }
+      const double vi = i == k + 1 ? 1.0 : cii * scale;
+      if (act && gl == 0) {
+        V[(int64_t)k * m + i] = vi;
+        if (i == k + 1) {
+          e[k] = beta;
+          tau[k] = tk;
+        }
+      }
+#pragma unroll
+      for (int t = 0; t < R; ++t) {
+        const int j = gl + LPC * t;
+        v[t] = j == k + 1 ? 1.0 : v[t] * scale;
+      }
+      mb_wait_bounded(&mbP[b], par, 4, k);
+      SPB_TS(3)
+      const double* pb = pbuf + b * Mp;
+      double nxt = 0.0, dot = 0.0;
+#pragma unroll
+      for (int t = 0; t < R; ++t) {
+        const int j = gl + LPC * t;
+        if (j > k && j < m) {
+          const double pj = pb[j];
+          w[t] = fma(-v[t], pi, fma(-pj, vi, w[t]));
+          dot = fma(pj, v[t], dot);
+        }
+        if (j == k + 1) nxt = w[t];
+      }
+      nxt = __shfl_sync(full, nxt, gb + (k + 1) % LPC);
+      const int b1 = (k + 1) & 1;
+      if (BULK) {
+        if (lane == 0) stR[b1 * nc + lc] = nxt;
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        asm volatile("bar.sync 2, %0;" ::"r"(32 * nact) : "memory");
+        if (lc == ncl - 1 && lane < C && cmax_of(lane) > k + 1)
+          bulk_s2cluster(rowb + b1 * Mp + c0, stR + b1 * nc, 8u * nc, &mbR[b1], lane);
+      } else if (act) {
+        for (int r = gl; r < C; r += LPC)
+          if (cmax_of(r) > k + 1) st_async_f64(rowb + b1 * m + i, &mbR[b1], r, nxt);
+      }
+      SPB_TS(4)
+#pragma unroll
+      for (int o = LPC / 2; o > 0; o >>= 1) dot += __shfl_xor_sync(full, dot, o);
+      Kp = 0.5 * tk * dot;
+      const double kv = 2.0 * Kp * vi;
+#pragma unroll
+      for (int t = 0; t < R; ++t) {
+        const int j = gl + LPC * t;
+        if (j > k && j < m) w[t] = fma(kv, v[t], w[t]);
+      }
+    }
+    if (warp * G < ncl && c0 + lcw == m - 1) {
+      // rows m-2, m-1 need no reflector: d, e from row m-2 (completed) and the last diagonal
+      const int kk = m - 2;
+      mb_wait_bounded(&mbR[kk & 1], (uint32_t)((kk >> 1) & 1), 5, kk);
+      if (i == m - 1) {
+        const double* row = rowb + (kk & 1) * Mp;
+        const double twoK = 2.0 * Kp;
+#pragma unroll
+        for (int t = 0; t < R; ++t) {
+          const int j = gl + LPC * t;
+          if (j == m - 2) d[m - 2] = fma(twoK, v[t], row[j]);
+          if (j == m - 1) {
+            e[m - 2] = fma(twoK, v[t], row[j]);
+            d[m - 1] = w[t];
+          }
+        }
+        if (gl == 0) {
+          tau[m - 2] = 0.0;
+          tau[m - 1] = 0.0;
+          e[m - 1] = 0.0;
+        }
+      }
+    }
+  }
+  cluster_sync_all();  // no CTA leaves while a peer may still address its shared memory
+#undef SPB_TS
+#undef cmax_of
+#undef RBYTES
+#undef PBYTES
+}
+
+struct WcShape {
+  int C, lpc;
+};
+
+WcShape tridiag_warpcol_shape(int m) {
+  // one warp per column (lane groups of 8 / 16 per column were measured slower: the
+  // per-lane row loops become issue-bound); by default the widest cluster, so each SM
+  // runs as few column warps as possible (SPB_WC_C overrides for measurements)
+  if (m < kTriClusterMin || m > 256) return {0, 0};
+  static const int env_c = getenv("SPB_WC_C") ? atoi(getenv("SPB_WC_C")) : 16;
+  const int C = env_c == 2 || env_c == 4 || env_c == 8 ? env_c : 16;
+  if ((m + C - 1) / C > kWcWarps) return {0, 0};
+  return {C, 32};
+}
+
+int tridiag_warpcol_cluster(int m) { return tridiag_warpcol_shape(m).C; }
+
+bool launch_tridiag_warpcol(const double* Asrc, int m, int symmetrize, double* V, double* tau,
+                            double* d, double* e, const SmallStatus* status, cudaStream_t st,
+                            long long* trace) {
+  const WcShape sh = tridiag_warpcol_shape(m);
+  if (!sh.C) return false;
+  const int C = sh.C, lpc = sh.lpc;
+  // SPB_WC_BULK=1: slices gathered per CTA and sent by bulk copies (measured slower: the
+  // two named barriers per step cost more than the per-value st.async they replace)
+  static const bool bulk = getenv("SPB_WC_BULK") ? atoi(getenv("SPB_WC_BULK")) != 0 : false;
+  const int nc = bulk ? (((m + C - 1) / C + 1) & ~1) : (m + C - 1) / C;
+  if (nc > kWcWarps) return false;
+  const int nw = (nc + 32 / lpc - 1) / (32 / lpc);
+  const int Mp = bulk ? C * nc : m;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(C);
+  cfg.blockDim = dim3(32 * (nw + 1));
+  cfg.dynamicSmemBytes = sizeof(double) * (4 * (size_t)Mp + 4 * (size_t)nc);
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = C;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  const int R = (m + lpc - 1) / lpc;
+#define SPB_WC1(RR, LL, BB)                                                                    \
+  {                                                                                            \
+    static bool attr = false;                                                                  \
+    if (!attr) {                                                                               \
+      cudaFuncSetAttribute(tridiag_warpcol<RR, LL, BB>,                                        \
+                           cudaFuncAttributeNonPortableClusterSizeAllowed, 1);                 \
+      attr = true;                                                                             \
+    }                                                                                          \
+    cudaLaunchKernelEx(&cfg, tridiag_warpcol<RR, LL, BB>, Asrc, m, symmetrize, V, tau, d, e,   \
+                       status, trace);                                                         \
+    return true;                                                                               \
+  }
+#define SPB_WC(RR, LL) \
+  {                    \
+    if (bulk)          \
+      SPB_WC1(RR, LL, true) \
+    else               \
+      SPB_WC1(RR, LL, false) \
+  }
+  if (R <= 2) SPB_WC(2, 32)
+  if (R <= 3) SPB_WC(3, 32)
+  if (R <= 4) SPB_WC(4, 32)
+  if (R <= 5) SPB_WC(5, 32)
+  if (R <= 6) SPB_WC(6, 32)
+  if (R <= 8) SPB_WC(8, 32)
+#undef SPB_WC
+#undef SPB_WC1
+  return false;
+}
+
 size_t chol_cluster_smem(int m, int C) {
   const int nc = (m + C - 1) / C;
   return sizeof(double) * ((size_t)m * nc + 2 * (size_t)m);
@@ -1697,10 +2070,35 @@ void launch_tridiag(const double* Asrc, int m, int symmetrize, double* Wg, doubl
     at[0].val.clusterDim.z = 1;
     cfg.attrs = at;
     cfg.numAttrs = 1;
-    static const int variant = getenv("SPB_TRI_VARIANT") ? atoi(getenv("SPB_TRI_VARIANT")) : 1;
+    static const int variant = getenv("SPB_TRI_VARIANT") ? atoi(getenv("SPB_TRI_VARIANT")) : 3;
+    if (variant == 3) {
+      // SPB_TRI_TRACE=<file>: per-step clock64 stamps of the last column's warp (diagnostics)
+      static const char* tf = getenv("SPB_TRI_TRACE");
+      static long long* tbuf = nullptr;
+      if (tf && !tbuf) cudaMalloc(&tbuf, sizeof(long long) * 8 * 4096);
+      long long* trace = (tf && m <= 4096) ? tbuf : nullptr;
+      if (launch_tridiag_warpcol(Asrc, m, symmetrize, V, tau, d, e, status, st, trace)) {
+        if (trace) {
+          std::vector<long long> h((size_t)8 * m);
+          cudaMemcpyAsync(h.data(), trace, sizeof(long long) * 8 * m, cudaMemcpyDeviceToHost, st);
+          cudaStreamSynchronize(st);
+          if (FILE* f = fopen(tf, "a")) {
+            fprintf(f, "m %d C %d lpc %d warpcol\n", m, tridiag_warpcol_shape(m).C, tridiag_warpcol_shape(m).lpc);
+            for (int k = 0; k + 2 < m; ++k) {
+              for (int j = 0; j < 7; ++j) fprintf(f, "%lld ", h[(size_t)k * 8 + j]);
+              fprintf(f, "\n");
+            }
+            fclose(f);
+          }
+        }
+        return;
+      }
+    }
     if (variant == 0)
       cudaLaunchKernelEx(&cfg, tridiag_cluster, Asrc, m, symmetrize, V, tau, d, e, status);
-    else if (variant == 1)
+    else if (variant == 2)
+      cudaLaunchKernelEx(&cfg, tridiag_fused, Asrc, m, symmetrize, V, tau, d, e, status);
+    else  // variant 1, and 3 where the warp-per-column kernel does not apply
     {
       // SPB_TRI_TRACE=<file>: per-step clock64 phase stamps of the last CTA's
       // thread 0 appended to <file> (diagnostics only; synchronises the stream)
@@ -1723,8 +2121,6 @@ void launch_tridiag(const double* Asrc, int m, int symmetrize, double* Wg, doubl
         }
       }
     }
-    else
-      cudaLaunchKernelEx(&cfg, tridiag_fused, Asrc, m, symmetrize, V, tau, d, e, status);
     return;
   }
   const int rows = (m + 31) / 32;
@@ -1842,22 +2238,34 @@ __device__ __forceinline__ int sturm_count(const double* sd, const double* se2, 
     // division-free three-term recurrence p_i = (d_i - x) p_{i-1} - e_{i-1}^2 p_{i-2},
     // exact power-of-two rescaling; a pivot p_i / p_{i-1} below pivmin in magnitude
     // is taken as -pivmin, as in the ratio form
+    // the range check runs once per 8 steps, off the recurrence's dependency chain
+    // (8 steps move |p| by far less than the 2^500 margin to over/underflow)
     double p0 = 1.0, p1 = sd[0] - x;
     if (fabs(p1) < pivmin) p1 = -pivmin;
     c = p1 < 0.0;
-#pragma unroll 8
-    for (int i = 1; i < m; ++i) {
-      double p2 = fma(sd[i] - x, p1, -se2[i - 1] * p0);
-      if (fabs(p2) < pivmin * fabs(p1)) p2 = -pivmin * p1;
-      c += (p2 < 0.0) != (p1 < 0.0);
-      p0 = p1;
-      p1 = p2;
+    int i = 1;
+    for (; i + 8 <= m; i += 8) {
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        double p2 = fma(sd[i + u] - x, p1, -se2[i + u - 1] * p0);
+        p2 = fabs(p2) < pivmin * fabs(p1) ? -pivmin * p1 : p2;
+        c += (p2 < 0.0) != (p1 < 0.0);
+        p0 = p1;
+        p1 = p2;
+      }
       if (fabs(p1) > 0x1p500 || fabs(p1) < 0x1p-500) {
         int ex;
         frexp(p1, &ex);
         p1 = ldexp(p1, -ex);
         p0 = ldexp(p0, -ex);
       }
+    }
+    for (; i < m; ++i) {
+      double p2 = fma(sd[i] - x, p1, -se2[i - 1] * p0);
+      p2 = fabs(p2) < pivmin * fabs(p1) ? -pivmin * p1 : p2;
+      c += (p2 < 0.0) != (p1 < 0.0);
+      p0 = p1;
+      p1 = p2;
     }
   } else {
     double q = sd[0] - x;

@@ -24,7 +24,7 @@ def _spd_pair(m, seed, cond_b=10.0):
     return a, b
 
 
-@pytest.mark.parametrize("m", [1, 2, 3, 7, 21, 47, 63, 147, 164, 165, 170, 324, 401, 528])
+@pytest.mark.parametrize("m", [1, 2, 3, 7, 21, 47, 48, 63, 100, 147, 164, 165, 170, 256, 257, 324, 401, 528])
 def test_sygv_matches_lapack(spb, m):
     from paper_1708_07481_b200.lobpcg import _solve_small
 
