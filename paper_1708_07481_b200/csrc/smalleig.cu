@@ -804,6 +804,90 @@ small_gemm(int ta, int tb, int M, int N, int K, const double* __restrict__ A, in
   }
 }
 
+// Same product with the whole K extent of the 32-row A panel and the 32-column B
+// panel staged in shared memory by one batch of independent loads (8 in flight per
+// thread), then one barrier: the tiled loop above pays a global round trip per
+// 32-deep tile, which dominated at the projected sizes (m <= 390).
+__global__ void __launch_bounds__(256)
+small_gemm_fk(int ta, int tb, int M, int N, int K, const double* __restrict__ A, int lda,
+              const double* __restrict__ B, int ldb, double* __restrict__ C, int ldc) {
+  extern __shared__ double gsm[];
+  const int KP = K | 1;  // odd row stride: conflict-free column walks
+  double* As = gsm;            // As[r * KP + k] = A(i0 + r, k)
+  double* Bs = gsm + 32 * KP;  // Bs[c * KP + k] = B(k, j0 + c)
+  const int tid = threadIdx.x;
+  const int i0 = blockIdx.y * 32, j0 = blockIdx.x * 32;
+  const int total = 32 * K;
+  for (int e0 = tid; e0 < total; e0 += 256 * 8) {
+    double va[8], vb[8];
+    int ra[8], ka[8], rb[8], kb[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int e = e0 + u * 256;
+      // element order follows the contiguous direction of each operand (coalesced)
+      int r, k;
+      if (ta) { k = e >> 5; r = e & 31; } else { r = e / K; k = e - r * K; }
+      int c, k2;
+      if (tb) { c = e / K; k2 = e - c * K; } else { k2 = e >> 5; c = e & 31; }
+      ra[u] = r; ka[u] = k; rb[u] = c; kb[u] = k2;
+      double a = 0.0, b = 0.0;
+      if (e < total) {
+        const int gi = i0 + r, gj = j0 + c;
+        if (gi < M) a = ta ? A[(int64_t)k * lda + gi] : A[(int64_t)gi * lda + k];
+        if (gj < N) b = tb ? B[(int64_t)gj * ldb + k2] : B[(int64_t)k2 * ldb + gj];
+      }
+      va[u] = a;
+      vb[u] = b;
+    }
+#pragma unroll
+    for (int u = 0; u < 8; ++u)
+      if (e0 + u * 256 < total) {
+        As[ra[u] * KP + ka[u]] = va[u];
+        Bs[rb[u] * KP + kb[u]] = vb[u];
+      }
+  }
+  __syncthreads();
+  const int tx = tid & 31, ty = tid >> 5;
+  double acc[4][2] = {{0, 0}, {0, 0}, {0, 0}, {0, 0}};
+  const double* bp = Bs + tx * KP;
+  const double* ap = As + ty * 4 * KP;
+  int k = 0;
+#pragma unroll 4
+  for (; k + 1 < K; k += 2) {
+    const double b0 = bp[k], b1 = bp[k + 1];
+#pragma unroll
+    for (int a = 0; a < 4; ++a) {
+      acc[a][0] = fma(ap[a * KP + k], b0, acc[a][0]);
+      acc[a][1] = fma(ap[a * KP + k + 1], b1, acc[a][1]);
+    }
+  }
+  if (k < K)
+#pragma unroll
+    for (int a = 0; a < 4; ++a) acc[a][0] = fma(ap[a * KP + k], bp[k], acc[a][0]);
+#pragma unroll
+  for (int a = 0; a < 4; ++a) {
+    const int gi = i0 + ty * 4 + a, gj = j0 + tx;
+    if (gi < M && gj < N) C[(int64_t)gi * ldc + gj] = acc[a][0] + acc[a][1];
+  }
+}
+
+void launch_small_gemm(int ta, int tb, int M, int N, int K, const double* A, int lda,
+                       const double* B, int ldb, double* C, int ldc, cudaStream_t st) {
+  dim3 grid((unsigned)((N + 31) / 32), (unsigned)((M + 31) / 32));
+  const size_t smem = sizeof(double) * 64 * (size_t)(K | 1);
+  static const int tiled = getenv("SPB_SMALL_GEMM_TILED") ? atoi(getenv("SPB_SMALL_GEMM_TILED")) : 0;
+  if (!((tiled >> (ta * 2 + tb)) & 1) && smem <= 200 * 1024) {
+    static bool attr = false;
+    if (!attr) {
+      cudaFuncSetAttribute(small_gemm_fk, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+      attr = true;
+    }
+    small_gemm_fk<<<grid, 256, smem, st>>>(ta, tb, M, N, K, A, lda, B, ldb, C, ldc);
+  } else {
+    small_gemm<<<grid, 256, 0, st>>>(ta, tb, M, N, K, A, lda, B, ldb, C, ldc);
+  }
+}
+
 // Householder tridiagonalisation of the symmetric part of Asrc (m x m).
 // V row k holds v_k (v_k[k+1] = 1, zeros before), tau[k]; d, e diagonals.
 // Three CTA barriers per step: (1) warp 0 forms the reflector of row k;
@@ -2526,8 +2610,8 @@ __global__ void invit(const double* __restrict__ d_g, const double* __restrict__
 // wy_apply: the columns of Y are independent, so each CTA owns BCW of them in
 // shared memory and runs the block loop W1 = V_b' Y, W2 = T_b W1, Y -= V_b W2
 // with V_b staged per block.
-constexpr int BCW = 8;     // Y columns per CTA
-constexpr int BAT = 256;   // threads of wy_apply (= 32 reflectors x BCW columns)
+constexpr int BCW = 4;     // Y columns per CTA
+constexpr int BAT = 32 * BCW;  // threads of wy_apply (= 32 reflectors x BCW columns)
 
 __global__ void __launch_bounds__(256)
 wy_tfactors(const double* __restrict__ V, const double* __restrict__ tau, int m,
@@ -2605,11 +2689,31 @@ wy_apply(const double* __restrict__ V, int m, const double* __restrict__ Tall, d
   for (int kb = ((nrefl - 1) / 32) * 32; kb >= 0; kb -= 32) {
     const int nb = min(32, nrefl - kb);
     const double* T = Tall + (size_t)(kb / 32) * 1024;
-    for (int x = tid; x < nb * m; x += BAT) {
-      const int j = x / m, r = x - (x / m) * m;
-      Vb[j * vld + r] = V[(size_t)(kb + j) * m + r];
+    // rows kb..kb+nb-1 of V are contiguous: stage them with 8 loads in flight per thread
+    const double* Vsrc = V + (size_t)kb * m;
+    for (int x0 = tid; x0 < nb * m; x0 += BAT * 8) {
+      double tv[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) tv[u] = x0 + u * BAT < nb * m ? Vsrc[x0 + u * BAT] : 0.0;
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int x = x0 + u * BAT;
+        if (x < nb * m) {
+          const int j = x / m, r = x - (x / m) * m;
+          Vb[j * vld + r] = tv[u];
+        }
+      }
     }
-    for (int x = tid; x < 1024; x += BAT) Tb[(x >> 5) * 33 + (x & 31)] = T[x];
+    {
+      double tt[1024 / BAT];
+#pragma unroll
+      for (int u = 0; u < 1024 / BAT; ++u) tt[u] = T[tid + u * BAT];
+#pragma unroll
+      for (int u = 0; u < 1024 / BAT; ++u) {
+        const int x = tid + u * BAT;
+        Tb[(x >> 5) * 33 + (x & 31)] = tt[u];
+      }
+    }
     __syncthreads();
     // W1 = V_b' Y (v_{kb+j}[r] = 0 for r <= kb + j)
     if (jj < nb) {
@@ -3025,9 +3129,8 @@ int sygv_enqueue(const double* ga, const double* gb, int ldg, int m, int nev, do
   if (!ident) {
     launch_chol(w.B, m, w.L, w.Linv, 0, status, st);
     SPB_LAUNCH_CHECK();
-    dim3 grid((unsigned)ceil_div(m, 32), (unsigned)ceil_div(m, 32));
-    small_gemm<<<grid, 256, 0, st>>>(0, 0, m, m, m, w.Linv, m, w.A, m, w.M, m);
-    small_gemm<<<grid, 256, 0, st>>>(0, 1, m, m, m, w.M, m, w.Linv, m, w.Ap, m);
+    launch_small_gemm(0, 0, m, m, m, w.Linv, m, w.A, m, w.M, m, st);
+    launch_small_gemm(0, 1, m, m, m, w.M, m, w.Linv, m, w.Ap, m, st);
     SPB_LAUNCH_CHECK();
     Atri = w.Ap;
   }
@@ -3052,8 +3155,7 @@ int sygv_enqueue(const double* ga, const double* gb, int ldg, int m, int nev, do
   launch_wy_apply(w.V, m, w.scratch, w.Y, nev, status, st);
   SPB_LAUNCH_CHECK();
   if (!ident) {
-    dim3 grid((unsigned)ceil_div(nev, 32), (unsigned)ceil_div(m, 32));
-    small_gemm<<<grid, 256, 0, st>>>(1, 0, m, nev, m, w.Linv, m, w.Y, nev, C, ldc);
+    launch_small_gemm(1, 0, m, nev, m, w.Linv, m, w.Y, nev, C, ldc, st);
   } else {
     copy_cols<<<(int)ceil_div((int64_t)m * nev, 256), 256, 0, st>>>(w.Y, nev, m, nev, C, ldc);
   }
@@ -3131,11 +3233,10 @@ int normal_eq_inverse(const double* s, int k, double* inv, double* ws, size_t ws
   double* L = ws + kk;
   double* Li = ws + 2 * kk;
   double* T = ws + 3 * kk;
-  dim3 grid((unsigned)ceil_div(k, 32), (unsigned)ceil_div(k, 32));
-  small_gemm<<<grid, 256, 0, st>>>(1, 0, k, k, k, s, k, s, k, G, k);  // S'S
+  launch_small_gemm(1, 0, k, k, k, s, k, s, k, G, k, st);  // S'S
   launch_chol(G, k, L, Li, 0, status, st);
-  small_gemm<<<grid, 256, 0, st>>>(0, 1, k, k, k, Li, k, s, k, T, k);   // L^-1 S'
-  small_gemm<<<grid, 256, 0, st>>>(1, 0, k, k, k, Li, k, T, k, inv, k);  // L^-T (L^-1 S')
+  launch_small_gemm(0, 1, k, k, k, Li, k, s, k, T, k, st);   // L^-1 S'
+  launch_small_gemm(1, 0, k, k, k, Li, k, T, k, inv, k, st);  // L^-T (L^-1 S')
   SPB_LAUNCH_CHECK();
   return SPB_OK;
 }
@@ -3157,3 +3258,4 @@ int jacobi_svd_inverse(const double* s, int k, double* inv, double* ws, size_t w
 }
 
 }  // namespace spb
+

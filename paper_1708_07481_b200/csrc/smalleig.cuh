@@ -19,6 +19,7 @@ struct SmallStatus {
 
 constexpr double kEps64 = 2.220446049250313e-16;
 constexpr double kCondMax = 67108864.0;  // 1/sqrt(eps) (lobpcg.py:35)
+constexpr double kCondMaxF32 = 1e5;      // float32-storage guard on the RR basis (lobpcg.cu)
 
 size_t sygv_ws_doubles(int m, int nev);
 // G_A, G_B: device float64 m x m (ld ldg); gb may be null (B = I).

@@ -306,7 +306,7 @@ def lobpcg_solve(operator, x0, config: SolverConfig, precond=None, n_converge: i
                            np.array(conv[:], dtype=bool), work_blocks=6)
         state.solve_stats = dict(zip(("iterations", "spmm_calls", "rr_calls", "drop_p",
                                       "rebuild"), [int(s) for s in stats[:5]]))
-        state.solve_stats.update(spmm_us=int(stats[7]), spmm_bytes=int(stats[8]),
+        state.solve_stats.update(orth_p=int(stats[5]), spmm_us=int(stats[7]), spmm_bytes=int(stats[8]),
                                  spmm_cols=int(stats[9]))
         state.precision = precision
     del ws

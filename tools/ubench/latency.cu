@@ -101,6 +101,36 @@ __global__ void k_p1(int reps, int variant, long long* out) {
   if (tid == 0) out[0] = (t1 - t0) / (reps * 32);
 }
 
+
+__global__ void k_dfma(int iters, double x, long long* out, double* sink) {
+  double a = x, b = 1.0000001, c = 1e-9;
+  long long t0 = clock64();
+  for (int i = 0; i < iters; ++i) a = fma(a, b, c);
+  long long t1 = clock64();
+  if (threadIdx.x == 0) { out[0] = (t1 - t0) / iters; sink[0] = a; }
+}
+
+__global__ void k_dfma_tp(int iters, double x, long long* out, double* sink) {
+  double a0 = x, a1 = x + 1, a2 = x + 2, a3 = x + 3, a4 = x + 4, a5 = x + 5, a6 = x + 6, a7 = x + 7;
+  const double b = 1.0000001, c = 1e-9;
+  long long t0 = clock64();
+  for (int i = 0; i < iters; ++i) {
+    a0 = fma(a0, b, c); a1 = fma(a1, b, c); a2 = fma(a2, b, c); a3 = fma(a3, b, c);
+    a4 = fma(a4, b, c); a5 = fma(a5, b, c); a6 = fma(a6, b, c); a7 = fma(a7, b, c);
+  }
+  long long t1 = clock64();
+  if (threadIdx.x == 0) { out[0] = (t1 - t0) * 100 / iters; }
+  sink[threadIdx.x] = a0 + a1 + a2 + a3 + a4 + a5 + a6 + a7;
+}
+
+__global__ void k_shfl(int iters, double x, long long* out, double* sink) {
+  double a = x + threadIdx.x;
+  long long t0 = clock64();
+  for (int i = 0; i < iters; ++i) a += __shfl_xor_sync(0xffffffffu, a, 1 + (i & 15));
+  long long t1 = clock64();
+  if (threadIdx.x == 0) { out[0] = (t1 - t0) / iters; sink[0] = a; }
+}
+
 int main() {
   long long* d;
   double* sink;
@@ -118,6 +148,12 @@ int main() {
   k_ddiv<<<1, 32>>>(10000, 0.5, d, sink); cudaMemcpy(&h, d, 8, cudaMemcpyDeviceToHost); printf("dependent 1/x (DDIV): %lld cycles\n", h);
   k_drcp<<<1, 32>>>(10000, 0.5, d, sink); cudaMemcpy(&h, d, 8, cudaMemcpyDeviceToHost); printf("dependent __drcp_rn: %lld cycles\n", h);
   k_dsqrt<<<1, 32>>>(10000, 0.5, d, sink); cudaMemcpy(&h, d, 8, cudaMemcpyDeviceToHost); printf("dependent sqrt: %lld cycles\n", h);
+  k_dfma<<<1, 32>>>(10000, 0.5, d, sink); cudaMemcpy(&h, d, 8, cudaMemcpyDeviceToHost); printf("dependent DFMA: %lld cycles\n", h);
+  k_shfl<<<1, 32>>>(10000, 0.5, d, sink); cudaMemcpy(&h, d, 8, cudaMemcpyDeviceToHost); printf("dependent f64 shfl+DADD: %lld cycles\n", h);
+  for (int nt : {32, 128, 256, 512, 1024}) {
+    k_dfma_tp<<<1, nt>>>(10000, 0.5, d, sink); cudaMemcpy(&h, d, 8, cudaMemcpyDeviceToHost);
+    printf("8 indep DFMA per iter, %4d thr: %.2f cycles/iter\n", nt, h / 100.0);
+  }
   for (int nt : {32, 1024}) {
     k_smem_chain<<<1, nt>>>(10000, d); cudaMemcpy(&h, d, 8, cudaMemcpyDeviceToHost);
     printf("smem load->fma->store chain (%d thr): %lld cycles\n", nt, h);
