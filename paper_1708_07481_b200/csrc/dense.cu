@@ -374,13 +374,16 @@ int launch_gram_cfg(GramBatch bb, int64_t n, int out_rows, int out_cols, double*
 // of <= 32 warps can hold; 64-tiles pad 176 -> 192, 1.19x.)
 int gram_tile_for(const GramBatch& b) {
   static const int forced = getenv("SPB_GRAM_TILE") ? atoi(getenv("SPB_GRAM_TILE")) : 0;
-  if (forced == 64 || forced == 112) return forced;
+  if (forced == 56 || forced == 64 || forced == 112) return forced;
   int wmin = 1 << 30, wmax = 0;
   for (int j = 0; j < b.njobs; ++j) {
     wmax = std::max(wmax, std::max(b.job[j].p, b.job[j].q));
     wmin = std::min(wmin, std::max(b.job[j].p, b.job[j].q));
   }
-  return (wmax > 64 && wmax <= 112 && wmin > 64) ? 112 : 64;
+  if (wmax > 64 && wmax <= 112 && wmin > 64) return 112;
+  // C2's l = 49 blocks: 56 x 56 tiles pad 1.31x instead of 1.71x with 64-tiles
+  if (wmax > 32 && wmax <= 56) return 56;
+  return 64;
 }
 
 // Fixed-order reduction of the split-K partials: a CTA owns 32 consecutive
@@ -849,9 +852,18 @@ int gram_batched(int dtype, const GramBatch& b, int64_t n, int out_rows, int out
     else
       gram_kernel<double><<<grid, 128, 0, st>>>(b, n, kchunk, out_cols, stride, partial);
     SPB_LAUNCH_CHECK();
+  } else if (n > 0 && gram_tile_for(b) == 56) {
+    // 56 x 56: 7 warps of 8 x 56 (1 x 7 m8n8 tiles each), two CTAs per SM in the split
+    static const int cps = getenv("SPB_GRAM56_CPS") ? atoi(getenv("SPB_GRAM56_CPS")) : 2;
+    const int rc =
+        dtype == SPB_F32
+            ? launch_gram_cfg<float, 1, 7, 7, 1, 32>(b, n, out_rows, out_cols, partial, partial_cap,
+                                                     cps, &ks, st)
+            : launch_gram_cfg<double, 1, 7, 7, 1, 32>(b, n, out_rows, out_cols, partial, partial_cap,
+                                                      cps, &ks, st);
+    if (rc != SPB_OK) return rc;
   } else if (n > 0 && gram_tile_for(b) != 64) {
-    const int tw = gram_tile_for(b);
-    (void)tw;  // 112 x 112: 7 x 2 warps of 16 x 56 (2 x 7 m8n8 tiles each)
+    // 112 x 112: 7 x 2 warps of 16 x 56 (2 x 7 m8n8 tiles each)
     const int rc =
         dtype == SPB_F32
             ? launch_gram_cfg<float, 2, 7, 7, 2, 16>(b, n, out_rows, out_cols, partial, partial_cap, 1,

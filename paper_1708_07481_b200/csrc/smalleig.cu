@@ -2107,6 +2107,244 @@ bool launch_tridiag_warpcol(const double* Asrc, int m, int symmetrize, double* V
   return false;
 }
 
+// Row-per-warp Cholesky (default for kCholRwMin <= m <= 16 * kCrWarps): the rows of
+// B are split over a 16-CTA cluster, warp w of CTA r owns row i = r*nc + w and keeps
+// it in registers (lane L holds columns L + 32t). Step k needs column k of the
+// current Schur complement, whose entry j is owned by row j: every row pushes that one
+// value (st.async into each consumer CTA) as soon as its own update of step k-1 has
+// produced it, so a step costs one DSMEM exchange and no CTA barrier:
+//   a_ij -= (a_ik / a_kk) a_jk   (k < j <= i),
+// row k's pivot d_k = a_kk arriving with the column; L_ik = a_ik / sqrt(d_k).
+// A controller warp per CTA arms the expected bytes of the double-buffered column
+// mbarriers and stops with the rows when a pivot is not positive. The inverse is
+// formed afterwards by trinv_cols; chol_finish adds the norms / tests as for chol_cluster.
+constexpr int kCrWarps = 24;
+constexpr int kCrThreads = 32 * (kCrWarps + 1);
+constexpr int kCholRwMin = 165;  // below: chol_wsync (single CTA) measured faster
+
+template <int R>
+__global__ void __launch_bounds__(kCrThreads)
+chol_rowwarp(const double* __restrict__ Bsrc, int m, double* __restrict__ Lg, int mode,
+             SmallStatus* status) {
+  if (status->nonfinite) return;  // uniform over the cluster
+  unsigned rank_u, csize_u;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;\n" : "=r"(rank_u));
+  asm volatile("mov.u32 %0, %%cluster_nctarank;\n" : "=r"(csize_u));
+  const int rank = (int)rank_u, C = (int)csize_u;
+  const int nc = (m + C - 1) / C;
+  const int c0 = rank * nc;
+  const int ncl = max(0, min(m, c0 + nc) - c0);
+  const int cmax = ncl > 0 ? c0 + ncl - 1 : -1;
+  extern __shared__ __align__(16) double crs[];
+  double* colb = crs;  // [2][m] column k (parity k & 1), entries k..m-1
+  __shared__ __align__(8) uint64_t mbC[2];
+  __shared__ int s_fail;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const unsigned full = 0xffffffffu;
+#define cmax_of(r) ((r) * nc < m ? min(m, ((r) + 1) * nc) - 1 : -1)
+  if (warp == 0) {
+    int f0 = 0;
+    if (mode == 1) {  // diag > 0 and min diag > (eps na)^2 max diag (lobpcg.py:229-231)
+      double dmin, dmax;
+      warp_minmax(Bsrc, (int64_t)m + 1, m, false, &dmin, &dmax);
+      if (rank == 0 && lane == 0) {
+        status->dmin = dmin;
+        status->dmax = dmax;
+      }
+      const double t = kEps64 * m;
+      if (!(dmin > 0.0) || !(dmin > t * t * dmax)) f0 = 1;
+    }
+    if (lane == 0) {
+      s_fail = f0;
+      mb_init(&mbC[0], 1);
+      mb_init(&mbC[1], 1);
+      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+  }
+  __syncthreads();
+  if (s_fail) {  // the same test in every CTA: uniform
+    if (rank == 0 && threadIdx.x == 0) status->fallback = 1;
+    return;
+  }
+  cluster_sync_all();
+  const int nw = nc;
+  if (warp == nw) {
+    // controller: arm column k (8 (m-k) bytes) for consumers (rows > k); stop on a bad pivot
+    if (lane == 0 && cmax >= 0) {
+      if (cmax > 0) mb_expect(&mbC[0], 8u * (uint32_t)m);
+      if (cmax > 1) mb_expect(&mbC[1], 8u * (uint32_t)(m - 1));
+      for (int k = 0; k < m - 1 && cmax > k; ++k) {
+        const int b = k & 1;
+        mb_wait_bounded(&mbC[b], (uint32_t)((k >> 1) & 1), 11, k);
+        if (!(colb[b * m + k] > 0.0)) break;
+        if (k + 2 <= m - 1 && cmax > k + 2) mb_expect(&mbC[b], 8u * (uint32_t)(m - k - 2));
+      }
+    }
+  } else if (warp < ncl) {
+    const int i = c0 + warp;
+    double w[R];
+#pragma unroll
+    for (int t = 0; t < R; ++t) {
+      const int j = lane + 32 * t;
+      w[t] = j <= i && j < m ? Bsrc[(int64_t)i * m + j] : 0.0;
+    }
+    // upper triangle of L row i
+    for (int j = i + 1 + lane; j < m; j += 32) Lg[(int64_t)i * m + j] = 0.0;
+    {
+      const double a0 = __shfl_sync(full, w[0], 0);
+      if (lane < C && cmax_of(lane) > 0) st_async_f64(colb + i, &mbC[0], lane, a0);
+    }
+    bool ok = true;
+    for (int k = 0; k < i; ++k) {
+      const int b = k & 1;
+      mb_wait_bounded(&mbC[b], (uint32_t)((k >> 1) & 1), 12, k);
+      const double* col = colb + b * m;
+      const double dk = col[k];
+      if (!(dk > 0.0)) {
+        ok = false;
+        break;
+      }
+      double aik = 0.0;
+#pragma unroll
+      for (int t = 0; t < R; ++t)
+        if (lane + 32 * t == k) aik = w[t];
+      aik = __shfl_sync(full, aik, k & 31);
+      const double rs = rsqrt(dk);
+      if (lane == 0) Lg[(int64_t)i * m + k] = aik * rs;  // L_ik
+      const double f = aik / dk;
+      // the entry of column k+1 first, pushed at once; then the rest of the row
+      double nxt = 0.0;
+#pragma unroll
+      for (int t = 0; t < R; ++t) {
+        const int j = lane + 32 * t;
+        if (j == k + 1) {
+          w[t] = fma(-f, col[j], w[t]);
+          nxt = w[t];
+        }
+      }
+      nxt = __shfl_sync(full, nxt, (k + 1) & 31);
+      const int b1 = (k + 1) & 1;
+      if (lane < C && cmax_of(lane) > k + 1) st_async_f64(colb + b1 * m + i, &mbC[b1], lane, nxt);
+#pragma unroll
+      for (int t = 0; t < R; ++t) {
+        const int j = lane + 32 * t;
+        if (j > k + 1 && j <= i) w[t] = fma(-f, col[j], w[t]);
+      }
+    }
+    if (ok) {
+      // own pivot: d_i = a_ii after step i-1
+      double dii = 0.0;
+#pragma unroll
+      for (int t = 0; t < R; ++t)
+        if (lane + 32 * t == i) dii = w[t];
+      dii = __shfl_sync(full, dii, i & 31);
+      if (lane == 0) {
+        if (dii > 0.0) {
+          Lg[(int64_t)i * m + i] = sqrt(dii);
+        } else {
+          if (mode == 0) status->not_pd = 1;
+          else status->fallback = 1;
+        }
+      }
+    }
+  }
+  cluster_sync_all();  // no CTA leaves while a peer may still address its shared memory
+#undef cmax_of
+}
+
+// L^-1 (row-major, lower) from L (row-major): one warp per column c solves L z = e_c
+// right-looking (z_k = r_k / L_kk, r_j -= L_jk z_k), the lane holding rows
+// L + 32t; columns of L are staged in shared memory 32 at a time.
+template <int R>
+__global__ void __launch_bounds__(512)
+trinv_cols(const double* __restrict__ Lg, int m, double* __restrict__ Linv,
+           const SmallStatus* status) {
+  if (status->nonfinite || status->not_pd || status->fallback) return;
+  extern __shared__ __align__(16) double tis[];
+  double* rd = tis;           // [m] 1 / L_kk
+  double* Ls = tis + m;       // [32][m] columns k0..k0+31 of L (column-major)
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarp = blockDim.x >> 5;
+  const int c = blockIdx.x * nwarp + warp;  // column of L^-1 this warp forms
+  const int cfirst = blockIdx.x * nwarp;
+  for (int k = threadIdx.x; k < m; k += blockDim.x) rd[k] = 1.0 / Lg[(int64_t)k * m + k];
+  double r[R];
+#pragma unroll
+  for (int t = 0; t < R; ++t) r[t] = lane + 32 * t == c ? 1.0 : 0.0;
+  if (c < m)
+    for (int k = lane; k < c; k += 32) Linv[(int64_t)k * m + c] = 0.0;
+  for (int k0 = (cfirst / 32) * 32; k0 < m; k0 += 32) {
+    const int kn = min(32, m - k0);
+    __syncthreads();  // previous chunk consumed (and rd written)
+    for (int x = threadIdx.x; x < m * kn; x += blockDim.x) {
+      const int j = x / kn, q = x - (x / kn) * kn;  // row j, column k0 + q (coalesced rows)
+      Ls[q * m + j] = Lg[(int64_t)j * m + k0 + q];
+    }
+    __syncthreads();
+    if (c < m)
+      for (int q = 0; q < kn; ++q) {
+        const int k = k0 + q;
+        if (k < c) continue;
+        double rk = 0.0;
+#pragma unroll
+        for (int t = 0; t < R; ++t)
+          if (lane + 32 * t == k) rk = r[t];
+        const double zk = __shfl_sync(0xffffffffu, rk, k & 31) * rd[k];
+        if (lane == 0) Linv[(int64_t)k * m + c] = zk;
+        const double* lc = Ls + q * m;
+#pragma unroll
+        for (int t = 0; t < R; ++t) {
+          const int j = lane + 32 * t;
+          if (j > k && j < m) r[t] = fma(-lc[j], zk, r[t]);
+        }
+      }
+  }
+}
+
+bool launch_chol_rowwarp(const double* B, int m, double* L, double* Linv, int mode,
+                         SmallStatus* status, cudaStream_t st) {
+  static const bool off = getenv("SPB_CHOL_ROWWARP") && atoi(getenv("SPB_CHOL_ROWWARP")) == 0;
+  if (off || m < kCholRwMin) return false;
+  const int C = 16, nc = (m + C - 1) / C;
+  const int R = (m + 31) / 32;
+  if (nc > kCrWarps || R > 12) return false;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(C);
+  cfg.blockDim = dim3(32 * (nc + 1));
+  cfg.dynamicSmemBytes = sizeof(double) * 2 * (size_t)m;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = C;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  const size_t ti_smem = sizeof(double) * 33 * (size_t)m;
+  const int ti_warps = 16;
+  const dim3 ti_grid((unsigned)((m + ti_warps - 1) / ti_warps));
+#define SPB_CR(RR)                                                                               \
+  {                                                                                              \
+    static bool attr = false;                                                                    \
+    if (!attr) {                                                                                 \
+      cudaFuncSetAttribute(chol_rowwarp<RR>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1); \
+      cudaFuncSetAttribute(trinv_cols<RR>, cudaFuncAttributeMaxDynamicSharedMemorySize,          \
+                           200 * 1024);                                                          \
+      attr = true;                                                                               \
+    }                                                                                            \
+    cudaLaunchKernelEx(&cfg, chol_rowwarp<RR>, B, m, L, mode, status);                          \
+    trinv_cols<RR><<<ti_grid, 32 * ti_warps, ti_smem, st>>>(L, m, Linv, status);               \
+    chol_finish<<<1, ET, 0, st>>>(B, m, L, Linv, mode, status);                                 \
+    return true;                                                                                 \
+  }
+  if (R <= 2) SPB_CR(2)
+  if (R <= 4) SPB_CR(4)
+  if (R <= 6) SPB_CR(6)
+  if (R <= 8) SPB_CR(8)
+  if (R <= 12) SPB_CR(12)
+#undef SPB_CR
+  return false;
+}
+
 size_t chol_cluster_smem(int m, int C) {
   const int nc = (m + C - 1) / C;
   return sizeof(double) * ((size_t)m * nc + 2 * (size_t)m);
@@ -3041,6 +3279,7 @@ void launch_chol(const double* B, int m, double* L, double* Linv, int mode, Smal
                                                          : kCholLdlMax + 1;
   static const int cfix = getenv("SPB_CHOL_CLUSTER_C") ? atoi(getenv("SPB_CHOL_CLUSTER_C")) : 0;
   static const bool unblocked = getenv("SPB_CHOL_LDL") != nullptr;  // A/B switch
+  if (!old && !unblocked && launch_chol_rowwarp(B, m, L, Linv, mode, status, st)) return;
   if (!old && !unblocked && m < cmin && m <= kCholLdlMax && chol_wsync_smem(m) <= 217 * 1024) {
     // SPB_CHOL_TRACE=<file>: clock64 phase stamps appended to <file> (diagnostics)
     static const char* tf = getenv("SPB_CHOL_TRACE");
