@@ -20,7 +20,8 @@
 //             regions (double-buffered);
 //   warps 2-5 splitters: hi written in place over the staged tile, lo into its
 //             own buffer (elementwise, so the swizzled layout is preserved);
-//   warps 6-9 epilogue: per chunk, tcgen05.ld the region and add it into
+//   warps 6-9 epilogue (6-13 when q > 128, two warps per lane quarter, each
+//             owning half of the columns): per chunk, tcgen05.ld the region and add it into
 //             float32 registers (round-to-nearest: the tensor cores' own
 //             accumulation, which is not, then spans 12 MMAs only); at every
 //             emit, store the running sum (+ init) as float32 rows.
@@ -35,7 +36,8 @@ constexpr int UTM = 128;             // rows per CTA (UMMA M)
 constexpr int UTK = 32;              // K per chunk (one 128-byte swizzle atom of fp32)
 constexpr int UTS_MAX = 4;           // pipeline stages (runtime: 2 when two CTAs fit per SM)
 constexpr int kUtA = UTM * UTK * 4;  // A tile bytes (16 KB)
-constexpr int kUtThreads = 320;
+constexpr int kUtThreads = 320;  // 6 + 4 EW warps; EW = 1 (q <= 128)
+constexpr int kUtThreadsW = 448; // EW = 2 (q <= 192: each epilogue warp owns half the columns)
 
 __device__ __forceinline__ uint32_t ut_smem(const void* p) {
   return (uint32_t)__cvta_generic_to_shared(p);
@@ -157,8 +159,8 @@ __global__ void tc_stage_coeffs(UpdParams P, int npad, float* __restrict__ dst) 
   }
 }
 
-template <int NPMAX>
-__global__ void __launch_bounds__(kUtThreads, 1)
+template <int NPMAX, int EW>
+__global__ void __launch_bounds__(EW == 1 ? kUtThreads : kUtThreadsW, 1)
 update_tc_kernel(const __grid_constant__ CUtensorMap map0, const __grid_constant__ CUtensorMap map1,
                  const __grid_constant__ CUtensorMap map2, UtParams P) {
   extern __shared__ __align__(1024) uint8_t usm_raw[];
@@ -187,7 +189,7 @@ update_tc_kernel(const __grid_constant__ CUtensorMap map0, const __grid_constant
     }
     for (int e = 0; e < 2; ++e) {
       ut_mbar_init(&rdone[e], 1);
-      ut_mbar_init(&rfree[e], 128);
+      ut_mbar_init(&rfree[e], 128 * EW);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -277,18 +279,20 @@ update_tc_kernel(const __grid_constant__ CUtensorMap map0, const __grid_constant
     // chunk's 32-deep partial product is added into float32 registers
     // (round-to-nearest), so the tensor cores' accumulation covers only 12
     // MMAs; the running sum is written at every emit.
+    constexpr int NH = NPMAX / EW;         // columns per epilogue warp
     const int quarter = warp & 3;
+    const int cb = ((warp - 6) >> 2) * NH;  // first column of this warp
     int kc = 0;
     for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
     const int64_t row = (int64_t)tile * UTM + quarter * 32 + lane;
-    float acc[NPMAX];
+    float acc[NH];
 #pragma unroll
-    for (int i = 0; i < NPMAX; ++i) acc[i] = 0.0f;
+    for (int i = 0; i < NH; ++i) acc[i] = 0.0f;
     if (P.init && row < P.n) {
-      const float* irow = P.init + row * P.ldi;
+      const float* irow = P.init + row * P.ldi + cb;
 #pragma unroll
-      for (int i = 0; i < NPMAX; ++i)
-        if (i < P.q) acc[i] = irow[i];
+      for (int i = 0; i < NH; ++i)
+        if (cb + i < P.q) acc[i] = irow[i];
     }
     for (int s = 0; s < P.nseg; ++s) {
       for (int c = 0; c < P.seg[s].chunks; ++c, ++kc) {
@@ -296,11 +300,11 @@ update_tc_kernel(const __grid_constant__ CUtensorMap map0, const __grid_constant
         ut_wait(&rdone[rg], (kc >> 1) & 1);
         asm volatile("tcgen05.fence::after_thread_sync;");
 #pragma unroll
-        for (int c0 = 0; c0 < NPMAX; c0 += 16) {
-          if (c0 < P.npad) {
+        for (int c0 = 0; c0 < NH; c0 += 16) {
+          if (cb + c0 < P.npad) {
             uint32_t r[16];
             const uint32_t taddr =
-                tmem + ((uint32_t)(quarter * 32) << 16) + (uint32_t)(rg * P.npad + c0);
+                tmem + ((uint32_t)(quarter * 32) << 16) + (uint32_t)(rg * P.npad + cb + c0);
             asm volatile(
                 "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, "
                 "%10, %11, %12, %13, %14, %15}, [%16];"
@@ -317,17 +321,17 @@ update_tc_kernel(const __grid_constant__ CUtensorMap map0, const __grid_constant
         ut_arrive(&rfree[rg]);
       }
       if (P.seg[s].emit && row < P.n) {
-        float* orow = P.seg[s].out + row * P.seg[s].ldo;
+        float* orow = P.seg[s].out + row * P.seg[s].ldo + cb;
         const bool vec = (reinterpret_cast<uintptr_t>(orow) & 15) == 0;
 #pragma unroll
-        for (int c0 = 0; c0 < NPMAX; c0 += 4) {
-          if (vec && c0 + 4 <= P.q)
+        for (int c0 = 0; c0 < NH; c0 += 4) {
+          if (vec && cb + c0 + 4 <= P.q)
             *reinterpret_cast<float4*>(orow + c0) =
                 make_float4(acc[c0], acc[c0 + 1], acc[c0 + 2], acc[c0 + 3]);
           else
 #pragma unroll
             for (int i = 0; i < 4; ++i)
-              if (c0 + i < P.q) orow[c0 + i] = acc[c0 + i];
+              if (cb + c0 + i < P.q) orow[c0 + i] = acc[c0 + i];
         }
       }
     }
@@ -395,7 +399,7 @@ bool update_tc(const UpdParams& p, int64_t n, cudaStream_t st) {
     chunks += (g.w + UTK - 1) / UTK;
     wtot += g.w;
   }
-  if (nemit < 1 || !p.seg[p.nseg - 1].emit || npad > 128) return false;
+  if (nemit < 1 || !p.seg[p.nseg - 1].emit || npad > 192) return false;
   uint32_t cols = 32;
   while (cols < (uint32_t)(2 * npad)) cols <<= 1;
   const size_t need = (size_t)chunks * 2 * npad * UTK;
@@ -433,8 +437,9 @@ bool update_tc(const UpdParams& p, int64_t n, cudaStream_t st) {
   const size_t smem = (size_t)stages * kStage + 1024 + 256;
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(update_tc_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-    cudaFuncSetAttribute(update_tc_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    cudaFuncSetAttribute(update_tc_kernel<64, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    cudaFuncSetAttribute(update_tc_kernel<128, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    cudaFuncSetAttribute(update_tc_kernel<192, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
     attr = true;
   }
   if (smem > 227 * 1024) return false;
@@ -442,9 +447,11 @@ bool update_tc(const UpdParams& p, int64_t n, cudaStream_t st) {
   const int per_sm = 2 * (smem + 2048) <= 228 * 1024 ? 2 : 1;
   const unsigned grid = (unsigned)std::min<int64_t>(ceil_div(n, UTM), (int64_t)per_sm * num_sms());
   if (npad <= 64)
-    update_tc_kernel<64><<<grid, kUtThreads, smem, st>>>(maps[0], maps[1], maps[2], P);
+    update_tc_kernel<64, 1><<<grid, kUtThreads, smem, st>>>(maps[0], maps[1], maps[2], P);
+  else if (npad <= 128)
+    update_tc_kernel<128, 1><<<grid, kUtThreads, smem, st>>>(maps[0], maps[1], maps[2], P);
   else
-    update_tc_kernel<128><<<grid, kUtThreads, smem, st>>>(maps[0], maps[1], maps[2], P);
+    update_tc_kernel<192, 2><<<grid, kUtThreadsW, smem, st>>>(maps[0], maps[1], maps[2], P);
   return true;
 }
 

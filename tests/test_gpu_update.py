@@ -30,7 +30,8 @@ def _run(mode, a, c, scale, init, ld_out):
 
 @pytest.mark.parametrize("mode", [0, 1])
 @pytest.mark.parametrize("n,w,q", [(1000, 49, 49), (5003, 147, 49), (20000, 108, 108),
-                                   (777, 32, 16), (4096, 324, 108), (3000, 200, 256)])
+                                   (777, 32, 16), (4096, 324, 108), (3000, 200, 256),
+                                   (3001, 528, 176), (2048, 176, 144), (1500, 96, 192)])
 @pytest.mark.parametrize("with_init", [False, True])
 def test_update_accuracy(mode, n, w, q, with_init):
     g = torch.Generator(device="cuda").manual_seed(n + w + q)
