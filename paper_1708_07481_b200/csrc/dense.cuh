@@ -85,6 +85,10 @@ int laplacian_spmm(int dtype, int32_t r0, int32_t r1, const int32_t* rp, const i
 // tcgen05 3xTF32 Gram (gram_tc.cu): out[p x (q0+q1)] = U' [V0 | V1], float32 operands.
 bool gram_tc_supported();
 size_t gram_tc_partial_doubles(int64_t n, int p, int qtot);
+// Rayleigh-Ritz Grams on the int8 tensor cores with the Ozaki splitting (gram_oz.cu):
+// Gb = B'B and Ga = B'LB (ld ldo), float32 operands n x cols, float64-accurate.
+int gram_oz_rr(const float* B, const float* LB, int64_t ld, int64_t n, int cols, double* Ga,
+               double* Gb, int ldo, cudaStream_t st);
 int gram_tc(const float* U, int64_t ldu, int p, const float* V0, int64_t ldv0, int q0,
             const float* V1, int64_t ldv1, int q1, int64_t n, double* partial, size_t partial_cap,
             double* out, int ldo, cudaStream_t st);

@@ -3,9 +3,10 @@
 //
 //   G[p x q] = U' V,   U: n x p, V: n x q (float32, vertex-major, row stride ld)
 //
-// Every column c of U (and of V) gets a power-of-two scale 2^e_c > max|x|; the
-// scaled entries r in (-1, 1) are written as S = 6 signed 7-bit digits,
-// r = sum_t a_t 2^(-7t) + eps, |eps| < 2^-42 (exact digit extraction in fp32).
+// Every column c of U (and of V) gets a power-of-two scale 2^e_c > 2 max|x|; the
+// scaled entries r in (-1/2, 1/2) are written as S = 6 signed digits in [-64, 64]
+// (round to nearest), r = sum_t a_t 2^(-7t) + eps, |eps| <= 2^-43 (exact digit
+// extraction in fp32).
 // Then G_cd = 2^(e_c + e_d) sum_{t+u <= S+1} 2^(-7(t+u)) (A_t' B_u)_cd: 21 int8
 // GEMMs with exact int32 accumulation, grouped by the level t+u into six TMEM
 // accumulators, converted to fp64 and combined smallest level first. The
@@ -92,6 +93,15 @@ __device__ __forceinline__ void oz_commit(uint64_t* bar) {
 }
 
 // Column maxima |x| (as float bits; non-negative floats order like their bits).
+// Column scale exponent: 2^e > 2 max|x| (the scaled entries lie in (-1/2, 1/2), so the
+// round-to-nearest digits below stay within [-64, 64]).
+__device__ __forceinline__ int oz_exp(unsigned cm) {
+  const float mx = __uint_as_float(cm);
+  int e = 0;
+  if (mx > 0.f) frexpf(mx, &e);  // mx < 2^e
+  return e + 1;
+}
+
 __global__ void oz_colmax(const float* __restrict__ X, int64_t ldx, int64_t n, int cols,
                           unsigned* __restrict__ cmax) {
   const int c = blockIdx.y * 32 + (threadIdx.x & 31);
@@ -120,11 +130,8 @@ oz_pack(const float* __restrict__ X, int64_t ldx, int64_t n, int cols, int ncg, 
     const int64_t kh = t / cpad;
     const int h = (int)(kh & 1);
     const int64_t kb = kh >> 1;
-    int e = 0;
-    if (c < cols) {
-      const float mx = __uint_as_float(cmax[c]);
-      if (mx > 0.f) frexpf(mx, &e);  // mx < 2^e
-    }
+    const int e = c < cols ? oz_exp(cmax[c]) : 0;
+    const float sc = ldexpf(1.0f, -e);  // exact power of two (normal range)
     float xv[16];
 #pragma unroll
     for (int i = 0; i < 16; ++i) {
@@ -136,15 +143,20 @@ oz_pack(const float* __restrict__ X, int64_t ldx, int64_t n, int cols, int ncg, 
     for (int sd = 0; sd < OZ_S; ++sd)
 #pragma unroll
       for (int q = 0; q < 4; ++q) w[sd][q] = 0u;
+    // digits by round-to-nearest through the 1.5 * 2^23 magic constant: the digit is
+    // the low byte of t's bit pattern (two's complement), no float -> int conversion
+    // (the F2I pipe runs at a quarter of the FP32 rate and bound this kernel)
+    constexpr float kMagic = 12582912.0f;
 #pragma unroll
     for (int i = 0; i < 16; ++i) {
-      float v = ldexpf(xv[i], -e);  // exact: power-of-two scaling
+      float v = xv[i] * sc;  // exact: power-of-two scaling, |v| < 1/2
 #pragma unroll
       for (int sd = 0; sd < OZ_S; ++sd) {
-        const float y = v * 128.f;
-        const float a = truncf(y);  // |a| <= 127 since |v| < 1
-        v = y - a;                  // exact
-        w[sd][i >> 2] |= ((uint32_t)(uint8_t)(int8_t)(int)a) << (8 * (i & 3));
+        const float y = v * 128.f;   // exact, |y| < 64 (+ rounding carry of the level above)
+        const float t = y + kMagic;  // round(y) in the low mantissa bits
+        const float a = t - kMagic;  // exact
+        v = y - a;                   // exact, |v| <= 1/2
+        w[sd][i >> 2] |= (__float_as_uint(t) & 0xffu) << (8 * (i & 3));
       }
     }
     const int64_t off = (((kb * ncg + (c >> 3)) * 2 + h) * 8 + (c & 7)) * 16;
@@ -260,11 +272,7 @@ gram_oz_kernel(const int8_t* __restrict__ PA, const int8_t* __restrict__ PB,
     }
     const int quarter = warp & 3;
     const int row = m0 + quarter * 32 + lane;
-    int eA = 0;
-    if (row < P.p) {
-      const float mx = __uint_as_float(cmaxA[row]);
-      if (mx > 0.f) frexpf(mx, &eA);
-    }
+    const int eA = row < P.p ? oz_exp(cmaxA[row]) : 0;
     double* out = part + (int64_t)blockIdx.y * P.split_stride;
     for (int c0 = 0; c0 < OZ_N; c0 += 16) {
       double acc[16];
@@ -293,10 +301,7 @@ gram_oz_kernel(const int8_t* __restrict__ PA, const int8_t* __restrict__ PB,
         for (int i = 0; i < 16; ++i) {
           const int col = n0 + c0 + i;
           if (col < P.q) {
-            int eB = 0;
-            const float mx = __uint_as_float(cmaxB[col]);
-            if (mx > 0.f) frexpf(mx, &eB);
-            out[(int64_t)row * P.q + col] = ldexp(acc[i], eA + eB);
+            out[(int64_t)row * P.q + col] = ldexp(acc[i], eA + oz_exp(cmaxB[col]));
           }
         }
       }
@@ -310,16 +315,16 @@ gram_oz_kernel(const int8_t* __restrict__ PA, const int8_t* __restrict__ PB,
   }
 }
 
-// Device scratch for the packed planes (grown on demand, never shrunk).
+// Device scratch (grown on demand, never shrunk), one slot per use.
 struct OzScratch {
   void* p = nullptr;
   size_t cap = 0;
 };
-void* oz_scratch(size_t bytes) {
-  static OzScratch s[16];
+void* oz_scratch_slot(int slot, size_t bytes) {
+  static OzScratch s[16][4];
   int dev = 0;
   cudaGetDevice(&dev);
-  OzScratch& x = s[dev & 15];
+  OzScratch& x = s[dev & 15][slot & 3];
   if (x.cap < bytes) {
     if (x.p) cudaFree(x.p);
     x.p = nullptr;
@@ -334,6 +339,41 @@ void* oz_scratch(size_t bytes) {
 
 }  // namespace
 
+// One operand in the packed digit layout (planes + per-column max bits).
+struct OzOperand {
+  int8_t* planes = nullptr;
+  unsigned* cmax = nullptr;
+  int cols = 0, ncg = 0;
+  int64_t n = 0, nkb = 0, plane_bytes = 0;
+};
+
+size_t oz_operand_bytes(int64_t n, int cols) {
+  const int64_t nkb = ceil_div(std::max<int64_t>(n, 1), OZ_KB);
+  // rounded to 1 KB: the next operand's planes are bulk-copy sources (16-byte aligned)
+  const size_t b = (size_t)OZ_S * nkb * ceil_div(cols, 8) * 256 + sizeof(unsigned) * (size_t)cols;
+  return (b + 1023) / 1024 * 1024;
+}
+
+// Column maxima and digit planes of X (n x cols, float32, row stride ldx) into mem.
+int oz_prepare(const float* X, int64_t ldx, int64_t n, int cols, void* mem, OzOperand* op,
+               cudaStream_t st) {
+  op->cols = cols;
+  op->n = n;
+  op->nkb = ceil_div(std::max<int64_t>(n, 1), OZ_KB);
+  op->ncg = (int)ceil_div(cols, 8);
+  op->plane_bytes = op->nkb * op->ncg * 256;
+  op->planes = (int8_t*)mem;
+  op->cmax = (unsigned*)(op->planes + OZ_S * op->plane_bytes);
+  SPB_CUDA(cudaMemsetAsync(op->cmax, 0, sizeof(unsigned) * (size_t)cols, st));
+  const int gx = (int)std::min<int64_t>(ceil_div(n, 8), 4 * num_sms());
+  oz_colmax<<<dim3(gx, (unsigned)ceil_div(cols, 32)), 256, 0, st>>>(X, ldx, n, cols, op->cmax);
+  const int64_t t = op->nkb * 2 * op->ncg * 8;
+  oz_pack<<<(int)std::min<int64_t>(ceil_div(t, 256), 16 * num_sms()), 256, 0, st>>>(
+      X, ldx, n, cols, op->ncg, op->nkb, op->cmax, op->planes, op->plane_bytes);
+  SPB_LAUNCH_CHECK();
+  return SPB_OK;
+}
+
 size_t gram_oz_partial_doubles(int64_t n, int p, int q) {
   const int tiles = (int)(ceil_div(p, OZ_M) * ceil_div(q, OZ_N));
   const int64_t nkb = ceil_div(std::max<int64_t>(n, 1), OZ_KB);
@@ -342,9 +382,10 @@ size_t gram_oz_partial_doubles(int64_t n, int p, int q) {
   return (size_t)std::max<int64_t>(ks, 1) * p * q;
 }
 
-// out[p x q] (ld ldo) = U' V with float32 operands, float64-accurate.
-int gram_oz(const float* U, int64_t ldu, int p, const float* V, int64_t ldv, int q, int64_t n,
-            double* partial, size_t partial_cap, double* out, int ldo, cudaStream_t st) {
+// out[A.cols x B.cols] (ld ldo) = A' B from two prepared operands.
+int oz_gemm(const OzOperand& A, const OzOperand& B, double* partial, size_t partial_cap,
+            double* out, int ldo, cudaStream_t st) {
+  const int p = A.cols, q = B.cols;
   if (p <= 0 || q <= 0) return SPB_OK;
   static bool attr = false;
   if (!attr) {
@@ -352,41 +393,17 @@ int gram_oz(const float* U, int64_t ldu, int p, const float* V, int64_t ldv, int
                                   kOzSmem));
     attr = true;
   }
-  const int64_t nkb = ceil_div(std::max<int64_t>(n, 1), OZ_KB);
-  const int ncgA = (int)ceil_div(p, 8), ncgB = (int)ceil_div(q, 8);
-  const int64_t planeA = nkb * ncgA * 256, planeB = nkb * ncgB * 256;
-  const size_t need = (size_t)OZ_S * (planeA + planeB) + sizeof(unsigned) * (size_t)(p + q) + 256;
-  uint8_t* scr = (uint8_t*)oz_scratch(need);
-  if (!scr) {
-    set_error("Ozaki Gram scratch allocation failed (%zu bytes)", need);
-    return SPB_ERR_CUDA;
-  }
-  int8_t* PA = (int8_t*)scr;
-  int8_t* PB = PA + OZ_S * planeA;
-  unsigned* cmA = (unsigned*)(PB + OZ_S * planeB);
-  unsigned* cmB = cmA + p;
-  SPB_CUDA(cudaMemsetAsync(cmA, 0, sizeof(unsigned) * (size_t)(p + q), st));
-  {
-    const int gx = (int)std::min<int64_t>(ceil_div(n, 8), 4 * num_sms());
-    oz_colmax<<<dim3(gx, (unsigned)ceil_div(p, 32)), 256, 0, st>>>(U, ldu, n, p, cmA);
-    oz_colmax<<<dim3(gx, (unsigned)ceil_div(q, 32)), 256, 0, st>>>(V, ldv, n, q, cmB);
-    const int64_t ta = nkb * 2 * ncgA * 8, tb = nkb * 2 * ncgB * 8;
-    oz_pack<<<(int)std::min<int64_t>(ceil_div(ta, 256), 16 * num_sms()), 256, 0, st>>>(
-        U, ldu, n, p, ncgA, nkb, cmA, PA, planeA);
-    oz_pack<<<(int)std::min<int64_t>(ceil_div(tb, 256), 16 * num_sms()), 256, 0, st>>>(
-        V, ldv, n, q, ncgB, nkb, cmB, PB, planeB);
-    SPB_LAUNCH_CHECK();
-  }
+  const int64_t nkb = A.nkb;
   OzParams P{};
   P.p = p;
   P.q = q;
   P.mtiles = (int)ceil_div(p, OZ_M);
   P.ntiles = (int)ceil_div(q, OZ_N);
-  P.ncgA = ncgA;
-  P.ncgB = ncgB;
+  P.ncgA = A.ncg;
+  P.ncgB = B.ncg;
   P.nkb = nkb;
-  P.planeA = planeA;
-  P.planeB = planeB;
+  P.planeA = A.plane_bytes;
+  P.planeB = B.plane_bytes;
   const int tiles = P.mtiles * P.ntiles;
   int64_t ks = std::max<int64_t>(ceil_div(2 * num_sms(), tiles), ceil_div(nkb, OZ_MAXROWS / OZ_KB));
   ks = std::min<int64_t>(ks, nkb);
@@ -398,9 +415,45 @@ int gram_oz(const float* U, int64_t ldu, int p, const float* V, int64_t ldv, int
     return SPB_ERR_WORKSPACE;
   }
   P.split_stride = (int64_t)p * q;
-  gram_oz_kernel<<<dim3(tiles, (unsigned)ks), 192, kOzSmem, st>>>(PA, PB, cmA, cmB, P, partial);
+  gram_oz_kernel<<<dim3(tiles, (unsigned)ks), 192, kOzSmem, st>>>(A.planes, B.planes, A.cmax,
+                                                                   B.cmax, P, partial);
   SPB_LAUNCH_CHECK();
   return oz_sum_splits(partial, (int)ks, P.split_stride, p, q, out, ldo, st);
+}
+
+// out[p x q] (ld ldo) = U' V with float32 operands, float64-accurate.
+int gram_oz(const float* U, int64_t ldu, int p, const float* V, int64_t ldv, int q, int64_t n,
+            double* partial, size_t partial_cap, double* out, int ldo, cudaStream_t st) {
+  if (p <= 0 || q <= 0) return SPB_OK;
+  const size_t ba = oz_operand_bytes(n, p), bb = oz_operand_bytes(n, q);
+  uint8_t* scr = (uint8_t*)oz_scratch_slot(0, ba + bb);
+  if (!scr) {
+    set_error("Ozaki Gram scratch allocation failed (%zu bytes)", ba + bb);
+    return SPB_ERR_CUDA;
+  }
+  OzOperand A, B;
+  SPB_TRY(oz_prepare(U, ldu, n, p, scr, &A, st));
+  SPB_TRY(oz_prepare(V, ldv, n, q, scr + ba, &B, st));
+  return oz_gemm(A, B, partial, partial_cap, out, ldo, st);
+}
+
+// The Rayleigh-Ritz Grams of the solver: Gb = B'B (ld ldo) and Ga = B'LB (ld ldo), B
+// and LB n x cols (row stride ld), each operand packed once; scratch owned here.
+int gram_oz_rr(const float* B, const float* LB, int64_t ld, int64_t n, int cols, double* Ga,
+               double* Gb, int ldo, cudaStream_t st) {
+  const size_t bo = oz_operand_bytes(n, cols);
+  uint8_t* scr = (uint8_t*)oz_scratch_slot(1, 2 * bo);
+  const size_t pc = gram_oz_partial_doubles(n, cols, cols);
+  double* part = (double*)oz_scratch_slot(2, pc * sizeof(double));
+  if (!scr || !part) {
+    set_error("Ozaki Gram scratch allocation failed (%zu bytes)", 2 * bo + pc * sizeof(double));
+    return SPB_ERR_CUDA;
+  }
+  OzOperand OB, OL;
+  SPB_TRY(oz_prepare(B, ld, n, cols, scr, &OB, st));
+  SPB_TRY(oz_prepare(LB, ld, n, cols, scr + bo, &OL, st));
+  SPB_TRY(oz_gemm(OB, OB, part, pc, Gb, ldo, st));
+  return oz_gemm(OB, OL, part, pc, Ga, ldo, st);
 }
 
 }  // namespace spb

@@ -36,6 +36,7 @@ struct SolveWs {
   double *G;          // mmax x 2mmax: [G_A | G_B]
   double *Gpad;       // 3lp x 6lp: [B'B | B'LB] over the padded basis (tensor-core path)
   bool use_tc;        // float32 storage on sm_100: Grams on tcgen05 (3xTF32)
+  bool use_oz;        // float32 storage, large n: RR Grams on int8 tcgen05 (Ozaki)
   double *gpart;      // gram split partials
   size_t gpart_cap;
   double *Gs;         // small Gram (lp x lp)
@@ -81,6 +82,7 @@ SolveWs carve(Arena& a, int dtype, int n, int l, int nranks = 1, int n_max = 0) 
   w.gpart_cap = gram_partial_doubles(n, std::min(12, 18 * seg_tiles), mm, 2 * mm, nullptr);
   w.gpart_cap = std::max(w.gpart_cap, gram_partial_doubles(n, seg_tiles, w.lp, w.lp, nullptr));
   w.use_tc = false;
+  w.use_oz = false;
   if (dtype == SPB_F32) {
     // Opt-in: the 3xTF32 tensor-core Gram accumulates in fp32 inside a CTA's row
     // range; measured against the reference it moves Ritz values by ~2e-3 after
@@ -88,6 +90,10 @@ SolveWs carve(Arena& a, int dtype, int n, int l, int nranks = 1, int n_max = 0) 
     // default ("Gram precision").
     const char* env = getenv("SPB_GRAM");
     w.use_tc = env && std::strcmp(env, "tc") == 0;
+    // Ozaki int8 Grams (float64-accurate, ~3e-14 relative) for the RR products once
+    // the basis is large enough for the digit packing to pay (C3, C4); SPB_GRAM=oz /
+    // dmma force either
+    w.use_oz = !w.use_tc && (env ? std::strcmp(env, "oz") == 0 : (double)n * w.ld >= 5e7);
     w.gpart_cap = std::max(w.gpart_cap, gram_tc_partial_doubles(n, w.ld, 2 * w.ld));
   }
   w.gpart = a.take<double>(w.gpart_cap);
@@ -227,6 +233,20 @@ struct Driver {
 
   // [G_A | G_B] for the basis [X (l) | R (na) | P (pw)] and images.
   int rr_grams(int na, int pw) {
+    if (w.use_oz) {
+      // [B'B | B'LB] over the padded basis from one packing of B and of LB, then
+      // gather the m x m blocks (as the tcgen05 path below)
+      const int pe = pw > 0 ? 2 * w.lp + pw : w.lp + na;
+      SPB_TRY(gram_oz_rr((const float*)w.B, (const float*)w.LB, w.ld, w.n, pe, w.Gpad + pe,
+                         w.Gpad, 2 * pe, st));
+      SPB_TRY(allreduce(w.Gpad, (size_t)pe * 2 * pe));
+      const int m = w.l + na + pw;
+      gather_pad_grams<<<(int)std::min<int64_t>(ceil_div((int64_t)m * m, 256), 1024), 256, 0, st>>>(
+          w.Gpad, 2 * pe, pe, m, w.l, na, w.lp, w.G, 2 * w.mmax, w.mmax);
+      SPB_LAUNCH_CHECK();
+      tc_full_grams = true;
+      return SPB_OK;
+    }
     if (w.use_tc) {
       // one GEMM over the padded basis: [B'B | B'LB], then gather the m x m blocks
       const int pe = pw > 0 ? 2 * w.lp + pw : w.lp + na;
@@ -430,6 +450,7 @@ struct Driver {
 
   // sygv with the ladder's ConditioningError semantics; *ok = success.
   bool p_ill = false;  // set by small_gen_eigh: see the float32 note there
+  int cur_pw = 0;      // P columns in the basis of the current Rayleigh-Ritz solve
 
   // P <- orthonormal basis of (I - X X')(I - R R') P (rank-revealing CholQR), LP = L P.
   int orth_p(int na, int* pw) {
@@ -480,7 +501,7 @@ struct Driver {
     // The ladder decision itself keeps the reference's 1/sqrt(eps64) threshold.
     static const double f32_lo =  // SPB_F32_COND_LO: A/B override of the threshold
         getenv("SPB_F32_COND_LO") ? atof(getenv("SPB_F32_COND_LO")) : kCondMaxF32;
-    p_ill = w.dtype == SPB_F32 && !identity_b && m > seg2 && hs.cond_lo > f32_lo;
+    p_ill = w.dtype == SPB_F32 && !identity_b && cur_pw > 0 && hs.cond_lo > f32_lo;
     if (hs.cond_state == 2) {
       double cond = 0.0;
       // sygv's workspace holds the symmetrised G_B in its B slot; recompute from G
@@ -673,8 +694,10 @@ struct Driver {
           grams_ready = true;
         }
         const int m = l + na + pw;
+        cur_pw = pw;
         if (tc_full_grams) SPB_TRY(small_gen_eigh(m, false, &ok));
         else SPB_TRY(small_gen_eigh(m, false, &ok, l, l + na));
+        cur_pw = 0;
         if (ok && p_ill && pw > 0) {
           stats[5]++;
           SPB_TRY(orth_p(na, &pw));
