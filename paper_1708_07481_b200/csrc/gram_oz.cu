@@ -114,6 +114,42 @@ __global__ void oz_colmax(const float* __restrict__ X, int64_t ldx, int64_t n, i
   atomicMax(&cmax[c], m);
 }
 
+// Same with 16-byte loads: a warp covers 128 consecutive columns of a row.
+__global__ void oz_colmax4(const float* __restrict__ X, int64_t ldx, int64_t n, int cols,
+                           unsigned* __restrict__ cmax) {
+  __shared__ uint4 wm[8][32];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int c = blockIdx.y * 128 + lane * 4;
+  unsigned m0 = 0, m1 = 0, m2 = 0, m3 = 0;
+  if (c < cols) {
+    const int64_t step = (int64_t)gridDim.x * (blockDim.x >> 5);
+#pragma unroll 8
+    for (int64_t r = (int64_t)blockIdx.x * (blockDim.x >> 5) + warp; r < n; r += step) {
+      const float4 v = __ldg(reinterpret_cast<const float4*>(X + r * ldx + c));
+      m0 = max(m0, __float_as_uint(fabsf(v.x)));
+      m1 = max(m1, __float_as_uint(fabsf(v.y)));
+      m2 = max(m2, __float_as_uint(fabsf(v.z)));
+      m3 = max(m3, __float_as_uint(fabsf(v.w)));
+    }
+  }
+  wm[warp][lane] = make_uint4(m0, m1, m2, m3);
+  __syncthreads();
+  // one atomic per column per CTA (8x fewer on the same addresses)
+  if (warp == 0 && c < cols) {
+    for (int q = 1; q < 8; ++q) {
+      const uint4 o = wm[q][lane];
+      m0 = max(m0, o.x);
+      m1 = max(m1, o.y);
+      m2 = max(m2, o.z);
+      m3 = max(m3, o.w);
+    }
+    atomicMax(&cmax[c], m0);
+    if (c + 1 < cols) atomicMax(&cmax[c + 1], m1);
+    if (c + 2 < cols) atomicMax(&cmax[c + 2], m2);
+    if (c + 3 < cols) atomicMax(&cmax[c + 3], m3);
+  }
+}
+
 // Digits of x / 2^e_c into the packed planes (see the header comment). One
 // thread per (k-block, k half, column): 16 consecutive rows of one column, the
 // lanes of a warp on 32 consecutive columns (coalesced row reads); the 16 digit
@@ -175,6 +211,7 @@ struct OzParams {
   int64_t kbchunk;   // k-blocks per split
   int64_t planeA, planeB;  // bytes per plane
   int64_t split_stride;
+  int upper;         // U == V: tiles strictly below the diagonal are skipped (symmetric)
 };
 
 __global__ void __launch_bounds__(192, 1)
@@ -190,6 +227,7 @@ gram_oz_kernel(const int8_t* __restrict__ PA, const int8_t* __restrict__ PB,
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int mt = blockIdx.x % P.mtiles, nt = blockIdx.x / P.mtiles;
   const int m0 = mt * OZ_M, n0 = nt * OZ_N;
+  if (P.upper && n0 + OZ_N <= m0) return;  // every column of the tile below every row
   const int64_t kb0 = (int64_t)blockIdx.y * P.kbchunk;
   const int64_t kb1 = min(P.nkb, kb0 + P.kbchunk);
   const int nk = kb1 > kb0 ? (int)(kb1 - kb0) : 0;
@@ -366,7 +404,12 @@ int oz_prepare(const float* X, int64_t ldx, int64_t n, int cols, void* mem, OzOp
   op->cmax = (unsigned*)(op->planes + OZ_S * op->plane_bytes);
   SPB_CUDA(cudaMemsetAsync(op->cmax, 0, sizeof(unsigned) * (size_t)cols, st));
   const int gx = (int)std::min<int64_t>(ceil_div(n, 8), 4 * num_sms());
-  oz_colmax<<<dim3(gx, (unsigned)ceil_div(cols, 32)), 256, 0, st>>>(X, ldx, n, cols, op->cmax);
+  if ((reinterpret_cast<uintptr_t>(X) & 15) == 0 && (ldx & 3) == 0)
+    oz_colmax4<<<dim3((unsigned)std::min<int64_t>(ceil_div(n, 64), 2 * num_sms()),
+                      (unsigned)ceil_div(cols, 128)),
+                 256, 0, st>>>(X, ldx, n, cols, op->cmax);
+  else
+    oz_colmax<<<dim3(gx, (unsigned)ceil_div(cols, 32)), 256, 0, st>>>(X, ldx, n, cols, op->cmax);
   const int64_t t = op->nkb * 2 * op->ncg * 8;
   oz_pack<<<(int)std::min<int64_t>(ceil_div(t, 256), 16 * num_sms()), 256, 0, st>>>(
       X, ldx, n, cols, op->ncg, op->nkb, op->cmax, op->planes, op->plane_bytes);
@@ -384,7 +427,7 @@ size_t gram_oz_partial_doubles(int64_t n, int p, int q) {
 
 // out[A.cols x B.cols] (ld ldo) = A' B from two prepared operands.
 int oz_gemm(const OzOperand& A, const OzOperand& B, double* partial, size_t partial_cap,
-            double* out, int ldo, cudaStream_t st) {
+            double* out, int ldo, cudaStream_t st, bool upper = false) {
   const int p = A.cols, q = B.cols;
   if (p <= 0 || q <= 0) return SPB_OK;
   static bool attr = false;
@@ -415,6 +458,7 @@ int oz_gemm(const OzOperand& A, const OzOperand& B, double* partial, size_t part
     return SPB_ERR_WORKSPACE;
   }
   P.split_stride = (int64_t)p * q;
+  P.upper = upper ? 1 : 0;
   gram_oz_kernel<<<dim3(tiles, (unsigned)ks), 192, kOzSmem, st>>>(A.planes, B.planes, A.cmax,
                                                                    B.cmax, P, partial);
   SPB_LAUNCH_CHECK();
@@ -437,7 +481,8 @@ int gram_oz(const float* U, int64_t ldu, int p, const float* V, int64_t ldv, int
   return oz_gemm(A, B, partial, partial_cap, out, ldo, st);
 }
 
-// The Rayleigh-Ritz Grams of the solver: Gb = B'B (ld ldo) and Ga = B'LB (ld ldo), B
+// The Rayleigh-Ritz Grams of the solver: Gb = B'B (upper triangle valid, ld ldo) and
+// Ga = B'LB (ld ldo), B
 // and LB n x cols (row stride ld), each operand packed once; scratch owned here.
 int gram_oz_rr(const float* B, const float* LB, int64_t ld, int64_t n, int cols, double* Ga,
                double* Gb, int ldo, cudaStream_t st) {
@@ -452,7 +497,7 @@ int gram_oz_rr(const float* B, const float* LB, int64_t ld, int64_t n, int cols,
   OzOperand OB, OL;
   SPB_TRY(oz_prepare(B, ld, n, cols, scr, &OB, st));
   SPB_TRY(oz_prepare(LB, ld, n, cols, scr + bo, &OL, st));
-  SPB_TRY(oz_gemm(OB, OB, part, pc, Gb, ldo, st));
+  SPB_TRY(oz_gemm(OB, OB, part, pc, Gb, ldo, st, true));  // upper tiles (read as such)
   return oz_gemm(OB, OL, part, pc, Ga, ldo, st);
 }
 

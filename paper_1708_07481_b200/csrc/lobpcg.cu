@@ -131,7 +131,8 @@ __global__ void gather_pad_grams(const double* __restrict__ gp, int ldp, int pe,
     const int pi = i < l ? i : (i < l + na ? lp + (i - l) : 2 * lp + (i - l - na));
     const int pj = j < l ? j : (j < l + na ? lp + (j - l) : 2 * lp + (j - l - na));
     G[(size_t)i * ldg + j] = gp[(size_t)pi * ldp + pe + pj];         // G_A = B' LB
-    G[(size_t)i * ldg + mmax + j] = gp[(size_t)pi * ldp + pj];       // G_B = B' B
+    // G_B = B' B from its upper triangle (the Ozaki path computes only that)
+    G[(size_t)i * ldg + mmax + j] = gp[(size_t)min(pi, pj) * ldp + max(pi, pj)];
   }
 }
 
