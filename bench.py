@@ -222,7 +222,10 @@ def ten_x_tol(spb, g, x0, l, k, precision):
 
 def gram_roofline(n, l, precision):
     """Rayleigh-Ritz Gram [X R P]'[X R P] (n x 3l, solver layout) timed alone with
-    CUDA events on the launching stream: float64 products on the DMMA pipe."""
+    CUDA events on the launching stream, on the path the solver takes for this size:
+    float64 products on the DMMA pipe, or (float32 storage, n * ld >= 5e7: C3, C4)
+    the Ozaki int8 tcgen05 Gram (column maxima + digit packing + 21 int8 MMAs per
+    product, timed together)."""
     import torch
 
     from paper_1708_07481_b200 import _native as N
@@ -236,9 +239,11 @@ def gram_roofline(n, l, precision):
     L = N.lib()
     wsb = L.spb_gram_workspace(m, m, n)
     ws = torch.empty(wsb, dtype=torch.uint8, device="cuda")
+    oz = precision == "float32" and n * ld >= 5e7 and os.environ.get("SPB_GRAM", "") != "dmma"
+    mode = 2 if oz else 0
 
     def run():
-        N.check(L.spb_gram(code, 0, N.ptr(u), ld, m, N.ptr(u), ld, m, n, N.ptr(out), m,
+        N.check(L.spb_gram(code, mode, N.ptr(u), ld, m, N.ptr(u), ld, m, n, N.ptr(out), m,
                            N.ptr(ws), wsb, N.stream()))
 
     for _ in range(3):
@@ -253,6 +258,14 @@ def gram_roofline(n, l, precision):
     ms = e0.elapsed_time(e1) / reps
     tflops = 2.0 * n * m * m / (ms * 1e-3) / 1e12
     peak = 37.0  # B200 FP64 tensor (DMMA) spec per GPU; no measured FP64 peak in MEASURED_PEAKS.json
+    if oz:
+        tops = 21 * 2.0 * n * m * m / (ms * 1e-3) / 1e12
+        return {"bound": "tensor (int8 tcgen05, Ozaki splitting)", "achieved": tflops, "peak": peak,
+                "unit": "TFLOP/s (float64-equivalent, against the FP64 DMMA spec)",
+                "frac": tflops / peak, "peak_kind": "spec", "shape": f"{n}x{m} -> {m}x{m}",
+                "ms_per_launch": ms, "kernel": "spb::gram_oz_kernel (+ oz_colmax, oz_pack)",
+                "int8": {"achieved": tops, "peak": 4500.0, "unit": "TOPS (21 int8 MMAs per product)",
+                         "frac": tops / 4500.0, "peak_kind": "spec (dense int8)"}}
     return {"bound": "tensor (fp64 DMMA)", "achieved": tflops, "peak": peak, "unit": "TFLOP/s",
             "frac": tflops / peak, "peak_kind": "spec", "shape": f"{n}x{m} -> {m}x{m}",
             "ms_per_launch": ms, "kernel": "spb::gram_dmma"}
