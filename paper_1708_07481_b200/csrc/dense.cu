@@ -755,6 +755,79 @@ colreduce_kernel(int kind, const T* __restrict__ A, int64_t lda, int cols, int64
   }
 }
 
+// float32, 16-byte rows: the same reduction with float4 loads (a thread owns four
+// adjacent columns; 256 / ceil(cols/4 -> 32) row groups per CTA), for the wide blocks
+// of C3 / C4 where the scalar kernel had too few bytes in flight for HBM.
+__global__ void __launch_bounds__(256)
+colreduce4_kernel(int kind, const float* __restrict__ A, int64_t lda, int cols, int64_t n,
+                  int64_t rows_per_block, const float* __restrict__ X, int64_t ldx,
+                  const double* __restrict__ theta, float* __restrict__ R, int64_t ldr,
+                  double* __restrict__ part) {
+  extern __shared__ double sred[];  // [ry][cw * 4]
+  const int c4 = (cols + 3) / 4;
+  const int cw = ((c4 + 31) / 32) * 32;  // <= 256 (cols <= 1024)
+  const int nry = 256 / cw;
+  const int tid = threadIdx.x;
+  const int cx = tid % cw, ry = tid / cw;
+  const int c = cx * 4;
+  const int64_t rb = (int64_t)blockIdx.x * rows_per_block;
+  const int64_t re = min(n, rb + rows_per_block);
+  double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+  if (ry < nry && c < cols) {
+    float t0 = 0.f, t1 = 0.f, t2 = 0.f, t3 = 0.f;
+    if (kind == CR_RESIDUAL) {
+      t0 = (float)theta[c];
+      t1 = c + 1 < cols ? (float)theta[c + 1] : 0.f;
+      t2 = c + 2 < cols ? (float)theta[c + 2] : 0.f;
+      t3 = c + 3 < cols ? (float)theta[c + 3] : 0.f;
+    }
+#pragma unroll 4
+    for (int64_t r = rb + ry; r < re; r += nry) {
+      float4 v = *reinterpret_cast<const float4*>(A + r * lda + c);
+      if (kind == CR_RESIDUAL) {
+        const float4 x = *reinterpret_cast<const float4*>(X + r * ldx + c);
+        v.x = v.x - x.x * t0;
+        v.y = v.y - x.y * t1;
+        v.z = v.z - x.z * t2;
+        v.w = v.w - x.w * t3;
+        *reinterpret_cast<float4*>(R + r * ldr + c) = v;
+      }
+      if (kind == CR_SUM) {
+        s0 += (double)v.x; s1 += (double)v.y; s2 += (double)v.z; s3 += (double)v.w;
+      } else {
+        s0 += (double)v.x * v.x; s1 += (double)v.y * v.y; s2 += (double)v.z * v.z; s3 += (double)v.w * v.w;
+      }
+    }
+  }
+  if (ry < nry) {
+    double* q = sred + (ry * cw + cx) * 4;
+    q[0] = s0; q[1] = s1; q[2] = s2; q[3] = s3;
+  }
+  __syncthreads();
+  for (int cc = tid; cc < cols; cc += 256) {
+    double t = 0.0;
+    for (int y = 0; y < nry; ++y) t += sred[(y * cw + cc / 4) * 4 + (cc & 3)];
+    part[(int64_t)blockIdx.x * cols + cc] = t;
+  }
+}
+
+// float32 column scaling with float4 rows (no 64-bit division per element).
+__global__ void scale_cols4_kernel(float* __restrict__ A, int64_t lda, int n, const double* __restrict__ s,
+                                   int count) {
+  const int c4 = (count + 3) / 4;
+  const int total = n * c4;
+  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < total; e += gridDim.x * blockDim.x) {
+    const int r = e / c4, c = (e - r * c4) * 4;
+    float4* p = reinterpret_cast<float4*>(A + (int64_t)r * lda + c);
+    float4 v = *p;
+    v.x = (float)((double)v.x * s[c]);
+    if (c + 1 < count) v.y = (float)((double)v.y * s[c + 1]);
+    if (c + 2 < count) v.z = (float)((double)v.z * s[c + 2]);
+    if (c + 3 < count) v.w = (float)((double)v.w * s[c + 3]);
+    *p = v;
+  }
+}
+
 // One warp per column: lane-strided partial sums then a fixed shuffle tree
 // (deterministic: same order every call).
 __global__ void colreduce_final(const double* __restrict__ part, int blocks, int cols,
@@ -931,7 +1004,16 @@ int column_reduce(int dtype, int kind, const void* A, int64_t lda, int cols, int
   const int blocks = colreduce_blocks(n);
   const int64_t rpb = ceil_div(std::max<int64_t>(n, 1), blocks);
   const size_t smem = sizeof(double) * CRB;
-  if (dtype == SPB_F32)
+  const bool v4 = dtype == SPB_F32 && cols >= 64 && cols <= 1024 && (lda & 3) == 0 &&
+                  (reinterpret_cast<uintptr_t>(A) & 15) == 0 &&
+                  (kind != CR_RESIDUAL || ((ldx & 3) == 0 && (ldr & 3) == 0 &&
+                                           (reinterpret_cast<uintptr_t>(X) & 15) == 0 &&
+                                           (reinterpret_cast<uintptr_t>(R) & 15) == 0));
+  if (v4)
+    colreduce4_kernel<<<blocks, 256, sizeof(double) * 256 * 4, st>>>(
+        kind, (const float*)A, lda, cols, n, rpb, (const float*)X, ldx, theta, (float*)R, ldr,
+        partial);
+  else if (dtype == SPB_F32)
     colreduce_kernel<float><<<blocks, CRB, smem, st>>>(kind, (const float*)A, lda, cols, n, rpb,
                                                        (const float*)X, ldx, theta, (float*)R,
                                                        ldr, partial);
@@ -963,7 +1045,11 @@ int gather_columns(int dtype, void* A, int64_t lda, int64_t n, const int* idx, i
 int scale_columns(int dtype, void* A, int64_t lda, int64_t n, const double* s, int count,
                   cudaStream_t st) {
   if (n <= 0 || count <= 0) return SPB_OK;
-  if (dtype == SPB_F32)
+  if (dtype == SPB_F32 && (lda & 3) == 0 && (reinterpret_cast<uintptr_t>(A) & 15) == 0 &&
+      n * ((count + 3) / 4) < INT32_MAX)
+    scale_cols4_kernel<<<grid_1d(n * ((count + 3) / 4)), 256, 0, st>>>((float*)A, lda, (int)n, s,
+                                                                          count);
+  else if (dtype == SPB_F32)
     scale_cols_kernel<float><<<grid_1d(n * count), 256, 0, st>>>((float*)A, lda, n, s, count);
   else
     scale_cols_kernel<double><<<grid_1d(n * count), 256, 0, st>>>((double*)A, lda, n, s, count);
