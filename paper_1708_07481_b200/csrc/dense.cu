@@ -374,13 +374,15 @@ int launch_gram_cfg(GramBatch bb, int64_t n, int out_rows, int out_cols, double*
 // of <= 32 warps can hold; 64-tiles pad 176 -> 192, 1.19x.)
 int gram_tile_for(const GramBatch& b) {
   static const int forced = getenv("SPB_GRAM_TILE") ? atoi(getenv("SPB_GRAM_TILE")) : 0;
-  if (forced == 56 || forced == 64 || forced == 112) return forced;
+  if (forced == 56 || forced == 64 || forced == 88 || forced == 112) return forced;
   int wmin = 1 << 30, wmax = 0;
   for (int j = 0; j < b.njobs; ++j) {
     wmax = std::max(wmax, std::max(b.job[j].p, b.job[j].q));
     wmin = std::min(wmin, std::max(b.job[j].p, b.job[j].q));
   }
   if (wmax > 64 && wmax <= 112 && wmin > 64) return 112;
+  // C4's l = 176 blocks: 2 x 2 tiles of 88 pad nothing (64-tiles: 192 = 1.19x)
+  if (wmax > 112 && wmax <= 176 && wmin > 88) return 88;
   // C2's l = 49 blocks: 56 x 56 tiles pad 1.31x instead of 1.71x with 64-tiles
   if (wmax > 32 && wmax <= 56) return 56;
   return 64;
@@ -934,6 +936,15 @@ int gram_batched(int dtype, const GramBatch& b, int64_t n, int out_rows, int out
                                                      cps, &ks, st)
             : launch_gram_cfg<double, 1, 7, 7, 1, 32>(b, n, out_rows, out_cols, partial, partial_cap,
                                                       cps, &ks, st);
+    if (rc != SPB_OK) return rc;
+  } else if (n > 0 && gram_tile_for(b) == 88) {
+    // 88 x 88: 11 warps of 8 x 88 (1 x 11 m8n8 tiles each)
+    const int rc =
+        dtype == SPB_F32
+            ? launch_gram_cfg<float, 1, 11, 11, 1, 32>(b, n, out_rows, out_cols, partial, partial_cap,
+                                                       1, &ks, st)
+            : launch_gram_cfg<double, 1, 11, 11, 1, 32>(b, n, out_rows, out_cols, partial,
+                                                        partial_cap, 1, &ks, st);
     if (rc != SPB_OK) return rc;
   } else if (n > 0 && gram_tile_for(b) != 64) {
     // 112 x 112: 7 x 2 warps of 16 x 56 (2 x 7 m8n8 tiles each)
