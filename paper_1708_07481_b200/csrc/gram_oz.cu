@@ -32,9 +32,9 @@ int oz_sum_splits(const double* part, int ks, int64_t stride, int rows, int cols
 
 namespace {
 
-constexpr int OZ_S = 6;          // digits per value
+constexpr int OZ_S = 5;          // digits per value (2^-35 of the column maxima)
 constexpr int OZ_M = 128;        // UMMA M (columns of U per tile)
-constexpr int OZ_N = 80;         // UMMA N (columns of V per tile); OZ_S * OZ_N <= 512 TMEM columns
+constexpr int OZ_N = 96;         // UMMA N (columns of V per tile); OZ_S * OZ_N <= 512 TMEM columns
 constexpr int OZ_KB = 32;        // rows per k-block (one UMMA K step for 8-bit operands)
 constexpr int OZ_KS = 4;         // pipeline stages
 constexpr int OZ_MAXROWS = 16384;  // rows per CTA: 6 pairs x 127^2 x 16384 < 2^31

@@ -59,8 +59,8 @@ def test_fp64_mode_gram():
                                    (40000, 176, 352), (70000, 324, 324), (300, 8, 8), (77, 3, 5),
                                    (33000, 130, 90)])
 def test_ozaki_int8_gram_accuracy(n, p, q):
-    """spb_gram mode 2: int8 tcgen05 with six 7-bit digits per value and exact int32
-    sums (error O(2^-42) of the column maxima per product)."""
+    """spb_gram mode 2: int8 tcgen05 with five signed 7-bit digits per value and exact
+    int32 sums (error O(2^-35) of the column maxima per product)."""
     rng = np.random.default_rng(n + 7 * p + q)
     u = rng.standard_normal((n, p)).astype(np.float32)
     v = rng.standard_normal((n, q)).astype(np.float32)
@@ -73,8 +73,45 @@ def test_ozaki_int8_gram_accuracy(n, p, q):
         assert np.all(np.isfinite(g)) and np.all(g[:, 0] == 0.0)
         return (np.abs(g - exact) / np.maximum(scale, 1e-300)).max()
 
-    assert rel_err(u, v) < 1e-12
+    assert rel_err(u, v) < 1e-10
     # one entry 1e3 x larger per column of U: the shared column scale costs
     # ~10 bits of the other entries' digits (the scheme's known dynamic-range cost)
     u[5, :] *= 1e3
-    assert rel_err(u, v) < 1e-9
+    assert rel_err(u, v) < 1e-7
+
+
+def test_ozaki_rr_grams_track_dmma_in_the_solver():
+    """The solver's Rayleigh-Ritz Grams on the Ozaki int8 path (default for C3/C4-sized
+    bases) follow the float64 DMMA path: same iteration count, Ritz values within 1e-6
+    relative, residual histories within 0.01 in log10, labels agree."""
+    import os
+
+    import paper_1708_07481_b200 as spb
+    from paper_1708_07481_b200.dcsbm import DcsbmSpec, generate_dcsbm
+
+    spec = DcsbmSpec(n=60000, blocks=20, arcs=1_200_000, alpha=3.0, ratio=5.0, seed=4)
+    e, truth = generate_dcsbm(spec)
+    g = spb.from_edges(e, spec.n)
+    l = spb.block_size_for(spec.blocks)
+    x0 = np.random.default_rng(4).standard_normal((spec.n, l))
+    out = {}
+    old = os.environ.get("SPB_GRAM")
+    try:
+        for mode in ("dmma", "oz"):
+            os.environ["SPB_GRAM"] = mode
+            hist = []
+            part, st, _ = spb.partition_static(
+                g, spb.SolverConfig(block_size=l, tol=1e-12, max_iter=12, seed=4), k_expected=spec.blocks,
+                fix_k=True, x0=x0, callback=lambda it, th, nr: hist.append(nr[:spec.blocks].max()))
+            out[mode] = (part.labels, st, np.array(hist))
+    finally:
+        if old is None:
+            os.environ.pop("SPB_GRAM", None)
+        else:
+            os.environ["SPB_GRAM"] = old
+    (la, sa, ha), (lb, sb, hb) = out["dmma"], out["oz"]
+    assert sa.iterations == sb.iterations
+    rel = np.abs(sa.eigenvalues - sb.eigenvalues) / np.maximum(np.abs(sa.eigenvalues), 1e-6 * sa.eigenvalues.max())
+    assert rel.max() < 1e-6, rel.max()
+    assert np.abs(np.log10(ha) - np.log10(hb)).max() < 0.01
+    assert spb.partition_match(spb.contingency(la, lb)) > 0.999
