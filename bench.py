@@ -76,24 +76,43 @@ class ClockSampler:
         self.index = index
         self.proc = None
         self.lines = []
+        self.t0 = self.t1 = None
 
-    def __enter__(self):
+    def start(self):
+        """Start nvidia-smi ahead of the timed region and wait for its first sample:
+        its start-up (NVML init, driver locks) stalled the solver's per-iteration
+        synchronisations by tens of ms when it overlapped the timed steps."""
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.FIELDS}",
-                 "--format=csv,noheader,nounits", "-lms", "200"],
+                 "--format=csv,noheader,nounits", "-lms", "100"],
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.t = threading.Thread(target=self._read, daemon=True)
             self.t.start()
+            deadline = time.time() + 20
+            while not self.lines and time.time() < deadline and self.proc.poll() is None:
+                time.sleep(0.01)
         except (OSError, FileNotFoundError):
             self.proc = None
         return self
 
     def _read(self):
         for line in self.proc.stdout:
-            self.lines.append(line.strip())
+            self.lines.append((time.time(), line.strip()))
+
+    def __enter__(self):
+        if self.proc is None:
+            self.start()
+        self.t0 = time.time()
+        return self
 
     def __exit__(self, *exc):
+        self.t1 = time.time()
+        # one more sample after the region, then stop
+        deadline = time.time() + 0.5
+        n = len(self.lines)
+        while len(self.lines) == n and time.time() < deadline:
+            time.sleep(0.01)
         if self.proc is not None:
             self.proc.terminate()
             try:
@@ -104,7 +123,15 @@ class ClockSampler:
     def summary(self):
         sm, mx, reasons = [], [], set()
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for ln in self.lines:
+        # samples inside the timed region, plus the last one before and the first after
+        # it (a 100 ms period can fall entirely around a short region)
+        lines = self.lines
+        if self.t0 is not None and self.t1 is not None and lines:
+            inside = [x for x in lines if self.t0 <= x[0] <= self.t1]
+            before = [x for x in lines if x[0] < self.t0][-1:]
+            after = [x for x in lines if x[0] > self.t1][:1]
+            lines = before + inside + after
+        for _, ln in lines:
             parts = [p.strip() for p in ln.split(",")]
             if len(parts) < 9:
                 continue
@@ -320,6 +347,7 @@ def run_ours(args):
         stats.append(st.solve_stats)
         return labels, st
 
+    clk = ClockSampler(local).start()  # running (and initialised) before the timed steps
     for _ in range(args.warmup):
         step_device()
     torch.cuda.synchronize()
@@ -330,7 +358,7 @@ def run_ours(args):
         dist.barrier()
     torch.cuda.synchronize()
     labels = None
-    with ClockSampler(local) as clk:
+    with clk:
         for i in range(args.steps):
             flush.zero_()
             ev[i][0].record()
@@ -432,7 +460,7 @@ def run_ours(args):
                     "d2h_bytes_per_step": int(4 * spec.n + 16 * l)},
             "gpu_launches": int(launches_per_step * args.steps) if launches_per_step is not None else None,
             "kernel_shares": shares,
-            "clocks": clk.summary(),
+            "clocks": clk.summary(), "step_ms": [round(x, 3) for x in step_ms],
             "partition_seconds": t_ms / args.steps / 1e3,
             "e2e_partition_seconds": sum(e2e_times) / args.steps,
             "quality": {"PM_vs_truth": pm},

@@ -2732,6 +2732,8 @@ __global__ void invit(const double* __restrict__ d_g, const double* __restrict__
   const double tnorm = fmax(tn, DBL_MIN);
   const double ctol = 1e-8 * tnorm;
   if (j0 > 0 && theta[j0] - theta[j0 - 1] <= ctol) return;  // not a cluster head
+  // use_smem == 2: isolated eigenvalues were solved by twisted_vec
+  if (use_smem == 2 && !(j0 + 1 < nev && theta[j0 + 1] - theta[j0] <= ctol)) return;
   auto at = [&](int a2, int i) -> double& { return scratch[a2 * m + i]; };
   const double pert = kEps64 * tnorm;
   double lam_prev = -DBL_MAX;
@@ -2839,6 +2841,138 @@ __global__ void invit(const double* __restrict__ d_g, const double* __restrict__
     }
     for (int i = 0; i < m; ++i) Y[(size_t)i * ldy + j] = at(4, i);
   }
+}
+
+// Eigenvectors of T (d, e) for isolated eigenvalues by one twisted factorization
+// (the core of LAPACK's dlar1v): T - lam I = L D+ L' = U D- U' (stationary qd, lane 0
+// forward and lane 1 backward in parallel), twist index r = argmin |gamma_r| with
+// gamma_r = D+_r + D-_r - (d_r - lam), then z_r = 1, z_i = -(e_i / D+_i) z_{i+1} below
+// and z_i = -(e_{i-1} / D-_i) z_{i-1} above (again one lane each), normalised. With
+// bisection-accurate lam the residual is O(eps ||T||) after this single solve (two
+// serial sweeps instead of invit's LU + two inverse iterations). Eigenvalues within
+// ctol = 1e-8 ||T|| of a neighbour are left to invit (MGS inside the cluster).
+__global__ void __launch_bounds__(32)
+twisted_vec(const double* __restrict__ d_g, const double* __restrict__ e_g, int m, int nev,
+            const double* __restrict__ theta, double* __restrict__ Y, int ldy,
+            const SmallStatus* status) {
+  extern __shared__ double tws[];
+  if (status && (status->nonfinite || status->not_pd)) return;
+  const int j = blockIdx.x;
+  if (j >= nev) return;
+  const int lane = threadIdx.x & 31;
+  if (m == 1) {
+    if (lane == 0) Y[j] = 1.0;
+    return;
+  }
+  double* d = tws;           // m
+  double* e = d + m;         // m (e[m-1] = 0)
+  double* rp = e + m;        // e_i / D+_i
+  double* rm = rp + m;       // e_{i-1} / D-_i
+  double* gp = rm + m;       // D+_i
+  double* gm = gp + m;       // D-_i
+  double* z = gm + m;        // vector
+  double tn = 0.0, e2max = 0.0;
+  for (int i = lane; i < m; i += 32) {
+    const double di = d_g[i], ei = i + 1 < m ? e_g[i] : 0.0;
+    d[i] = di;
+    e[i] = ei;
+    tn = fmax(tn, fabs(di) + (i > 0 ? fabs(e_g[i - 1]) : 0.0) + fabs(ei));
+    e2max = fmax(e2max, ei * ei);
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    tn = fmax(tn, __shfl_xor_sync(0xffffffffu, tn, o));
+    e2max = fmax(e2max, __shfl_xor_sync(0xffffffffu, e2max, o));
+  }
+  const double tnorm = fmax(tn, DBL_MIN);
+  const double ctol = 1e-8 * tnorm;
+  const double lam = theta[j];
+  if ((j > 0 && lam - theta[j - 1] <= ctol) || (j + 1 < nev && theta[j + 1] - lam <= ctol))
+    return;  // clustered: invit
+  const double pivmin = DBL_MIN * fmax(1.0, e2max);
+  __syncwarp();
+  if (lane == 0) {
+    double D = d[0] - lam;
+    for (int i = 0; i + 1 < m; ++i) {
+      if (fabs(D) < pivmin) D = -pivmin;
+      gp[i] = D;
+      const double r = e[i] / D;
+      rp[i] = r;
+      D = (d[i + 1] - lam) - e[i] * r;
+    }
+    gp[m - 1] = D;
+  } else if (lane == 1) {
+    double D = d[m - 1] - lam;
+    for (int i = m - 1; i > 0; --i) {
+      if (fabs(D) < pivmin) D = -pivmin;
+      gm[i] = D;
+      const double r = e[i - 1] / D;
+      rm[i] = r;
+      D = (d[i - 1] - lam) - e[i - 1] * r;
+    }
+    gm[0] = D;
+  }
+  __syncwarp();
+  // twist index: smallest |gamma_r| (lowest r on ties)
+  double best = DBL_MAX;
+  int br = 0;
+  for (int r = lane; r < m; r += 32) {
+    const double g = fabs(gp[r] + gm[r] - (d[r] - lam));
+    if (g < best) {
+      best = g;
+      br = r;
+    }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const double ob = __shfl_xor_sync(0xffffffffu, best, o);
+    const int orr = __shfl_xor_sync(0xffffffffu, br, o);
+    if (ob < best || (ob == best && orr < br)) {
+      best = ob;
+      br = orr;
+    }
+  }
+  // the two halves from z_r = 1, with power-of-two rescaling so neither overflows;
+  // each lane tracks its exponent and the halves are reconciled afterwards
+  int ex = 0;
+  if (lane == 0) {
+    double zc = 1.0;
+    z[br] = 1.0;
+    for (int i = br - 1; i >= 0; --i) {
+      zc = -rp[i] * zc;
+      if (fabs(zc) > 0x1p400) {  // rescale this half (entries i+1 .. br)
+        for (int q = i + 1; q <= br; ++q) z[q] = ldexp(z[q], -400);
+        zc = ldexp(zc, -400);
+        ex += 400;
+      }
+      z[i] = zc;
+    }
+  } else if (lane == 1) {
+    double zc = 1.0;
+    for (int i = br + 1; i < m; ++i) {
+      zc = -rm[i] * zc;
+      if (fabs(zc) > 0x1p400) {  // rescale entries br+1 .. i-1 (z[br] belongs to lane 0)
+        for (int q = br + 1; q < i; ++q) z[q] = ldexp(z[q], -400);
+        zc = ldexp(zc, -400);
+        ex += 400;
+      }
+      z[i] = zc;
+    }
+  }
+  const int ex0 = __shfl_sync(0xffffffffu, ex, 0), ex1 = __shfl_sync(0xffffffffu, ex, 1);
+  __syncwarp();
+  // common scale 2^-max(ex): the half with the smaller exponent is scaled down
+  const int emax = max(ex0, ex1);
+  double ss = 0.0;
+  for (int i = lane; i < m; i += 32) {
+    const int ei = i <= br ? ex0 : ex1;
+    const double v = ldexp(z[i], ei - emax);
+    z[i] = v;
+    ss = fma(v, v, ss);
+  }
+  ss = warp_sum(ss);
+  const double inv = 1.0 / sqrt(ss);
+  for (int i = lane; i < m; i += 32) Y[(size_t)i * ldy + j] = z[i] * inv;
 }
 
 // Z = Q Y with Q = H_0 H_1 ... H_{m-3}, applied in blocks of 32 reflectors
@@ -3386,8 +3520,13 @@ int sygv_enqueue(const double* ga, const double* gb, int ldg, int m, int nev, do
     SPB_LAUNCH_CHECK();
   }
   {
+    // SPB_INVIT_ONLY=1: inverse iteration for every eigenvalue (A/B switch)
+    static const bool invit_only = getenv("SPB_INVIT_ONLY") != nullptr;
+    if (!invit_only)
+      twisted_vec<<<nev, 32, 7 * sizeof(double) * (size_t)m, st>>>(w.d, w.e, m, nev, theta, w.Y,
+                                                                   nev, status);
     invit<<<nev, 32, 8 * sizeof(double) * (size_t)m, st>>>(w.d, w.e, m, nev, theta, w.Y, nev,
-                                                           nullptr, 1, status);
+                                                           nullptr, invit_only ? 1 : 2, status);
   }
   SPB_LAUNCH_CHECK();
   SPB_CUDA(cudaStreamWaitEvent(st, side->join, 0));
