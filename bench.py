@@ -85,7 +85,7 @@ class ClockSampler:
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.FIELDS}",
-                 "--format=csv,noheader,nounits", "-lms", "100"],
+                 "--format=csv,noheader,nounits", "-lms", "250"],
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.t = threading.Thread(target=self._read, daemon=True)
             self.t.start()
@@ -124,7 +124,7 @@ class ClockSampler:
         sm, mx, reasons = [], [], set()
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         # samples inside the timed region, plus the last one before and the first after
-        # it (a 100 ms period can fall entirely around a short region)
+        # it (a 250 ms period can fall entirely around a short region)
         lines = self.lines
         if self.t0 is not None and self.t1 is not None and lines:
             inside = [x for x in lines if self.t0 <= x[0] <= self.t1]
