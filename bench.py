@@ -25,6 +25,7 @@ numpy + scipy, as the reference itself) on the host cores, same workload.
 from __future__ import annotations
 
 import argparse
+import gc
 import json
 import os
 import statistics
@@ -68,7 +69,8 @@ def workload(config: str):
 class ClockSampler:
     """nvidia-smi clocks / throttle reasons sampled during the timed region."""
 
-    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+    # no power.draw: the lighter the query, the less it can stall the solver's syncs
+    FIELDS = ("index,clocks.sm,clocks.max.sm,clocks_event_reasons.active,"
               "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
               "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
 
@@ -133,14 +135,14 @@ class ClockSampler:
             lines = before + inside + after
         for _, ln in lines:
             parts = [p.strip() for p in ln.split(",")]
-            if len(parts) < 9:
+            if len(parts) < 8:
                 continue
             try:
                 sm.append(float(parts[1]))
                 mx.append(float(parts[2]))
             except ValueError:
                 continue
-            for nm, v in zip(names, parts[5:9]):
+            for nm, v in zip(names, parts[4:8]):
                 if v.lower().startswith("active"):
                     reasons.add(nm)
         if not sm:
@@ -183,9 +185,12 @@ def run_reference(args):
             best = (th, tot)
     threads = best[0]
     times = []
+    gc.collect()
+    gc.disable()  # same collector hygiene as the GPU arm
     for _ in range(args.steps):
         _, tot, it, _ = cpu_baseline(edges, spec.n, k, l, x0, max_iter, threads)
         times.append(tot)
+    gc.enable()
     total = sum(times)
     value = max_iter * args.steps / total
     line = {
@@ -358,6 +363,10 @@ def run_ours(args):
         dist.barrier()
     torch.cuda.synchronize()
     labels = None
+    # no garbage-collector pass inside the timed steps (a gen-2 collection stalled a
+    # step's per-iteration synchronisations by a whole step's length)
+    gc.collect()
+    gc.disable()
     with clk:
         for i in range(args.steps):
             flush.zero_()
@@ -365,6 +374,7 @@ def run_ours(args):
             labels, st = step_device()
             ev[i][1].record()
         torch.cuda.synchronize()
+    gc.enable()
     if dist is not None:
         dist.barrier()
     step_ms = [a.elapsed_time(b) for a, b in ev]
@@ -397,6 +407,8 @@ def run_ours(args):
     edges_pinned = torch.from_numpy(np.ascontiguousarray(edges)).pin_memory().numpy()
     x0_host = x0.numpy() if isinstance(x0, torch.Tensor) else x0
     x0 = torch.from_numpy(np.ascontiguousarray(x0_host)).pin_memory().numpy()  # pinned host input
+    gc.collect()
+    gc.disable()
     for i in range(args.steps):
         torch.cuda.synchronize()
         t0 = time.perf_counter()
@@ -410,6 +422,7 @@ def run_ours(args):
                                                  precision=args.precision)
         torch.cuda.synchronize()
         e2e_times.append(time.perf_counter() - t0)
+    gc.enable()
     e2e_iters = st.iterations * args.steps
     e2e_value = e2e_iters / sum(e2e_times)
     if dist is not None:
