@@ -81,6 +81,8 @@ class ClockSampler:
         self.t0 = self.t1 = None
 
     def start(self):
+        if os.environ.get("SPB_BENCH_NO_SAMPLER"):  # diagnostics: no nvidia-smi at all
+            return self
         """Start nvidia-smi ahead of the timed region and wait for its first sample:
         its start-up (NVML init, driver locks) stalled the solver's per-iteration
         synchronisations by tens of ms when it overlapped the timed steps."""
