@@ -39,6 +39,10 @@ import numpy as np
 
 ROOT = Path(__file__).resolve().parent
 sys.path.insert(0, str(ROOT))
+# Load every CUDA module at context creation (a lazily loaded module first touched inside
+# the timed steps was one suspect for a sporadic 12-73 ms stall of the second C2 step;
+# eager loading made it rarer, not gone). Set before torch / the library create a context.
+os.environ.setdefault("CUDA_MODULE_LOADING", "EAGER")
 
 METRIC = "LOBPCG iters/s (end-to-end DC-SBM partition: CSR build + LOBPCG + QRCP)"
 UNIT = "iters/s"
