@@ -4,22 +4,29 @@
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
                     [--config c2] [--precision float32]
 
-Workload (BASELINE.json configs[1], the metric's N=1 configuration): DC-SBM
-N=50,000, B=44 (Dirichlet alpha=1, within:between 2:1, power-law degrees
-10..100), 1M directed arcs, seeded synthetic input (the Graph Challenge
-datasets are absent); block size l = block_size_for(44) = 49; 20 LOBPCG
-iterations from the seeded N(0,1) init (tol 1e-12 so exactly 20 run), then
-QRCP assignment with k = 44 — partition_static(..., fix_k=True).
+Workload (N=1 headline): BASELINE.json configs[2] (C3), the largest config that
+fits one GPU — DC-SBM N=500,000, B=98 (Dirichlet alpha=3, within:between 5:1,
+power-law degrees 10..100), 10M directed arcs, seeded synthetic input (the Graph
+Challenge datasets are absent); l = block_size_for(98) = 108; LOBPCG from the
+seeded N(0,1) init under the SURVEY §8(d) "10x" stop rule (tol = 0.1 r0 / scale,
+the value the reference itself produced, tests/golden/large_c3.npz), at most 30
+iterations; QRCP assignment with k = 98 — partition_static(..., fix_k=True).
+--config c1|c2|c4 select the other configs; with N > 1 GPUs C3/C4 run one
+partition row-sharded over the ranks (strong scaling).
 
 One step = one whole partition: device CSR build from the arc list, LOBPCG
-(setup RR, 20 iterations, polish), QRCP assignment -> labels.
-``value`` = LOBPCG iterations/s over the timed steps with the arc list and x0
-already in HBM (labels left on the device); ``e2e`` = the same metric through
-the public API from host numpy arrays to host labels (H2D and D2H inside).
+(setup RR, iterations, polish), QRCP assignment -> labels.
+``value`` = LOBPCG iterations/s over the timed steps (iterations / whole-partition
+time, so setup, polish and assignment count against it) with the arc list and x0
+already in HBM (labels left on the device); ``e2e`` = the same metric through the
+public API from plain pageable numpy arrays to host labels (H2D and D2H inside).
 L2 is flushed (256 MiB write) between timed steps, outside the step events.
 
---impl reference: the CPU restatement of the reference algorithm (oracle/,
-numpy + scipy, as the reference itself) on the host cores, same workload.
+--impl reference: the UNMODIFIED reference package (specpart 0.1.0, installed into
+baseline/_ref) on the host cores with all BLAS threads: from_edges +
+partition_static on the same input; one step = one LOBPCG iteration of one solve,
+W warm-up iterations then K timed ones from the reference's own per-iteration
+callback (a whole C3 partition per step would not fit the arm's time limit).
 """
 
 from __future__ import annotations
@@ -157,61 +164,135 @@ class ClockSampler:
                 "samples": len(sm)}
 
 
-def cpu_baseline(edges, n, k, l, x0, max_iter, threads=None):
-    """The CPU restatement (oracle/) on the host cores: bounded sample."""
-    import oracle
+REF_DIR = ROOT / "baseline" / "_ref"
+
+
+def import_reference():
+    """The unmodified reference package installed into baseline/_ref."""
+    if str(REF_DIR) not in sys.path:
+        sys.path.insert(0, str(REF_DIR))
+    import specpart
+
+    return specpart
+
+
+class _StopSample(Exception):
+    pass
+
+
+def reference_sample(edges, n, k, l, x0, tol, iters, threads):
+    """Time the REAL reference (specpart from baseline/_ref) on the host cores.
+
+    ``from_edges`` + ``partition_static(..., fix_k=True, x0=x0)`` exactly as the
+    reference mapping, stopped from its own per-iteration callback
+    (lobpcg.py:348-349) once ``iters`` basis expansions have run, so one bounded sample
+    fits the driver's arm limit. Returns (stamps, setup_s): stamps[j] is the callback
+    time after j expansions (stamps[0] = end of setup).
+    """
     from threadpoolctl import threadpool_limits
 
-    threads = threads or os.cpu_count() or 1
+    sp = import_reference()
+    from specpart import graph as rg
+    from specpart import lobpcg as rl
+    from specpart import spectral as rs
+
     stamps = []
+
+    def cb(it, theta, norms):
+        stamps.append(time.perf_counter())
+        if it >= iters:
+            raise _StopSample()
+
+    orig = rs.lobpcg_solve
+
+    def spy(op, x, c, precond=None, n_converge=None, callback=None):
+        return orig(op, x, c, precond=precond, n_converge=n_converge, callback=cb)
+
     with threadpool_limits(threads):
         t0 = time.perf_counter()
-        oracle.partition_static_ref(
-            edges, n, oracle.SolverCfg(block_size=l, tol=1e-12, max_iter=max_iter, seed=0),
-            k_expected=k, x0=x0, callback=lambda it, t, r: stamps.append(time.perf_counter()))
-        total = time.perf_counter() - t0
-    iters = len(stamps) - 1
-    rate = iters / (stamps[-1] - stamps[0]) if iters > 0 else float("nan")
-    return rate, total, iters, threads
+        rs.lobpcg_solve = spy
+        try:
+            g = rg.from_edges(edges, n)
+            rs.partition_static(g, rl.SolverConfig(block_size=l, tol=tol, max_iter=max(iters, 1),
+                                                   seed=0), k_expected=k, fix_k=True, x0=x0)
+        except _StopSample:
+            pass
+        finally:
+            rs.lobpcg_solve = orig
+    assert sp.__version__ == "0.1.0"
+    return stamps, stamps[0] - t0
+
+
+def config_dict(args, spec, l, k, max_iter, tol):
+    """The workload, identical in both arms' lines (no implementation keys)."""
+    world = args.gpus
+    if args.config in ("c3", "c4"):
+        stop = f"10x residual reduction (tol={tol:.6g} relative to scale), at most {max_iter} iterations"
+        par = "single GPU" if world == 1 else f"rows sharded over {world} GPUs (NCCL)"
+    else:
+        stop = f"exactly {max_iter} iterations (tol=1e-12)"
+        par = "single GPU" if world == 1 else f"{world} independent replicas"
+    return {"workload": f"{args.config}: DC-SBM n={spec.n} B={spec.blocks} arcs={spec.arcs}, "
+                        f"l={l}, LOBPCG ({stop}), QRCP k={k}",
+            "n": spec.n, "blocks": spec.blocks, "arcs": spec.arcs, "block_size": l,
+            "max_iter": max_iter, "tol": tol, "stop_rule": stop, "parallelism": par,
+            "l2": "GPU arm: 256 MiB L2 flush between timed steps; CPU arm: n/a"}
+
+
+def golden_tol(config):
+    """The 10x-rule tolerance the reference itself produced (tests/golden/large_c3.npz,
+    large_c4full.npz), so both arms stop on the same number; None without a fixture."""
+    name = {"c3": "large_c3.npz", "c4": "large_c4full.npz"}.get(config)
+    f = ROOT / "tests" / "golden" / name if name else None
+    if f is None or not f.exists():
+        return None
+    with np.load(f) as d:
+        return float(d[f"{config}_s0/tol"])
 
 
 def run_reference(args):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return 0
+    try:
+        import_reference()
+    except ImportError as e:
+        print(json.dumps({"impl": "reference", "unavailable": f"specpart not installed in "
+                                                              f"baseline/_ref ({e})"}), flush=True)
+        return 0
     spec, edges, truth, k, l, x0, max_iter = workload(args.config)
-    # warm-up steps also pick the faster BLAS thread count (1 vs all cores):
-    # OpenBLAS' threaded TN dgemm is slower than serial at small widths (SURVEY.md §3)
-    cands = [os.cpu_count() or 1, 1]
-    best = None
-    for i in range(max(1, args.warmup)):
-        th = cands[i % 2] if args.warmup >= 2 else cands[0]
-        r, tot, it, _ = cpu_baseline(edges, spec.n, k, l, x0, max_iter, th)
-        if best is None or tot < best[1]:
-            best = (th, tot)
-    threads = best[0]
-    times = []
+    tol = golden_tol(args.config) or 1e-12
+    threads = os.cpu_count() or 1
+    # One "step" = one LOBPCG iteration of the reference's own solve: W warm-up
+    # iterations then K timed ones, read from the reference's per-iteration callback.
+    w, k_steps = max(args.warmup, 0), args.steps
     gc.collect()
-    gc.disable()  # same collector hygiene as the GPU arm
-    for _ in range(args.steps):
-        _, tot, it, _ = cpu_baseline(edges, spec.n, k, l, x0, max_iter, threads)
-        times.append(tot)
+    gc.disable()
+    stamps, setup_s = reference_sample(edges, spec.n, k, l, x0, tol, w + k_steps, threads)
     gc.enable()
-    total = sum(times)
-    value = max_iter * args.steps / total
+    done = len(stamps) - 1  # expansions that ran (the stop rule may end the solve early)
+    timed = max(0, done - w)
+    if timed == 0:
+        w, timed = 0, done
+    total = stamps[w + timed] - stamps[w]
+    value = timed / total if total > 0 else float("nan")
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": 1e3 * total / args.steps, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": f"{args.config}: DC-SBM n={spec.n} B={spec.blocks} arcs={spec.arcs}, "
-                               f"l={l}, {max_iter} LOBPCG iterations, QRCP k={k}",
-                   "n": spec.n, "blocks": spec.blocks, "arcs": spec.arcs, "block_size": l,
-                   "iterations": max_iter},
+        "warmup": args.warmup, "ms_per_step": 1e3 * total / max(timed, 1), "higher_is_better": True,
+        "scaling": "strong" if args.config in ("c3", "c4") else "weak", "vs_baseline": None,
+        "dtype": "f64", "data": "synthetic",
+        "config": config_dict(args, spec, l, k, max_iter, tol),
         "impl": "reference",
-        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port",
-                         "sample": f"full {args.config} partition per step (oracle/ numpy+scipy "
-                                   f"restatement of specpart), {args.steps} steps"},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "reference",
+                         "sample": f"specpart 0.1.0 (unmodified, baseline/_ref) from_edges + "
+                                   f"partition_static on the {args.config} input, one solve: "
+                                   f"{w} warm-up + {timed} timed LOBPCG iterations from its "
+                                   f"callback; setup {setup_s:.1f} s excluded"},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "reference_timing": {"setup_s": setup_s, "per_iteration_s": total / max(timed, 1),
+                             "iterations_timed": timed, "blas_threads": threads,
+                             "note": "setup = from_edges + LaplacianOperator + orthonormalize + "
+                                     "SpMM + initial Rayleigh-Ritz (until the it=0 callback)"},
     }
     print(json.dumps(line), flush=True)
     return 0
@@ -262,7 +343,7 @@ def gram_roofline(n, l, precision):
     """Rayleigh-Ritz Gram [X R P]'[X R P] (n x 3l, solver layout) timed alone with
     CUDA events on the launching stream, on the path the solver takes for this size:
     float64 products on the DMMA pipe, or (float32 storage, n * ld >= 5e7: C3, C4)
-    the Ozaki int8 tcgen05 Gram (column maxima + digit packing + 21 int8 MMAs per
+    the Ozaki int8 tcgen05 Gram (column maxima + digit packing + 15 int8 MMAs per
     product, timed together)."""
     import torch
 
@@ -295,18 +376,29 @@ def gram_roofline(n, l, precision):
     torch.cuda.synchronize()
     ms = e0.elapsed_time(e1) / reps
     tflops = 2.0 * n * m * m / (ms * 1e-3) / 1e12
-    peak = 37.0  # B200 FP64 tensor (DMMA) spec per GPU; no measured FP64 peak in MEASURED_PEAKS.json
+    pk = {}
+    pf = ROOT / "profiles" / "r02" / "peaks_tensor.json"
+    if pf.exists():
+        pk = json.loads(pf.read_text())
+    fp64 = pk.get("fp64_tflops")
+    fp64_peak, fp64_kind = (fp64, "measured (cuBLAS DGEMM 8192^3, profiles/r02/peaks_tensor.json)") \
+        if fp64 else (37.0, "spec")
     if oz:
-        tops = 21 * 2.0 * n * m * m / (ms * 1e-3) / 1e12
-        return {"bound": "tensor (int8 tcgen05, Ozaki splitting)", "achieved": tflops, "peak": peak,
-                "unit": "TFLOP/s (float64-equivalent, against the FP64 DMMA spec)",
-                "frac": tflops / peak, "peak_kind": "spec", "shape": f"{n}x{m} -> {m}x{m}",
-                "ms_per_launch": ms, "kernel": "spb::gram_oz_kernel (+ oz_colmax, oz_pack)",
-                "int8": {"achieved": tops, "peak": 4500.0, "unit": "TOPS (21 int8 MMAs per product)",
-                         "frac": tops / 4500.0, "peak_kind": "spec (dense int8)"}}
-    return {"bound": "tensor (fp64 DMMA)", "achieved": tflops, "peak": peak, "unit": "TFLOP/s",
-            "frac": tflops / peak, "peak_kind": "spec", "shape": f"{n}x{m} -> {m}x{m}",
-            "ms_per_launch": ms, "kernel": "spb::gram_dmma"}
+        # OZ_S = 5 digits per value; the digit products with i + j <= OZ_S + 1 ... are the
+        # 15 int8 MMAs per output tile and k-block the kernel issues (gram_oz.cu, OZ_S)
+        tops = 15 * 2.0 * n * m * m / (ms * 1e-3) / 1e12
+        i8 = pk.get("int8_tops")
+        i8_peak, i8_kind = (i8, "measured (torch._int_mm 8192^3)") if i8 else (4500.0, "spec (dense int8)")
+        return {"bound": "tensor", "pipe": "int8 tcgen05 (Ozaki splitting)", "achieved": tops,
+                "peak": i8_peak, "unit": "TOPS (15 int8 MMAs per product)", "frac": tops / i8_peak,
+                "peak_kind": i8_kind, "shape": f"{n}x{m} -> {m}x{m}", "ms_per_launch": ms,
+                "kernel": "spb::gram_oz_kernel (+ oz_colmax, oz_pack)",
+                "fp64_equivalent": {"achieved": tflops, "unit": "TFLOP/s", "vs_fp64_peak": tflops / fp64_peak,
+                                    "fp64_peak": fp64_peak, "fp64_peak_kind": fp64_kind,
+                                    "note": "speed-up over the FP64 pipe, not a roofline fraction"}}
+    return {"bound": "tensor", "pipe": "fp64 DMMA", "achieved": tflops, "peak": fp64_peak,
+            "unit": "TFLOP/s", "frac": tflops / fp64_peak, "peak_kind": fp64_kind,
+            "shape": f"{n}x{m} -> {m}x{m}", "ms_per_launch": ms, "kernel": "spb::gram_dmma"}
 
 
 def run_ours(args):
@@ -332,7 +424,8 @@ def run_ours(args):
     x0_d = torch.from_numpy(x0).to(dev)
     tol = 1e-12
     if args.config in ("c3", "c4"):
-        tol = ten_x_tol(spb, spb.from_edges((src, dst), spec.n), x0_d, l, k, args.precision)
+        tol = golden_tol(args.config) or ten_x_tol(spb, spb.from_edges((src, dst), spec.n), x0_d,
+                                                   l, k, args.precision)
     cfg = spb.SolverConfig(block_size=l, tol=tol, max_iter=max_iter, seed=0)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
     stats = []
@@ -410,15 +503,15 @@ def run_ours(args):
     # e2e: public API from host arrays to host labels
     e2e_times = []
     part = None
-    edges_pinned = torch.from_numpy(np.ascontiguousarray(edges)).pin_memory().numpy()
-    x0_host = x0.numpy() if isinstance(x0, torch.Tensor) else x0
-    x0 = torch.from_numpy(np.ascontiguousarray(x0_host)).pin_memory().numpy()  # pinned host input
+    # plain pageable numpy inputs, as a drop-in caller holds them
+    edges_host = np.array(edges, dtype=np.int64, copy=True)
+    x0 = np.array(x0.numpy() if isinstance(x0, torch.Tensor) else x0, dtype=np.float64, copy=True)
     gc.collect()
     gc.disable()
     for i in range(args.steps):
         torch.cuda.synchronize()
         t0 = time.perf_counter()
-        g = spb.from_edges(edges_pinned, spec.n)
+        g = spb.from_edges(edges_host, spec.n)
         if sharded:
             part, st, gap = partition_static_sharded(g, cfg, k, fix_k=True, x0=x0,
                                                      precision=args.precision,
@@ -443,23 +536,35 @@ def run_ours(args):
         pm = spb.partition_match(spb.contingency(truth, part.labels if hasattr(part, "labels") else part))
         cpu = None
         if world == 1 and not args.no_cpu_baseline:
-            rate, tot, it, cores = cpu_baseline(edges, spec.n, k, l, x0, args.cpu_iters)
-            cpu = {"value": rate, "unit": UNIT, "cores": cores, "kind": "port",
-                   "sample": f"{args.config} partition_static with max_iter={args.cpu_iters} "
-                             f"(oracle/ numpy+scipy restatement); rate = iterations between "
-                             f"first and last callback / elapsed ({tot:.1f} s total)"}
+            threads = os.cpu_count() or 1
+            try:
+                stamps, setup_s = reference_sample(edges, spec.n, k, l, x0, tol, args.cpu_iters,
+                                                   threads)
+                done = len(stamps) - 1
+                rate = done / (stamps[-1] - stamps[0]) if done > 0 else float("nan")
+                cpu = {"value": rate, "unit": UNIT, "cores": threads, "kind": "reference",
+                       "sample": f"specpart 0.1.0 (unmodified, baseline/_ref) on the "
+                                 f"{args.config} input: {done} LOBPCG iterations after a "
+                                 f"{setup_s:.1f} s setup, rate from its per-iteration callback"}
+            except ImportError as e:
+                cpu = {"value": None, "unit": UNIT, "cores": threads, "kind": "reference",
+                       "sample": f"unavailable: {e}"}
+        quality = {"PM_vs_truth": pm}
+        gf = ROOT / "tests" / "golden" / f"large_{args.config}.npz"
+        if args.config == "c3" and gf.exists():
+            with np.load(gf) as d:
+                ref_lab = d["c3_s0/labels"].astype(np.int64)
+                quality["reference_iterations"] = int(d["c3_s0/iterations"])
+            ours_lab = part.labels if hasattr(part, "labels") else part.cpu().numpy()
+            quality["PM_vs_reference_labels"] = spb.partition_match(spb.contingency(ref_lab, ours_lab))
+            quality["iterations"] = int(st.iterations)
         out = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": t_ms / args.steps, "higher_is_better": True,
-            "scaling": "strong" if sharded else "weak", "vs_baseline": None,
+            "scaling": "strong" if args.config in ("c3", "c4") else "weak", "vs_baseline": None,
             "dtype": "f32" if args.precision == "float32" else "f64", "data": "synthetic",
-            "config": {"workload": f"{args.config}: DC-SBM n={spec.n} B={spec.blocks} "
-                                   f"arcs={spec.arcs}, l={l}, {max_iter} LOBPCG iterations, QRCP k={k}",
-                       "n": spec.n, "blocks": spec.blocks, "arcs": spec.arcs, "block_size": l,
-                       "iterations": max_iter, "precision": args.precision,
-                       "l2": "flushed between steps (256 MiB write)",
-                       "tol": tol,
-                       "parallelism": ("row-sharded" if sharded else "replicas") if world > 1 else "single"},
+            "config": config_dict(args, spec, l, k, max_iter, tol),
+            "precision": args.precision,
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": (achieved / peak) if achieved else None, "traffic": traffic,
                          "kernel": "spb::spmm_vb (Laplacian SpMM)", "peak_kind": peak_kind,
@@ -475,14 +580,14 @@ def run_ours(args):
                                   "kernel_shares (latency-bound small dense solves dominate at C1/C2)")},
             "cpu_baseline": cpu,
             "e2e": {"value": e2e_value, "unit": UNIT,
-                    "h2d_bytes_per_step": int(edges.nbytes + x0.nbytes),
+                    "h2d_bytes_per_step": int(edges_host.nbytes + x0.nbytes),
                     "d2h_bytes_per_step": int(4 * spec.n + 16 * l)},
             "gpu_launches": int(launches_per_step * args.steps) if launches_per_step is not None else None,
             "kernel_shares": shares,
             "clocks": clk.summary(), "step_ms": [round(x, 3) for x in step_ms],
             "partition_seconds": t_ms / args.steps / 1e3,
             "e2e_partition_seconds": sum(e2e_times) / args.steps,
-            "quality": {"PM_vs_truth": pm},
+            "quality": quality,
         }
         print(json.dumps(out), flush=True)
     if dist is not None:
@@ -497,9 +602,9 @@ def main():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    ap.add_argument("--config", default="c2", choices=["c1", "c2", "c3", "c4"])
+    ap.add_argument("--config", default="c3", choices=["c1", "c2", "c3", "c4"])
     ap.add_argument("--precision", default="float32", choices=["float32", "float64"])
-    ap.add_argument("--cpu-iters", type=int, default=4)
+    ap.add_argument("--cpu-iters", type=int, default=2)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
     if args.impl == "reference":

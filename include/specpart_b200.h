@@ -107,9 +107,14 @@ SPB_API int spb_gram(int dtype, int mode, const void* u, int64_t ldu, int32_t p,
 
 /* ---------------- (c)(d) LOBPCG -----------------------------------------------
  * Operator handle for the solve (graph.py:300-317 / lobpcg.py:132-151). */
-enum { SPB_OP_LAPLACIAN = 0, SPB_OP_DENSE = 1 };
+enum { SPB_OP_LAPLACIAN = 0, SPB_OP_DENSE = 1, SPB_OP_HOST = 2 };
+/* SPB_OP_HOST: any object with the reference's operator protocol (.n, .scale_hint,
+ * .apply(x, out); lobpcg.py:273, graph.py:300-317) -- out = A in, host float64
+ * row-major rows x cols; return 0 on success. The solve stays on the device; only
+ * the operator apply crosses to the host. */
+typedef int (*spb_apply_cb)(void* user, int64_t rows, int32_t cols, const double* in, double* out);
 typedef struct {
-  int kind;              /* SPB_OP_LAPLACIAN or SPB_OP_DENSE                       */
+  int kind;              /* SPB_OP_LAPLACIAN, SPB_OP_DENSE or SPB_OP_HOST          */
   int32_t n;             /* operator dimension                                     */
   const int32_t* row_ptr;/* LAPLACIAN: CSR of W (device)                           */
   const int32_t* col;
@@ -117,6 +122,8 @@ typedef struct {
   const void* deg;       /* dtype degrees                                          */
   const double* dense;   /* DENSE: device float64 n x n row-major                  */
   double scale_hint;     /* max degree (graph.py:314) / max row abs-sum (lobpcg.py:143) */
+  spb_apply_cb apply;    /* HOST: the operator's apply                             */
+  void* apply_user;      /* HOST: passed back to apply                             */
 } spb_operator;
 
 /* SolverConfig (lobpcg.py:38-81) plus the solve arguments of lobpcg_solve
@@ -147,10 +154,11 @@ SPB_API size_t spb_lobpcg_workspace(int dtype, int32_t n, int32_t l);
  * (status OK or SOLVER) the solver's X block is left in the workspace and
  * copied to vectors_out (device float64 n x l) when vectors_out != NULL;
  * theta_out/norms_out/converged_out are host arrays of length l;
- * stats_out (host int64[16], may be NULL) receives {iterations, operator applies,
- * Rayleigh-Ritz solves, drop_p rungs, rebuild rungs, final scale bits hi, lo,
- * SpMM event time (us), SpMM algorithmic bytes, SpMM columns, 0...}; the two
- * SpMM timing entries are filled when cfg->reserved has bit 0 set. */
+ * stats_out (host int64[16], may be NULL) receives {[0] iterations, [1] operator
+ * applies, [2] Rayleigh-Ritz solves, [3] drop_p rungs, [4] rebuild rungs, [5] float32
+ * orth_p re-solves, [6] 0, [7] SpMM event time (us), [8] SpMM algorithmic bytes,
+ * [9] SpMM columns, [10] final scale bits hi, [11] lo, 0...}; the SpMM timing
+ * entries are filled when cfg->reserved has bit 0 set. */
 SPB_API int spb_lobpcg_solve(const spb_operator* op, int dtype, const double* x0,
                      const spb_solver_config* cfg, spb_iter_cb cb, spb_refill_cb refill,
                      spb_precond_cb precond, void* user, void* ws, size_t ws_bytes,

@@ -23,15 +23,19 @@ LIB_PATH = Path(__file__).resolve().parent / "_lib" / "libspb200.so"
 OK, E_CONTRACT, E_DOMAIN, E_COND, E_SOLVER, E_SOLVER_NOSTATE, E_ASSIGN, E_CUDA, E_WS, E_CB, E_PARSE = range(11)
 F32, F64 = 0, 1
 CSR_DIRECTED, CSR_SYMMETRIZED, CSR_AS_SYMMETRIC = 0, 1, 2
-OP_LAPLACIAN, OP_DENSE = 0, 1
+OP_LAPLACIAN, OP_DENSE, OP_HOST = 0, 1, 2
 
 vp = C.c_void_p
 i32, i64, f64, sz = C.c_int32, C.c_int64, C.c_double, C.c_size_t
 
 
+APPLY_CB = C.CFUNCTYPE(C.c_int, vp, i64, i32, C.POINTER(f64), C.POINTER(f64))
+
+
 class Operator(C.Structure):
     _fields_ = [("kind", C.c_int), ("n", i32), ("row_ptr", vp), ("col", vp), ("val", vp),
-                ("deg", vp), ("dense", vp), ("scale_hint", f64)]
+                ("deg", vp), ("dense", vp), ("scale_hint", f64), ("apply", APPLY_CB),
+                ("apply_user", vp)]
 
 
 class Shard(C.Structure):

@@ -2,6 +2,7 @@
 #pragma once
 
 #include <cuda_runtime.h>
+#include <atomic>
 #include <cstdint>
 #include <cstdio>
 #include <string>
@@ -62,6 +63,21 @@ inline int num_sms() {
     if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess) sms = 148;
   }
   return sms;
+}
+
+// Kernel attributes (dynamic shared memory, cluster sizes) belong to a device
+// context: remember per device ordinal that they were set. Setting them twice is
+// harmless, so two threads racing here both set them before launching.
+inline uint64_t device_bit() {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  return 1ull << (dev & 63);
+}
+inline bool done_on_device(const std::atomic<uint64_t>& mask) {
+  return (mask.load(std::memory_order_acquire) & device_bit()) != 0;
+}
+inline void mark_on_device(std::atomic<uint64_t>& mask) {
+  mask.fetch_or(device_bit(), std::memory_order_release);
 }
 
 template <typename T>

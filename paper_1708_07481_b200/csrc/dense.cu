@@ -354,11 +354,11 @@ int launch_gram_cfg(GramBatch bb, int64_t n, int out_rows, int out_cols, double*
     return SPB_ERR_WORKSPACE;
   }
   const int64_t kchunk = round_up(ceil_div(std::max<int64_t>(n, 1), ks), DKT);
-  static bool attr = false;
-  if (!attr) {
+  static std::atomic<uint64_t> attr{0};
+  if (!done_on_device(attr)) {
     SPB_CUDA(cudaFuncSetAttribute(gram_dmma_t<T, MT, NT, WM, WN, DKT>,
                                   cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    attr = true;
+    mark_on_device(attr);
   }
   dim3 grid(tiles, (unsigned)ks);
   gram_dmma_t<T, MT, NT, WM, WN, DKT><<<grid, NTHR, smem, st>>>(
@@ -650,10 +650,10 @@ template <int NCG, int RG>
 void launch_update_f32(const UpdParams& p, int64_t n, cudaStream_t st) {
   constexpr int ROWS = RG * 8, COLS = NCG * 8;
   const size_t smem = sizeof(float) * (UNS * ROWS * UAP + UNS * UKT * COLS);
-  static bool attr = false;
-  if (!attr) {
+  static std::atomic<uint64_t> attr{0};
+  if (!done_on_device(attr)) {
     cudaFuncSetAttribute(update_f32<NCG, RG>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    attr = true;
+    mark_on_device(attr);
   }
   stage_coeffs<<<32, 256, 0, st>>>(p, COLS);
   update_f32<NCG, RG><<<(unsigned)ceil_div(n, ROWS), NCG * RG, smem, st>>>(p, n);
@@ -956,13 +956,13 @@ int gram_batched(int dtype, const GramBatch& b, int64_t n, int out_rows, int out
                                                       1, &ks, st);
     if (rc != SPB_OK) return rc;
   } else if (n > 0) {
-    static bool attr = false;
-    if (!attr) {
+    static std::atomic<uint64_t> attr{0};
+    if (!done_on_device(attr)) {
       SPB_CUDA(cudaFuncSetAttribute(gram_dmma<float>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     (int)kDmmaSmem));
       SPB_CUDA(cudaFuncSetAttribute(gram_dmma<double>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     (int)kDmmaSmem));
-      attr = true;
+      mark_on_device(attr);
     }
     if (dtype == SPB_F32)
       gram_dmma<float><<<grid, 128, kDmmaSmem, st>>>(b, n, kchunk, out_cols, stride, partial);

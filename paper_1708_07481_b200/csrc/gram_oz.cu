@@ -430,11 +430,11 @@ int oz_gemm(const OzOperand& A, const OzOperand& B, double* partial, size_t part
             double* out, int ldo, cudaStream_t st, bool upper = false) {
   const int p = A.cols, q = B.cols;
   if (p <= 0 || q <= 0) return SPB_OK;
-  static bool attr = false;
-  if (!attr) {
+  static std::atomic<uint64_t> attr{0};
+  if (!done_on_device(attr)) {
     SPB_CUDA(cudaFuncSetAttribute(gram_oz_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   kOzSmem));
-    attr = true;
+    mark_on_device(attr);
   }
   const int64_t nkb = A.nkb;
   OzParams P{};

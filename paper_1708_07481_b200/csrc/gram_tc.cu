@@ -370,11 +370,11 @@ int gram_tc(const float* U, int64_t ldu, int p, const float* V0, int64_t ldv0, i
             const float* V1, int64_t ldv1, int q1, int64_t n, double* partial, size_t partial_cap,
             double* out, int ldo, cudaStream_t st) {
   if (p <= 0 || q0 <= 0) return SPB_OK;
-  static bool attr = false;
-  if (!attr) {
+  static std::atomic<uint64_t> attr{0};
+  if (!done_on_device(attr)) {
     SPB_CUDA(cudaFuncSetAttribute(gram_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   kSmemBytes));
-    attr = true;
+    mark_on_device(attr);
   }
   CUtensorMap mu, mv0, mv1;
   SPB_TRY(make_map(&mu, U, n, p, ldu));

@@ -153,16 +153,15 @@ struct Driver {
   void* user;
   cudaStream_t st;
   int64_t stats[16] = {0};
-  // optional CUDA-event timing of every operator apply (cfg->reserved & 1)
-  // (events come from a process-wide pool: creating/destroying them per solve
-  // perturbed the timed steps)
+  // optional CUDA-event timing of every operator apply (cfg->reserved & 1); the
+  // events belong to this solve (created on first use, destroyed with the driver)
   bool profile = false;
   size_t ev_used = 0;
   double spmm_bytes = 0.0;
   int64_t nnz = 0;
-  static std::vector<cudaEvent_t>& event_pool() {
-    static std::vector<cudaEvent_t> pool;
-    return pool;
+  std::vector<cudaEvent_t> events;
+  ~Driver() {
+    for (cudaEvent_t e : events) cudaEventDestroy(e);
   }
   std::vector<double> h_theta, h_norms;  // last residual step
   double h_scale = 0.0;
@@ -170,9 +169,10 @@ struct Driver {
 
   int apply(const void* src, int cols, void* dst) {
     stats[1]++;
+    if (op->kind == SPB_OP_HOST) return host_apply(src, cols, dst);
     if (op->kind != SPB_OP_LAPLACIAN)
       return dense_apply(op->dense, op->n, src, w.ld, cols, dst, w.ld, w.dtype, nullptr, st);
-    std::vector<cudaEvent_t>& ev = event_pool();
+    std::vector<cudaEvent_t>& ev = events;
     if (profile) {
       while (ev.size() < ev_used + 2) {
         cudaEvent_t e;
@@ -204,9 +204,36 @@ struct Driver {
     return SPB_OK;
   }
 
+  // duck-typed operator (lobpcg.py:273): the block goes to the host as float64
+  // row-major, the caller's apply fills the image, which comes back to dst
+  int host_apply(const void* src, int cols, void* dst) {
+    if (!op->apply) {
+      set_error("host operator without an apply callback");
+      return SPB_ERR_CONTRACT;
+    }
+    std::vector<double> hin((size_t)w.n * cols), hout((size_t)w.n * cols);
+    double* d = nullptr;
+    SPB_CUDA(cudaMallocAsync((void**)&d, sizeof(double) * hin.size() + 8, st));
+    int s = copy_block(w.dtype, src, w.ld, SPB_F64, d, cols, w.n, cols, st);
+    if (s == SPB_OK) {
+      SPB_CUDA(cudaMemcpyAsync(hin.data(), d, sizeof(double) * hin.size(), cudaMemcpyDeviceToHost, st));
+      SPB_CUDA(cudaStreamSynchronize(st));
+      if (op->apply(op->apply_user, w.n, cols, hin.data(), hout.data()) != 0) {
+        cudaFreeAsync(d, st);
+        set_error("operator apply callback failed");
+        return SPB_ERR_CALLBACK;
+      }
+      SPB_CUDA(cudaMemcpyAsync(d, hout.data(), sizeof(double) * hout.size(), cudaMemcpyHostToDevice, st));
+      s = copy_block(SPB_F64, d, cols, w.dtype, dst, w.ld, w.n, cols, st);
+    }
+    cudaFreeAsync(d, st);
+    SPB_CUDA(cudaStreamSynchronize(st));
+    return s;
+  }
+
   int finish_profile() {
     if (!profile || ev_used == 0) return SPB_OK;
-    std::vector<cudaEvent_t>& ev = event_pool();
+    std::vector<cudaEvent_t>& ev = events;
     SPB_CUDA(cudaStreamSynchronize(st));
     double ms = 0.0;
     for (size_t i = 0; i < ev_used; i += 2) {
@@ -846,8 +873,8 @@ static int solve_impl(const spb_operator* op, const spb_shard* sh, int dtype, co
   d.stats[0] = d.iterations;
   uint64_t bits;
   std::memcpy(&bits, &d.h_scale, 8);
-  d.stats[5] = (int64_t)(bits >> 32);
-  d.stats[6] = (int64_t)(bits & 0xffffffffu);
+  d.stats[10] = (int64_t)(bits >> 32);
+  d.stats[11] = (int64_t)(bits & 0xffffffffu);
   if (stats_out)
     for (int i = 0; i < 16; ++i) stats_out[i] = d.stats[i];
   return s;

@@ -877,10 +877,10 @@ void launch_small_gemm(int ta, int tb, int M, int N, int K, const double* A, int
   const size_t smem = sizeof(double) * 64 * (size_t)(K | 1);
   static const int tiled = getenv("SPB_SMALL_GEMM_TILED") ? atoi(getenv("SPB_SMALL_GEMM_TILED")) : 0;
   if (!((tiled >> (ta * 2 + tb)) & 1) && smem <= 200 * 1024) {
-    static bool attr = false;
-    if (!attr) {
+    static std::atomic<uint64_t> attr{0};
+    if (!done_on_device(attr)) {
       cudaFuncSetAttribute(small_gemm_fk, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-      attr = true;
+      mark_on_device(attr);
     }
     small_gemm_fk<<<grid, 256, smem, st>>>(ta, tb, M, N, K, A, lda, B, ldb, C, ldc);
   } else {
@@ -2079,11 +2079,11 @@ bool launch_tridiag_warpcol(const double* Asrc, int m, int symmetrize, double* V
   const int R = (m + lpc - 1) / lpc;
 #define SPB_WC1(RR, LL, BB)                                                                    \
   {                                                                                            \
-    static bool attr = false;                                                                  \
-    if (!attr) {                                                                               \
+    static std::atomic<uint64_t> attr{0}; \
+    if (!done_on_device(attr)) {                                                                               \
       cudaFuncSetAttribute(tridiag_warpcol<RR, LL, BB>,                                        \
                            cudaFuncAttributeNonPortableClusterSizeAllowed, 1);                 \
-      attr = true;                                                                             \
+      mark_on_device(attr);                                                                             \
     }                                                                                          \
     cudaLaunchKernelEx(&cfg, tridiag_warpcol<RR, LL, BB>, Asrc, m, symmetrize, V, tau, d, e,   \
                        status, trace);                                                         \
@@ -2324,12 +2324,12 @@ bool launch_chol_rowwarp(const double* B, int m, double* L, double* Linv, int mo
   const dim3 ti_grid((unsigned)((m + ti_warps - 1) / ti_warps));
 #define SPB_CR(RR)                                                                               \
   {                                                                                              \
-    static bool attr = false;                                                                    \
-    if (!attr) {                                                                                 \
+    static std::atomic<uint64_t> attr{0}; \
+    if (!done_on_device(attr)) {                                                                                 \
       cudaFuncSetAttribute(chol_rowwarp<RR>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1); \
       cudaFuncSetAttribute(trinv_cols<RR>, cudaFuncAttributeMaxDynamicSharedMemorySize,          \
                            200 * 1024);                                                          \
-      attr = true;                                                                               \
+      mark_on_device(attr);                                                                               \
     }                                                                                            \
     cudaLaunchKernelEx(&cfg, chol_rowwarp<RR>, B, m, L, mode, status);                          \
     trinv_cols<RR><<<ti_grid, 32 * ti_warps, ti_smem, st>>>(L, m, Linv, status);               \
@@ -2370,15 +2370,15 @@ size_t tridiag_cluster_smem(int m, int C) {
 void launch_tridiag(const double* Asrc, int m, int symmetrize, double* Wg, double* V, double* tau,
                     double* d, double* e, const SmallStatus* status, size_t smem, cudaStream_t st) {
   if (const int C = tridiag_cluster_size(m)) {
-    static bool attr = false;
-    if (!attr) {
+    static std::atomic<uint64_t> attr{0};
+    if (!done_on_device(attr)) {
       cudaFuncSetAttribute(tridiag_cluster, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
       cudaFuncSetAttribute(tridiag_cluster, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
       cudaFuncSetAttribute(tridiag_cluster_mb, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
       cudaFuncSetAttribute(tridiag_cluster_mb, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
       cudaFuncSetAttribute(tridiag_fused, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
       cudaFuncSetAttribute(tridiag_fused, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
-      attr = true;
+      mark_on_device(attr);
     }
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(C);
@@ -3437,11 +3437,11 @@ void launch_chol(const double* B, int m, double* L, double* Linv, int mode, Smal
     int C = m <= 400 ? 8 : 16;
     if ((cfix == 2 || cfix == 4 || cfix == 8 || cfix == 16) && (m + cfix - 1) / cfix * 8 <= CCT)
       C = cfix;
-    static bool attr = false;
-    if (!attr) {
+    static std::atomic<uint64_t> attr{0};
+    if (!done_on_device(attr)) {
       cudaFuncSetAttribute(chol_cluster, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
       cudaFuncSetAttribute(chol_cluster, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
-      attr = true;
+      mark_on_device(attr);
     }
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(C);
@@ -3463,8 +3463,8 @@ void launch_chol(const double* B, int m, double* L, double* Linv, int mode, Smal
 }
 
 int set_smem_attrs() {
-  static bool done = false;
-  if (done) return SPB_OK;
+  static std::atomic<uint64_t> done{0};
+  if (done_on_device(done)) return SPB_OK;
   SPB_CUDA(cudaFuncSetAttribute(chol_linv, cudaFuncAttributeMaxDynamicSharedMemorySize, 224 * 1024));
   SPB_CUDA(cudaFuncSetAttribute(chol_ldl, cudaFuncAttributeMaxDynamicSharedMemorySize, 224 * 1024));
   SPB_CUDA(cudaFuncSetAttribute(chol_wsync, cudaFuncAttributeMaxDynamicSharedMemorySize, 217 * 1024));
@@ -3477,7 +3477,7 @@ int set_smem_attrs() {
   SPB_CUDA(cudaFuncSetAttribute(invit, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
   SPB_CUDA(cudaFuncSetAttribute(wy_apply, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
   SPB_CUDA(cudaFuncSetAttribute(wy_tfactors, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-  done = true;
+  mark_on_device(done);
   return SPB_OK;
 }
 

@@ -435,12 +435,12 @@ bool update_tc(const UpdParams& p, int64_t n, cudaStream_t st) {
   if ((size_t)stages * kStage + 1280 > 227 * 1024) stages = 2;
   P.stages = stages;
   const size_t smem = (size_t)stages * kStage + 1024 + 256;
-  static bool attr = false;
-  if (!attr) {
+  static std::atomic<uint64_t> attr{0};
+  if (!done_on_device(attr)) {
     cudaFuncSetAttribute(update_tc_kernel<64, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
     cudaFuncSetAttribute(update_tc_kernel<128, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
     cudaFuncSetAttribute(update_tc_kernel<192, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-    attr = true;
+    mark_on_device(attr);
   }
   if (smem > 227 * 1024) return false;
   tc_stage_coeffs<<<64, 256, 0, st>>>(p, npad, p.cstage);

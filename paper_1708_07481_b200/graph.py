@@ -343,7 +343,10 @@ def symmetrize(g: SparseGraph, mode: str = "algebraic") -> SparseGraph:
     """Graph holding W = A + A' (graph.py:220-236), built on the device."""
     if mode not in ("algebraic", "logical"):
         raise DomainError(f"unknown symmetrize mode {mode!r}")
-    row_ptr, col, val, nnz = g.device_csr()
+    # always A + A' of the stored arcs (graph.py:227), also when g.is_symmetric: its
+    # arcs are W itself, so symmetrize() doubles them, as the reference does
+    c = _build_csr(g._src, g._dst, g._w, g._m, g.n_vertices, N.CSR_SYMMETRIZED)
+    row_ptr, col, val, nnz = c.row_ptr, c.col, c.val, c.nnz
     rows = torch.repeat_interleave(
         torch.arange(g.n_vertices, device=row_ptr.device, dtype=torch.int64),
         (row_ptr[1:] - row_ptr[:-1]).to(torch.int64))

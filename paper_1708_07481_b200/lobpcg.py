@@ -20,6 +20,7 @@ from __future__ import annotations
 import ctypes as C
 import dataclasses
 import os
+import warnings
 from dataclasses import dataclass
 from pathlib import Path
 
@@ -43,11 +44,27 @@ __all__ = [
 ]
 
 
-def default_precision() -> str:
-    p = os.environ.get("SPB_PRECISION", "float32")
-    if p not in DTYPES:
-        raise DomainError(f"SPB_PRECISION must be one of {sorted(DTYPES)}, got {p!r}")
-    return p
+# Below this relative tolerance float32 storage cannot converge: its residuals
+# bottom out near eps32 * ||L|| (~1e-7 * scale), so the stop test would never pass.
+F32_TOL_FLOOR = 1e-6
+
+
+def default_precision(tol: float | None = None) -> str:
+    """Storage precision when the caller did not choose one: ``SPB_PRECISION`` if set,
+    else float32 -- promoted to float64 (with a warning) for a tolerance below the
+    float32 residual floor, so e.g. ``SolverConfig.high_accuracy`` converges as in the
+    reference instead of running max_iter iterations."""
+    p = os.environ.get("SPB_PRECISION")
+    if p is not None:
+        if p not in DTYPES:
+            raise DomainError(f"SPB_PRECISION must be one of {sorted(DTYPES)}, got {p!r}")
+        return p
+    if tol is not None and tol < F32_TOL_FLOOR:
+        warnings.warn(f"tol={tol:g} is below the float32 residual floor ({F32_TOL_FLOOR:g}); "
+                      "solving with float64 storage (pass precision='float32' to override)",
+                      stacklevel=3)
+        return "float64"
+    return "float32"
 
 
 @dataclass(frozen=True)
@@ -231,14 +248,55 @@ class _Bridge:
         self.pre = N.PRECOND_CB(pre_cb) if precond is not None else N.PRECOND_CB()
 
 
+class _HostOperator:
+    """Any object with the reference's operator protocol -- ``.n``, ``.scale_hint``,
+    ``.apply(x, out=None) -> out`` (graph.py:300-317; duck-typed at lobpcg.py:273,
+    :308, :374) -- bridged as an SPB_OP_HOST callback: the solve stays on the device,
+    each operator apply receives a host float64 (n, cols) block."""
+
+    def __init__(self, operator):
+        self.operator = operator
+        self.exc = None
+        n = int(operator.n)
+
+        def apply_cb(_u, rows, cols, x_in, y_out):
+            try:
+                shape = (int(rows), int(cols))
+                x = np.ctypeslib.as_array(x_in, (shape[0] * shape[1],)).reshape(shape).copy()
+                y = np.ctypeslib.as_array(y_out, (shape[0] * shape[1],)).reshape(shape)
+                r = operator.apply(x, out=y)
+                if r is not None and r is not y:
+                    r = np.asarray(r, dtype=np.float64)
+                    if r.shape != shape:
+                        raise ContractError(f"operator.apply returned shape {r.shape}, expected {shape}")
+                    y[...] = r
+                return 0
+            except BaseException as e:  # noqa: BLE001 - re-raised after the solve
+                self.exc = e
+                return 1
+
+        self.cb = N.APPLY_CB(apply_cb)
+        self.n = n
+
+    def native(self) -> N.Operator:
+        op = N.Operator()
+        op.kind = N.OP_HOST
+        op.n = self.n
+        op.scale_hint = float(self.operator.scale_hint)
+        op.apply = self.cb
+        return op
+
+
 def _native_operator(operator, dtype: str):
     if isinstance(operator, (LaplacianOperator, DenseOperator)):
         if isinstance(operator, DenseOperator) and dtype != "float64":
             dtype = "float64"
-        return operator.native(dtype), dtype
-    raise ContractError(
-        "operator must be a paper_1708_07481_b200 LaplacianOperator or DenseOperator "
-        "(the solve runs on the device)")
+        return operator.native(dtype), dtype, None
+    if all(hasattr(operator, a) for a in ("n", "scale_hint", "apply")):
+        host = _HostOperator(operator)
+        return host.native(), dtype, host
+    raise ContractError("operator must provide .n, .scale_hint and .apply(x, out=None) "
+                        "(the reference's operator protocol, graph.py:300-317)")
 
 
 def _x0_device(x0, n, l):
@@ -257,12 +315,15 @@ def lobpcg_solve(operator, x0, config: SolverConfig, precond=None, n_converge: i
     Raises ContractError / DomainError on bad arguments, SolverError (with the
     last valid state) when the iteration cannot continue.
     """
-    precision = precision or default_precision()
+    precision = precision or default_precision(config.tol)
     if isinstance(x0, torch.Tensor):
         shape = tuple(x0.shape)
     else:
         x0 = np.asarray(x0, dtype=np.float64)
         shape = x0.shape
+    if not all(hasattr(operator, a) for a in ("n", "scale_hint", "apply")):
+        raise ContractError("operator must provide .n, .scale_hint and .apply(x, out=None) "
+                            "(the reference's operator protocol, graph.py:300-317)")
     n = operator.n
     if len(shape) != 2 or shape[0] != n:
         raise ContractError(f"x0 must be ({n}, block_size)")
@@ -274,7 +335,7 @@ def lobpcg_solve(operator, x0, config: SolverConfig, precond=None, n_converge: i
     nc = l if n_converge is None else int(n_converge)
     if not 1 <= nc <= l:
         raise DomainError("n_converge must be in [1, block_size]")
-    op, precision = _native_operator(operator, precision)
+    op, precision, host_op = _native_operator(operator, precision)
     code, tdt = DTYPES[precision]
     L = N.lib()
     x0_d = _x0_device(x0, n, l)
@@ -295,6 +356,8 @@ def lobpcg_solve(operator, x0, config: SolverConfig, precond=None, n_converge: i
                                 theta, norms, conv, stats, N.stream())
     if bridge.exc is not None:
         raise bridge.exc
+    if host_op is not None and host_op.exc is not None:
+        raise host_op.exc
     state = None
     if status in (N.OK, N.E_SOLVER):
         xp = C.c_void_p()

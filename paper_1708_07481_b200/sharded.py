@@ -133,7 +133,7 @@ class RowShardedLaplacian:
 def lobpcg_solve_sharded(op: RowShardedLaplacian, x0, config: SolverConfig, n_converge=None,
                          callback=None, *, precision: str | None = None) -> EigenState:
     """lobpcg_solve on this rank's rows; x0 is the global (n, l) block (host)."""
-    precision = precision or default_precision()
+    precision = precision or default_precision(config.tol)
     if not isinstance(x0, torch.Tensor):
         x0 = np.asarray(x0, dtype=np.float64)
     if x0.ndim != 2 or x0.shape[0] != op.n:

@@ -120,3 +120,25 @@ def test_load_edge_list_native_matches_from_edges(spb, tmp_path):
     bad.write_text("1 2\n2 3\n3 x\n")
     with pytest.raises(spb.ParseError, match="line 3"):
         spb.load_edge_list(bad)
+
+
+def test_symmetrize_twice_doubles_weights(spb):
+    """reference test_graph.py:193-198: W(W) = 2W (AS_SYMMETRIC graphs)."""
+    g = spb.from_edges([(0, 1, 2.0), (1, 2, 1.0), (2, 0, 0.5)], 3)
+    once = spb.symmetrize(g)
+    twice = spb.symmetrize(once)
+    assert np.array_equal(twice.col_indices, once.col_indices)
+    assert np.allclose(twice.weights, 2.0 * once.weights)
+    assert np.array_equal(spb.degrees(twice), 2.0 * spb.degrees(once))
+
+
+def test_symmetrize_modes(spb):
+    """reference test_graph.py:182-191, :201-210."""
+    g = spb.symmetrize(spb.from_edges([(0, 1, 1.0)], 2))
+    assert g.to_dense().tolist() == [[0.0, 1.0], [1.0, 0.0]]
+    d = spb.symmetrize(spb.from_edges([(0, 1, 2.0), (1, 0, 3.0)], 2)).to_dense()
+    assert d[0, 1] == 5.0 and d[1, 0] == 5.0
+    g = spb.symmetrize(spb.from_edges([(0, 1, 2.0), (1, 0, 3.0), (1, 2, 4.0)], 3), mode="logical")
+    assert set(g.weights.tolist()) == {1.0}
+    with pytest.raises(spb.DomainError):
+        spb.symmetrize(spb.from_edges([(0, 1)], 2), mode="other")

@@ -1,0 +1,179 @@
+"""GPU parity at the large configs against the REAL reference's own outputs.
+
+Fixtures (tests/golden/make_golden_large.py, specpart 0.1.0 run here with one BLAS
+thread): large_c3.npz (C3 = 500K vertices, B=98, the SURVEY §8(d) 10x stop rule),
+large_c4.npz (C4 = 2M vertices, B=160: CSR/degree shas and a max_iter=3 pin) and
+stream_c5.npz (C5 = the C2 graph streamed over 10 stages, emerging and BFS-snowball
+orders, warm and random starts). Tolerances are the north star's: bit-exact CSR and
+degrees, Ritz values within 1e-4 relative (floor 1e-4 |theta_{l-1}|), residual
+history |log10 ratio| <= 0.01 above the storage floor, iteration counts exact,
+partition agreement with the reference's labels, PR/PP within 0.005.
+"""
+
+import numpy as np
+import pytest
+
+import oracle
+from tests.conftest import GOLDEN, load_golden
+from tests.helpers import config_input, sha
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def spb():
+    import paper_1708_07481_b200 as spb
+
+    return spb
+
+
+def _theta_close(got, want, rel=1e-4):
+    floor = rel * np.abs(want).max()
+    return np.all(np.abs(got - want) <= rel * np.abs(want) + floor)
+
+
+def _need(name):
+    if not (GOLDEN / f"{name}.npz").exists():
+        pytest.skip(f"tests/golden/{name}.npz not generated")
+    return load_golden(name)
+
+
+@pytest.fixture(scope="module")
+def c3_input():
+    return config_input("c3", seed=0)
+
+
+def test_c3_graph_bit_exact(spb, c3_input):
+    gold = _need("large_c3")
+    spec, edges, _ = c3_input
+    assert sha(edges) == str(gold["c3_s0/edges_sha"])
+    g = spb.from_edges(edges, spec.n)
+    assert sha(g.row_offsets, g.col_indices, g.weights) == str(gold["c3_s0/a_sha"])
+    s = spb.symmetrize(g)
+    assert sha(s.row_offsets, s.col_indices, s.weights) == str(gold["c3_s0/w_sha"])
+    assert sha(spb.degrees(g)) == str(gold["c3_s0/deg_sha"])
+
+
+@pytest.mark.parametrize("precision", ["float32", "float64"])
+def test_c3_partition_parity(spb, c3_input, precision):
+    gold = _need("large_c3")
+    key = "c3_s0"
+    spec, edges, truth = c3_input
+    k = spec.blocks
+    l = spb.block_size_for(k)
+    x0 = np.random.default_rng(0).standard_normal((spec.n, l))
+    g = spb.from_edges(edges, spec.n)
+    cfg = spb.SolverConfig(block_size=l, tol=float(gold[f"{key}/tol"]),
+                           max_iter=int(gold[f"{key}/max_iter"]), seed=0)
+    hr = []
+    part, st, _ = spb.partition_static(g, cfg, k_expected=k, fix_k=True, x0=x0, precision=precision,
+                                       callback=lambda it, t, r: hr.append(r))
+    ss = st.solve_stats
+    print(f"\nC3 {precision}: iterations {st.iterations} (reference {int(gold[f'{key}/iterations'])}), "
+          f"orth_p re-solves {ss['orth_p']}, drop_p {ss['drop_p']}, rebuild {ss['rebuild']}, "
+          f"RR solves {ss['rr_calls']}")
+    assert st.iterations == int(gold[f"{key}/iterations"])
+    assert _theta_close(st.eigenvalues, gold[f"{key}/theta"])
+    ref_h = gold[f"{key}/hist_norms"]
+    assert len(hr) == len(ref_h)
+    a, b = np.array(hr)[:, : k + 1], ref_h[:, : k + 1]
+    eps = 1e-16 if precision == "float64" else 6e-8
+    big = b > 1e3 * eps * g.device_degrees().max().item()
+    dev = np.max(np.abs(np.log10(a[big] / b[big])))
+    print(f"C3 {precision}: max |log10 residual ratio| {dev:.2e}")
+    assert dev <= 0.01
+    ref_labels = gold[f"{key}/labels"].astype(np.int64)
+    agree = oracle.partition_match(ref_labels, part.labels)
+    pr = oracle.pairwise_recall(truth, part.labels)
+    pp = oracle.pairwise_precision(truth, part.labels)
+    rp = gold[f"{key}/pm_pr_pp"]
+    print(f"C3 {precision}: label agreement with the reference {agree:.5f}; PR {pr:.4f} "
+          f"(ref {rp[1]:.4f}), PP {pp:.4f} (ref {rp[2]:.4f})")
+    assert agree >= 0.999, agree
+    assert abs(pr - rp[1]) <= 0.005 and abs(pp - rp[2]) <= 0.005
+
+
+def test_c4_graph_and_three_iterations(spb):
+    """C4 (2M vertices, 40M arcs): int32 row_ptr / 42-bit radix keys near their
+    limits, bit-exact against the reference; the first 3 LOBPCG expansions and the
+    resulting labels pinned (a full 30-iteration reference solve is ~1 h of CPU)."""
+    gold = _need("large_c4")
+    key = "c4_s0"
+    spec, edges, truth = config_input("c4", seed=0)
+    assert sha(edges) == str(gold[f"{key}/edges_sha"])
+    g = spb.from_edges(edges, spec.n)
+    assert sha(g.row_offsets, g.col_indices, g.weights) == str(gold[f"{key}/a_sha"])
+    s = spb.symmetrize(g)
+    assert sha(s.row_offsets, s.col_indices, s.weights) == str(gold[f"{key}/w_sha"])
+    del s
+    assert sha(spb.degrees(g)) == str(gold[f"{key}/deg_sha"])
+    k = spec.blocks
+    l = spb.block_size_for(k)
+    x0 = np.random.default_rng(0).standard_normal((spec.n, l))
+    cfg = spb.SolverConfig(block_size=l, tol=float(gold[f"{key}/tol"]),
+                           max_iter=int(gold[f"{key}/max_iter"]), seed=0)
+    hr = []
+    part, st, _ = spb.partition_static(g, cfg, k_expected=k, fix_k=True, x0=x0,
+                                       precision="float32", callback=lambda it, t, r: hr.append(r))
+    assert st.iterations == int(gold[f"{key}/iterations"])
+    assert _theta_close(st.eigenvalues, gold[f"{key}/theta"])
+    a, b = np.array(hr)[:, : k + 1], gold[f"{key}/hist_norms"][:, : k + 1]
+    assert a.shape == b.shape
+    dev = np.max(np.abs(np.log10(a / b)))
+    agree = oracle.partition_match(gold[f"{key}/labels"].astype(np.int64), part.labels)
+    print(f"\nC4 float32 (3 iterations): max |log10 residual ratio| {dev:.2e}, "
+          f"label agreement {agree:.5f}, orth_p {st.solve_stats['orth_p']}")
+    assert dev <= 0.01
+    assert agree >= 0.999, agree
+
+
+def _c5_streams():
+    from paper_1708_07481_b200.dcsbm import emerging_slices, snowball_slices
+
+    spec, edges, truth = config_input("c2")
+    relabel, snow = snowball_slices(edges, spec.n, 10, seed=spec.seed)
+    return spec, edges, {
+        "emerging": ([(d, spec.n) for d in emerging_slices(edges, 10, seed=spec.seed)], truth),
+        "snowball": (snow, truth[np.argsort(relabel)]),
+    }
+
+
+@pytest.fixture(scope="module")
+def c5():
+    return _c5_streams()
+
+
+@pytest.mark.parametrize("precision", ["float64", "float32"])
+@pytest.mark.parametrize("key", ["emerging_warm", "emerging_random", "snowball_warm", "snowball_random"])
+def test_c5_stream_parity(spb, c5, key, precision):
+    from paper_1708_07481_b200.streaming import StreamStage, partition_stream
+
+    gold = _need("stream_c5")
+    spec, edges, streams = c5
+    assert sha(edges) == str(gold["edges_sha"])
+    mode, init = key.split("_")
+    st, truth = streams[mode]
+    stages = [StreamStage(index=i + 1, mode=mode, edge_delta=d, n_after=n) for i, (d, n) in enumerate(st)]
+    k = spec.blocks
+    cfg = spb.SolverConfig(block_size=spb.block_size_for(k), tol=float(gold["tol"]),
+                           max_iter=int(gold["max_iter"]), seed=spec.seed)
+    res = partition_stream(spb.empty_graph(0), stages, cfg, init_mode=init, k_expected=k,
+                           fix_k=True, precision=precision)
+    want_it = gold[f"{key}/iterations"]
+    got_it = np.array([r.iterations for r in res])
+    print(f"\nC5 {key} {precision}: iterations {got_it.tolist()} (reference {want_it.tolist()})")
+    assert np.array_equal(got_it, want_it), (got_it, want_it)
+    for i, r in enumerate(res):
+        want = gold[f"{key}/theta{i}"]
+        eps = 2.2e-16 if precision == "float64" else 6e-8
+        floor = 1e-4 * np.abs(want).max() + 8 * eps * 2 * 100.0
+        assert np.all(np.abs(r.eigenstate.eigenvalues - want) <= 1e-4 * np.abs(want) + floor), i
+    agree = oracle.partition_match(gold[f"{key}/labels_last"].astype(np.int64), res[-1].partition.labels)
+    print(f"C5 {key} {precision}: final-stage label agreement {agree:.5f}")
+    assert agree >= 0.999, agree
+    pm = gold[f"{key}/pm_pr_pp"]
+    for i, r in enumerate(res):
+        n_i = len(r.partition.labels)
+        pr = oracle.pairwise_recall(truth[:n_i], r.partition.labels)
+        pp = oracle.pairwise_precision(truth[:n_i], r.partition.labels)
+        assert abs(pr - pm[i, 1]) <= 0.005 and abs(pp - pm[i, 2]) <= 0.005, i

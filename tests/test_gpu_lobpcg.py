@@ -218,3 +218,84 @@ def test_tensor_core_gram_mode_runs(spb, golden_partition, monkeypatch):
                                        precision="float32")
     assert _theta_close(st.eigenvalues, gold["c1_s0/theta"], rel=1e-2)
     assert oracle.partition_match(gold["c1_s0/labels"].astype(np.int64), part.labels) >= 0.99
+
+
+class _ScipyLaplacian:
+    """A plain reference-protocol operator (.n, .scale_hint, .apply(x, out)) that is
+    not one of this package's classes (lobpcg.py:273 duck typing)."""
+
+    def __init__(self, edges, n):
+        import scipy.sparse as sp
+
+        e = np.asarray(edges)
+        a = sp.coo_matrix((np.ones(len(e)), (e[:, 0], e[:, 1])), shape=(n, n)).tocsr()
+        a.setdiag(0)
+        a.eliminate_zeros()
+        w = (a + a.T).tocsr()
+        self.d = np.asarray(w.sum(axis=1)).ravel()
+        self.w = w
+        self.n = n
+        self.scale_hint = float(self.d.max())
+        self.calls = 0
+
+    def apply(self, x, out=None):
+        self.calls += 1
+        y = self.d[:, None] * x - self.w @ x
+        if out is None:
+            return y
+        out[...] = y
+        return out
+
+
+def test_duck_typed_operator_matches_laplacian(spb):
+    """Any object with the operator protocol runs through the device solver and gives
+    the same solve as the built-in LaplacianOperator (float64)."""
+    spec, edges, _ = config_input("c1", seed=0)
+    l = 21
+    x0 = np.random.default_rng(0).standard_normal((spec.n, l))
+    cfg = spb.SolverConfig(block_size=l, tol=1e-12, max_iter=10, seed=0)
+    duck = _ScipyLaplacian(edges, spec.n)
+    a = spb.lobpcg_solve(duck, x0, cfg, n_converge=20, precision="float64")
+    b = spb.lobpcg_solve(spb.LaplacianOperator(spb.from_edges(edges, spec.n)), x0, cfg,
+                         n_converge=20, precision="float64")
+    assert a.iterations == b.iterations == 10
+    assert duck.calls == a.solve_stats["spmm_calls"]
+    assert _theta_close(a.eigenvalues, b.eigenvalues, 1e-9)
+    with pytest.raises(spb.ContractError):
+        spb.lobpcg_solve(object(), x0, cfg)
+
+
+def test_duck_typed_operator_errors_propagate(spb):
+    class Bad(_ScipyLaplacian):
+        def apply(self, x, out=None):
+            raise ValueError("boom")
+
+    spec, edges, _ = config_input("c1", seed=0)
+    x0 = np.random.default_rng(0).standard_normal((spec.n, 4))
+    with pytest.raises(ValueError, match="boom"):
+        spb.lobpcg_solve(Bad(edges, spec.n), x0, spb.SolverConfig(block_size=4, max_iter=3))
+
+
+@pytest.mark.parametrize("precision", PRECISIONS)
+def test_residual_norms_audit(spb, precision):
+    """residual_norms (lobpcg.py:457-461) recomputes the state's final norms."""
+    spec, edges, _ = config_input("c1", seed=1)
+    g = spb.from_edges(edges, spec.n)
+    op = spb.LaplacianOperator(g)
+    st = spb.lobpcg_solve(op, spb.random_init(spec.n, 8, 1), spb.SolverConfig(block_size=8, max_iter=15),
+                          precision=precision)
+    r = spb.residual_norms(op, st)
+    floor = (1e-9 if precision == "float64" else 1e-4) * op.scale_hint
+    assert np.all(np.abs(r - st.residual_norms) <= 1e-3 * st.residual_norms + floor)
+
+
+def test_high_accuracy_default_precision_converges(spb, monkeypatch):
+    """the default (float32) storage cannot reach tol=1e-10; an unspecified
+    precision is promoted to float64 and converges as the reference does."""
+    monkeypatch.delenv("SPB_PRECISION", raising=False)
+    g = spb.from_edges([(0, 1), (1, 2), (2, 3), (3, 0), (0, 2), (4, 5), (5, 6), (6, 4), (3, 4)], 7)
+    with pytest.warns(UserWarning):
+        st = spb.lobpcg_solve(spb.LaplacianOperator(g), spb.random_init(7, 3, 0),
+                              spb.SolverConfig.high_accuracy(3, seed=0))
+    assert st.precision == "float64"
+    assert st.converged.all() and st.iterations < 500

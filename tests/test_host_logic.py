@@ -106,3 +106,32 @@ class TestGenerators:
             if len(delta):
                 assert delta.max() < n_after
             prev = n_after
+
+
+class TestPrecisionAndState:
+    def test_default_precision_promotes_below_f32_floor(self, monkeypatch):
+        from paper_1708_07481_b200.lobpcg import default_precision
+
+        monkeypatch.delenv("SPB_PRECISION", raising=False)
+        assert default_precision() == "float32"
+        assert default_precision(1e-4) == "float32"
+        with pytest.warns(UserWarning, match="float32 residual floor"):
+            assert default_precision(spb.SolverConfig.high_accuracy(4).tol) == "float64"
+        monkeypatch.setenv("SPB_PRECISION", "float32")
+        assert default_precision(1e-12) == "float32"  # explicit choice wins
+
+    def test_eigenstate_save_load_roundtrip(self, tmp_path):
+        """EigenState.save/load as .npz (lobpcg.py:108-129)."""
+        rng = np.random.default_rng(0)
+        st = spb.EigenState(np.array([0.0, 1.5, 2.0]), rng.standard_normal((7, 3)),
+                            np.array([1e-3, 2e-3, 3e-3]), 11, np.array([True, False, True]),
+                            work_blocks=6)
+        path = tmp_path / "state.npz"
+        st.save(path)
+        back = spb.EigenState.load(path)
+        assert np.array_equal(back.eigenvalues, st.eigenvalues)
+        assert np.array_equal(back.vectors, st.vectors)
+        assert np.array_equal(back.residual_norms, st.residual_norms)
+        assert back.iterations == 11 and back.work_blocks == 6
+        assert np.array_equal(back.converged, st.converged)
+        assert back.block_size == 3
