@@ -183,12 +183,34 @@ typedef struct {
 SPB_API int spb_comm_unique_id(void* out, int32_t bytes);
 SPB_API int spb_comm_init(int32_t nranks, int32_t rank, const void* unique_id, void** comm_out);
 SPB_API int spb_comm_destroy(void* comm);
+/* Host-transport communicator: the same sharded solver, with each collective
+ * staged through host memory and performed by the caller's callbacks (e.g. a
+ * torch.distributed gloo group). For testing the row-sharded code path with
+ * several ranks when fewer GPUs than ranks exist (ranks never wait on each other
+ * inside a kernel: every exchange happens between launches, on the host), and
+ * for hosts without NCCL. allreduce: in-place float64 sum of count values;
+ * allgather: recv[r * bytes ... ] = send of rank r. Return 0 on success. */
+typedef int (*spb_allreduce_cb)(void* user, double* buf, int64_t count);
+typedef int (*spb_allgather_cb)(void* user, const void* send, void* recv, int64_t bytes);
+SPB_API int spb_comm_init_host(int32_t nranks, int32_t rank, spb_allreduce_cb allreduce,
+                               spb_allgather_cb allgather, void* user, void** comm_out);
 /* Local CSR of rows [row_begin, row_end) of a global CSR, columns remapped to
  * rank(col) * n_max + (col - bounds[rank(col)]); bounds: device int32[nranks+1]. */
 SPB_API int spb_csr_shard(const int32_t* row_ptr, const int32_t* col, const double* val,
                           int32_t row_begin, int32_t row_end, const int32_t* bounds,
                           int32_t nranks, int32_t n_max, int32_t* out_row_ptr, int32_t* out_col,
                           double* out_val, void* stream);
+/* This rank's rows [row_begin, row_end) of W = A + A' built directly from the
+ * whole arc list (no whole-graph CSR on any rank): bit-identical to those rows of
+ * spb_csr_build(SYMMETRIZED) (same per-entry summation order), columns remapped as
+ * spb_csr_shard does, local degrees in deg (float64[row_end - row_begin]).
+ * ws: spb_csr_build_workspace(m, n, SPB_CSR_SYMMETRIZED) bytes; col/val capacity
+ * 2m. bounds: device int32[nranks + 1]. */
+SPB_API int spb_csr_build_rows(const int64_t* src, const int64_t* dst, const double* w,
+                               int64_t m_edges, int32_t n, int32_t row_begin, int32_t row_end,
+                               const int32_t* bounds, int32_t nranks, int32_t n_max, void* ws,
+                               size_t ws_bytes, int32_t* row_ptr, int32_t* col, double* val,
+                               double* deg, int64_t* nnz_out, void* stream);
 SPB_API size_t spb_lobpcg_workspace_sharded(int dtype, int32_t n_local, int32_t l, int32_t nranks,
                                             int32_t n_max);
 SPB_API int spb_lobpcg_solve_sharded(const spb_operator* op, const spb_shard* shard, int dtype,

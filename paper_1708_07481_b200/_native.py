@@ -52,6 +52,8 @@ class SolverConfigC(C.Structure):
 ITER_CB = C.CFUNCTYPE(C.c_int, vp, i32, C.POINTER(f64), C.POINTER(f64), i32)
 REFILL_CB = C.CFUNCTYPE(C.c_int, vp, i64, i32, C.POINTER(f64))
 PRECOND_CB = C.CFUNCTYPE(C.c_int, vp, i64, i32, C.POINTER(f64))
+ALLREDUCE_CB = C.CFUNCTYPE(C.c_int, vp, C.POINTER(f64), i64)
+ALLGATHER_CB = C.CFUNCTYPE(C.c_int, vp, vp, vp, i64)
 
 _SIGS = {
     "spb_last_error": (C.c_char_p, []),
@@ -78,6 +80,9 @@ _SIGS = {
     "spb_comm_unique_id": (C.c_int, [vp, i32]),
     "spb_comm_init": (C.c_int, [i32, i32, vp, C.POINTER(vp)]),
     "spb_comm_destroy": (C.c_int, [vp]),
+    "spb_comm_init_host": (C.c_int, [i32, i32, ALLREDUCE_CB, ALLGATHER_CB, vp, C.POINTER(vp)]),
+    "spb_csr_build_rows": (C.c_int, [vp, vp, vp, i64, i32, i32, i32, vp, i32, i32, vp, sz, vp, vp,
+                                     vp, vp, C.POINTER(i64), vp]),
     "spb_csr_shard": (C.c_int, [vp, vp, vp, i32, i32, vp, i32, i32, vp, vp, vp, vp]),
     "spb_lobpcg_workspace_sharded": (sz, [C.c_int, i32, i32, i32, i32]),
     "spb_lobpcg_solve_sharded": (C.c_int, [C.POINTER(Operator), C.POINTER(Shard), C.c_int, vp,

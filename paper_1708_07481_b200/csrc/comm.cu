@@ -6,6 +6,8 @@
 // shared object itself has no link-time dependency on NCCL.
 #include <dlfcn.h>
 
+#include <vector>
+
 #include <nccl.h>
 
 #include "comm.cuh"
@@ -55,6 +57,18 @@ int nccl_fail(ncclResult_t r, const char* what) {
 
 int comm_allreduce_f64(const Comm* c, double* buf, size_t count, cudaStream_t st) {
   if (!c || c->nranks <= 1 || count == 0) return SPB_OK;
+  if (c->host_allreduce) {
+    std::vector<double> h(count);
+    SPB_CUDA(cudaMemcpyAsync(h.data(), buf, sizeof(double) * count, cudaMemcpyDeviceToHost, st));
+    SPB_CUDA(cudaStreamSynchronize(st));
+    if (c->host_allreduce(c->host_user, h.data(), (int64_t)count) != 0) {
+      set_error("host allreduce callback failed");
+      return SPB_ERR_CALLBACK;
+    }
+    SPB_CUDA(cudaMemcpyAsync(buf, h.data(), sizeof(double) * count, cudaMemcpyHostToDevice, st));
+    SPB_CUDA(cudaStreamSynchronize(st));
+    return SPB_OK;
+  }
   ncclResult_t r = api().allReduce(buf, buf, count, ncclFloat64, ncclSum, (ncclComm_t)c->nccl, st);
   return r == ncclSuccess ? SPB_OK : nccl_fail(r, "allreduce");
 }
@@ -64,6 +78,18 @@ int comm_allgather_bytes(const Comm* c, const void* send, void* recv, size_t byt
   if (!c || c->nranks <= 1) {
     if (send != recv && bytes_per_rank)
       SPB_CUDA(cudaMemcpyAsync(recv, send, bytes_per_rank, cudaMemcpyDeviceToDevice, st));
+    return SPB_OK;
+  }
+  if (c->host_allgather) {
+    std::vector<char> hs(bytes_per_rank), hr(bytes_per_rank * (size_t)c->nranks);
+    SPB_CUDA(cudaMemcpyAsync(hs.data(), send, bytes_per_rank, cudaMemcpyDeviceToHost, st));
+    SPB_CUDA(cudaStreamSynchronize(st));
+    if (c->host_allgather(c->host_user, hs.data(), hr.data(), (int64_t)bytes_per_rank) != 0) {
+      set_error("host allgather callback failed");
+      return SPB_ERR_CALLBACK;
+    }
+    SPB_CUDA(cudaMemcpyAsync(recv, hr.data(), hr.size(), cudaMemcpyHostToDevice, st));
+    SPB_CUDA(cudaStreamSynchronize(st));
     return SPB_OK;
   }
   ncclResult_t r = api().allGather(send, recv, bytes_per_rank, ncclInt8, (ncclComm_t)c->nccl, st);
@@ -115,6 +141,23 @@ extern "C" int spb_comm_init(int32_t nranks, int32_t rank, const void* id, void*
     }
     c->nccl = nc;
   }
+  *comm_out = c;
+  return SPB_OK;
+}
+
+extern "C" int spb_comm_init_host(int32_t nranks, int32_t rank, spb_allreduce_cb allreduce,
+                                  spb_allgather_cb allgather, void* user, void** comm_out) {
+  if (nranks < 1 || rank < 0 || rank >= nranks || !allreduce || !allgather) {
+    set_error("bad host communicator");
+    return SPB_ERR_CONTRACT;
+  }
+  Comm* c = new Comm();
+  c->nranks = nranks;
+  c->rank = rank;
+  c->nccl = nullptr;
+  c->host_allreduce = allreduce;
+  c->host_allgather = allgather;
+  c->host_user = user;
   *comm_out = c;
   return SPB_OK;
 }

@@ -5,9 +5,13 @@
 namespace spb {
 
 struct Comm {
-  void* nccl;  // ncclComm_t (null for a single rank)
+  void* nccl;  // ncclComm_t (null for a single rank or the host transport)
   int nranks;
   int rank;
+  // host transport (spb_comm_init_host): collectives staged through host memory
+  spb_allreduce_cb host_allreduce = nullptr;
+  spb_allgather_cb host_allgather = nullptr;
+  void* host_user = nullptr;
 };
 
 // In-place float64 sum over ranks (no-op for one rank).

@@ -214,6 +214,54 @@ __global__ void row_degrees(const int32_t* __restrict__ row_ptr, const double* _
   }
 }
 
+// Row-shard build (multi-GPU): only the entries of W whose row is
+// in [r0, r1) are kept -- the forward arc s->d when r0 <= s < r1 and the reverse
+// d->s when r0 <= d < r1 -- compacted in emission order (slot 2e, 2e+1), so every
+// (row, col) group is summed in the same order as in the whole-graph build and
+// the local rows are bit-identical to it. Rows are local (row - r0); columns are
+// remapped to the all-gathered layout rank(col) * n_max + (col - bounds[rank]).
+__device__ __forceinline__ uint64_t gathered_col(int64_t c, const int32_t* __restrict__ bounds,
+                                                 int nranks, int32_t n_max) {
+  int lo = 0, hi = nranks;  // owner: bounds[lo] <= c < bounds[lo + 1]
+  while (hi - lo > 1) {
+    const int mid = (lo + hi) >> 1;
+    if (bounds[mid] <= c) lo = mid; else hi = mid;
+  }
+  return (uint64_t)lo * (uint64_t)n_max + (uint64_t)(c - bounds[lo]);
+}
+
+__global__ void rows_flags(const int64_t* __restrict__ src, const int64_t* __restrict__ dst,
+                           int64_t m, int64_t r0, int64_t r1, int* __restrict__ flag) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < m;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t a = src[e], b = dst[e];
+    const bool loop = a == b;
+    flag[2 * e] = !loop && a >= r0 && a < r1;
+    flag[2 * e + 1] = !loop && b >= r0 && b < r1;
+  }
+}
+
+__global__ void rows_emit(const int64_t* __restrict__ src, const int64_t* __restrict__ dst,
+                          int64_t m, int64_t r0, const int32_t* __restrict__ bounds, int nranks,
+                          int32_t n_max, int b, const int* __restrict__ flag,
+                          const int* __restrict__ slot, uint64_t* __restrict__ keys,
+                          uint32_t* __restrict__ pay) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < m;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t a = src[e], c = dst[e];
+    if (flag[2 * e]) {
+      const int s = slot[2 * e];
+      keys[s] = ((uint64_t)(a - r0) << b) | gathered_col(c, bounds, nranks, n_max);
+      pay[s] = (uint32_t)(2 * e);
+    }
+    if (flag[2 * e + 1]) {
+      const int s = slot[2 * e + 1];
+      keys[s] = ((uint64_t)(c - r0) << b) | gathered_col(a, bounds, nranks, n_max);
+      pay[s] = (uint32_t)(2 * e + 1);
+    }
+  }
+}
+
 int key_bits(int32_t n) {
   int b = 1;
   while ((int64_t(1) << b) <= (int64_t)n) ++b;
@@ -252,6 +300,10 @@ BuildLayout carve(Arena& a, int64_t cap) {
   L.flags = a.take<BuildFlags>(1);
   return L;
 }
+
+int sort_reduce_scatter(BuildLayout& L, const double* w, int64_t count, int64_t valid, int b,
+                        bool symmetrized, int32_t n, int32_t* row_ptr, int32_t* col, double* val,
+                        double* deg, int64_t* nnz_out, cudaStream_t st);
 
 int grid_for(int64_t work, int threads = 256) {
   int64_t g = ceil_div(std::max<int64_t>(work, 1), threads);
@@ -338,12 +390,24 @@ extern "C" int spb_csr_build(const int64_t* src, const int64_t* dst, const doubl
   const int64_t count = (two ? 2 : 1) * m;
   emit_entries<<<grid_for(m), 256, 0, st>>>(src, dst, m, b, two, L.ka, L.pa);
   SPB_LAUNCH_CHECK();
+  // self-loops carry the sentinel key and sort to the end
+  const int64_t valid = count - (two ? 2 : 1) * (int64_t)hf.self_loops;
+  return sort_reduce_scatter(L, w, count, valid, b, mode == SPB_CSR_SYMMETRIZED, n, row_ptr, col,
+                             val, deg, nnz_out, st);
+}
 
+namespace spb {
+namespace {
+// Stable radix sort of the emitted (key, payload) pairs, per-(row, col) sums,
+// compaction into the CSR arrays, row pointers and degrees (steps 3-6 above).
+int sort_reduce_scatter(BuildLayout& L, const double* w, int64_t count, int64_t valid, int b,
+                        bool symmetrized, int32_t n, int32_t* row_ptr, int32_t* col, double* val,
+                        double* deg, int64_t* nnz_out, cudaStream_t st) {
   // stable LSD radix sort over 2b key bits
   const int64_t ntiles = ceil_div(count, kSortTile);
   uint64_t *kin = L.ka, *kout = L.kb;
   uint32_t *pin = L.pa, *pout = L.pb;
-  for (int shift = 0; shift < 2 * b; shift += 8) {
+  for (int shift = 0; count > 0 && shift < 2 * b; shift += 8) {
     radix_hist<<<ntiles, kSortThreads, 0, st>>>(kin, count, shift, ntiles, L.counts);
     SPB_TRY(exclusive_scan_i32(L.counts, L.counts, (int64_t)kRadix * ntiles, L.scan_tmp,
                                nullptr, st));
@@ -353,13 +417,10 @@ extern "C" int spb_csr_build(const int64_t* src, const int64_t* dst, const doubl
     std::swap(kin, kout);
     std::swap(pin, pout);
   }
-  // self-loops carry the sentinel key and sort to the end
-  const int64_t valid = count - (two ? 2 : 1) * (int64_t)hf.self_loops;
   int32_t* dev_total = L.dev_ints;
   int64_t nnz = 0;
   if (valid > 0) {
-    group_reduce<<<grid_for(valid), 256, 0, st>>>(kin, pin, valid, w,
-                                                   mode == SPB_CSR_SYMMETRIZED, L.keep, L.fsum,
+    group_reduce<<<grid_for(valid), 256, 0, st>>>(kin, pin, valid, w, symmetrized, L.keep, L.fsum,
                                                    L.rsum, L.has);
     SPB_LAUNCH_CHECK();
     SPB_TRY(exclusive_scan_i32(L.keep, L.slot, valid, L.scan_tmp, dev_total, st));
@@ -375,12 +436,79 @@ extern "C" int spb_csr_build(const int64_t* src, const int64_t* dst, const doubl
   fill_row_ptr<<<grid_for(nnz + 1), 256, 0, st>>>(L.orow, nnz, n, row_ptr);
   SPB_LAUNCH_CHECK();
   if (deg) {
-    row_degrees<<<grid_for(n), 256, 0, st>>>(row_ptr, L.ofs, L.ors, L.ohas, n,
-                                              mode == SPB_CSR_SYMMETRIZED, deg);
+    row_degrees<<<grid_for(n), 256, 0, st>>>(row_ptr, L.ofs, L.ors, L.ohas, n, symmetrized, deg);
     SPB_LAUNCH_CHECK();
   }
   *nnz_out = nnz;
   return SPB_OK;
+}
+}  // namespace
+}  // namespace spb
+
+extern "C" int spb_csr_build_rows(const int64_t* src, const int64_t* dst, const double* w,
+                                  int64_t m, int32_t n, int32_t row_begin, int32_t row_end,
+                                  const int32_t* bounds, int32_t nranks, int32_t n_max, void* ws,
+                                  size_t ws_bytes, int32_t* row_ptr, int32_t* col, double* val,
+                                  double* deg, int64_t* nnz_out, void* stream) {
+  cudaStream_t st = (cudaStream_t)stream;
+  if (n < 0 || m < 0 || row_begin < 0 || row_end < row_begin || row_end > n || nranks < 1 ||
+      n_max < row_end - row_begin || !deg) {
+    set_error("csr row-shard build contract violated");
+    return SPB_ERR_CONTRACT;
+  }
+  if (m >= (int64_t(1) << 30)) {
+    set_error("edge count %lld exceeds 2^30 per build", (long long)m);
+    return SPB_ERR_CONTRACT;
+  }
+  const int32_t nl = row_end - row_begin;
+  const int64_t cap = 2 * std::max<int64_t>(m, 1);
+  Arena a;
+  a.base = (char*)ws;
+  a.cap = ws_bytes;
+  BuildLayout L = carve(a, cap);
+  if (a.used > ws_bytes) {
+    set_error("csr build workspace too small (%zu < %zu)", ws_bytes, a.used);
+    return SPB_ERR_WORKSPACE;
+  }
+  SPB_CUDA(cudaMemsetAsync(L.flags, 0, sizeof(BuildFlags), st));
+  if (m > 0) {
+    validate_edges<<<grid_for(m), 256, 0, st>>>(src, dst, w, m, n, L.flags);
+    SPB_LAUNCH_CHECK();
+  }
+  BuildFlags hf;
+  SPB_CUDA(cudaMemcpyAsync(&hf, L.flags, sizeof(hf), cudaMemcpyDeviceToHost, st));
+  SPB_CUDA(cudaStreamSynchronize(st));
+  if (hf.bad_endpoint) {
+    set_error("edge endpoint out of range");
+    return SPB_ERR_DOMAIN;
+  }
+  if (hf.bad_weight) {
+    set_error("negative edge weight");
+    return SPB_ERR_DOMAIN;
+  }
+  if (m == 0 || nl == 0) {
+    SPB_CUDA(cudaMemsetAsync(row_ptr, 0, sizeof(int32_t) * (nl + 1), st));
+    if (nl) SPB_CUDA(cudaMemsetAsync(deg, 0, sizeof(double) * nl, st));
+    *nnz_out = 0;
+    return SPB_OK;
+  }
+  // compaction of this rank's entries, in emission order (keep/slot reused)
+  rows_flags<<<grid_for(m), 256, 0, st>>>(src, dst, m, row_begin, row_end, L.keep);
+  SPB_LAUNCH_CHECK();
+  SPB_TRY(exclusive_scan_i32(L.keep, L.slot, 2 * m, L.scan_tmp, L.dev_ints, st));
+  int htot = 0;
+  SPB_CUDA(cudaMemcpyAsync(&htot, L.dev_ints, sizeof(int), cudaMemcpyDeviceToHost, st));
+  SPB_CUDA(cudaStreamSynchronize(st));
+  const int b = key_bits(std::max<int32_t>(nl, (int32_t)std::min<int64_t>(
+                                                   (int64_t)nranks * n_max, INT32_MAX)));
+  if (2 * b > 64) {
+    set_error("row-shard key does not fit 64 bits");
+    return SPB_ERR_CONTRACT;
+  }
+  rows_emit<<<grid_for(m), 256, 0, st>>>(src, dst, m, row_begin, bounds, nranks, n_max, b, L.keep,
+                                         L.slot, L.ka, L.pa);
+  SPB_LAUNCH_CHECK();
+  return sort_reduce_scatter(L, w, htot, htot, b, true, nl, row_ptr, col, val, deg, nnz_out, st);
 }
 
 // ---------------------------------------------------------------------------

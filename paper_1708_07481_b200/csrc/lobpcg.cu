@@ -527,8 +527,9 @@ struct Driver {
     // bracket exceeds kCondMaxF32 the caller re-solves on [X R P'] with P' orthonormalised against [X R] (orth_p): the
     // same subspace, so the reference's Ritz values, from a well-conditioned basis.
     // The ladder decision itself keeps the reference's 1/sqrt(eps64) threshold.
-    static const double f32_lo =  // SPB_F32_COND_LO: A/B override of the threshold
-        getenv("SPB_F32_COND_LO") ? atof(getenv("SPB_F32_COND_LO")) : kCondMaxF32;
+    // SPB_F32_COND_LO overrides the threshold (tests force the re-solve with it)
+    const char* lo_env = getenv("SPB_F32_COND_LO");
+    const double f32_lo = lo_env ? atof(lo_env) : kCondMaxF32;
     p_ill = w.dtype == SPB_F32 && !identity_b && cur_pw > 0 && hs.cond_lo > f32_lo;
     if (hs.cond_state == 2) {
       double cond = 0.0;

@@ -217,6 +217,14 @@ def from_edges(edges, n: int, weights=None, *, symmetric: bool = False) -> Spars
     ``edges`` may also be a pair of device int64 tensors ``(src, dst)``.
     """
     n = int(n)
+    src, dst, w = _device_arcs(edges, n, weights)
+    g = SparseGraph(n, src, dst, w, is_symmetric=symmetric)
+    g._w_csr  # build W eagerly: the hot path needs it; errors surface here
+    return g
+
+
+def _device_arcs(edges, n: int, weights=None):
+    """Arc arrays (src, dst int64, w float64|None) on the device (graph.py:106-132)."""
     if isinstance(edges, tuple) and len(edges) == 2 and isinstance(edges[0], torch.Tensor):
         src, dst = (e.to(device=_device(), dtype=torch.int64) for e in edges)
         w = None if weights is None else torch.as_tensor(weights, dtype=torch.float64, device=_device())
@@ -237,9 +245,7 @@ def from_edges(edges, n: int, weights=None, *, symmetric: bool = False) -> Spars
         if hs.size and (min(hs.min(), hd.min()) < 0 or max(hs.max(), hd.max()) >= n):
             raise DomainError("edge endpoint out of range")
         src, dst, w = _to_device(hs, torch.int64), _to_device(hd, torch.int64), _to_device(hw, torch.float64)
-    g = SparseGraph(n, src, dst, w, is_symmetric=symmetric)
-    g._w_csr  # build W eagerly: the hot path needs it; errors surface here
-    return g
+    return src, dst, w
 
 
 def empty_graph(n: int = 0) -> SparseGraph:
