@@ -401,6 +401,34 @@ def gram_roofline(n, l, precision):
             "shape": f"{n}x{m} -> {m}x{m}", "ms_per_launch": ms, "kernel": "spb::gram_dmma"}
 
 
+def csr_roofline(spb, src, dst, n, nnz_w, reps=5):
+    """(a) CSR build (from_edges: validate, emit, radix sort, segmented sums, row_ptr,
+    degrees) timed alone with CUDA events, against HBM: algorithmic bytes = the arc
+    list in (2 x int64 per arc) + W out (int32 row_ptr, int32 col + float64 val per
+    entry, float64 degrees) -- SURVEY §8(d) with this build's output formats."""
+    import torch
+
+    m = int(src.numel())
+    for _ in range(2):
+        spb.from_edges((src, dst), n)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(reps):
+        spb.from_edges((src, dst), n)
+    e1.record()
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / reps
+    nbytes = 16.0 * m + 4.0 * (n + 1) + 12.0 * nnz_w + 8.0 * n
+    peak, kind = load_peaks()
+    gbs = nbytes / (ms * 1e-3) / 1e9
+    return {"bound": "hbm", "achieved": gbs, "peak": peak, "unit": "GB/s", "frac": gbs / peak,
+            "peak_kind": kind, "ms_per_build": ms, "bytes": nbytes, "arcs": m, "nnz_w": nnz_w,
+            "note": "whole build (all its kernels and its two host synchronisations) per from_edges "
+                    "call; the LSD radix sort moves 12 B per entry per 8-bit pass, "
+                    "ceil(2 * key_bits(n) / 8) passes, on top of the algorithmic bytes"}
+
+
 def run_ours(args):
     import torch
 
@@ -496,6 +524,7 @@ def run_ours(args):
     gather_bytes = spmm_bytes + esz * nnz_w * sum(s["spmm_cols"] for s in stats)
     gather_achieved = (gather_bytes / (spmm_us * 1e-6)) / 1e9 if spmm_us else None
     gram = gram_roofline(spec.n, l, args.precision)
+    csr = csr_roofline(spb, src, dst, spec.n, nnz_w)
     traffic = None
     tf = ROOT / "profiles" / "spmm_traffic.json"
     if tf.exists():
@@ -575,6 +604,7 @@ def run_ours(args):
                                           "frac": (gather_achieved / peak) if gather_achieved else None,
                                           "bytes_model": "compulsory + esz*nnz*cols"},
                          "gram": gram,
+                         "csr_build": csr,
                          "note": ("roofline of the path's HBM-streaming kernel (SpMM) and of the "
                                   "Rayleigh-Ritz Gram (DMMA); the step's time split by kernel is "
                                   "kernel_shares (latency-bound small dense solves dominate at C1/C2)")},

@@ -142,7 +142,7 @@ def static_case(cfg_name, max_iter, ten_x, fname, seed=0):
     np.savez_compressed(HERE / fname, **out)
 
 
-def stream_case():
+def stream_case(sens=False):
     spec = CONFIGS["c2"]
     edges, truth = generate_dcsbm(spec)
     k = spec.blocks
@@ -159,10 +159,11 @@ def stream_case():
                      truth),
         "snowball": (snow, truth[np.argsort(relabel)]),
     }
+    fname = "stream_c5_sens.npz" if sens else "stream_c5.npz"
     for mode, (st, tr) in streams.items():
         stages = [rstr.StreamStage(index=i + 1, mode=mode, edge_delta=d, n_after=n)
                   for i, (d, n) in enumerate(st)]
-        for init in ("warm", "random"):
+        for init in (("warm",) if sens else ("warm", "random")):
             cfg = rl.SolverConfig(block_size=l, tol=tol, max_iter=30, seed=spec.seed)
             hists = []
             orig = rstr.lobpcg_solve
@@ -194,7 +195,7 @@ def stream_case():
             out[f"{key}/labels_last"] = res[-1].partition.labels.astype(np.uint8)
             print(key, [r.iterations for r in res],
                   [round(r.wall_time, 1) for r in res], flush=True)
-            np.savez_compressed(HERE / "stream_c5.npz", **out)
+            np.savez_compressed(HERE / fname, **out)
 
 
 def main():
@@ -208,6 +209,11 @@ def main():
         static_case("c4", 30, True, "large_c4full.npz")
     elif what == "c5":
         stream_case()
+    elif what == "c5sens":
+        # the reference's own round-off sensitivity: the warm streams again with
+        # OPENBLAS_NUM_THREADS=8 (a different BLAS summation order)
+        assert os.environ.get("OPENBLAS_NUM_THREADS") == "8"
+        stream_case(sens=True)
     else:
         raise SystemExit(f"unknown case {what}")
 

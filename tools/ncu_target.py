@@ -1,4 +1,7 @@
-"""Small deterministic target for ncu: warm-up + one C2 partition step (no profiler inside)."""
+"""Small deterministic target for ncu: N partition steps of a config (no profiler inside).
+
+    python tools/ncu_target.py [c2|c3|c4] [steps]
+"""
 import sys
 from pathlib import Path
 
@@ -21,7 +24,12 @@ dev = torch.device("cuda", 0)
 src = torch.from_numpy(np.ascontiguousarray(edges[:, 0])).to(dev)
 dst = torch.from_numpy(np.ascontiguousarray(edges[:, 1])).to(dev)
 x0_d = torch.from_numpy(x0).to(dev)
-cfg = spb.SolverConfig(block_size=l, tol=1e-12, max_iter=20, seed=0)
+tol, max_iter = 1e-12, 20
+if cfg_name in ("c3", "c4"):  # the 10x stop rule the reference produced (bench.golden_tol)
+    import bench
+
+    tol, max_iter = bench.golden_tol(cfg_name) or 1e-12, 30
+cfg = spb.SolverConfig(block_size=l, tol=tol, max_iter=max_iter, seed=0)
 for _ in range(steps):
     g = spb.from_edges((src, dst), spec.n)
     partition_device(g, cfg, k, fix_k=True, x0=x0_d)
