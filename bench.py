@@ -462,18 +462,22 @@ def run_ours(args):
     sharded = world > 1 and args.config in ("c3", "c4")
     comm = None
     if sharded:
-        from paper_1708_07481_b200.sharded import RowShardedLaplacian, _Comm, partition_static_sharded
+        from paper_1708_07481_b200.graph import SparseGraph
+        from paper_1708_07481_b200.sharded import (RowShardedLaplacian, _Comm,
+                                                   partition_edges_sharded, partition_static_sharded)
 
         comm = _Comm()
 
     def step_device():
-        g = spb.from_edges((src, dst), spec.n)
         if sharded:
+            # each rank builds only its rows of W from the arc list (no whole-graph CSR)
+            g = SparseGraph(spec.n, src, dst, None)
             op = RowShardedLaplacian(g, comm=comm)
             part_, st, gap = partition_static_sharded(g, cfg, k, fix_k=True, x0=x0_d,
                                                       precision=args.precision, op=op)
-            stats.append(dict(st.solve_stats, spmm_us=0, spmm_bytes=0))
+            stats.append(st.solve_stats)
             return part_, st
+        g = spb.from_edges((src, dst), spec.n)
         labels, kf, st, gap = partition_device(g, cfg, k, fix_k=True, x0=x0_d,
                                                precision=args.precision)
         stats.append(st.solve_stats)
@@ -540,12 +544,11 @@ def run_ours(args):
     for i in range(args.steps):
         torch.cuda.synchronize()
         t0 = time.perf_counter()
-        g = spb.from_edges(edges_host, spec.n)
         if sharded:
-            part, st, gap = partition_static_sharded(g, cfg, k, fix_k=True, x0=x0,
-                                                     precision=args.precision,
-                                                     op=RowShardedLaplacian(g, comm=comm))
+            part, st, gap = partition_edges_sharded(edges_host, spec.n, cfg, k, comm=comm,
+                                                    fix_k=True, x0=x0, precision=args.precision)
         else:
+            g = spb.from_edges(edges_host, spec.n)
             part, st, gap = spb.partition_static(g, cfg, k, fix_k=True, x0=x0,
                                                  precision=args.precision)
         torch.cuda.synchronize()

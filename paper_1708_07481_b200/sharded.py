@@ -24,6 +24,7 @@ kernel on every rank, so every rank returns the same labels.
 from __future__ import annotations
 
 import ctypes as C
+import os
 
 import numpy as np
 import torch
@@ -259,7 +260,7 @@ def lobpcg_solve_sharded(op: RowShardedLaplacian, x0, config: SolverConfig, n_co
     ws = torch.empty(wsb, dtype=torch.uint8, device=dev)
     cfg = N.SolverConfigC(block_size=l, max_iter=config.max_iter, tol=config.tol,
                           lock_tol=config.lock_tol, n_converge=nc, deflate_ones=int(config.deflate_ones),
-                          has_precond=0, reserved=0)
+                          has_precond=0, reserved=1 if os.environ.get("SPB_PROFILE_SPMM") == "1" else 0)
     bridge = _Bridge(callback, np.random.default_rng(config.seed), None, l)
     theta, norms, conv, stats = (C.c_double * l)(), (C.c_double * l)(), (C.c_uint8 * l)(), (C.c_int64 * 16)()
     status = L.spb_lobpcg_solve_sharded(C.byref(native), C.byref(sh), code, N.ptr(x0_d), C.byref(cfg),
@@ -279,6 +280,8 @@ def lobpcg_solve_sharded(op: RowShardedLaplacian, x0, config: SolverConfig, n_co
                            np.array(conv[:], dtype=bool), work_blocks=6)
         state.solve_stats = dict(zip(("iterations", "spmm_calls", "rr_calls", "drop_p",
                                       "rebuild", "orth_p"), [int(x) for x in stats[:6]]))
+        state.solve_stats.update(spmm_us=int(stats[7]), spmm_bytes=int(stats[8]),
+                                 spmm_cols=int(stats[9]))
         state.row_range = (op.row_begin, op.row_end)
     if status == N.OK:
         return state
