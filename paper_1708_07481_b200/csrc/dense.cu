@@ -20,98 +20,8 @@
 namespace spb {
 namespace {
 
-// ----------------------------------------------------------------------------
-// Gram: 64x64 output tile per CTA, 128 threads, 8x4 fp64 micro-tile each.
-// Operands stay in their storage type in shared memory (double-buffered,
-// 32-row chunks) and are widened to fp64 in registers; the next chunk's global
-// loads are issued before the current chunk's FMAs (register prefetch).
 constexpr int GT = 64;
 constexpr int GK = 32;
-
-template <typename T>
-__global__ void __launch_bounds__(128)
-gram_kernel(GramBatch b, int64_t n, int64_t kchunk, int ldo, int64_t split_stride,
-            double* __restrict__ part) {
-  constexpr int GK = sizeof(T) == 4 ? 32 : 16;  // static smem <= 48 KB
-  __shared__ T Us[2][GK][GT];
-  __shared__ T Vs[2][GK][GT];
-  const int tile = blockIdx.x;
-  int j = 0;
-  while (j + 1 < b.njobs && tile >= b.tile_start[j + 1]) ++j;
-  const GramJob jb = b.job[j];
-  const int local = tile - b.tile_start[j];
-  const int tq_count = (jb.q + GT - 1) / GT;
-  const int tp = local / tq_count, tq = local % tq_count;
-  const int p0 = tp * GT, q0 = tq * GT;
-  const int64_t k0 = (int64_t)blockIdx.y * kchunk;
-  const int64_t k1 = min(n, k0 + kchunk);
-  const int tid = threadIdx.x, tx = tid & 15, ty = tid >> 4;  // ty 0..7 (8 rows), tx 0..15 (4 cols)
-  const T* U = (const T*)jb.U;
-  const T* V = (const T*)jb.V;
-  // loader mapping: 2 * GK * GT elements per chunk, 32 per thread
-  constexpr int PER = GK * GT / 128;  // 16 per operand
-  T ru[PER], rv[PER];
-  auto load = [&](int64_t kb) {
-#pragma unroll
-    for (int t = 0; t < PER; ++t) {
-      const int e = tid + 128 * t;
-      const int r = e / GT, c = e % GT;
-      const int64_t k = kb + r;
-      ru[t] = (k < k1 && p0 + c < jb.p) ? U[k * jb.ldu + p0 + c] : T(0);
-      rv[t] = (k < k1 && q0 + c < jb.q) ? V[k * jb.ldv + q0 + c] : T(0);
-    }
-  };
-  auto store = [&](int buf) {
-#pragma unroll
-    for (int t = 0; t < PER; ++t) {
-      const int e = tid + 128 * t;
-      const int r = e / GT, c = e % GT;
-      Us[buf][r][c] = ru[t];
-      Vs[buf][r][c] = rv[t];
-    }
-  };
-  double acc[8][4];
-#pragma unroll
-  for (int a = 0; a < 8; ++a)
-#pragma unroll
-    for (int c = 0; c < 4; ++c) acc[a][c] = 0.0;
-  int buf = 0;
-  if (k0 < k1) {
-    load(k0);
-    store(0);
-  }
-  __syncthreads();
-  for (int64_t kb = k0; kb < k1; kb += GK) {
-    const bool more = kb + GK < k1;
-    if (more) load(kb + GK);
-#pragma unroll 8
-    for (int k = 0; k < GK; ++k) {
-      double av[8], bv[4];
-#pragma unroll
-      for (int i = 0; i < 8; ++i) av[i] = (double)Us[buf][k][ty * 8 + i];
-#pragma unroll
-      for (int i = 0; i < 4; ++i) bv[i] = (double)Vs[buf][k][tx * 4 + i];
-#pragma unroll
-      for (int x = 0; x < 8; ++x)
-#pragma unroll
-        for (int y = 0; y < 4; ++y) acc[x][y] = fma(av[x], bv[y], acc[x][y]);
-    }
-    if (more) store(buf ^ 1);
-    __syncthreads();
-    buf ^= 1;
-  }
-  double* out = part + (int64_t)blockIdx.y * split_stride;
-#pragma unroll
-  for (int x = 0; x < 8; ++x) {
-    const int i = p0 + ty * 8 + x;
-    if (i >= jb.p) continue;
-#pragma unroll
-    for (int y = 0; y < 4; ++y) {
-      const int c = q0 + tx * 4 + y;
-      if (c < jb.q) out[(int64_t)(jb.out_r + i) * ldo + jb.out_c + c] = acc[x][y];
-    }
-  }
-}
 
 // Gram on the FP64 tensor pipe: mma.sync m8n8k4 f64 (DMMA). 64x64 output tile
 // per CTA, 4 warps as 2x2 of 32x32 (4x4 DMMA tiles each). Operands are widened
@@ -345,8 +255,8 @@ int launch_gram_cfg(GramBatch bb, int64_t n, int out_rows, int out_cols, double*
   }
   bb.tile_start[bb.njobs] = tiles;
   int64_t ks = std::max<int64_t>(1, (int64_t)ctas_per_sm * num_sms() / std::max(tiles, 1));
-  static const int minrows = getenv("SPB_GRAM_MINROWS") ? atoi(getenv("SPB_GRAM_MINROWS")) : 128;
-  ks = std::min<int64_t>(ks, ceil_div(n, std::max(32, minrows)));
+  constexpr int minrows = 128;  // rows per split at least
+  ks = std::min<int64_t>(ks, ceil_div(n, minrows));
   ks = std::max<int64_t>(ks, 1);
   while (ks > 1 && (size_t)ks * out_rows * out_cols > partial_cap) --ks;
   if ((size_t)ks * out_rows * out_cols > partial_cap) {
@@ -373,8 +283,6 @@ int launch_gram_cfg(GramBatch bb, int64_t n, int out_rows, int out_cols, double*
 // (A 176-wide tile for C4 needs more accumulator registers than a warp grid
 // of <= 32 warps can hold; 64-tiles pad 176 -> 192, 1.19x.)
 int gram_tile_for(const GramBatch& b) {
-  static const int forced = getenv("SPB_GRAM_TILE") ? atoi(getenv("SPB_GRAM_TILE")) : 0;
-  if (forced == 56 || forced == 64 || forced == 88 || forced == 112) return forced;
   int wmin = 1 << 30, wmax = 0;
   for (int j = 0; j < b.njobs; ++j) {
     wmax = std::max(wmax, std::max(b.job[j].p, b.job[j].q));
@@ -428,12 +336,11 @@ int sum_splits_grid(int64_t total) {
 int choose_ksplit(int64_t n, int tiles) {
   // one full wave of the DMMA Gram (3 CTAs per SM): tiles * ks <= 3 * SMs; the
   // per-SM work is the same for fewer, longer splits, but the fixed-order
-  // reduction reads ks partial tiles, so SPB_GRAM_WAVE can trade the two
-  static const int per_sm = getenv("SPB_GRAM_WAVE") ? atoi(getenv("SPB_GRAM_WAVE")) : 3;
-  const int target = std::max(1, per_sm) * num_sms();
+  // reduction reads ks partial tiles (2 and 4 CTAs per SM measured slower)
+  const int target = 3 * num_sms();
   int64_t ks = std::max<int64_t>(1, target / std::max(tiles, 1));
-  static const int minrows = getenv("SPB_GRAM_MINROWS") ? atoi(getenv("SPB_GRAM_MINROWS")) : 128;
-  ks = std::min<int64_t>(ks, ceil_div(n, std::max(32, minrows)));
+  constexpr int minrows = 128;  // rows per split at least
+  ks = std::min<int64_t>(ks, ceil_div(n, minrows));
   return (int)std::max<int64_t>(ks, 1);
 }
 
@@ -681,19 +588,13 @@ static int g_update_mode = -1;  // spb_block_update's override (-1: default)
 
 template <typename T>
 void launch_update(const UpdParams& p, int64_t n, cudaStream_t st) {
-  static const bool generic = getenv("SPB_UPDATE_GENERIC") != nullptr;  // A/B switch
-  // float32: 3xTF32 on the tensor cores (update_tc.cu) unless SPB_UPDATE_TC=0
-  static const bool tc_env = !getenv("SPB_UPDATE_TC") || atoi(getenv("SPB_UPDATE_TC")) != 0;
-  const bool tc = g_update_mode < 0 ? tc_env : g_update_mode == 1;
-  if (sizeof(T) == 4 && tc && !generic && update_tc(p, n, st)) return;
-  // narrow blocks (q <= 64, C1/C2) measure faster on the generic kernel
-  static const int narrow = getenv("SPB_UPDATE_NARROW") ? atoi(getenv("SPB_UPDATE_NARROW")) : 0;
-  if (sizeof(T) == 4 && !generic && narrow && p.q > 32 && p.q <= 64 && update_f32_ok(p)) {
-    if (narrow == 1) launch_update_f32<8, 16>(p, n, st);
-    else launch_update_f32<8, 32>(p, n, st);
-    return;
-  }
-  if (sizeof(T) == 4 && !generic && p.q > 64 && update_f32_ok(p)) {
+  // float32: 3xTF32 on the tensor cores (update_tc.cu) unless spb_block_update
+  // asked for the FMA kernel (mode 0)
+  const bool tc = g_update_mode != 0;
+  if (sizeof(T) == 4 && tc && update_tc(p, n, st)) return;
+  // (narrow blocks, q <= 64 at C1/C2: the generic kernel below measured faster than
+  // update_f32's 8-row-group variants)
+  if (sizeof(T) == 4 && p.q > 64 && update_f32_ok(p)) {
     if (p.q <= 128) launch_update_f32<16, 8>(p, n, st);
     else if (p.q <= 192) launch_update_f32<24, 8>(p, n, st);
     else launch_update_f32<32, 8>(p, n, st);
@@ -920,16 +821,9 @@ int gram_batched(int dtype, const GramBatch& b, int64_t n, int out_rows, int out
   const int64_t kchunk = round_up(ceil_div(std::max<int64_t>(n, 1), ks), GK);
   const int64_t stride = (int64_t)out_rows * out_cols;
   dim3 grid(tiles, ks);
-  static const bool use_fma = getenv("SPB_GRAM_FMA") != nullptr;  // A/B switch (CUDA-core DFMA)
-  if (n > 0 && use_fma) {
-    if (dtype == SPB_F32)
-      gram_kernel<float><<<grid, 128, 0, st>>>(b, n, kchunk, out_cols, stride, partial);
-    else
-      gram_kernel<double><<<grid, 128, 0, st>>>(b, n, kchunk, out_cols, stride, partial);
-    SPB_LAUNCH_CHECK();
-  } else if (n > 0 && gram_tile_for(b) == 56) {
+  if (n > 0 && gram_tile_for(b) == 56) {
     // 56 x 56: 7 warps of 8 x 56 (1 x 7 m8n8 tiles each), two CTAs per SM in the split
-    static const int cps = getenv("SPB_GRAM56_CPS") ? atoi(getenv("SPB_GRAM56_CPS")) : 2;
+    constexpr int cps = 2;
     const int rc =
         dtype == SPB_F32
             ? launch_gram_cfg<float, 1, 7, 7, 1, 32>(b, n, out_rows, out_cols, partial, partial_cap,

@@ -513,10 +513,6 @@ struct Driver {
                          seg2));
     SmallStatus hs;
     SPB_TRY(read_status(&hs));
-    static const bool dbg = getenv("SPB_DEBUG_COND") != nullptr;  // diagnostics
-    if (dbg)
-      fprintf(stderr, "rr m=%d seg=%d,%d cond=[%.3g, %.3g] state=%d\n", m, seg1, seg2, hs.cond_lo,
-              hs.cond_hi, hs.cond_state);
     *ok = 0;
     if (hs.nonfinite || hs.not_pd || hs.cond_state == 1) return SPB_OK;
     // float32 storage: the images L[X R P] carry float32 rounding, so G_A is not the

@@ -875,8 +875,7 @@ void launch_small_gemm(int ta, int tb, int M, int N, int K, const double* A, int
                        const double* B, int ldb, double* C, int ldc, cudaStream_t st) {
   dim3 grid((unsigned)((N + 31) / 32), (unsigned)((M + 31) / 32));
   const size_t smem = sizeof(double) * 64 * (size_t)(K | 1);
-  static const int tiled = getenv("SPB_SMALL_GEMM_TILED") ? atoi(getenv("SPB_SMALL_GEMM_TILED")) : 0;
-  if (!((tiled >> (ta * 2 + tb)) & 1) && smem <= 200 * 1024) {
+  if (smem <= 200 * 1024) {
     static std::atomic<uint64_t> attr{0};
     if (!done_on_device(attr)) {
       cudaFuncSetAttribute(small_gemm_fk, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
@@ -1004,7 +1003,9 @@ tridiag(const double* __restrict__ Asrc, int m, int symmetrize, double* __restri
   }
 }
 
-// Cluster variant (m in [kTriClusterMin, kTriClusterMax]): the columns of the
+// Cluster reduction (m in [kTriClusterMin, kTriClusterMax]; round 1 also had a
+// cluster-barrier variant and a fused one-exchange variant, both measured slower
+// and removed): the columns of the
 // matrix are split over the C CTAs of one thread-block cluster and stay in their
 // shared memory for the whole reduction; per step k every CTA
 //   (1) forms the reflector of row k redundantly from an all-gathered copy of
@@ -1028,156 +1029,6 @@ __device__ __forceinline__ void dsmem_store(double* local_addr, int rank, double
   uint32_t a = (uint32_t)__cvta_generic_to_shared(local_addr), r;
   asm volatile("mapa.shared::cluster.u32 %0, %1, %2;\n" : "=r"(r) : "r"(a), "r"(rank));
   asm volatile("st.shared::cluster.f64 [%0], %1;\n" ::"r"(r), "d"(v) : "memory");
-}
-
-__global__ void __launch_bounds__(TCT)
-tridiag_cluster(const double* __restrict__ Asrc, int m, int symmetrize, double* __restrict__ V,
-                double* __restrict__ tau, double* __restrict__ d, double* __restrict__ e,
-                const SmallStatus* status) {
-  if (status && (status->nonfinite || status->not_pd)) return;  // uniform over the cluster
-  unsigned rank_u, csize_u;
-  asm volatile("mov.u32 %0, %%cluster_ctarank;\n" : "=r"(rank_u));
-  asm volatile("mov.u32 %0, %%cluster_nctarank;\n" : "=r"(csize_u));
-  const int rank = (int)rank_u, C = (int)csize_u;
-  const int nc = (m + C - 1) / C;
-  const int c0 = rank * nc;
-  const int ncl = max(0, min(m, c0 + nc) - c0);
-  extern __shared__ double tsm[];
-  double* Wl = tsm;                        // m x nc, row j / local column c
-  double* rowbuf = Wl + (size_t)m * nc;    // [2][m]  row k (all-gathered)
-  double* pbuf = rowbuf + 2 * m;           // [2][m]  p (all-gathered)
-  double* vbuf = pbuf + 2 * m;             // [m]     v of the current step
-  double* dotbuf = vbuf + m;               // [2][16] per-CTA shares of p'v
-  double* red = dotbuf + 32;               // [G][nc]
-  __shared__ double wdot[2];
-  __shared__ double sc[2];
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int G = TCT / nc;
-  const int g = tid / nc, lc = tid - (tid / nc) * nc;
-  const bool active = g < G && lc < ncl;
-  const int icol = c0 + lc;
-  for (int x = tid; x < m * ncl; x += TCT) {
-    const int j = x / ncl, c = x - (x / ncl) * ncl, i = c0 + c;
-    const double a = Asrc[(int64_t)j * m + i];
-    Wl[j * nc + c] = symmetrize ? 0.5 * (a + Asrc[(int64_t)i * m + j]) : a;
-    V[(int64_t)j * m + i] = 0.0;
-  }
-  __syncthreads();
-  for (int x = tid; x < ncl * C; x += TCT) {
-    const int r = x / ncl, c = x - (x / ncl) * ncl;
-    dsmem_store(rowbuf + c0 + c, r, Wl[c]);
-  }
-  cluster_sync_all();
-  for (int k = 0; k + 2 < m; ++k) {
-    const int b = k & 1;
-    const double* row = rowbuf + b * m;
-    double* pb = pbuf + b * m;
-    double* nextrow = rowbuf + (b ^ 1) * m;
-    // (1) reflector of row k (warp 0), v into vbuf
-    if (warp == 0) {
-      double ss = 0.0;
-      for (int i = k + 2 + lane; i < m; i += 32) ss = fma(row[i], row[i], ss);
-      ss = warp_sum(ss);
-      const double alpha = row[k + 1];
-      double tk = 0.0, scale = 0.0, beta = alpha;
-      if (ss != 0.0) {
-        beta = -copysign(sqrt(alpha * alpha + ss), alpha);
-        tk = (beta - alpha) / beta;
-        scale = 1.0 / (alpha - beta);
-      }
-      for (int i = k + 1 + lane; i < m; i += 32) vbuf[i] = i == k + 1 ? 1.0 : row[i] * scale;
-      if (lane == 0) {
-        sc[0] = tk;
-        if (rank == 0) {
-          d[k] = row[k];
-          e[k] = beta;
-          tau[k] = tk;
-        }
-      }
-    }
-    __syncthreads();
-    const double tk = sc[0];
-    const int j0 = k + 1 + g;
-    const bool own = active && icol > k;
-    if (tid < ncl && icol > k) V[(int64_t)k * m + icol] = vbuf[icol];
-    if (tk == 0.0) {  // identity reflector: row k+1 is unchanged, pass it on
-      if (tid < ncl && icol > k) {
-        const double wv = Wl[(k + 1) * nc + tid];
-        for (int r = 0; r < C; ++r) dsmem_store(nextrow + icol, r, wv);
-      }
-      cluster_sync_all();
-      continue;
-    }
-    // (2) p = tau W v on own columns
-    if (own) {
-      double a0 = 0.0, a1 = 0.0;
-      const double* wp = Wl + j0 * nc + lc;
-      const double* vp = vbuf + j0;
-      const int step = G * nc;
-      int j = j0;
-      for (; j + G < m; j += 2 * G, wp += 2 * step, vp += 2 * G) {
-        a0 = fma(wp[0], vp[0], a0);
-        a1 = fma(wp[step], vp[G], a1);
-      }
-      if (j < m) a0 = fma(wp[0], vp[0], a0);
-      red[g * nc + lc] = a0 + a1;
-    }
-    __syncthreads();
-    if (tid < 64) {
-      double pv = 0.0;
-      if (tid < ncl && icol > k) {
-        double sacc = 0.0;
-        const int gmax = min(G, m - (k + 1));  // groups that saw a row
-        for (int q = 0; q < gmax; ++q) sacc += red[q * nc + tid];
-        const double p = tk * sacc;
-        pv = p * vbuf[icol];
-        for (int r = 0; r < C; ++r) dsmem_store(pb + icol, r, p);
-      }
-      pv = warp_sum(pv);
-      if (lane == 0) wdot[tid >> 5] = pv;
-      asm volatile("bar.sync 1, 64;\n" ::: "memory");
-      if (tid < C) dsmem_store(dotbuf + b * 16 + rank, tid, wdot[0] + wdot[1]);
-    }
-    cluster_sync_all();
-    // (3) rank-2 update of own columns, push row k+1
-    if (own) {
-      double tot = 0.0;
-      for (int r = 0; r < C; ++r) tot += dotbuf[b * 16 + r];
-      const double K = 0.5 * tk * tot;
-      const double vi = vbuf[icol];
-      const double wi = fma(-K, vi, pb[icol]);
-      double* wp = Wl + j0 * nc + lc;
-      const double* vp = vbuf + j0;
-      const double* pp = pb + j0;
-      const int step = G * nc;
-      int j = j0;
-      if (g == 0) {  // row k+1 goes to every CTA for the next reflector
-        const double wj = fma(-K, vp[0], pp[0]);
-        const double wv = fma(-vp[0], wi, fma(-wj, vi, wp[0]));
-        wp[0] = wv;
-        for (int r = 0; r < C; ++r) dsmem_store(nextrow + icol, r, wv);
-        j += G, wp += step, vp += G, pp += G;
-      }
-#pragma unroll 2
-      for (; j < m; j += G, wp += step, vp += G, pp += G) {
-        const double vj = vp[0];
-        const double wj = fma(-K, vj, pp[0]);
-        wp[0] = fma(-vj, wi, fma(-wj, vi, wp[0]));
-      }
-    }
-    cluster_sync_all();
-  }
-  if (m >= 2) {
-    const double* row = rowbuf + ((m - 2) & 1) * m;
-    if (rank == 0 && tid == 0) {
-      d[m - 2] = row[m - 2];
-      e[m - 2] = row[m - 1];
-      tau[m - 2] = 0.0;
-      tau[m - 1] = 0.0;
-      e[m - 1] = 0.0;
-    }
-    if (tid == 0 && m - 1 >= c0 && m - 1 < c0 + ncl) d[m - 1] = Wl[(m - 1) * nc + (m - 1 - c0)];
-  }
 }
 
 // Same reduction with the two per-step exchanges carried by st.async stores that
@@ -1435,189 +1286,6 @@ tridiag_cluster_mb(const double* __restrict__ Asrc, int m, int symmetrize, doubl
       }
     }
     if (tid == 0 && m - 1 >= c0 && m - 1 < c0 + ncl) d[m - 1] = Wl[(m - 1) * nc + (m - 1 - c0)];
-  }
-  cluster_sync_all();  // no CTA leaves while its shared memory can still be written
-}
-
-// One exchange per step. Exchange E_k carries p_k = tau_k W v_k (own columns),
-// each CTA's share of p_k'v_k, and each CTA's slice of row k+1 BEFORE update k.
-// Every CTA then forms w_k = p_k - K v_k for all indices, applies update k to
-// the gathered row k+1 itself (the same fma the owner uses, so the copies agree
-// bit for bit) and computes reflector k+1 redundantly; one fused pass over its
-// own columns applies update k and accumulates p_{k+1} with v_{k+1}; the row
-// k+2 slice falls out of the same pass. The exchange parity buffers are safe to
-// reuse because E_{k+1} can only be sent after every CTA sent E_k.
-__global__ void __launch_bounds__(TCT)
-tridiag_fused(const double* __restrict__ Asrc, int m, int symmetrize, double* __restrict__ V,
-              double* __restrict__ tau, double* __restrict__ d, double* __restrict__ e,
-              const SmallStatus* status) {
-  if (status && (status->nonfinite || status->not_pd)) return;  // uniform over the cluster
-  unsigned rank_u, csize_u;
-  asm volatile("mov.u32 %0, %%cluster_ctarank;\n" : "=r"(rank_u));
-  asm volatile("mov.u32 %0, %%cluster_nctarank;\n" : "=r"(csize_u));
-  const int rank = (int)rank_u, C = (int)csize_u;
-  const int nc = (m + C - 1) / C;
-  const int c0 = rank * nc;
-  const int ncl = max(0, min(m, c0 + nc) - c0);
-  extern __shared__ double tsm[];
-  double* Wl = tsm;                        // m x nc, row j / local column c
-  double* xrow = Wl + (size_t)m * nc;      // [2][m] gathered row slices (row k+1 before update k)
-  double* xp = xrow + 2 * m;               // [2][m] gathered p
-  double* vb = xp + 2 * m;                 // [2][m] v_k by parity
-  double* wv = vb + 2 * m;                 // [m]    w_k
-  double* xdot = wv + m;                   // [2][16]
-  double* red = xdot + 32;                 // [G][nc]
-  __shared__ double wdot[2];
-  __shared__ double sc[4];  // tau by parity
-  __shared__ __align__(8) uint64_t mbE[2], mbI;
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int G = TCT / nc;
-  const int g = tid / nc, lc = tid - (tid / nc) * nc;
-  const bool active = g < G && lc < ncl;
-  const int icol = c0 + lc;
-  if (tid == 0) {
-    mb_init(&mbE[0], 1);
-    mb_init(&mbE[1], 1);
-    mb_init(&mbI, 1);
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  }
-  for (int x = tid; x < m * ncl; x += TCT) {
-    const int j = x / ncl, c = x - (x / ncl) * ncl, i = c0 + c;
-    const double a = Asrc[(int64_t)j * m + i];
-    Wl[j * nc + c] = symmetrize ? 0.5 * (a + Asrc[(int64_t)i * m + j]) : a;
-    V[(int64_t)j * m + i] = 0.0;
-  }
-  cluster_sync_all();
-  // row 0 to everyone (reflector 0), into xrow[1] (free until E_1)
-  for (int x = tid; x < ncl * C; x += TCT) {
-    const int r = x / ncl, c = x - (x / ncl) * ncl;
-    st_async_f64(xrow + m + c0 + c, &mbI, r, Wl[c]);
-  }
-  // warp 0: Householder reflector of a gathered row `row` at step kk -> vb[kk&1], sc
-  auto reflect = [&](const double* row, int kk) {
-    double ss = 0.0;
-    for (int i = kk + 2 + lane; i < m; i += 32) ss = fma(row[i], row[i], ss);
-    ss = warp_sum(ss);
-    const double alpha = row[kk + 1];
-    double tk = 0.0, scale = 0.0, beta = alpha;
-    if (ss != 0.0) {
-      beta = -copysign(sqrt(alpha * alpha + ss), alpha);
-      tk = (beta - alpha) / beta;
-      scale = 1.0 / (alpha - beta);
-    }
-    double* v = vb + (kk & 1) * m;
-    for (int i = kk + 1 + lane; i < m; i += 32) v[i] = i == kk + 1 ? 1.0 : row[i] * scale;
-    if (lane == 0) {
-      sc[kk & 1] = tk;
-      if (rank == 0) {
-        d[kk] = row[kk];
-        e[kk] = beta;
-        tau[kk] = tk;
-      }
-    }
-  };
-  // p_kk partial over own columns i > kk with v = vb[kk&1]; red + push E_kk (p, dot, row kk+1 slice)
-  auto push_exchange = [&](int kk, double acc, double rowslice) {
-    const int bb = kk & 1;
-    if (active && icol > kk) red[g * nc + lc] = acc;
-    __syncthreads();
-    if (tid < 64) {
-      double pv = 0.0;
-      if (tid < ncl && icol > kk) {
-        double sacc = 0.0;  // every group wrote its slot (zero when it saw no row)
-        for (int q = 0; q < G; ++q) sacc += red[q * nc + tid];
-        const double p = sc[bb] * sacc;
-        pv = p * vb[bb * m + icol];
-        for (int r = 0; r < C; ++r) st_async_f64(xp + bb * m + icol, &mbE[bb], r, p);
-      }
-      pv = warp_sum(pv);
-      if (lane == 0) wdot[tid >> 5] = pv;
-      asm volatile("bar.sync 1, 64;\n" ::: "memory");
-      if (tid < C) st_async_f64(xdot + bb * 16 + rank, &mbE[bb], tid, wdot[0] + wdot[1]);
-    }
-    // row kk+1 slice (before update kk) from the g == 0 thread of each own column i > kk
-    if (active && g == 0 && icol > kk)
-      for (int r = 0; r < C; ++r) st_async_f64(xrow + bb * m + icol, &mbE[bb], r, rowslice);
-  };
-  if (m > 2) {
-    if (warp == 0) {
-      if (lane == 0) mb_expect(&mbI, 8u * (uint32_t)m);
-      mb_wait(&mbI, 0);
-      reflect(xrow + m, 0);
-    }
-    __syncthreads();
-    // pass 0: p_0 = tau_0 A v_0 on own columns, row 1 slice
-    double acc = 0.0, rs = 0.0;
-    if (active && icol > 0) {
-      const double* v = vb;
-      for (int j = 1 + g; j < m; j += G) acc = fma(Wl[j * nc + lc], v[j], acc);
-      rs = Wl[1 * nc + lc];
-      if (icol >= 1 && tid < ncl) V[icol] = v[icol];
-    }
-    push_exchange(0, acc, rs);
-  }
-  for (int k = 0; k + 2 < m; ++k) {
-    const int b = k & 1;
-    if (tid == 0) mb_expect(&mbE[b], 8u * (uint32_t)(2 * (m - k - 1) + C));
-    mb_wait(&mbE[b], (uint32_t)((k >> 1) & 1));
-    const double tk = sc[b];
-    const double* v = vb + b * m;
-    const double* pk = xp + b * m;
-    double tot = 0.0;
-    for (int r = 0; r < C; ++r) tot += xdot[b * 16 + r];
-    const double K = 0.5 * tk * tot;
-    for (int j = k + 1 + tid; j < m; j += TCT) wv[j] = fma(-K, v[j], pk[j]);
-    __syncthreads();
-    const bool more = k + 3 < m;  // a reflector k+1 exists
-    if (warp == 0) {
-      // updated row k+1 (entries i >= k+1), as the owner's fused pass computes them
-      double* row = xrow + b * m;
-      const double wk1 = wv[k + 1];
-      for (int i = k + 1 + lane; i < m; i += 32)
-        row[i] = fma(-1.0, wv[i], fma(-wk1, v[i], row[i]));
-      __syncwarp();
-      if (more) {
-        reflect(row, k + 1);
-      } else if (rank == 0 && lane == 0) {  // k + 1 == m - 2: the last 2x2 block
-        d[m - 2] = row[m - 2];
-        e[m - 2] = row[m - 1];
-        tau[m - 2] = 0.0;
-        tau[m - 1] = 0.0;
-        e[m - 1] = 0.0;
-      }
-    }
-    __syncthreads();
-    // fused pass: update k on own columns i > k, p_{k+1} with v_{k+1}, row k+2 slice
-    const double* vn = vb + (b ^ 1) * m;
-    double acc = 0.0, rs = 0.0;
-    if (active && icol > k) {
-      const double vi = v[icol], wi = wv[icol];
-      const bool pcol = more && icol > k + 1;
-      for (int j = k + 1 + g; j < m; j += G) {
-        double* wp = Wl + j * nc + lc;
-        const double nw = fma(-v[j], wi, fma(-wv[j], vi, wp[0]));
-        wp[0] = nw;
-        if (pcol && j > k + 1) acc = fma(nw, vn[j], acc);
-        if (j == k + 2) rs = nw;
-      }
-      if (more && tid < ncl && icol > k + 1) V[(int64_t)(k + 1) * m + icol] = vn[icol];
-    }
-    if (more) {
-      // the row k+2 slice is produced by the thread whose j loop visited j = k+2;
-      // route it to the g == 0 thread of the column through red's last slot use
-      // (the (j - k - 1) % G == 1 group): stage it in wv-free scratch via red
-      __syncthreads();
-      const int gsrc = 1 % G;  // j = k + 2 is visited by group (k+2 - (k+1)) % G
-      if (active && g == gsrc && icol > k + 1) red[lc] = rs;
-      __syncthreads();
-      const double row2 = (active && g == 0 && icol > k + 1) ? red[lc] : 0.0;
-      __syncthreads();
-      push_exchange(k + 1, (active && icol > k + 1) ? acc : 0.0, row2);
-    }
-  }
-  if (m >= 2 && tid == 0 && m - 1 >= c0 && m - 1 < c0 + ncl) d[m - 1] = Wl[(m - 1) * nc + (m - 1 - c0)];
-  if (m == 2 && rank == 0 && tid == 0) {
-    d[0] = Wl[0];
   }
   cluster_sync_all();  // no CTA leaves while its shared memory can still be written
 }
@@ -2040,16 +1708,13 @@ struct WcShape {
 
 WcShape tridiag_warpcol_shape(int m) {
   // one warp per column (lane groups of 8 / 16 per column were measured slower: the
-  // per-lane row loops become issue-bound); by default the widest cluster, so each SM
-  // runs as few column warps as possible (SPB_WC_C overrides for measurements)
+  // per-lane row loops become issue-bound); the widest cluster, so each SM runs as
+  // few column warps as possible (2 / 4 / 8 CTAs measured slower)
   if (m < kTriClusterMin || m > 256) return {0, 0};
-  static const int env_c = getenv("SPB_WC_C") ? atoi(getenv("SPB_WC_C")) : 16;
-  const int C = env_c == 2 || env_c == 4 || env_c == 8 ? env_c : 16;
+  constexpr int C = 16;
   if ((m + C - 1) / C > kWcWarps) return {0, 0};
   return {C, 32};
 }
-
-int tridiag_warpcol_cluster(int m) { return tridiag_warpcol_shape(m).C; }
 
 bool launch_tridiag_warpcol(const double* Asrc, int m, int symmetrize, double* V, double* tau,
                             double* d, double* e, const SmallStatus* status, cudaStream_t st,
@@ -2057,9 +1722,9 @@ bool launch_tridiag_warpcol(const double* Asrc, int m, int symmetrize, double* V
   const WcShape sh = tridiag_warpcol_shape(m);
   if (!sh.C) return false;
   const int C = sh.C, lpc = sh.lpc;
-  // SPB_WC_BULK=1: slices gathered per CTA and sent by bulk copies (measured slower: the
-  // two named barriers per step cost more than the per-value st.async they replace)
-  static const bool bulk = getenv("SPB_WC_BULK") ? atoi(getenv("SPB_WC_BULK")) != 0 : false;
+  // (slices gathered per CTA and sent by bulk copies measured slower: the two named
+  // barriers per step cost more than the per-value st.async they replace)
+  constexpr bool bulk = false;
   const int nc = bulk ? (((m + C - 1) / C + 1) & ~1) : (m + C - 1) / C;
   if (nc > kWcWarps) return false;
   const int nw = (nc + 32 / lpc - 1) / (32 / lpc);
@@ -2302,8 +1967,7 @@ trinv_cols(const double* __restrict__ Lg, int m, double* __restrict__ Linv,
 
 bool launch_chol_rowwarp(const double* B, int m, double* L, double* Linv, int mode,
                          SmallStatus* status, cudaStream_t st) {
-  static const bool off = getenv("SPB_CHOL_ROWWARP") && atoi(getenv("SPB_CHOL_ROWWARP")) == 0;
-  if (off || m < kCholRwMin) return false;
+  if (m < kCholRwMin) return false;
   const int C = 16, nc = (m + C - 1) / C;
   const int R = (m + 31) / 32;
   if (nc > kCrWarps || R > 12) return false;
@@ -2353,12 +2017,7 @@ size_t chol_cluster_smem(int m, int C) {
 size_t tridiag_cluster_smem(int m, int C);
 
 int tridiag_cluster_size(int m) {
-  static const int forced = getenv("SPB_TRI_CLUSTER") ? atoi(getenv("SPB_TRI_CLUSTER")) : 0;
   if (m < kTriClusterMin || m > kTriClusterMax) return 0;
-  if (forced == 2 || forced == 4 || forced == 8 || forced == 16)
-    if ((m + forced - 1) / forced <= (forced == 2 ? 128 : 64) &&
-        tridiag_cluster_smem(m, forced) <= 200 * 1024)
-      return forced;  // C == 2 (nc up to 128) only for the default mbarrier variant
   return m <= 160 ? 4 : (m <= 400 ? 8 : 16);
 }
 
@@ -2372,12 +2031,8 @@ void launch_tridiag(const double* Asrc, int m, int symmetrize, double* Wg, doubl
   if (const int C = tridiag_cluster_size(m)) {
     static std::atomic<uint64_t> attr{0};
     if (!done_on_device(attr)) {
-      cudaFuncSetAttribute(tridiag_cluster, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-      cudaFuncSetAttribute(tridiag_cluster, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
       cudaFuncSetAttribute(tridiag_cluster_mb, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
       cudaFuncSetAttribute(tridiag_cluster_mb, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
-      cudaFuncSetAttribute(tridiag_fused, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-      cudaFuncSetAttribute(tridiag_fused, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
       mark_on_device(attr);
     }
     cudaLaunchConfig_t cfg = {};
@@ -2392,57 +2047,11 @@ void launch_tridiag(const double* Asrc, int m, int symmetrize, double* Wg, doubl
     at[0].val.clusterDim.z = 1;
     cfg.attrs = at;
     cfg.numAttrs = 1;
-    static const int variant = getenv("SPB_TRI_VARIANT") ? atoi(getenv("SPB_TRI_VARIANT")) : 3;
-    if (variant == 3) {
-      // SPB_TRI_TRACE=<file>: per-step clock64 stamps of the last column's warp (diagnostics)
-      static const char* tf = getenv("SPB_TRI_TRACE");
-      static long long* tbuf = nullptr;
-      if (tf && !tbuf) cudaMalloc(&tbuf, sizeof(long long) * 8 * 4096);
-      long long* trace = (tf && m <= 4096) ? tbuf : nullptr;
-      if (launch_tridiag_warpcol(Asrc, m, symmetrize, V, tau, d, e, status, st, trace)) {
-        if (trace) {
-          std::vector<long long> h((size_t)8 * m);
-          cudaMemcpyAsync(h.data(), trace, sizeof(long long) * 8 * m, cudaMemcpyDeviceToHost, st);
-          cudaStreamSynchronize(st);
-          if (FILE* f = fopen(tf, "a")) {
-            fprintf(f, "m %d C %d lpc %d warpcol\n", m, tridiag_warpcol_shape(m).C, tridiag_warpcol_shape(m).lpc);
-            for (int k = 0; k + 2 < m; ++k) {
-              for (int j = 0; j < 7; ++j) fprintf(f, "%lld ", h[(size_t)k * 8 + j]);
-              fprintf(f, "\n");
-            }
-            fclose(f);
-          }
-        }
-        return;
-      }
-    }
-    if (variant == 0)
-      cudaLaunchKernelEx(&cfg, tridiag_cluster, Asrc, m, symmetrize, V, tau, d, e, status);
-    else if (variant == 2)
-      cudaLaunchKernelEx(&cfg, tridiag_fused, Asrc, m, symmetrize, V, tau, d, e, status);
-    else  // variant 1, and 3 where the warp-per-column kernel does not apply
-    {
-      // SPB_TRI_TRACE=<file>: per-step clock64 phase stamps of the last CTA's
-      // thread 0 appended to <file> (diagnostics only; synchronises the stream)
-      static const char* tf = getenv("SPB_TRI_TRACE");
-      static long long* tbuf = nullptr;
-      if (tf && !tbuf) cudaMalloc(&tbuf, sizeof(long long) * 8 * 4096);
-      long long* trace = (tf && m <= 4096) ? tbuf : nullptr;
-      cudaLaunchKernelEx(&cfg, tridiag_cluster_mb, Asrc, m, symmetrize, V, tau, d, e, status, trace);
-      if (trace) {
-        std::vector<long long> h((size_t)8 * m);
-        cudaMemcpyAsync(h.data(), trace, sizeof(long long) * 8 * m, cudaMemcpyDeviceToHost, st);
-        cudaStreamSynchronize(st);
-        if (FILE* f = fopen(tf, "a")) {
-          fprintf(f, "m %d C %d\n", m, C);
-          for (int k = 0; k + 2 < m; ++k) {
-            for (int j = 0; j < 8; ++j) fprintf(f, "%lld ", h[(size_t)k * 8 + j]);
-            fprintf(f, "\n");
-          }
-          fclose(f);
-        }
-      }
-    }
+    // warp-per-column register kernel for 48 <= m <= 256, else the shared-memory
+    // column split with mbarrier-tracked exchanges
+    if (launch_tridiag_warpcol(Asrc, m, symmetrize, V, tau, d, e, status, st, nullptr)) return;
+    cudaLaunchKernelEx(&cfg, tridiag_cluster_mb, Asrc, m, symmetrize, V, tau, d, e, status,
+                       (long long*)nullptr);
     return;
   }
   const int rows = (m + 31) / 32;
@@ -2682,10 +2291,7 @@ bisect_cta(const double* __restrict__ d, const double* __restrict__ e, int m, in
 // Sturm pivots by true division (dstebz's arithmetic) unless SPB_BISECT_RCP is
 // set: the reciprocal variant is faster but its last-bit differences measurably
 // change long LOBPCG trajectories (tests/test_gpu_lobpcg.py rand150).
-int bisect_div() {
-  static const int v = getenv("SPB_BISECT_RCP") ? 0 : (getenv("SPB_BISECT_DIV") ? 1 : 2);
-  return v;
-}
+int bisect_div() { return 2; }
 
 __device__ __forceinline__ double hash_uniform(uint32_t a, uint32_t b) {
   uint32_t h = a * 0x9E3779B1u ^ (b + 0x7F4A7C15u) * 0x85EBCA77u;
@@ -3408,35 +3014,13 @@ size_t tridiag_smem(int m) {
 
 void launch_chol(const double* B, int m, double* L, double* Linv, int mode, SmallStatus* status,
                  cudaStream_t st) {
-  static const bool old = getenv("SPB_CHOL_BLOCKED") != nullptr;  // A/B switch
-  static const int cmin = getenv("SPB_CHOL_CLUSTER_MIN") ? atoi(getenv("SPB_CHOL_CLUSTER_MIN"))
-                                                         : kCholLdlMax + 1;
-  static const int cfix = getenv("SPB_CHOL_CLUSTER_C") ? atoi(getenv("SPB_CHOL_CLUSTER_C")) : 0;
-  static const bool unblocked = getenv("SPB_CHOL_LDL") != nullptr;  // A/B switch
-  if (!old && !unblocked && launch_chol_rowwarp(B, m, L, Linv, mode, status, st)) return;
-  if (!old && !unblocked && m < cmin && m <= kCholLdlMax && chol_wsync_smem(m) <= 217 * 1024) {
-    // SPB_CHOL_TRACE=<file>: clock64 phase stamps appended to <file> (diagnostics)
-    static const char* tf = getenv("SPB_CHOL_TRACE");
-    static long long* tbuf = nullptr;
-    if (tf && !tbuf) cudaMalloc(&tbuf, sizeof(long long) * 48);
-    chol_wsync<<<1, CWT, chol_wsync_smem(m), st>>>(B, m, L, Linv, mode, status, tf ? tbuf : nullptr);
-    if (tf) {
-      long long h[48];
-      cudaMemcpyAsync(h, tbuf, sizeof(h), cudaMemcpyDeviceToHost, st);
-      cudaStreamSynchronize(st);
-      if (FILE* f = fopen(tf, "a")) {
-        fprintf(f, "m %d\n", m);
-        for (int j = 0; j < 46; ++j) fprintf(f, "%lld ", h[j]);
-        fprintf(f, "\n");
-        fclose(f);
-      }
-    }
-  } else if (!old && m < cmin && m <= kCholLdlMax && chol_ldl_smem(m) <= 224 * 1024) {
+  if (launch_chol_rowwarp(B, m, L, Linv, mode, status, st)) return;
+  if (m <= kCholLdlMax && chol_wsync_smem(m) <= 217 * 1024) {
+    chol_wsync<<<1, CWT, chol_wsync_smem(m), st>>>(B, m, L, Linv, mode, status, nullptr);
+  } else if (m <= kCholLdlMax && chol_ldl_smem(m) <= 224 * 1024) {
     chol_ldl<<<1, ET, chol_ldl_smem(m), st>>>(B, m, L, Linv, mode, status);
-  } else if (!old && m <= kCholClusterMax) {
-    int C = m <= 400 ? 8 : 16;
-    if ((cfix == 2 || cfix == 4 || cfix == 8 || cfix == 16) && (m + cfix - 1) / cfix * 8 <= CCT)
-      C = cfix;
+  } else if (m <= kCholClusterMax) {
+    const int C = m <= 400 ? 8 : 16;
     static std::atomic<uint64_t> attr{0};
     if (!done_on_device(attr)) {
       cudaFuncSetAttribute(chol_cluster, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
@@ -3520,13 +3104,10 @@ int sygv_enqueue(const double* ga, const double* gb, int ldg, int m, int nev, do
     SPB_LAUNCH_CHECK();
   }
   {
-    // SPB_INVIT_ONLY=1: inverse iteration for every eigenvalue (A/B switch)
-    static const bool invit_only = getenv("SPB_INVIT_ONLY") != nullptr;
-    if (!invit_only)
-      twisted_vec<<<nev, 32, 7 * sizeof(double) * (size_t)m, st>>>(w.d, w.e, m, nev, theta, w.Y,
-                                                                   nev, status);
+    twisted_vec<<<nev, 32, 7 * sizeof(double) * (size_t)m, st>>>(w.d, w.e, m, nev, theta, w.Y,
+                                                                 nev, status);
     invit<<<nev, 32, 8 * sizeof(double) * (size_t)m, st>>>(w.d, w.e, m, nev, theta, w.Y, nev,
-                                                           nullptr, invit_only ? 1 : 2, status);
+                                                           nullptr, 2, status);
   }
   SPB_LAUNCH_CHECK();
   SPB_CUDA(cudaStreamWaitEvent(st, side->join, 0));

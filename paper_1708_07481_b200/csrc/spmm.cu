@@ -221,29 +221,22 @@ int launch_spmm(int32_t r0, int32_t r1, const int32_t* rp, const int32_t* ci, co
     SPB_LAUNCH_CHECK();
     return SPB_OK;
   }
-  // Full-width rows by default: each gathered neighbour row is one contiguous
-  // run (432 B at C3), and the CSR is read once. L2-sized column panels (the
-  // earlier design) re-read the CSR per panel and measured 28 % slower at C3
-  // (X = 216 MB); SPB_SPMM_PANEL=<cols> restores them for experiments.
-  static const int forced = getenv("SPB_SPMM_PANEL") ? atoi(getenv("SPB_SPMM_PANEL")) : 0;
+  // Full-width rows: each gathered neighbour row is one contiguous run (432 B at
+  // C3) and the CSR is read once. (L2-sized column panels, which re-read the CSR
+  // per panel, measured 28 % slower at C3 in round 1 and were removed.)
   (void)x_rows;
-  int64_t panel = forced > 0 ? forced : ncols;
-  if (panel >= ncols) panel = ncols;
-  for (int c0 = 0; c0 < ncols; c0 += (int)panel) {
-    const int pc = (int)std::min<int64_t>(panel, ncols - c0);
+  {
+    const int c0 = 0, pc = ncols;
     const int nvec = (pc + VN - 1) / VN;
-    // spmm_vb (2 gathers in flight per lane, 128-thread blocks so short rows
-    // free their slots early) for rows of more than 8 vectors: -7 % at C2, -9 %
-    // at C3 against spmm_vec; SPB_SPMM_VARIANT=0 selects spmm_vec
-    static const int variant = getenv("SPB_SPMM_VARIANT") ? atoi(getenv("SPB_SPMM_VARIANT")) : 2;
-    if (variant >= 1 && nvec > 8) {
-      auto kf = nvec <= 16 ? (variant == 1 ? spmm_vb<T, 16, 4, 6> : variant == 2 ? spmm_vb<T, 16, 2, 8> : spmm_vb<T, 16, 8, 4>)
-                           : (variant == 1 ? spmm_vb<T, 32, 4, 6> : variant == 2 ? spmm_vb<T, 32, 2, 8> : spmm_vb<T, 32, 8, 4>);
-      static const int vt = getenv("SPB_SPMM_THREADS") ? atoi(getenv("SPB_SPMM_THREADS")) : 128;
-      const int64_t vblocks = ceil_div(rows * 32, vt);
-      kf<<<vblocks, vt, 0, st>>>(r0, r1, rp, ci, cv, deg, x, ldx, c0, pc, y, ldy, xoff);
+    // rows of more than 8 vectors: spmm_vb (2 gathers in flight per lane, 128-thread
+    // blocks so short rows free their slots early): -7 % at C2, -9 % at C3 against
+    // spmm_vec (round 1); U = 4 / 8 gathers in flight measured equal or slower
+    if (nvec > 8) {
+      auto kf = nvec <= 16 ? spmm_vb<T, 16, 2, 8> : spmm_vb<T, 32, 2, 8>;
+      const int64_t vblocks = ceil_div(rows * 32, 128);
+      kf<<<vblocks, 128, 0, st>>>(r0, r1, rp, ci, cv, deg, x, ldx, c0, pc, y, ldy, xoff);
       SPB_LAUNCH_CHECK();
-      continue;
+      return SPB_OK;
     }
     if (nvec <= 1)
       spmm_vec<T, 1><<<blocks, threads, 0, st>>>(r0, r1, rp, ci, cv, deg, x, ldx, c0, pc, y, ldy, xoff);
