@@ -34,6 +34,7 @@ namespace {
 
 constexpr int UTM = 128;             // rows per CTA (UMMA M)
 constexpr int UTK = 32;              // K per chunk (one 128-byte swizzle atom of fp32)
+constexpr int kUtCpg = 2;            // chunks per TMEM accumulation group (64-deep)
 constexpr int UTS_MAX = 4;           // pipeline stages (runtime: 2 when two CTAs fit per SM)
 constexpr int kUtA = UTM * UTK * 4;  // A tile bytes (16 KB)
 constexpr int kUtThreads = 320;  // 6 + 4 EW warps; EW = 1 (q <= 128)
@@ -129,6 +130,9 @@ struct UtParams {
   const float* init;
   int64_t ldi;
   const float* coef;        // staged chunks: [chunk][hi | lo][npad rows x 128 B, swizzled]
+  // chunk groups (per tile, chunk index j < nk): a group of up to UT_CPG chunks of one
+  // segment accumulates in one TMEM region before the epilogue adds it into registers
+  uint8_t gstart[32], gend[32];
   int64_t n;
   uint32_t tmem_cols;
   int stages;
@@ -227,10 +231,15 @@ update_tc_kernel(const __grid_constant__ CUtensorMap map0, const __grid_constant
       const uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) |  // F32 acc, TF32 A/B, K-major
                              ((uint32_t)(P.npad >> 3) << 17) | ((uint32_t)(UTM >> 4) << 24);
       const int total = ((ntiles - (int)blockIdx.x + (int)gridDim.x - 1) / (int)gridDim.x) * nk;
+      int G = 0, rg = 0;  // chunk group counter / its TMEM region (double-buffered)
       for (int kc = 0; kc < total; ++kc) {
         const int st = kc % UTS, u = kc / UTS;
-        const int rg = kc & 1;  // TMEM region of this chunk (double-buffered)
-        if (kc >= 2) ut_wait(&rfree[rg], ((kc >> 1) - 1) & 1);
+        const int j = kc % nk;
+        const bool first = P.gstart[j] != 0;
+        if (first) {
+          rg = G & 1;
+          if (G >= 2) ut_wait(&rfree[rg], ((G >> 1) - 1) & 1);
+        }
         ut_wait(&split[st], u & 1);
         asm volatile("tcgen05.fence::after_thread_sync;");
         uint8_t* sb = base + st * kStage;
@@ -242,12 +251,15 @@ update_tc_kernel(const __grid_constant__ CUtensorMap map0, const __grid_constant
           const uint32_t off = (uint32_t)kk * 32;
           const uint64_t dah = ut_desc_sw128(ahi + off), dal = ut_desc_sw128(alo + off);
           const uint64_t dbh = ut_desc_sw128(bhi + off), dbl = ut_desc_sw128(blo + off);
-          ut_mma(dacc, dah, dbl, idesc, kk == 0 ? 0u : 1u);  // small terms first
+          ut_mma(dacc, dah, dbl, idesc, (kk == 0 && first) ? 0u : 1u);  // small terms first
           ut_mma(dacc, dal, dbh, idesc, 1u);
           ut_mma(dacc, dah, dbh, idesc, 1u);
         }
         ut_commit(&empty[st]);
-        ut_commit(&rdone[rg]);
+        if (P.gend[j]) {
+          ut_commit(&rdone[rg]);
+          ++G;
+        }
       }
     }
   } else if (warp < 6) {
@@ -276,13 +288,13 @@ update_tc_kernel(const __grid_constant__ CUtensorMap map0, const __grid_constant
     }
   } else {
     // epilogue: warps 6..9 -> TMEM lane quarter (warp & 3) = tile rows. Every
-    // chunk's 32-deep partial product is added into float32 registers
-    // (round-to-nearest), so the tensor cores' accumulation covers only 12
-    // MMAs; the running sum is written at every emit.
+    // chunk group's partial product (UT_CPG x 32 deep) is added into float32
+    // registers (round-to-nearest), so the tensor cores' own accumulation covers
+    // at most 24 MMAs; the running sum is written at every emit.
     constexpr int NH = NPMAX / EW;         // columns per epilogue warp
     const int quarter = warp & 3;
     const int cb = ((warp - 6) >> 2) * NH;  // first column of this warp
-    int kc = 0;
+    int kc = 0, G = 0;
     for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
     const int64_t row = (int64_t)tile * UTM + quarter * 32 + lane;
     float acc[NH];
@@ -296,8 +308,9 @@ update_tc_kernel(const __grid_constant__ CUtensorMap map0, const __grid_constant
     }
     for (int s = 0; s < P.nseg; ++s) {
       for (int c = 0; c < P.seg[s].chunks; ++c, ++kc) {
-        const int rg = kc & 1;
-        ut_wait(&rdone[rg], (kc >> 1) & 1);
+        if (!P.gend[kc % nk]) continue;  // the group accumulates on in TMEM
+        const int rg = G & 1;
+        ut_wait(&rdone[rg], (G >> 1) & 1);
         asm volatile("tcgen05.fence::after_thread_sync;");
 #pragma unroll
         for (int c0 = 0; c0 < NH; c0 += 16) {
@@ -319,6 +332,7 @@ update_tc_kernel(const __grid_constant__ CUtensorMap map0, const __grid_constant
         }
         asm volatile("tcgen05.fence::before_thread_sync;");
         ut_arrive(&rfree[rg]);
+        ++G;
       }
       if (P.seg[s].emit && row < P.n) {
         float* orow = P.seg[s].out + row * P.seg[s].ldo + cb;
@@ -419,6 +433,15 @@ bool update_tc(const UpdParams& p, int64_t n, cudaStream_t st) {
     P.seg[s].ldo = p.seg[s].ldo;
   }
   P.nseg = p.nseg;
+  {
+    int j = 0;
+    for (int s = 0; s < p.nseg; ++s)
+      for (int c = 0; c < P.seg[s].chunks; ++c, ++j) {
+        P.gstart[j] = (c % kUtCpg) == 0;
+        P.gend[j] = (c % kUtCpg) == kUtCpg - 1 || c == P.seg[s].chunks - 1;
+      }
+    if (j > 32) return false;
+  }
   P.q = p.q;
   P.npad = npad;
   P.nemit = nemit;

@@ -18,12 +18,13 @@ ap = argparse.ArgumentParser()
 ap.add_argument("--config", default="c2")
 ap.add_argument("--reps", type=int, default=20)
 ap.add_argument("--cols", type=int, default=0)
+ap.add_argument("--ld", type=int, default=0, help="row stride of X/Y (solver: 3 * padded l)")
 a = ap.parse_args()
 spec = CONFIGS[a.config]
 edges, _ = generate_dcsbm(spec)
 g = spb.from_edges(edges, spec.n)
 l = a.cols or spb.block_size_for(spec.blocks)
-ld = ((l + 7) // 8) * 8
+ld = a.ld or ((l + 7) // 8) * 8
 n = spec.n
 row_ptr, col, _, nnz = g.device_csr()
 vals = g._w_csr.values("float32")
