@@ -1,6 +1,6 @@
 """Small deterministic target for ncu: N partition steps of a config (no profiler inside).
 
-    python tools/ncu_target.py [c2|c3|c4] [steps]
+    python tools/ncu_target.py [c2|c3|c4] [steps] [float32|float64]
 """
 import sys
 from pathlib import Path
@@ -15,6 +15,7 @@ from paper_1708_07481_b200.spectral import partition_device  # noqa: E402
 
 cfg_name = sys.argv[1] if len(sys.argv) > 1 else "c2"
 steps = int(sys.argv[2]) if len(sys.argv) > 2 else 1
+precision = sys.argv[3] if len(sys.argv) > 3 else "float32"  # explicit: no tol-based promotion
 spec = CONFIGS[cfg_name]
 edges, truth = generate_dcsbm(spec)
 k = spec.blocks
@@ -32,6 +33,6 @@ if cfg_name in ("c3", "c4"):  # the 10x stop rule the reference produced (bench.
 cfg = spb.SolverConfig(block_size=l, tol=tol, max_iter=max_iter, seed=0)
 for _ in range(steps):
     g = spb.from_edges((src, dst), spec.n)
-    partition_device(g, cfg, k, fix_k=True, x0=x0_d)
+    partition_device(g, cfg, k, fix_k=True, x0=x0_d, precision=precision)
 torch.cuda.synchronize()
 print("done")
