@@ -9,6 +9,7 @@
 // vectors (float4 / double2). When the row is narrower than a warp's vector
 // width the warp splits into lane groups that walk different neighbours and
 // are combined with xor-shuffles at the end.
+#include <algorithm>
 #include <cstdlib>
 
 #include "common.cuh"
@@ -63,6 +64,16 @@ __device__ __forceinline__ double2 ldg_hint(const double2* p, uint64_t pol) {
                : "=d"(v.x), "=d"(v.y)
                : "l"(p), "l"(pol));
   return v;
+}
+__device__ __forceinline__ void stg_hint(float4* p, const float4& v, uint64_t pol) {
+  asm volatile("st.global.L2::cache_hint.v4.f32 [%0], {%1, %2, %3, %4}, %5;" ::"l"(p), "f"(v.x),
+               "f"(v.y), "f"(v.z), "f"(v.w), "l"(pol)
+               : "memory");
+}
+__device__ __forceinline__ void stg_hint(double2* p, const double2& v, uint64_t pol) {
+  asm volatile("st.global.L2::cache_hint.v2.f64 [%0], {%1, %2}, %3;" ::"l"(p), "d"(v.x), "d"(v.y),
+               "l"(pol)
+               : "memory");
 }
 __device__ __forceinline__ int32_t ldg_hint(const int32_t* p, uint64_t pol) {
   int32_t v;
@@ -208,7 +219,8 @@ spmm_vb(int32_t r0, int32_t r1, const int32_t* __restrict__ rp, const int32_t* _
       V out = vaxpy_out(d, xi, acc);
       T* yp = y + (int64_t)row * ldy + coff;
       if (coff - c0 + VN <= ncols) {
-        *reinterpret_cast<V*>(yp) = out;
+        if (HINT) stg_hint(reinterpret_cast<V*>(yp), out, pol_s);
+        else *reinterpret_cast<V*>(yp) = out;
       } else {
         for (int q = 0; q < VN && coff - c0 + q < ncols; ++q) yp[q] = vget(out, q);
       }
@@ -265,8 +277,10 @@ int launch_spmm(int32_t r0, int32_t r1, const int32_t* rp, const int32_t* ci, co
   // C3) and the CSR is read once. (L2-sized column panels, which re-read the CSR
   // per panel, measured 28 % slower at C3 in round 1 and were removed.)
   (void)x_rows;
-  {
-    const int c0 = 0, pc = ncols;
+  static const int panel_env = getenv("SPB_SPMM_PANEL") ? atoi(getenv("SPB_SPMM_PANEL")) : 0;
+  const int panel = panel_env > 0 ? std::max(VN, panel_env / VN * VN) : ncols;
+  for (int c0 = 0; c0 < ncols; c0 += panel) {
+    const int pc = std::min(panel, ncols - c0);
     const int nvec = (pc + VN - 1) / VN;
     // rows of more than 8 vectors: spmm_vb (2 gathers in flight per lane, 128-thread
     // blocks so short rows free their slots early): -7 % at C2, -9 % at C3 against
@@ -278,7 +292,7 @@ int launch_spmm(int32_t r0, int32_t r1, const int32_t* rp, const int32_t* ci, co
       const int64_t vblocks = ceil_div(rows * 32, 128);
       kf<<<vblocks, 128, 0, st>>>(r0, r1, rp, ci, cv, deg, x, ldx, c0, pc, y, ldy, xoff, keep);
       SPB_LAUNCH_CHECK();
-      return SPB_OK;
+      continue;
     }
     if (nvec <= 1)
       spmm_vec<T, 1><<<blocks, threads, 0, st>>>(r0, r1, rp, ci, cv, deg, x, ldx, c0, pc, y, ldy, xoff);
