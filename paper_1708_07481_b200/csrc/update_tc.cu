@@ -34,7 +34,11 @@ namespace {
 
 constexpr int UTM = 128;             // rows per CTA (UMMA M)
 constexpr int UTK = 32;              // K per chunk (one 128-byte swizzle atom of fp32)
-constexpr int kUtCpg = 2;            // chunks per TMEM accumulation group (64-deep)
+// chunks per TMEM accumulation group: the tensor cores' fp32 accumulation is not
+// round-to-nearest (biased), so its error grows with the MMAs it spans; 2 (64-deep,
+// 24 MMAs, half the epilogue round trips) measurably moved float32 trajectories
+// (C3 stopped after 23 instead of the reference's 25 iterations), 1 keeps 12
+constexpr int kUtCpg = 1;
 constexpr int UTS_MAX = 4;           // pipeline stages (runtime: 2 when two CTAs fit per SM)
 constexpr int kUtA = UTM * UTK * 4;  // A tile bytes (16 KB)
 constexpr int kUtThreads = 320;  // 6 + 4 EW warps; EW = 1 (q <= 128)
