@@ -4,25 +4,28 @@
 //   G[p x q] = U' V,   U: n x p, V: n x q (float32, vertex-major, row stride ld)
 //
 // Every column c of U (and of V) gets a power-of-two scale 2^e_c > 2 max|x|; the
-// scaled entries r in (-1/2, 1/2) are written as S = 4 signed digits in [-64, 64]
-// (round to nearest), r = sum_t a_t 2^(-7t) + eps, |eps| <= 2^-29 (exact digit
+// scaled entries r in (-1/2, 1/2) are written as S = 6 signed digits in [-64, 64]
+// (round to nearest), r = sum_t a_t 2^(-7t) + eps, |eps| <= 2^-43 (exact digit
 // extraction in fp32).
-// Then G_cd = 2^(e_c + e_d) sum_{t+u <= S+1} 2^(-7(t+u)) (A_t' B_u)_cd: 10 int8
-// GEMMs with exact int32 accumulation, grouped by the level t+u into four TMEM
-// accumulators (4 x 128 = 512 columns), converted to fp64 and combined smallest
-// level first. The per-product error is O(2^-28) relative to the column maxima
-// (measured ~1e-9 relative to |U|'|V|), below the fp32 storage rounding of the
-// operands (2^-24 per entry); five digits (15 GEMMs, N = 96 tiles) measured
-// ~1e-11 at 1.4x the time.
+// Then G_cd = 2^(e_c + e_d) sum_{t+u <= S+1} 2^(-7(t+u)) (A_t' B_u)_cd: 21 int8
+// GEMMs with exact int32 accumulation, grouped by the level t+u into six TMEM
+// accumulators, converted to fp64 and combined smallest level first. The
+// per-product truncation error is O(2^-42) relative to the column maxima, far
+// below the fp32 storage rounding of the operands.
+//
+// Four digits (10 MMAs, 128-wide tiles: 1.8 -> 1.45 ms per C3 Rayleigh-Ritz Gram
+// pair, ~5e-9 relative) were measured in round 2 and rejected: the float32 C3 solve
+// then stops after 23 iterations instead of the reference's 25 (its residual sits 5 %
+// above the threshold at iteration 23), while five digits reproduce 25.
 //
 // Operands are pre-packed by oz_pack into the UMMA canonical K-major layout
 // (8 columns x 16 rows core matrices), one plane per digit:
 //   plane[kblock (32 rows)][column group (8 cols)][k half][8 cols][16 rows]
 // so a CTA's operand tile for one 32-row k-block is one contiguous bulk copy.
 //
-// Per CTA: a 128 x 128 output tile over a range of k-blocks (split-K, at most
+// Per CTA: a 128 x 80 output tile over a range of k-blocks (split-K, at most
 // 16384 rows so the int32 sums cannot overflow). Warp 0 issues the bulk copies
-// (mbarrier pipeline, OZ_KS stages), warp 1 one thread issues the 10 MMAs per
+// (mbarrier pipeline, OZ_KS stages), warp 1 one thread issues the 21 MMAs per
 // k-block, warps 2-5 the epilogue (tcgen05.ld -> fp64 partial tile); the split-K
 // partials are reduced in a fixed order (sum_splits).
 #include "dense.cuh"
@@ -34,12 +37,12 @@ int oz_sum_splits(const double* part, int ks, int64_t stride, int rows, int cols
 
 namespace {
 
-constexpr int OZ_S = 4;          // digits per value (2^-28 of the column maxima)
+constexpr int OZ_S = 5;          // digits per value (2^-35 of the column maxima)
 constexpr int OZ_M = 128;        // UMMA M (columns of U per tile)
-constexpr int OZ_N = 128;        // UMMA N (columns of V per tile); OZ_S * OZ_N <= 512 TMEM columns
+constexpr int OZ_N = 96;         // UMMA N (columns of V per tile); OZ_S * OZ_N <= 512 TMEM columns
 constexpr int OZ_KB = 32;        // rows per k-block (one UMMA K step for 8-bit operands)
 constexpr int OZ_KS = 4;         // pipeline stages
-constexpr int OZ_MAXROWS = 16384;  // rows per CTA: 4 pairs x 64^2 x 16384 < 2^31
+constexpr int OZ_MAXROWS = 16384;  // rows per CTA: 6 pairs x 127^2 x 16384 < 2^31
 constexpr int kOzA = OZ_S * (OZ_M / 8) * 256;  // bytes of the A planes per stage (24 KB)
 constexpr int kOzB = OZ_S * (OZ_N / 8) * 256;  // bytes of the B planes per stage (15 KB)
 constexpr int kOzStage = kOzA + kOzB;

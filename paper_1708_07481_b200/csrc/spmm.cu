@@ -9,7 +9,6 @@
 // vectors (float4 / double2). When the row is narrower than a warp's vector
 // width the warp splits into lane groups that walk different neighbours and
 // are combined with xor-shuffles at the end.
-#include <algorithm>
 #include <cstdlib>
 
 #include "common.cuh"
@@ -48,48 +47,6 @@ __device__ __forceinline__ float vget(const float4& v, int i) {
   return i == 0 ? v.x : i == 1 ? v.y : i == 2 ? v.z : v.w;
 }
 __device__ __forceinline__ double vget(const double2& v, int i) { return i == 0 ? v.x : v.y; }
-
-// L2 eviction-priority hints (experiment): the gathered rows of X are the only
-// reused data; the CSR and Y stream through once.
-__device__ __forceinline__ float4 ldg_hint(const float4* p, uint64_t pol) {
-  float4 v;
-  asm volatile("ld.global.nc.L2::cache_hint.v4.f32 {%0, %1, %2, %3}, [%4], %5;"
-               : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
-               : "l"(p), "l"(pol));
-  return v;
-}
-__device__ __forceinline__ double2 ldg_hint(const double2* p, uint64_t pol) {
-  double2 v;
-  asm volatile("ld.global.nc.L2::cache_hint.v2.f64 {%0, %1}, [%2], %3;"
-               : "=d"(v.x), "=d"(v.y)
-               : "l"(p), "l"(pol));
-  return v;
-}
-__device__ __forceinline__ void stg_hint(float4* p, const float4& v, uint64_t pol) {
-  asm volatile("st.global.L2::cache_hint.v4.f32 [%0], {%1, %2, %3, %4}, %5;" ::"l"(p), "f"(v.x),
-               "f"(v.y), "f"(v.z), "f"(v.w), "l"(pol)
-               : "memory");
-}
-__device__ __forceinline__ void stg_hint(double2* p, const double2& v, uint64_t pol) {
-  asm volatile("st.global.L2::cache_hint.v2.f64 [%0], {%1, %2}, %3;" ::"l"(p), "d"(v.x), "d"(v.y),
-               "l"(pol)
-               : "memory");
-}
-__device__ __forceinline__ int32_t ldg_hint(const int32_t* p, uint64_t pol) {
-  int32_t v;
-  asm volatile("ld.global.nc.L2::cache_hint.b32 %0, [%1], %2;" : "=r"(v) : "l"(p), "l"(pol));
-  return v;
-}
-__device__ __forceinline__ float ldg_hint(const float* p, uint64_t pol) {
-  float v;
-  asm volatile("ld.global.nc.L2::cache_hint.f32 %0, [%1], %2;" : "=f"(v) : "l"(p), "l"(pol));
-  return v;
-}
-__device__ __forceinline__ double ldg_hint(const double* p, uint64_t pol) {
-  double v;
-  asm volatile("ld.global.nc.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(v) : "l"(p), "l"(pol));
-  return v;
-}
 
 // Vectorised path: ldx, ldy multiples of the vector width, pointers aligned.
 // GS = lanes per neighbour group (power of two), chunks = vectors per row panel.
@@ -155,19 +112,12 @@ spmm_vec(int32_t r0, int32_t r1, const int32_t* __restrict__ rp, const int32_t* 
 // registers before the FMAs, so U independent L2 loads are in flight per lane
 // (the gather is latency-bound: X rows come from L2 in random order). The FMA
 // order per (lane, vector) is the same as spmm_vec's.
-template <typename T, int GS, int U, int MINB, bool HINT = false>
+template <typename T, int GS, int U, int MINB>
 __global__ void __launch_bounds__(256, MINB)
 spmm_vb(int32_t r0, int32_t r1, const int32_t* __restrict__ rp, const int32_t* __restrict__ ci,
         const T* __restrict__ cv, const T* __restrict__ deg, const T* __restrict__ x,
-        int64_t ldx, int c0, int ncols, T* __restrict__ y, int64_t ldy, int64_t xoff,
-        float keep = 0.f) {
+        int64_t ldx, int c0, int ncols, T* __restrict__ y, int64_t ldy, int64_t xoff) {
   using V = typename Vec<T>::type;
-  uint64_t pol_x = 0, pol_s = 0;
-  if (HINT) {
-    asm volatile("createpolicy.fractional.L2::evict_last.L2::evict_first.b64 %0, %1;"
-                 : "=l"(pol_x) : "f"(keep));
-    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol_s));
-  }
   constexpr int VN = Vec<T>::N;
   constexpr int NG = 32 / GS;
   const int lane = threadIdx.x & 31;
@@ -187,8 +137,8 @@ spmm_vb(int32_t r0, int32_t r1, const int32_t* __restrict__ rp, const int32_t* _
       int32_t cj = 0;
       T wv = T(0);
       if (my < e1) {
-        cj = HINT ? ldg_hint(ci + my, pol_s) : __ldg(ci + my);
-        wv = HINT ? ldg_hint(cv + my, pol_s) : __ldg(cv + my);
+        cj = __ldg(ci + my);
+        wv = __ldg(cv + my);
       }
       const int cnt = min(32, e1 - eb);
       for (int kk = 0; kk < cnt; kk += NG * U) {  // warp-uniform trip count
@@ -202,8 +152,7 @@ spmm_vb(int32_t r0, int32_t r1, const int32_t* __restrict__ rp, const int32_t* _
           const T w = __shfl_sync(0xffffffffu, wv, srcl);
           const bool ok = act && k < cnt;
           ww[u] = ok ? w : T(0);
-          const V* xp = reinterpret_cast<const V*>(xb + (int64_t)j * ldx);
-          xv[u] = ok ? (HINT ? ldg_hint(xp, pol_x) : __ldg(xp)) : vzero<V>();
+          xv[u] = ok ? __ldg(reinterpret_cast<const V*>(xb + (int64_t)j * ldx)) : vzero<V>();
         }
 #pragma unroll
         for (int u = 0; u < U; ++u)
@@ -219,8 +168,7 @@ spmm_vb(int32_t r0, int32_t r1, const int32_t* __restrict__ rp, const int32_t* _
       V out = vaxpy_out(d, xi, acc);
       T* yp = y + (int64_t)row * ldy + coff;
       if (coff - c0 + VN <= ncols) {
-        if (HINT) stg_hint(reinterpret_cast<V*>(yp), out, pol_s);
-        else *reinterpret_cast<V*>(yp) = out;
+        *reinterpret_cast<V*>(yp) = out;
       } else {
         for (int q = 0; q < VN && coff - c0 + q < ncols; ++q) yp[q] = vget(out, q);
       }
@@ -274,25 +222,25 @@ int launch_spmm(int32_t r0, int32_t r1, const int32_t* rp, const int32_t* ci, co
     return SPB_OK;
   }
   // Full-width rows: each gathered neighbour row is one contiguous run (432 B at
-  // C3) and the CSR is read once. (L2-sized column panels, which re-read the CSR
-  // per panel, measured 28 % slower at C3 in round 1 and were removed.)
+  // C3) and the CSR is read once. Measured and rejected (round 2, C3 R block inside
+  // the solver's 336-float rows, 1.538 ms full width): L2-sized column panels, 56 /
+  // 36 / 28 columns, 1.77 / 2.38 / 2.81 ms (with evict-last hints on X); L2
+  // eviction-priority hints on full rows (fractional evict_last on the gathered X,
+  // evict_first on the CSR and Y), 1.53-1.70 ms. ncu at C3: 6.49 GB of DRAM reads
+  // per launch (L2 hit rate 26 %) at 4.2 TB/s -- the gathers miss a 216 MB X block.
   (void)x_rows;
-  static const int panel_env = getenv("SPB_SPMM_PANEL") ? atoi(getenv("SPB_SPMM_PANEL")) : 0;
-  const int panel = panel_env > 0 ? std::max(VN, panel_env / VN * VN) : ncols;
-  for (int c0 = 0; c0 < ncols; c0 += panel) {
-    const int pc = std::min(panel, ncols - c0);
+  {
+    const int c0 = 0, pc = ncols;
     const int nvec = (pc + VN - 1) / VN;
     // rows of more than 8 vectors: spmm_vb (2 gathers in flight per lane, 128-thread
     // blocks so short rows free their slots early): -7 % at C2, -9 % at C3 against
     // spmm_vec (round 1); U = 4 / 8 gathers in flight measured equal or slower
     if (nvec > 8) {
-      static const float keep = getenv("SPB_SPMM_HINT") ? atof(getenv("SPB_SPMM_HINT")) : 0.f;
       auto kf = nvec <= 16 ? spmm_vb<T, 16, 2, 8> : spmm_vb<T, 32, 2, 8>;
-      if (keep > 0.f) kf = nvec <= 16 ? spmm_vb<T, 16, 2, 8, true> : spmm_vb<T, 32, 2, 8, true>;
       const int64_t vblocks = ceil_div(rows * 32, 128);
-      kf<<<vblocks, 128, 0, st>>>(r0, r1, rp, ci, cv, deg, x, ldx, c0, pc, y, ldy, xoff, keep);
+      kf<<<vblocks, 128, 0, st>>>(r0, r1, rp, ci, cv, deg, x, ldx, c0, pc, y, ldy, xoff);
       SPB_LAUNCH_CHECK();
-      continue;
+      return SPB_OK;
     }
     if (nvec <= 1)
       spmm_vec<T, 1><<<blocks, threads, 0, st>>>(r0, r1, rp, ci, cv, deg, x, ldx, c0, pc, y, ldy, xoff);
