@@ -43,6 +43,12 @@ struct UpdParams {
   int q;
   float* cstage;        // optional fp32 coefficient staging (fast fp32 path)
   size_t cstage_cap;    // floats; see update_cstage_floats()
+  // argmin epilogue (k-means assignment, tensor-core path only): instead of writing
+  // the last emit's rows, labels[i] = argmin_j (bias[j] - 2 acc[i][j]) (lowest j on
+  // ties) and *changed += rows whose label moved
+  const float* argmin_bias;
+  int* argmin_labels;
+  unsigned long long* argmin_changed;
 };
 
 // Staging floats the fp32 update needs for segments of total width w_total.

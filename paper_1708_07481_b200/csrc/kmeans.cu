@@ -4,17 +4,29 @@
 //
 // Lloyd iterations from given initial centroids (the QRCP seed rows by default):
 //   assign : argmin_c ||x_i - mu_c||^2 = argmin_c (||mu_c||^2 - 2 x_i . mu_c)
-//            thread per row, centroids and their norms staged in shared memory
-//            (the "distance GEMM + argmin"), changes counted per block;
+//            float32 embeddings (k <= 192, no row normalisation): the distance GEMM
+//            X mu' on the tcgen05 tensor cores (3xTF32, TMA-fed; update_tc.cu)
+//            with the argmin fused into its epilogue -- X is read once per Lloyd
+//            step and no n x k distance matrix is written; otherwise a thread per
+//            row with the centroids and their norms in shared memory; changes are
+//            counted for the stop test;
 //   update : per-cluster sums as a segmented reduction (float64 atomics into
 //            k x d accumulators, then mu = sum / count; empty clusters keep
 //            their previous centroid).
-#include "common.cuh"
+#include "dense.cuh"
 
 namespace spb {
 namespace {
 
 constexpr int KT = 256;
+
+// coefficients of the distance GEMM: C[t][j] = mu[j][t] (d x k, float64)
+__global__ void km_coeffs(const float* __restrict__ mu, int k, int d, double* __restrict__ c) {
+  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < k * d; e += gridDim.x * blockDim.x) {
+    const int t = e / k, j = e % k;
+    c[e] = (double)mu[(size_t)j * d + t];
+  }
+}
 
 template <typename T>
 __global__ void __launch_bounds__(KT)
@@ -133,8 +145,8 @@ __global__ void km_init(const T* __restrict__ X, int64_t ldx, int d, int k, cons
 template <typename T>
 int kmeans_t(const void* xv, int64_t ldx, int n, int d, int k, const int* seeds, int max_iter,
              int normalize, int* labels, float* mu, float* mu2, double* sums,
-             unsigned long long* counts, unsigned long long* changed, int* iters_out,
-             cudaStream_t st) {
+             unsigned long long* counts, unsigned long long* changed, double* coef,
+             float* cstage, size_t cstage_cap, int* iters_out, cudaStream_t st) {
   const T* X = (const T*)xv;
   km_init<T><<<k, 128, 0, st>>>(X, ldx, d, k, seeds, normalize, mu);
   SPB_CUDA(cudaMemsetAsync(sums, 0, sizeof(double) * (size_t)k * d, st));
@@ -147,8 +159,25 @@ int kmeans_t(const void* xv, int64_t ldx, int n, int d, int k, const int* seeds,
   int it = 0;
   for (; it < max_iter; ++it) {
     SPB_CUDA(cudaMemsetAsync(changed, 0, sizeof(unsigned long long), st));
-    km_assign<T><<<(int)ceil_div(n, KT), KT, smem, st>>>(X, ldx, n, d, k, mu, mu2, labels,
-                                                         normalize, changed);
+    bool tc = false;
+    if (sizeof(T) == 4 && !normalize && coef && cstage) {
+      km_coeffs<<<(int)std::min<int64_t>(ceil_div((int64_t)k * d, 256), 256), 256, 0, st>>>(mu, k, d,
+                                                                                          coef);
+      UpdParams p{};
+      p.nseg = 1;
+      p.q = k;
+      p.seg[0] = {X, ldx, coef, k, nullptr, 0, 1.0, d, 1};
+      p.cstage = cstage;
+      p.cstage_cap = cstage_cap;
+      p.argmin_bias = mu2;
+      p.argmin_labels = labels;
+      p.argmin_changed = changed;
+      tc = update_tc(p, n, st);
+    }
+    if (!tc)
+      km_assign<T><<<(int)ceil_div(n, KT), KT, smem, st>>>(X, ldx, n, d, k, mu, mu2, labels,
+                                                           normalize, changed);
+    SPB_LAUNCH_CHECK();
     unsigned long long h = 0;
     SPB_CUDA(cudaMemcpyAsync(&h, changed, sizeof(h), cudaMemcpyDeviceToHost, st));
     SPB_CUDA(cudaStreamSynchronize(st));
@@ -170,7 +199,15 @@ int kmeans_t(const void* xv, int64_t ldx, int n, int d, int k, const int* seeds,
 using namespace spb;
 
 extern "C" size_t spb_kmeans_workspace(int32_t k, int32_t d) {
-  return (size_t)k * d * (sizeof(float) + sizeof(double)) + (size_t)k * (sizeof(float) + 8) + 1024;
+  Arena a;
+  a.dry = true;
+  a.take<double>((size_t)k * d);            // sums
+  a.take<float>(k);                         // mu2
+  a.take<unsigned long long>(k);            // counts
+  a.take<unsigned long long>(1);            // changed
+  a.take<double>((size_t)k * d);            // distance-GEMM coefficients
+  a.take<float>(update_tc_cstage_floats(d, 1, k));  // their TF32 split staging
+  return a.used + 1024;
 }
 
 extern "C" int spb_kmeans(int dtype, const void* x, int64_t ldx, int32_t n, int32_t d, int32_t k,
@@ -196,6 +233,9 @@ extern "C" int spb_kmeans(int dtype, const void* x, int64_t ldx, int32_t n, int3
   float* mu2 = a.take<float>(k);
   unsigned long long* counts = a.take<unsigned long long>(k);
   unsigned long long* changed = a.take<unsigned long long>(1);
+  double* coef = a.take<double>((size_t)k * d);
+  const size_t cstage_cap = update_tc_cstage_floats(d, 1, k);
+  float* cstage = a.take<float>(cstage_cap);
   if (a.used > ws_bytes) {
     set_error("kmeans workspace too small");
     return SPB_ERR_WORKSPACE;
@@ -204,9 +244,11 @@ extern "C" int spb_kmeans(int dtype, const void* x, int64_t ldx, int32_t n, int3
   cudaStream_t st = (cudaStream_t)stream;
   int s = dtype == SPB_F32
               ? kmeans_t<float>(x, ldx, n, d, k, seeds, max_iter, normalize_rows, labels_out,
-                                centroids_out, mu2, sums, counts, changed, &it, st)
+                                centroids_out, mu2, sums, counts, changed, coef, cstage,
+                                cstage_cap, &it, st)
               : kmeans_t<double>(x, ldx, n, d, k, seeds, max_iter, normalize_rows, labels_out,
-                                 centroids_out, mu2, sums, counts, changed, &it, st);
+                                 centroids_out, mu2, sums, counts, changed, nullptr, nullptr, 0,
+                                 &it, st);
   *iterations_out = it;
   return s;
 }

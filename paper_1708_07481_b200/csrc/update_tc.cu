@@ -140,7 +140,17 @@ struct UtParams {
   int64_t n;
   uint32_t tmem_cols;
   int stages;
+  const float* argmin_bias;          // argmin epilogue (see UpdParams)
+  int* argmin_labels;
+  unsigned long long* argmin_changed;
 };
+
+// Orderable 64-bit key of (distance, column): unsigned compare = (dist, col) lexicographic.
+__device__ __forceinline__ unsigned long long ut_argkey(float d, int j) {
+  const uint32_t b = __float_as_uint(d);
+  const uint32_t o = (b & 0x80000000u) ? ~b : (b | 0x80000000u);
+  return ((unsigned long long)o << 32) | (uint32_t)j;
+}
 
 // Coefficient chunks: element (output column j, k) of chunk c of segment s is
 // scale_s C_s[32 c + k][j], stored at the 128-byte-swizzled K-major position.
@@ -182,6 +192,8 @@ update_tc_kernel(const __grid_constant__ CUtensorMap map0, const __grid_constant
   uint64_t* rdone = empty + UTS_MAX;                // [2] chunk partial ready in TMEM
   uint64_t* rfree = rdone + 2;                      // [2] region read by the epilogue
   uint32_t* tmem_slot = (uint32_t*)(rfree + 2);
+  // argmin keys [tile parity][column half][row]
+  unsigned long long* akeys = (unsigned long long*)(base + UTS * kStage + 256);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int ntiles = (int)((P.n + UTM - 1) / UTM);
   // persistent: tiles blockIdx.x, blockIdx.x + gridDim.x, ...; chunk counters
@@ -338,7 +350,41 @@ update_tc_kernel(const __grid_constant__ CUtensorMap map0, const __grid_constant
         ut_arrive(&rfree[rg]);
         ++G;
       }
-      if (P.seg[s].emit && row < P.n) {
+      if (P.argmin_labels && s == P.nseg - 1) {
+        // k-means assignment: argmin over this warp's columns, then (EW = 2) over the
+        // two column halves through shared memory, double-buffered by tile parity
+        float best = INFINITY;
+        int bj = 0;
+#pragma unroll
+        for (int i = 0; i < NH; ++i) {
+          if (cb + i < P.q) {
+            const float dist = fmaf(-2.0f, acc[i], P.argmin_bias[cb + i]);
+            if (dist < best) {  // strict: lowest column on ties
+              best = dist;
+              bj = cb + i;
+            }
+          }
+        }
+        const int par = ((tile - (int)blockIdx.x) / (int)gridDim.x) & 1;
+        const int half = (warp - 6) >> 2;
+        int lab = bj;
+        if (EW == 2) {
+          akeys[(par * 2 + half) * UTM + quarter * 32 + lane] = ut_argkey(best, bj);
+          asm volatile("bar.sync 1, %0;" ::"r"(32 * 4 * EW) : "memory");
+          const unsigned long long k0 = akeys[(par * 2) * UTM + quarter * 32 + lane];
+          const unsigned long long k1 = akeys[(par * 2 + 1) * UTM + quarter * 32 + lane];
+          lab = (int)(uint32_t)(k0 <= k1 ? k0 : k1);
+        }
+        if (half == 0) {
+          int moved = 0;
+          if (row < P.n) {
+            moved = P.argmin_labels[row] != lab;
+            P.argmin_labels[row] = lab;
+          }
+          const unsigned m = __ballot_sync(0xffffffffu, moved);
+          if (lane == 0 && m) atomicAdd(P.argmin_changed, (unsigned long long)__popc(m));
+        }
+      } else if (P.seg[s].emit && row < P.n) {
         float* orow = P.seg[s].out + row * P.seg[s].ldo + cb;
         const bool vec = (reinterpret_cast<uintptr_t>(orow) & 15) == 0;
 #pragma unroll
@@ -452,16 +498,20 @@ bool update_tc(const UpdParams& p, int64_t n, cudaStream_t st) {
   P.init = (const float*)p.init;
   P.ldi = p.ldi;
   P.coef = p.cstage;
+  P.argmin_bias = p.argmin_bias;
+  P.argmin_labels = p.argmin_labels;
+  P.argmin_changed = p.argmin_changed;
   P.n = n;
   P.tmem_cols = cols;
   const int kB = 2 * npad * UTK * 4;
   const size_t kStage = 2 * kUtA + kB;
   // two stages when two CTAs fit per SM (one CTA's epilogue overlaps the other's
   // MMAs), else three
-  int stages = 2 * (2 * kStage + 1280) <= 227 * 1024 ? 2 : 3;
-  if ((size_t)stages * kStage + 1280 > 227 * 1024) stages = 2;
+  constexpr size_t kExtra = 1024 + 256 + 4 * UTM * 8;  // alignment, barriers, argmin keys
+  int stages = 2 * (2 * kStage + kExtra) <= 227 * 1024 ? 2 : 3;
+  if ((size_t)stages * kStage + kExtra > 227 * 1024) stages = 2;
   P.stages = stages;
-  const size_t smem = (size_t)stages * kStage + 1024 + 256;
+  const size_t smem = (size_t)stages * kStage + kExtra;
   static std::atomic<uint64_t> attr{0};
   if (!done_on_device(attr)) {
     cudaFuncSetAttribute(update_tc_kernel<64, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);

@@ -77,6 +77,33 @@ def test_kmeans_float32_and_normalize():
     assert partition_match(_lloyd(xn, seeds), pn.labels) > 0.995
 
 
+@pytest.mark.parametrize("k", [44, 98, 160])
+def test_kmeans_tensor_core_distance_gemm(k):
+    """float32 embeddings take the tcgen05 distance GEMM with the fused argmin epilogue
+    (k <= 128: one epilogue warp per row; 128 < k <= 192, C4's k = 160: two column
+    halves combined through shared memory). Against a float64 numpy Lloyd from the same
+    seeds; clusters are well separated, so near-ties are rare."""
+    import torch
+
+    import paper_1708_07481_b200 as spb
+    from oracle import partition_match
+
+    rng = np.random.default_rng(k)
+    n_per = 300
+    centers = rng.standard_normal((k, k)) * 3.0
+    x = np.concatenate([c + rng.standard_normal((n_per, k)) for c in centers])
+    perm = rng.permutation(len(x))
+    x = x[perm]
+    inv = np.argsort(perm)
+    seeds = np.sort(inv[np.arange(k) * n_per])  # one row of each cluster
+    xt = torch.tensor(x, dtype=torch.float32, device="cuda")
+    part, info = spb.assign_clusters_kmeans(xt, k, seeds=seeds, return_info=True)
+    want = _lloyd(x.astype(np.float32).astype(np.float64), seeds)
+    agree = partition_match(want, part.labels)
+    print(f"\nk={k}: tensor-core k-means agreement {agree:.5f}, {info['iterations']} Lloyd steps")
+    assert agree > 0.999
+
+
 def test_kmeans_contract_errors():
     import paper_1708_07481_b200 as spb
 
