@@ -358,28 +358,6 @@ gram_oz_kernel(const int8_t* __restrict__ PA, const int8_t* __restrict__ PB,
   }
 }
 
-// Device scratch (grown on demand, never shrunk), one slot per use.
-struct OzScratch {
-  void* p = nullptr;
-  size_t cap = 0;
-};
-void* oz_scratch_slot(int slot, size_t bytes) {
-  static OzScratch s[16][4];
-  int dev = 0;
-  cudaGetDevice(&dev);
-  OzScratch& x = s[dev & 15][slot & 3];
-  if (x.cap < bytes) {
-    if (x.p) cudaFree(x.p);
-    x.p = nullptr;
-    if (cudaMalloc(&x.p, bytes) != cudaSuccess) {
-      x.cap = 0;
-      return nullptr;
-    }
-    x.cap = bytes;
-  }
-  return x.p;
-}
-
 }  // namespace
 
 // One operand in the packed digit layout (planes + per-column max bits).
@@ -470,16 +448,25 @@ int oz_gemm(const OzOperand& A, const OzOperand& B, double* partial, size_t part
   return oz_sum_splits(partial, (int)ks, P.split_stride, p, q, out, ldo, st);
 }
 
-// out[p x q] (ld ldo) = U' V with float32 operands, float64-accurate.
+// Workspace of gram_oz: both operands' digit planes, then the split-K partials.
+size_t gram_oz_ws_bytes(int64_t n, int p, int q) {
+  return oz_operand_bytes(n, p) + oz_operand_bytes(n, q) +
+         gram_oz_partial_doubles(n, p, q) * sizeof(double) + 1024;
+}
+
+// out[p x q] (ld ldo) = U' V with float32 operands, float64-accurate; ws is caller
+// memory of gram_oz_ws_bytes(n, p, q) bytes (no allocation here).
 int gram_oz(const float* U, int64_t ldu, int p, const float* V, int64_t ldv, int q, int64_t n,
-            double* partial, size_t partial_cap, double* out, int ldo, cudaStream_t st) {
+            void* ws, size_t ws_bytes, double* out, int ldo, cudaStream_t st) {
   if (p <= 0 || q <= 0) return SPB_OK;
   const size_t ba = oz_operand_bytes(n, p), bb = oz_operand_bytes(n, q);
-  uint8_t* scr = (uint8_t*)oz_scratch_slot(0, ba + bb);
-  if (!scr) {
-    set_error("Ozaki Gram scratch allocation failed (%zu bytes)", ba + bb);
-    return SPB_ERR_CUDA;
+  if (ws_bytes < gram_oz_ws_bytes(n, p, q)) {
+    set_error("Ozaki Gram workspace too small (%zu < %zu bytes)", ws_bytes, gram_oz_ws_bytes(n, p, q));
+    return SPB_ERR_WORKSPACE;
   }
+  uint8_t* scr = (uint8_t*)ws;
+  double* partial = (double*)(scr + ba + bb);
+  const size_t partial_cap = (ws_bytes - ba - bb) / sizeof(double);
   OzOperand A, B;
   SPB_TRY(oz_prepare(U, ldu, n, p, scr, &A, st));
   SPB_TRY(oz_prepare(V, ldv, n, q, scr + ba, &B, st));
@@ -487,18 +474,18 @@ int gram_oz(const float* U, int64_t ldu, int p, const float* V, int64_t ldv, int
 }
 
 // The Rayleigh-Ritz Grams of the solver: Gb = B'B (upper triangle valid, ld ldo) and
-// Ga = B'LB (ld ldo), B
-// and LB n x cols (row stride ld), each operand packed once; scratch owned here.
+// Ga = B'LB (ld ldo), B and LB n x cols (row stride ld), each operand packed once;
+// ws: gram_oz_ws_bytes(n, cols, cols) bytes of the solver's workspace.
 int gram_oz_rr(const float* B, const float* LB, int64_t ld, int64_t n, int cols, double* Ga,
-               double* Gb, int ldo, cudaStream_t st) {
+               double* Gb, int ldo, void* ws, size_t ws_bytes, cudaStream_t st) {
   const size_t bo = oz_operand_bytes(n, cols);
-  uint8_t* scr = (uint8_t*)oz_scratch_slot(1, 2 * bo);
-  const size_t pc = gram_oz_partial_doubles(n, cols, cols);
-  double* part = (double*)oz_scratch_slot(2, pc * sizeof(double));
-  if (!scr || !part) {
-    set_error("Ozaki Gram scratch allocation failed (%zu bytes)", 2 * bo + pc * sizeof(double));
-    return SPB_ERR_CUDA;
+  if (ws_bytes < gram_oz_ws_bytes(n, cols, cols)) {
+    set_error("Ozaki Gram workspace too small");
+    return SPB_ERR_WORKSPACE;
   }
+  uint8_t* scr = (uint8_t*)ws;
+  double* part = (double*)(scr + 2 * bo);
+  const size_t pc = (ws_bytes - 2 * bo) / sizeof(double);
   OzOperand OB, OL;
   SPB_TRY(oz_prepare(B, ld, n, cols, scr, &OB, st));
   SPB_TRY(oz_prepare(LB, ld, n, cols, scr + bo, &OL, st));

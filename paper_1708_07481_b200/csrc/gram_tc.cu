@@ -416,9 +416,9 @@ int gram_tc(const float* U, int64_t ldu, int p, const float* V0, int64_t ldv0, i
 using namespace spb;
 
 namespace spb {
-size_t gram_oz_partial_doubles(int64_t n, int p, int q);
+size_t gram_oz_ws_bytes(int64_t n, int p, int q);
 int gram_oz(const float* U, int64_t ldu, int p, const float* V, int64_t ldv, int q, int64_t n,
-            double* partial, size_t partial_cap, double* out, int ldo, cudaStream_t st);
+            void* ws, size_t ws_bytes, double* out, int ldo, cudaStream_t st);
 }  // namespace spb
 
 extern "C" int spb_gram(int dtype, int mode, const void* u, int64_t ldu, int32_t p, const void* v,
@@ -440,7 +440,7 @@ extern "C" int spb_gram(int dtype, int mode, const void* u, int64_t ldu, int32_t
       set_error("tensor-core Gram needs an sm_100 device");
       return SPB_ERR_CUDA;
     }
-    return gram_oz((const float*)u, ldu, p, (const float*)v, ldv, q, n, part, cap, out, (int)ldo, st);
+    return gram_oz((const float*)u, ldu, p, (const float*)v, ldv, q, n, ws, ws_bytes, out, (int)ldo, st);
   }
   if (mode == 1) {
     if (dtype != SPB_F32) {
@@ -465,6 +465,6 @@ extern "C" int spb_gram(int dtype, int mode, const void* u, int64_t ldu, int32_t
 extern "C" size_t spb_gram_workspace(int32_t p, int32_t q, int64_t n) {
   size_t a = gram_tc_partial_doubles(n, p, q);
   size_t b = gram_partial_doubles(n, (int)(ceil_div(p, 64) * ceil_div(q, 64)), p, q, nullptr);
-  size_t c = gram_oz_partial_doubles(n, p, q);
+  const size_t c = gram_oz_ws_bytes(n, p, q) / sizeof(double) + 1;
   return (std::max(std::max(a, b), c) + 64) * sizeof(double);
 }

@@ -54,6 +54,8 @@ struct SolveWs {
   int *idx, *perm;
   SmallStatus* status;
   void *gsend, *grecv;  // row-sharded solves: packed local rows / all-gathered block
+  void* oz_ws;          // Ozaki Gram digit planes + partials (use_oz)
+  size_t oz_ws_bytes;
 };
 
 SolveWs carve(Arena& a, int dtype, int n, int l, int nranks = 1, int n_max = 0) {
@@ -114,6 +116,12 @@ SolveWs carve(Arena& a, int dtype, int n, int l, int nranks = 1, int n_max = 0) 
   w.idx = a.take<int>(w.lp + 8);
   w.perm = a.take<int>(w.lp + 8);
   w.status = a.take<SmallStatus>(1);
+  w.oz_ws = nullptr;
+  w.oz_ws_bytes = 0;
+  if (w.use_oz) {
+    w.oz_ws_bytes = gram_oz_ws_bytes(n, w.ld, w.ld);
+    w.oz_ws = a.take<char>(w.oz_ws_bytes);
+  }
   w.gsend = w.grecv = nullptr;
   if (n_max > 0) {  // row-sharded solve (any rank count): gather buffers
     w.gsend = a.take<char>((size_t)n_max * w.lp * w.esz);
@@ -266,7 +274,7 @@ struct Driver {
       // gather the m x m blocks (as the tcgen05 path below)
       const int pe = pw > 0 ? 2 * w.lp + pw : w.lp + na;
       SPB_TRY(gram_oz_rr((const float*)w.B, (const float*)w.LB, w.ld, w.n, pe, w.Gpad + pe,
-                         w.Gpad, 2 * pe, st));
+                         w.Gpad, 2 * pe, w.oz_ws, w.oz_ws_bytes, st));
       SPB_TRY(allreduce(w.Gpad, (size_t)pe * 2 * pe));
       const int m = w.l + na + pw;
       gather_pad_grams<<<(int)std::min<int64_t>(ceil_div((int64_t)m * m, 256), 1024), 256, 0, st>>>(
