@@ -599,6 +599,13 @@ def run_ours(args):
             "precision": args.precision,
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": (achieved / peak) if achieved else None, "traffic": traffic,
+                         "traffic_achieved": (traffic / (spmm_us * 1e-6 / max(spmm_calls, 1)) / 1e9)
+                         if (traffic and spmm_us) else None,
+                         "traffic_frac": (traffic / (spmm_us * 1e-6 / max(spmm_calls, 1)) / 1e9 / peak)
+                         if (traffic and spmm_us) else None,
+                         "traffic_note": "ncu dram__bytes_read+write of one launch (profiles/spmm_traffic.json) "
+                                         "over this run's average launch time: the DRAM bandwidth the "
+                                         "SpMM actually sustains (the gathers miss the 216 MB X block)",
                          "kernel": "spb::spmm_vb (Laplacian SpMM)", "peak_kind": peak_kind,
                          "launches": spmm_calls,
                          "avg_launch_us": spmm_us / max(spmm_calls, 1),
