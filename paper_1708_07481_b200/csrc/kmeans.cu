@@ -102,6 +102,35 @@ __global__ void km_accumulate(const T* __restrict__ X, int64_t ldx, int n, int d
   if (lane == 0) atomicAdd(&counts[c], 1ull);
 }
 
+// Segmented centroid sums with the k x d accumulator privatised in shared memory
+// (float64 shared atomics, one flush of k x d global float64 atomics per CTA)
+// instead of n x d global atomics.
+template <typename T>
+__global__ void __launch_bounds__(256)
+km_accumulate_smem(const T* __restrict__ X, int64_t ldx, int n, int d, int k,
+                   const int* __restrict__ labels, double* __restrict__ sums,
+                   unsigned long long* __restrict__ counts) {
+  extern __shared__ double acc[];  // k x d sums, then k counts (as double)
+  double* cnt = acc + (size_t)k * d;
+  for (int x = threadIdx.x; x < k * d + k; x += blockDim.x) acc[x] = 0.0;
+  __syncthreads();
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t rows_per = ceil_div(n, gridDim.x);
+  const int64_t r0 = blockIdx.x * rows_per, r1 = min((int64_t)n, r0 + rows_per);
+  for (int64_t row = r0 + warp; row < r1; row += blockDim.x >> 5) {
+    const int c = labels[row];
+    const T* xr = X + row * ldx;
+    double* a = acc + (size_t)c * d;
+    for (int t = lane; t < d; t += 32) atomicAdd(&a[t], (double)xr[t]);
+    if (lane == 0) atomicAdd(&cnt[c], 1.0);
+  }
+  __syncthreads();
+  for (int x = threadIdx.x; x < k * d; x += blockDim.x)
+    if (acc[x] != 0.0) atomicAdd(&sums[x], acc[x]);
+  for (int c = threadIdx.x; c < k; c += blockDim.x)
+    if (cnt[c] != 0.0) atomicAdd(&counts[c], (unsigned long long)cnt[c]);
+}
+
 __global__ void km_finalize(const double* __restrict__ sums, const unsigned long long* __restrict__ counts,
                             int k, int d, float* __restrict__ mu, float* __restrict__ mu2) {
   const int c = blockIdx.x;
@@ -154,19 +183,39 @@ int kmeans_t(const void* xv, int64_t ldx, int n, int d, int k, const int* seeds,
   km_finalize<<<k, 128, 0, st>>>(sums, counts, k, d, mu, mu2);  // norms of the initial centroids
   SPB_CUDA(cudaMemsetAsync(labels, 0xff, sizeof(int) * n, st));
   const size_t smem = sizeof(float) * ((size_t)k * d + k);
+  // the tensor-core path reads X through a TMA map: 16-byte aligned rows; an
+  // unaligned float32 embedding is copied once into padded rows for the Lloyd loop
+  const float* Xtc = nullptr;
+  int64_t ldtc = ldx;
+  float* xpad = nullptr;
+  if (sizeof(T) == 4 && !normalize && coef) {
+    if ((reinterpret_cast<uintptr_t>(X) & 15) == 0 && (ldx & 3) == 0) {
+      Xtc = (const float*)X;
+    } else {
+      ldtc = round_up(d, 4);
+      if (cudaMallocAsync((void**)&xpad, sizeof(float) * (size_t)n * ldtc, st) == cudaSuccess) {
+        SPB_CUDA(cudaMemcpy2DAsync(xpad, sizeof(float) * ldtc, X, sizeof(T) * ldx, sizeof(float) * d, n,
+                                   cudaMemcpyDeviceToDevice, st));
+        Xtc = xpad;
+      } else {
+        cudaGetLastError();
+        xpad = nullptr;
+      }
+    }
+  }
   SPB_CUDA(cudaFuncSetAttribute(km_assign<T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 (int)std::max<size_t>(smem, 48 * 1024)));
   int it = 0;
   for (; it < max_iter; ++it) {
     SPB_CUDA(cudaMemsetAsync(changed, 0, sizeof(unsigned long long), st));
     bool tc = false;
-    if (sizeof(T) == 4 && !normalize && coef && cstage) {
+    if (sizeof(T) == 4 && !normalize && coef && cstage && Xtc) {
       km_coeffs<<<(int)std::min<int64_t>(ceil_div((int64_t)k * d, 256), 256), 256, 0, st>>>(mu, k, d,
                                                                                           coef);
       UpdParams p{};
       p.nseg = 1;
       p.q = k;
-      p.seg[0] = {X, ldx, coef, k, nullptr, 0, 1.0, d, 1};
+      p.seg[0] = {Xtc, ldtc, coef, k, nullptr, 0, 1.0, d, 1};
       p.cstage = cstage;
       p.cstage_cap = cstage_cap;
       p.argmin_bias = mu2;
@@ -184,12 +233,21 @@ int kmeans_t(const void* xv, int64_t ldx, int n, int d, int k, const int* seeds,
     if (h == 0) break;
     SPB_CUDA(cudaMemsetAsync(sums, 0, sizeof(double) * (size_t)k * d, st));
     SPB_CUDA(cudaMemsetAsync(counts, 0, sizeof(unsigned long long) * k, st));
-    km_accumulate<T><<<(int)ceil_div((int64_t)n * 32, 256), 256, 0, st>>>(X, ldx, n, d, labels,
-                                                                         normalize, sums, counts);
+    const size_t acc_smem = sizeof(double) * ((size_t)k * d + k);
+    if (!normalize && acc_smem <= 220 * 1024) {
+      SPB_CUDA(cudaFuncSetAttribute(km_accumulate_smem<T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    (int)std::max<size_t>(acc_smem, 48 * 1024)));
+      const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(n, 256), num_sms()));
+      km_accumulate_smem<T><<<grid, 256, acc_smem, st>>>(X, ldx, n, d, k, labels, sums, counts);
+    } else {
+      km_accumulate<T><<<(int)ceil_div((int64_t)n * 32, 256), 256, 0, st>>>(X, ldx, n, d, labels,
+                                                                           normalize, sums, counts);
+    }
     km_finalize<<<k, 128, 0, st>>>(sums, counts, k, d, mu, mu2);
     SPB_LAUNCH_CHECK();
   }
   *iters_out = it;
+  if (xpad) SPB_CUDA(cudaFreeAsync(xpad, st));
   return SPB_OK;
 }
 

@@ -24,6 +24,7 @@ from pathlib import Path
 import numpy as np
 import torch
 
+from . import _h2d
 from . import _native as N
 from .errors import ContractError, DomainError, ParseError
 
@@ -233,12 +234,11 @@ def _device_arcs(edges, n: int, weights=None):
     elif (weights is None and isinstance(edges, np.ndarray) and edges.ndim == 2
           and edges.shape[1] == 2 and edges.dtype == np.int64 and edges.flags.c_contiguous
           and edges.shape[0] > 0):
-        # fast path: one H2D copy of the arc block (asynchronous from pinned
-        # memory; pageable blocks go through the driver's staged copy, which is
-        # steadier than a per-call pin_memory), columns split on the device; the
+        # fast path: one H2D copy of the arc block (large pageable blocks through a
+        # multi-threaded pinned ring, _h2d.py), columns split on the device; the
         # endpoint range check happens in the CSR build's validation pass (same
         # DomainError)
-        dev = torch.from_numpy(edges).to(device=_device(), non_blocking=True)
+        dev = _h2d.to_device(edges, _device())
         src, dst, w = dev[:, 0].contiguous(), dev[:, 1].contiguous(), None
     else:
         hs, hd, hw = _coerce_edges(edges, weights)

@@ -27,6 +27,7 @@ from pathlib import Path
 import numpy as np
 import torch
 
+from . import _h2d
 from . import _native as N
 from .errors import ConditioningError, ContractError, DomainError, SolverError, SpecpartError
 from .graph import DTYPES, LaplacianOperator, _device
@@ -304,8 +305,7 @@ def _x0_device(x0, n, l):
         t = x0.to(device=_device(), dtype=torch.float64)
         return t.contiguous()
     arr = np.ascontiguousarray(x0, dtype=np.float64)
-    # asynchronous from pinned memory; pageable arrays take the driver's staged copy
-    return torch.from_numpy(arr).to(_device(), non_blocking=True)
+    return _h2d.to_device(arr, _device())  # multi-threaded pinned ring for large blocks
 
 
 def lobpcg_solve(operator, x0, config: SolverConfig, precond=None, n_converge: int | None = None,

@@ -29,6 +29,7 @@ import os
 import numpy as np
 import torch
 
+from . import _h2d
 from . import _native as N
 from .errors import ContractError, DomainError, SolverError, SpecpartError
 from .graph import DTYPES, SparseGraph, _device, _device_arcs
@@ -255,7 +256,7 @@ def lobpcg_solve_sharded(op: RowShardedLaplacian, x0, config: SolverConfig, n_co
     if isinstance(x0, torch.Tensor):
         x0_d = x0[op.row_begin:op.row_end].to(device=dev, dtype=torch.float64).contiguous()
     else:
-        x0_d = torch.from_numpy(np.ascontiguousarray(x0[op.row_begin:op.row_end])).to(dev)
+        x0_d = _h2d.to_device(np.ascontiguousarray(x0[op.row_begin:op.row_end]), dev)
     wsb = L.spb_lobpcg_workspace_sharded(code, op.n_local, l, op.nranks, op.n_max)
     ws = torch.empty(wsb, dtype=torch.uint8, device=dev)
     cfg = N.SolverConfigC(block_size=l, max_iter=config.max_iter, tol=config.tol,
