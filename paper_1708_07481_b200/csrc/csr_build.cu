@@ -262,6 +262,170 @@ __global__ void rows_emit(const int64_t* __restrict__ src, const int64_t* __rest
   }
 }
 
+// ---------------------------------------------------------------------------
+// Bucket build (default): no global sort. Entries are counted per row (integer
+// atomics), scattered into their row's bucket (atomic cursor: arbitrary order
+// inside the bucket), then every row is sorted in shared memory by (col, payload)
+// -- payload = emission index 2e / 2e+1, so duplicate (row, col) entries come out
+// in the same order as the stable radix sort and every sum below is bit-identical
+// to the radix path's -- reduced, and compacted. Rows of more than kBkMaxRow
+// entries fall back to the radix path.
+constexpr int kBkMaxRow = 1024;   // entries per row sorted in shared memory
+constexpr int kBkWarps = 4;       // rows (warps) per CTA (32 KB of static shared memory)
+
+struct BkSpec {
+  int two_sided;                  // reverse entries (SYMMETRIZED)
+  int64_t r0, r1;                 // rows kept (row-shard build), else [0, n)
+  const int32_t* bounds;          // non-null: columns remapped to the gathered layout
+  int nranks;
+  int32_t n_max;
+};
+
+__device__ __forceinline__ uint32_t bk_col(const BkSpec& S, int64_t c) {
+  if (!S.bounds) return (uint32_t)c;
+  int lo = 0, hi = S.nranks;
+  while (hi - lo > 1) {
+    const int mid = (lo + hi) >> 1;
+    if (S.bounds[mid] <= c) lo = mid; else hi = mid;
+  }
+  return (uint32_t)((int64_t)lo * S.n_max + (c - S.bounds[lo]));
+}
+
+__global__ void bk_count(const int64_t* __restrict__ src, const int64_t* __restrict__ dst, int64_t m,
+                         BkSpec S, int* __restrict__ cnt) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < m;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t a = src[e], b = dst[e];
+    if (a == b) continue;
+    if (a >= S.r0 && a < S.r1) atomicAdd(&cnt[a - S.r0], 1);
+    if (S.two_sided && b >= S.r0 && b < S.r1) atomicAdd(&cnt[b - S.r0], 1);
+  }
+}
+
+__global__ void bk_max(const int* __restrict__ cnt, int64_t n, int* __restrict__ out) {
+  int mx = 0;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    mx = max(mx, cnt[i]);
+  for (int o = 16; o > 0; o >>= 1) mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+  if ((threadIdx.x & 31) == 0) atomicMax(out, mx);
+}
+
+__global__ void bk_scatter(const int64_t* __restrict__ src, const int64_t* __restrict__ dst, int64_t m,
+                           BkSpec S, int* __restrict__ cursor, uint64_t* __restrict__ keys) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < m;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t a = src[e], b = dst[e];
+    if (a == b) continue;
+    if (a >= S.r0 && a < S.r1) {
+      const int p = atomicAdd(&cursor[a - S.r0], 1);
+      keys[p] = ((uint64_t)bk_col(S, b) << 32) | (uint32_t)(2 * e);
+    }
+    if (S.two_sided && b >= S.r0 && b < S.r1) {
+      const int p = atomicAdd(&cursor[b - S.r0], 1);
+      keys[p] = ((uint64_t)bk_col(S, a) << 32) | (uint32_t)(2 * e + 1);
+    }
+  }
+}
+
+// Warp per row: sort the bucket, sum each (row, col) group in payload order
+// (forward and reverse weights apart, as group_reduce), keep non-zero sums
+// (SYMMETRIZED), write the row's unique entries at the start of its bucket and its
+// degree (forward sums then reverse sums, each in column order, as row_degrees).
+__global__ void __launch_bounds__(32 * kBkWarps)
+bk_rows(const int* __restrict__ off, int32_t nrows, const uint64_t* __restrict__ keys,
+        const double* __restrict__ w, int drop_zero, int with_reverse, int32_t* __restrict__ tcol,
+        double* __restrict__ tval, int* __restrict__ ucnt, double* __restrict__ deg) {
+  __shared__ uint64_t buf[kBkWarps][kBkMaxRow];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  uint64_t* b = buf[wid];
+  for (int64_t row = (int64_t)blockIdx.x * kBkWarps + wid; row < nrows;
+       row += (int64_t)gridDim.x * kBkWarps) {
+    const int o0 = off[row], cnt = off[row + 1] - o0;
+    int P = 1;
+    while (P < cnt) P <<= 1;
+    for (int i = lane; i < P; i += 32) b[i] = i < cnt ? keys[o0 + i] : ~0ull;
+    __syncwarp();
+    for (int k = 2; k <= P; k <<= 1)
+      for (int j = k >> 1; j > 0; j >>= 1) {
+        for (int i = lane; i < P; i += 32) {
+          const int ixj = i ^ j;
+          if (ixj > i) {
+            const uint64_t x = b[i], y = b[ixj];
+            if ((x > y) == ((i & k) == 0)) {
+              b[i] = y;
+              b[ixj] = x;
+            }
+          }
+        }
+        __syncwarp();
+      }
+    int u0 = 0;
+    double a = 0.0, c = 0.0;
+    for (int base = 0; base < cnt; base += 32) {
+      const int i = base + lane;
+      bool head = false, keep = false;
+      double f = 0.0, r = 0.0;
+      int hf = 0, hr = 0;
+      uint32_t col = 0;
+      if (i < cnt) {
+        col = (uint32_t)(b[i] >> 32);
+        head = i == 0 || (uint32_t)(b[i - 1] >> 32) != col;
+        if (head) {
+          for (int j = i; j < cnt && (uint32_t)(b[j] >> 32) == col; ++j) {
+            const uint32_t p = (uint32_t)b[j];
+            const double x = w ? w[p >> 1] : 1.0;
+            if (p & 1u) {
+              r = hr ? r + x : x;
+              hr = 1;
+            } else {
+              f = hf ? f + x : x;
+              hf = 1;
+            }
+          }
+          const double tot = hf ? (hr ? f + r : f) : r;
+          keep = drop_zero ? tot != 0.0 : true;
+        }
+      }
+      const unsigned km = __ballot_sync(0xffffffffu, keep);
+      if (keep) {
+        const int u = u0 + __popc(km & ((1u << lane) - 1u));
+        tcol[o0 + u] = (int32_t)col;
+        tval[o0 + u] = hf ? (hr ? f + r : f) : r;
+      }
+      // degree: forward then reverse group sums in column order (lane order here)
+      const double fk = (keep && hf) ? f : 0.0, rk = (keep && hr) ? r : 0.0;
+      const bool fh = keep && hf, rh = keep && hr;
+      const unsigned fm = __ballot_sync(0xffffffffu, fh), rm = __ballot_sync(0xffffffffu, rh);
+      for (int t = 0; t < 32; ++t) {
+        const double ft = __shfl_sync(0xffffffffu, fk, t), rt = __shfl_sync(0xffffffffu, rk, t);
+        if ((fm >> t) & 1u) a += ft;
+        if ((rm >> t) & 1u) c += rt;
+      }
+      u0 += __popc(km);
+    }
+    if (lane == 0) {
+      ucnt[row] = u0;
+      if (deg) deg[row] = with_reverse ? a + c : a;
+    }
+    __syncwarp();
+  }
+}
+
+__global__ void bk_copy(const int* __restrict__ off, const int32_t* __restrict__ row_ptr,
+                        int32_t nrows, const int32_t* __restrict__ tcol, const double* __restrict__ tval,
+                        int32_t* __restrict__ col, double* __restrict__ val) {
+  const int lane = threadIdx.x & 31;
+  for (int64_t row = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; row < nrows;
+       row += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+    const int o0 = off[row], d0 = row_ptr[row], cnt = row_ptr[row + 1] - d0;
+    for (int i = lane; i < cnt; i += 32) {
+      col[d0 + i] = tcol[o0 + i];
+      val[d0 + i] = tval[o0 + i];
+    }
+  }
+}
+
 int key_bits(int32_t n) {
   int b = 1;
   while ((int64_t(1) << b) <= (int64_t)n) ++b;
@@ -272,13 +436,14 @@ struct BuildLayout {
   uint64_t *ka, *kb;
   uint32_t *pa, *pb;
   int *counts, *scan_tmp, *keep, *slot, *dev_ints;
+  int *bcnt, *boff, *bcur, *bucnt;  // bucket path, per row (n + 1)
   double *fsum, *rsum, *ofs, *ors;
   uint8_t *has, *ohas;
   int32_t* orow;
   BuildFlags* flags;
 };
 
-BuildLayout carve(Arena& a, int64_t cap) {
+BuildLayout carve(Arena& a, int64_t cap, int64_t nrows) {
   BuildLayout L;
   int64_t ntiles = ceil_div(cap, kSortTile);
   L.ka = a.take<uint64_t>(cap);
@@ -286,7 +451,12 @@ BuildLayout carve(Arena& a, int64_t cap) {
   L.pa = a.take<uint32_t>(cap);
   L.pb = a.take<uint32_t>(cap);
   L.counts = a.take<int>((size_t)kRadix * ntiles + 1);
-  L.scan_tmp = a.take<int>(scan_workspace_ints(std::max<int64_t>(cap, kRadix * ntiles)) + 8);
+  L.scan_tmp = a.take<int>(
+      scan_workspace_ints(std::max<int64_t>(std::max<int64_t>(cap, kRadix * ntiles), nrows + 1)) + 8);
+  L.bcnt = a.take<int>(nrows + 1);
+  L.boff = a.take<int>(nrows + 1);
+  L.bcur = a.take<int>(nrows + 1);
+  L.bucnt = a.take<int>(nrows + 1);
   L.keep = a.take<int>(cap + 1);
   L.slot = a.take<int>(cap + 1);
   L.fsum = a.take<double>(cap);
@@ -304,6 +474,9 @@ BuildLayout carve(Arena& a, int64_t cap) {
 int sort_reduce_scatter(BuildLayout& L, const double* w, int64_t count, int64_t valid, int b,
                         bool symmetrized, int32_t n, int32_t* row_ptr, int32_t* col, double* val,
                         double* deg, int64_t* nnz_out, cudaStream_t st);
+int bucket_build(BuildLayout& L, const int64_t* src, const int64_t* dst, const double* w, int64_t m,
+                 int32_t nrows, const BkSpec& S, bool symmetrized, int32_t* row_ptr, int32_t* col,
+                 double* val, double* deg, int64_t* nnz_out, bool* fell_back, cudaStream_t st);
 
 int grid_for(int64_t work, int threads = 256) {
   int64_t g = ceil_div(std::max<int64_t>(work, 1), threads);
@@ -319,8 +492,7 @@ extern "C" size_t spb_csr_build_workspace(int64_t m_edges, int32_t n, int mode) 
   Arena a;
   a.dry = true;
   int64_t cap = (mode == SPB_CSR_SYMMETRIZED ? 2 : 1) * std::max<int64_t>(m_edges, 1);
-  carve(a, cap);
-  (void)n;
+  carve(a, cap, std::max<int32_t>(n, 0));
   return a.used + 1024;
 }
 
@@ -350,7 +522,7 @@ extern "C" int spb_csr_build(const int64_t* src, const int64_t* dst, const doubl
   Arena a;
   a.base = (char*)ws;
   a.cap = ws_bytes;
-  BuildLayout L = carve(a, cap);
+  BuildLayout L = carve(a, cap, n);
   if (a.used > ws_bytes) {
     set_error("csr build workspace too small (%zu < %zu)", ws_bytes, a.used);
     return SPB_ERR_WORKSPACE;
@@ -385,6 +557,13 @@ extern "C" int spb_csr_build(const int64_t* src, const int64_t* dst, const doubl
     if (deg) SPB_CUDA(cudaMemsetAsync(deg, 0, sizeof(double) * n, st));
     *nnz_out = 0;
     return SPB_OK;
+  }
+  {
+    const BkSpec S{two, 0, n, nullptr, 1, 0};
+    bool fb = false;
+    SPB_TRY(bucket_build(L, src, dst, w, m, n, S, mode == SPB_CSR_SYMMETRIZED, row_ptr, col, val, deg,
+                         nnz_out, &fb, st));
+    if (!fb) return SPB_OK;
   }
   const int b = key_bits(n);
   const int64_t count = (two ? 2 : 1) * m;
@@ -445,6 +624,49 @@ int sort_reduce_scatter(BuildLayout& L, const double* w, int64_t count, int64_t 
 }  // namespace
 }  // namespace spb
 
+namespace spb {
+namespace {
+// The bucket build (see bk_rows); *fell_back when a row exceeds kBkMaxRow entries
+// (nothing written then: the caller runs the radix path).
+int bucket_build(BuildLayout& L, const int64_t* src, const int64_t* dst, const double* w, int64_t m,
+                 int32_t nrows, const BkSpec& S, bool symmetrized, int32_t* row_ptr, int32_t* col,
+                 double* val, double* deg, int64_t* nnz_out, bool* fell_back, cudaStream_t st) {
+  *fell_back = false;
+  SPB_CUDA(cudaMemsetAsync(L.bcnt, 0, sizeof(int) * (size_t)nrows, st));
+  SPB_CUDA(cudaMemsetAsync(L.dev_ints, 0, sizeof(int) * 4, st));
+  bk_count<<<grid_for(m), 256, 0, st>>>(src, dst, m, S, L.bcnt);
+  SPB_LAUNCH_CHECK();
+  SPB_TRY(exclusive_scan_i32(L.bcnt, L.boff, nrows, L.scan_tmp, L.boff + nrows, st));
+  bk_max<<<grid_for(nrows), 256, 0, st>>>(L.bcnt, nrows, L.dev_ints + 1);
+  SPB_LAUNCH_CHECK();
+  int h[2] = {0, 0};
+  SPB_CUDA(cudaMemcpyAsync(&h[0], L.boff + nrows, sizeof(int), cudaMemcpyDeviceToHost, st));
+  SPB_CUDA(cudaMemcpyAsync(&h[1], L.dev_ints + 1, sizeof(int), cudaMemcpyDeviceToHost, st));
+  SPB_CUDA(cudaStreamSynchronize(st));
+  if (h[1] > kBkMaxRow) {
+    *fell_back = true;
+    return SPB_OK;
+  }
+  SPB_CUDA(cudaMemcpyAsync(L.bcur, L.boff, sizeof(int) * (size_t)nrows, cudaMemcpyDeviceToDevice, st));
+  bk_scatter<<<grid_for(m), 256, 0, st>>>(src, dst, m, S, L.bcur, L.ka);
+  SPB_LAUNCH_CHECK();
+  int32_t* tcol = reinterpret_cast<int32_t*>(L.pa);
+  const int rblocks = (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(nrows, kBkWarps), num_sms() * 8));
+  bk_rows<<<rblocks, 32 * kBkWarps, 0, st>>>(L.boff, nrows, L.ka, w, symmetrized ? 1 : 0,
+                                             symmetrized ? 1 : 0, tcol, L.fsum, L.bucnt, deg);
+  SPB_LAUNCH_CHECK();
+  SPB_TRY(exclusive_scan_i32(L.bucnt, row_ptr, nrows, L.scan_tmp, row_ptr + nrows, st));
+  int nnz = 0;
+  SPB_CUDA(cudaMemcpyAsync(&nnz, row_ptr + nrows, sizeof(int), cudaMemcpyDeviceToHost, st));
+  SPB_CUDA(cudaStreamSynchronize(st));
+  bk_copy<<<grid_for((int64_t)nrows * 32), 256, 0, st>>>(L.boff, row_ptr, nrows, tcol, L.fsum, col, val);
+  SPB_LAUNCH_CHECK();
+  *nnz_out = nnz;
+  return SPB_OK;
+}
+}  // namespace
+}  // namespace spb
+
 extern "C" int spb_csr_build_rows(const int64_t* src, const int64_t* dst, const double* w,
                                   int64_t m, int32_t n, int32_t row_begin, int32_t row_end,
                                   const int32_t* bounds, int32_t nranks, int32_t n_max, void* ws,
@@ -465,7 +687,7 @@ extern "C" int spb_csr_build_rows(const int64_t* src, const int64_t* dst, const 
   Arena a;
   a.base = (char*)ws;
   a.cap = ws_bytes;
-  BuildLayout L = carve(a, cap);
+  BuildLayout L = carve(a, cap, n);
   if (a.used > ws_bytes) {
     set_error("csr build workspace too small (%zu < %zu)", ws_bytes, a.used);
     return SPB_ERR_WORKSPACE;
@@ -492,7 +714,13 @@ extern "C" int spb_csr_build_rows(const int64_t* src, const int64_t* dst, const 
     *nnz_out = 0;
     return SPB_OK;
   }
-  // compaction of this rank's entries, in emission order (keep/slot reused)
+  {
+    const BkSpec S{1, row_begin, row_end, bounds, nranks, n_max};
+    bool fb = false;
+    SPB_TRY(bucket_build(L, src, dst, w, m, nl, S, true, row_ptr, col, val, deg, nnz_out, &fb, st));
+    if (!fb) return SPB_OK;
+  }
+  // radix fallback: compaction of this rank's entries, in emission order (keep/slot reused)
   rows_flags<<<grid_for(m), 256, 0, st>>>(src, dst, m, row_begin, row_end, L.keep);
   SPB_LAUNCH_CHECK();
   SPB_TRY(exclusive_scan_i32(L.keep, L.slot, 2 * m, L.scan_tmp, L.dev_ints, st));

@@ -142,3 +142,26 @@ def test_symmetrize_modes(spb):
     assert set(g.weights.tolist()) == {1.0}
     with pytest.raises(spb.DomainError):
         spb.symmetrize(spb.from_edges([(0, 1)], 2), mode="other")
+
+
+@pytest.mark.parametrize("hub", [900, 3000])
+def test_hub_rows_both_build_paths(spb, hub):
+    """Rows up to 1024 entries take the bucket build (shared-memory row sort); a hub
+    row beyond that sends the whole build down the radix-sort path. Both bit-exact
+    against the oracle, with duplicate, antiparallel and weighted arcs."""
+    rng = np.random.default_rng(hub)
+    n = hub + 50
+    leaves = rng.integers(1, n, size=hub)
+    edges = np.concatenate([np.stack([np.zeros(hub, np.int64), leaves], 1),
+                            np.stack([leaves[: hub // 3], np.zeros(hub // 3, np.int64)], 1),
+                            rng.integers(0, n, size=(4 * n, 2))])
+    w = rng.integers(1, 4, size=len(edges)).astype(np.float64) * 0.5
+    g = spb.from_edges(np.column_stack([edges, w]), n)
+    ip, ix, dv = oracle.directed_csr(np.column_stack([edges, w]), n)
+    assert np.array_equal(g.row_offsets, ip) and np.array_equal(g.col_indices, ix)
+    assert np.array_equal(g.weights, dv)
+    wp, wx, wv = oracle.symmetrize_csr(ip, ix, dv, n)
+    s = spb.symmetrize(g)
+    assert np.array_equal(s.row_offsets, wp) and np.array_equal(s.col_indices, wx)
+    assert np.array_equal(s.weights, wv)
+    assert np.array_equal(spb.degrees(g), oracle.directed_degrees(ip, ix, dv, n))
