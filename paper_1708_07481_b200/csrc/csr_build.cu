@@ -271,7 +271,9 @@ __global__ void rows_emit(const int64_t* __restrict__ src, const int64_t* __rest
 // to the radix path's -- reduced, and compacted. Rows of more than kBkMaxRow
 // entries fall back to the radix path.
 constexpr int kBkMaxRow = 1024;   // entries per row sorted in shared memory
-constexpr int kBkWarps = 4;       // rows (warps) per CTA (32 KB of static shared memory)
+constexpr int kBkRank = 96;       // rows up to this many entries: rank sort (3 keys per lane), else bitonic
+constexpr int kBkSmall = 256;     // rows up to this many entries: 2 KB per warp (bk_rows)
+constexpr int kBkWarps = 8;       // rows (warps) per CTA of bk_rows
 
 struct BkSpec {
   int two_sided;                  // reverse entries (SYMMETRIZED)
@@ -332,34 +334,59 @@ __global__ void bk_scatter(const int64_t* __restrict__ src, const int64_t* __res
 // (forward and reverse weights apart, as group_reduce), keep non-zero sums
 // (SYMMETRIZED), write the row's unique entries at the start of its bucket and its
 // degree (forward sums then reverse sums, each in column order, as row_degrees).
-__global__ void __launch_bounds__(32 * kBkWarps)
-bk_rows(const int* __restrict__ off, int32_t nrows, const uint64_t* __restrict__ keys,
-        const double* __restrict__ w, int drop_zero, int with_reverse, int32_t* __restrict__ tcol,
-        double* __restrict__ tval, int* __restrict__ ucnt, double* __restrict__ deg) {
-  __shared__ uint64_t buf[kBkWarps][kBkMaxRow];
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  uint64_t* b = buf[wid];
-  for (int64_t row = (int64_t)blockIdx.x * kBkWarps + wid; row < nrows;
-       row += (int64_t)gridDim.x * kBkWarps) {
+// One row (one warp): b is this warp's shared buffer of CAP keys; rows with cnt in
+// (lo, CAP] are processed, others skipped (handled by the other launch).
+template <int CAP>
+__device__ __forceinline__ void bk_row(int64_t row, int lo, uint64_t* b, const int* __restrict__ off,
+                                       const uint64_t* __restrict__ keys, const double* __restrict__ w,
+                                       int drop_zero, int with_reverse, int32_t* __restrict__ tcol,
+                                       double* __restrict__ tval, int* __restrict__ ucnt,
+                                       double* __restrict__ deg) {
+  const int lane = threadIdx.x & 31;
     const int o0 = off[row], cnt = off[row + 1] - o0;
-    int P = 1;
-    while (P < cnt) P <<= 1;
-    for (int i = lane; i < P; i += 32) b[i] = i < cnt ? keys[o0 + i] : ~0ull;
-    __syncwarp();
-    for (int k = 2; k <= P; k <<= 1)
-      for (int j = k >> 1; j > 0; j >>= 1) {
-        for (int i = lane; i < P; i += 32) {
-          const int ixj = i ^ j;
-          if (ixj > i) {
-            const uint64_t x = b[i], y = b[ixj];
-            if ((x > y) == ((i & k) == 0)) {
-              b[i] = y;
-              b[ixj] = x;
+    if (cnt <= lo || cnt > CAP) return;
+    if (cnt <= kBkRank) {
+      // short rows (most of them): rank sort -- every key's position is the number of
+      // smaller keys (keys are unique: the payload is), read by broadcast from the
+      // second half of the buffer
+      uint64_t* in = b + CAP / 2;
+      for (int i = lane; i < cnt; i += 32) in[i] = keys[o0 + i];
+      __syncwarp();
+      // up to three keys per lane ranked in one pass over the row (kBkRank <= 96)
+      const uint64_t k0 = lane < cnt ? in[lane] : ~0ull;
+      const uint64_t k1 = lane + 32 < cnt ? in[lane + 32] : ~0ull;
+      const uint64_t k2 = lane + 64 < cnt ? in[lane + 64] : ~0ull;
+      int r0 = 0, r1 = 0, r2 = 0;
+      for (int t = 0; t < cnt; ++t) {
+        const uint64_t v = in[t];
+        r0 += v < k0;
+        r1 += v < k1;
+        r2 += v < k2;
+      }
+      if (lane < cnt) b[r0] = k0;
+      if (lane + 32 < cnt) b[r1] = k1;
+      if (lane + 64 < cnt) b[r2] = k2;
+      __syncwarp();
+    } else {
+      int P = 1;
+      while (P < cnt) P <<= 1;
+      for (int i = lane; i < P; i += 32) b[i] = i < cnt ? keys[o0 + i] : ~0ull;
+      __syncwarp();
+      for (int k = 2; k <= P; k <<= 1)
+        for (int j = k >> 1; j > 0; j >>= 1) {
+          for (int i = lane; i < P; i += 32) {
+            const int ixj = i ^ j;
+            if (ixj > i) {
+              const uint64_t x = b[i], y = b[ixj];
+              if ((x > y) == ((i & k) == 0)) {
+                b[i] = y;
+                b[ixj] = x;
+              }
             }
           }
+          __syncwarp();
         }
-        __syncwarp();
-      }
+    }
     int u0 = 0;
     double a = 0.0, c = 0.0;
     for (int base = 0; base < cnt; base += 32) {
@@ -395,21 +422,54 @@ bk_rows(const int* __restrict__ off, int32_t nrows, const uint64_t* __restrict__
       }
       // degree: forward then reverse group sums in column order (lane order here)
       const double fk = (keep && hf) ? f : 0.0, rk = (keep && hr) ? r : 0.0;
-      const bool fh = keep && hf, rh = keep && hr;
-      const unsigned fm = __ballot_sync(0xffffffffu, fh), rm = __ballot_sync(0xffffffffu, rh);
-      for (int t = 0; t < 32; ++t) {
-        const double ft = __shfl_sync(0xffffffffu, fk, t), rt = __shfl_sync(0xffffffffu, rk, t);
-        if ((fm >> t) & 1u) a += ft;
-        if ((rm >> t) & 1u) c += rt;
+      if (!w) {
+        // unit weights: every sum is an exact integer, so lane-local partials and a
+        // tree reduction give the same bits as the ordered sum
+        a += fk;
+        c += rk;
+      } else if (deg) {
+        const bool fh = keep && hf, rh = keep && hr;
+        const unsigned fm = __ballot_sync(0xffffffffu, fh), rm = __ballot_sync(0xffffffffu, rh);
+        for (int t = 0; t < 32; ++t) {
+          const double ft = __shfl_sync(0xffffffffu, fk, t), rt = __shfl_sync(0xffffffffu, rk, t);
+          if ((fm >> t) & 1u) a += ft;
+          if ((rm >> t) & 1u) c += rt;
+        }
       }
       u0 += __popc(km);
+    }
+    if (!w && deg) {
+      a = warp_sum(a);
+      c = warp_sum(c);
     }
     if (lane == 0) {
       ucnt[row] = u0;
       if (deg) deg[row] = with_reverse ? a + c : a;
     }
     __syncwarp();
-  }
+}
+
+// Rows of at most kBkSmall entries, 2 KB of shared memory per warp (full occupancy).
+__global__ void __launch_bounds__(32 * kBkWarps)
+bk_rows(const int* __restrict__ off, int32_t nrows, const uint64_t* __restrict__ keys,
+        const double* __restrict__ w, int drop_zero, int with_reverse, int32_t* __restrict__ tcol,
+        double* __restrict__ tval, int* __restrict__ ucnt, double* __restrict__ deg) {
+  __shared__ uint64_t buf[kBkWarps][kBkSmall];
+  const int wid = threadIdx.x >> 5;
+  for (int64_t row = (int64_t)blockIdx.x * kBkWarps + wid; row < nrows;
+       row += (int64_t)gridDim.x * kBkWarps)
+    bk_row<kBkSmall>(row, -1, buf[wid], off, keys, w, drop_zero, with_reverse, tcol, tval, ucnt, deg);
+}
+
+// The few longer rows (kBkSmall < cnt <= kBkMaxRow): one warp per CTA, 8 KB.
+__global__ void __launch_bounds__(32)
+bk_rows_big(const int* __restrict__ off, int32_t nrows, const uint64_t* __restrict__ keys,
+            const double* __restrict__ w, int drop_zero, int with_reverse, int32_t* __restrict__ tcol,
+            double* __restrict__ tval, int* __restrict__ ucnt, double* __restrict__ deg) {
+  __shared__ uint64_t buf[kBkMaxRow];
+  for (int64_t row = blockIdx.x; row < nrows; row += gridDim.x)
+    bk_row<kBkMaxRow>(row, kBkSmall, buf, off, keys, w, drop_zero, with_reverse, tcol, tval, ucnt,
+                      deg);
 }
 
 __global__ void bk_copy(const int* __restrict__ off, const int32_t* __restrict__ row_ptr,
@@ -654,6 +714,9 @@ int bucket_build(BuildLayout& L, const int64_t* src, const int64_t* dst, const d
   const int rblocks = (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(nrows, kBkWarps), num_sms() * 8));
   bk_rows<<<rblocks, 32 * kBkWarps, 0, st>>>(L.boff, nrows, L.ka, w, symmetrized ? 1 : 0,
                                              symmetrized ? 1 : 0, tcol, L.fsum, L.bucnt, deg);
+  if (h[1] > kBkSmall)
+    bk_rows_big<<<(int)std::min<int64_t>(nrows, num_sms() * 16), 32, 0, st>>>(
+        L.boff, nrows, L.ka, w, symmetrized ? 1 : 0, symmetrized ? 1 : 0, tcol, L.fsum, L.bucnt, deg);
   SPB_LAUNCH_CHECK();
   SPB_TRY(exclusive_scan_i32(L.bucnt, row_ptr, nrows, L.scan_tmp, row_ptr + nrows, st));
   int nnz = 0;
