@@ -27,6 +27,8 @@
 //             emit, store the running sum (+ init) as float32 rows.
 #include <cuda.h>
 
+#include <cstdlib>
+
 #include "dense.cuh"
 
 namespace spb {
@@ -106,6 +108,28 @@ __device__ __forceinline__ void ut_commit(uint64_t* bar) {
                    ut_smem(bar))
                : "memory");
 }
+// A from tensor memory (the split operands written by the splitter warps with
+// tcgen05.st), B from shared memory.
+__device__ __forceinline__ void ut_mma_ts(uint32_t tmem_d, uint32_t tmem_a, uint64_t b, uint32_t idesc,
+                                          uint32_t accum) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, p;\n\t}" ::"r"(tmem_d),
+      "r"(tmem_a), "l"(b), "r"(idesc), "r"(accum));
+}
+__device__ __forceinline__ void ut_tmem_st32(uint32_t taddr, const float* v) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, "
+      "%12, %13, %14, %15, %16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, "
+      "%30, %31, %32};" ::"r"(taddr),
+      "f"(v[0]), "f"(v[1]), "f"(v[2]), "f"(v[3]), "f"(v[4]), "f"(v[5]), "f"(v[6]), "f"(v[7]),
+      "f"(v[8]), "f"(v[9]), "f"(v[10]), "f"(v[11]), "f"(v[12]), "f"(v[13]), "f"(v[14]), "f"(v[15]),
+      "f"(v[16]), "f"(v[17]), "f"(v[18]), "f"(v[19]), "f"(v[20]), "f"(v[21]), "f"(v[22]), "f"(v[23]),
+      "f"(v[24]), "f"(v[25]), "f"(v[26]), "f"(v[27]), "f"(v[28]), "f"(v[29]), "f"(v[30]), "f"(v[31])
+      : "memory");
+}
+
 // Round to the nearest TF32 value (a float32 container with 13 zero low bits).
 __device__ __forceinline__ float tf32_rna(float x) {
   uint32_t r;
@@ -177,14 +201,20 @@ __global__ void tc_stage_coeffs(UpdParams P, int npad, float* __restrict__ dst) 
   }
 }
 
-template <int NPMAX, int EW>
+// ATM (A in tensor memory, npad <= 128): the splitters read their row of the TMA'd
+// A tile, split it and store hi / lo into per-stage TMEM columns (256 + 64 s ...),
+// so a stage is only [A raw][B hi|lo] in shared memory -- four stages instead of
+// three -- and the MMAs read A from TMEM instead of shared memory.
+template <int NPMAX, int EW, bool ATM = false>
 __global__ void __launch_bounds__(EW == 1 ? kUtThreads : kUtThreadsW, 1)
 update_tc_kernel(const __grid_constant__ CUtensorMap map0, const __grid_constant__ CUtensorMap map1,
                  const __grid_constant__ CUtensorMap map2, UtParams P) {
   extern __shared__ __align__(1024) uint8_t usm_raw[];
   uint8_t* base = (uint8_t*)(((uintptr_t)usm_raw + 1023) & ~(uintptr_t)1023);
   const int kB = 2 * P.npad * UTK * 4;              // coefficient chunk bytes (hi | lo)
-  const int kStage = 2 * kUtA + kB;                 // [A hi (staged in place)][A lo][B hi|lo]
+  // [A hi (staged in place)][A lo][B hi|lo], or with ATM [A raw][B hi|lo]
+  const int kStage = (ATM ? 1 : 2) * kUtA + kB;
+  const int kBoff = (ATM ? 1 : 2) * kUtA;          // B offset inside a stage
   const int UTS = P.stages;
   uint64_t* full = (uint64_t*)(base + UTS * kStage);
   uint64_t* split = full + UTS_MAX;
@@ -237,7 +267,7 @@ update_tc_kernel(const __grid_constant__ CUtensorMap map0, const __grid_constant
             uint8_t* sb = base + st * kStage;
             ut_expect(&full[st], (uint32_t)(kUtA + kB));
             ut_tma2d(sb, map, &full[st], c * UTK, tile * UTM);
-            ut_bulk(sb + 2 * kUtA, P.coef + (size_t)kc * 2 * P.npad * UTK, (uint32_t)kB, &full[st]);
+            ut_bulk(sb + kBoff, P.coef + (size_t)kc * 2 * P.npad * UTK, (uint32_t)kB, &full[st]);
           }
         }
       }
@@ -259,17 +289,29 @@ update_tc_kernel(const __grid_constant__ CUtensorMap map0, const __grid_constant
         ut_wait(&split[st], u & 1);
         asm volatile("tcgen05.fence::after_thread_sync;");
         uint8_t* sb = base + st * kStage;
-        const uint32_t ahi = ut_smem(sb), alo = ut_smem(sb + kUtA);
-        const uint32_t bhi = ut_smem(sb + 2 * kUtA), blo = bhi + (uint32_t)(P.npad * UTK * 4);
+        const uint32_t bhi = ut_smem(sb + kBoff), blo = bhi + (uint32_t)(P.npad * UTK * 4);
         const uint32_t dacc = tmem + (uint32_t)(rg * P.npad);
+        if constexpr (ATM) {
+          const uint32_t ta = tmem + 256u + (uint32_t)st * 64u;  // hi at +0, lo at +32
 #pragma unroll
-        for (int kk = 0; kk < UTK / 8; ++kk) {
-          const uint32_t off = (uint32_t)kk * 32;
-          const uint64_t dah = ut_desc_sw128(ahi + off), dal = ut_desc_sw128(alo + off);
-          const uint64_t dbh = ut_desc_sw128(bhi + off), dbl = ut_desc_sw128(blo + off);
-          ut_mma(dacc, dah, dbl, idesc, (kk == 0 && first) ? 0u : 1u);  // small terms first
-          ut_mma(dacc, dal, dbh, idesc, 1u);
-          ut_mma(dacc, dah, dbh, idesc, 1u);
+          for (int kk = 0; kk < UTK / 8; ++kk) {
+            const uint32_t off = (uint32_t)kk * 32;
+            const uint64_t dbh = ut_desc_sw128(bhi + off), dbl = ut_desc_sw128(blo + off);
+            ut_mma_ts(dacc, ta + kk * 8, dbl, idesc, (kk == 0 && first) ? 0u : 1u);
+            ut_mma_ts(dacc, ta + 32 + kk * 8, dbh, idesc, 1u);
+            ut_mma_ts(dacc, ta + kk * 8, dbh, idesc, 1u);
+          }
+        } else {
+          const uint32_t ahi = ut_smem(sb), alo = ut_smem(sb + kUtA);
+#pragma unroll
+          for (int kk = 0; kk < UTK / 8; ++kk) {
+            const uint32_t off = (uint32_t)kk * 32;
+            const uint64_t dah = ut_desc_sw128(ahi + off), dal = ut_desc_sw128(alo + off);
+            const uint64_t dbh = ut_desc_sw128(bhi + off), dbl = ut_desc_sw128(blo + off);
+            ut_mma(dacc, dah, dbl, idesc, (kk == 0 && first) ? 0u : 1u);  // small terms first
+            ut_mma(dacc, dal, dbh, idesc, 1u);
+            ut_mma(dacc, dah, dbh, idesc, 1u);
+          }
         }
         ut_commit(&empty[st]);
         if (P.gend[j]) {
@@ -285,6 +327,28 @@ update_tc_kernel(const __grid_constant__ CUtensorMap map0, const __grid_constant
     for (int kc = 0; kc < total; ++kc) {
       const int st = kc % UTS, u = kc / UTS;
       ut_wait(&full[st], u & 1);
+      if constexpr (ATM) {
+        // this thread's row of the 128B-swizzled tile: 16-byte chunk c of row r sits at
+        // position c ^ (r & 7) (conflict-free: 8 rows cover all banks)
+        const int r = 32 * (warp & 3) + lane;
+        const float4* row4 = reinterpret_cast<const float4*>(base + st * kStage + r * 128);
+        float hi[32], lo[32];
+#pragma unroll
+        for (int c = 0; c < 8; ++c) {
+          const float4 x = row4[c ^ (r & 7)];
+          tf32_split(x.x, hi[4 * c], lo[4 * c]);
+          tf32_split(x.y, hi[4 * c + 1], lo[4 * c + 1]);
+          tf32_split(x.z, hi[4 * c + 2], lo[4 * c + 2]);
+          tf32_split(x.w, hi[4 * c + 3], lo[4 * c + 3]);
+        }
+        const uint32_t ta = tmem + ((uint32_t)(32 * (warp & 3)) << 16) + 256u + (uint32_t)st * 64u;
+        ut_tmem_st32(ta, hi);
+        ut_tmem_st32(ta + 32, lo);
+        asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+        asm volatile("tcgen05.fence::before_thread_sync;");
+        ut_arrive(&split[st]);
+        continue;
+      }
       float4* a = reinterpret_cast<float4*>(base + st * kStage);
       float4* lo = reinterpret_cast<float4*>(base + st * kStage + kUtA);
 #pragma unroll
@@ -502,14 +566,20 @@ bool update_tc(const UpdParams& p, int64_t n, cudaStream_t st) {
   P.argmin_labels = p.argmin_labels;
   P.argmin_changed = p.argmin_changed;
   P.n = n;
+  // A in tensor memory for 64 < npad <= 128 (C3's l = 108): 2 x npad accumulator
+  // columns + 4 stages x 64 split-operand columns fit the 512 TMEM columns
+  static const bool atm_env = !getenv("SPB_UT_ATM") || atoi(getenv("SPB_UT_ATM")) != 0;
+  const bool atm = atm_env && npad > 64 && npad <= 128;
+  if (atm) cols = 512;
   P.tmem_cols = cols;
   const int kB = 2 * npad * UTK * 4;
-  const size_t kStage = 2 * kUtA + kB;
+  const size_t kStage = (atm ? 1 : 2) * kUtA + kB;
   // two stages when two CTAs fit per SM (one CTA's epilogue overlaps the other's
   // MMAs), else three
   constexpr size_t kExtra = 1024 + 256 + 4 * UTM * 8;  // alignment, barriers, argmin keys
   int stages = 2 * (2 * kStage + kExtra) <= 227 * 1024 ? 2 : 3;
   if ((size_t)stages * kStage + kExtra > 227 * 1024) stages = 2;
+  if (atm) stages = 4;
   P.stages = stages;
   const size_t smem = (size_t)stages * kStage + kExtra;
   static std::atomic<uint64_t> attr{0};
@@ -517,13 +587,16 @@ bool update_tc(const UpdParams& p, int64_t n, cudaStream_t st) {
     cudaFuncSetAttribute(update_tc_kernel<64, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
     cudaFuncSetAttribute(update_tc_kernel<128, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
     cudaFuncSetAttribute(update_tc_kernel<192, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    cudaFuncSetAttribute(update_tc_kernel<128, 1, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
     mark_on_device(attr);
   }
   if (smem > 227 * 1024) return false;
   tc_stage_coeffs<<<64, 256, 0, st>>>(p, npad, p.cstage);
-  const int per_sm = 2 * (smem + 2048) <= 228 * 1024 ? 2 : 1;
+  const int per_sm = !atm && 2 * (smem + 2048) <= 228 * 1024 ? 2 : 1;
   const unsigned grid = (unsigned)std::min<int64_t>(ceil_div(n, UTM), (int64_t)per_sm * num_sms());
-  if (npad <= 64)
+  if (atm)
+    update_tc_kernel<128, 1, true><<<grid, kUtThreads, smem, st>>>(maps[0], maps[1], maps[2], P);
+  else if (npad <= 64)
     update_tc_kernel<64, 1><<<grid, kUtThreads, smem, st>>>(maps[0], maps[1], maps[2], P);
   else if (npad <= 128)
     update_tc_kernel<128, 1><<<grid, kUtThreads, smem, st>>>(maps[0], maps[1], maps[2], P);
