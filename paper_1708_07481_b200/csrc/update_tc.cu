@@ -331,11 +331,14 @@ update_tc_kernel(const __grid_constant__ CUtensorMap map0, const __grid_constant
         // this thread's row of the 128B-swizzled tile: 16-byte chunk c of row r sits at
         // position c ^ (r & 7) (conflict-free: 8 rows cover all banks)
         const int r = 32 * (warp & 3) + lane;
-        const float4* row4 = reinterpret_cast<const float4*>(base + st * kStage + r * 128);
+        const uint32_t row_s = ut_smem(base + st * kStage + r * 128);  // explicit ld.shared
         float hi[32], lo[32];
 #pragma unroll
         for (int c = 0; c < 8; ++c) {
-          const float4 x = row4[c ^ (r & 7)];
+          float4 x;
+          asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
+                       : "=f"(x.x), "=f"(x.y), "=f"(x.z), "=f"(x.w)
+                       : "r"(row_s + (uint32_t)((c ^ (r & 7)) * 16)));
           tf32_split(x.x, hi[4 * c], lo[4 * c]);
           tf32_split(x.y, hi[4 * c + 1], lo[4 * c + 1]);
           tf32_split(x.z, hi[4 * c + 2], lo[4 * c + 2]);
@@ -349,19 +352,23 @@ update_tc_kernel(const __grid_constant__ CUtensorMap map0, const __grid_constant
         ut_arrive(&split[st]);
         continue;
       }
-      float4* a = reinterpret_cast<float4*>(base + st * kStage);
-      float4* lo = reinterpret_cast<float4*>(base + st * kStage + kUtA);
+      // explicit shared-space accesses (generic pointers derived from the aligned
+      // dynamic-smem base compiled to generic LD/ST: lg_throttle stalls in ncu)
+      const uint32_t a_s = ut_smem(base + st * kStage), lo_s = a_s + kUtA;
 #pragma unroll
       for (int i = 0; i < kUtA / 16 / 128; ++i) {
-        const int e = i * 128 + t;
-        const float4 x = a[e];
-        float4 h, l;
+        const uint32_t e = (uint32_t)(i * 128 + t) * 16u;
+        float4 x, h, l;
+        asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
+                     : "=f"(x.x), "=f"(x.y), "=f"(x.z), "=f"(x.w) : "r"(a_s + e));
         tf32_split(x.x, h.x, l.x);
         tf32_split(x.y, h.y, l.y);
         tf32_split(x.z, h.z, l.z);
         tf32_split(x.w, h.w, l.w);
-        a[e] = h;
-        lo[e] = l;
+        asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(a_s + e), "f"(h.x), "f"(h.y),
+                     "f"(h.z), "f"(h.w) : "memory");
+        asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(lo_s + e), "f"(l.x), "f"(l.y),
+                     "f"(l.z), "f"(l.w) : "memory");
       }
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       ut_arrive(&split[st]);
