@@ -399,30 +399,12 @@ update_tc_kernel(const __grid_constant__ CUtensorMap map0, const __grid_constant
         const int rg = G & 1;
         ut_wait(&rdone[rg], (G >> 1) & 1);
         asm volatile("tcgen05.fence::after_thread_sync;");
-        // 32 TMEM columns per tcgen05.ld (x32) and wait::ld where they fit: 4 round
-        // trips per chunk at npad = 112 instead of 7
 #pragma unroll
-        for (int c0 = 0; c0 < NH; c0 += 32) {
-          const uint32_t taddr =
-              tmem + ((uint32_t)(quarter * 32) << 16) + (uint32_t)(rg * P.npad + cb + c0);
-          if (c0 + 32 <= NH && cb + c0 + 32 <= P.npad) {
-            uint32_t r[32];
-            asm volatile(
-                "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, "
-                "%10, %11, %12, %13, %14, %15, %16, %17, %18, %19, %20, %21, %22, %23, %24, %25, "
-                "%26, %27, %28, %29, %30, %31}, [%32];"
-                : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]),
-                  "=r"(r[6]), "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]),
-                  "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]), "=r"(r[16]), "=r"(r[17]),
-                  "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]),
-                  "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]),
-                  "=r"(r[30]), "=r"(r[31])
-                : "r"(taddr));
-            asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-#pragma unroll
-            for (int i = 0; i < 32; ++i) acc[c0 + i] += __uint_as_float(r[i]);
-          } else if (cb + c0 < P.npad) {
+        for (int c0 = 0; c0 < NH; c0 += 16) {
+          if (cb + c0 < P.npad) {
             uint32_t r[16];
+            const uint32_t taddr =
+                tmem + ((uint32_t)(quarter * 32) << 16) + (uint32_t)(rg * P.npad + cb + c0);
             asm volatile(
                 "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, "
                 "%10, %11, %12, %13, %14, %15}, [%16];"
@@ -432,8 +414,7 @@ update_tc_kernel(const __grid_constant__ CUtensorMap map0, const __grid_constant
                 : "r"(taddr));
             asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 #pragma unroll
-            for (int i = 0; i < 16; ++i)
-              if (c0 + i < NH) acc[c0 + i] += __uint_as_float(r[i]);
+            for (int i = 0; i < 16; ++i) acc[c0 + i] += __uint_as_float(r[i]);
           }
         }
         asm volatile("tcgen05.fence::before_thread_sync;");
