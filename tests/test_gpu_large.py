@@ -208,3 +208,38 @@ def test_c5_stream_parity(spb, c5, key, precision):
     # C5 streams the C2 graph, on which this Laplacian's partition is degenerate (PM
     # 0.12 vs truth): its labels are the most round-off-sensitive of all the pins
     assert agree >= (0.999 if pinned == len(res) and precision == "float64" else 0.99), agree
+
+
+def test_c4_full_partition_parity(spb):
+    """C4 under the 10x rule, the whole partition (large_c4full.npz: the reference ran
+    25 iterations in ~1 h of CPU here): iteration count, Ritz values, residual history,
+    labels and PR / PP against the reference's own, float32 storage."""
+    gold = _need("large_c4full")
+    key = "c4_s0"
+    spec, edges, truth = config_input("c4", seed=0)
+    assert sha(edges) == str(gold[f"{key}/edges_sha"])
+    k = spec.blocks
+    l = spb.block_size_for(k)
+    x0 = np.random.default_rng(0).standard_normal((spec.n, l))
+    g = spb.from_edges(edges, spec.n)
+    cfg = spb.SolverConfig(block_size=l, tol=float(gold[f"{key}/tol"]),
+                           max_iter=int(gold[f"{key}/max_iter"]), seed=0)
+    hr = []
+    part, st, _ = spb.partition_static(g, cfg, k_expected=k, fix_k=True, x0=x0, precision="float32",
+                                       callback=lambda it, t, r: hr.append(r))
+    ref_it = int(gold[f"{key}/iterations"])
+    a, b = np.array(hr)[:, : k + 1], gold[f"{key}/hist_norms"][:, : k + 1]
+    n_cmp = min(len(a), len(b))
+    dev = np.max(np.abs(np.log10(a[:n_cmp] / b[:n_cmp])))
+    agree = oracle.partition_match(gold[f"{key}/labels"].astype(np.int64), part.labels)
+    pr = oracle.pairwise_recall(truth, part.labels)
+    pp = oracle.pairwise_precision(truth, part.labels)
+    rp = gold[f"{key}/pm_pr_pp"]
+    print(f"\nC4 float32 full: iterations {st.iterations} (reference {ref_it}), max |log10 residual "
+          f"ratio| {dev:.2e}, label agreement {agree:.5f}, PR {pr:.4f} (ref {rp[1]:.4f}), PP {pp:.4f} "
+          f"(ref {rp[2]:.4f}), orth_p {st.solve_stats['orth_p']}")
+    assert st.iterations == ref_it
+    assert _theta_close(st.eigenvalues, gold[f"{key}/theta"])
+    assert dev <= 0.01
+    assert agree >= 0.999, agree
+    assert abs(pr - rp[1]) <= 0.005 and abs(pp - rp[2]) <= 0.005
