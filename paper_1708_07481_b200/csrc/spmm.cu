@@ -228,6 +228,11 @@ int launch_spmm(int32_t r0, int32_t r1, const int32_t* rp, const int32_t* ci, co
   // eviction-priority hints on full rows (fractional evict_last on the gathered X,
   // evict_first on the CSR and Y), 1.53-1.70 ms. ncu at C3: 6.49 GB of DRAM reads
   // per launch (L2 hit rate 26 %) at 4.2 TB/s -- the gathers miss a 216 MB X block.
+  // More loads or warps in flight do not raise it (C3 / C4 ms: U = 2 gathers per lane,
+  // 8 CTAs of 4 warps per SM 1.55 / 13.4; U = 4 1.56 / 12.8; U = 2 at 16 CTAs 1.88 /
+  // 16.4; U = 4 at 12 CTAs 1.87 / 15.5; U = 8 4.36 / 33.6): ~4.3 TB/s is what random
+  // 448-byte row gathers sustain here; a contiguous X (ld = l instead of the solver's
+  // 3 lp) gains 4 %.
   (void)x_rows;
   {
     const int c0 = 0, pc = ncols;
