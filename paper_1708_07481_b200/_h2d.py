@@ -29,30 +29,43 @@ def _executor() -> ThreadPoolExecutor:
     return _pool
 
 
-def to_device(arr: np.ndarray, device) -> torch.Tensor:
-    """Copy a C-contiguous numpy array to ``device`` (same dtype, same shape)."""
+def to_device(arr: np.ndarray, device, dtype=None) -> torch.Tensor:
+    """Copy a C-contiguous numpy array to ``device``; with ``dtype`` (a numpy dtype)
+    the host threads convert while staging (round to nearest, as numpy's astype), so
+    only the converted bytes cross the link."""
+    if dtype is not None and np.dtype(dtype) != arr.dtype:
+        if arr.nbytes < _SMALL or not arr.flags.c_contiguous:
+            return torch.from_numpy(arr.astype(dtype)).to(device, non_blocking=True)
+        return _staged(arr, device, np.dtype(dtype))
     src = torch.from_numpy(arr)
     if arr.nbytes < _SMALL or not arr.flags.c_contiguous:
         return src.to(device, non_blocking=True)
-    out = torch.empty(arr.shape, dtype=src.dtype, device=device)
-    flat = arr.reshape(-1).view(np.uint8)
+    return _staged(arr, device, arr.dtype)
+
+
+def _staged(arr: np.ndarray, device, dtype: np.dtype) -> torch.Tensor:
+    out = torch.empty(arr.shape, dtype=torch.from_numpy(np.empty(0, dtype)).dtype, device=device)
+    esz_out = dtype.itemsize
+    flat = arr.reshape(-1)
     dflat = out.view(-1).view(torch.uint8)
     stream = torch.cuda.current_stream(device)
     bufs = [torch.empty(_CHUNK, dtype=torch.uint8, pin_memory=True) for _ in range(3)]
     done = [None, None, None]
     pool = _executor()
-    nb = flat.size
-    for i, off in enumerate(range(0, nb, _CHUNK)):
+    per = _CHUNK // esz_out  # elements per chunk
+    n = flat.size
+    for i, off in enumerate(range(0, n, per)):
         b = i % 3
         if done[b] is not None:
             done[b].synchronize()  # the DMA that last read this buffer has finished
-        m = min(_CHUNK, nb - off)
-        hb = bufs[b].numpy()
+        m = min(per, n - off)
+        hb = bufs[b].numpy().view(dtype)
         step = -(-m // _THREADS)
         list(pool.map(lambda j: np.copyto(hb[j * step:min(m, (j + 1) * step)],
-                                          flat[off + j * step:off + min(m, (j + 1) * step)]),
+                                          flat[off + j * step:off + min(m, (j + 1) * step)],
+                                          casting="unsafe"),
                       range(_THREADS)))
-        dflat[off:off + m].copy_(bufs[b][:m], non_blocking=True)
+        dflat[off * esz_out:(off + m) * esz_out].copy_(bufs[b][:m * esz_out], non_blocking=True)
         ev = torch.cuda.Event()
         ev.record(stream)
         done[b] = ev

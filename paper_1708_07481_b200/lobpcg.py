@@ -300,11 +300,15 @@ def _native_operator(operator, dtype: str):
                         "(the reference's operator protocol, graph.py:300-317)")
 
 
-def _x0_device(x0, n, l):
+def _x0_device(x0, n, l, precision="float64"):
     if isinstance(x0, torch.Tensor):
         t = x0.to(device=_device(), dtype=torch.float64)
         return t.contiguous()
     arr = np.ascontiguousarray(x0, dtype=np.float64)
+    if precision == "float32":
+        # the solver rounds x0 to float32 storage first thing (copy_block, round to
+        # nearest): round on the host while staging (same bits) and move half the bytes
+        return _h2d.to_device(arr, _device(), np.float32).double()
     return _h2d.to_device(arr, _device())  # multi-threaded pinned ring for large blocks
 
 
@@ -338,7 +342,7 @@ def lobpcg_solve(operator, x0, config: SolverConfig, precond=None, n_converge: i
     op, precision, host_op = _native_operator(operator, precision)
     code, tdt = DTYPES[precision]
     L = N.lib()
-    x0_d = _x0_device(x0, n, l)
+    x0_d = _x0_device(x0, n, l, precision)
     ws_bytes = L.spb_lobpcg_workspace(code, n, l)
     ws = torch.empty(ws_bytes, dtype=torch.uint8, device=x0_d.device)
     cfg = N.SolverConfigC(block_size=l, max_iter=config.max_iter, tol=config.tol,
