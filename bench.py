@@ -620,7 +620,9 @@ def run_ours(args):
                                   "kernel_shares (latency-bound small dense solves dominate at C1/C2)")},
             "cpu_baseline": cpu,
             "e2e": {"value": e2e_value, "unit": UNIT,
-                    "h2d_bytes_per_step": int(edges_host.nbytes + x0.nbytes),
+                    # arcs as int64; x0 crosses as float32 for float32 storage (_h2d.py)
+                    "h2d_bytes_per_step": int(edges_host.nbytes + x0.nbytes
+                                              // (2 if args.precision == "float32" else 1)),
                     "d2h_bytes_per_step": int(4 * spec.n + 16 * l)},
             "gpu_launches": int(launches_per_step * args.steps) if launches_per_step is not None else None,
             "kernel_shares": shares,
