@@ -560,9 +560,8 @@ def run_ours(args):
         t = torch.tensor([sum(e2e_times)], dtype=torch.float64, device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         e2e_value = e2e_iters * (1 if sharded else world) / float(t.item())
-    launches_per_step, shares = None, None
-    if not sharded:
-        launches_per_step, _, shares = count_launches(step_device)
+    # every rank runs the profiled step (the sharded step has collectives); rank 0 reports
+    launches_per_step, _, shares = count_launches(step_device)
     out = None
     if rank == 0:
         pm = spb.partition_match(spb.contingency(truth, part.labels if hasattr(part, "labels") else part))
