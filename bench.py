@@ -434,13 +434,18 @@ def run_ours(args):
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0")) % max(1, torch.cuda.device_count())
     torch.cuda.set_device(local)
     dist = None
     if world > 1:
         import torch.distributed as dist
 
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        # SPB_SHARD_TRANSPORT=host: gloo process group and the host-staged transport, so
+        # the N > 1 bench path can be exercised with several ranks on one GPU (tests)
+        if os.environ.get("SPB_SHARD_TRANSPORT") == "host":
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     os.environ["SPB_PROFILE_SPMM"] = "1"
     import paper_1708_07481_b200 as spb
     from paper_1708_07481_b200.spectral import partition_device
@@ -466,7 +471,7 @@ def run_ours(args):
         from paper_1708_07481_b200.sharded import (RowShardedLaplacian, _Comm,
                                                    partition_edges_sharded, partition_static_sharded)
 
-        comm = _Comm()
+        comm = _Comm(transport=os.environ.get("SPB_SHARD_TRANSPORT", "nccl"))
 
     def step_device():
         if sharded:
