@@ -585,6 +585,58 @@ def run_ours(args):
             except ImportError as e:
                 cpu = {"value": None, "unit": UNIT, "cores": threads, "kind": "reference",
                        "sample": f"unavailable: {e}"}
+        spmm_roof = {
+            "bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+            "frac": (achieved / peak) if achieved else None, "traffic": traffic,
+            "traffic_achieved": (traffic / (spmm_us * 1e-6 / max(spmm_calls, 1)) / 1e9)
+            if (traffic and spmm_us) else None,
+            "traffic_frac": (traffic / (spmm_us * 1e-6 / max(spmm_calls, 1)) / 1e9 / peak)
+            if (traffic and spmm_us) else None,
+            "traffic_note": "ncu dram__bytes_read+write of one launch (profiles/spmm_traffic.json) over "
+                            "this run's average launch time: the DRAM bandwidth the SpMM sustains",
+            "kernel": "spb::spmm_vb (Laplacian SpMM)", "peak_kind": peak_kind, "launches": spmm_calls,
+            "avg_launch_us": spmm_us / max(spmm_calls, 1), "live_ms_total": spmm_us / 1e3,
+            "bytes_model": "compulsory 4(n+1)+(4+esz)nnz+esz*n+2*esz*n*cols per apply",
+            "gather_model": {"achieved": gather_achieved,
+                             "frac": (gather_achieved / peak) if gather_achieved else None,
+                             "bytes_model": "compulsory + esz*nnz*cols"}}
+        # Rayleigh-Ritz Gram pairs timed live inside the solves (CUDA events around every
+        # pair on the solver's stream, lobpcg.cu rr_grams): algorithmic flops 4 n m^2 each
+        g_us = sum(s.get("gram_us", 0) for s in stats)
+        g_mflop = sum(s.get("gram_mflop", 0) for s in stats)
+        g_calls = sum(s.get("gram_calls", 0) for s in stats)
+        pk = json.loads((ROOT / "profiles" / "r02" / "peaks_tensor.json").read_text()) \
+            if (ROOT / "profiles" / "r02" / "peaks_tensor.json").exists() else {}
+        oz = "oz" in gram.get("kernel", "")
+        g_tf = (g_mflop * 1e6 / (g_us * 1e-6) / 1e12) if g_us else None
+        if oz:
+            i8 = pk.get("int8_tops") or 4500.0
+            tops = 15 * g_tf if g_tf else None
+            gram_roof = {"bound": "tensor", "pipe": "int8 tcgen05 (Ozaki splitting, 5 digits)",
+                         "achieved": tops, "peak": i8, "unit": "TOPS", "frac": tops / i8 if tops else None,
+                         "peak_kind": "measured (torch._int_mm 8192^3, profiles/r02/peaks_tensor.json)"
+                         if pk.get("int8_tops") else "spec",
+                         "fp64_equivalent_tflops": g_tf,
+                         "ops_model": "15 int8 digit-pair GEMMs x 4 n m^2 (G_A = B'LB, G_B = B'B) per pair, "
+                                      "time incl. column maxima, digit packing, split-K reduction",
+                         "kernel": "spb::gram_oz_kernel (+ oz_colmax4, oz_pack, sum_splits)"}
+        else:
+            f64 = pk.get("fp64_tflops") or 37.0
+            gram_roof = {"bound": "tensor", "pipe": "fp64 DMMA", "achieved": g_tf, "peak": f64,
+                         "unit": "TFLOP/s", "frac": g_tf / f64 if g_tf else None,
+                         "peak_kind": "measured (cuBLAS DGEMM 8192^3)" if pk.get("fp64_tflops") else "spec",
+                         "ops_model": "4 n m^2 per Rayleigh-Ritz pair (G_A = B'LB, G_B = B'B)",
+                         "kernel": "spb::gram_dmma_t (+ sum_splits)"}
+        gram_roof.update({"launches": g_calls, "avg_launch_us": g_us / max(g_calls, 1),
+                          "live_ms_total": g_us / 1e3, "standalone": gram})
+        # the dominant of the two (by live time in this run) is the headline roofline
+        if g_us >= spmm_us:
+            roofline = dict(gram_roof, spmm=spmm_roof, csr_build=csr)
+        else:
+            roofline = dict(spmm_roof, gram=gram_roof, csr_build=csr)
+        roofline["note"] = ("headline = whichever of the Rayleigh-Ritz Gram pair and the SpMM took "
+                            "more live time in the timed steps; the other is nested; kernel_shares "
+                            "splits the step by kernel")
         quality = {"PM_vs_truth": pm}
         gf = ROOT / "tests" / "golden" / f"large_{args.config}.npz"
         if args.config == "c3" and gf.exists():
@@ -601,27 +653,7 @@ def run_ours(args):
             "dtype": "f32" if args.precision == "float32" else "f64", "data": "synthetic",
             "config": config_dict(args, spec, l, k, max_iter, tol),
             "precision": args.precision,
-            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                         "frac": (achieved / peak) if achieved else None, "traffic": traffic,
-                         "traffic_achieved": (traffic / (spmm_us * 1e-6 / max(spmm_calls, 1)) / 1e9)
-                         if (traffic and spmm_us) else None,
-                         "traffic_frac": (traffic / (spmm_us * 1e-6 / max(spmm_calls, 1)) / 1e9 / peak)
-                         if (traffic and spmm_us) else None,
-                         "traffic_note": "ncu dram__bytes_read+write of one launch (profiles/spmm_traffic.json) "
-                                         "over this run's average launch time: the DRAM bandwidth the "
-                                         "SpMM actually sustains (the gathers miss the 216 MB X block)",
-                         "kernel": "spb::spmm_vb (Laplacian SpMM)", "peak_kind": peak_kind,
-                         "launches": spmm_calls,
-                         "avg_launch_us": spmm_us / max(spmm_calls, 1),
-                         "bytes_model": "compulsory 4(n+1)+(4+esz)nnz+esz*n+2*esz*n*cols per apply",
-                         "gather_model": {"achieved": gather_achieved,
-                                          "frac": (gather_achieved / peak) if gather_achieved else None,
-                                          "bytes_model": "compulsory + esz*nnz*cols"},
-                         "gram": gram,
-                         "csr_build": csr,
-                         "note": ("roofline of the path's HBM-streaming kernel (SpMM) and of the "
-                                  "Rayleigh-Ritz Gram (DMMA); the step's time split by kernel is "
-                                  "kernel_shares (latency-bound small dense solves dominate at C1/C2)")},
+            "roofline": roofline,
             "cpu_baseline": cpu,
             "e2e": {"value": e2e_value, "unit": UNIT,
                     # arcs as int64; x0 crosses as float32 for float32 storage (_h2d.py)

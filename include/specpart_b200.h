@@ -157,8 +157,9 @@ SPB_API size_t spb_lobpcg_workspace(int dtype, int32_t n, int32_t l);
  * stats_out (host int64[16], may be NULL) receives {[0] iterations, [1] operator
  * applies, [2] Rayleigh-Ritz solves, [3] drop_p rungs, [4] rebuild rungs, [5] float32
  * orth_p re-solves, [6] 0, [7] SpMM event time (us), [8] SpMM algorithmic bytes,
- * [9] SpMM columns, [10] final scale bits hi, [11] lo, 0...}; the SpMM timing
- * entries are filled when cfg->reserved has bit 0 set. */
+ * [9] SpMM columns, [10] final scale bits hi, [11] lo, [12] Rayleigh-Ritz Gram event
+ * time (us), [13] Gram pairs, [14] their algorithmic MFLOP (4 n m^2 each), 0...}; the
+ * timing entries are filled when cfg->reserved has bit 0 set. */
 SPB_API int spb_lobpcg_solve(const spb_operator* op, int dtype, const double* x0,
                      const spb_solver_config* cfg, spb_iter_cb cb, spb_refill_cb refill,
                      spb_precond_cb precond, void* user, void* ws, size_t ws_bytes,

@@ -170,6 +170,7 @@ struct Driver {
   std::vector<cudaEvent_t> events;
   ~Driver() {
     for (cudaEvent_t e : events) cudaEventDestroy(e);
+    for (cudaEvent_t e : gevents) cudaEventDestroy(e);
   }
   std::vector<double> h_theta, h_norms;  // last residual step
   double h_scale = 0.0;
@@ -251,6 +252,15 @@ struct Driver {
     }
     stats[7] = (int64_t)(ms * 1000.0);  // microseconds
     stats[8] = (int64_t)spmm_bytes;
+    double gms = 0.0;
+    for (size_t i = 0; i < gev_used; i += 2) {
+      float t = 0.f;
+      SPB_CUDA(cudaEventElapsedTime(&t, gevents[i], gevents[i + 1]));
+      gms += t;
+    }
+    stats[12] = (int64_t)(gms * 1000.0);     // Rayleigh-Ritz Gram microseconds
+    stats[13] = (int64_t)(gev_used / 2);     // Gram pairs
+    stats[14] = (int64_t)(gram_flops / 1e6); // their algorithmic MFLOP
     return SPB_OK;
   }
 
@@ -268,7 +278,27 @@ struct Driver {
   }
 
   // [G_A | G_B] for the basis [X (l) | R (na) | P (pw)] and images.
+  // Rayleigh-Ritz Gram pair, CUDA-event timed when profiling (stats 12-14)
+  std::vector<cudaEvent_t> gevents;
+  size_t gev_used = 0;
+  double gram_flops = 0.0;
   int rr_grams(int na, int pw) {
+    if (!profile) return rr_grams_body(na, pw);
+    while (gevents.size() < gev_used + 2) {
+      cudaEvent_t e;
+      SPB_CUDA(cudaEventCreate(&e));
+      gevents.push_back(e);
+    }
+    SPB_CUDA(cudaEventRecord(gevents[gev_used], st));
+    SPB_TRY(rr_grams_body(na, pw));
+    SPB_CUDA(cudaEventRecord(gevents[gev_used + 1], st));
+    gev_used += 2;
+    const double m = (double)(w.l + na + pw);
+    gram_flops += 4.0 * (double)w.n * m * m;  // G_A = B'LB and G_B = B'B
+    return SPB_OK;
+  }
+
+  int rr_grams_body(int na, int pw) {
     if (w.use_oz) {
       // [B'B | B'LB] over the padded basis from one packing of B and of LB, then
       // gather the m x m blocks (as the tcgen05 path below)

@@ -374,7 +374,9 @@ def lobpcg_solve(operator, x0, config: SolverConfig, precond=None, n_converge: i
         state.solve_stats = dict(zip(("iterations", "spmm_calls", "rr_calls", "drop_p",
                                       "rebuild"), [int(s) for s in stats[:5]]))
         state.solve_stats.update(orth_p=int(stats[5]), spmm_us=int(stats[7]), spmm_bytes=int(stats[8]),
-                                 spmm_cols=int(stats[9]))
+                                 spmm_cols=int(stats[9]),
+                                 gram_us=int(stats[12]), gram_calls=int(stats[13]),
+                                 gram_mflop=int(stats[14]))
         state.precision = precision
     del ws
     if status == N.OK:

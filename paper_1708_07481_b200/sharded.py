@@ -282,7 +282,9 @@ def lobpcg_solve_sharded(op: RowShardedLaplacian, x0, config: SolverConfig, n_co
         state.solve_stats = dict(zip(("iterations", "spmm_calls", "rr_calls", "drop_p",
                                       "rebuild", "orth_p"), [int(x) for x in stats[:6]]))
         state.solve_stats.update(spmm_us=int(stats[7]), spmm_bytes=int(stats[8]),
-                                 spmm_cols=int(stats[9]))
+                                 spmm_cols=int(stats[9]),
+                                 gram_us=int(stats[12]), gram_calls=int(stats[13]),
+                                 gram_mflop=int(stats[14]))
         state.row_range = (op.row_begin, op.row_end)
     if status == N.OK:
         return state
