@@ -617,15 +617,18 @@ def run_ours(args):
                          "peak_kind": "measured (torch._int_mm 8192^3, profiles/r02/peaks_tensor.json)"
                          if pk.get("int8_tops") else "spec",
                          "fp64_equivalent_tflops": g_tf,
-                         "ops_model": "15 int8 digit-pair GEMMs x 4 n m^2 (G_A = B'LB, G_B = B'B) per pair, "
-                                      "time incl. column maxima, digit packing, split-K reduction",
+                         "ops_model": "15 int8 digit-pair GEMMs x 4 n m^2 (SURVEY 8(d): G_A = B'LB and "
+                                      "G_B = B'B) per pair; the kernel computes only G_B's upper tiles, "
+                                      "so it issues ~25 % fewer int8 ops than counted; time incl. column "
+                                      "maxima, digit packing, split-K reduction",
                          "kernel": "spb::gram_oz_kernel (+ oz_colmax4, oz_pack, sum_splits)"}
         else:
             f64 = pk.get("fp64_tflops") or 37.0
             gram_roof = {"bound": "tensor", "pipe": "fp64 DMMA", "achieved": g_tf, "peak": f64,
                          "unit": "TFLOP/s", "frac": g_tf / f64 if g_tf else None,
                          "peak_kind": "measured (cuBLAS DGEMM 8192^3)" if pk.get("fp64_tflops") else "spec",
-                         "ops_model": "4 n m^2 per Rayleigh-Ritz pair (G_A = B'LB, G_B = B'B)",
+                         "ops_model": "4 n m^2 per Rayleigh-Ritz pair (SURVEY 8(d): G_A = B'LB, G_B = B'B; "
+                                      "the kernel computes G_B's upper blocks only)",
                          "kernel": "spb::gram_dmma_t (+ sum_splits)"}
         gram_roof.update({"launches": g_calls, "avg_launch_us": g_us / max(g_calls, 1),
                           "live_ms_total": g_us / 1e3, "standalone": gram})
