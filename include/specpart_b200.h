@@ -93,6 +93,29 @@ SPB_API int spb_laplacian_spmm(int dtype, int32_t row_begin, int32_t row_end, co
                        const int32_t* col, const void* val, const void* deg, const void* x,
                        int64_t ldx, int32_t ncols, void* y, int64_t ldy, void* stream);
 
+/* ---------------- (b') locality ordering for the SpMM -----------------------
+ * Not a reference function: an internal relabelling of the solve (the
+ * reference's laplacian_apply, graph.py:253-278, keeps the input order). The
+ * vertices are renumbered so that a block-model graph's blocks become
+ * contiguous runs (random-walk-smoothed seeded random columns, 16-bit sign
+ * keys, stable radix sort): perm[new] = old. val/deg are dtype values of W.
+ * spb_csr_permute writes the CSR of P W P' (row i = old row perm[i], its
+ * entries in their original order with renumbered columns, so every SpMM row
+ * sum is bit-identical), the permuted degrees and inv[old] = new.
+ * spb_permute_rows: scatter == 0: dst[i] = src[idx[i]]; else dst[idx[i]] = src[i]. */
+SPB_API size_t spb_vertex_order_workspace(int32_t n);
+SPB_API int spb_vertex_order(int dtype, int32_t n, const int32_t* row_ptr, const int32_t* col,
+                             const void* val, const void* deg, int32_t steps, uint64_t seed,
+                             void* ws, size_t ws_bytes, int32_t* perm, void* stream);
+SPB_API size_t spb_csr_permute_workspace(int32_t n);
+SPB_API int spb_csr_permute(int dtype, int32_t n, const int32_t* row_ptr, const int32_t* col,
+                            const void* val, const void* deg, const int32_t* perm, void* ws,
+                            size_t ws_bytes, int32_t* inv, int32_t* out_row_ptr, int32_t* out_col,
+                            void* out_val, void* out_deg, void* stream);
+SPB_API int spb_permute_rows(int src_dtype, const void* src, int64_t lds, int dst_dtype, void* dst,
+                             int64_t ldd, int64_t rows, int32_t cols, const int32_t* idx,
+                             int scatter, void* stream);
+
 /* ---------------- (c) tall-skinny Gram ---------------------------------------
  * out[p x q] (float64, row stride ldo) = U' V for vertex-major blocks U (n x p),
  * V (n x q): the Gram products of lobpcg.py:228, :366, :418. mode 0: float64
@@ -124,6 +147,10 @@ typedef struct {
   double scale_hint;     /* max degree (graph.py:314) / max row abs-sum (lobpcg.py:143) */
   spb_apply_cb apply;    /* HOST: the operator's apply                             */
   void* apply_user;      /* HOST: passed back to apply                             */
+  const int32_t* perm;   /* LAPLACIAN, optional (NULL: identity): the CSR and deg are
+                            in the spb_vertex_order numbering, perm[new] = old; x0,
+                            refills, preconditioner blocks and vectors_out stay in
+                            the caller's order (single-GPU solves only)             */
 } spb_operator;
 
 /* SolverConfig (lobpcg.py:38-81) plus the solve arguments of lobpcg_solve
@@ -220,7 +247,8 @@ SPB_API int spb_lobpcg_solve_sharded(const spb_operator* op, const spb_shard* sh
                                      size_t ws_bytes, double* theta_out, double* norms_out,
                                      uint8_t* converged_out, int64_t* stats_out, void* stream);
 
-/* Device pointer/ld of the solver's final X block inside ``ws`` (dtype). */
+/* Device pointer/ld of the solver's final X block inside ``ws`` (dtype); rows in
+ * the operator's numbering (map them back through op->perm when it was set). */
 SPB_API int spb_lobpcg_result_block(int dtype, int32_t n, int32_t l, void* ws, void** x_out,
                             int64_t* ld_out);
 

@@ -35,7 +35,7 @@ APPLY_CB = C.CFUNCTYPE(C.c_int, vp, i64, i32, C.POINTER(f64), C.POINTER(f64))
 class Operator(C.Structure):
     _fields_ = [("kind", C.c_int), ("n", i32), ("row_ptr", vp), ("col", vp), ("val", vp),
                 ("deg", vp), ("dense", vp), ("scale_hint", f64), ("apply", APPLY_CB),
-                ("apply_user", vp)]
+                ("apply_user", vp), ("perm", vp)]
 
 
 class Shard(C.Structure):
@@ -66,6 +66,11 @@ _SIGS = {
     "spb_copy_block": (C.c_int, [C.c_int, vp, i64, C.c_int, vp, i64, i64, i32, vp]),
     "spb_max_f64": (C.c_int, [vp, i64, C.POINTER(f64), vp]),
     "spb_laplacian_spmm": (C.c_int, [C.c_int, i32, i32, vp, vp, vp, vp, vp, i64, i32, vp, i64, vp]),
+    "spb_vertex_order_workspace": (sz, [i32]),
+    "spb_vertex_order": (C.c_int, [C.c_int, i32, vp, vp, vp, vp, i32, C.c_uint64, vp, sz, vp, vp]),
+    "spb_csr_permute_workspace": (sz, [i32]),
+    "spb_csr_permute": (C.c_int, [C.c_int, i32, vp, vp, vp, vp, vp, vp, sz, vp, vp, vp, vp, vp, vp]),
+    "spb_permute_rows": (C.c_int, [C.c_int, vp, i64, C.c_int, vp, i64, i64, i32, vp, C.c_int, vp]),
     "spb_gram_workspace": (sz, [i32, i32, i64]),
     "spb_gram": (C.c_int, [C.c_int, C.c_int, vp, i64, i32, vp, i64, i32, i64, vp, i64, vp, sz, vp]),
     "spb_block_update_workspace": (sz, [i32, i32]),

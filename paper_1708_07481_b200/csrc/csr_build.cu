@@ -16,15 +16,12 @@
 //   6. row_ptr from the row of each output entry; degrees per row as
 //      (sum_j A_ij in column order) + (sum_j A_ji in column order)
 #include "common.cuh"
+#include "radix.cuh"
 #include "scan.cuh"
 
 namespace spb {
 namespace {
 
-constexpr int kSortThreads = 256;
-constexpr int kSortRounds = 16;
-constexpr int kSortTile = kSortThreads * kSortRounds;  // 4096 items per tile
-constexpr int kRadix = 256;
 
 struct BuildFlags {
   int bad_endpoint;
@@ -71,60 +68,6 @@ __global__ void emit_entries(const int64_t* __restrict__ src, const int64_t* __r
       keys[e] = loop ? sentinel : ((s << b) | d);
       pay[e] = (uint32_t)(2 * e);
     }
-  }
-}
-
-__global__ void radix_hist(const uint64_t* __restrict__ keys, int64_t count, int shift,
-                           int64_t ntiles, int* __restrict__ counts) {
-  __shared__ int h[kRadix];
-  h[threadIdx.x] = 0;
-  __syncthreads();
-  int64_t base = (int64_t)blockIdx.x * kSortTile;
-#pragma unroll 4
-  for (int r = 0; r < kSortRounds; ++r) {
-    int64_t i = base + r * kSortThreads + threadIdx.x;
-    if (i < count) atomicAdd(&h[(keys[i] >> shift) & 0xff], 1);
-  }
-  __syncthreads();
-  counts[(int64_t)threadIdx.x * ntiles + blockIdx.x] = h[threadIdx.x];
-}
-
-// Stable scatter: items of a tile are ranked in index order (round, warp, lane).
-__global__ void radix_scatter(const uint64_t* __restrict__ kin, const uint32_t* __restrict__ pin,
-                              int64_t count, int shift, int64_t ntiles,
-                              const int* __restrict__ offsets, uint64_t* __restrict__ kout,
-                              uint32_t* __restrict__ pout) {
-  __shared__ int running[kRadix];
-  __shared__ int wcnt[kSortThreads / 32][kRadix];
-  const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
-  running[t] = offsets[(int64_t)t * ntiles + blockIdx.x];
-  int64_t base = (int64_t)blockIdx.x * kSortTile;
-  const unsigned lt = (1u << lane) - 1u;
-  for (int r = 0; r < kSortRounds; ++r) {
-#pragma unroll
-    for (int w = 0; w < kSortThreads / 32; ++w) wcnt[w][t] = 0;
-    __syncthreads();
-    int64_t i = base + r * kSortThreads + t;
-    bool valid = i < count;
-    uint64_t k = valid ? kin[i] : 0;
-    uint32_t p = valid ? pin[i] : 0;
-    int d = valid ? (int)((k >> shift) & 0xff) : kRadix;  // kRadix = none
-    unsigned peers = __match_any_sync(0xffffffffu, d);
-    int lrank = __popc(peers & lt);
-    if (valid && lrank == 0) wcnt[warp][d] = __popc(peers);
-    __syncthreads();
-    if (valid) {
-      int pos = running[d] + lrank;
-      for (int w = 0; w < warp; ++w) pos += wcnt[w][d];
-      kout[pos] = k;
-      pout[pos] = p;
-    }
-    __syncthreads();
-    int add = 0;
-#pragma unroll
-    for (int w = 0; w < kSortThreads / 32; ++w) add += wcnt[w][t];
-    running[t] += add;
-    __syncthreads();
   }
 }
 
@@ -643,19 +586,9 @@ int sort_reduce_scatter(BuildLayout& L, const double* w, int64_t count, int64_t 
                         bool symmetrized, int32_t n, int32_t* row_ptr, int32_t* col, double* val,
                         double* deg, int64_t* nnz_out, cudaStream_t st) {
   // stable LSD radix sort over 2b key bits
-  const int64_t ntiles = ceil_div(count, kSortTile);
   uint64_t *kin = L.ka, *kout = L.kb;
   uint32_t *pin = L.pa, *pout = L.pb;
-  for (int shift = 0; count > 0 && shift < 2 * b; shift += 8) {
-    radix_hist<<<ntiles, kSortThreads, 0, st>>>(kin, count, shift, ntiles, L.counts);
-    SPB_TRY(exclusive_scan_i32(L.counts, L.counts, (int64_t)kRadix * ntiles, L.scan_tmp,
-                               nullptr, st));
-    radix_scatter<<<ntiles, kSortThreads, 0, st>>>(kin, pin, count, shift, ntiles, L.counts,
-                                                   kout, pout);
-    SPB_LAUNCH_CHECK();
-    std::swap(kin, kout);
-    std::swap(pin, pout);
-  }
+  SPB_TRY(radix_sort_pairs(&kin, &pin, &kout, &pout, count, 2 * b, L.counts, L.scan_tmp, st));
   int32_t* dev_total = L.dev_ints;
   int64_t nnz = 0;
   if (valid > 0) {

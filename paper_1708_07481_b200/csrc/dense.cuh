@@ -82,6 +82,9 @@ int dense_apply(const double* Adense, int64_t n, const void* X, int64_t ldx, int
                 int64_t ldy, int dtype, double* scratch, cudaStream_t st);
 int copy_block(int sdt, const void* s, int64_t lds, int ddt, void* d, int64_t ldd, int64_t rows,
                int32_t cols, cudaStream_t st);
+// scatter == 0: d[i] = s[idx[i]]; else d[idx[i]] = s[i] (rows, with dtype conversion)
+int permute_rows(int sdt, const void* s, int64_t lds, int ddt, void* d, int64_t ldd, int64_t rows,
+                 int32_t cols, const int32_t* idx, int scatter, cudaStream_t st);
 // Rows [r0, r1) of W; the row's own X entry is x[(xoff + row) * ldx]; x_rows =
 // rows of x the gathers can touch (L2 panel sizing; 0 -> r1).
 int laplacian_spmm(int dtype, int32_t r0, int32_t r1, const int32_t* rp, const int32_t* ci,

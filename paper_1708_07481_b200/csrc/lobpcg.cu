@@ -176,6 +176,19 @@ struct Driver {
   double h_scale = 0.0;
   int iterations = 0;
 
+  // op->perm (spb_vertex_order): the solve runs in the operator's numbering; blocks
+  // that cross the boundary (x0, refills, preconditioner, results) are mapped
+  const int32_t* perm() const { return op ? op->perm : nullptr; }
+  // dst (caller's order) <- src (solver's order), or the reverse
+  int to_caller(int sdt, const void* s, int64_t lds, int ddt, void* d, int64_t ldd, int cols) {
+    if (!perm()) return copy_block(sdt, s, lds, ddt, d, ldd, w.n, cols, st);
+    return permute_rows(sdt, s, lds, ddt, d, ldd, w.n, cols, perm(), 1, st);
+  }
+  int from_caller(int sdt, const void* s, int64_t lds, int ddt, void* d, int64_t ldd, int cols) {
+    if (!perm()) return copy_block(sdt, s, lds, ddt, d, ldd, w.n, cols, st);
+    return permute_rows(sdt, s, lds, ddt, d, ldd, w.n, cols, perm(), 0, st);
+  }
+
   int apply(const void* src, int cols, void* dst) {
     stats[1]++;
     if (op->kind == SPB_OP_HOST) return host_apply(src, cols, dst);
@@ -489,7 +502,7 @@ struct Driver {
     SPB_CUDA(cudaMemcpyAsync(d, h.data() + r0 * cols, sizeof(double) * (size_t)w.n * cols,
                              cudaMemcpyHostToDevice, st));
     char* dst = (char*)B + (size_t)c0 * w.esz;
-    int s = copy_block(SPB_F64, d, cols, w.dtype, dst, w.ld, w.n, cols, st);
+    int s = from_caller(SPB_F64, d, cols, w.dtype, dst, w.ld, cols);
     cudaFreeAsync(d, st);
     SPB_CUDA(cudaStreamSynchronize(st));
     return s;
@@ -499,7 +512,7 @@ struct Driver {
     std::vector<double> h((size_t)w.n * na);
     double* d = nullptr;
     SPB_CUDA(cudaMallocAsync((void**)&d, sizeof(double) * h.size() + 8, st));
-    SPB_TRY(copy_block(w.dtype, w.R, w.ld, SPB_F64, d, na, w.n, na, st));
+    SPB_TRY(to_caller(w.dtype, w.R, w.ld, SPB_F64, d, na, na));
     SPB_CUDA(cudaMemcpyAsync(h.data(), d, sizeof(double) * h.size(), cudaMemcpyDeviceToHost, st));
     SPB_CUDA(cudaStreamSynchronize(st));
     if (precond(user, w.n, na, h.data()) != 0) {
@@ -508,7 +521,7 @@ struct Driver {
       return SPB_ERR_CALLBACK;
     }
     SPB_CUDA(cudaMemcpyAsync(d, h.data(), sizeof(double) * h.size(), cudaMemcpyHostToDevice, st));
-    SPB_TRY(copy_block(SPB_F64, d, na, w.dtype, w.R, w.ld, w.n, na, st));
+    SPB_TRY(from_caller(SPB_F64, d, na, w.dtype, w.R, w.ld, na));
     cudaFreeAsync(d, st);
     SPB_CUDA(cudaStreamSynchronize(st));
     return SPB_OK;
@@ -647,7 +660,7 @@ struct Driver {
     // zero padding columns once, load x0 (float64 n x l) into X
     const size_t blk = (size_t)n * w.ld * w.esz;
     for (void* b : {w.B, w.LB}) SPB_CUDA(cudaMemsetAsync(b, 0, blk, st));
-    SPB_TRY(copy_block(SPB_F64, x0, l, w.dtype, w.X, w.ld, n, l, st));
+    SPB_TRY(from_caller(SPB_F64, x0, l, w.dtype, w.X, w.ld, l));
     if (cfg->deflate_ones) SPB_TRY(deflate(w.X, l));
     SPB_TRY(orthonormalize(w.X, l));
     SPB_TRY(apply(w.X, l, w.LX));
@@ -848,6 +861,10 @@ static int solve_impl(const spb_operator* op, const spb_shard* sh, int dtype, co
     set_error("row-sharded solves take a Laplacian operator and no preconditioner");
     return SPB_ERR_CONTRACT;
   }
+  if (op->perm && (sh || op->kind != SPB_OP_LAPLACIAN)) {
+    set_error("a vertex order (op->perm) applies to single-GPU Laplacian solves only");
+    return SPB_ERR_CONTRACT;
+  }
   if (l < 1 || l > n_glob) {
     set_error("block_size %d exceeds operator dimension %d", l, n);
     return SPB_ERR_DOMAIN;
@@ -896,7 +913,7 @@ static int solve_impl(const spb_operator* op, const spb_shard* sh, int dtype, co
       converged_out[j] = norms_out[j] < cfg->tol * d.h_scale;
     }
     if (vectors_out) {
-      int c = copy_block(dtype, d.w.X, d.w.ld, SPB_F64, vectors_out, l, n, l, d.st);
+      int c = d.to_caller(dtype, d.w.X, d.w.ld, SPB_F64, vectors_out, l, l);
       if (s == SPB_OK) s = c;
       cudaError_t e = cudaStreamSynchronize(d.st);
       if (s == SPB_OK && e != cudaSuccess) {

@@ -3,6 +3,7 @@
 #include "common.cuh"
 
 namespace spb {
+namespace {  // internal linkage: every TU that includes this gets its own copy
 
 constexpr int kScanThreads = 1024;
 constexpr int kScanItems = 4;
@@ -100,4 +101,5 @@ inline int exclusive_scan_i32(const int* in, int* out, int64_t n, int* tmp, int*
   return SPB_OK;
 }
 
+}  // namespace
 }  // namespace spb

@@ -81,6 +81,59 @@ class _Csr:
         return self._cast[key]
 
 
+# Locality ordering for the SpMM (csrc/reorder.cu): used when the gathered X block
+# (n x block columns) is too large to stay L2-resident (126 MB L2 on a B200).
+ORDER_MIN_BYTES = 64 << 20
+ORDER_STEPS = 5
+ORDER_SEED = 0x5EED
+
+
+class _VertexOrder:
+    """perm[new] = old from spb_vertex_order on W, and W renumbered by it per dtype
+    (spb_csr_permute: every row keeps its entry order, so SpMM rows are bit-identical)."""
+
+    def __init__(self, c: _Csr, n: int):
+        L = N.lib()
+        dev = c.row_ptr.device
+        self.n = n
+        self.perm = torch.empty(max(n, 1), dtype=torch.int32, device=dev)
+        wsb = L.spb_vertex_order_workspace(n)
+        ws = torch.empty(wsb, dtype=torch.uint8, device=dev)
+        N.check(L.spb_vertex_order(N.F64, n, N.ptr(c.row_ptr), N.ptr(c.col), N.ptr(c.val),
+                                   N.ptr(c.deg), ORDER_STEPS, ORDER_SEED, N.ptr(ws), wsb,
+                                   N.ptr(self.perm), N.stream()))
+        self._csr = {}
+
+    def csr(self, c: _Csr, dtype: str):
+        """(row_ptr, col, values) of P W P' in the solve dtype."""
+        if dtype not in self._csr:
+            L = N.lib()
+            dev = c.row_ptr.device
+            n = self.n
+            rp = torch.empty(n + 1, dtype=torch.int32, device=dev)
+            col = torch.empty(max(c.nnz, 1), dtype=torch.int32, device=dev)
+            tdt = DTYPES[dtype][1]
+            val = torch.empty(max(c.nnz, 1), dtype=tdt, device=dev)
+            inv = torch.empty(max(n, 1), dtype=torch.int32, device=dev)
+            wsb = L.spb_csr_permute_workspace(n)
+            ws = torch.empty(wsb, dtype=torch.uint8, device=dev)
+            N.check(L.spb_csr_permute(DTYPES[dtype][0], n, N.ptr(c.row_ptr), N.ptr(c.col),
+                                      N.ptr(c.values(dtype)), None, N.ptr(self.perm), N.ptr(ws),
+                                      wsb, N.ptr(inv), N.ptr(rp), N.ptr(col), N.ptr(val), None,
+                                      N.stream()))
+            self._csr[dtype] = (rp, col, val)
+        return self._csr[dtype]
+
+    def gather(self, v: torch.Tensor) -> torch.Tensor:
+        """out[i] = v[perm[i]] for a device vector of the solve dtype."""
+        out = torch.empty_like(v)
+        code = N.F32 if v.dtype == torch.float32 else N.F64
+        if self.n:
+            N.check(N.lib().spb_permute_rows(code, N.ptr(v), 1, code, N.ptr(out), 1, self.n, 1,
+                                             N.ptr(self.perm), 0, N.stream()))
+        return out
+
+
 def _build_csr(src, dst, w, m, n, mode) -> _Csr:
     dev = _device()
     L = N.lib()
@@ -129,6 +182,10 @@ class SparseGraph:
 
     def device_degrees(self):
         return self._w_csr.deg[: self.n_vertices]
+
+    @cached_property
+    def _vertex_order(self) -> _VertexOrder:
+        return _VertexOrder(self._w_csr, self.n_vertices)
 
     # ---- reference-shaped host views (graph.py:35-103) ---------------------
     @cached_property
@@ -447,9 +504,13 @@ class LaplacianOperator:
     The eigensolver uses the device CSR directly (no host round trip).
     """
 
-    def __init__(self, g: SparseGraph, d=None):
+    def __init__(self, g: SparseGraph, d=None, *, vertex_order="auto"):
+        if vertex_order not in ("auto", True, False):
+            raise ContractError("vertex_order must be 'auto', True or False")
         self.graph = g
         self.n = g.n_vertices
+        self.vertex_order = vertex_order
+        self._deg_perm = {}
         if d is None:
             self._deg64 = g.device_degrees() if self.n else torch.zeros(1, dtype=torch.float64, device=_device())
             self._own_deg = False
@@ -478,18 +539,40 @@ class LaplacianOperator:
             self._deg_cast[dtype] = out
         return self._deg_cast[dtype]
 
-    def native(self, dtype: str) -> N.Operator:
-        row_ptr, col, _, _ = self.graph.device_csr()
+    def uses_vertex_order(self, cols: int, dtype: str) -> bool:
+        """Whether a solve with ``cols`` block columns runs in the locality order:
+        'auto' when the gathered X block (n x cols) would not stay L2-resident."""
+        if self.vertex_order == "auto":
+            esz = 4 if dtype == "float32" else 8
+            return self.n * cols * esz >= ORDER_MIN_BYTES
+        return bool(self.vertex_order) and self.n > 0
+
+    def native(self, dtype: str, cols: int | None = None) -> N.Operator:
+        """Operator handle for the device solver; with ``cols`` (the block width)
+        the CSR may be the locality-ordered one (op.perm set, see reorder.cu)."""
         op = N.Operator()
         op.kind = N.OP_LAPLACIAN
         op.n = self.n
-        op.row_ptr = N.ptr(row_ptr)
-        op.col = N.ptr(col)
-        op.val = N.ptr(self.graph._w_csr.values(dtype))
-        op.deg = N.ptr(self.device_degrees(dtype))
         op.dense = None
         op.scale_hint = self.scale_hint
-        op._keep = (row_ptr, col)
+        if cols is not None and self.uses_vertex_order(cols, dtype):
+            order = self.graph._vertex_order
+            row_ptr, col, val = order.csr(self.graph._w_csr, dtype)
+            if dtype not in self._deg_perm:
+                self._deg_perm[dtype] = order.gather(self.device_degrees(dtype)[: max(self.n, 1)])
+            deg = self._deg_perm[dtype]
+            op.perm = N.ptr(order.perm)
+            op._keep = (row_ptr, col, val, deg, order.perm)
+        else:
+            row_ptr, col, _, _ = self.graph.device_csr()
+            val = self.graph._w_csr.values(dtype)
+            deg = self.device_degrees(dtype)
+            op.perm = None
+            op._keep = (row_ptr, col)
+        op.row_ptr = N.ptr(row_ptr)
+        op.col = N.ptr(col)
+        op.val = N.ptr(val)
+        op.deg = N.ptr(deg)
         return op
 
     def apply(self, x, out=None):

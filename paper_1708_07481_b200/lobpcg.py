@@ -288,11 +288,11 @@ class _HostOperator:
         return op
 
 
-def _native_operator(operator, dtype: str):
-    if isinstance(operator, (LaplacianOperator, DenseOperator)):
-        if isinstance(operator, DenseOperator) and dtype != "float64":
-            dtype = "float64"
-        return operator.native(dtype), dtype, None
+def _native_operator(operator, dtype: str, cols: int):
+    if isinstance(operator, LaplacianOperator):
+        return operator.native(dtype, cols), dtype, None
+    if isinstance(operator, DenseOperator):
+        return operator.native("float64"), "float64", None
     if all(hasattr(operator, a) for a in ("n", "scale_hint", "apply")):
         host = _HostOperator(operator)
         return host.native(), dtype, host
@@ -339,7 +339,7 @@ def lobpcg_solve(operator, x0, config: SolverConfig, precond=None, n_converge: i
     nc = l if n_converge is None else int(n_converge)
     if not 1 <= nc <= l:
         raise DomainError("n_converge must be in [1, block_size]")
-    op, precision, host_op = _native_operator(operator, precision)
+    op, precision, host_op = _native_operator(operator, precision, l)
     code, tdt = DTYPES[precision]
     L = N.lib()
     x0_d = _x0_device(x0, n, l, precision)
@@ -368,7 +368,12 @@ def lobpcg_solve(operator, x0, config: SolverConfig, precond=None, n_converge: i
         ldx = C.c_int64()
         N.check(L.spb_lobpcg_result_block(code, n, l, N.ptr(ws), C.byref(xp), C.byref(ldx)))
         vec = torch.empty((n, l), dtype=tdt, device=ws.device)
-        N.check(L.spb_copy_block(code, xp.value, ldx.value, code, N.ptr(vec), l, n, l, N.stream()))
+        if op.perm:  # the solve ran in the operator's locality order: back to the caller's rows
+            N.check(L.spb_permute_rows(code, xp.value, ldx.value, code, N.ptr(vec), l, n, l,
+                                       op.perm, 1, N.stream()))
+        else:
+            N.check(L.spb_copy_block(code, xp.value, ldx.value, code, N.ptr(vec), l, n, l,
+                                     N.stream()))
         state = EigenState(np.array(theta[:]), vec, np.array(norms[:]), int(stats[0]),
                            np.array(conv[:], dtype=bool), work_blocks=6)
         state.solve_stats = dict(zip(("iterations", "spmm_calls", "rr_calls", "drop_p",

@@ -1,0 +1,159 @@
+"""SpMM locality ordering (csrc/reorder.cu): a pure relabelling of the solve.
+
+* spb_vertex_order returns a permutation, deterministically, that groups the
+  planted blocks of a DC-SBM graph;
+* the renumbered CSR gives SpMM rows bit-identical to the original ones;
+* solves in the locality order match solves in the caller's order (the
+  reference's, graph.py:253-278) -- iteration counts, Ritz values, vectors and
+  labels -- including the preconditioner and refill callbacks, which always see
+  the caller's row order.
+"""
+
+import numpy as np
+import pytest
+
+from tests.helpers import config_input
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def spb():
+    import paper_1708_07481_b200 as spb
+
+    return spb
+
+
+@pytest.fixture(scope="module")
+def c2(spb):
+    spec, edges, truth = config_input("c2")
+    return spec, spb.from_edges(edges, spec.n), truth
+
+
+def _order(spb, g):
+    from paper_1708_07481_b200.graph import _VertexOrder
+
+    return _VertexOrder(g._w_csr, g.n_vertices)
+
+
+def test_order_is_deterministic_permutation(spb, c2):
+    spec, g, _ = c2
+    p1 = _order(spb, g).perm.cpu().numpy()
+    p2 = _order(spb, g).perm.cpu().numpy()
+    assert np.array_equal(p1, p2)
+    assert np.array_equal(np.sort(p1), np.arange(spec.n))
+
+
+def test_order_groups_planted_blocks(spb):
+    # C3-like mixing (5:1 within : between) at 50K vertices
+    from paper_1708_07481_b200.dcsbm import DcsbmSpec, generate_dcsbm
+
+    spec = DcsbmSpec(n=50_000, blocks=40, arcs=1_000_000, alpha=3.0, ratio=5.0, seed=2)
+    edges, truth = generate_dcsbm(spec)
+    g = spb.from_edges(edges, spec.n)
+    perm = _order(spb, g).perm.cpu().numpy()
+    same_next = np.mean(truth[perm[1:]] == truth[perm[:-1]])
+    assert same_next > 0.9, same_next  # natural order: ~1/40
+    # edge span in the new numbering is a fraction of the natural one
+    inv = np.empty_like(perm)
+    inv[perm] = np.arange(spec.n)
+    span_new = np.median(np.abs(inv[edges[:, 0]] - inv[edges[:, 1]]))
+    span_old = np.median(np.abs(edges[:, 0] - edges[:, 1]))
+    assert span_new < 0.2 * span_old, (span_new, span_old)
+
+
+@pytest.mark.parametrize("dtype", ["float32", "float64"])
+def test_permuted_spmm_rows_bit_identical(spb, c2, dtype):
+    import torch
+
+    from paper_1708_07481_b200 import _native as N
+    from paper_1708_07481_b200.graph import DTYPES
+
+    spec, g, _ = c2
+    n = spec.n
+    code, tdt = DTYPES[dtype]
+    op = spb.LaplacianOperator(g, vertex_order=True)
+    nat = spb.LaplacianOperator(g, vertex_order=False)
+    h_o = op.native(dtype, 49)
+    h_n = nat.native(dtype, 49)
+    assert h_o.perm and not h_n.perm
+    perm = op.graph._vertex_order.perm.long()
+    x = torch.randn((n, 52), dtype=tdt, device="cuda")
+    xp = x[perm].contiguous()
+    y = torch.empty_like(x)
+    yp = torch.empty_like(x)
+    L = N.lib()
+    N.check(L.spb_laplacian_spmm(code, 0, n, h_n.row_ptr, h_n.col, h_n.val, h_n.deg, N.ptr(x), 52,
+                                 49, N.ptr(y), 52, N.stream()))
+    N.check(L.spb_laplacian_spmm(code, 0, n, h_o.row_ptr, h_o.col, h_o.val, h_o.deg, N.ptr(xp), 52,
+                                 49, N.ptr(yp), 52, N.stream()))
+    assert torch.equal(yp[:, :49], y[perm][:, :49])
+
+
+def test_permute_rows_roundtrip(spb, c2):
+    import torch
+
+    from paper_1708_07481_b200 import _native as N
+
+    spec, g, _ = c2
+    perm = _order(spb, g).perm
+    x = torch.randn((spec.n, 7), dtype=torch.float64, device="cuda")
+    fwd = torch.empty((spec.n, 8), dtype=torch.float32, device="cuda")
+    back = torch.empty((spec.n, 7), dtype=torch.float64, device="cuda")
+    L = N.lib()
+    N.check(L.spb_permute_rows(N.F64, N.ptr(x), 7, N.F32, N.ptr(fwd), 8, spec.n, 7, N.ptr(perm), 0,
+                               N.stream()))
+    assert torch.equal(fwd[:, :7], x[perm.long()].float())
+    N.check(L.spb_permute_rows(N.F32, N.ptr(fwd), 8, N.F64, N.ptr(back), 7, spec.n, 7, N.ptr(perm), 1,
+                               N.stream()))
+    assert torch.equal(back, x.float().double())
+
+
+@pytest.mark.parametrize("precision", ["float64", "float32"])
+def test_solve_in_order_matches_caller_order(spb, precision):
+    spec, edges, truth = config_input("c1")
+    g = spb.from_edges(edges, spec.n)
+    l = spb.block_size_for(spec.blocks)
+    x0 = np.random.default_rng(0).standard_normal((spec.n, l))
+    cfg = spb.SolverConfig(block_size=l, tol=1e-3, max_iter=20, seed=0)
+    runs = {}
+    for vo in (False, True):
+        part, st, _ = spb.partition_static(g, cfg, k_expected=spec.blocks, fix_k=True, x0=x0,
+                                           precision=precision, vertex_order=vo)
+        runs[vo] = (part, st)
+    (p0, s0), (p1, s1) = runs[False], runs[True]
+    assert s0.iterations == s1.iterations
+    tol = 1e-10 if precision == "float64" else 1e-5
+    assert np.allclose(s1.eigenvalues, s0.eigenvalues, rtol=tol, atol=tol * s0.eigenvalues.max())
+    v0, v1 = s0.vectors, s1.vectors
+    assert np.abs(np.abs(np.sum(v0 * v1, axis=0)) - 1.0).max() < (1e-8 if precision == "float64" else 1e-3)
+    assert np.mean(p0.labels == p1.labels) > 0.999
+
+
+def test_callbacks_see_caller_order(spb):
+    """Preconditioner blocks and Gaussian refills cross in the caller's row order."""
+    spec, edges, _ = config_input("c1")
+    g = spb.from_edges(edges, spec.n)
+    d = spb.degrees(g)
+    l = 8
+    x0 = np.random.default_rng(3).standard_normal((spec.n, l))
+    x0[:, 3] = x0[:, 1]  # rank-deficient start: the refill callback runs
+    cfg = spb.SolverConfig(block_size=l, tol=1e-6, max_iter=30, seed=5)
+    seen = []
+
+    def precond(r):
+        seen.append(r[:4, 0].copy())
+        return r / d[:, None]
+
+    out = {}
+    for vo in (False, True):
+        seen.clear()
+        st = spb.lobpcg_solve(spb.LaplacianOperator(g, vertex_order=vo), x0, cfg, precond=precond,
+                              precision="float64")
+        out[vo] = (st, [s.copy() for s in seen])
+    (s0, c0), (s1, c1) = out[False], out[True]
+    assert s0.iterations == s1.iterations
+    assert np.allclose(s0.eigenvalues, s1.eigenvalues, rtol=1e-9, atol=1e-9)
+    assert len(c0) == len(c1)
+    for a, b in zip(c0[:3], c1[:3]):  # Ritz vector signs are arbitrary (either order)
+        assert np.allclose(a, b, rtol=1e-8, atol=1e-12) or np.allclose(a, -b, rtol=1e-8, atol=1e-12)
