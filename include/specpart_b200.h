@@ -291,6 +291,17 @@ SPB_API size_t spb_assign_workspace(int32_t n, int32_t k);
 SPB_API int spb_assign_qrcp(int dtype, const void* x, int64_t ldx, int32_t n, int32_t k, void* ws,
                     size_t ws_bytes, int32_t* labels_out, int32_t* pivots_out,
                     double* info_out, void* stream);
+/* Row-sharded assign_clusters_qrcp: this rank holds rows
+ * [shard->row_begin, +n_local) of the embedding. The k pivot steps are global
+ * argmax steps (two all-gathers of one record per rank per step over
+ * shard->comm); the pivots (global row ids, identical on every rank and equal to
+ * the single-GPU ones), the seed block and S^-1 are replicated, the labels of the
+ * local rows are written to labels_out (int32[n_local]); info_out as above, global. */
+SPB_API size_t spb_assign_workspace_sharded(int32_t n_local, int32_t k, int32_t nranks);
+SPB_API int spb_assign_qrcp_sharded(int dtype, const void* x, int64_t ldx, int32_t n_local,
+                                    int32_t k, const spb_shard* shard, void* ws, size_t ws_bytes,
+                                    int32_t* labels_out, int32_t* pivots_out, double* info_out,
+                                    void* stream);
 
 /* ---------------- (f.2) edge-list ingestion ---------------------------------
  * load_edge_list (graph.py:152-209): tab-separated "src dst [weight]" text in a

@@ -108,6 +108,9 @@ _SIGS = {
                              C.POINTER(i32), vp]),
     "spb_assign_workspace": (sz, [i32, i32]),
     "spb_assign_qrcp": (C.c_int, [C.c_int, vp, i64, i32, i32, vp, sz, vp, vp, C.POINTER(f64), vp]),
+    "spb_assign_workspace_sharded": (sz, [i32, i32, i32]),
+    "spb_assign_qrcp_sharded": (C.c_int, [C.c_int, vp, i64, i32, i32, vp, vp, sz, vp, vp,
+                                          C.POINTER(f64), vp]),
 }
 
 EXPORTED = tuple(_SIGS)

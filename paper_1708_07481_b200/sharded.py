@@ -34,7 +34,7 @@ from . import _native as N
 from .errors import ContractError, DomainError, SolverError, SpecpartError
 from .graph import DTYPES, SparseGraph, _device, _device_arcs
 from .lobpcg import EigenState, SolverConfig, _Bridge, default_precision, random_init
-from .spectral import GapResult, Partition, _assign_device, block_size_for, detect_gap
+from .spectral import GapResult, Partition, block_size_for, detect_gap
 
 __all__ = ["partition_rows", "arc_row_bounds", "RowShardedLaplacian", "lobpcg_solve_sharded",
            "partition_static_sharded", "partition_edges_sharded"]
@@ -306,6 +306,34 @@ def _gather_rows(op: RowShardedLaplacian, local: torch.Tensor, group=None) -> to
     return torch.cat(parts).contiguous()
 
 
+def assign_clusters_qrcp_sharded(op: RowShardedLaplacian, emb: torch.Tensor, k: int):
+    """assign_clusters_qrcp (spectral.py:134-170) on the row-sharded embedding
+    (this rank's rows): k global argmax pivot steps over the communicator
+    (spb_assign_qrcp_sharded), labels of the local rows.
+
+    Returns (local labels int32 device tensor, pivots (global rows, device), info)."""
+    if emb.dtype not in (torch.float32, torch.float64):
+        raise ContractError("embedding must be float32 or float64")
+    emb = emb if emb.stride(1) == 1 else emb.contiguous()
+    code = N.F32 if emb.dtype == torch.float32 else N.F64
+    L = N.lib()
+    _, sh = op.native("float64")
+    nl = emb.shape[0]
+    if nl != op.n_local:
+        raise ContractError("embedding rows do not match this rank's rows")
+    wsb = L.spb_assign_workspace_sharded(nl, k, op.nranks)
+    ws = torch.empty(wsb, dtype=torch.uint8, device=emb.device)
+    labels = torch.empty(max(nl, 1), dtype=torch.int32, device=emb.device)
+    pivots = torch.empty(k, dtype=torch.int32, device=emb.device)
+    info = (C.c_double * 4)()
+    status = L.spb_assign_qrcp_sharded(code, N.ptr(emb), emb.stride(0), nl, k, C.byref(sh),
+                                       N.ptr(ws), wsb, N.ptr(labels), N.ptr(pivots), info, N.stream())
+    if getattr(op.comm, "exc", None) is not None:
+        raise op.comm.exc
+    N.check(status)
+    return labels[:nl], pivots, list(info)
+
+
 def partition_static_sharded(g: SparseGraph, cfg: SolverConfig, k_expected: int | None = None, *,
                              alpha: float = 3.0, k_min: int = 2, fix_k: bool = False, x0=None,
                              precision: str | None = None, group=None, op: RowShardedLaplacian | None = None,
@@ -325,8 +353,9 @@ def partition_static_sharded(g: SparseGraph, cfg: SolverConfig, k_expected: int 
     gap = (detect_gap(state.eigenvalues, k_min=min(k_min, l - 1), alpha=alpha) if l >= 2
            else GapResult(k=1, increments=np.empty(0), confidence=0.0, reliable=False))
     k_used = k_expected if (fix_k and k_expected is not None) else gap.k
-    emb = _gather_rows(op, state.device_vectors[:, :k_used].contiguous(), group)
-    labels, _, info = _assign_device(emb, k_used)
+    # distributed QRCP: global argmax pivot steps, local labels, then one gather of labels
+    local, _, info = assign_clusters_qrcp_sharded(op, state.device_vectors[:, :k_used], k_used)
+    labels = _gather_rows(op, local.view(-1, 1), group).view(-1)
     return Partition(labels.cpu().numpy().astype(np.int64), int(info[0])), state, gap
 
 

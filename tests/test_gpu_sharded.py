@@ -70,3 +70,30 @@ def test_multirank_sharded_solve_host_transport(tmp_path, world, cfg, precision)
           f"max |dtheta| {np.abs(th - ref).max():.2e}, label agreement {agree:.5f}, "
           f"bounds {d['bounds'].tolist()}")
     assert agree >= 0.999
+    # distributed QRCP (global argmax steps) == single-GPU QRCP on the same embedding
+    assert int(d["qrcp_equal"]) == 1
+
+
+@pytest.mark.parametrize("precision", ["float32", "float64"])
+def test_single_rank_sharded_qrcp_equals_cooperative(precision):
+    """The split-kernel pivot loop of spb_assign_qrcp_sharded (one rank: the
+    all-gathers are copies) selects the cooperative kernel's pivots (dgeqp3's)."""
+    import torch
+
+    import paper_1708_07481_b200 as spb
+    from paper_1708_07481_b200.sharded import RowShardedLaplacian, assign_clusters_qrcp_sharded
+    from paper_1708_07481_b200.spectral import _assign_device
+
+    spec, edges, _ = config_input("c2", seed=0)
+    g = spb.from_edges(edges, spec.n)
+    op = RowShardedLaplacian(g)
+    rng = np.random.default_rng(1)
+    for k in (5, 44, 160):
+        q, _ = np.linalg.qr(rng.standard_normal((spec.n, k)) * rng.random(spec.n)[:, None] ** 4)
+        tdt = torch.float32 if precision == "float32" else torch.float64
+        emb = torch.from_numpy(q).to("cuda", tdt)
+        lab_s, piv_s, info_s = assign_clusters_qrcp_sharded(op, emb, k)
+        lab_1, piv_1, info_1 = _assign_device(emb, k)
+        assert torch.equal(piv_s, piv_1), k
+        assert torch.equal(lab_s, lab_1), k
+        assert info_s[0] == info_1[0]

@@ -53,12 +53,27 @@ def main():
                and np.array_equal(g.device_degrees()[r0:r1].cpu().numpy(), op.deg64.cpu().numpy()))
     ok = torch.tensor([int(rows_ok)])
     dist.all_reduce(ok, op=dist.ReduceOp.MIN)
+    # distributed QRCP on this solve's embedding against the single-GPU QRCP of the
+    # gathered embedding: identical pivots (global rows) and labels
+    from paper_1708_07481_b200.sharded import _gather_rows, assign_clusters_qrcp_sharded
+    from paper_1708_07481_b200.spectral import _assign_device
+
+    sop = RowShardedLaplacian(spb.graph.SparseGraph(spec.n, g._src, g._dst, g._w), transport="host")
+    emb_local = st.device_vectors[:, :k].contiguous()
+    lab_l, piv_s, info_s = assign_clusters_qrcp_sharded(sop, emb_local, k)
+    emb = _gather_rows(sop, emb_local)
+    lab_1, piv_1, info_1 = _assign_device(emb, k)
+    lab_s = _gather_rows(sop, lab_l.view(-1, 1)).view(-1)
+    qok = torch.tensor([int(torch.equal(piv_s.cpu(), piv_1.cpu()) and torch.equal(lab_s.cpu(), lab_1.cpu())
+                            and info_s[0] == info_1[0])])
+    dist.all_reduce(qok, op=dist.ReduceOp.MIN)
     if rank == 0:
         ref_part, ref_st, _ = spb.partition_static(g, cfg, k, fix_k=True, x0=x0, precision=precision)
         np.savez(out, world=world, rows_bit_exact=int(ok.item()), iterations=st.iterations,
                  ref_iterations=ref_st.iterations, theta=st.eigenvalues, ref_theta=ref_st.eigenvalues,
                  labels=part.labels, ref_labels=ref_part.labels, hist=np.array(hist),
-                 spmm_calls=st.solve_stats["spmm_calls"], bounds=bounds)
+                 spmm_calls=st.solve_stats["spmm_calls"], bounds=bounds,
+                 qrcp_equal=int(qok.item()), pivots=piv_1.cpu().numpy())
     dist.barrier()
     dist.destroy_process_group()
 
