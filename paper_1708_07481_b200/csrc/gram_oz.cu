@@ -208,21 +208,29 @@ oz_pack(const float* __restrict__ X, int64_t ldx, int64_t n, int cols, int ncg, 
   }
 }
 
+// One Gram of a launch: out = A' B from two packed operands.
+struct OzJob {
+  const int8_t* PA;
+  const int8_t* PB;
+  const unsigned* cmaxA;
+  const unsigned* cmaxB;
+  int64_t planeA, planeB;  // bytes per plane
+  int ncgA, ncgB;          // column groups of the packed planes
+  int p, q;                // output rows (A columns), columns (B columns)
+  double* part;            // split-K partials, ks x p x q
+};
+
+constexpr int kOzMaxTiles = 96;
+
 struct OzParams {
-  int p, q;          // output rows (U columns), columns (V columns)
-  int mtiles, ntiles;
-  int ncgA, ncgB;    // column groups of the packed planes
+  OzJob job[2];
+  uint8_t tm[kOzMaxTiles], tn[kOzMaxTiles], tj[kOzMaxTiles];  // active (m tile, n tile, job)
   int64_t nkb;       // k-blocks
   int64_t kbchunk;   // k-blocks per split
-  int64_t planeA, planeB;  // bytes per plane
-  int64_t split_stride;
-  int upper;         // U == V: tiles strictly below the diagonal are skipped (symmetric)
 };
 
 __global__ void __launch_bounds__(192, 1)
-gram_oz_kernel(const int8_t* __restrict__ PA, const int8_t* __restrict__ PB,
-               const unsigned* __restrict__ cmaxA, const unsigned* __restrict__ cmaxB, OzParams P,
-               double* __restrict__ part) {
+gram_oz_kernel(const __grid_constant__ OzParams P) {
   extern __shared__ __align__(1024) uint8_t osm[];
   uint8_t* base = (uint8_t*)(((uintptr_t)osm + 1023) & ~(uintptr_t)1023);
   uint64_t* full = (uint64_t*)(base + OZ_KS * kOzStage);
@@ -230,15 +238,16 @@ gram_oz_kernel(const int8_t* __restrict__ PA, const int8_t* __restrict__ PB,
   uint64_t* accb = empty + OZ_KS;
   uint32_t* tmem_slot = (uint32_t*)(accb + 1);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int mt = blockIdx.x % P.mtiles, nt = blockIdx.x / P.mtiles;
-  const int m0 = mt * OZ_M, n0 = nt * OZ_N;
-  if (P.upper && n0 + OZ_N <= m0) return;  // every column of the tile below every row
+  const OzJob& J = P.job[P.tj[blockIdx.x]];
+  const int8_t* __restrict__ PA = J.PA;
+  const int8_t* __restrict__ PB = J.PB;
+  const int m0 = P.tm[blockIdx.x] * OZ_M, n0 = P.tn[blockIdx.x] * OZ_N;
   const int64_t kb0 = (int64_t)blockIdx.y * P.kbchunk;
   const int64_t kb1 = min(P.nkb, kb0 + P.kbchunk);
   const int nk = kb1 > kb0 ? (int)(kb1 - kb0) : 0;
   const int gA = m0 / 8, gB = n0 / 8;
-  const int cgA = min(OZ_M / 8, P.ncgA - gA);  // column groups present in this tile
-  const int cgB = min(OZ_N / 8, P.ncgB - gB);
+  const int cgA = min(OZ_M / 8, J.ncgA - gA);  // column groups present in this tile
+  const int cgB = min(OZ_N / 8, J.ncgB - gB);
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < OZ_KS; ++s) {
@@ -274,9 +283,9 @@ gram_oz_kernel(const int8_t* __restrict__ PA, const int8_t* __restrict__ PB,
         const int64_t kb = kb0 + kc;
 #pragma unroll
         for (int d = 0; d < OZ_S; ++d) {
-          bulk_g2s(st + d * (OZ_M / 8) * 256, PA + d * P.planeA + (kb * P.ncgA + gA) * 256, bytesA,
+          bulk_g2s(st + d * (OZ_M / 8) * 256, PA + d * J.planeA + (kb * J.ncgA + gA) * 256, bytesA,
                    &full[s]);
-          bulk_g2s(st + kOzA + d * (OZ_N / 8) * 256, PB + d * P.planeB + (kb * P.ncgB + gB) * 256,
+          bulk_g2s(st + kOzA + d * (OZ_N / 8) * 256, PB + d * J.planeB + (kb * J.ncgB + gB) * 256,
                    bytesB, &full[s]);
         }
       }
@@ -315,8 +324,8 @@ gram_oz_kernel(const int8_t* __restrict__ PA, const int8_t* __restrict__ PB,
     }
     const int quarter = warp & 3;
     const int row = m0 + quarter * 32 + lane;
-    const int eA = row < P.p ? oz_exp(cmaxA[row]) : 0;
-    double* out = part + (int64_t)blockIdx.y * P.split_stride;
+    const int eA = row < J.p ? oz_exp(J.cmaxA[row]) : 0;
+    double* out = J.part + (int64_t)blockIdx.y * J.p * J.q;
     for (int c0 = 0; c0 < OZ_N; c0 += 16) {
       double acc[16];
 #pragma unroll
@@ -339,12 +348,12 @@ gram_oz_kernel(const int8_t* __restrict__ PA, const int8_t* __restrict__ PB,
           for (int i = 0; i < 16; ++i) acc[i] = fma((double)(int)r[i], sc, acc[i]);
         }
       }
-      if (row < P.p) {
+      if (row < J.p) {
 #pragma unroll
         for (int i = 0; i < 16; ++i) {
           const int col = n0 + c0 + i;
-          if (col < P.q) {
-            out[(int64_t)row * P.q + col] = ldexp(acc[i], eA + oz_exp(cmaxB[col]));
+          if (col < J.q) {
+            out[(int64_t)row * J.q + col] = ldexp(acc[i], eA + oz_exp(J.cmaxB[col]));
           }
         }
       }
@@ -400,58 +409,115 @@ int oz_prepare(const float* X, int64_t ldx, int64_t n, int cols, void* mem, OzOp
   return SPB_OK;
 }
 
+// Split-K factor of a launch with `tiles` output tiles over nkb k-blocks: at most
+// OZ_MAXROWS rows per split (exact int32 sums), at least two CTAs per SM, and
+// among the next few candidates the one with the fewest idle CTA slots in the
+// last wave (one CTA per SM).
+int64_t oz_splits(int64_t nkb, int tiles) {
+  const int64_t lo = std::max<int64_t>(ceil_div(2 * num_sms(), tiles), ceil_div(nkb, OZ_MAXROWS / OZ_KB));
+  int64_t best = std::min<int64_t>(lo, nkb);
+  double best_eff = 0.0;
+  for (int64_t ks = best; ks <= std::min<int64_t>(nkb, lo + 16); ++ks) {
+    const int64_t kb = ceil_div(nkb, ks), kse = ceil_div(nkb, kb);  // effective splits
+    const int64_t units = (int64_t)tiles * kse;
+    const double eff = (double)units / (double)(ceil_div(units, num_sms()) * num_sms());
+    if (eff > best_eff + 1e-9) {
+      best_eff = eff;
+      best = ks;
+    }
+  }
+  return best;
+}
+
 size_t gram_oz_partial_doubles(int64_t n, int p, int q) {
   const int tiles = (int)(ceil_div(p, OZ_M) * ceil_div(q, OZ_N));
   const int64_t nkb = ceil_div(std::max<int64_t>(n, 1), OZ_KB);
-  int64_t ks = std::max<int64_t>(ceil_div(2 * num_sms(), tiles), ceil_div(nkb, OZ_MAXROWS / OZ_KB));
-  ks = std::min<int64_t>(ks, nkb);
+  // the Rayleigh-Ritz launch runs two jobs (G_B upper tiles + G_A) in one grid
+  int64_t ks = std::max(oz_splits(nkb, tiles), oz_splits(nkb, 2 * tiles));
+  ks = std::max<int64_t>(ks, ceil_div(2 * num_sms(), tiles));
+  ks = std::min<int64_t>(ks + 16, nkb);
   return (size_t)std::max<int64_t>(ks, 1) * p * q;
 }
 
-// out[A.cols x B.cols] (ld ldo) = A' B from two prepared operands.
-int oz_gemm(const OzOperand& A, const OzOperand& B, double* partial, size_t partial_cap,
-            double* out, int ldo, cudaStream_t st, bool upper = false) {
-  const int p = A.cols, q = B.cols;
-  if (p <= 0 || q <= 0) return SPB_OK;
+// outs[j][A_j.cols x B_j.cols] (ld ldo) = A_j' B_j for one or two jobs in ONE launch
+// (all k-blocks of every job split the same way); upper[j]: B_j == A_j, only tiles
+// reaching the diagonal are computed. partial: per job gram_oz_partial_doubles.
+int oz_gemm_jobs(int njobs, const OzOperand* const* A, const OzOperand* const* B, const bool* upper,
+                 double* const* partial, size_t partial_cap, double* const* out, int ldo,
+                 cudaStream_t st) {
   static std::atomic<uint64_t> attr{0};
   if (!done_on_device(attr)) {
     SPB_CUDA(cudaFuncSetAttribute(gram_oz_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   kOzSmem));
     mark_on_device(attr);
   }
-  const int64_t nkb = A.nkb;
   OzParams P{};
-  P.p = p;
-  P.q = q;
-  P.mtiles = (int)ceil_div(p, OZ_M);
-  P.ntiles = (int)ceil_div(q, OZ_N);
-  P.ncgA = A.ncg;
-  P.ncgB = B.ncg;
+  int tiles = 0;
+  for (int j = 0; j < njobs; ++j) {
+    const int p = A[j]->cols, q = B[j]->cols;
+    if (p <= 0 || q <= 0) continue;
+    OzJob& J = P.job[j];
+    J.PA = A[j]->planes;
+    J.PB = B[j]->planes;
+    J.cmaxA = A[j]->cmax;
+    J.cmaxB = B[j]->cmax;
+    J.planeA = A[j]->plane_bytes;
+    J.planeB = B[j]->plane_bytes;
+    J.ncgA = A[j]->ncg;
+    J.ncgB = B[j]->ncg;
+    J.p = p;
+    J.q = q;
+    J.part = partial[j];
+    const int mtiles = (int)ceil_div(p, OZ_M), ntiles = (int)ceil_div(q, OZ_N);
+    for (int nt = 0; nt < ntiles; ++nt)
+      for (int mt = 0; mt < mtiles; ++mt) {
+        if (upper[j] && (nt + 1) * OZ_N <= mt * OZ_M) continue;  // wholly below the diagonal
+        if (tiles == kOzMaxTiles) {
+          set_error("Ozaki Gram: more than %d output tiles", kOzMaxTiles);
+          return SPB_ERR_CONTRACT;
+        }
+        P.tm[tiles] = (uint8_t)mt;
+        P.tn[tiles] = (uint8_t)nt;
+        P.tj[tiles] = (uint8_t)j;
+        ++tiles;
+      }
+  }
+  if (tiles == 0) return SPB_OK;
+  const int64_t nkb = A[0]->nkb;
+  int64_t ks = oz_splits(nkb, tiles);
+  size_t need = 0;
+  for (int j = 0; j < njobs; ++j) need = std::max(need, (size_t)P.job[j].p * P.job[j].q);
+  while (ks > 1 && (size_t)ks * need > partial_cap) --ks;
   P.nkb = nkb;
-  P.planeA = A.plane_bytes;
-  P.planeB = B.plane_bytes;
-  const int tiles = P.mtiles * P.ntiles;
-  int64_t ks = std::max<int64_t>(ceil_div(2 * num_sms(), tiles), ceil_div(nkb, OZ_MAXROWS / OZ_KB));
-  ks = std::min<int64_t>(ks, nkb);
-  while (ks > 1 && (size_t)ks * p * q > partial_cap) --ks;
   P.kbchunk = ceil_div(nkb, ks);
   ks = ceil_div(nkb, P.kbchunk);
-  if ((size_t)ks * p * q > partial_cap || P.kbchunk * OZ_KB > OZ_MAXROWS) {
+  if ((size_t)ks * need > partial_cap || P.kbchunk * OZ_KB > OZ_MAXROWS) {
     set_error("Ozaki Gram partial workspace too small");
     return SPB_ERR_WORKSPACE;
   }
-  P.split_stride = (int64_t)p * q;
-  P.upper = upper ? 1 : 0;
-  gram_oz_kernel<<<dim3(tiles, (unsigned)ks), 192, kOzSmem, st>>>(A.planes, B.planes, A.cmax,
-                                                                   B.cmax, P, partial);
+  gram_oz_kernel<<<dim3(tiles, (unsigned)ks), 192, kOzSmem, st>>>(P);
   SPB_LAUNCH_CHECK();
-  return oz_sum_splits(partial, (int)ks, P.split_stride, p, q, out, ldo, st);
+  for (int j = 0; j < njobs; ++j)
+    if (P.job[j].p > 0 && P.job[j].q > 0)
+      SPB_TRY(oz_sum_splits(P.job[j].part, (int)ks, (int64_t)P.job[j].p * P.job[j].q, P.job[j].p,
+                            P.job[j].q, out[j], ldo, st));
+  return SPB_OK;
+}
+
+// out[A.cols x B.cols] (ld ldo) = A' B from two prepared operands.
+int oz_gemm(const OzOperand& A, const OzOperand& B, double* partial, size_t partial_cap,
+            double* out, int ldo, cudaStream_t st, bool upper = false) {
+  const OzOperand* a[1] = {&A};
+  const OzOperand* b[1] = {&B};
+  double* pp[1] = {partial};
+  double* oo[1] = {out};
+  return oz_gemm_jobs(1, a, b, &upper, pp, partial_cap, oo, ldo, st);
 }
 
 // Workspace of gram_oz: both operands' digit planes, then the split-K partials.
 size_t gram_oz_ws_bytes(int64_t n, int p, int q) {
   return oz_operand_bytes(n, p) + oz_operand_bytes(n, q) +
-         gram_oz_partial_doubles(n, p, q) * sizeof(double) + 1024;
+         2 * gram_oz_partial_doubles(n, p, q) * sizeof(double) + 2048;
 }
 
 // out[p x q] (ld ldo) = U' V with float32 operands, float64-accurate; ws is caller
@@ -485,12 +551,17 @@ int gram_oz_rr(const float* B, const float* LB, int64_t ld, int64_t n, int cols,
   }
   uint8_t* scr = (uint8_t*)ws;
   double* part = (double*)(scr + 2 * bo);
-  const size_t pc = (ws_bytes - 2 * bo) / sizeof(double);
+  const size_t pc = (ws_bytes - 2 * bo) / sizeof(double) / 2;
   OzOperand OB, OL;
   SPB_TRY(oz_prepare(B, ld, n, cols, scr, &OB, st));
   SPB_TRY(oz_prepare(LB, ld, n, cols, scr + bo, &OL, st));
-  SPB_TRY(oz_gemm(OB, OB, part, pc, Gb, ldo, st, true));  // upper tiles (read as such)
-  return oz_gemm(OB, OL, part, pc, Ga, ldo, st);
+  // G_B (upper tiles, read as such) and G_A in one launch: one grid, one tail
+  const OzOperand* a[2] = {&OB, &OB};
+  const OzOperand* b[2] = {&OB, &OL};
+  const bool up[2] = {true, false};
+  double* pp[2] = {part, part + pc};
+  double* oo[2] = {Gb, Ga};
+  return oz_gemm_jobs(2, a, b, up, pp, pc, oo, ldo, st);
 }
 
 }  // namespace spb

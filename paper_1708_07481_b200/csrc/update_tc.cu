@@ -389,9 +389,29 @@ update_tc_kernel(const __grid_constant__ CUtensorMap map0, const __grid_constant
     for (int i = 0; i < NH; ++i) acc[i] = 0.0f;
     if (P.init && row < P.n) {
       const float* irow = P.init + row * P.ldi + cb;
+      const bool vec = (reinterpret_cast<uintptr_t>(irow) & 15) == 0;
 #pragma unroll
-      for (int i = 0; i < NH; ++i)
-        if (cb + i < P.q) acc[i] = irow[i];
+      for (int c0 = 0; c0 < NH; c0 += 4) {
+        if (vec && cb + c0 + 4 <= P.q) {
+          const float4 v = __ldg(reinterpret_cast<const float4*>(irow + c0));
+          acc[c0] = v.x;
+          acc[c0 + 1] = v.y;
+          acc[c0 + 2] = v.z;
+          acc[c0 + 3] = v.w;
+        } else {
+#pragma unroll
+          for (int i = 0; i < 4; ++i)
+            if (cb + c0 + i < P.q) acc[c0 + i] = irow[c0 + i];
+        }
+      }
+    }
+    // the next tile's rows of init: into L2 while this tile's chunks stream through
+    if (P.init && tile + (int)gridDim.x < ntiles) {
+      const int64_t nrow = row + (int64_t)gridDim.x * UTM;
+      if (nrow < P.n) {
+        const char* p = reinterpret_cast<const char*>(P.init + nrow * P.ldi + cb);
+        for (int b = 0; b < NH * 4; b += 128) asm volatile("prefetch.global.L2 [%0];" ::"l"(p + b));
+      }
     }
     for (int s = 0; s < P.nseg; ++s) {
       for (int c = 0; c < P.seg[s].chunks; ++c, ++kc) {
