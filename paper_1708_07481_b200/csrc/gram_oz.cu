@@ -41,7 +41,10 @@ constexpr int OZ_S = 5;          // digits per value (2^-35 of the column maxima
 constexpr int OZ_M = 128;        // UMMA M (columns of U per tile)
 constexpr int OZ_N = 96;         // UMMA N (columns of V per tile); OZ_S * OZ_N <= 512 TMEM columns
 constexpr int OZ_KB = 32;        // rows per k-block (one UMMA K step for 8-bit operands)
-constexpr int OZ_KS = 4;         // pipeline stages
+#ifndef OZ_STAGES
+#define OZ_STAGES 4
+#endif
+constexpr int OZ_KS = OZ_STAGES;  // pipeline stages
 constexpr int OZ_MAXROWS = 16384;  // rows per CTA: 6 pairs x 127^2 x 16384 < 2^31
 constexpr int kOzA = OZ_S * (OZ_M / 8) * 256;  // bytes of the A planes per stage (24 KB)
 constexpr int kOzB = OZ_S * (OZ_N / 8) * 256;  // bytes of the B planes per stage (15 KB)
@@ -90,6 +93,16 @@ __device__ __forceinline__ void umma_i8(uint32_t tmem_d, uint64_t a, uint64_t b,
       "setp.ne.b32 p, %4, 0;\n\t"
       "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
       "l"(a), "l"(b), "r"(idesc), "r"(accum));
+}
+// one lane of a converged warp (elect.sync)
+__device__ __forceinline__ bool oz_elect() {
+  uint32_t pred = 0;
+  asm volatile(
+      "{\n\t.reg .pred P;\n\t"
+      "elect.sync _|P, 0xffffffff;\n\t"
+      "selp.b32 %0, 1, 0, P;\n\t}"
+      : "=r"(pred));
+  return pred != 0;
 }
 __device__ __forceinline__ void oz_commit(uint64_t* bar) {
   asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
@@ -291,30 +304,40 @@ gram_oz_kernel(const __grid_constant__ OzParams P) {
       }
     }
   } else if (warp == 1) {
-    if (lane == 0 && nk > 0) {
+    // the whole warp walks the pipeline (converged: descriptors and TMEM addresses
+    // stay in uniform registers); one elected lane issues the MMAs and commits
+    if (nk > 0) {
       const uint32_t idesc = (2u << 4) | (1u << 7) | (1u << 10) |  // S32 acc, s8 A/B, K-major
                              ((uint32_t)(OZ_N >> 3) << 17) | ((uint32_t)(OZ_M >> 4) << 24);
+      const uint64_t dA0 = oz_desc(s_u32(base), 128, 256);
+      const uint64_t dB0 = oz_desc(s_u32(base + kOzA), 128, 256);
       for (int kc = 0; kc < nk; ++kc) {
         const int s = kc % OZ_KS, u = kc / OZ_KS;
         oz_mbar_wait(&full[s], u & 1);
         asm volatile("tcgen05.fence::after_thread_sync;");
-        const uint32_t sa = s_u32(base + s * kOzStage), sb = sa + kOzA;
-        // level L = t + u - 2 accumulates digit pairs (t, u), t + u <= S + 1
+        // descriptor start addresses advance in 16-byte units (no carry out of the
+        // 14-bit field: every shared-memory address is < 256 KB)
+        const uint64_t ds = (uint64_t)((s * kOzStage) >> 4);
+        if (oz_elect()) {
+          // level L = t + u - 2 accumulates digit pairs (t, u), t + u <= S + 1
 #pragma unroll
-        for (int t = 1; t <= OZ_S; ++t)
+          for (int t = 1; t <= OZ_S; ++t)
 #pragma unroll
-          for (int uu = 1; uu <= OZ_S; ++uu) {
-            if (t + uu > OZ_S + 1) continue;
-            const int L = t + uu - 2;
-            const uint64_t da = oz_desc(sa + (t - 1) * (OZ_M / 8) * 256, 128, 256);
-            const uint64_t db = oz_desc(sb + (uu - 1) * (OZ_N / 8) * 256, 128, 256);
-            // first write of level L in this CTA: the (1, L+1) pair at kc == 0
-            const uint32_t acc = (kc > 0 || t > 1) ? 1u : 0u;
-            umma_i8(tmem + (uint32_t)(L * OZ_N), da, db, idesc, acc);
-          }
-        oz_commit(&empty[s]);
+            for (int uu = 1; uu <= OZ_S; ++uu) {
+              if (t + uu > OZ_S + 1) continue;
+              const int L = t + uu - 2;
+              const uint64_t da = dA0 + ds + (uint64_t)(((t - 1) * (OZ_M / 8) * 256) >> 4);
+              const uint64_t db = dB0 + ds + (uint64_t)(((uu - 1) * (OZ_N / 8) * 256) >> 4);
+              // first write of level L in this CTA: the (1, L+1) pair at kc == 0
+              const uint32_t acc = (kc > 0 || t > 1) ? 1u : 0u;
+              umma_i8(tmem + (uint32_t)(L * OZ_N), da, db, idesc, acc);
+            }
+          oz_commit(&empty[s]);
+        }
+        __syncwarp();
       }
-      oz_commit(accb);
+      if (oz_elect()) oz_commit(accb);
+      __syncwarp();
     }
   } else {
     // epilogue: warps 2..5 -> TMEM lanes 32*(warp & 3) .. +31 = tile rows

@@ -103,6 +103,16 @@ __device__ __forceinline__ void ut_mma(uint32_t tmem_d, uint64_t a, uint64_t b, 
       "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
       "l"(a), "l"(b), "r"(idesc), "r"(accum));
 }
+// one lane of a converged warp (elect.sync)
+__device__ __forceinline__ bool ut_elect() {
+  uint32_t pred = 0;
+  asm volatile(
+      "{\n\t.reg .pred P;\n\t"
+      "elect.sync _|P, 0xffffffff;\n\t"
+      "selp.b32 %0, 1, 0, P;\n\t}"
+      : "=r"(pred));
+  return pred != 0;
+}
 __device__ __forceinline__ void ut_commit(uint64_t* bar) {
   asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
                    ut_smem(bar))
@@ -273,10 +283,14 @@ update_tc_kernel(const __grid_constant__ CUtensorMap map0, const __grid_constant
       }
     }
   } else if (warp == 1) {
-    if (lane == 0) {
+    // the whole warp walks the pipeline (converged: descriptors and TMEM addresses
+    // stay in uniform registers); one elected lane issues the MMAs and commits
+    {
       const uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) |  // F32 acc, TF32 A/B, K-major
                              ((uint32_t)(P.npad >> 3) << 17) | ((uint32_t)(UTM >> 4) << 24);
       const int total = ((ntiles - (int)blockIdx.x + (int)gridDim.x - 1) / (int)gridDim.x) * nk;
+      const uint64_t dbase = ut_desc_sw128(ut_smem(base + kBoff));  // stage 0's B hi
+      const uint32_t blo_off = (uint32_t)(P.npad * UTK * 4) >> 4;
       int G = 0, rg = 0;  // chunk group counter / its TMEM region (double-buffered)
       for (int kc = 0; kc < total; ++kc) {
         const int st = kc % UTS, u = kc / UTS;
@@ -288,36 +302,37 @@ update_tc_kernel(const __grid_constant__ CUtensorMap map0, const __grid_constant
         }
         ut_wait(&split[st], u & 1);
         asm volatile("tcgen05.fence::after_thread_sync;");
-        uint8_t* sb = base + st * kStage;
-        const uint32_t bhi = ut_smem(sb + kBoff), blo = bhi + (uint32_t)(P.npad * UTK * 4);
+        // descriptor start addresses advance in 16-byte units (no carry: smem < 256 KB)
+        const uint64_t dbh0 = dbase + (uint64_t)(((uint32_t)st * (uint32_t)kStage) >> 4);
+        const uint64_t dbl0 = dbh0 + blo_off;
         const uint32_t dacc = tmem + (uint32_t)(rg * P.npad);
-        if constexpr (ATM) {
-          const uint32_t ta = tmem + 256u + (uint32_t)st * 64u;  // hi at +0, lo at +32
+        if (ut_elect()) {
+          if constexpr (ATM) {
+            const uint32_t ta = tmem + 256u + (uint32_t)st * 64u;  // hi at +0, lo at +32
 #pragma unroll
-          for (int kk = 0; kk < UTK / 8; ++kk) {
-            const uint32_t off = (uint32_t)kk * 32;
-            const uint64_t dbh = ut_desc_sw128(bhi + off), dbl = ut_desc_sw128(blo + off);
-            ut_mma_ts(dacc, ta + kk * 8, dbl, idesc, (kk == 0 && first) ? 0u : 1u);
-            ut_mma_ts(dacc, ta + 32 + kk * 8, dbh, idesc, 1u);
-            ut_mma_ts(dacc, ta + kk * 8, dbh, idesc, 1u);
-          }
-        } else {
-          const uint32_t ahi = ut_smem(sb), alo = ut_smem(sb + kUtA);
+            for (int kk = 0; kk < UTK / 8; ++kk) {
+              const uint64_t dbh = dbh0 + (uint64_t)(kk * 2), dbl = dbl0 + (uint64_t)(kk * 2);
+              ut_mma_ts(dacc, ta + kk * 8, dbl, idesc, (kk == 0 && first) ? 0u : 1u);
+              ut_mma_ts(dacc, ta + 32 + kk * 8, dbh, idesc, 1u);
+              ut_mma_ts(dacc, ta + kk * 8, dbh, idesc, 1u);
+            }
+          } else {
+            const uint64_t dah0 = ut_desc_sw128(ut_smem(base)) +
+                                  (uint64_t)(((uint32_t)st * (uint32_t)kStage) >> 4);
+            const uint64_t dal0 = dah0 + (uint64_t)(kUtA >> 4);
 #pragma unroll
-          for (int kk = 0; kk < UTK / 8; ++kk) {
-            const uint32_t off = (uint32_t)kk * 32;
-            const uint64_t dah = ut_desc_sw128(ahi + off), dal = ut_desc_sw128(alo + off);
-            const uint64_t dbh = ut_desc_sw128(bhi + off), dbl = ut_desc_sw128(blo + off);
-            ut_mma(dacc, dah, dbl, idesc, (kk == 0 && first) ? 0u : 1u);  // small terms first
-            ut_mma(dacc, dal, dbh, idesc, 1u);
-            ut_mma(dacc, dah, dbh, idesc, 1u);
+            for (int kk = 0; kk < UTK / 8; ++kk) {
+              const uint64_t o = (uint64_t)(kk * 2);  // 32 bytes per K step of 8 tf32
+              ut_mma(dacc, dah0 + o, dbl0 + o, idesc, (kk == 0 && first) ? 0u : 1u);  // small terms first
+              ut_mma(dacc, dal0 + o, dbh0 + o, idesc, 1u);
+              ut_mma(dacc, dah0 + o, dbh0 + o, idesc, 1u);
+            }
           }
+          ut_commit(&empty[st]);
+          if (P.gend[j]) ut_commit(&rdone[rg]);
         }
-        ut_commit(&empty[st]);
-        if (P.gend[j]) {
-          ut_commit(&rdone[rg]);
-          ++G;
-        }
+        __syncwarp();
+        if (P.gend[j]) ++G;
       }
     }
   } else if (warp < 6) {
