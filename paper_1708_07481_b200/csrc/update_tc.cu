@@ -177,6 +177,8 @@ struct UtParams {
   const float* argmin_bias;          // argmin epilogue (see UpdParams)
   int* argmin_labels;
   unsigned long long* argmin_changed;
+  int tma_store;        // emits go out as TMA tensor stores from swizzled smem staging
+  uint32_t stg_off;     // staging offset from the aligned smem base: [EW][2][128 rows][128 B]
 };
 
 // Orderable 64-bit key of (distance, column): unsigned compare = (dist, col) lexicographic.
@@ -218,7 +220,9 @@ __global__ void tc_stage_coeffs(UpdParams P, int npad, float* __restrict__ dst) 
 template <int NPMAX, int EW, bool ATM = false>
 __global__ void __launch_bounds__(EW == 1 ? kUtThreads : kUtThreadsW, 1)
 update_tc_kernel(const __grid_constant__ CUtensorMap map0, const __grid_constant__ CUtensorMap map1,
-                 const __grid_constant__ CUtensorMap map2, UtParams P) {
+                 const __grid_constant__ CUtensorMap map2, const __grid_constant__ CUtensorMap omap0,
+                 const __grid_constant__ CUtensorMap omap1, const __grid_constant__ CUtensorMap omap2,
+                 UtParams P) {
   extern __shared__ __align__(1024) uint8_t usm_raw[];
   uint8_t* base = (uint8_t*)(((uintptr_t)usm_raw + 1023) & ~(uintptr_t)1023);
   const int kB = 2 * P.npad * UTK * 4;              // coefficient chunk bytes (hi | lo)
@@ -266,18 +270,18 @@ update_tc_kernel(const __grid_constant__ CUtensorMap map0, const __grid_constant
 
   if (warp == 0) {
     if (lane == 0) {
-      int g = 0;
+      int st = 0, u = 0;  // stage ring position (no integer division in the loops)
       for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
         int kc = 0;
         for (int s = 0; s < P.nseg; ++s) {
           const CUtensorMap* map = s == 0 ? &map0 : (s == 1 ? &map1 : &map2);
-          for (int c = 0; c < P.seg[s].chunks; ++c, ++kc, ++g) {
-            const int st = g % UTS, u = g / UTS;
+          for (int c = 0; c < P.seg[s].chunks; ++c, ++kc) {
             if (u > 0) ut_wait(&empty[st], (u - 1) & 1);
             uint8_t* sb = base + st * kStage;
             ut_expect(&full[st], (uint32_t)(kUtA + kB));
             ut_tma2d(sb, map, &full[st], c * UTK, tile * UTM);
             ut_bulk(sb + kBoff, P.coef + (size_t)kc * 2 * P.npad * UTK, (uint32_t)kB, &full[st]);
+            if (++st == UTS) { st = 0; ++u; }
           }
         }
       }
@@ -292,9 +296,8 @@ update_tc_kernel(const __grid_constant__ CUtensorMap map0, const __grid_constant
       const uint64_t dbase = ut_desc_sw128(ut_smem(base + kBoff));  // stage 0's B hi
       const uint32_t blo_off = (uint32_t)(P.npad * UTK * 4) >> 4;
       int G = 0, rg = 0;  // chunk group counter / its TMEM region (double-buffered)
+      int st = 0, u = 0, j = 0;  // stage ring position, chunk index within the tile
       for (int kc = 0; kc < total; ++kc) {
-        const int st = kc % UTS, u = kc / UTS;
-        const int j = kc % nk;
         const bool first = P.gstart[j] != 0;
         if (first) {
           rg = G & 1;
@@ -333,14 +336,16 @@ update_tc_kernel(const __grid_constant__ CUtensorMap map0, const __grid_constant
         }
         __syncwarp();
         if (P.gend[j]) ++G;
+        if (++st == UTS) { st = 0; ++u; }
+        if (++j == nk) j = 0;
       }
     }
   } else if (warp < 6) {
     // splitters: hi in place, lo to its own buffer (elementwise: layout preserved)
     const int t = threadIdx.x - 64;
     const int total = ((ntiles - (int)blockIdx.x + (int)gridDim.x - 1) / (int)gridDim.x) * nk;
-    for (int kc = 0; kc < total; ++kc) {
-      const int st = kc % UTS, u = kc / UTS;
+    int st = 0, u = 0;  // stage ring position (no integer division in the loop)
+    for (int kc = 0; kc < total; ++kc, st = (st + 1 == UTS) ? 0 : st + 1, u += (st == 0)) {
       ut_wait(&full[st], u & 1);
       if constexpr (ATM) {
         // this thread's row of the 128B-swizzled tile: 16-byte chunk c of row r sits at
@@ -396,9 +401,12 @@ update_tc_kernel(const __grid_constant__ CUtensorMap map0, const __grid_constant
     constexpr int NH = NPMAX / EW;         // columns per epilogue warp
     const int quarter = warp & 3;
     const int cb = ((warp - 6) >> 2) * NH;  // first column of this warp
-    int kc = 0, G = 0;
+    int G = 0, npass = 0;
+    const int half = (warp - 6) >> 2;
+    const bool issuer = (warp & 3) == 2 && lane == 0;  // first warp of this column half
     for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
     const int64_t row = (int64_t)tile * UTM + quarter * 32 + lane;
+    int j = 0;  // chunk index within the tile
     float acc[NH];
 #pragma unroll
     for (int i = 0; i < NH; ++i) acc[i] = 0.0f;
@@ -429,8 +437,8 @@ update_tc_kernel(const __grid_constant__ CUtensorMap map0, const __grid_constant
       }
     }
     for (int s = 0; s < P.nseg; ++s) {
-      for (int c = 0; c < P.seg[s].chunks; ++c, ++kc) {
-        if (!P.gend[kc % nk]) continue;  // the group accumulates on in TMEM
+      for (int c = 0; c < P.seg[s].chunks; ++c, ++j) {
+        if (!P.gend[j]) continue;  // the group accumulates on in TMEM
         const int rg = G & 1;
         ut_wait(&rdone[rg], (G >> 1) & 1);
         asm volatile("tcgen05.fence::after_thread_sync;");
@@ -490,6 +498,39 @@ update_tc_kernel(const __grid_constant__ CUtensorMap map0, const __grid_constant
           const unsigned m = __ballot_sync(0xffffffffu, moved);
           if (lane == 0 && m) atomicAdd(P.argmin_changed, (unsigned long long)__popc(m));
         }
+      } else if (P.seg[s].emit && P.tma_store) {
+        // 32-column slices of the 128-row tile: each thread writes its row into the
+        // 128B-swizzled staging buffer (conflict-free), then one thread stores the slice
+        // with a TMA tensor store (rows >= n and columns >= q are clipped by the map);
+        // two buffers per column half, the previous store's smem read awaited by the
+        // issuer before the barrier that releases the next writes
+        const CUtensorMap* om = s == 0 ? &omap0 : (s == 1 ? &omap1 : &omap2);
+        const int r = quarter * 32 + lane;
+        const int ncol = P.q - cb;
+#pragma unroll
+        for (int c0 = 0; c0 < NH; c0 += 32) {
+          if (c0 < ncol) {
+            const uint32_t buf = ut_smem(base + P.stg_off) + (uint32_t)((half * 2 + (npass & 1)) * 16384);
+#pragma unroll
+            for (int k = 0; k < 8; ++k) {
+              const uint32_t a = buf + (uint32_t)(r * 128 + ((k ^ (r & 7)) << 4));
+              asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(a), "f"(acc[c0 + 4 * k]),
+                           "f"(acc[c0 + 4 * k + 1]), "f"(acc[c0 + 4 * k + 2]), "f"(acc[c0 + 4 * k + 3])
+                           : "memory");
+            }
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            if (issuer) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+            asm volatile("bar.sync %0, 128;" ::"r"(2 + half) : "memory");
+            if (issuer) {
+              asm volatile(
+                  "cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%1, %2}], [%3];" ::"l"(om),
+                  "r"(cb + c0), "r"(tile * UTM), "r"(buf)
+                  : "memory");
+              asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+            }
+            ++npass;
+          }
+        }
       } else if (P.seg[s].emit && row < P.n) {
         float* orow = P.seg[s].out + row * P.seg[s].ldo + cb;
         const bool vec = (reinterpret_cast<uintptr_t>(orow) & 15) == 0;
@@ -506,6 +547,7 @@ update_tc_kernel(const __grid_constant__ CUtensorMap map0, const __grid_constant
       }
     }
     }  // tile
+    if (issuer && P.tma_store) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
   }
   asm volatile("tcgen05.fence::before_thread_sync;");
   __syncthreads();
@@ -548,6 +590,20 @@ bool ut_map(CUtensorMap* m, const void* ptr, int64_t rows, int cols, int64_t ld)
             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
+// {q (inner) x rows} float32 output view with row pitch ld: 32 x 128 boxes (one
+// 128-byte swizzle span per row), the epilogue's staging layout
+bool ut_map_out(CUtensorMap* m, const void* ptr, int64_t rows, int cols, int64_t ld) {
+  UtEncodeFn fn = ut_encode();
+  if (!fn) return false;
+  const cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
+  const cuuint64_t strides[1] = {(cuuint64_t)ld * 4};
+  const cuuint32_t box[2] = {32u, (cuuint32_t)UTM};
+  const cuuint32_t estr[2] = {1, 1};
+  return fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<void*>(ptr), dims, strides, box, estr,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+            CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 }  // namespace
 
 size_t update_tc_cstage_floats(int w_total, int nseg, int q) {
@@ -576,10 +632,19 @@ bool update_tc(const UpdParams& p, int64_t n, cudaStream_t st) {
   if (!p.cstage || need > p.cstage_cap || need > update_tc_cstage_floats(wtot, p.nseg, p.q) ||
       (reinterpret_cast<uintptr_t>(p.cstage) & 15))
     return false;
-  CUtensorMap maps[3];
+  CUtensorMap maps[3], omaps[3];
   for (int s = 0; s < 3; ++s) {
     const UpdSeg& g = p.seg[s < p.nseg ? s : 0];
     if (!ut_map(&maps[s], g.A, n, g.w, g.lda)) return false;
+  }
+  // output maps for the TMA-store epilogue (emitting segments only)
+  bool omaps_ok = true;
+  for (int s = 0; s < 3; ++s) {
+    const UpdSeg& g = p.seg[s < p.nseg ? s : p.nseg - 1];
+    const UpdSeg& e = g.emit ? g : p.seg[p.nseg - 1];
+    if ((reinterpret_cast<uintptr_t>(e.out) & 15) || (e.ldo & 3) ||
+        !ut_map_out(&omaps[s], e.out, n, p.q, e.ldo))
+      omaps_ok = false;
   }
   UtParams P{};
   for (int s = 0; s < p.nseg; ++s) {
@@ -623,7 +688,19 @@ bool update_tc(const UpdParams& p, int64_t n, cudaStream_t st) {
   if ((size_t)stages * kStage + kExtra > 227 * 1024) stages = 2;
   if (atm) stages = 4;
   P.stages = stages;
-  const size_t smem = (size_t)stages * kStage + kExtra;
+  size_t smem = (size_t)stages * kStage + kExtra;
+  // TMA-store epilogue when its staging ([EW][2][16 KB], 1 KB aligned) fits beside the
+  // stages without costing a stage or a second CTA per SM: the C3 (A in TMEM) and
+  // C4 (two epilogue warp groups) shapes; row-wise st.global of 448-704-byte rows
+  // otherwise (one 16-byte piece of 32 rows per warp store: LSU-bound at tile ends)
+  const int ew = npad > 128 ? 2 : 1;
+  const size_t stg_off = round_up((size_t)stages * kStage + 256 + 4 * UTM * 8, 1024);
+  const size_t smem_tma = stg_off + (size_t)ew * 2 * 16384 + 1024;
+  if (omaps_ok && !p.argmin_labels && (atm || ew == 2) && smem_tma <= 227 * 1024) {
+    P.tma_store = 1;
+    P.stg_off = (uint32_t)stg_off;
+    smem = std::max(smem, smem_tma);
+  }
   static std::atomic<uint64_t> attr{0};
   if (!done_on_device(attr)) {
     cudaFuncSetAttribute(update_tc_kernel<64, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
@@ -637,13 +714,17 @@ bool update_tc(const UpdParams& p, int64_t n, cudaStream_t st) {
   const int per_sm = !atm && 2 * (smem + 2048) <= 228 * 1024 ? 2 : 1;
   const unsigned grid = (unsigned)std::min<int64_t>(ceil_div(n, UTM), (int64_t)per_sm * num_sms());
   if (atm)
-    update_tc_kernel<128, 1, true><<<grid, kUtThreads, smem, st>>>(maps[0], maps[1], maps[2], P);
+    update_tc_kernel<128, 1, true><<<grid, kUtThreads, smem, st>>>(maps[0], maps[1], maps[2], omaps[0],
+                                                                   omaps[1], omaps[2], P);
   else if (npad <= 64)
-    update_tc_kernel<64, 1><<<grid, kUtThreads, smem, st>>>(maps[0], maps[1], maps[2], P);
+    update_tc_kernel<64, 1><<<grid, kUtThreads, smem, st>>>(maps[0], maps[1], maps[2], omaps[0],
+                                                            omaps[1], omaps[2], P);
   else if (npad <= 128)
-    update_tc_kernel<128, 1><<<grid, kUtThreads, smem, st>>>(maps[0], maps[1], maps[2], P);
+    update_tc_kernel<128, 1><<<grid, kUtThreads, smem, st>>>(maps[0], maps[1], maps[2], omaps[0],
+                                                             omaps[1], omaps[2], P);
   else
-    update_tc_kernel<192, 2><<<grid, kUtThreadsW, smem, st>>>(maps[0], maps[1], maps[2], P);
+    update_tc_kernel<192, 2><<<grid, kUtThreadsW, smem, st>>>(maps[0], maps[1], maps[2], omaps[0],
+                                                              omaps[1], omaps[2], P);
   return true;
 }
 
