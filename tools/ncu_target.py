@@ -2,6 +2,7 @@
 
     python tools/ncu_target.py [c2|c3|c4] [steps] [float32|float64]
 """
+import os
 import sys
 from pathlib import Path
 
@@ -10,6 +11,10 @@ import torch
 
 sys.path.insert(0, str(Path(__file__).resolve().parent.parent))
 import paper_1708_07481_b200 as spb  # noqa: E402
+from paper_1708_07481_b200 import _native as _N  # noqa: E402
+
+if os.environ.get("SPB_LIBV"):  # experiment builds (tools/build_variant.py)
+    _N.LIB_PATH = Path(os.environ["SPB_LIBV"])
 from paper_1708_07481_b200.dcsbm import CONFIGS, generate_dcsbm  # noqa: E402
 from paper_1708_07481_b200.spectral import partition_device  # noqa: E402
 
