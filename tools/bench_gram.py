@@ -10,6 +10,10 @@ import torch
 
 sys.path.insert(0, str(Path(__file__).resolve().parent.parent))
 from paper_1708_07481_b200 import _native as N  # noqa: E402
+import os  # noqa: E402
+
+if os.environ.get("SPB_LIBV"):  # experiment builds (tools/build_variant.py)
+    N.LIB_PATH = Path(os.environ["SPB_LIBV"])
 
 ap = argparse.ArgumentParser()
 ap.add_argument("--mode", type=int, default=0)
