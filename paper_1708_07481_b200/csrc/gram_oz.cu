@@ -19,9 +19,12 @@
 // above the threshold at iteration 23), while five digits reproduce 25.
 //
 // Operands are pre-packed by oz_pack into the UMMA canonical K-major layout
-// (8 columns x 16 rows core matrices), one plane per digit:
-//   plane[kblock (32 rows)][column group (8 cols)][k half][8 cols][16 rows]
-// so a CTA's operand tile for one 32-row k-block is one contiguous bulk copy.
+// (core matrices of 8 columns x 16 bytes of K), the digits interleaved per group:
+//   [kblock (32 rows)][column group (8 cols)][digit][k half][8 cols][16 rows]
+// so a CTA's operand tile for one 32-row k-block -- all digits of its column
+// groups -- is ONE contiguous bulk copy (digit plane t of a group at +256 t;
+// 8-column groups OZ_S * 256 bytes apart = the descriptors' stride). Ten bulk
+// copies per k-block (one per digit and operand) had cost ~20 % of the kernel.
 //
 // Per CTA: a 128 x 80 output tile over a range of k-blocks (split-K, at most
 // 16384 rows so the int32 sums cannot overflow). Warp 0 issues the bulk copies
@@ -41,10 +44,7 @@ constexpr int OZ_S = 5;          // digits per value (2^-35 of the column maxima
 constexpr int OZ_M = 128;        // UMMA M (columns of U per tile)
 constexpr int OZ_N = 96;         // UMMA N (columns of V per tile); OZ_S * OZ_N <= 512 TMEM columns
 constexpr int OZ_KB = 32;        // rows per k-block (one UMMA K step for 8-bit operands)
-#ifndef OZ_STAGES
-#define OZ_STAGES 4
-#endif
-constexpr int OZ_KS = OZ_STAGES;  // pipeline stages
+constexpr int OZ_KS = 4;         // pipeline stages (5, 6 measured equal)
 constexpr int OZ_MAXROWS = 16384;  // rows per CTA: 6 pairs x 127^2 x 16384 < 2^31
 constexpr int kOzA = OZ_S * (OZ_M / 8) * 256;  // bytes of the A planes per stage (24 KB)
 constexpr int kOzB = OZ_S * (OZ_N / 8) * 256;  // bytes of the B planes per stage (15 KB)
@@ -213,11 +213,11 @@ oz_pack(const float* __restrict__ X, int64_t ldx, int64_t n, int cols, int ncg, 
         w[sd][i >> 2] |= (__float_as_uint(t) & 0xffu) << (8 * (i & 3));
       }
     }
-    const int64_t off = (((kb * ncg + (c >> 3)) * 2 + h) * 8 + (c & 7)) * 16;
+    const int64_t off = ((kb * ncg + (c >> 3)) * OZ_S * 2 + h) * 128 + (c & 7) * 16;
+    (void)plane_bytes;
 #pragma unroll
     for (int sd = 0; sd < OZ_S; ++sd)
-      *reinterpret_cast<uint4*>(planes + sd * plane_bytes + off) =
-          make_uint4(w[sd][0], w[sd][1], w[sd][2], w[sd][3]);
+      *reinterpret_cast<uint4*>(planes + off + sd * 256) = make_uint4(w[sd][0], w[sd][1], w[sd][2], w[sd][3]);
   }
 }
 
@@ -287,20 +287,15 @@ gram_oz_kernel(const __grid_constant__ OzParams P) {
 
   if (warp == 0) {
     if (lane == 0 && nk > 0) {
-      const uint32_t bytesA = (uint32_t)cgA * 256, bytesB = (uint32_t)cgB * 256;
+      const uint32_t bytesA = (uint32_t)cgA * OZ_S * 256, bytesB = (uint32_t)cgB * OZ_S * 256;
       for (int kc = 0; kc < nk; ++kc) {
         const int s = kc % OZ_KS, u = kc / OZ_KS;
         if (u > 0) oz_mbar_wait(&empty[s], (u - 1) & 1);
         uint8_t* st = base + s * kOzStage;
-        oz_mbar_expect(&full[s], OZ_S * (bytesA + bytesB));
+        oz_mbar_expect(&full[s], bytesA + bytesB);
         const int64_t kb = kb0 + kc;
-#pragma unroll
-        for (int d = 0; d < OZ_S; ++d) {
-          bulk_g2s(st + d * (OZ_M / 8) * 256, PA + d * J.planeA + (kb * J.ncgA + gA) * 256, bytesA,
-                   &full[s]);
-          bulk_g2s(st + kOzA + d * (OZ_N / 8) * 256, PB + d * J.planeB + (kb * J.ncgB + gB) * 256,
-                   bytesB, &full[s]);
-        }
+        bulk_g2s(st, PA + (kb * J.ncgA + gA) * OZ_S * 256, bytesA, &full[s]);
+        bulk_g2s(st + kOzA, PB + (kb * J.ncgB + gB) * OZ_S * 256, bytesB, &full[s]);
       }
     }
   } else if (warp == 1) {
@@ -309,8 +304,8 @@ gram_oz_kernel(const __grid_constant__ OzParams P) {
     if (nk > 0) {
       const uint32_t idesc = (2u << 4) | (1u << 7) | (1u << 10) |  // S32 acc, s8 A/B, K-major
                              ((uint32_t)(OZ_N >> 3) << 17) | ((uint32_t)(OZ_M >> 4) << 24);
-      const uint64_t dA0 = oz_desc(s_u32(base), 128, 256);
-      const uint64_t dB0 = oz_desc(s_u32(base + kOzA), 128, 256);
+      const uint64_t dA0 = oz_desc(s_u32(base), 128, OZ_S * 256);
+      const uint64_t dB0 = oz_desc(s_u32(base + kOzA), 128, OZ_S * 256);
       for (int kc = 0; kc < nk; ++kc) {
         const int s = kc % OZ_KS, u = kc / OZ_KS;
         oz_mbar_wait(&full[s], u & 1);
@@ -326,8 +321,8 @@ gram_oz_kernel(const __grid_constant__ OzParams P) {
             for (int uu = 1; uu <= OZ_S; ++uu) {
               if (t + uu > OZ_S + 1) continue;
               const int L = t + uu - 2;
-              const uint64_t da = dA0 + ds + (uint64_t)(((t - 1) * (OZ_M / 8) * 256) >> 4);
-              const uint64_t db = dB0 + ds + (uint64_t)(((uu - 1) * (OZ_N / 8) * 256) >> 4);
+              const uint64_t da = dA0 + ds + (uint64_t)(((t - 1) * 256) >> 4);
+              const uint64_t db = dB0 + ds + (uint64_t)(((uu - 1) * 256) >> 4);
               // first write of level L in this CTA: the (1, L+1) pair at kc == 0
               const uint32_t acc = (kc > 0 || t > 1) ? 1u : 0u;
               umma_i8(tmem + (uint32_t)(L * OZ_N), da, db, idesc, acc);
