@@ -99,6 +99,9 @@ size_t gram_tc_partial_doubles(int64_t n, int p, int qtot);
 size_t gram_oz_ws_bytes(int64_t n, int p, int q);
 int gram_oz_rr(const float* B, const float* LB, int64_t ld, int64_t n, int cols, double* Ga,
                double* Gb, int ldo, void* ws, size_t ws_bytes, cudaStream_t st);
+// out = U'V (p x q, ld ldo) through the Ozaki int8 path; U == V (p == q): packed once
+int gram_oz(const float* U, int64_t ldu, int p, const float* V, int64_t ldv, int q, int64_t n,
+            void* ws, size_t ws_bytes, double* out, int ldo, cudaStream_t st);
 int gram_tc(const float* U, int64_t ldu, int p, const float* V0, int64_t ldv0, int q0,
             const float* V1, int64_t ldv1, int q1, int64_t n, double* partial, size_t partial_cap,
             double* out, int ldo, cudaStream_t st);

@@ -553,6 +553,8 @@ int gram_oz(const float* U, int64_t ldu, int p, const float* V, int64_t ldv, int
   const size_t partial_cap = (ws_bytes - ba - bb) / sizeof(double);
   OzOperand A, B;
   SPB_TRY(oz_prepare(U, ldu, n, p, scr, &A, st));
+  if (U == V && ldu == ldv && p == q)  // U'U: one operand, packed once
+    return oz_gemm(A, A, partial, partial_cap, out, ldo, st);
   SPB_TRY(oz_prepare(V, ldv, n, q, scr + ba, &B, st));
   return oz_gemm(A, B, partial, partial_cap, out, ldo, st);
 }
