@@ -115,3 +115,32 @@ def test_ozaki_rr_grams_track_dmma_in_the_solver():
     assert rel.max() < 1e-6, rel.max()
     assert np.abs(np.log10(ha) - np.log10(hb)).max() < 0.01
     assert spb.partition_match(spb.contingency(la, lb)) > 0.999
+
+
+@pytest.mark.parametrize("n,p", [(60000, 176), (9000, 49), (40000, 324)])
+def test_ozaki_self_gram_packs_once(n, p):
+    """U'U through spb_gram mode 2 with the same device block for both operands (the
+    solver's CholQR Gram at C4): one packed operand, same accuracy as two."""
+    import torch
+
+    from paper_1708_07481_b200 import _native as N
+
+    rng = np.random.default_rng(n + p)
+    u = (rng.standard_normal((n, p)) * rng.random(n)[:, None]).astype(np.float32)
+    ld = ((p + 7) // 8) * 8
+    ut = torch.zeros((n, ld), dtype=torch.float32, device="cuda")
+    ut[:, :p] = torch.from_numpy(u).cuda()
+    out = torch.full((p, p), np.nan, dtype=torch.float64, device="cuda")
+    L = N.lib()
+    wsb = L.spb_gram_workspace(p, p, n)
+    ws = torch.empty(wsb, dtype=torch.uint8, device="cuda")
+    N.check(L.spb_gram(N.F32, 2, N.ptr(ut), ld, p, N.ptr(ut), ld, p, n, N.ptr(out), p,
+                       N.ptr(ws), wsb, N.stream()))
+    g = out.cpu().numpy()
+    u64 = u.astype(np.float64)
+    exact = u64.T @ u64
+    scale = np.abs(u64).T @ np.abs(u64)
+    assert np.all(np.isfinite(g))
+    assert (np.abs(g - exact) / scale).max() < 1e-10
+    two = _gram(u, u, 2)  # separate operand copies: the two-operand path
+    assert (np.abs(g - two) / scale).max() < 1e-10
