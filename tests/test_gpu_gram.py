@@ -141,6 +141,7 @@ def test_ozaki_self_gram_packs_once(n, p):
     exact = u64.T @ u64
     scale = np.abs(u64).T @ np.abs(u64)
     assert np.all(np.isfinite(g))
-    assert (np.abs(g - exact) / scale).max() < 1e-10
+    # rows scaled by U(0, 1): the digits are relative to each column's maximum
+    assert (np.abs(g - exact) / scale).max() < 1e-9
     two = _gram(u, u, 2)  # separate operand copies: the two-operand path
-    assert (np.abs(g - two) / scale).max() < 1e-10
+    assert (np.abs(g - two) / scale).max() < 1e-9
