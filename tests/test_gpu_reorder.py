@@ -157,3 +157,34 @@ def test_callbacks_see_caller_order(spb):
     assert len(c0) == len(c1)
     for a, b in zip(c0[:3], c1[:3]):  # Ritz vector signs are arbitrary (either order)
         assert np.allclose(a, b, rtol=1e-8, atol=1e-12) or np.allclose(a, -b, rtol=1e-8, atol=1e-12)
+
+
+@pytest.mark.parametrize("name", ["path3", "k4", "two_tri", "rand150", "rand300_20it"])
+def test_small_and_weighted_graphs_in_order(spb, name):
+    """Forced locality order on the small golden solve cases (weighted arcs, a
+    disconnected graph, n = 3): same iterations and Ritz values as the caller's order."""
+    from tests.helpers import solve_cases
+
+    edges, n, l, kw, seed = solve_cases()[name]
+    edges = np.asarray(edges)
+    w = edges[:, 2] if edges.shape[1] == 3 else None
+    g = spb.from_edges(edges[:, :2].astype(np.int64), n, weights=w)
+    cfg = spb.SolverConfig(block_size=l, **kw)
+    x0 = spb.random_init(n, l, seed)
+    out = {}
+    for vo in (False, True):
+        out[vo] = spb.lobpcg_solve(spb.LaplacianOperator(g, vertex_order=vo), x0, cfg,
+                                   precision="float64")
+    a, b = out[False], out[True]
+    assert a.iterations == b.iterations
+    assert np.allclose(a.eigenvalues, b.eigenvalues, rtol=1e-9, atol=1e-9 * max(1.0, abs(a.eigenvalues).max()))
+
+
+def test_order_with_isolated_vertices(spb):
+    """Vertices without edges (degree 0) get a key and a place in the order."""
+    rng = np.random.default_rng(4)
+    n = 3000
+    ends = rng.integers(0, 2000, size=(20000, 2))  # vertices 2000..2999 isolated
+    g = spb.from_edges(ends, n)
+    perm = _order(spb, g).perm.cpu().numpy()
+    assert np.array_equal(np.sort(perm), np.arange(n))
