@@ -128,14 +128,18 @@ wmean_partial(int32_t n, const T* __restrict__ deg, const float* __restrict__ y,
   }
 }
 
+// one warp per column: lane-strided partials, then a fixed shuffle tree
 __global__ void wmean_final(const double* __restrict__ part, int nb, float* __restrict__ mean) {
-  if (threadIdx.x > kWalkCols) return;
+  const int lane = threadIdx.x & 31, c = threadIdx.x >> 5;
+  if (c > kWalkCols) return;
   double v = 0.0, d = 0.0;
-  for (int b = 0; b < nb; ++b) {
-    v += part[b * (kWalkCols + 1) + threadIdx.x];
+  for (int b = lane; b < nb; b += 32) {
+    v += part[b * (kWalkCols + 1) + c];
     d += part[b * (kWalkCols + 1) + kWalkCols];
   }
-  if (threadIdx.x < kWalkCols) mean[threadIdx.x] = d > 0.0 ? (float)(v / d) : 0.f;
+  v = warp_sum(v);
+  d = warp_sum(d);
+  if (lane == 0 && c < kWalkCols) mean[c] = d > 0.0 ? (float)(v / d) : 0.f;
 }
 
 __global__ void walk_keys(int32_t n, const float* __restrict__ y, const float* __restrict__ mean,
@@ -248,7 +252,7 @@ int vertex_order_t(int32_t n, const int32_t* rp, const int32_t* ci, const T* cv,
     std::swap(yi, yo);
   }
   wmean_partial<T><<<kMeanBlocks, 256, 0, st>>>(n, deg, yi, L.part);
-  wmean_final<<<1, 32, 0, st>>>(L.part, kMeanBlocks, L.mean);
+  wmean_final<<<1, 32 * (kWalkCols + 1), 0, st>>>(L.part, kMeanBlocks, L.mean);
   walk_keys<<<grid_rows(n), 256, 0, st>>>(n, yi, L.mean, L.ka, L.pa);
   SPB_LAUNCH_CHECK();
   uint64_t *kin = L.ka, *kout = L.kb;

@@ -99,9 +99,12 @@ class _VertexOrder:
         self.perm = torch.empty(max(n, 1), dtype=torch.int32, device=dev)
         wsb = L.spb_vertex_order_workspace(n)
         ws = torch.empty(wsb, dtype=torch.uint8, device=dev)
-        N.check(L.spb_vertex_order(N.F64, n, N.ptr(c.row_ptr), N.ptr(c.col), N.ptr(c.val),
-                                   N.ptr(c.deg), ORDER_STEPS, ORDER_SEED, N.ptr(ws), wsb,
-                                   N.ptr(self.perm), N.stream()))
+        # float32 copies of W and d (the float32 solve's own; the walk computes in
+        # float32 either way, the copies only halve its value traffic)
+        N.check(L.spb_vertex_order(N.F32, n, N.ptr(c.row_ptr), N.ptr(c.col),
+                                   N.ptr(c.values("float32")), N.ptr(c.degrees("float32")),
+                                   ORDER_STEPS, ORDER_SEED, N.ptr(ws), wsb, N.ptr(self.perm),
+                                   N.stream()))
         self._csr = {}
 
     def csr(self, c: _Csr, dtype: str):
