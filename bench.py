@@ -632,6 +632,14 @@ def run_ours(args):
                          "kernel": "spb::gram_dmma_t (+ sum_splits)"}
         gram_roof.update({"launches": g_calls, "avg_launch_us": g_us / max(g_calls, 1),
                           "live_ms_total": g_us / 1e3, "standalone": gram})
+        gt = ROOT / "profiles" / "gram_traffic.json"
+        gtr = json.loads(gt.read_text()).get(args.config) if gt.exists() else None
+        gram_roof["traffic"] = gtr
+        if gtr:
+            gram_roof["traffic_note"] = (
+                "ncu dram__bytes_read+write of one Rayleigh-Ritz Gram launch (G_B and G_A together, "
+                "profiles/gram_traffic.json); the digit planes of B and LB are 5 bytes per float32 "
+                "value, so ~1.6 GB at C3 is the launch's compulsory stream")
         # the dominant of the two (by live time in this run) is the headline roofline
         if g_us >= spmm_us:
             roofline = dict(gram_roof, spmm=spmm_roof, csr_build=csr)
