@@ -133,8 +133,21 @@ __global__ void oz_colmax(const float* __restrict__ X, int64_t ldx, int64_t n, i
 }
 
 // Same with 16-byte loads: a warp covers 128 consecutive columns of a row.
-__global__ void oz_colmax4(const float* __restrict__ X, int64_t ldx, int64_t n, int cols,
-                           unsigned* __restrict__ cmax) {
+// Up to two operands in one launch (blockIdx.z), e.g. the Rayleigh-Ritz B and LB.
+struct OzSrc {
+  const float* X;
+  int64_t ldx;
+  unsigned* cmax;
+  int8_t* planes;
+};
+struct OzSrc2 {
+  OzSrc s[2];
+};
+
+__global__ void oz_colmax4(const OzSrc2 P2, int64_t n, int cols) {
+  const float* __restrict__ X = P2.s[blockIdx.z].X;
+  const int64_t ldx = P2.s[blockIdx.z].ldx;
+  unsigned* __restrict__ cmax = P2.s[blockIdx.z].cmax;
   __shared__ uint4 wm[8][32];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int c = blockIdx.y * 128 + lane * 4;
@@ -174,8 +187,11 @@ __global__ void oz_colmax4(const float* __restrict__ X, int64_t ldx, int64_t n, 
 // bytes of each plane are packed in registers and stored as one 16-byte vector
 // (a warp's stores form contiguous 128-byte runs).
 __global__ void __launch_bounds__(256)
-oz_pack(const float* __restrict__ X, int64_t ldx, int64_t n, int cols, int ncg, int64_t nkb,
-        const unsigned* __restrict__ cmax, int8_t* __restrict__ planes, int64_t plane_bytes) {
+oz_pack(const OzSrc2 P2, int64_t n, int cols, int ncg, int64_t nkb, int64_t plane_bytes) {
+  const float* __restrict__ X = P2.s[blockIdx.z].X;
+  const int64_t ldx = P2.s[blockIdx.z].ldx;
+  const unsigned* __restrict__ cmax = P2.s[blockIdx.z].cmax;
+  int8_t* __restrict__ planes = P2.s[blockIdx.z].planes;
   const int cpad = ncg * 8;
   const int64_t total = nkb * 2 * cpad;
   for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total;
@@ -403,28 +419,47 @@ size_t oz_operand_bytes(int64_t n, int cols) {
 }
 
 // Column maxima and digit planes of X (n x cols, float32, row stride ldx) into mem.
-int oz_prepare(const float* X, int64_t ldx, int64_t n, int cols, void* mem, OzOperand* op,
-               cudaStream_t st) {
-  op->cols = cols;
-  op->n = n;
-  op->nkb = ceil_div(std::max<int64_t>(n, 1), OZ_KB);
-  op->ncg = (int)ceil_div(cols, 8);
-  op->plane_bytes = op->nkb * op->ncg * 256;
-  op->planes = (int8_t*)mem;
-  op->cmax = (unsigned*)(op->planes + OZ_S * op->plane_bytes);
-  SPB_CUDA(cudaMemsetAsync(op->cmax, 0, sizeof(unsigned) * (size_t)cols, st));
-  const int gx = (int)std::min<int64_t>(ceil_div(n, 8), 4 * num_sms());
-  if ((reinterpret_cast<uintptr_t>(X) & 15) == 0 && (ldx & 3) == 0)
+// Column maxima and digit planes of nop (1 or 2) float32 operands X[i] (n x cols, row
+// stride ld[i]) into mem[i]: one colmax launch and one pack launch for both.
+int oz_prepare_n(int nop, const float* const* X, const int64_t* ld, int64_t n, int cols,
+                 void* const* mem, OzOperand* op, cudaStream_t st) {
+  OzSrc2 P2{};
+  bool vec = true;
+  for (int i = 0; i < nop; ++i) {
+    op[i].cols = cols;
+    op[i].n = n;
+    op[i].nkb = ceil_div(std::max<int64_t>(n, 1), OZ_KB);
+    op[i].ncg = (int)ceil_div(cols, 8);
+    op[i].plane_bytes = op[i].nkb * op[i].ncg * 256;
+    op[i].planes = (int8_t*)mem[i];
+    op[i].cmax = (unsigned*)(op[i].planes + OZ_S * op[i].plane_bytes);
+    SPB_CUDA(cudaMemsetAsync(op[i].cmax, 0, sizeof(unsigned) * (size_t)cols, st));
+    P2.s[i] = {X[i], ld[i], op[i].cmax, op[i].planes};
+    vec = vec && (reinterpret_cast<uintptr_t>(X[i]) & 15) == 0 && (ld[i] & 3) == 0;
+  }
+  if (vec) {
     oz_colmax4<<<dim3((unsigned)std::min<int64_t>(ceil_div(n, 64), 2 * num_sms()),
-                      (unsigned)ceil_div(cols, 128)),
-                 256, 0, st>>>(X, ldx, n, cols, op->cmax);
-  else
-    oz_colmax<<<dim3(gx, (unsigned)ceil_div(cols, 32)), 256, 0, st>>>(X, ldx, n, cols, op->cmax);
-  const int64_t t = op->nkb * 2 * op->ncg * 8;
-  oz_pack<<<(int)std::min<int64_t>(ceil_div(t, 256), 16 * num_sms()), 256, 0, st>>>(
-      X, ldx, n, cols, op->ncg, op->nkb, op->cmax, op->planes, op->plane_bytes);
+                      (unsigned)ceil_div(cols, 128), (unsigned)nop),
+                 256, 0, st>>>(P2, n, cols);
+  } else {
+    const int gx = (int)std::min<int64_t>(ceil_div(n, 8), 4 * num_sms());
+    for (int i = 0; i < nop; ++i)
+      oz_colmax<<<dim3(gx, (unsigned)ceil_div(cols, 32)), 256, 0, st>>>(X[i], ld[i], n, cols,
+                                                                         op[i].cmax);
+  }
+  const int64_t t = op[0].nkb * 2 * op[0].ncg * 8;
+  oz_pack<<<dim3((unsigned)std::min<int64_t>(ceil_div(t, 256), 16 * num_sms()), 1, (unsigned)nop), 256,
+            0, st>>>(P2, n, cols, op[0].ncg, op[0].nkb, op[0].plane_bytes);
   SPB_LAUNCH_CHECK();
   return SPB_OK;
+}
+
+int oz_prepare(const float* X, int64_t ldx, int64_t n, int cols, void* mem, OzOperand* op,
+               cudaStream_t st) {
+  const float* xs[1] = {X};
+  const int64_t ls[1] = {ldx};
+  void* ms[1] = {mem};
+  return oz_prepare_n(1, xs, ls, n, cols, ms, op, st);
 }
 
 // Split-K factor of a launch with `tiles` output tiles over nkb k-blocks: at most
@@ -572,9 +607,15 @@ int gram_oz_rr(const float* B, const float* LB, int64_t ld, int64_t n, int cols,
   uint8_t* scr = (uint8_t*)ws;
   double* part = (double*)(scr + 2 * bo);
   const size_t pc = (ws_bytes - 2 * bo) / sizeof(double) / 2;
-  OzOperand OB, OL;
-  SPB_TRY(oz_prepare(B, ld, n, cols, scr, &OB, st));
-  SPB_TRY(oz_prepare(LB, ld, n, cols, scr + bo, &OL, st));
+  OzOperand ops[2];
+  {
+    const float* xs[2] = {B, LB};
+    const int64_t ls[2] = {ld, ld};
+    void* ms[2] = {scr, scr + bo};
+    SPB_TRY(oz_prepare_n(2, xs, ls, n, cols, ms, ops, st));
+  }
+  const OzOperand& OB = ops[0];
+  const OzOperand& OL = ops[1];
   // G_B (upper tiles, read as such) and G_A in one launch: one grid, one tail
   const OzOperand* a[2] = {&OB, &OB};
   const OzOperand* b[2] = {&OB, &OL};
