@@ -237,26 +237,18 @@ int launch_spmm(int32_t r0, int32_t r1, const int32_t* rp, const int32_t* ci, co
   {
     const int c0 = 0, pc = ncols;
     const int nvec = (pc + VN - 1) / VN;
-    // rows of more than 8 vectors: spmm_vb (SPMM_U gathers in flight per lane, 128-thread
+    // rows of more than 8 vectors: spmm_vb (kU gathers in flight per lane, 128-thread
     // blocks so short rows free their slots early; round 1 with U = 2: -7 % at C2, -9 %
     // at C3 against spmm_vec in the natural order)
     if (nvec > 8) {
-// one gather in flight per lane (U = 1): with the locality order the gathers hit
-// L2 (69 % at C3) and U = 2 / 4 measured slower (C3 apply 0.94 / 1.02 / 1.19 ms,
-// C4 7.57 / 8.17 / 9.26 ms); 128-thread blocks, 8 per SM (64-thread blocks 0.97,
-// 4 per SM 1.08, 12 per SM 0.99 ms at C3; tools/bench_spmm_order.py)
-#ifndef SPMM_U
-#define SPMM_U 1
-#endif
-#ifndef SPMM_MINB
-#define SPMM_MINB 8
-#endif
-#ifndef SPMM_BLOCK
-#define SPMM_BLOCK 128
-#endif
-      auto kf = nvec <= 16 ? spmm_vb<T, 16, SPMM_U, SPMM_MINB> : spmm_vb<T, 32, SPMM_U, SPMM_MINB>;
-      const int64_t vblocks = ceil_div(rows * 32, SPMM_BLOCK);
-      kf<<<vblocks, SPMM_BLOCK, 0, st>>>(r0, r1, rp, ci, cv, deg, x, ldx, c0, pc, y, ldy, xoff);
+      // one gather in flight per lane (U = 1): with the locality order the gathers hit
+      // L2 (69 % at C3) and U = 2 / 4 measured slower (C3 apply 0.94 / 1.02 / 1.19 ms,
+      // C4 7.57 / 8.17 / 9.26 ms); 128-thread blocks, 8 per SM (64-thread blocks 0.97,
+      // 4 per SM 1.08, 12 per SM 0.99 ms at C3; tools/bench_spmm_order.py)
+      constexpr int kU = 1, kMinB = 8, kBlock = 128;
+      auto kf = nvec <= 16 ? spmm_vb<T, 16, kU, kMinB> : spmm_vb<T, 32, kU, kMinB>;
+      const int64_t vblocks = ceil_div(rows * 32, kBlock);
+      kf<<<vblocks, kBlock, 0, st>>>(r0, r1, rp, ci, cv, deg, x, ldx, c0, pc, y, ldy, xoff);
       SPB_LAUNCH_CHECK();
       return SPB_OK;
     }
