@@ -277,6 +277,9 @@ gram_oz_kernel(const __grid_constant__ OzParams P) {
   const int gA = m0 / 8, gB = n0 / 8;
   const int cgA = min(OZ_M / 8, J.ncgA - gA);  // column groups present in this tile
   const int cgB = min(OZ_N / 8, J.ncgB - gB);
+  // UMMA N of this tile: the last column tile of a narrow Gram (C3's 108 = 96 + 12
+  // columns) runs N = 16 instead of 96 (N: multiple of 16 for M = 128)
+  const int ntile = min(OZ_N, (J.q - n0 + 15) & ~15);
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < OZ_KS; ++s) {
@@ -319,7 +322,7 @@ gram_oz_kernel(const __grid_constant__ OzParams P) {
     // stay in uniform registers); one elected lane issues the MMAs and commits
     if (nk > 0) {
       const uint32_t idesc = (2u << 4) | (1u << 7) | (1u << 10) |  // S32 acc, s8 A/B, K-major
-                             ((uint32_t)(OZ_N >> 3) << 17) | ((uint32_t)(OZ_M >> 4) << 24);
+                             ((uint32_t)(ntile >> 3) << 17) | ((uint32_t)(OZ_M >> 4) << 24);
       const uint64_t dA0 = oz_desc(s_u32(base), 128, OZ_S * 256);
       const uint64_t dB0 = oz_desc(s_u32(base + kOzA), 128, OZ_S * 256);
       for (int kc = 0; kc < nk; ++kc) {
@@ -360,7 +363,7 @@ gram_oz_kernel(const __grid_constant__ OzParams P) {
     const int row = m0 + quarter * 32 + lane;
     const int eA = row < J.p ? oz_exp(J.cmaxA[row]) : 0;
     double* out = J.part + (int64_t)blockIdx.y * J.p * J.q;
-    for (int c0 = 0; c0 < OZ_N; c0 += 16) {
+    for (int c0 = 0; c0 < ntile; c0 += 16) {
       double acc[16];
 #pragma unroll
       for (int i = 0; i < 16; ++i) acc[i] = 0.0;
@@ -587,9 +590,19 @@ int gram_oz(const float* U, int64_t ldu, int p, const float* V, int64_t ldv, int
   double* partial = (double*)(scr + ba + bb);
   const size_t partial_cap = (ws_bytes - ba - bb) / sizeof(double);
   OzOperand A, B;
-  SPB_TRY(oz_prepare(U, ldu, n, p, scr, &A, st));
-  if (U == V && ldu == ldv && p == q)  // U'U: one operand, packed once
+  if (U == V && ldu == ldv && p == q) {  // U'U: one operand, packed once
+    SPB_TRY(oz_prepare(U, ldu, n, p, scr, &A, st));
     return oz_gemm(A, A, partial, partial_cap, out, ldo, st);
+  }
+  if (p == q) {  // both operands in one column-maxima and one packing launch
+    const float* xs[2] = {U, V};
+    const int64_t ls[2] = {ldu, ldv};
+    void* ms[2] = {scr, scr + ba};
+    OzOperand ops[2];
+    SPB_TRY(oz_prepare_n(2, xs, ls, n, p, ms, ops, st));
+    return oz_gemm(ops[0], ops[1], partial, partial_cap, out, ldo, st);
+  }
+  SPB_TRY(oz_prepare(U, ldu, n, p, scr, &A, st));
   SPB_TRY(oz_prepare(V, ldv, n, q, scr + ba, &B, st));
   return oz_gemm(A, B, partial, partial_cap, out, ldo, st);
 }

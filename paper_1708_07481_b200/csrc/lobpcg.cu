@@ -281,9 +281,10 @@ struct Driver {
   // path: CholQR squares their error into the orthogonality of the block, and
   // the assignment step checks ||X'X - I|| <= 1e-6 (spectral.py:149-151).
   int gram1(const void* U, int p, const void* V, int q, double* out, int ldo) {
-    // wide blocks (C4's l = 176) on the int8 Ozaki path: 2M x 176 X'R 4.5 -> 2.7 ms, R'R
-    // (packed once) ~2 ms; at C3's 108 columns it is no faster than the FP64 tensor pipe
-    if (w.use_oz && p > 128 && q > 128) {
+    // blocks wider than one Ozaki column tile (C3's l = 108, C4's 176) on the int8 Ozaki
+    // path: 2M x 176 X'R 4.5 -> 2.7 ms, R'R (packed once) ~2 ms; C3 partition -3 ms with
+    // the 108-wide Grams as 96 + 16 column tiles
+    if (w.use_oz && p > 96 && q > 96) {
       SPB_TRY(gram_oz((const float*)U, w.ld, p, (const float*)V, w.ld, q, w.n, w.oz_ws, w.oz_ws_bytes,
                       out, ldo, st));
       return allreduce(out, (size_t)(p - 1) * ldo + q);

@@ -20,7 +20,11 @@ ap.add_argument("--m", type=int, nargs="+", default=[147])
 ap.add_argument("--nev", type=int, default=0)
 ap.add_argument("--gb", action="store_true", help="generalized problem (Cholesky of G_B)")
 ap.add_argument("--reps", type=int, default=10)
+ap.add_argument("--lib", default="")
 a = ap.parse_args()
+if a.lib:
+    from paper_1708_07481_b200 import _native as N
+    N.LIB_PATH = Path(a.lib)
 for m in a.m:
     rng = np.random.default_rng(0)
     x = rng.standard_normal((m, m))
