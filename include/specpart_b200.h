@@ -211,6 +211,10 @@ typedef struct {
 SPB_API int spb_comm_unique_id(void* out, int32_t bytes);
 SPB_API int spb_comm_init(int32_t nranks, int32_t rank, const void* unique_id, void** comm_out);
 SPB_API int spb_comm_destroy(void* comm);
+/* Drives the run-time NCCL binding with a one-rank communicator (unique id, init,
+ * float64 all-reduce, byte all-gather, destroy) and checks the data: the part of
+ * the multi-GPU plumbing a single-GPU box can execute. */
+SPB_API int spb_comm_selftest(void* stream);
 /* Host-transport communicator: the same sharded solver, with each collective
  * staged through host memory and performed by the caller's callbacks (e.g. a
  * torch.distributed gloo group). For testing the row-sharded code path with

@@ -85,6 +85,7 @@ _SIGS = {
     "spb_comm_unique_id": (C.c_int, [vp, i32]),
     "spb_comm_init": (C.c_int, [i32, i32, vp, C.POINTER(vp)]),
     "spb_comm_destroy": (C.c_int, [vp]),
+    "spb_comm_selftest": (C.c_int, [vp]),
     "spb_comm_init_host": (C.c_int, [i32, i32, ALLREDUCE_CB, ALLGATHER_CB, vp, C.POINTER(vp)]),
     "spb_csr_build_rows": (C.c_int, [vp, vp, vp, i64, i32, i32, i32, vp, i32, i32, vp, sz, vp, vp,
                                      vp, vp, C.POINTER(i64), vp]),

@@ -162,6 +162,52 @@ extern "C" int spb_comm_init_host(int32_t nranks, int32_t rank, spb_allreduce_cb
   return SPB_OK;
 }
 
+// One-rank NCCL communicator driven through the same resolved entry points the
+// sharded solver uses (unique id, init, float64 all-reduce, byte all-gather,
+// destroy). A single-GPU box cannot form a larger communicator, so this is the
+// check that the run-time NCCL binding itself works where the library is loaded.
+extern "C" int spb_comm_selftest(void* stream) {
+  cudaStream_t st = (cudaStream_t)stream;
+  if (!api().ok) {
+    set_error("libnccl.so.2 not available in this process");
+    return SPB_ERR_CUDA;
+  }
+  ncclUniqueId id;
+  ncclResult_t r = api().getUniqueId(&id);
+  if (r != ncclSuccess) return nccl_fail(r, "getUniqueId");
+  ncclComm_t nc = nullptr;
+  r = api().commInitRank(&nc, 1, id, 0);
+  if (r != ncclSuccess) return nccl_fail(r, "commInitRank");
+  constexpr int kN = 1024;
+  std::vector<double> h(kN), back(kN), gathered(kN);
+  for (int i = 0; i < kN; ++i) h[i] = 0.5 * i - 3.0;
+  double *d = nullptr, *g = nullptr;
+  int rc = SPB_OK;
+  auto body = [&]() -> int {
+    SPB_CUDA(cudaMalloc(&d, sizeof(double) * kN));
+    SPB_CUDA(cudaMalloc(&g, sizeof(double) * kN));
+    SPB_CUDA(cudaMemcpyAsync(d, h.data(), sizeof(double) * kN, cudaMemcpyHostToDevice, st));
+    r = api().allReduce(d, d, kN, ncclFloat64, ncclSum, nc, st);
+    if (r != ncclSuccess) return nccl_fail(r, "allreduce");
+    r = api().allGather(d, g, sizeof(double) * kN, ncclInt8, nc, st);
+    if (r != ncclSuccess) return nccl_fail(r, "allgather");
+    SPB_CUDA(cudaMemcpyAsync(back.data(), d, sizeof(double) * kN, cudaMemcpyDeviceToHost, st));
+    SPB_CUDA(cudaMemcpyAsync(gathered.data(), g, sizeof(double) * kN, cudaMemcpyDeviceToHost, st));
+    SPB_CUDA(cudaStreamSynchronize(st));
+    for (int i = 0; i < kN; ++i)
+      if (back[i] != h[i] || gathered[i] != h[i]) {
+        set_error("NCCL one-rank collectives returned wrong data at %d", i);
+        return SPB_ERR_CUDA;
+      }
+    return SPB_OK;
+  };
+  rc = body();
+  cudaFree(d);
+  cudaFree(g);
+  api().commDestroy(nc);
+  return rc;
+}
+
 extern "C" int spb_comm_destroy(void* comm) {
   Comm* c = (Comm*)comm;
   if (!c) return SPB_OK;

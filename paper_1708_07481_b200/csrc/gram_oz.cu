@@ -421,7 +421,17 @@ size_t oz_operand_bytes(int64_t n, int cols) {
   return (b + 1023) / 1024 * 1024;
 }
 
-// Column maxima and digit planes of X (n x cols, float32, row stride ldx) into mem.
+// Where an operand of n x cols lives inside mem (no launch).
+void oz_describe(int64_t n, int cols, void* mem, OzOperand* op) {
+  op->cols = cols;
+  op->n = n;
+  op->nkb = ceil_div(std::max<int64_t>(n, 1), OZ_KB);
+  op->ncg = (int)ceil_div(cols, 8);
+  op->plane_bytes = op->nkb * op->ncg * 256;
+  op->planes = (int8_t*)mem;
+  op->cmax = (unsigned*)(op->planes + OZ_S * op->plane_bytes);
+}
+
 // Column maxima and digit planes of nop (1 or 2) float32 operands X[i] (n x cols, row
 // stride ld[i]) into mem[i]: one colmax launch and one pack launch for both.
 int oz_prepare_n(int nop, const float* const* X, const int64_t* ld, int64_t n, int cols,
@@ -429,13 +439,7 @@ int oz_prepare_n(int nop, const float* const* X, const int64_t* ld, int64_t n, i
   OzSrc2 P2{};
   bool vec = true;
   for (int i = 0; i < nop; ++i) {
-    op[i].cols = cols;
-    op[i].n = n;
-    op[i].nkb = ceil_div(std::max<int64_t>(n, 1), OZ_KB);
-    op[i].ncg = (int)ceil_div(cols, 8);
-    op[i].plane_bytes = op[i].nkb * op[i].ncg * 256;
-    op[i].planes = (int8_t*)mem[i];
-    op[i].cmax = (unsigned*)(op[i].planes + OZ_S * op[i].plane_bytes);
+    oz_describe(n, cols, mem[i], &op[i]);
     SPB_CUDA(cudaMemsetAsync(op[i].cmax, 0, sizeof(unsigned) * (size_t)cols, st));
     P2.s[i] = {X[i], ld[i], op[i].cmax, op[i].planes};
     vec = vec && (reinterpret_cast<uintptr_t>(X[i]) & 15) == 0 && (ld[i] & 3) == 0;
@@ -491,6 +495,12 @@ size_t gram_oz_partial_doubles(int64_t n, int p, int q) {
   // the Rayleigh-Ritz launch runs two jobs (G_B upper tiles + G_A) in one grid
   int64_t ks = std::max(oz_splits(nkb, tiles), oz_splits(nkb, 2 * tiles));
   ks = std::max<int64_t>(ks, ceil_div(2 * num_sms(), tiles));
+  if (p == q) {  // G_B alone (upper tiles only) when the two Grams go out as two launches
+    int ut = 0;
+    for (int nt = 0; nt < (int)ceil_div(q, OZ_N); ++nt)
+      for (int mt = 0; mt < (int)ceil_div(p, OZ_M); ++mt) ut += (nt + 1) * OZ_N > mt * OZ_M;
+    ks = std::max(ks, oz_splits(nkb, ut));
+  }
   ks = std::min<int64_t>(ks + 16, nkb);
   return (size_t)std::max<int64_t>(ks, 1) * p * q;
 }
@@ -610,8 +620,11 @@ int gram_oz(const float* U, int64_t ldu, int p, const float* V, int64_t ldv, int
 // The Rayleigh-Ritz Grams of the solver: Gb = B'B (upper triangle valid, ld ldo) and
 // Ga = B'LB (ld ldo), B and LB n x cols (row stride ld), each operand packed once;
 // ws: gram_oz_ws_bytes(n, cols, cols) bytes of the solver's workspace.
+// phase 0: both Grams in one launch. phase 1: B packed and Gb only; phase 2 (after
+// phase 1 on the same ws): LB packed and Ga -- the caller factors Gb on another
+// stream while phase 2 runs (lobpcg.cu, rr_grams_body).
 int gram_oz_rr(const float* B, const float* LB, int64_t ld, int64_t n, int cols, double* Ga,
-               double* Gb, int ldo, void* ws, size_t ws_bytes, cudaStream_t st) {
+               double* Gb, int ldo, void* ws, size_t ws_bytes, cudaStream_t st, int phase) {
   const size_t bo = oz_operand_bytes(n, cols);
   if (ws_bytes < gram_oz_ws_bytes(n, cols, cols)) {
     set_error("Ozaki Gram workspace too small");
@@ -621,11 +634,18 @@ int gram_oz_rr(const float* B, const float* LB, int64_t ld, int64_t n, int cols,
   double* part = (double*)(scr + 2 * bo);
   const size_t pc = (ws_bytes - 2 * bo) / sizeof(double) / 2;
   OzOperand ops[2];
-  {
+  if (phase == 0) {
     const float* xs[2] = {B, LB};
     const int64_t ls[2] = {ld, ld};
     void* ms[2] = {scr, scr + bo};
     SPB_TRY(oz_prepare_n(2, xs, ls, n, cols, ms, ops, st));
+  } else if (phase == 1) {
+    SPB_TRY(oz_prepare(B, ld, n, cols, scr, &ops[0], st));
+    return oz_gemm(ops[0], ops[0], part, pc, Gb, ldo, st, true);
+  } else {
+    oz_describe(n, cols, scr, &ops[0]);  // packed by phase 1
+    SPB_TRY(oz_prepare(LB, ld, n, cols, scr + bo, &ops[1], st));
+    return oz_gemm(ops[0], ops[1], part + pc, pc, Ga, ldo, st, false);
   }
   const OzOperand& OB = ops[0];
   const OzOperand& OL = ops[1];

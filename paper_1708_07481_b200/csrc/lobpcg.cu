@@ -132,15 +132,17 @@ SolveWs carve(Arena& a, int dtype, int n, int l, int nranks = 1, int n_max = 0) 
 
 // Compact [G_A | G_B] (m x m each) from the padded Gram [B'B | B'LB] (pe x 2pe):
 // basis index b -> padded column X: b, R: lp + (b - l), P: 2 lp + (b - l - na).
+// which: bit 0 G_A, bit 1 G_B.
 __global__ void gather_pad_grams(const double* __restrict__ gp, int ldp, int pe, int m, int l,
-                                 int na, int lp, double* __restrict__ G, int ldg, int mmax) {
+                                 int na, int lp, double* __restrict__ G, int ldg, int mmax,
+                                 int which = 3) {
   for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < m * m; e += gridDim.x * blockDim.x) {
     const int i = e / m, j = e % m;
     const int pi = i < l ? i : (i < l + na ? lp + (i - l) : 2 * lp + (i - l - na));
     const int pj = j < l ? j : (j < l + na ? lp + (j - l) : 2 * lp + (j - l - na));
-    G[(size_t)i * ldg + j] = gp[(size_t)pi * ldp + pe + pj];         // G_A = B' LB
+    if (which & 1) G[(size_t)i * ldg + j] = gp[(size_t)pi * ldp + pe + pj];  // G_A = B' LB
     // G_B = B' B from its upper triangle (the Ozaki path computes only that)
-    G[(size_t)i * ldg + mmax + j] = gp[(size_t)min(pi, pj) * ldp + max(pi, pj)];
+    if (which & 2) G[(size_t)i * ldg + mmax + j] = gp[(size_t)min(pi, pj) * ldp + max(pi, pj)];
   }
 }
 
@@ -324,10 +326,33 @@ struct Driver {
       // [B'B | B'LB] over the padded basis from one packing of B and of LB, then
       // gather the m x m blocks (as the tcgen05 path below)
       const int pe = pw > 0 ? 2 * w.lp + pw : w.lp + na;
+      const int m = w.l + na + pw;
+      if (!comm || comm->nranks <= 1) {
+        // One GPU: G_B goes out first and its half of the small eigenproblem
+        // (symmetrise, Cholesky, inverse, cond bracket: a few SMs for ~0.6 ms at
+        // m = 324) runs on a side stream under the packing of LB and the G_A launch.
+        const int gg = (int)std::min<int64_t>(ceil_div((int64_t)m * m, 256), 1024);
+        SPB_TRY(drain_prefactor());
+        SPB_TRY(reset_status());
+        SPB_TRY(gram_oz_rr((const float*)w.B, (const float*)w.LB, w.ld, w.n, pe, w.Gpad + pe,
+                           w.Gpad, 2 * pe, w.oz_ws, w.oz_ws_bytes, st, 1));
+        gather_pad_grams<<<gg, 256, 0, st>>>(w.Gpad, 2 * pe, pe, m, w.l, na, w.lp, w.G,
+                                             2 * w.mmax, w.mmax, 2);
+        SPB_LAUNCH_CHECK();
+        SPB_TRY(sygv_prefactor_b(w.G + w.mmax, 2 * w.mmax, m, w.l, w.sygv_ws, w.sygv_cap, w.status,
+                                 st));
+        b_ready_m = m;
+        SPB_TRY(gram_oz_rr((const float*)w.B, (const float*)w.LB, w.ld, w.n, pe, w.Gpad + pe,
+                           w.Gpad, 2 * pe, w.oz_ws, w.oz_ws_bytes, st, 2));
+        gather_pad_grams<<<gg, 256, 0, st>>>(w.Gpad, 2 * pe, pe, m, w.l, na, w.lp, w.G,
+                                             2 * w.mmax, w.mmax, 1);
+        SPB_LAUNCH_CHECK();
+        tc_full_grams = true;
+        return SPB_OK;
+      }
       SPB_TRY(gram_oz_rr((const float*)w.B, (const float*)w.LB, w.ld, w.n, pe, w.Gpad + pe,
                          w.Gpad, 2 * pe, w.oz_ws, w.oz_ws_bytes, st));
       SPB_TRY(allreduce(w.Gpad, (size_t)pe * 2 * pe));
-      const int m = w.l + na + pw;
       gather_pad_grams<<<(int)std::min<int64_t>(ceil_div((int64_t)m * m, 256), 1024), 256, 0, st>>>(
           w.Gpad, 2 * pe, pe, m, w.l, na, w.lp, w.G, 2 * w.mmax, w.mmax);
       SPB_LAUNCH_CHECK();
@@ -375,6 +400,15 @@ struct Driver {
     SPB_TRY(gram_batched(w.dtype, b, w.n, m, w.mmax + m, w.gpart, w.gpart_cap, w.G, 2 * w.mmax,
                          st));
     return allreduce(w.G, (size_t)(m - 1) * 2 * w.mmax + w.mmax + m);
+  }
+
+  // m of the Rayleigh-Ritz problem whose G_B half is being factored on the side
+  // stream (rr_grams_body), -1 when none is pending.
+  int b_ready_m = -1;
+  int drain_prefactor() {
+    if (b_ready_m >= 0) SPB_TRY(sygv_prefactor_join(st));
+    b_ready_m = -1;
+    return SPB_OK;
   }
 
   int read_status(SmallStatus* h) {
@@ -566,10 +600,15 @@ struct Driver {
   int small_gen_eigh(int m, bool identity_b, int* ok, int seg1 = 1 << 30, int seg2 = 1 << 30) {
     stats[2]++;
     p_ill = false;
-    SPB_TRY(reset_status());
+    const bool pre = !identity_b && b_ready_m == m;  // G_B already factored (rr_grams_body)
+    if (pre) b_ready_m = -1;
+    else {
+      SPB_TRY(drain_prefactor());
+      SPB_TRY(reset_status());
+    }
     SPB_TRY(sygv_enqueue(w.G, identity_b ? nullptr : w.G + w.mmax, 2 * w.mmax, m, w.l,
                          w.theta_new, w.Cm, w.l, w.sygv_ws, w.sygv_cap, w.status, st, seg1,
-                         seg2));
+                         seg2, pre));
     SmallStatus hs;
     SPB_TRY(read_status(&hs));
     *ok = 0;
@@ -912,6 +951,7 @@ static int solve_impl(const spb_operator* op, const spb_shard* sh, int dtype, co
   }
   bool valid = false;
   int s = d.solve(x0, theta_out, norms_out, converged_out, &valid);
+  d.drain_prefactor();  // an error return may leave side-stream work on this workspace
   int sp = d.finish_profile();
   if (s == SPB_OK) s = sp;
   if (valid) {

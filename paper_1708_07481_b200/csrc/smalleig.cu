@@ -2755,6 +2755,7 @@ void launch_wy_apply(const double* V, int m, const double* Tscratch, double* Y, 
 struct SideStream {
   cudaStream_t s = nullptr;
   cudaEvent_t fork = nullptr, join = nullptr;
+  cudaEvent_t pre_fork = nullptr, pre_join = nullptr;  // sygv_prefactor_b
 };
 SideStream* side_stream() {
   static SideStream ss[16];
@@ -2765,6 +2766,8 @@ SideStream* side_stream() {
     cudaStreamCreateWithFlags(&x.s, cudaStreamNonBlocking);
     cudaEventCreateWithFlags(&x.fork, cudaEventDisableTiming);
     cudaEventCreateWithFlags(&x.join, cudaEventDisableTiming);
+    cudaEventCreateWithFlags(&x.pre_fork, cudaEventDisableTiming);
+    cudaEventCreateWithFlags(&x.pre_join, cudaEventDisableTiming);
   }
   return &x;
 }
@@ -3070,9 +3073,38 @@ int set_smem_attrs() {
 
 size_t sygv_ws_doubles(int m, int nev) { return sygv_ws_count(m, nev); }
 
+// B-side of sygv_enqueue ahead of time: sym(G_B), its Cholesky factor, inverse and
+// cond bracket, enqueued on the side stream behind everything already on st. The
+// caller keeps st busy (the G_A Gram) and then calls sygv_enqueue(..., b_ready =
+// true) with the same m, nev and workspace, which joins before it needs L^-1.
+int sygv_prefactor_b(const double* gb, int ldg, int m, int nev, double* ws, size_t ws_doubles,
+                     SmallStatus* status, cudaStream_t st, int seg1, int seg2) {
+  if (ws_doubles < sygv_ws_count(m, nev)) {
+    set_error("sygv workspace too small");
+    return SPB_ERR_WORKSPACE;
+  }
+  SPB_TRY(set_smem_attrs());
+  const SygvWs w = carve_sygv(ws, m, nev);
+  SideStream* side = side_stream();
+  SPB_CUDA(cudaEventRecord(side->pre_fork, st));
+  SPB_CUDA(cudaStreamWaitEvent(side->s, side->pre_fork, 0));
+  const int g1 = (int)std::min<int64_t>(ceil_div((int64_t)m * m, 256), 1024);
+  sym_prep<<<g1, 256, 0, side->s>>>(gb, nullptr, ldg, m, w.B, nullptr, status, seg1, seg2);
+  launch_chol(w.B, m, w.L, w.Linv, 0, status, side->s);
+  SPB_LAUNCH_CHECK();
+  SPB_CUDA(cudaEventRecord(side->pre_join, side->s));
+  return SPB_OK;
+}
+
+// st waits for the last sygv_prefactor_b (used when its result is not consumed).
+int sygv_prefactor_join(cudaStream_t st) {
+  SPB_CUDA(cudaStreamWaitEvent(st, side_stream()->pre_join, 0));
+  return SPB_OK;
+}
+
 int sygv_enqueue(const double* ga, const double* gb, int ldg, int m, int nev, double* theta,
                  double* C, int ldc, double* ws, size_t ws_doubles, SmallStatus* status,
-                 cudaStream_t st, int seg1, int seg2) {
+                 cudaStream_t st, int seg1, int seg2, bool b_ready) {
   if (ws_doubles < sygv_ws_count(m, nev)) {
     set_error("sygv workspace too small");
     return SPB_ERR_WORKSPACE;
@@ -3081,11 +3113,14 @@ int sygv_enqueue(const double* ga, const double* gb, int ldg, int m, int nev, do
   const SygvWs w = carve_sygv(ws, m, nev);
   const bool ident = (gb == nullptr);
   const int g1 = (int)std::min<int64_t>(ceil_div((int64_t)m * m, 256), 1024);
-  sym_prep<<<g1, 256, 0, st>>>(ga, gb, ldg, m, w.A, ident ? nullptr : w.B, status, seg1, seg2);
+  const bool pre = b_ready && !ident;
+  sym_prep<<<g1, 256, 0, st>>>(ga, pre ? nullptr : gb, ldg, m, w.A, ident || pre ? nullptr : w.B,
+                               status, seg1, seg2);
   SPB_LAUNCH_CHECK();
   const double* Atri = w.A;
   if (!ident) {
-    launch_chol(w.B, m, w.L, w.Linv, 0, status, st);
+    if (pre) SPB_TRY(sygv_prefactor_join(st));
+    else launch_chol(w.B, m, w.L, w.Linv, 0, status, st);
     SPB_LAUNCH_CHECK();
     launch_small_gemm(0, 0, m, m, m, w.Linv, m, w.A, m, w.M, m, st);
     launch_small_gemm(0, 1, m, m, m, w.M, m, w.Linv, m, w.Ap, m, st);

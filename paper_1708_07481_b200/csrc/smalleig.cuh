@@ -28,7 +28,14 @@ size_t sygv_ws_doubles(int m, int nev);
 // blocks of the Grams were computed (default: one block, full symmetrisation).
 int sygv_enqueue(const double* ga, const double* gb, int ldg, int m, int nev, double* theta,
                  double* C, int ldc, double* ws, size_t ws_doubles, SmallStatus* status,
-                 cudaStream_t st, int seg1 = 1 << 30, int seg2 = 1 << 30);
+                 cudaStream_t st, int seg1 = 1 << 30, int seg2 = 1 << 30, bool b_ready = false);
+// The G_B half of sygv_enqueue (symmetrise, Cholesky, inverse, cond bracket) on a
+// side stream ordered after st's current work; sygv_enqueue(..., b_ready = true)
+// with the same m / nev / ws then skips it and joins. sygv_prefactor_join makes st
+// wait for it when the result ends up unused.
+int sygv_prefactor_b(const double* gb, int ldg, int m, int nev, double* ws, size_t ws_doubles,
+                     SmallStatus* status, cudaStream_t st, int seg1 = 1 << 30, int seg2 = 1 << 30);
+int sygv_prefactor_join(cudaStream_t st);
 // Exact cond2 of the symmetrised G_B (tridiagonal + bisection for the extreme
 // eigenvalues), for the undecided case; writes host *cond.
 int exact_cond_spd(const double* gb, int ldg, int m, double* ws, size_t ws_doubles, double* cond,

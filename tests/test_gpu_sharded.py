@@ -30,6 +30,17 @@ def test_single_rank_sharded_equals_unsharded(precision):
     assert np.array_equal(a.labels, b.labels)
 
 
+def test_nccl_binding_one_rank_selftest():
+    """The run-time NCCL binding (comm.cu: unique id, commInitRank, float64 all-reduce,
+    byte all-gather, destroy) executed with a one-rank communicator -- the part of the
+    multi-GPU data plane a single-GPU box can run through NCCL itself."""
+    import torch  # noqa: F401  (loads the venv's libnccl.so.2 into the process)
+
+    from paper_1708_07481_b200 import _native as N
+
+    N.check(N.lib().spb_comm_selftest(N.stream()))
+
+
 def _free_port():
     import socket
 
