@@ -97,7 +97,7 @@ size_t gram_tc_partial_doubles(int64_t n, int p, int qtot);
 // Rayleigh-Ritz Grams on the int8 tensor cores with the Ozaki splitting (gram_oz.cu):
 // Gb = B'B and Ga = B'LB (ld ldo), float32 operands n x cols, float64-accurate.
 size_t gram_oz_ws_bytes(int64_t n, int p, int q);
-// phase 0: one launch for both; phase 1: B packed, Gb only; phase 2 (after 1): LB packed, Ga.
+// phase 0: one launch for both; 1: pack B, 2: Gb, 3: pack LB, 4: Ga (in this order).
 int gram_oz_rr(const float* B, const float* LB, int64_t ld, int64_t n, int cols, double* Ga,
                double* Gb, int ldo, void* ws, size_t ws_bytes, cudaStream_t st, int phase = 0);
 // out = U'V (p x q, ld ldo) through the Ozaki int8 path; U == V (p == q): packed once

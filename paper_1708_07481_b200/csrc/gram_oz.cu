@@ -620,9 +620,9 @@ int gram_oz(const float* U, int64_t ldu, int p, const float* V, int64_t ldv, int
 // The Rayleigh-Ritz Grams of the solver: Gb = B'B (upper triangle valid, ld ldo) and
 // Ga = B'LB (ld ldo), B and LB n x cols (row stride ld), each operand packed once;
 // ws: gram_oz_ws_bytes(n, cols, cols) bytes of the solver's workspace.
-// phase 0: both Grams in one launch. phase 1: B packed and Gb only; phase 2 (after
-// phase 1 on the same ws): LB packed and Ga -- the caller factors Gb on another
-// stream while phase 2 runs (lobpcg.cu, rr_grams_body).
+// phase 0: both Grams in one launch. Phases 1-4 split it for the caller's stream
+// overlap (lobpcg.cu, rr_grams_body), in this order on the same ws: 1 packs B, 2
+// launches Gb, 3 packs LB (may run beside 2 on another stream), 4 launches Ga.
 int gram_oz_rr(const float* B, const float* LB, int64_t ld, int64_t n, int cols, double* Ga,
                double* Gb, int ldo, void* ws, size_t ws_bytes, cudaStream_t st, int phase) {
   const size_t bo = oz_operand_bytes(n, cols);
@@ -639,12 +639,12 @@ int gram_oz_rr(const float* B, const float* LB, int64_t ld, int64_t n, int cols,
     const int64_t ls[2] = {ld, ld};
     void* ms[2] = {scr, scr + bo};
     SPB_TRY(oz_prepare_n(2, xs, ls, n, cols, ms, ops, st));
-  } else if (phase == 1) {
-    SPB_TRY(oz_prepare(B, ld, n, cols, scr, &ops[0], st));
-    return oz_gemm(ops[0], ops[0], part, pc, Gb, ldo, st, true);
   } else {
-    oz_describe(n, cols, scr, &ops[0]);  // packed by phase 1
-    SPB_TRY(oz_prepare(LB, ld, n, cols, scr + bo, &ops[1], st));
+    oz_describe(n, cols, scr, &ops[0]);
+    oz_describe(n, cols, scr + bo, &ops[1]);
+    if (phase == 1) return oz_prepare(B, ld, n, cols, scr, &ops[0], st);
+    if (phase == 2) return oz_gemm(ops[0], ops[0], part, pc, Gb, ldo, st, true);
+    if (phase == 3) return oz_prepare(LB, ld, n, cols, scr + bo, &ops[1], st);
     return oz_gemm(ops[0], ops[1], part + pc, pc, Ga, ldo, st, false);
   }
   const OzOperand& OB = ops[0];

@@ -334,16 +334,26 @@ struct Driver {
         const int gg = (int)std::min<int64_t>(ceil_div((int64_t)m * m, 256), 1024);
         SPB_TRY(drain_prefactor());
         SPB_TRY(reset_status());
-        SPB_TRY(gram_oz_rr((const float*)w.B, (const float*)w.LB, w.ld, w.n, pe, w.Gpad + pe,
-                           w.Gpad, 2 * pe, w.oz_ws, w.oz_ws_bytes, st, 1));
+        SPB_TRY(ensure_pack_stream());
+        auto oz = [&](int phase, cudaStream_t s) {
+          return gram_oz_rr((const float*)w.B, (const float*)w.LB, w.ld, w.n, pe, w.Gpad + pe,
+                            w.Gpad, 2 * pe, w.oz_ws, w.oz_ws_bytes, s, phase);
+        };
+        SPB_TRY(oz(1, st));  // pack B
+        // LB is packed (HBM-bound) on its own stream beside the G_B launch (tensor / L2)
+        SPB_CUDA(cudaEventRecord(pack_fork, st));
+        SPB_CUDA(cudaStreamWaitEvent(pack_st, pack_fork, 0));
+        SPB_TRY(oz(3, pack_st));
+        SPB_CUDA(cudaEventRecord(pack_join, pack_st));
+        SPB_TRY(oz(2, st));  // G_B
         gather_pad_grams<<<gg, 256, 0, st>>>(w.Gpad, 2 * pe, pe, m, w.l, na, w.lp, w.G,
                                              2 * w.mmax, w.mmax, 2);
         SPB_LAUNCH_CHECK();
         SPB_TRY(sygv_prefactor_b(w.G + w.mmax, 2 * w.mmax, m, w.l, w.sygv_ws, w.sygv_cap, w.status,
                                  st));
         b_ready_m = m;
-        SPB_TRY(gram_oz_rr((const float*)w.B, (const float*)w.LB, w.ld, w.n, pe, w.Gpad + pe,
-                           w.Gpad, 2 * pe, w.oz_ws, w.oz_ws_bytes, st, 2));
+        SPB_CUDA(cudaStreamWaitEvent(st, pack_join, 0));
+        SPB_TRY(oz(4, st));  // G_A
         gather_pad_grams<<<gg, 256, 0, st>>>(w.Gpad, 2 * pe, pe, m, w.l, na, w.lp, w.G,
                                              2 * w.mmax, w.mmax, 1);
         SPB_LAUNCH_CHECK();
@@ -405,6 +415,25 @@ struct Driver {
   // m of the Rayleigh-Ritz problem whose G_B half is being factored on the side
   // stream (rr_grams_body), -1 when none is pending.
   int b_ready_m = -1;
+  // stream on which LB is packed beside the G_B launch (created on first use,
+  // destroyed with the solve)
+  cudaStream_t pack_st = nullptr;
+  cudaEvent_t pack_fork = nullptr, pack_join = nullptr;
+  int ensure_pack_stream() {
+    if (pack_st) return SPB_OK;
+    SPB_CUDA(cudaStreamCreateWithFlags(&pack_st, cudaStreamNonBlocking));
+    SPB_CUDA(cudaEventCreateWithFlags(&pack_fork, cudaEventDisableTiming));
+    SPB_CUDA(cudaEventCreateWithFlags(&pack_join, cudaEventDisableTiming));
+    return SPB_OK;
+  }
+  void release_pack_stream() {
+    if (!pack_st) return;
+    cudaStreamWaitEvent(st, pack_join, 0);  // nothing of this solve outlives st's order
+    cudaEventDestroy(pack_fork);
+    cudaEventDestroy(pack_join);
+    cudaStreamDestroy(pack_st);  // the runtime frees it once its work has drained
+    pack_st = nullptr;
+  }
   int drain_prefactor() {
     if (b_ready_m >= 0) SPB_TRY(sygv_prefactor_join(st));
     b_ready_m = -1;
@@ -952,6 +981,7 @@ static int solve_impl(const spb_operator* op, const spb_shard* sh, int dtype, co
   bool valid = false;
   int s = d.solve(x0, theta_out, norms_out, converged_out, &valid);
   d.drain_prefactor();  // an error return may leave side-stream work on this workspace
+  d.release_pack_stream();
   int sp = d.finish_profile();
   if (s == SPB_OK) s = sp;
   if (valid) {
