@@ -797,8 +797,11 @@ struct Driver {
       SPB_TRY(cholesky_orth(w.R, na, &kept));
       na = kept;
       if (na == 0) break;
-      SPB_TRY(apply(w.R, na, w.LR));
+      // P and LP are normalised (and, with locked columns, compacted) on the packing
+      // stream while the main stream runs the SpMM: HBM-bound column passes beside a
+      // gather-bound kernel, independent of R / LR
       int pw = 0;
+      bool p_side = false;
       if (have_p) {
         std::vector<int> sel;
         std::vector<double> sc;
@@ -811,16 +814,25 @@ struct Driver {
         if (pw) {
           bool identity = pw == l;
           for (int j = 0; j < pw && identity; ++j) identity = sel[j] == j;
+          SPB_TRY(ensure_pack_stream());
+          SPB_CUDA(cudaEventRecord(pack_fork, st));  // after the R gather's use of w.idx
+          SPB_CUDA(cudaStreamWaitEvent(pack_st, pack_fork, 0));
           if (!identity) {
-            SPB_TRY(set_idx(sel));
-            SPB_TRY(gather_columns(w.dtype, w.P, w.ld, n, w.idx, pw, st));
-            SPB_TRY(gather_columns(w.dtype, w.LP, w.ld, n, w.idx, pw, st));
+            SPB_CUDA(cudaMemcpyAsync(w.idx, sel.data(), sizeof(int) * sel.size(),
+                                     cudaMemcpyHostToDevice, pack_st));
+            SPB_TRY(gather_columns(w.dtype, w.P, w.ld, n, w.idx, pw, pack_st));
+            SPB_TRY(gather_columns(w.dtype, w.LP, w.ld, n, w.idx, pw, pack_st));
           }
-          SPB_CUDA(cudaMemcpyAsync(w.pscale, sc.data(), sizeof(double) * pw, cudaMemcpyHostToDevice, st));
-          SPB_TRY(scale_columns(w.dtype, w.P, w.ld, n, w.pscale, pw, st));
-          SPB_TRY(scale_columns(w.dtype, w.LP, w.ld, n, w.pscale, pw, st));
+          SPB_CUDA(cudaMemcpyAsync(w.pscale, sc.data(), sizeof(double) * pw, cudaMemcpyHostToDevice,
+                                   pack_st));
+          SPB_TRY(scale_columns(w.dtype, w.P, w.ld, n, w.pscale, pw, pack_st));
+          SPB_TRY(scale_columns(w.dtype, w.LP, w.ld, n, w.pscale, pw, pack_st));
+          SPB_CUDA(cudaEventRecord(pack_join, pack_st));
+          p_side = true;
         }
       }
+      SPB_TRY(apply(w.R, na, w.LR));
+      if (p_side) SPB_CUDA(cudaStreamWaitEvent(st, pack_join, 0));
       // Rayleigh-Ritz ladder (lobpcg.py:397-429)
       bool solved = false;
       bool grams_ready = false;
