@@ -244,7 +244,8 @@ struct OzJob {
   const unsigned* cmaxA;
   const unsigned* cmaxB;
   int64_t planeA, planeB;  // bytes per plane
-  int ncgA, ncgB;          // column groups of the packed planes
+  int ncgA, ncgB;          // column groups of the operands
+  int strideA, strideB;    // column groups per k-block of the buffers they live in
   int p, q;                // output rows (A columns), columns (B columns)
   double* part;            // split-K partials, ks x p x q
 };
@@ -313,8 +314,8 @@ gram_oz_kernel(const __grid_constant__ OzParams P) {
         uint8_t* st = base + s * kOzStage;
         oz_mbar_expect(&full[s], bytesA + bytesB);
         const int64_t kb = kb0 + kc;
-        bulk_g2s(st, PA + (kb * J.ncgA + gA) * OZ_S * 256, bytesA, &full[s]);
-        bulk_g2s(st + kOzA, PB + (kb * J.ncgB + gB) * OZ_S * 256, bytesB, &full[s]);
+        bulk_g2s(st, PA + (kb * J.strideA + gA) * OZ_S * 256, bytesA, &full[s]);
+        bulk_g2s(st + kOzA, PB + (kb * J.strideB + gB) * OZ_S * 256, bytesB, &full[s]);
       }
     }
   } else if (warp == 1) {
@@ -411,6 +412,7 @@ struct OzOperand {
   int8_t* planes = nullptr;
   unsigned* cmax = nullptr;
   int cols = 0, ncg = 0;
+  int stride = 0;  // column groups per k-block of the buffer (== ncg unless a view)
   int64_t n = 0, nkb = 0, plane_bytes = 0;
 };
 
@@ -427,6 +429,7 @@ void oz_describe(int64_t n, int cols, void* mem, OzOperand* op) {
   op->n = n;
   op->nkb = ceil_div(std::max<int64_t>(n, 1), OZ_KB);
   op->ncg = (int)ceil_div(cols, 8);
+  op->stride = op->ncg;
   op->plane_bytes = op->nkb * op->ncg * 256;
   op->planes = (int8_t*)mem;
   op->cmax = (unsigned*)(op->planes + OZ_S * op->plane_bytes);
@@ -531,6 +534,8 @@ int oz_gemm_jobs(int njobs, const OzOperand* const* A, const OzOperand* const* B
     J.planeB = B[j]->plane_bytes;
     J.ncgA = A[j]->ncg;
     J.ncgB = B[j]->ncg;
+    J.strideA = A[j]->stride;
+    J.strideB = B[j]->stride;
     J.p = p;
     J.q = q;
     J.part = partial[j];
@@ -615,6 +620,35 @@ int gram_oz(const float* U, int64_t ldu, int p, const float* V, int64_t ldv, int
   SPB_TRY(oz_prepare(U, ldu, n, p, scr, &A, st));
   SPB_TRY(oz_prepare(V, ldv, n, q, scr + ba, &B, st));
   return oz_gemm(A, B, partial, partial_cap, out, ldo, st);
+}
+
+// Columns [col0, col0 + cols) of a packed operand (col0 a multiple of 8) as an
+// operand of their own: same planes, the parent's k-block stride.
+OzOperand oz_view(const OzOperand& W, int col0, int cols) {
+  OzOperand v = W;
+  v.planes = W.planes + (size_t)(col0 / 8) * OZ_S * 256;
+  v.cmax = W.cmax + col0;
+  v.cols = cols;
+  v.ncg = (int)ceil_div(cols, 8);
+  return v;
+}
+
+// out[(c1 + q) x q] (ld ldo) = W' W[:, c1 : c1 + q] for W = the first c1 + q columns of
+// a float32 block (row stride ld, c1 a multiple of 8), packed once: rows [0, c1) are
+// X'R and rows [c1, c1 + q) are R'R when W = [X | R] (lobpcg.cu, project_orth).
+int gram_oz_xr(const float* W, int64_t ld, int64_t n, int c1, int q, void* ws, size_t ws_bytes,
+               double* out, int ldo, cudaStream_t st) {
+  const int cols = c1 + q;
+  const size_t bw = oz_operand_bytes(n, cols);
+  if ((c1 & 7) || ws_bytes < bw + gram_oz_partial_doubles(n, cols, q) * sizeof(double)) {
+    set_error("Ozaki [X R]'R Gram: bad split or workspace too small");
+    return SPB_ERR_WORKSPACE;
+  }
+  uint8_t* scr = (uint8_t*)ws;
+  OzOperand Wop;
+  SPB_TRY(oz_prepare(W, ld, n, cols, scr, &Wop, st));
+  const OzOperand R = oz_view(Wop, c1, q);
+  return oz_gemm(Wop, R, (double*)(scr + bw), (ws_bytes - bw) / sizeof(double), out, ldo, st);
 }
 
 // The Rayleigh-Ritz Grams of the solver: Gb = B'B (upper triangle valid, ld ldo) and

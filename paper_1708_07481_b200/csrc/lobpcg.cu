@@ -146,6 +146,30 @@ __global__ void gather_pad_grams(const double* __restrict__ gp, int ldp, int pe,
   }
 }
 
+// Fused projection + CholQR (Driver::project_orth): from O = [X | R]'R (rows [0, l)
+// S = X'R, rows [lp, lp + na) T = R'R; ld ldo) the Gram of the projected block,
+// G = (R - X S)'(R - X S) = T - S'S for orthonormal X.
+__global__ void projected_gram(const double* __restrict__ O, int ldo, int l, int lp, int na,
+                               double* __restrict__ G, int ldg) {
+  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < na * na; e += gridDim.x * blockDim.x) {
+    const int i = e / na, j = e % na;
+    double s = 0.0;
+    for (int k = 0; k < l; ++k) s = fma(O[(size_t)k * ldo + i], O[(size_t)k * ldo + j], s);
+    G[(size_t)i * ldg + j] = O[(size_t)(lp + i) * ldo + j] - s;
+  }
+}
+// Cx = -S Rinv (l x na, ld ldc): the X coefficients of R <- (R - X S) Rinv.
+__global__ void projected_xcoef(const double* __restrict__ O, int ldo, int l, int na,
+                                const double* __restrict__ Rinv, int ldr, double* __restrict__ Cx,
+                                int ldc) {
+  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < l * na; e += gridDim.x * blockDim.x) {
+    const int k = e / na, j = e % na;
+    double s = 0.0;
+    for (int i = 0; i <= j; ++i) s = fma(O[(size_t)k * ldo + i], Rinv[(size_t)i * ldr + j], s);
+    Cx[(size_t)k * ldc + j] = -s;
+  }
+}
+
 struct Driver {
   bool tc_full_grams = false;  // last rr_grams computed every block (no upper-only mirror)
   const spb_shard* sh = nullptr;  // row-sharded solve (null: one GPU owns every row)
@@ -476,6 +500,48 @@ struct Driver {
     return block_update(w.dtype, p, w.n, st);
   }
 
+  // project_out_x (lobpcg.py:365-369) followed by _cholesky_orth (lobpcg.py:218-247)
+  // on R. On the Ozaki path both Grams come from ONE packing of [X | R] and one
+  // launch, O = [X | R]'R: S = X'R and T = R'R of the unprojected block; the Gram of
+  // the projected block is T - S'S (X orthonormal), and R <- (R - X S) Rinv is one
+  // update pass R Rinv + X (-S Rinv) instead of a projection pass and a CholQR pass.
+  // Anything but the accepted CholQR branch falls back to the two-step sequence.
+  int project_orth(int na, int* kept) {
+    const int l = w.l;
+    if (!(w.use_oz && l > 96 && na > 96)) {
+      SPB_TRY(project_out_x(na));
+      return cholesky_orth(w.R, na, kept);
+    }
+    double* O = w.Gpad;  // (lp + na) x na, free until the Rayleigh-Ritz Grams
+    SPB_TRY(gram_oz_xr((const float*)w.B, w.ld, w.n, w.lp, na, w.oz_ws, w.oz_ws_bytes, O, na, st));
+    SPB_TRY(allreduce(O, (size_t)(w.lp + na) * na));
+    projected_gram<<<(int)ceil_div((int64_t)na * na, 256), 256, 0, st>>>(O, na, l, w.lp, na, w.Gs,
+                                                                        w.lp);
+    SPB_LAUNCH_CHECK();
+    SPB_TRY(reset_status());
+    SPB_TRY(cholqr_enqueue(w.Gs, w.lp, na, w.coef, w.chol_ws, w.status, st));
+    // Cx into Gs (cholqr works on its own copy of the Gram); harmless if rejected
+    projected_xcoef<<<(int)ceil_div((int64_t)l * na, 256), 256, 0, st>>>(O, na, l, na, w.coef, na,
+                                                                        w.Gs, na);
+    SPB_LAUNCH_CHECK();
+    SmallStatus hs;
+    SPB_TRY(read_status(&hs));
+    if (hs.fallback || hs.nonfinite) {
+      SPB_TRY(project_out_x(na));
+      return cholesky_orth(w.R, na, kept);
+    }
+    UpdParams p{};
+    p.nseg = 2;
+    p.q = na;
+    p.seg[0] = {w.R, w.ld, w.coef, na, w.R, w.ld, 1.0, na, 0};
+    p.seg[1] = {w.X, w.ld, w.Gs, na, w.R, w.ld, 1.0, l, 1};
+    p.cstage = w.cstage;
+    p.cstage_cap = w.cstage_cap;
+    SPB_TRY(block_update(w.dtype, p, w.n, st));
+    *kept = na;
+    return SPB_OK;
+  }
+
   // _cholesky_orth (lobpcg.py:218-247) on the first na columns of B; *kept = width.
   int cholesky_orth(void* B, int na, int* kept) {
     if (na == 0) {
@@ -792,9 +858,8 @@ struct Driver {
       }
       if (cfg->has_precond) SPB_TRY(run_precond(na));
       if (cfg->deflate_ones) SPB_TRY(deflate(w.R, na));
-      SPB_TRY(project_out_x(na));
       int kept = 0;
-      SPB_TRY(cholesky_orth(w.R, na, &kept));
+      SPB_TRY(project_orth(na, &kept));
       na = kept;
       if (na == 0) break;
       // P and LP are normalised (and, with locked columns, compacted) on the packing
@@ -845,9 +910,8 @@ struct Driver {
           stats[4]++;
           SPB_TRY(orthonormalize(w.X, l));
           SPB_TRY(apply(w.X, l, w.LX));
-          SPB_TRY(project_out_x(na));
           int k2 = 0;
-          SPB_TRY(cholesky_orth(w.R, na, &k2));
+          SPB_TRY(project_orth(na, &k2));
           na = k2;
           if (na == 0) break;
           SPB_TRY(apply(w.R, na, w.LR));

@@ -80,16 +80,20 @@ def test_ozaki_int8_gram_accuracy(n, p, q):
     assert rel_err(u, v) < 1e-7
 
 
-def test_ozaki_rr_grams_track_dmma_in_the_solver():
+@pytest.mark.parametrize("n,blocks,arcs", [(60000, 20, 1_200_000), (40000, 98, 1_000_000)])
+def test_ozaki_rr_grams_track_dmma_in_the_solver(n, blocks, arcs):
     """The solver's Rayleigh-Ritz Grams on the Ozaki int8 path (default for C3/C4-sized
     bases) follow the float64 DMMA path: same iteration count, Ritz values within 1e-6
-    relative, residual histories within 0.01 in log10, labels agree."""
+    relative, residual histories within 0.01 in log10, labels agree. With 98 blocks
+    (l = 108 > one Ozaki column tile) the Ozaki run also takes the fused projection +
+    CholQR step ([X | R]'R from one packing, lobpcg.cu project_orth) and the split
+    G_B / G_A launches with the side-stream Cholesky, against the two-step float64 path."""
     import os
 
     import paper_1708_07481_b200 as spb
     from paper_1708_07481_b200.dcsbm import DcsbmSpec, generate_dcsbm
 
-    spec = DcsbmSpec(n=60000, blocks=20, arcs=1_200_000, alpha=3.0, ratio=5.0, seed=4)
+    spec = DcsbmSpec(n=n, blocks=blocks, arcs=arcs, alpha=3.0, ratio=5.0, seed=4)
     e, truth = generate_dcsbm(spec)
     g = spb.from_edges(e, spec.n)
     l = spb.block_size_for(spec.blocks)
