@@ -99,11 +99,14 @@ size_t gram_tc_partial_doubles(int64_t n, int p, int qtot);
 size_t gram_oz_ws_bytes(int64_t n, int p, int q);
 // phase 0: one launch for both; 1: pack B, 2: Gb, 3: pack LB, 4: Ga (in this order).
 int gram_oz_rr(const float* B, const float* LB, int64_t ld, int64_t n, int cols, double* Ga,
-               double* Gb, int ldo, void* ws, size_t ws_bytes, cudaStream_t st, int phase = 0);
+               double* Gb, int ldo, void* ws, size_t ws_bytes, cudaStream_t st, int phase = 0,
+               int keep_cols = 0);
 // out[(c1 + q) x q] = W' W[:, c1 : c1 + q], W = the first c1 + q columns (c1 % 8 == 0),
-// packed once; ws as for gram_oz(n, c1 + q, c1 + q).
+// packed once; ws as for gram_oz(n, c1 + q, c1 + q). rr_cols > 0: packed inside the
+// Rayleigh-Ritz B operand of rr_cols columns on the same ws, whose leading c1 columns
+// gram_oz_rr(phase 1, keep_cols = c1) then keeps.
 int gram_oz_xr(const float* W, int64_t ld, int64_t n, int c1, int q, void* ws, size_t ws_bytes,
-               double* out, int ldo, cudaStream_t st);
+               double* out, int ldo, cudaStream_t st, int rr_cols = 0);
 // out = U'V (p x q, ld ldo) through the Ozaki int8 path; U == V (p == q): packed once
 int gram_oz(const float* U, int64_t ldu, int p, const float* V, int64_t ldv, int q, int64_t n,
             void* ws, size_t ws_bytes, double* out, int ldo, cudaStream_t st);

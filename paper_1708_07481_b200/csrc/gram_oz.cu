@@ -187,7 +187,7 @@ __global__ void oz_colmax4(const OzSrc2 P2, int64_t n, int cols) {
 // bytes of each plane are packed in registers and stored as one 16-byte vector
 // (a warp's stores form contiguous 128-byte runs).
 __global__ void __launch_bounds__(256)
-oz_pack(const OzSrc2 P2, int64_t n, int cols, int ncg, int64_t nkb, int64_t plane_bytes) {
+oz_pack(const OzSrc2 P2, int64_t n, int cols, int ncg, int64_t nkb, int stride) {
   const float* __restrict__ X = P2.s[blockIdx.z].X;
   const int64_t ldx = P2.s[blockIdx.z].ldx;
   const unsigned* __restrict__ cmax = P2.s[blockIdx.z].cmax;
@@ -229,8 +229,8 @@ oz_pack(const OzSrc2 P2, int64_t n, int cols, int ncg, int64_t nkb, int64_t plan
         w[sd][i >> 2] |= (__float_as_uint(t) & 0xffu) << (8 * (i & 3));
       }
     }
-    const int64_t off = ((kb * ncg + (c >> 3)) * OZ_S * 2 + h) * 128 + (c & 7) * 16;
-    (void)plane_bytes;
+    // stride: column groups per k-block of the buffer (> ncg when packing a view)
+    const int64_t off = ((kb * stride + (c >> 3)) * OZ_S * 2 + h) * 128 + (c & 7) * 16;
 #pragma unroll
     for (int sd = 0; sd < OZ_S; ++sd)
       *reinterpret_cast<uint4*>(planes + off + sd * 256) = make_uint4(w[sd][0], w[sd][1], w[sd][2], w[sd][3]);
@@ -435,14 +435,27 @@ void oz_describe(int64_t n, int cols, void* mem, OzOperand* op) {
   op->cmax = (unsigned*)(op->planes + OZ_S * op->plane_bytes);
 }
 
-// Column maxima and digit planes of nop (1 or 2) float32 operands X[i] (n x cols, row
-// stride ld[i]) into mem[i]: one colmax launch and one pack launch for both.
-int oz_prepare_n(int nop, const float* const* X, const int64_t* ld, int64_t n, int cols,
-                 void* const* mem, OzOperand* op, cudaStream_t st) {
+// Columns [col0, col0 + cols) of a packed operand (col0 a multiple of 8) as an
+// operand of their own: same planes, the parent's k-block stride.
+OzOperand oz_view(const OzOperand& W, int col0, int cols) {
+  OzOperand v = W;
+  v.planes = W.planes + (size_t)(col0 / 8) * OZ_S * 256;
+  v.cmax = W.cmax + col0;
+  v.cols = cols;
+  v.ncg = (int)ceil_div(cols, 8);
+  return v;
+}
+
+// Column maxima and digit planes of nop (1 or 2) described operands (whole buffers
+// or views of the same shape: equal cols / ncg / stride) from the float32 blocks X[i]
+// (n x cols, row stride ld[i]): one colmax launch and one pack launch for all.
+int oz_fill_n(int nop, const float* const* X, const int64_t* ld, const OzOperand* op,
+              cudaStream_t st) {
   OzSrc2 P2{};
   bool vec = true;
+  const int64_t n = op[0].n;
+  const int cols = op[0].cols;
   for (int i = 0; i < nop; ++i) {
-    oz_describe(n, cols, mem[i], &op[i]);
     SPB_CUDA(cudaMemsetAsync(op[i].cmax, 0, sizeof(unsigned) * (size_t)cols, st));
     P2.s[i] = {X[i], ld[i], op[i].cmax, op[i].planes};
     vec = vec && (reinterpret_cast<uintptr_t>(X[i]) & 15) == 0 && (ld[i] & 3) == 0;
@@ -459,9 +472,16 @@ int oz_prepare_n(int nop, const float* const* X, const int64_t* ld, int64_t n, i
   }
   const int64_t t = op[0].nkb * 2 * op[0].ncg * 8;
   oz_pack<<<dim3((unsigned)std::min<int64_t>(ceil_div(t, 256), 16 * num_sms()), 1, (unsigned)nop), 256,
-            0, st>>>(P2, n, cols, op[0].ncg, op[0].nkb, op[0].plane_bytes);
+            0, st>>>(P2, n, cols, op[0].ncg, op[0].nkb, op[0].stride);
   SPB_LAUNCH_CHECK();
   return SPB_OK;
+}
+
+// The same for whole operands laid out in mem[i].
+int oz_prepare_n(int nop, const float* const* X, const int64_t* ld, int64_t n, int cols,
+                 void* const* mem, OzOperand* op, cudaStream_t st) {
+  for (int i = 0; i < nop; ++i) oz_describe(n, cols, mem[i], &op[i]);
+  return oz_fill_n(nop, X, ld, op, st);
 }
 
 int oz_prepare(const float* X, int64_t ldx, int64_t n, int cols, void* mem, OzOperand* op,
@@ -622,33 +642,39 @@ int gram_oz(const float* U, int64_t ldu, int p, const float* V, int64_t ldv, int
   return oz_gemm(A, B, partial, partial_cap, out, ldo, st);
 }
 
-// Columns [col0, col0 + cols) of a packed operand (col0 a multiple of 8) as an
-// operand of their own: same planes, the parent's k-block stride.
-OzOperand oz_view(const OzOperand& W, int col0, int cols) {
-  OzOperand v = W;
-  v.planes = W.planes + (size_t)(col0 / 8) * OZ_S * 256;
-  v.cmax = W.cmax + col0;
-  v.cols = cols;
-  v.ncg = (int)ceil_div(cols, 8);
-  return v;
-}
-
 // out[(c1 + q) x q] (ld ldo) = W' W[:, c1 : c1 + q] for W = the first c1 + q columns of
 // a float32 block (row stride ld, c1 a multiple of 8), packed once: rows [0, c1) are
 // X'R and rows [c1, c1 + q) are R'R when W = [X | R] (lobpcg.cu, project_orth).
+// rr_cols > 0: W is packed in place inside the Rayleigh-Ritz B operand of rr_cols
+// columns that gram_oz_rr will use on the same ws (its k-block stride), so the planes
+// and column scales of the leading c1 columns (X) are already there for it
+// (gram_oz_rr's keep_cols).
 int gram_oz_xr(const float* W, int64_t ld, int64_t n, int c1, int q, void* ws, size_t ws_bytes,
-               double* out, int ldo, cudaStream_t st) {
+               double* out, int ldo, cudaStream_t st, int rr_cols) {
   const int cols = c1 + q;
-  const size_t bw = oz_operand_bytes(n, cols);
-  if ((c1 & 7) || ws_bytes < bw + gram_oz_partial_doubles(n, cols, q) * sizeof(double)) {
+  uint8_t* scr = (uint8_t*)ws;
+  OzOperand Wop;
+  size_t poff;  // split-K partials behind the operand area
+  if (rr_cols > 0) {
+    if (rr_cols < cols || ws_bytes < gram_oz_ws_bytes(n, rr_cols, rr_cols)) {
+      set_error("Ozaki [X R]'R Gram: Rayleigh-Ritz operand narrower than [X R]");
+      return SPB_ERR_CONTRACT;
+    }
+    OzOperand RR;
+    oz_describe(n, rr_cols, scr, &RR);
+    Wop = oz_view(RR, 0, cols);
+    poff = 2 * oz_operand_bytes(n, rr_cols);
+  } else {
+    oz_describe(n, cols, scr, &Wop);
+    poff = oz_operand_bytes(n, cols);
+  }
+  if ((c1 & 7) || ws_bytes < poff + gram_oz_partial_doubles(n, cols, q) * sizeof(double)) {
     set_error("Ozaki [X R]'R Gram: bad split or workspace too small");
     return SPB_ERR_WORKSPACE;
   }
-  uint8_t* scr = (uint8_t*)ws;
-  OzOperand Wop;
-  SPB_TRY(oz_prepare(W, ld, n, cols, scr, &Wop, st));
+  SPB_TRY(oz_fill_n(1, &W, &ld, &Wop, st));
   const OzOperand R = oz_view(Wop, c1, q);
-  return oz_gemm(Wop, R, (double*)(scr + bw), (ws_bytes - bw) / sizeof(double), out, ldo, st);
+  return oz_gemm(Wop, R, (double*)(scr + poff), (ws_bytes - poff) / sizeof(double), out, ldo, st);
 }
 
 // The Rayleigh-Ritz Grams of the solver: Gb = B'B (upper triangle valid, ld ldo) and
@@ -657,8 +683,11 @@ int gram_oz_xr(const float* W, int64_t ld, int64_t n, int c1, int q, void* ws, s
 // phase 0: both Grams in one launch. Phases 1-4 split it for the caller's stream
 // overlap (lobpcg.cu, rr_grams_body), in this order on the same ws: 1 packs B, 2
 // launches Gb, 3 packs LB (may run beside 2 on another stream), 4 launches Ga.
+// keep_cols (phase 1; a multiple of 8): the leading keep_cols columns of B were packed
+// into this operand by gram_oz_xr(..., rr_cols = cols) and are unchanged since.
 int gram_oz_rr(const float* B, const float* LB, int64_t ld, int64_t n, int cols, double* Ga,
-               double* Gb, int ldo, void* ws, size_t ws_bytes, cudaStream_t st, int phase) {
+               double* Gb, int ldo, void* ws, size_t ws_bytes, cudaStream_t st, int phase,
+               int keep_cols) {
   const size_t bo = oz_operand_bytes(n, cols);
   if (ws_bytes < gram_oz_ws_bytes(n, cols, cols)) {
     set_error("Ozaki Gram workspace too small");
@@ -676,7 +705,13 @@ int gram_oz_rr(const float* B, const float* LB, int64_t ld, int64_t n, int cols,
   } else {
     oz_describe(n, cols, scr, &ops[0]);
     oz_describe(n, cols, scr + bo, &ops[1]);
-    if (phase == 1) return oz_prepare(B, ld, n, cols, scr, &ops[0], st);
+    if (phase == 1) {
+      if (keep_cols <= 0 || keep_cols >= cols || (keep_cols & 7))
+        return oz_prepare(B, ld, n, cols, scr, &ops[0], st);
+      const OzOperand rest = oz_view(ops[0], keep_cols, cols - keep_cols);
+      const float* src = B + keep_cols;
+      return oz_fill_n(1, &src, &ld, &rest, st);
+    }
     if (phase == 2) return oz_gemm(ops[0], ops[0], part, pc, Gb, ldo, st, true);
     if (phase == 3) return oz_prepare(LB, ld, n, cols, scr + bo, &ops[1], st);
     return oz_gemm(ops[0], ops[1], part + pc, pc, Ga, ldo, st, false);

@@ -359,9 +359,13 @@ struct Driver {
         SPB_TRY(drain_prefactor());
         SPB_TRY(reset_status());
         SPB_TRY(ensure_pack_stream());
+        // X's digit planes are already in the B operand when project_orth packed
+        // [X | R] inside it for this width and X has not changed since
+        const int keep = x_planes_pe == pe ? w.lp : 0;
+        x_planes_pe = -1;
         auto oz = [&](int phase, cudaStream_t s) {
           return gram_oz_rr((const float*)w.B, (const float*)w.LB, w.ld, w.n, pe, w.Gpad + pe,
-                            w.Gpad, 2 * pe, w.oz_ws, w.oz_ws_bytes, s, phase);
+                            w.Gpad, 2 * pe, w.oz_ws, w.oz_ws_bytes, s, phase, keep);
         };
         SPB_TRY(oz(1, st));  // pack B
         // LB is packed (HBM-bound) on its own stream beside the G_B launch (tensor / L2)
@@ -506,14 +510,20 @@ struct Driver {
   // the projected block is T - S'S (X orthonormal), and R <- (R - X S) Rinv is one
   // update pass R Rinv + X (-S Rinv) instead of a projection pass and a CholQR pass.
   // Anything but the accepted CholQR branch falls back to the two-step sequence.
-  int project_orth(int na, int* kept) {
+  // rr_cols > 0: the width of the Rayleigh-Ritz basis that follows; [X | R] is then
+  // packed inside that operand and rr_grams_body keeps the digit planes of X.
+  int x_planes_pe = -1;  // RR width whose B operand already holds X's planes
+  int project_orth(int na, int* kept, int rr_cols = 0) {
     const int l = w.l;
+    x_planes_pe = -1;
+    if (comm && comm->nranks > 1) rr_cols = 0;  // the sharded RR Grams go out as one launch
     if (!(w.use_oz && l > 96 && na > 96)) {
       SPB_TRY(project_out_x(na));
       return cholesky_orth(w.R, na, kept);
     }
     double* O = w.Gpad;  // (lp + na) x na, free until the Rayleigh-Ritz Grams
-    SPB_TRY(gram_oz_xr((const float*)w.B, w.ld, w.n, w.lp, na, w.oz_ws, w.oz_ws_bytes, O, na, st));
+    SPB_TRY(gram_oz_xr((const float*)w.B, w.ld, w.n, w.lp, na, w.oz_ws, w.oz_ws_bytes, O, na, st,
+                       rr_cols));
     SPB_TRY(allreduce(O, (size_t)(w.lp + na) * na));
     projected_gram<<<(int)ceil_div((int64_t)na * na, 256), 256, 0, st>>>(O, na, l, w.lp, na, w.Gs,
                                                                         w.lp);
@@ -539,6 +549,7 @@ struct Driver {
     p.cstage_cap = w.cstage_cap;
     SPB_TRY(block_update(w.dtype, p, w.n, st));
     *kept = na;
+    if (rr_cols > 0) x_planes_pe = rr_cols;
     return SPB_OK;
   }
 
@@ -858,43 +869,43 @@ struct Driver {
       }
       if (cfg->has_precond) SPB_TRY(run_precond(na));
       if (cfg->deflate_ones) SPB_TRY(deflate(w.R, na));
-      int kept = 0;
-      SPB_TRY(project_orth(na, &kept));
-      na = kept;
-      if (na == 0) break;
-      // P and LP are normalised (and, with locked columns, compacted) on the packing
-      // stream while the main stream runs the SpMM: HBM-bound column passes beside a
-      // gather-bound kernel, independent of R / LR
+      // columns of P that enter the basis (known from the norms read above)
       int pw = 0;
-      bool p_side = false;
-      if (have_p) {
-        std::vector<int> sel;
-        std::vector<double> sc;
+      std::vector<int> sel;
+      std::vector<double> sc;
+      if (have_p)
         for (int j : idx)
           if (pn[j] > 0.0) {
             sel.push_back(j);
             sc.push_back(1.0 / pn[j]);
           }
-        pw = (int)sel.size();
-        if (pw) {
-          bool identity = pw == l;
-          for (int j = 0; j < pw && identity; ++j) identity = sel[j] == j;
-          SPB_TRY(ensure_pack_stream());
-          SPB_CUDA(cudaEventRecord(pack_fork, st));  // after the R gather's use of w.idx
-          SPB_CUDA(cudaStreamWaitEvent(pack_st, pack_fork, 0));
-          if (!identity) {
-            SPB_CUDA(cudaMemcpyAsync(w.idx, sel.data(), sizeof(int) * sel.size(),
-                                     cudaMemcpyHostToDevice, pack_st));
-            SPB_TRY(gather_columns(w.dtype, w.P, w.ld, n, w.idx, pw, pack_st));
-            SPB_TRY(gather_columns(w.dtype, w.LP, w.ld, n, w.idx, pw, pack_st));
-          }
-          SPB_CUDA(cudaMemcpyAsync(w.pscale, sc.data(), sizeof(double) * pw, cudaMemcpyHostToDevice,
-                                   pack_st));
-          SPB_TRY(scale_columns(w.dtype, w.P, w.ld, n, w.pscale, pw, pack_st));
-          SPB_TRY(scale_columns(w.dtype, w.LP, w.ld, n, w.pscale, pw, pack_st));
-          SPB_CUDA(cudaEventRecord(pack_join, pack_st));
-          p_side = true;
+      pw = (int)sel.size();
+      int kept = 0;
+      SPB_TRY(project_orth(na, &kept, pw > 0 ? 2 * w.lp + pw : w.lp + na));
+      na = kept;
+      if (na == 0) break;
+      // P and LP are normalised (and, with locked columns, compacted) on the packing
+      // stream while the main stream runs the SpMM: HBM-bound column passes beside a
+      // gather-bound kernel, independent of R / LR
+      bool p_side = false;
+      if (pw) {
+        bool identity = pw == l;
+        for (int j = 0; j < pw && identity; ++j) identity = sel[j] == j;
+        SPB_TRY(ensure_pack_stream());
+        SPB_CUDA(cudaEventRecord(pack_fork, st));  // after the R gather's use of w.idx
+        SPB_CUDA(cudaStreamWaitEvent(pack_st, pack_fork, 0));
+        if (!identity) {
+          SPB_CUDA(cudaMemcpyAsync(w.idx, sel.data(), sizeof(int) * sel.size(),
+                                   cudaMemcpyHostToDevice, pack_st));
+          SPB_TRY(gather_columns(w.dtype, w.P, w.ld, n, w.idx, pw, pack_st));
+          SPB_TRY(gather_columns(w.dtype, w.LP, w.ld, n, w.idx, pw, pack_st));
         }
+        SPB_CUDA(cudaMemcpyAsync(w.pscale, sc.data(), sizeof(double) * pw, cudaMemcpyHostToDevice,
+                                 pack_st));
+        SPB_TRY(scale_columns(w.dtype, w.P, w.ld, n, w.pscale, pw, pack_st));
+        SPB_TRY(scale_columns(w.dtype, w.LP, w.ld, n, w.pscale, pw, pack_st));
+        SPB_CUDA(cudaEventRecord(pack_join, pack_st));
+        p_side = true;
       }
       SPB_TRY(apply(w.R, na, w.LR));
       if (p_side) SPB_CUDA(cudaStreamWaitEvent(st, pack_join, 0));
