@@ -153,9 +153,22 @@ __global__ void projected_gram(const double* __restrict__ O, int ldo, int l, int
                                double* __restrict__ G, int ldg) {
   for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < na * na; e += gridDim.x * blockDim.x) {
     const int i = e / na, j = e % na;
-    double s = 0.0;
-    for (int k = 0; k < l; ++k) s = fma(O[(size_t)k * ldo + i], O[(size_t)k * ldo + j], s);
-    G[(size_t)i * ldg + j] = O[(size_t)(lp + i) * ldo + j] - s;
+    // four independent chains: the loads of a batch are issued together (the loop is
+    // load-latency-bound; same summation order for (i, j) and (j, i))
+    double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+    int k = 0;
+    for (; k + 4 <= l; k += 4) {
+      const double a0 = O[(size_t)k * ldo + i], b0 = O[(size_t)k * ldo + j];
+      const double a1 = O[(size_t)(k + 1) * ldo + i], b1 = O[(size_t)(k + 1) * ldo + j];
+      const double a2 = O[(size_t)(k + 2) * ldo + i], b2 = O[(size_t)(k + 2) * ldo + j];
+      const double a3 = O[(size_t)(k + 3) * ldo + i], b3 = O[(size_t)(k + 3) * ldo + j];
+      s0 = fma(a0, b0, s0);
+      s1 = fma(a1, b1, s1);
+      s2 = fma(a2, b2, s2);
+      s3 = fma(a3, b3, s3);
+    }
+    for (; k < l; ++k) s0 = fma(O[(size_t)k * ldo + i], O[(size_t)k * ldo + j], s0);
+    G[(size_t)i * ldg + j] = O[(size_t)(lp + i) * ldo + j] - ((s0 + s1) + (s2 + s3));
   }
 }
 // Cx = -S Rinv (l x na, ld ldc): the X coefficients of R <- (R - X S) Rinv.
@@ -164,9 +177,20 @@ __global__ void projected_xcoef(const double* __restrict__ O, int ldo, int l, in
                                 int ldc) {
   for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < l * na; e += gridDim.x * blockDim.x) {
     const int k = e / na, j = e % na;
-    double s = 0.0;
-    for (int i = 0; i <= j; ++i) s = fma(O[(size_t)k * ldo + i], Rinv[(size_t)i * ldr + j], s);
-    Cx[(size_t)k * ldc + j] = -s;
+    double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+    int i = 0;
+    for (; i + 3 <= j; i += 4) {  // Rinv is upper triangular: rows 0..j
+      const double a0 = O[(size_t)k * ldo + i], b0 = Rinv[(size_t)i * ldr + j];
+      const double a1 = O[(size_t)k * ldo + i + 1], b1 = Rinv[(size_t)(i + 1) * ldr + j];
+      const double a2 = O[(size_t)k * ldo + i + 2], b2 = Rinv[(size_t)(i + 2) * ldr + j];
+      const double a3 = O[(size_t)k * ldo + i + 3], b3 = Rinv[(size_t)(i + 3) * ldr + j];
+      s0 = fma(a0, b0, s0);
+      s1 = fma(a1, b1, s1);
+      s2 = fma(a2, b2, s2);
+      s3 = fma(a3, b3, s3);
+    }
+    for (; i <= j; ++i) s0 = fma(O[(size_t)k * ldo + i], Rinv[(size_t)i * ldr + j], s0);
+    Cx[(size_t)k * ldc + j] = -((s0 + s1) + (s2 + s3));
   }
 }
 
