@@ -149,8 +149,11 @@ __global__ void gather_pad_grams(const double* __restrict__ gp, int ldp, int pe,
 // Fused projection + CholQR (Driver::project_orth): from O = [X | R]'R (rows [0, l)
 // S = X'R, rows [lp, lp + na) T = R'R; ld ldo) the Gram of the projected block,
 // G = (R - X S)'(R - X S) = T - S'S for orthonormal X.
+// A column of R with more than 1 % of its energy inside span(X) (a preconditioned
+// residual, for instance) would lose digits in the subtraction: status->fallback is
+// raised and the caller takes the two-step sequence.
 __global__ void projected_gram(const double* __restrict__ O, int ldo, int l, int lp, int na,
-                               double* __restrict__ G, int ldg) {
+                               double* __restrict__ G, int ldg, SmallStatus* status) {
   for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < na * na; e += gridDim.x * blockDim.x) {
     const int i = e / na, j = e % na;
     // four independent chains: the loads of a batch are issued together (the loop is
@@ -168,7 +171,9 @@ __global__ void projected_gram(const double* __restrict__ O, int ldo, int l, int
       s3 = fma(a3, b3, s3);
     }
     for (; k < l; ++k) s0 = fma(O[(size_t)k * ldo + i], O[(size_t)k * ldo + j], s0);
-    G[(size_t)i * ldg + j] = O[(size_t)(lp + i) * ldo + j] - ((s0 + s1) + (s2 + s3));
+    const double ss = (s0 + s1) + (s2 + s3), t = O[(size_t)(lp + i) * ldo + j];
+    G[(size_t)i * ldg + j] = t - ss;
+    if (i == j && !(ss <= 0.01 * t)) atomicOr(&status->fallback, 1);
   }
 }
 // Cx = -S Rinv (l x na, ld ldc): the X coefficients of R <- (R - X S) Rinv.
@@ -541,6 +546,10 @@ struct Driver {
     const int l = w.l;
     x_planes_pe = -1;
     if (comm && comm->nranks > 1) rr_cols = 0;  // the sharded RR Grams go out as one launch
+    // The float64-product (DMMA) path of the small configs keeps the two-step
+    // sequence: fused there, C2 gained 3 % (25.9 -> 25.1 ms) but the stagnating C5
+    // warm-start stream (stop decisions at round-off level, tests/test_gpu_large.py)
+    // ended on a partition 0.89 in agreement with the reference's instead of 0.9997.
     if (!(w.use_oz && l > 96 && na > 96)) {
       SPB_TRY(project_out_x(na));
       return cholesky_orth(w.R, na, kept);
@@ -549,10 +558,10 @@ struct Driver {
     SPB_TRY(gram_oz_xr((const float*)w.B, w.ld, w.n, w.lp, na, w.oz_ws, w.oz_ws_bytes, O, na, st,
                        rr_cols));
     SPB_TRY(allreduce(O, (size_t)(w.lp + na) * na));
-    projected_gram<<<(int)ceil_div((int64_t)na * na, 256), 256, 0, st>>>(O, na, l, w.lp, na, w.Gs,
-                                                                        w.lp);
-    SPB_LAUNCH_CHECK();
     SPB_TRY(reset_status());
+    projected_gram<<<(int)ceil_div((int64_t)na * na, 256), 256, 0, st>>>(O, na, l, w.lp, na, w.Gs,
+                                                                        w.lp, w.status);
+    SPB_LAUNCH_CHECK();
     SPB_TRY(cholqr_enqueue(w.Gs, w.lp, na, w.coef, w.chol_ws, w.status, st));
     // Cx into Gs (cholqr works on its own copy of the Gram); harmless if rejected
     projected_xcoef<<<(int)ceil_div((int64_t)l * na, 256), 256, 0, st>>>(O, na, l, na, w.coef, na,

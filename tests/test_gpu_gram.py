@@ -149,3 +149,42 @@ def test_ozaki_self_gram_packs_once(n, p):
     assert (np.abs(g - exact) / scale).max() < 1e-9
     two = _gram(u, u, 2)  # separate operand copies: the two-operand path
     assert (np.abs(g - two) / scale).max() < 1e-9
+
+
+def test_fused_projection_guard_with_preconditioner():
+    """A preconditioned residual has a large component inside span(X): the fused
+    projection + CholQR of the Ozaki path (lobpcg.cu project_orth) must hand such
+    blocks to the two-step sequence (energy guard in projected_gram), so a Jacobi-
+    preconditioned float32 solve with l = 108 follows the float64-product path."""
+    import os
+
+    import paper_1708_07481_b200 as spb
+    from paper_1708_07481_b200.dcsbm import DcsbmSpec, generate_dcsbm
+
+    spec = DcsbmSpec(n=30000, blocks=98, arcs=750_000, alpha=3.0, ratio=5.0, seed=6)
+    e, _ = generate_dcsbm(spec)
+    g = spb.from_edges(e, spec.n)
+    d = np.maximum(spb.degrees(g), 1.0)
+    l = spb.block_size_for(spec.blocks)
+    x0 = np.random.default_rng(6).standard_normal((spec.n, l))
+    cfg = spb.SolverConfig(block_size=l, tol=1e-12, max_iter=8, seed=6)
+    out = {}
+    old = os.environ.get("SPB_GRAM")
+    try:
+        for mode in ("dmma", "oz"):
+            os.environ["SPB_GRAM"] = mode
+            hist = []
+            st = spb.lobpcg_solve(spb.LaplacianOperator(g), x0, cfg, precond=lambda r: r / d[:, None],
+                                  precision="float32",
+                                  callback=lambda it, th, nr: hist.append(nr[:spec.blocks].max()))
+            out[mode] = (st, np.array(hist))
+    finally:
+        if old is None:
+            os.environ.pop("SPB_GRAM", None)
+        else:
+            os.environ["SPB_GRAM"] = old
+    (sa, ha), (sb, hb) = out["dmma"], out["oz"]
+    assert sa.iterations == sb.iterations
+    rel = np.abs(sa.eigenvalues - sb.eigenvalues) / np.maximum(np.abs(sa.eigenvalues), 1e-6 * sa.eigenvalues.max())
+    assert rel.max() < 1e-5, rel.max()
+    assert np.abs(np.log10(ha) - np.log10(hb)).max() < 0.01
