@@ -496,14 +496,17 @@ int oz_prepare(const float* X, int64_t ldx, int64_t n, int cols, void* mem, OzOp
 // OZ_MAXROWS rows per split (exact int32 sums), at least two CTAs per SM, and
 // among the next few candidates the one with the fewest idle CTA slots in the
 // last wave (one CTA per SM).
-int64_t oz_splits(int64_t nkb, int tiles) {
-  const int64_t lo = std::max<int64_t>(ceil_div(2 * num_sms(), tiles), ceil_div(nkb, OZ_MAXROWS / OZ_KB));
+// sms: the SMs the launch can count on (fewer than the device's when a cluster kernel
+// runs beside it on another stream).
+int64_t oz_splits(int64_t nkb, int tiles, int sms = 0) {
+  if (sms <= 0) sms = num_sms();
+  const int64_t lo = std::max<int64_t>(ceil_div(2 * sms, tiles), ceil_div(nkb, OZ_MAXROWS / OZ_KB));
   int64_t best = std::min<int64_t>(lo, nkb);
   double best_eff = 0.0;
   for (int64_t ks = best; ks <= std::min<int64_t>(nkb, lo + 16); ++ks) {
     const int64_t kb = ceil_div(nkb, ks), kse = ceil_div(nkb, kb);  // effective splits
     const int64_t units = (int64_t)tiles * kse;
-    const double eff = (double)units / (double)(ceil_div(units, num_sms()) * num_sms());
+    const double eff = (double)units / (double)(ceil_div(units, sms) * sms);
     if (eff > best_eff + 1e-9) {
       best_eff = eff;
       best = ks;
@@ -533,7 +536,7 @@ size_t gram_oz_partial_doubles(int64_t n, int p, int q) {
 // reaching the diagonal are computed. partial: per job gram_oz_partial_doubles.
 int oz_gemm_jobs(int njobs, const OzOperand* const* A, const OzOperand* const* B, const bool* upper,
                  double* const* partial, size_t partial_cap, double* const* out, int ldo,
-                 cudaStream_t st) {
+                 cudaStream_t st, int sms = 0) {
   static std::atomic<uint64_t> attr{0};
   if (!done_on_device(attr)) {
     SPB_CUDA(cudaFuncSetAttribute(gram_oz_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -575,7 +578,7 @@ int oz_gemm_jobs(int njobs, const OzOperand* const* A, const OzOperand* const* B
   }
   if (tiles == 0) return SPB_OK;
   const int64_t nkb = A[0]->nkb;
-  int64_t ks = oz_splits(nkb, tiles);
+  int64_t ks = oz_splits(nkb, tiles, sms);
   size_t need = 0;
   for (int j = 0; j < njobs; ++j) need = std::max(need, (size_t)P.job[j].p * P.job[j].q);
   while (ks > 1 && (size_t)ks * need > partial_cap) --ks;
@@ -597,12 +600,12 @@ int oz_gemm_jobs(int njobs, const OzOperand* const* A, const OzOperand* const* B
 
 // out[A.cols x B.cols] (ld ldo) = A' B from two prepared operands.
 int oz_gemm(const OzOperand& A, const OzOperand& B, double* partial, size_t partial_cap,
-            double* out, int ldo, cudaStream_t st, bool upper = false) {
+            double* out, int ldo, cudaStream_t st, bool upper = false, int sms = 0) {
   const OzOperand* a[1] = {&A};
   const OzOperand* b[1] = {&B};
   double* pp[1] = {partial};
   double* oo[1] = {out};
-  return oz_gemm_jobs(1, a, b, &upper, pp, partial_cap, oo, ldo, st);
+  return oz_gemm_jobs(1, a, b, &upper, pp, partial_cap, oo, ldo, st, sms);
 }
 
 // Workspace of gram_oz: both operands' digit planes, then the split-K partials.
@@ -714,7 +717,8 @@ int gram_oz_rr(const float* B, const float* LB, int64_t ld, int64_t n, int cols,
     }
     if (phase == 2) return oz_gemm(ops[0], ops[0], part, pc, Gb, ldo, st, true);
     if (phase == 3) return oz_prepare(LB, ld, n, cols, scr + bo, &ops[1], st);
-    return oz_gemm(ops[0], ops[1], part + pc, pc, Ga, ldo, st, false);
+    // the G_B factorisation's 16-CTA cluster runs beside this launch (lobpcg.cu)
+    return oz_gemm(ops[0], ops[1], part + pc, pc, Ga, ldo, st, false, num_sms() - 16);
   }
   const OzOperand& OB = ops[0];
   const OzOperand& OL = ops[1];
