@@ -489,9 +489,15 @@ def run_ours(args):
         return labels, st
 
     clk = ClockSampler(local).start()  # running (and initialised) before the timed steps
-    for _ in range(args.warmup):
+    # W warm-up steps, and at least 2.5 s of them: about 1.2 s after sustained load
+    # begins the GPU goes through a ~0.3 s clock transient (two consecutive C3 steps
+    # +6 %, between nvidia-smi's 250 ms samples); with W = 3 it fell into timed steps
+    # 3-4 of every second run (tools/step_jitter.py)
+    t_warm, done = time.perf_counter(), 0
+    while done < args.warmup or time.perf_counter() - t_warm < 2.5:
         step_device()
-    torch.cuda.synchronize()
+        torch.cuda.synchronize()
+        done += 1
     stats.clear()
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
           for _ in range(args.steps)]

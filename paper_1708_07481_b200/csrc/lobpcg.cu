@@ -397,12 +397,15 @@ struct Driver {
                             w.Gpad, 2 * pe, w.oz_ws, w.oz_ws_bytes, s, phase, keep);
         };
         SPB_TRY(oz(1, st));  // pack B
-        // LB is packed (HBM-bound) on its own stream beside the G_B launch (tensor / L2)
+        // LB is packed (HBM-bound) on its own stream beside the G_B launch (tensor / L2).
+        // G_B is enqueued first: its one CTA per SM takes its shared memory and the
+        // packing CTAs fill the remaining thread slots (the other way round eight
+        // packing CTAs hold every thread slot of an SM and G_B starts late)
         SPB_CUDA(cudaEventRecord(pack_fork, st));
+        SPB_TRY(oz(2, st));  // G_B
         SPB_CUDA(cudaStreamWaitEvent(pack_st, pack_fork, 0));
         SPB_TRY(oz(3, pack_st));
         SPB_CUDA(cudaEventRecord(pack_join, pack_st));
-        SPB_TRY(oz(2, st));  // G_B
         gather_pad_grams<<<gg, 256, 0, st>>>(w.Gpad, 2 * pe, pe, m, w.l, na, w.lp, w.G,
                                              2 * w.mmax, w.mmax, 2);
         SPB_LAUNCH_CHECK();
