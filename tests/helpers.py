@@ -6,7 +6,7 @@ import hashlib
 
 import numpy as np
 
-from paper_1708_07481_b200.dcsbm import CONFIGS, generate_dcsbm
+from paper_1708_07481_b200.dcsbm import CONFIGS, DcsbmSpec, generate_dcsbm
 
 
 def sha(*arrays) -> str:
@@ -19,8 +19,14 @@ def sha(*arrays) -> str:
     return h.hexdigest()
 
 
+# l = 108 > one Ozaki column tile at a size the one-GPU multi-rank tests can run: with
+# SPB_GRAM=oz the solve takes the int8 Rayleigh-Ritz Grams and the fused projection +
+# CholQR step (lobpcg.cu project_orth) that C3 / C4 take by default.
+OZ108 = DcsbmSpec(n=40000, blocks=98, arcs=1_000_000, alpha=3.0, ratio=5.0, seed=4)
+
+
 def config_input(name, seed=None):
-    spec = CONFIGS[name]
+    spec = OZ108 if name == "oz108" else CONFIGS[name]
     if seed is not None:
         spec = spec.__class__(**{**spec.__dict__, "seed": seed})
     edges, truth = generate_dcsbm(spec)

@@ -50,13 +50,15 @@ def _free_port():
 
 
 @pytest.mark.parametrize("world,cfg,precision", [(2, "c1", "float64"), (2, "c2", "float32"),
-                                                 (3, "c1", "float32")])
+                                                 (3, "c1", "float32"), (2, "oz108", "float32")])
 def test_multirank_sharded_solve_host_transport(tmp_path, world, cfg, precision):
     """world > 1 ranks (processes sharing the one GPU, host/gloo transport) run the real
     row-sharded driver: per-rank CSR rows bit-exact against the whole-graph build,
     every Gram / norm all-reduced, the operator input all-gathered before each SpMM;
     the result matches the unsharded solve (iterations exact, Ritz values 1e-6 rel.,
-    labels >= 99.9 %)."""
+    labels >= 99.9 %). "oz108" (l = 108, SPB_GRAM=oz) puts the sharded solve on the
+    path a 2-GPU C3 run takes: int8 Ozaki Grams in one all-reduced launch and the fused
+    projection + CholQR step, against the one-GPU solve with its split launches."""
     import subprocess
     import sys
 

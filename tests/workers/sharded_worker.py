@@ -22,6 +22,8 @@ import torch.distributed as dist  # noqa: E402
 
 def main():
     out, cfg_name, precision = sys.argv[1], sys.argv[2], sys.argv[3]
+    if cfg_name == "oz108":  # the Ozaki Grams / fused projection path at a small size
+        os.environ["SPB_GRAM"] = "oz"
     dist.init_process_group("gloo")
     rank, world = dist.get_rank(), dist.get_world_size()
     torch.cuda.set_device(0)
@@ -33,7 +35,7 @@ def main():
     k = spec.blocks
     l = spb.block_size_for(k)
     x0 = np.random.default_rng(0).standard_normal((spec.n, l))
-    cfg = spb.SolverConfig(block_size=l, tol=1e-12, max_iter=20, seed=0)
+    cfg = spb.SolverConfig(block_size=l, tol=1e-12, max_iter=8 if cfg_name == "oz108" else 20, seed=0)
     hist = []
     part, st, gap = partition_edges_sharded(edges, spec.n, cfg, k, fix_k=True, x0=x0,
                                             precision=precision, transport="host",
