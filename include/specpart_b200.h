@@ -79,6 +79,16 @@ SPB_API int spb_csr_build(const int64_t* src, const int64_t* dst, const double* 
 
 /* float64 -> dtype conversion of a device vector (operator values/degrees). */
 SPB_API int spb_cast(const double* in, int64_t count, int dtype, void* out, void* stream);
+/* Host -> device copy of a large pageable host array (the public API's numpy inputs:
+ * from_edges' arc list, graph.py:106-145; lobpcg_solve's x0, lobpcg.py:263) through a
+ * caller-provided pinned ring of spb_h2d_ring_bytes(threads) bytes, staged by `threads`
+ * host threads; src_esz == dst_esz copies bytes, 8 -> 4 narrows float64 to float32
+ * (round to nearest even) on the way. Ordered on `stream`; the ring is free again on
+ * return. */
+SPB_API size_t spb_h2d_ring_bytes(int32_t threads);
+SPB_API int spb_h2d_staged(const void* src, int64_t count, int32_t src_esz, int32_t dst_esz,
+                           void* dst_dev, void* pinned_ring, size_t ring_bytes, int32_t threads,
+                           void* stream);
 /* Strided 2-D copy/convert between float64 and dtype blocks (device). */
 SPB_API int spb_copy_block(int src_dtype, const void* src, int64_t lds, int dst_dtype, void* dst,
                    int64_t ldd, int64_t rows, int32_t cols, void* stream);

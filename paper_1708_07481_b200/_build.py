@@ -68,7 +68,7 @@ def build(force: bool = False, jobs: int | None = None) -> Path:
         objs = list(ex.map(lambda s: _compile(s, force), sources))
     if force or not OUT.exists() or OUT.stat().st_mtime < max(o.stat().st_mtime for o in objs):
         tmp = OUT.with_suffix(".so.tmp")
-        cmd = [nvcc(), *ARCH, "-shared", "-cudart", "static", "-o", str(tmp), *map(str, objs), "-ldl"]
+        cmd = [nvcc(), *ARCH, "-shared", "-cudart", "static", "-o", str(tmp), *map(str, objs), "-ldl", "-lpthread"]
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
             raise RuntimeError(f"link failed:\n{r.stderr}")

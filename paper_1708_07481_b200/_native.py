@@ -63,6 +63,8 @@ _SIGS = {
     "spb_csr_build": (C.c_int, [vp, vp, vp, i64, i32, C.c_int, vp, sz, vp, vp, vp, vp,
                                 C.POINTER(i64), vp]),
     "spb_cast": (C.c_int, [vp, i64, C.c_int, vp, vp]),
+    "spb_h2d_ring_bytes": (C.c_size_t, [i32]),
+    "spb_h2d_staged": (C.c_int, [vp, i64, i32, i32, vp, vp, C.c_size_t, i32, vp]),
     "spb_copy_block": (C.c_int, [C.c_int, vp, i64, C.c_int, vp, i64, i64, i32, vp]),
     "spb_max_f64": (C.c_int, [vp, i64, C.POINTER(f64), vp]),
     "spb_laplacian_spmm": (C.c_int, [C.c_int, i32, i32, vp, vp, vp, vp, vp, i64, i32, vp, i64, vp]),

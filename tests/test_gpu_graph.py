@@ -165,3 +165,23 @@ def test_hub_rows_both_build_paths(spb, hub):
     assert np.array_equal(s.row_offsets, wp) and np.array_equal(s.col_indices, wx)
     assert np.array_equal(s.weights, wv)
     assert np.array_equal(spb.degrees(g), oracle.directed_degrees(ip, ix, dv, n))
+
+
+@pytest.mark.parametrize("rows,cols", [(300_001, 7), (2_100_000, 3)])
+def test_staged_h2d_copies_and_narrows_bit_exactly(rows, cols):
+    """spb_h2d_staged (csrc/h2d.cu), the multi-threaded pinned-ring upload behind
+    from_edges / lobpcg_solve for large numpy inputs: a ragged element count (last chunk
+    partial, chunks spread over the threads) arrives bit-identical, and float64 ->
+    float32 narrowing equals numpy's astype."""
+    import torch
+
+    from paper_1708_07481_b200 import _h2d
+
+    rng = np.random.default_rng(rows)
+    x = rng.standard_normal((rows, cols)) * 10.0 ** rng.integers(-30, 30, size=(rows, 1))
+    assert x.nbytes >= _h2d._SMALL
+    dev = torch.device("cuda", 0)
+    assert torch.equal(_h2d.to_device(x, dev).cpu(), torch.from_numpy(x))
+    assert torch.equal(_h2d.to_device(x, dev, np.float32).cpu(), torch.from_numpy(x.astype(np.float32)))
+    e = rng.integers(-2**62, 2**62, size=(rows, cols))
+    assert torch.equal(_h2d.to_device(e, dev).cpu(), torch.from_numpy(e))
