@@ -2645,7 +2645,13 @@ wy_tfactors(const double* __restrict__ V, const double* __restrict__ tau, int m,
   }
 }
 
-__global__ void __launch_bounds__(BAT)
+// WYT threads: the first BAT = 32 x BCW of them own one (reflector, column) pair of
+// the 32 x BCW products; all of them stage the reflector block (83 KB from L2 per step
+// at m = 324 -- with 128 threads that staging was most of a step), split the long
+// V_b'Y dots four ways and share the Y update.
+constexpr int WYT = 4 * BAT;
+
+__global__ void __launch_bounds__(WYT)
 wy_apply(const double* __restrict__ V, int m, const double* __restrict__ Tall, double* Y,
          int ldy, int nev, const SmallStatus* status) {
   extern __shared__ double wsm[];
@@ -2653,69 +2659,64 @@ wy_apply(const double* __restrict__ V, int m, const double* __restrict__ Tall, d
   const int vld = m | 1;                       // odd row stride: conflict-free column reads
   double* Ys = wsm;                            // [m][BCW]
   double* Vb = Ys + (size_t)m * BCW;           // [32][vld]
-  double* W1 = Vb + 32 * (size_t)vld;          // [32][BCW]
-  double* W2 = W1 + 32 * BCW;                  // [32][BCW]
+  double* W1 = Vb + 32 * (size_t)vld;          // [4][32][BCW] partial dots, then [32][BCW]
+  double* W2 = W1 + 4 * 32 * BCW;              // [32][BCW]
   double* Tb = W2 + 32 * BCW;                  // [32][33]
   const int tid = threadIdx.x;
   const int c0 = blockIdx.x * BCW;
   const int nc = min(BCW, nev - c0);
-  for (int x = tid; x < m * BCW; x += BAT) {
+  for (int x = tid; x < m * BCW; x += WYT) {
     const int r = x / BCW, c = x % BCW;
     Ys[x] = c < nc ? Y[(size_t)r * ldy + c0 + c] : 0.0;
   }
   const int nrefl = m - 2;
-  const int jj = tid / BCW, cc = tid % BCW;  // (reflector, column) of this thread
+  const int part = tid / BAT, pt = tid % BAT;  // quarter of the dot, (reflector, column) pair
+  const int jj = pt / BCW, cc = pt % BCW;
   for (int kb = ((nrefl - 1) / 32) * 32; kb >= 0; kb -= 32) {
     const int nb = min(32, nrefl - kb);
     const double* T = Tall + (size_t)(kb / 32) * 1024;
     // rows kb..kb+nb-1 of V are contiguous: stage them with 8 loads in flight per thread
     const double* Vsrc = V + (size_t)kb * m;
-    for (int x0 = tid; x0 < nb * m; x0 += BAT * 8) {
+    for (int x0 = tid; x0 < nb * m; x0 += WYT * 8) {
       double tv[8];
 #pragma unroll
-      for (int u = 0; u < 8; ++u) tv[u] = x0 + u * BAT < nb * m ? Vsrc[x0 + u * BAT] : 0.0;
+      for (int u = 0; u < 8; ++u) tv[u] = x0 + u * WYT < nb * m ? Vsrc[x0 + u * WYT] : 0.0;
 #pragma unroll
       for (int u = 0; u < 8; ++u) {
-        const int x = x0 + u * BAT;
+        const int x = x0 + u * WYT;
         if (x < nb * m) {
           const int j = x / m, r = x - (x / m) * m;
           Vb[j * vld + r] = tv[u];
         }
       }
     }
-    {
-      double tt[1024 / BAT];
-#pragma unroll
-      for (int u = 0; u < 1024 / BAT; ++u) tt[u] = T[tid + u * BAT];
-#pragma unroll
-      for (int u = 0; u < 1024 / BAT; ++u) {
-        const int x = tid + u * BAT;
-        Tb[(x >> 5) * 33 + (x & 31)] = tt[u];
-      }
-    }
+    for (int x = tid; x < 1024; x += WYT) Tb[(x >> 5) * 33 + (x & 31)] = T[x];
     __syncthreads();
-    // W1 = V_b' Y (v_{kb+j}[r] = 0 for r <= kb + j)
+    // W1 = V_b' Y (v_{kb+j}[r] = 0 for r <= kb + j): rows r = r0 + part, r0 + part + 4, ...
     if (jj < nb) {
       double a0 = 0.0, a1 = 0.0;
       const double* vr = Vb + jj * vld;
-      int r = kb + jj + 1;
-      for (; r + 1 < m; r += 2) {
+      int r = kb + jj + 1 + part;
+      for (; r + 4 < m; r += 8) {
         a0 = fma(vr[r], Ys[r * BCW + cc], a0);
-        a1 = fma(vr[r + 1], Ys[(r + 1) * BCW + cc], a1);
+        a1 = fma(vr[r + 4], Ys[(r + 4) * BCW + cc], a1);
       }
       if (r < m) a0 = fma(vr[r], Ys[r * BCW + cc], a0);
-      W1[jj * BCW + cc] = a0 + a1;
+      W1[part * BAT + pt] = a0 + a1;
     }
     __syncthreads();
+    if (part == 0 && jj < nb)
+      W1[pt] = (W1[pt] + W1[BAT + pt]) + (W1[2 * BAT + pt] + W1[3 * BAT + pt]);
+    __syncthreads();
     // W2 = T_b W1 (upper triangular)
-    if (jj < nb) {
+    if (part == 0 && jj < nb) {
       double acc = 0.0;
       for (int q = jj; q < nb; ++q) acc = fma(Tb[jj * 33 + q], W1[q * BCW + cc], acc);
       W2[jj * BCW + cc] = acc;
     }
     __syncthreads();
     // Y -= V_b W2
-    for (int x = tid; x < (m - kb - 1) * BCW; x += BAT) {
+    for (int x = tid; x < (m - kb - 1) * BCW; x += WYT) {
       const int r = kb + 1 + x / BCW, c = x % BCW;
       const int jmax = min(nb, r - kb);
       double acc = 0.0;
@@ -2724,14 +2725,14 @@ wy_apply(const double* __restrict__ V, int m, const double* __restrict__ Tall, d
     }
     __syncthreads();
   }
-  for (int x = tid; x < m * BCW; x += BAT) {
+  for (int x = tid; x < m * BCW; x += WYT) {
     const int r = x / BCW, c = x % BCW;
     if (c < nc) Y[(size_t)r * ldy + c0 + c] = Ys[x];
   }
 }
 
 size_t wy_apply_smem(int m) {
-  return sizeof(double) * ((size_t)m * BCW + 32 * (size_t)(m | 1) + 64 * BCW + 32 * 33);
+  return sizeof(double) * ((size_t)m * BCW + 32 * (size_t)(m | 1) + 5 * 32 * BCW + 32 * 33);
 }
 
 void launch_wy_tfactors(const double* V, const double* tau, int m, double* Tscratch,
@@ -2745,7 +2746,7 @@ void launch_wy_tfactors(const double* V, const double* tau, int m, double* Tscra
 void launch_wy_apply(const double* V, int m, const double* Tscratch, double* Y, int nev,
                      const SmallStatus* status, cudaStream_t st) {
   if (m - 2 <= 0 || nev <= 0) return;
-  wy_apply<<<(nev + BCW - 1) / BCW, BAT, wy_apply_smem(m), st>>>(V, m, Tscratch, Y, nev, nev,
+  wy_apply<<<(nev + BCW - 1) / BCW, WYT, wy_apply_smem(m), st>>>(V, m, Tscratch, Y, nev, nev,
                                                                   status);
 }
 
