@@ -1,7 +1,6 @@
 """Per-kernel device time of the projected eigensolve (spb_sygv) at given sizes.
 
     python tools/bench_small.py --m 147 [--gb] [--reps 10] [--nev 49]
-Environment switches (SPB_TRI_VARIANT, SPB_WC_C, ...) select kernel variants.
 """
 import argparse
 import sys
