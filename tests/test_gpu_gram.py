@@ -188,3 +188,55 @@ def test_fused_projection_guard_with_preconditioner():
     rel = np.abs(sa.eigenvalues - sb.eigenvalues) / np.maximum(np.abs(sa.eigenvalues), 1e-6 * sa.eigenvalues.max())
     assert rel.max() < 1e-5, rel.max()
     assert np.abs(np.log10(ha) - np.log10(hb)).max() < 0.01
+
+
+def test_ozaki_path_with_soft_locked_columns():
+    """Soft locking on the Ozaki path (l = 108): with a loose soft_lock_tol columns
+    leave the active set, so R is narrower than X (na < l), P is compacted and the
+    packed [X | R] view, the Rayleigh-Ritz operand width and the kept X planes all
+    change from iteration to iteration. Same iteration count, Ritz values and
+    residual history as the float64-product path."""
+    import os
+
+    import paper_1708_07481_b200 as spb
+    from paper_1708_07481_b200.dcsbm import DcsbmSpec, generate_dcsbm
+
+    spec = DcsbmSpec(n=30000, blocks=98, arcs=900_000, alpha=3.0, ratio=8.0, seed=9)
+    e, _ = generate_dcsbm(spec)
+    g = spb.from_edges(e, spec.n)
+    l = spb.block_size_for(spec.blocks)
+    x0 = np.random.default_rng(9).standard_normal((spec.n, l))
+    # probe: the lock threshold is the median residual after 6 iterations, so about half
+    # of the columns are locked from then on
+    probe = []
+    op = spb.LaplacianOperator(g)
+    spb.lobpcg_solve(op, x0, spb.SolverConfig(block_size=l, tol=1e-12, max_iter=6, seed=9),
+                     precision="float32", callback=lambda it, th, nr: probe.append((np.array(th), np.array(nr))))
+    th6, nr6 = probe[-1]
+    scale = max(abs(float(th6[-1])), op.scale_hint)
+    lock = float(np.median(nr6)) / scale
+    cfg = spb.SolverConfig(block_size=l, tol=1e-12, max_iter=14, seed=9, soft_lock_tol=lock)
+    out = {}
+    old = os.environ.get("SPB_GRAM")
+    try:
+        for mode in ("dmma", "oz"):
+            os.environ["SPB_GRAM"] = mode
+            hist = []
+            st = spb.lobpcg_solve(spb.LaplacianOperator(g), x0, cfg, precision="float32",
+                                  callback=lambda it, th, nr: hist.append(np.array(nr)))
+            out[mode] = (st, np.array(hist))
+    finally:
+        if old is None:
+            os.environ.pop("SPB_GRAM", None)
+        else:
+            os.environ["SPB_GRAM"] = old
+    (sa, ha), (sb, hb) = out["dmma"], out["oz"]
+    locked = int((ha[-1] < lock * scale).sum())
+    print(f"\nsoft lock: {locked} of {l} columns below the lock threshold at the end, "
+          f"iterations {sa.iterations} / {sb.iterations}")
+    assert locked > 0, "the case must lock columns to exercise na < l"
+    assert sa.iterations == sb.iterations
+    rel = np.abs(sa.eigenvalues - sb.eigenvalues) / np.maximum(np.abs(sa.eigenvalues), 1e-6 * sa.eigenvalues.max())
+    assert rel.max() < 1e-5, rel.max()
+    big = ha > 1e-3 * ha.max()
+    assert np.abs(np.log10(ha[big]) - np.log10(hb[big])).max() < 0.02
