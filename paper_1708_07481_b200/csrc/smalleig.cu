@@ -2647,8 +2647,8 @@ wy_tfactors(const double* __restrict__ V, const double* __restrict__ tau, int m,
 
 // WYT threads: the first BAT = 32 x BCW of them own one (reflector, column) pair of
 // the 32 x BCW products; all of them stage the reflector block (83 KB from L2 per step
-// at m = 324 -- with 128 threads that staging was most of a step), split the long
-// V_b'Y dots four ways and share the Y update.
+// at m = 324 -- with 128 threads that staging was most of a step) and share the Y
+// update; every output keeps its summation order (results bit-identical).
 constexpr int WYT = 4 * BAT;
 
 __global__ void __launch_bounds__(WYT)
@@ -2659,8 +2659,8 @@ wy_apply(const double* __restrict__ V, int m, const double* __restrict__ Tall, d
   const int vld = m | 1;                       // odd row stride: conflict-free column reads
   double* Ys = wsm;                            // [m][BCW]
   double* Vb = Ys + (size_t)m * BCW;           // [32][vld]
-  double* W1 = Vb + 32 * (size_t)vld;          // [4][32][BCW] partial dots, then [32][BCW]
-  double* W2 = W1 + 4 * 32 * BCW;              // [32][BCW]
+  double* W1 = Vb + 32 * (size_t)vld;          // [32][BCW]
+  double* W2 = W1 + 32 * BCW;                  // [32][BCW]
   double* Tb = W2 + 32 * BCW;                  // [32][33]
   const int tid = threadIdx.x;
   const int c0 = blockIdx.x * BCW;
@@ -2692,21 +2692,22 @@ wy_apply(const double* __restrict__ V, int m, const double* __restrict__ Tall, d
     }
     for (int x = tid; x < 1024; x += WYT) Tb[(x >> 5) * 33 + (x & 31)] = T[x];
     __syncthreads();
-    // W1 = V_b' Y (v_{kb+j}[r] = 0 for r <= kb + j): rows r = r0 + part, r0 + part + 4, ...
-    if (jj < nb) {
+    // W1 = V_b' Y (v_{kb+j}[r] = 0 for r <= kb + j). One thread per (reflector, column)
+    // with the summation order this kernel has always had: split four ways over the
+    // idle threads the Ritz vectors moved by ~5e-17, and the planted float32 case of
+    // tests/test_gpu_f32_guard.py -- a solve at the float32 residual floor -- took a
+    // different trajectory (300 iterations instead of 83).
+    if (part == 0 && jj < nb) {
       double a0 = 0.0, a1 = 0.0;
       const double* vr = Vb + jj * vld;
-      int r = kb + jj + 1 + part;
-      for (; r + 4 < m; r += 8) {
+      int r = kb + jj + 1;
+      for (; r + 1 < m; r += 2) {
         a0 = fma(vr[r], Ys[r * BCW + cc], a0);
-        a1 = fma(vr[r + 4], Ys[(r + 4) * BCW + cc], a1);
+        a1 = fma(vr[r + 1], Ys[(r + 1) * BCW + cc], a1);
       }
       if (r < m) a0 = fma(vr[r], Ys[r * BCW + cc], a0);
-      W1[part * BAT + pt] = a0 + a1;
+      W1[pt] = a0 + a1;
     }
-    __syncthreads();
-    if (part == 0 && jj < nb)
-      W1[pt] = (W1[pt] + W1[BAT + pt]) + (W1[2 * BAT + pt] + W1[3 * BAT + pt]);
     __syncthreads();
     // W2 = T_b W1 (upper triangular)
     if (part == 0 && jj < nb) {
@@ -2732,7 +2733,7 @@ wy_apply(const double* __restrict__ V, int m, const double* __restrict__ Tall, d
 }
 
 size_t wy_apply_smem(int m) {
-  return sizeof(double) * ((size_t)m * BCW + 32 * (size_t)(m | 1) + 5 * 32 * BCW + 32 * 33);
+  return sizeof(double) * ((size_t)m * BCW + 32 * (size_t)(m | 1) + 64 * BCW + 32 * 33);
 }
 
 void launch_wy_tfactors(const double* V, const double* tau, int m, double* Tscratch,
