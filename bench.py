@@ -650,9 +650,9 @@ def run_ours(args):
         gram_roof["traffic"] = gtr
         if gtr:
             gram_roof["traffic_note"] = (
-                "ncu dram__bytes_read+write of one Rayleigh-Ritz Gram launch (G_B and G_A together, "
-                "profiles/gram_traffic.json); the digit planes of B and LB are 5 bytes per float32 "
-                "value, so ~1.6 GB at C3 is the launch's compulsory stream")
+                "ncu dram__bytes_read+write of the two launches of one Rayleigh-Ritz Gram pair (G_B "
+                "upper tiles, then G_A; profiles/gram_traffic.json); the digit planes of B and LB are "
+                "5 bytes per float32 value (~1.6 GB at C3) and B's are read by both launches")
         # the dominant of the two (by live time in this run) is the headline roofline
         if g_us >= spmm_us:
             roofline = dict(gram_roof, spmm=spmm_roof, csr_build=csr)
