@@ -493,11 +493,19 @@ def run_ours(args):
     # begins the GPU goes through a ~0.3 s clock transient (two consecutive C3 steps
     # +6 %, between nvidia-smi's 250 ms samples); with W = 3 it fell into timed steps
     # 3-4 of every second run (tools/step_jitter.py)
-    t_warm, done = time.perf_counter(), 0
-    while done < args.warmup or time.perf_counter() - t_warm < 2.5:
+    t_warm = time.perf_counter()
+    for _ in range(max(args.warmup, 1)):
         step_device()
-        torch.cuda.synchronize()
-        done += 1
+    torch.cuda.synchronize()
+    spent = time.perf_counter() - t_warm
+    extra = 0 if spent >= 2.5 else int(np.ceil((2.5 - spent) / (spent / max(args.warmup, 1))))
+    if dist is not None:  # the sharded step has collectives: every rank runs rank 0's count
+        cnt = torch.tensor([extra], dtype=torch.int64,
+                           device=dev if dist.get_backend() == "nccl" else "cpu")
+        dist.broadcast(cnt, src=0)
+        extra = int(cnt.item())
+    for _ in range(min(extra, 64)):
+        step_device()
     stats.clear()
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
           for _ in range(args.steps)]
