@@ -19,6 +19,8 @@
 #include <cfloat>
 #include <cstdio>
 #include <cstdlib>
+#include <deque>
+#include <mutex>
 #include <vector>
 
 #include "smalleig.cuh"
@@ -2759,18 +2761,29 @@ struct SideStream {
   cudaEvent_t fork = nullptr, join = nullptr;
   cudaEvent_t pre_fork = nullptr, pre_join = nullptr;  // sygv_prefactor_b
 };
-SideStream* side_stream() {
-  static SideStream ss[16];
+// One side stream (and its events) per (device, caller stream): two solves running on
+// different streams never share events. Entries live for the process (a caller's
+// streams are few and pooled); the table is guarded by a mutex.
+SideStream* side_stream(cudaStream_t main) {
+  struct Key {
+    int dev;
+    cudaStream_t st;
+    SideStream ss;
+  };
+  static std::mutex mu;
+  static std::deque<Key> table;  // deque: stable addresses
   int dev = 0;
   cudaGetDevice(&dev);
-  SideStream& x = ss[dev & 15];
-  if (!x.s) {
-    cudaStreamCreateWithFlags(&x.s, cudaStreamNonBlocking);
-    cudaEventCreateWithFlags(&x.fork, cudaEventDisableTiming);
-    cudaEventCreateWithFlags(&x.join, cudaEventDisableTiming);
-    cudaEventCreateWithFlags(&x.pre_fork, cudaEventDisableTiming);
-    cudaEventCreateWithFlags(&x.pre_join, cudaEventDisableTiming);
-  }
+  std::lock_guard<std::mutex> lock(mu);
+  for (Key& k : table)
+    if (k.dev == dev && k.st == main) return &k.ss;
+  table.push_back(Key{dev, main, SideStream{}});
+  SideStream& x = table.back().ss;
+  cudaStreamCreateWithFlags(&x.s, cudaStreamNonBlocking);
+  cudaEventCreateWithFlags(&x.fork, cudaEventDisableTiming);
+  cudaEventCreateWithFlags(&x.join, cudaEventDisableTiming);
+  cudaEventCreateWithFlags(&x.pre_fork, cudaEventDisableTiming);
+  cudaEventCreateWithFlags(&x.pre_join, cudaEventDisableTiming);
   return &x;
 }
 
@@ -3087,7 +3100,7 @@ int sygv_prefactor_b(const double* gb, int ldg, int m, int nev, double* ws, size
   }
   SPB_TRY(set_smem_attrs());
   const SygvWs w = carve_sygv(ws, m, nev);
-  SideStream* side = side_stream();
+  SideStream* side = side_stream(st);
   SPB_CUDA(cudaEventRecord(side->pre_fork, st));
   SPB_CUDA(cudaStreamWaitEvent(side->s, side->pre_fork, 0));
   const int g1 = (int)std::min<int64_t>(ceil_div((int64_t)m * m, 256), 1024);
@@ -3100,7 +3113,7 @@ int sygv_prefactor_b(const double* gb, int ldg, int m, int nev, double* ws, size
 
 // st waits for the last sygv_prefactor_b (used when its result is not consumed).
 int sygv_prefactor_join(cudaStream_t st) {
-  SPB_CUDA(cudaStreamWaitEvent(st, side_stream()->pre_join, 0));
+  SPB_CUDA(cudaStreamWaitEvent(st, side_stream(st)->pre_join, 0));
   return SPB_OK;
 }
 
@@ -3131,7 +3144,7 @@ int sygv_enqueue(const double* ga, const double* gb, int ldg, int m, int nev, do
   }
   launch_tridiag(Atri, m, 1, w.W, w.V, w.tau, w.d, w.e, status, tridiag_smem(m), st);
   SPB_LAUNCH_CHECK();
-  SideStream* side = side_stream();
+  SideStream* side = side_stream(st);
   SPB_CUDA(cudaEventRecord(side->fork, st));
   SPB_CUDA(cudaStreamWaitEvent(side->s, side->fork, 0));
   launch_wy_tfactors(w.V, w.tau, m, w.scratch, status, side->s);  // overlaps bisect + invit
