@@ -11,6 +11,7 @@ returned tensor is ordered on the current stream.
 from __future__ import annotations
 
 import os
+import threading
 
 import numpy as np
 import torch
@@ -34,6 +35,7 @@ def to_device(arr: np.ndarray, device, dtype=None) -> torch.Tensor:
 
 
 _ring: dict = {}
+_ring_lock = threading.Lock()  # one staged upload at a time shares the pinned ring
 
 
 def _staged(arr: np.ndarray, device, dtype: np.dtype) -> torch.Tensor:
@@ -44,14 +46,14 @@ def _staged(arr: np.ndarray, device, dtype: np.dtype) -> torch.Tensor:
 
     out = torch.empty(arr.shape, dtype=torch.from_numpy(np.empty(0, dtype)).dtype, device=device)
     L = N.lib()
-    need = int(L.spb_h2d_ring_bytes(_THREADS))
-    ring = _ring.get(need)
-    if ring is None:
-        ring = _ring[need] = torch.empty(need, dtype=torch.uint8, pin_memory=True)
     narrow = arr.dtype == np.float64 and dtype == np.float32
     if arr.dtype != dtype and not narrow:
         return torch.from_numpy(arr.astype(dtype)).to(device, non_blocking=True)
-    with torch.cuda.device(device):
+    need = int(L.spb_h2d_ring_bytes(_THREADS))
+    with _ring_lock, torch.cuda.device(device):
+        ring = _ring.get(need)
+        if ring is None:
+            ring = _ring[need] = torch.empty(need, dtype=torch.uint8, pin_memory=True)
         N.check(L.spb_h2d_staged(arr.ctypes.data, arr.size, arr.dtype.itemsize, dtype.itemsize,
                                  out.data_ptr(), ring.data_ptr(), need, _THREADS,
                                  torch.cuda.current_stream(device).cuda_stream))
